@@ -1,0 +1,147 @@
+/*
+ * bz.h -- C ABI of the B200 Brouwer-Zimmermann enumeration core.
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `mindist` (arXiv 1603.06757): for one generator count g it visits every
+ * g-row combination of every systematic information-set matrix Gamma_j,
+ * XORs the bit-packed rows, popcounts the codeword and min-reduces it.
+ *
+ * Reference interfaces replaced (paths relative to the reference's
+ * pkg/src/mindist/):
+ *   bz_round      <- engine.py:208-211  the per-round loop
+ *                      `for idx, gamma in enumerate(gs.gammas):
+ *                           res = runner.run(idx, gamma, g, U)`
+ *                    i.e. _Runner.run (engine.py:136-150) dispatching to
+ *                    enumerate_basic/optimized/stack (enumeration.py:76,96,128)
+ *                    or enumerate_saved/_unrolled/_parallel
+ *                    (enumeration.py:305,351,385), each returning an
+ *                    EnumerationResult (enumeration.py:43-50) whose
+ *                    min_weight is clipped to ubound (enumeration.py:60-64).
+ *   bz_enumerate  <- one (Gamma, g) pass: enumerate_*(gamma, g, ubound)
+ *                    (enumeration.py:76-93) -> (min_weight, combinations).
+ *   bz_histogram  <- no reference counterpart (the reference keeps only the
+ *                    minimum); weight histogram of one (Gamma, g) pass, used
+ *                    as the bit-exact checksum of BASELINE.json config 4.
+ *   bz_load_gammas<- the packed row layout of BitMatrix.to_numpy()
+ *                    (gf2.py:74-79, word_width 64): little-endian words,
+ *                    bit j of the row = column j, zero padding past n-1.
+ *
+ * Conventions: plain C types only; every pointer is caller-owned host
+ * memory and is not retained past the call.  Calls on one context are not
+ * thread-safe (serialise them; the reference driver is single-threaded,
+ * SPEC.md:394).  Status codes map onto the reference's MindistError
+ * hierarchy (errors.py:6-71) in the Python wrapper.  There is no CPU
+ * fallback: without a usable sm_100 device bz_create fails with
+ * BZ_ERR_NO_DEVICE.
+ */
+#ifndef BZ_H_
+#define BZ_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BZ_ABI_VERSION 1
+
+/* limits of the device kernels */
+#define BZ_MAX_K 128 /* rows per Gamma (prefix masks are 128-bit)      */
+#define BZ_MAX_N 256 /* columns: 8 x 32-bit words per row              */
+
+/* status codes */
+#define BZ_OK 0
+#define BZ_ERR_INVALID_ARITY 1      /* g outside 1..k        -> InvalidArity      */
+#define BZ_ERR_INVALID_DIMENSIONS 2 /* bad m/k/n/padding     -> InvalidDimensions */
+#define BZ_ERR_TOO_LARGE 3          /* k>128, n>256, C(k,g) >= 2^62 -> TooLarge  */
+#define BZ_ERR_CUDA 4               /* CUDA runtime failure                      */
+#define BZ_ERR_NO_DEVICE 5          /* no sm_100 device visible                  */
+#define BZ_ERR_STATE 6              /* no Gamma loaded / bad gamma index         */
+#define BZ_ERR_ARGUMENT 7           /* null pointer, bad shard                   */
+
+typedef struct bz_ctx bz_ctx;
+
+/* Library / ABI version (BZ_ABI_VERSION). */
+int bz_abi_version(void);
+
+/* Number of visible CUDA devices (0 when none); never fails. */
+int bz_device_count(void);
+
+/* Create a context on CUDA device `device` (one process per GPU). */
+int bz_create(int device, bz_ctx **out);
+
+/* Destroy a context and free its device memory; NULL is ignored. */
+void bz_destroy(bz_ctx *ctx);
+
+/* Human-readable description of the last error on ctx (never NULL). */
+const char *bz_last_error(const bz_ctx *ctx);
+
+/* Upload the m systematic matrices of one generator: `rows` holds
+ * m*k*ceil(n/64) little-endian uint64 words, matrix-major then row-major
+ * (bit j of a row = column j; bits past n-1 must be zero).  Replaces any
+ * previously loaded family. */
+int bz_load_gammas(bz_ctx *ctx, const uint64_t *rows, int m, int k, int n);
+
+/* One Brouwer-Zimmermann round: enumerate every g-combination of every
+ * loaded Gamma_j and report, per Gamma, min(true minimum weight, upper)
+ * in out_min[j] and the number of combinations visited in out_combos[j].
+ *
+ * lower_prev is the certified lower bound before this round; the kernel
+ * stops early only once the running minimum reaches lower_prev (then the
+ * round's result is exactly lower_prev, as in the reference trace).  Pass
+ * lower_prev = 0 to disable early exit.
+ *
+ * shard/nshards split the round's work into nshards disjoint parts (one
+ * per GPU/process); nshards = 1 is the whole round.  Results of the shards
+ * combine by min (out_min) and sum (out_combos). */
+int bz_round(bz_ctx *ctx, int g, int lower_prev, int upper, int shard,
+             int nshards, int32_t *out_min, uint64_t *out_combos);
+
+/* One (Gamma_gamma, g) pass without early exit; out_min is the unclipped
+ * minimum weight (INT32_MAX when the shard is empty). */
+int bz_enumerate(bz_ctx *ctx, int gamma, int g, int shard, int nshards,
+                 int32_t *out_min, uint64_t *out_combos);
+
+/* Weight histogram of one (Gamma_gamma, g) pass: out_hist[w] (n+1 bins)
+ * counts the g-combinations whose codeword has weight w. */
+int bz_histogram(bz_ctx *ctx, int gamma, int g, int shard, int nshards,
+                 uint64_t *out_hist, int32_t *out_min, uint64_t *out_combos);
+
+/* Host-only: the work plan bz_round uses for (m, k, g), for inspection and
+ * for the CPU tests of the sharding logic.  Writes *out_ngroups groups of 6
+ * int64 each -- chunk_begin, nprefix, gamma, ell, prefixes_per_lane,
+ * combinations -- into out (capacity `cap` groups; out may be NULL to query
+ * the count) and the round's chunk count into *out_nchunks.  Chunk c of the
+ * round belongs to shard c % nshards; within a chunk of group (gamma, ell),
+ * lane l of the warp walks the colex ranks [(c_local*32 + l)*ppl, +ppl) of
+ * the (g-2)-subsets of [0, ell), each extended by ell and then by every
+ * suffix row e in (ell, k). */
+int bz_plan(int m, int k, int g, int64_t *out, int cap, int *out_ngroups,
+            uint64_t *out_nchunks);
+
+/* Device timing on the context's stream: bz_timer_start records a CUDA
+ * event, bz_timer_stop records a second one, synchronises and returns the
+ * elapsed milliseconds. */
+int bz_timer_start(bz_ctx *ctx);
+int bz_timer_stop(bz_ctx *ctx, float *ms);
+
+/* Device time (ms) of the enumeration kernel of the last bz_round /
+ * bz_enumerate / bz_histogram call, from CUDA events around that launch. */
+int bz_last_kernel_ms(bz_ctx *ctx, float *ms);
+
+/* Number of kernels this context has launched so far. */
+int bz_launch_count(bz_ctx *ctx, uint64_t *out);
+
+/* Integer-pipe microbenchmark on the context's device (roofline
+ * denominators): out[0] = POPC per second (whole GPU), out[1] = LOP3 per
+ * second, out[2] = SM clock in MHz during the run, out[3] = SM count,
+ * out[4] = POPC per clock per SM, out[5] = LOP3 per clock per SM,
+ * out[6] = codewords/s of a synthetic W-word XOR+POPC+min loop (w_words
+ * selects W, 1..8), out[7] = its codewords per clock per SM. */
+int bz_measure_int_peaks(bz_ctx *ctx, int w_words, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BZ_H_ */

@@ -1,0 +1,226 @@
+"""ctypes binding of the C ABI in include/bz.h (libbz.so, built in-tree).
+
+The library is the product: there is no CPU fallback.  If ``libbz.so`` is
+missing, or no sm_100 GPU is visible, every compute entry point raises
+``NoDevice`` -- loudly, never silently degrading.  ``bz_plan`` and the
+version/device-count queries need no GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import (DeviceError, InvalidArity, InvalidDimensions, MindistError,
+                     NoDevice, TooLarge)
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "libbz.so")
+ABI_VERSION = 1
+
+BZ_OK = 0
+_CODES = {
+    1: InvalidArity,
+    2: InvalidDimensions,
+    3: TooLarge,
+    4: DeviceError,
+    5: NoDevice,
+    6: MindistError,
+    7: ValueError,
+}
+
+# every symbol include/bz.h declares (checked by tests/test_abi.py)
+SYMBOLS = ("bz_abi_version", "bz_device_count", "bz_create", "bz_destroy",
+           "bz_last_error", "bz_load_gammas", "bz_round", "bz_enumerate",
+           "bz_histogram", "bz_plan", "bz_timer_start", "bz_timer_stop",
+           "bz_last_kernel_ms", "bz_launch_count", "bz_measure_int_peaks")
+
+_lib = None
+
+c_int, c_float, c_double = ctypes.c_int, ctypes.c_float, ctypes.c_double
+u64p = ctypes.POINTER(ctypes.c_uint64)
+i64p = ctypes.POINTER(ctypes.c_int64)
+i32p = ctypes.POINTER(ctypes.c_int32)
+vp = ctypes.c_void_p
+
+
+def lib():
+    """Load libbz.so (raises NoDevice if it was never built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NoDevice(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                       "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    L.bz_abi_version.restype = c_int
+    L.bz_device_count.restype = c_int
+    L.bz_create.argtypes = [c_int, ctypes.POINTER(vp)]
+    L.bz_destroy.argtypes = [vp]
+    L.bz_destroy.restype = None
+    L.bz_last_error.argtypes = [vp]
+    L.bz_last_error.restype = ctypes.c_char_p
+    L.bz_load_gammas.argtypes = [vp, u64p, c_int, c_int, c_int]
+    L.bz_round.argtypes = [vp, c_int, c_int, c_int, c_int, c_int, i32p, u64p]
+    L.bz_enumerate.argtypes = [vp, c_int, c_int, c_int, c_int, i32p, u64p]
+    L.bz_histogram.argtypes = [vp, c_int, c_int, c_int, c_int, u64p, i32p, u64p]
+    L.bz_plan.argtypes = [c_int, c_int, c_int, i64p, c_int, i32p, u64p]
+    L.bz_timer_start.argtypes = [vp]
+    L.bz_timer_stop.argtypes = [vp, ctypes.POINTER(c_float)]
+    L.bz_last_kernel_ms.argtypes = [vp, ctypes.POINTER(c_float)]
+    L.bz_launch_count.argtypes = [vp, u64p]
+    L.bz_measure_int_peaks.argtypes = [vp, c_int, ctypes.POINTER(c_double)]
+    if L.bz_abi_version() != ABI_VERSION:
+        raise NoDevice(f"libbz ABI {L.bz_abi_version()} != {ABI_VERSION}: rebuild")
+    _lib = L
+    return L
+
+
+def _ptr(a: np.ndarray, t):
+    return a.ctypes.data_as(ctypes.POINTER(t))
+
+
+def check(rc: int, ctx=None, what: str = "") -> None:
+    if rc == BZ_OK:
+        return
+    msg = ""
+    if ctx is not None:
+        raw = lib().bz_last_error(ctx)
+        msg = raw.decode() if raw else ""
+    exc = _CODES.get(rc, DeviceError)
+    raise exc(f"{what}: {msg}" if what else msg)
+
+
+def device_count() -> int:
+    return int(lib().bz_device_count())
+
+
+def plan(m: int, k: int, g: int):
+    """The device work plan for one round (host-only; see bz_plan)."""
+    L = lib()
+    ng = np.zeros(1, dtype=np.int32)
+    nc = np.zeros(1, dtype=np.uint64)
+    check(L.bz_plan(m, k, g, None, 0, _ptr(ng, ctypes.c_int32), _ptr(nc, ctypes.c_uint64)),
+          what="bz_plan")
+    out = np.zeros((int(ng[0]), 6), dtype=np.int64)
+    check(L.bz_plan(m, k, g, _ptr(out, ctypes.c_int64), int(ng[0]),
+                    _ptr(ng, ctypes.c_int32), _ptr(nc, ctypes.c_uint64)), what="bz_plan")
+    return [tuple(int(v) for v in row) for row in out], int(nc[0])
+
+
+class Context:
+    """One CUDA device.  Owns the device copy of the loaded Gamma family."""
+
+    def __init__(self, device: int = 0):
+        L = lib()
+        h = vp()
+        rc = L.bz_create(int(device), ctypes.byref(h))
+        self._h = h
+        if rc != BZ_OK:
+            try:
+                check(rc, h, f"bz_create(device={device})")
+            finally:
+                L.bz_destroy(h)
+                self._h = None
+        self.device = device
+        self.m = self.k = self.n = 0
+
+    def close(self) -> None:
+        if self._h is not None:
+            lib().bz_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise MindistError("context is closed")
+        return self._h
+
+    def load(self, words: np.ndarray, n: int) -> None:
+        """words: (m, k, ceil(n/64)) uint64 row image of the family."""
+        words = np.ascontiguousarray(words, dtype=np.uint64)
+        if words.ndim != 3:
+            raise InvalidDimensions("expected an (m, k, w64) array")
+        m, k, _ = words.shape
+        check(lib().bz_load_gammas(self.handle, _ptr(words, ctypes.c_uint64), m, k, n),
+              self.handle, "bz_load_gammas")
+        self.m, self.k, self.n = m, k, n
+
+    def round(self, g: int, lower_prev: int, upper: int, shard: int = 0,
+              nshards: int = 1):
+        mins = np.zeros(max(self.m, 1), dtype=np.int32)
+        combos = np.zeros(max(self.m, 1), dtype=np.uint64)
+        check(lib().bz_round(self.handle, g, lower_prev, upper, shard, nshards,
+                             _ptr(mins, ctypes.c_int32), _ptr(combos, ctypes.c_uint64)),
+              self.handle, f"bz_round(g={g})")
+        return [int(v) for v in mins[:self.m]], [int(v) for v in combos[:self.m]]
+
+    def enumerate(self, gamma: int, g: int, shard: int = 0, nshards: int = 1):
+        mn = np.zeros(1, dtype=np.int32)
+        c = np.zeros(1, dtype=np.uint64)
+        check(lib().bz_enumerate(self.handle, gamma, g, shard, nshards,
+                                 _ptr(mn, ctypes.c_int32), _ptr(c, ctypes.c_uint64)),
+              self.handle, f"bz_enumerate(g={g})")
+        return int(mn[0]), int(c[0])
+
+    def histogram(self, gamma: int, g: int, shard: int = 0, nshards: int = 1):
+        hist = np.zeros(self.n + 1, dtype=np.uint64)
+        mn = np.zeros(1, dtype=np.int32)
+        c = np.zeros(1, dtype=np.uint64)
+        check(lib().bz_histogram(self.handle, gamma, g, shard, nshards,
+                                 _ptr(hist, ctypes.c_uint64), _ptr(mn, ctypes.c_int32),
+                                 _ptr(c, ctypes.c_uint64)),
+              self.handle, f"bz_histogram(g={g})")
+        return hist, int(mn[0]), int(c[0])
+
+    def timer_start(self) -> None:
+        check(lib().bz_timer_start(self.handle), self.handle, "bz_timer_start")
+
+    def timer_stop(self) -> float:
+        ms = c_float()
+        check(lib().bz_timer_stop(self.handle, ctypes.byref(ms)), self.handle, "bz_timer_stop")
+        return float(ms.value)
+
+    def last_kernel_ms(self) -> float:
+        ms = c_float()
+        check(lib().bz_last_kernel_ms(self.handle, ctypes.byref(ms)), self.handle)
+        return float(ms.value)
+
+    def launch_count(self) -> int:
+        v = np.zeros(1, dtype=np.uint64)
+        check(lib().bz_launch_count(self.handle, _ptr(v, ctypes.c_uint64)), self.handle)
+        return int(v[0])
+
+    def measure_int_peaks(self, w_words: int) -> dict:
+        out = (c_double * 8)()
+        check(lib().bz_measure_int_peaks(self.handle, w_words, out), self.handle,
+              "bz_measure_int_peaks")
+        keys = ("popc_per_s", "lop3_per_s", "sm_mhz", "sm_count", "popc_per_clk_sm",
+                "lop3_per_clk_sm", "codeword_per_s", "codeword_per_clk_sm")
+        return dict(zip(keys, (float(v) for v in out)))
+
+
+_contexts: dict[int, Context] = {}
+
+
+def context(device: int = 0) -> Context:
+    """Process-wide context per device (created on first use)."""
+    ctx = _contexts.get(device)
+    if ctx is None or ctx._h is None:
+        ctx = Context(device)
+        _contexts[device] = ctx
+    return ctx

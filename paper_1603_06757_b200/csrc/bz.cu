@@ -1,0 +1,600 @@
+// bz.cu -- context management, round planning and the C ABI (include/bz.h)
+// for the B200 Brouwer-Zimmermann enumeration core.
+//
+// One context owns one CUDA device and one stream.  bz_load_gammas uploads
+// the padded 32-bit row image of every Gamma_j plus its prefix-XOR table
+// once per minimum-distance run; each bz_round then costs one small H2D of
+// the round's group table, one kernel launch and one D2H of m+1 minima and
+// m counters -- the host-side work that the reference does per round in
+// engine.py:204-217 stays in Python above this library.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/bz.h"
+#include "bz_kernels.cuh"
+
+using bz::Group;
+using bz::RoundArgs;
+
+struct bz_ctx {
+  int device = -1;
+  int sm_count = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;      // user timer
+  cudaEvent_t ev_k0 = nullptr, ev_k1 = nullptr;    // last kernel
+  std::string err;
+  uint64_t launches = 0;
+  float last_kernel_ms = 0.f;
+
+  // loaded family
+  int m = 0, k = 0, n = 0, w32 = 0, wp = 0;
+  uint32_t* d_rows = nullptr;   // m*k*wp
+  uint32_t* d_px = nullptr;     // m*(k+1)*wp
+  unsigned long long* d_binom = nullptr;
+  // per-round scratch
+  Group* d_groups = nullptr;
+  int groups_cap = 0;
+  int* d_bound = nullptr;                  // 1 + m
+  unsigned long long* d_combos = nullptr;  // m
+  unsigned long long* d_counter = nullptr;
+  unsigned long long* d_hist = nullptr;    // BZ_MAX_N + 1
+  int bound_cap = 0;
+  // pinned staging
+  Group* h_groups = nullptr;
+  int* h_bound = nullptr;
+  unsigned long long* h_combos = nullptr;
+  unsigned long long* h_hist = nullptr;
+};
+
+namespace {
+
+constexpr long long kLaneTarget = 4096;  // codewords per lane per chunk
+
+int fail(bz_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+#define CK(call)                                                              \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess)                                                    \
+      return fail(ctx, BZ_ERR_CUDA, "%s failed: %s", #call,                   \
+                  cudaGetErrorString(e_));                                    \
+  } while (0)
+
+// saturating binomial on the host
+unsigned long long binom_sat(int p, int q) {
+  if (q < 0 || p < 0 || q > p) return 0ull;
+  q = std::min(q, p - q);
+  unsigned __int128 r = 1;
+  for (int i = 1; i <= q; ++i) {
+    r = r * (unsigned)(p - q + i) / (unsigned)i;
+    if (r > (unsigned __int128)~0ull) return ~0ull;
+  }
+  return (unsigned long long)r;
+}
+
+int ensure_round_buffers(bz_ctx* ctx, int ngroups) {
+  if (ngroups > ctx->groups_cap) {
+    if (ctx->d_groups) cudaFree(ctx->d_groups);
+    if (ctx->h_groups) cudaFreeHost(ctx->h_groups);
+    ctx->d_groups = nullptr;
+    ctx->h_groups = nullptr;
+    int cap = std::max(ngroups, 1024);
+    CK(cudaMalloc(&ctx->d_groups, sizeof(Group) * cap));
+    CK(cudaMallocHost(&ctx->h_groups, sizeof(Group) * cap));
+    ctx->groups_cap = cap;
+  }
+  return BZ_OK;
+}
+
+// Work plan of one round (host only): one Group per (Gamma, ell) with its
+// chunk range.  gamma_only < 0: all m Gammas.
+int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, std::vector<Group>& gs,
+               unsigned long long* out_nchunks) {
+  gs.clear();
+  unsigned long long chunk = 0;
+  const int j0 = gamma_only < 0 ? 0 : gamma_only;
+  const int j1 = gamma_only < 0 ? m : gamma_only + 1;
+  for (int j = j0; j < j1; ++j) {
+    const int ell_lo = g == 1 ? -1 : g - 2;
+    const int ell_hi = g == 1 ? -1 : k - 2;
+    for (int ell = ell_lo; ell <= ell_hi; ++ell) {
+      const unsigned long long np = g == 1 ? 1ull : binom_sat(ell, g - 2);
+      if (np == 0) continue;
+      if (np >= (1ull << 62))
+        return fail(ctx, BZ_ERR_TOO_LARGE, "C(%d,%d) prefixes exceed 2^62", ell, g - 2);
+      const long long looplen = k - 1 - ell;
+      long long ppl = std::max(1ll, kLaneTarget / looplen);
+      const long long spread = (long long)((np + 31) / 32);
+      ppl = std::min(ppl, std::max(1ll, spread));
+      Group gr{};
+      gr.chunk_begin = chunk;
+      gr.nprefix = np;
+      gr.gamma = j;
+      gr.ell = ell;
+      gr.ppl = (int)ppl;
+      const unsigned long long per_chunk = 32ull * (unsigned long long)ppl;
+      chunk += (np + per_chunk - 1) / per_chunk;
+      gs.push_back(gr);
+    }
+  }
+  *out_nchunks = chunk;
+  return BZ_OK;
+}
+
+// Build the round's group table and upload it.
+int plan_round(bz_ctx* ctx, int g, int gamma_only, int* out_ngroups,
+               unsigned long long* out_nchunks) {
+  std::vector<Group> gs;
+  int rc = build_plan(ctx, ctx->m, ctx->k, g, gamma_only, gs, out_nchunks);
+  if (rc) return rc;
+  rc = ensure_round_buffers(ctx, (int)gs.size());
+  if (rc) return rc;
+  std::memcpy(ctx->h_groups, gs.data(), gs.size() * sizeof(Group));
+  CK(cudaMemcpyAsync(ctx->d_groups, ctx->h_groups, gs.size() * sizeof(Group),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  *out_ngroups = (int)gs.size();
+  return BZ_OK;
+}
+
+int check_g(bz_ctx* ctx, int g) {
+  if (!ctx->d_rows) return fail(ctx, BZ_ERR_STATE, "no Gamma family loaded");
+  if (g < 1 || g > ctx->k)
+    return fail(ctx, BZ_ERR_INVALID_ARITY, "g=%d not in 1..%d", g, ctx->k);
+  if (binom_sat(ctx->k, g) >= (1ull << 62))
+    return fail(ctx, BZ_ERR_TOO_LARGE, "C(%d,%d) >= 2^62 combinations", ctx->k, g);
+  return BZ_OK;
+}
+
+template <int W>
+int launch_w(bz_ctx* ctx, const RoundArgs& a, bool hist) {
+  size_t smem = bz::smem_base_bytes<W>(a.m, a.k, a.ngroups);
+  int threads = 256;
+  if (hist) {
+    smem = ((smem + 15) & ~size_t(15)) + (size_t)(a.n + 1) * 4;
+    // per-thread u16 histogram columns
+    int dev_max = 0;
+    CK(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+    while (threads > 32 && smem + (size_t)(a.n + 1) * threads * 2 > (size_t)dev_max / 2)
+      threads /= 2;
+    smem += (size_t)(a.n + 1) * threads * 2;
+    CK(cudaFuncSetAttribute(bz::k1h_histogram<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+  } else {
+    CK(cudaFuncSetAttribute(bz::k1_round_min<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+  }
+  int per_sm = 0;
+  if (hist)
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bz::k1h_histogram<W>, threads, smem));
+  else
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bz::k1_round_min<W>, threads, smem));
+  if (per_sm < 1) return fail(ctx, BZ_ERR_TOO_LARGE, "kernel does not fit on an SM (smem %zu)", smem);
+  // persistent grid: one wave, but no more warps than chunks need
+  unsigned long long warps_needed = (a.nchunks + a.nshards - 1) / a.nshards;
+  long long blocks = (long long)per_sm * ctx->sm_count;
+  long long need = (long long)((warps_needed + (threads / 32) - 1) / (threads / 32));
+  blocks = std::max(1ll, std::min(blocks, need));
+  CK(cudaEventRecord(ctx->ev_k0, ctx->stream));
+  if (hist)
+    bz::k1h_histogram<W><<<(unsigned)blocks, threads, smem, ctx->stream>>>(a);
+  else
+    bz::k1_round_min<W><<<(unsigned)blocks, threads, smem, ctx->stream>>>(a);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
+  ctx->launches += 1;
+  return BZ_OK;
+}
+
+int launch(bz_ctx* ctx, const RoundArgs& a, bool hist) {
+  switch (ctx->w32) {
+    case 1: return launch_w<1>(ctx, a, hist);
+    case 2: return launch_w<2>(ctx, a, hist);
+    case 3: return launch_w<3>(ctx, a, hist);
+    case 4: return launch_w<4>(ctx, a, hist);
+    case 5: return launch_w<5>(ctx, a, hist);
+    case 6: return launch_w<6>(ctx, a, hist);
+    case 7: return launch_w<7>(ctx, a, hist);
+    case 8: return launch_w<8>(ctx, a, hist);
+    default: return fail(ctx, BZ_ERR_TOO_LARGE, "unsupported word count %d", ctx->w32);
+  }
+}
+
+// Shared body of bz_round / bz_enumerate / bz_histogram.
+int run_pass(bz_ctx* ctx, int g, int gamma_only, int lower_prev, int upper,
+             int shard, int nshards, bool hist) {
+  if (nshards < 1 || shard < 0 || shard >= nshards)
+    return fail(ctx, BZ_ERR_ARGUMENT, "bad shard %d of %d", shard, nshards);
+  int rc = check_g(ctx, g);
+  if (rc) return rc;
+  int ngroups = 0;
+  unsigned long long nchunks = 0;
+  rc = plan_round(ctx, g, gamma_only, &ngroups, &nchunks);
+  if (rc) return rc;
+  const int m = ctx->m;
+  for (int i = 0; i <= m; ++i) ctx->h_bound[i] = upper;
+  CK(cudaMemcpyAsync(ctx->d_bound, ctx->h_bound, sizeof(int) * (m + 1),
+                     cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_combos, 0, sizeof(unsigned long long) * m, ctx->stream));
+  CK(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned long long), ctx->stream));
+  if (hist)
+    CK(cudaMemsetAsync(ctx->d_hist, 0, sizeof(unsigned long long) * (ctx->n + 1), ctx->stream));
+  RoundArgs a{};
+  a.rows = ctx->d_rows;
+  a.px = ctx->d_px;
+  a.groups = ctx->d_groups;
+  a.binom = ctx->d_binom;
+  a.bound = ctx->d_bound;
+  a.combos = ctx->d_combos;
+  a.counter = ctx->d_counter;
+  a.hist = ctx->d_hist;
+  a.nchunks = nchunks;
+  a.ngroups = ngroups;
+  a.m = m;
+  a.k = ctx->k;
+  a.g = g;
+  a.n = ctx->n;
+  a.shard = shard;
+  a.nshards = nshards;
+  a.lower_prev = lower_prev;
+  if (nchunks > 0 && (unsigned long long)shard < nchunks) {
+    rc = launch(ctx, a, hist);
+    if (rc) return rc;
+  } else {
+    CK(cudaEventRecord(ctx->ev_k0, ctx->stream));
+    CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
+  }
+  CK(cudaMemcpyAsync(ctx->h_bound, ctx->d_bound, sizeof(int) * (m + 1),
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->h_combos, ctx->d_combos, sizeof(unsigned long long) * m,
+                     cudaMemcpyDeviceToHost, ctx->stream));
+  if (hist)
+    CK(cudaMemcpyAsync(ctx->h_hist, ctx->d_hist, sizeof(unsigned long long) * (ctx->n + 1),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaEventElapsedTime(&ctx->last_kernel_ms, ctx->ev_k0, ctx->ev_k1));
+  return BZ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bz_abi_version(void) { return BZ_ABI_VERSION; }
+
+int bz_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int bz_create(int device, bz_ctx** out) {
+  if (!out) return BZ_ERR_ARGUMENT;
+  *out = nullptr;
+  bz_ctx* ctx = new bz_ctx();
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0 || device < 0 || device >= n) {
+    cudaGetLastError();
+    *out = ctx;  // carries the error text
+    return fail(ctx, BZ_ERR_NO_DEVICE, "no CUDA device %d (count %d: %s)", device, n,
+                e == cudaSuccess ? "ok" : cudaGetErrorString(e));
+  }
+  ctx->device = device;
+  *out = ctx;
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(ctx, BZ_ERR_NO_DEVICE, "device %d is sm_%d%d, this library is built for sm_100a",
+                device, prop.major, prop.minor);
+  ctx->sm_count = prop.multiProcessorCount;
+  CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&ctx->ev_a));
+  CK(cudaEventCreate(&ctx->ev_b));
+  CK(cudaEventCreate(&ctx->ev_k0));
+  CK(cudaEventCreate(&ctx->ev_k1));
+  // binomial table, saturating at UINT64_MAX
+  std::vector<unsigned long long> tab(bz::kBinomDim * bz::kBinomDim);
+  for (int p = 0; p < bz::kBinomDim; ++p)
+    for (int q = 0; q < bz::kBinomDim; ++q) tab[p * bz::kBinomDim + q] = binom_sat(p, q);
+  CK(cudaMalloc(&ctx->d_binom, tab.size() * sizeof(unsigned long long)));
+  CK(cudaMemcpy(ctx->d_binom, tab.data(), tab.size() * sizeof(unsigned long long),
+                cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&ctx->d_counter, sizeof(unsigned long long)));
+  CK(cudaMalloc(&ctx->d_hist, sizeof(unsigned long long) * (BZ_MAX_N + 1)));
+  CK(cudaMallocHost(&ctx->h_hist, sizeof(unsigned long long) * (BZ_MAX_N + 1)));
+  ctx->err.clear();
+  return BZ_OK;
+}
+
+void bz_destroy(bz_ctx* ctx) {
+  if (!ctx) return;
+  if (ctx->device >= 0) {
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->d_rows);
+    cudaFree(ctx->d_px);
+    cudaFree(ctx->d_binom);
+    cudaFree(ctx->d_groups);
+    cudaFree(ctx->d_bound);
+    cudaFree(ctx->d_combos);
+    cudaFree(ctx->d_counter);
+    cudaFree(ctx->d_hist);
+    if (ctx->h_groups) cudaFreeHost(ctx->h_groups);
+    if (ctx->h_bound) cudaFreeHost(ctx->h_bound);
+    if (ctx->h_combos) cudaFreeHost(ctx->h_combos);
+    if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
+    if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
+    if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
+    if (ctx->ev_k0) cudaEventDestroy(ctx->ev_k0);
+    if (ctx->ev_k1) cudaEventDestroy(ctx->ev_k1);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  }
+  delete ctx;
+}
+
+const char* bz_last_error(const bz_ctx* ctx) {
+  if (!ctx) return "null context";
+  return ctx->err.c_str();
+}
+
+int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
+  if (!ctx) return BZ_ERR_ARGUMENT;
+  if (ctx->device < 0) return fail(ctx, BZ_ERR_NO_DEVICE, "context has no device");
+  if (!rows) return fail(ctx, BZ_ERR_ARGUMENT, "rows is NULL");
+  if (m < 1 || k < 1 || n < 1)
+    return fail(ctx, BZ_ERR_INVALID_DIMENSIONS, "need m, k, n >= 1 (got %d, %d, %d)", m, k, n);
+  if (k > BZ_MAX_K) return fail(ctx, BZ_ERR_TOO_LARGE, "k=%d exceeds %d", k, BZ_MAX_K);
+  if (n > BZ_MAX_N) return fail(ctx, BZ_ERR_TOO_LARGE, "n=%d exceeds %d", n, BZ_MAX_N);
+  CK(cudaSetDevice(ctx->device));
+  const int w64 = (n + 63) / 64;
+  const int w32 = (n + 31) / 32;
+  const int wp = bz::padded_words(w32);
+  // validate padding, repack to padded 32-bit rows, build prefix-XOR tables
+  std::vector<uint32_t> img((size_t)m * k * wp, 0u);
+  std::vector<uint32_t> px((size_t)m * (k + 1) * wp, 0u);
+  for (int j = 0; j < m; ++j) {
+    for (int r = 0; r < k; ++r) {
+      const uint64_t* src = rows + ((size_t)j * k + r) * w64;
+      for (int w = 0; w < w64; ++w) {
+        uint64_t v = src[w];
+        const int lo_bit = 64 * w;
+        if (lo_bit + 64 > n) {
+          const int keep = n - lo_bit;
+          const uint64_t mask = keep >= 64 ? ~0ull : ((1ull << keep) - 1ull);
+          if (v & ~mask)
+            return fail(ctx, BZ_ERR_INVALID_DIMENSIONS,
+                        "Gamma %d row %d has bits outside columns 0..%d", j, r, n - 1);
+        }
+        const int w0 = 2 * w, w1 = 2 * w + 1;
+        if (w0 < w32) img[((size_t)j * k + r) * wp + w0] = (uint32_t)v;
+        if (w1 < w32) img[((size_t)j * k + r) * wp + w1] = (uint32_t)(v >> 32);
+      }
+    }
+    for (int r = 0; r < k; ++r)
+      for (int w = 0; w < wp; ++w)
+        px[((size_t)j * (k + 1) + r + 1) * wp + w] =
+            px[((size_t)j * (k + 1) + r) * wp + w] ^ img[((size_t)j * k + r) * wp + w];
+  }
+  cudaFree(ctx->d_rows);
+  cudaFree(ctx->d_px);
+  ctx->d_rows = nullptr;
+  ctx->d_px = nullptr;
+  CK(cudaMalloc(&ctx->d_rows, img.size() * 4));
+  CK(cudaMalloc(&ctx->d_px, px.size() * 4));
+  CK(cudaMemcpy(ctx->d_rows, img.data(), img.size() * 4, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(ctx->d_px, px.data(), px.size() * 4, cudaMemcpyHostToDevice));
+  if (m + 1 > ctx->bound_cap) {
+    cudaFree(ctx->d_bound);
+    cudaFree(ctx->d_combos);
+    if (ctx->h_bound) cudaFreeHost(ctx->h_bound);
+    if (ctx->h_combos) cudaFreeHost(ctx->h_combos);
+    ctx->d_bound = nullptr;
+    ctx->d_combos = nullptr;
+    ctx->h_bound = nullptr;
+    ctx->h_combos = nullptr;
+    const int cap = std::max(m + 1, 64);
+    CK(cudaMalloc(&ctx->d_bound, sizeof(int) * cap));
+    CK(cudaMalloc(&ctx->d_combos, sizeof(unsigned long long) * cap));
+    CK(cudaMallocHost(&ctx->h_bound, sizeof(int) * cap));
+    CK(cudaMallocHost(&ctx->h_combos, sizeof(unsigned long long) * cap));
+    ctx->bound_cap = cap;
+  }
+  ctx->m = m;
+  ctx->k = k;
+  ctx->n = n;
+  ctx->w32 = w32;
+  ctx->wp = wp;
+  return BZ_OK;
+}
+
+int bz_round(bz_ctx* ctx, int g, int lower_prev, int upper, int shard, int nshards,
+             int32_t* out_min, uint64_t* out_combos) {
+  if (!ctx) return BZ_ERR_ARGUMENT;
+  if (!out_min || !out_combos) return fail(ctx, BZ_ERR_ARGUMENT, "null output");
+  if (ctx->device < 0) return fail(ctx, BZ_ERR_NO_DEVICE, "context has no device");
+  CK(cudaSetDevice(ctx->device));
+  int rc = run_pass(ctx, g, -1, lower_prev, upper, shard, nshards, false);
+  if (rc) return rc;
+  for (int j = 0; j < ctx->m; ++j) {
+    out_min[j] = std::min(ctx->h_bound[1 + j], upper);
+    out_combos[j] = ctx->h_combos[j];
+  }
+  return BZ_OK;
+}
+
+int bz_enumerate(bz_ctx* ctx, int gamma, int g, int shard, int nshards, int32_t* out_min,
+                 uint64_t* out_combos) {
+  if (!ctx) return BZ_ERR_ARGUMENT;
+  if (!out_min || !out_combos) return fail(ctx, BZ_ERR_ARGUMENT, "null output");
+  if (ctx->device < 0) return fail(ctx, BZ_ERR_NO_DEVICE, "context has no device");
+  if (gamma < 0 || gamma >= ctx->m)
+    return fail(ctx, BZ_ERR_STATE, "gamma %d not in 0..%d", gamma, ctx->m - 1);
+  CK(cudaSetDevice(ctx->device));
+  int rc = run_pass(ctx, g, gamma, 0, INT32_MAX, shard, nshards, false);
+  if (rc) return rc;
+  *out_min = ctx->h_bound[1 + gamma];
+  *out_combos = ctx->h_combos[gamma];
+  return BZ_OK;
+}
+
+int bz_histogram(bz_ctx* ctx, int gamma, int g, int shard, int nshards, uint64_t* out_hist,
+                 int32_t* out_min, uint64_t* out_combos) {
+  if (!ctx) return BZ_ERR_ARGUMENT;
+  if (!out_hist || !out_min || !out_combos) return fail(ctx, BZ_ERR_ARGUMENT, "null output");
+  if (ctx->device < 0) return fail(ctx, BZ_ERR_NO_DEVICE, "context has no device");
+  if (gamma < 0 || gamma >= ctx->m)
+    return fail(ctx, BZ_ERR_STATE, "gamma %d not in 0..%d", gamma, ctx->m - 1);
+  CK(cudaSetDevice(ctx->device));
+  int rc = run_pass(ctx, g, gamma, 0, INT32_MAX, shard, nshards, true);
+  if (rc) return rc;
+  for (int b = 0; b <= ctx->n; ++b) out_hist[b] = ctx->h_hist[b];
+  *out_min = ctx->h_bound[0];
+  *out_combos = ctx->h_combos[gamma];
+  return BZ_OK;
+}
+
+int bz_plan(int m, int k, int g, int64_t* out, int cap, int* out_ngroups,
+            uint64_t* out_nchunks) {
+  if (!out_ngroups || !out_nchunks) return BZ_ERR_ARGUMENT;
+  if (m < 1 || k < 1) return BZ_ERR_INVALID_DIMENSIONS;
+  if (k > BZ_MAX_K) return BZ_ERR_TOO_LARGE;
+  if (g < 1 || g > k) return BZ_ERR_INVALID_ARITY;
+  if (binom_sat(k, g) >= (1ull << 62)) return BZ_ERR_TOO_LARGE;
+  std::vector<Group> gs;
+  unsigned long long nchunks = 0;
+  int rc = build_plan(nullptr, m, k, g, -1, gs, &nchunks);
+  if (rc) return rc;
+  *out_ngroups = (int)gs.size();
+  *out_nchunks = nchunks;
+  if (out) {
+    if ((int)gs.size() > cap) return BZ_ERR_ARGUMENT;
+    for (size_t i = 0; i < gs.size(); ++i) {
+      out[6 * i + 0] = (int64_t)gs[i].chunk_begin;
+      out[6 * i + 1] = (int64_t)gs[i].nprefix;
+      out[6 * i + 2] = gs[i].gamma;
+      out[6 * i + 3] = gs[i].ell;
+      out[6 * i + 4] = gs[i].ppl;
+      out[6 * i + 5] = (int64_t)gs[i].nprefix * (k - 1 - gs[i].ell);
+    }
+  }
+  return BZ_OK;
+}
+
+int bz_timer_start(bz_ctx* ctx) {
+  if (!ctx) return BZ_ERR_ARGUMENT;
+  if (ctx->device < 0) return fail(ctx, BZ_ERR_NO_DEVICE, "context has no device");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaEventRecord(ctx->ev_a, ctx->stream));
+  return BZ_OK;
+}
+
+int bz_timer_stop(bz_ctx* ctx, float* ms) {
+  if (!ctx || !ms) return BZ_ERR_ARGUMENT;
+  if (ctx->device < 0) return fail(ctx, BZ_ERR_NO_DEVICE, "context has no device");
+  CK(cudaSetDevice(ctx->device));
+  CK(cudaEventRecord(ctx->ev_b, ctx->stream));
+  CK(cudaEventSynchronize(ctx->ev_b));
+  CK(cudaEventElapsedTime(ms, ctx->ev_a, ctx->ev_b));
+  return BZ_OK;
+}
+
+int bz_last_kernel_ms(bz_ctx* ctx, float* ms) {
+  if (!ctx || !ms) return BZ_ERR_ARGUMENT;
+  *ms = ctx->last_kernel_ms;
+  return BZ_OK;
+}
+
+int bz_launch_count(bz_ctx* ctx, uint64_t* out) {
+  if (!ctx || !out) return BZ_ERR_ARGUMENT;
+  *out = ctx->launches;
+  return BZ_OK;
+}
+
+int bz_measure_int_peaks(bz_ctx* ctx, int w_words, double* out) {
+  if (!ctx || !out) return BZ_ERR_ARGUMENT;
+  if (ctx->device < 0) return fail(ctx, BZ_ERR_NO_DEVICE, "context has no device");
+  if (w_words < 1 || w_words > 8) return fail(ctx, BZ_ERR_ARGUMENT, "w_words=%d", w_words);
+  CK(cudaSetDevice(ctx->device));
+  const int threads = 256, per_sm = 4;  // 32 warps/SM, one wave
+  const int blocks = ctx->sm_count * per_sm;
+  uint32_t* d_out = nullptr;
+  long long* d_clk = nullptr;
+  CK(cudaMalloc(&d_out, sizeof(uint32_t) * blocks * threads));
+  CK(cudaMalloc(&d_clk, sizeof(long long) * blocks));
+  std::vector<long long> clk(blocks);
+  auto run = [&](int which, int iters, double* ops_per_s, double* ops_per_clk_sm,
+                 double* mhz) -> int {
+    for (int rep = 0; rep < 2; ++rep) {  // first pass warms up clocks
+      CK(cudaEventRecord(ctx->ev_a, ctx->stream));
+      if (which == 0)
+        bz::peak_popc<<<blocks, threads, 0, ctx->stream>>>(d_out, 12345u, iters, d_clk);
+      else if (which == 1)
+        bz::peak_lop3<<<blocks, threads, 0, ctx->stream>>>(d_out, 12345u, iters, d_clk);
+      else {
+        int* o = reinterpret_cast<int*>(d_out);
+        switch (w_words) {
+          case 1: bz::peak_codeword<1><<<blocks, threads, 0, ctx->stream>>>(o, 7u, iters, d_clk); break;
+          case 2: bz::peak_codeword<2><<<blocks, threads, 0, ctx->stream>>>(o, 7u, iters, d_clk); break;
+          case 3: bz::peak_codeword<3><<<blocks, threads, 0, ctx->stream>>>(o, 7u, iters, d_clk); break;
+          case 4: bz::peak_codeword<4><<<blocks, threads, 0, ctx->stream>>>(o, 7u, iters, d_clk); break;
+          case 5: bz::peak_codeword<5><<<blocks, threads, 0, ctx->stream>>>(o, 7u, iters, d_clk); break;
+          case 6: bz::peak_codeword<6><<<blocks, threads, 0, ctx->stream>>>(o, 7u, iters, d_clk); break;
+          case 7: bz::peak_codeword<7><<<blocks, threads, 0, ctx->stream>>>(o, 7u, iters, d_clk); break;
+          default: bz::peak_codeword<8><<<blocks, threads, 0, ctx->stream>>>(o, 7u, iters, d_clk); break;
+        }
+      }
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(ctx->ev_b, ctx->stream));
+      ctx->launches += 1;
+      CK(cudaEventSynchronize(ctx->ev_b));
+    }
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b));
+    CK(cudaMemcpy(clk.data(), d_clk, sizeof(long long) * blocks, cudaMemcpyDeviceToHost));
+    double max_clk = 0;
+    for (long long c : clk) max_clk = std::max(max_clk, (double)c);
+    const double per_thread = which == 2 ? 4.0 * iters : 128.0 * iters;
+    const double total = per_thread * threads * blocks;
+    *ops_per_s = total / (ms * 1e-3);
+    // per clock per SM: blocks resident concurrently (per_sm per SM)
+    *ops_per_clk_sm = total / ((double)ctx->sm_count * max_clk);
+    *mhz = max_clk / (ms * 1e-3) / 1e6;
+    return BZ_OK;
+  };
+  double popc_s, popc_clk, lop_s, lop_clk, cw_s, cw_clk, mhz0, mhz1, mhz2;
+  int rc = run(0, 2048, &popc_s, &popc_clk, &mhz0);
+  if (!rc) rc = run(1, 2048, &lop_s, &lop_clk, &mhz1);
+  if (!rc) rc = run(2, 16384, &cw_s, &cw_clk, &mhz2);
+  cudaFree(d_out);
+  cudaFree(d_clk);
+  if (rc) return rc;
+  out[0] = popc_s;
+  out[1] = lop_s;
+  out[2] = mhz0;
+  out[3] = ctx->sm_count;
+  out[4] = popc_clk;
+  out[5] = lop_clk;
+  out[6] = cw_s;
+  out[7] = cw_clk;
+  return BZ_OK;
+}
+
+}  // extern "C"

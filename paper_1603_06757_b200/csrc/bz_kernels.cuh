@@ -1,0 +1,498 @@
+// bz_kernels.cuh -- sm_100a enumeration kernels for the Brouwer-Zimmermann
+// minimum-distance round (the hot path of arXiv 1603.06757's mindist
+// package, pkg/src/mindist/enumeration.py:76-444).
+//
+// Work decomposition:
+//   A g-combination {c_1 < ... < c_g} of the k rows of Gamma_j is split into
+//   a prefix {c_1..c_{g-1}} with last element ell = c_{g-1} and a suffix
+//   element e = c_g in (ell, k).  Prefixes with the same ell form a *group*:
+//   they are the (g-2)-subsets of [0, ell) plus ell itself, C(ell, g-2) of
+//   them, each extended by the same k-1-ell suffix rows.  A warp takes a
+//   chunk of one group; each lane owns a contiguous colex range of its
+//   prefixes, keeps the prefix XOR in registers and steps through its range
+//   with Gosper's successor (three prefix-XOR-table rows per step, branch
+//   free).  All lanes then run the SAME suffix loop e = ell+1 .. k-1, so
+//   row e is one broadcast shared-memory read reused by 32 lanes and there
+//   is no divergence in the hot loop:
+//        w = sum_j popc(acc[j] ^ row_e[j]);   best = min(best, w)
+//   (W LOP3 + W POPC + IADD3s + one IMNMX per codeword).
+//   This is the warp-scale form of the paper's "saved additions" and
+//   "unrolling" ideas: every codeword costs
+//   one row XOR per word, and every row access is shared by 32 codewords.
+//
+// Scheduling: chunks are handed out dynamically through one global 64-bit
+// counter (the GPU analogue of the reference's locked unit cursor,
+// enumeration.py:413-423).  Multi-GPU shards take every nshards-th chunk.
+//
+// Early exit: the running round minimum lives in bound[0]; a warp stops
+// taking chunks once bound[0] <= lower_prev (the only exit that keeps the
+// reference's bounds trace bit-exact, SURVEY.md 8(a) invariant 5).
+#pragma once
+
+#include <cstdint>
+#include <climits>
+
+namespace bz {
+
+constexpr int kMaxK = 128;
+constexpr int kMaxW = 8;
+constexpr int kBinomDim = kMaxK + 1;  // C(p, q) for 0 <= p, q <= 128
+
+struct Group {
+  unsigned long long chunk_begin;  // first global chunk index of the group
+  unsigned long long nprefix;      // C(ell, g-2) prefixes in the group
+  int gamma;                       // matrix index
+  int ell;                         // last prefix element (-1 when g == 1)
+  int ppl;                         // prefixes per lane per chunk
+  int pad;
+};
+
+struct RoundArgs {
+  const uint32_t* rows;        // m * k * WP words (padded rows)
+  const uint32_t* px;          // m * (k+1) * WP prefix-XOR table
+  const Group* groups;         // ngroups, sorted by chunk_begin
+  const unsigned long long* binom;  // kBinomDim^2 saturating binomials
+  int* bound;                  // [0] round minimum, [1+j] per-Gamma minimum
+  unsigned long long* combos;  // per-Gamma visited combinations
+  unsigned long long* counter; // dynamic chunk cursor
+  unsigned long long* hist;    // n+1 bins (histogram kernel only)
+  unsigned long long nchunks;  // chunks of the whole round (all shards)
+  int ngroups;
+  int m, k, g, n;
+  int shard, nshards;
+  int lower_prev;              // early exit once bound[0] <= lower_prev
+};
+
+__host__ __device__ constexpr int padded_words(int w) {
+  return w <= 1 ? 1 : (w <= 2 ? 2 : (w <= 4 ? 4 : 8));
+}
+
+// 128-bit subset mask over row indices [0, 128).
+struct Mask {
+  unsigned long long lo, hi;
+};
+
+__device__ __forceinline__ int mask_ctz(const Mask& x) {
+  return x.lo ? __ffsll((long long)x.lo) - 1 : 64 + __ffsll((long long)x.hi) - 1;
+}
+
+__device__ __forceinline__ int mask_popc(const Mask& x) {
+  return __popcll(x.lo) + __popcll(x.hi);
+}
+
+__device__ __forceinline__ Mask mask_shr(const Mask& x, int s) {
+  Mask r;
+  if (s >= 128) {
+    r.lo = r.hi = 0;
+  } else if (s >= 64) {
+    r.lo = x.hi >> (s - 64);
+    r.hi = 0;
+  } else if (s == 0) {
+    r = x;
+  } else {
+    r.lo = (x.lo >> s) | (x.hi << (64 - s));
+    r.hi = x.hi >> s;
+  }
+  return r;
+}
+
+// Colex successor of a q-subset (Gosper's hack on 128 bits).  Returns the
+// three prefix-XOR-table indices whose rows XOR to the change of the
+// subset's row sum: the low run [s, s+L) is removed, bit s+L and the bits
+// [0, L-1) are added, so  delta = PX[s] ^ PX[s+L+1] ^ PX[L-1].
+__device__ __forceinline__ void colex_next(Mask& x, int& i0, int& i1, int& i2) {
+  const int s = mask_ctz(x);
+  Mask u;
+  u.lo = s < 64 ? (1ull << s) : 0ull;
+  u.hi = s < 64 ? 0ull : (1ull << (s - 64));
+  Mask v;
+  v.lo = x.lo + u.lo;
+  v.hi = x.hi + u.hi + (v.lo < x.lo ? 1ull : 0ull);
+  Mask d;
+  d.lo = v.lo ^ x.lo;
+  d.hi = v.hi ^ x.hi;
+  const int l1 = mask_popc(d);  // run length + 1
+  Mask t = mask_shr(d, s + 2);
+  x.lo = v.lo | t.lo;
+  x.hi = v.hi | t.hi;
+  i0 = s;
+  i1 = s + l1;
+  i2 = l1 - 2;
+}
+
+// Colex unrank of rank r among the q-subsets of [0, ell).
+__device__ __forceinline__ Mask colex_unrank(unsigned long long r, int q, int ell,
+                                             const unsigned long long* __restrict__ binom) {
+  Mask x{0ull, 0ull};
+  int c = ell - 1;
+  for (int i = q; i >= 1; --i) {
+    while (__ldg(binom + c * kBinomDim + i) > r) --c;
+    r -= __ldg(binom + c * kBinomDim + i);
+    if (c < 64) x.lo |= 1ull << c; else x.hi |= 1ull << (c - 64);
+    --c;
+  }
+  return x;
+}
+
+template <int W>
+__device__ __forceinline__ void load_row(uint32_t (&r)[W], const uint32_t* p) {
+  constexpr int WP = padded_words(W);
+  if constexpr (WP >= 4) {
+#pragma unroll
+    for (int j = 0; j < WP / 4; ++j) {
+      const uint4 v = reinterpret_cast<const uint4*>(p)[j];
+      if (4 * j + 0 < W) r[(4 * j + 0) % W] = v.x;
+      if (4 * j + 1 < W) r[(4 * j + 1) % W] = v.y;
+      if (4 * j + 2 < W) r[(4 * j + 2) % W] = v.z;
+      if (4 * j + 3 < W) r[(4 * j + 3) % W] = v.w;
+    }
+  } else if constexpr (WP == 2) {
+    const uint2 v = reinterpret_cast<const uint2*>(p)[0];
+    r[0] = v.x;
+    if (W > 1) r[W > 1 ? 1 : 0] = v.y;
+  } else {
+    r[0] = p[0];
+  }
+}
+
+template <int W>
+__device__ __forceinline__ void xor_row(uint32_t (&acc)[W], const uint32_t* p) {
+  uint32_t r[W];
+  load_row<W>(r, p);
+#pragma unroll
+  for (int j = 0; j < W; ++j) acc[j] ^= r[j];
+}
+
+template <int W>
+__device__ __forceinline__ int weight_xor(const uint32_t (&acc)[W], const uint32_t (&r)[W]) {
+  int w = 0;
+#pragma unroll
+  for (int j = 0; j < W; ++j) w += __popc(acc[j] ^ r[j]);
+  return w;
+}
+
+// Locate the group owning `chunk` (groups sorted by chunk_begin).
+__device__ __forceinline__ int find_group(const Group* sg, int ngroups,
+                                          unsigned long long chunk) {
+  int lo = 0, hi = ngroups - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (sg[mid].chunk_begin <= chunk) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+// Shared-memory layout: rows | px | groups  (+ per-thread u16 histogram)
+template <int W>
+__host__ __device__ inline size_t smem_base_bytes(int m, int k, int ngroups) {
+  constexpr int WP = padded_words(W);
+  size_t words = (size_t)m * k * WP + (size_t)m * (k + 1) * WP;
+  size_t bytes = words * 4;
+  bytes = (bytes + 15) & ~size_t(15);
+  return bytes + (size_t)ngroups * sizeof(Group);
+}
+
+template <int W>
+__device__ __forceinline__ void stage(const RoundArgs& a, uint32_t*& srows,
+                                      uint32_t*& spx, Group*& sgroups,
+                                      unsigned char* smem) {
+  constexpr int WP = padded_words(W);
+  const int nrow_words = a.m * a.k * WP;
+  const int npx_words = a.m * (a.k + 1) * WP;
+  srows = reinterpret_cast<uint32_t*>(smem);
+  spx = srows + nrow_words;
+  size_t off = ((size_t)(nrow_words + npx_words) * 4 + 15) & ~size_t(15);
+  sgroups = reinterpret_cast<Group*>(smem + off);
+  for (int i = threadIdx.x; i < nrow_words; i += blockDim.x) srows[i] = a.rows[i];
+  for (int i = threadIdx.x; i < npx_words; i += blockDim.x) spx[i] = a.px[i];
+  const int gw = a.ngroups * (int)(sizeof(Group) / 4);
+  const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(a.groups);
+  uint32_t* gdst = reinterpret_cast<uint32_t*>(sgroups);
+  for (int i = threadIdx.x; i < gw; i += blockDim.x) gdst[i] = gsrc[i];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// K1: minimum-weight enumeration of one round (all Gammas, one shard).
+template <int W>
+__global__ void __launch_bounds__(256)
+k1_round_min(const RoundArgs a) {
+  constexpr int WP = padded_words(W);
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t *srows, *spx;
+  Group* sgroups;
+  stage<W>(a, srows, spx, sgroups, smem);
+
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int k = a.k, q = a.g - 2;
+  volatile int* vbound = a.bound;
+
+  while (true) {
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(a.counter, 1ull);
+    c = __shfl_sync(FULL, c, 0);
+    const unsigned long long chunk = c * (unsigned long long)a.nshards + a.shard;
+    if (chunk >= a.nchunks) break;
+    if (vbound[0] <= a.lower_prev) break;
+
+    const Group gr = sgroups[find_group(sgroups, a.ngroups, chunk)];
+    const unsigned long long local = chunk - gr.chunk_begin;
+    const unsigned long long first = (local * 32ull + lane) * (unsigned long long)gr.ppl;
+    long long cnt = 0;
+    if (first < gr.nprefix) {
+      const unsigned long long left = gr.nprefix - first;
+      cnt = left < (unsigned long long)gr.ppl ? (long long)left : gr.ppl;
+    }
+    const long long maxcnt = __shfl_sync(FULL, cnt, 0);
+    const uint32_t* R = srows + gr.gamma * k * WP;
+    const uint32_t* PX = spx + gr.gamma * (k + 1) * WP;
+    const int e0 = gr.ell + 1;
+
+    uint32_t acc[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) acc[j] = 0u;
+    Mask x{0ull, 0ull};
+    if (cnt > 0 && gr.ell >= 0) {
+      xor_row<W>(acc, R + gr.ell * WP);
+      if (q > 0) {
+        x = colex_unrank(first, q, gr.ell, a.binom);
+        Mask y = x;
+        while (y.lo | y.hi) {
+          const int b = mask_ctz(y);
+          xor_row<W>(acc, R + b * WP);
+          if (b < 64) y.lo &= y.lo - 1; else y.hi &= y.hi - 1;
+        }
+      }
+    }
+
+    int best = INT_MAX;
+    for (long long p = 0; p < maxcnt; ++p) {
+      if (p < cnt) {
+        int pb = INT_MAX;
+        const uint32_t* re = R + e0 * WP;
+        int e = e0;
+#pragma unroll 1
+        for (; e + 2 <= k; e += 2, re += 2 * WP) {
+          uint32_t r0[W], r1[W];
+          load_row<W>(r0, re);
+          load_row<W>(r1, re + WP);
+          const int w0 = weight_xor<W>(acc, r0);
+          const int w1 = weight_xor<W>(acc, r1);
+          pb = min(pb, min(w0, w1));
+        }
+        if (e < k) {
+          uint32_t r0[W];
+          load_row<W>(r0, re);
+          pb = min(pb, weight_xor<W>(acc, r0));
+        }
+        best = min(best, pb);
+        if (p + 1 < cnt) {
+          int i0, i1, i2;
+          colex_next(x, i0, i1, i2);
+          xor_row<W>(acc, PX + i0 * WP);
+          xor_row<W>(acc, PX + i1 * WP);
+          xor_row<W>(acc, PX + i2 * WP);
+        }
+      }
+    }
+
+    // chunk epilogue: warp min -> per-Gamma and round minima; combos count
+    const int wbest = __reduce_min_sync(FULL, best);
+    const unsigned cnt_u = (unsigned)cnt;
+    const unsigned tot = __reduce_add_sync(FULL, cnt_u);
+    if (lane == 0) {
+      if (wbest < vbound[1 + gr.gamma]) atomicMin(a.bound + 1 + gr.gamma, wbest);
+      if (wbest < vbound[0]) atomicMin(a.bound, wbest);
+      atomicAdd(a.combos + gr.gamma, (unsigned long long)tot * (unsigned long long)(k - e0));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1h: weight histogram of one (Gamma, g) pass.  Each thread owns a private
+// u16 histogram column in shared memory (layout [bin][thread]: conflict-free
+// for any bin pattern), flushed into a block-wide u32 histogram before it
+// can overflow, and finally into the global u64 bins.
+template <int W>
+__global__ void __launch_bounds__(256)
+k1h_histogram(const RoundArgs a) {
+  constexpr int WP = padded_words(W);
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t *srows, *spx;
+  Group* sgroups;
+  const int nbins = a.n + 1;
+  // histogram region follows the staged data
+  size_t base = smem_base_bytes<W>(a.m, a.k, a.ngroups);
+  base = (base + 15) & ~size_t(15);
+  unsigned int* bhist = reinterpret_cast<unsigned int*>(smem + base);
+  unsigned short* th = reinterpret_cast<unsigned short*>(smem + base + (size_t)nbins * 4);
+  for (int i = threadIdx.x; i < nbins; i += blockDim.x) bhist[i] = 0u;
+  for (int i = threadIdx.x; i < nbins * (int)blockDim.x; i += blockDim.x) th[i] = 0;
+  stage<W>(a, srows, spx, sgroups, smem);  // ends with __syncthreads
+
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const int tid = threadIdx.x;
+  const int bd = blockDim.x;
+  const int k = a.k, q = a.g - 2;
+  unsigned int since_flush = 0;
+  int best = INT_MAX;
+
+  auto flush = [&]() {
+    for (int b = 0; b < nbins; ++b) {
+      const unsigned short v = th[b * bd + tid];
+      if (v) {
+        atomicAdd(bhist + b, (unsigned)v);
+        th[b * bd + tid] = 0;
+      }
+    }
+    since_flush = 0;
+  };
+
+  while (true) {
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(a.counter, 1ull);
+    c = __shfl_sync(FULL, c, 0);
+    const unsigned long long chunk = c * (unsigned long long)a.nshards + a.shard;
+    if (chunk >= a.nchunks) break;
+
+    const Group gr = sgroups[find_group(sgroups, a.ngroups, chunk)];
+    const unsigned long long local = chunk - gr.chunk_begin;
+    const unsigned long long first = (local * 32ull + lane) * (unsigned long long)gr.ppl;
+    long long cnt = 0;
+    if (first < gr.nprefix) {
+      const unsigned long long left = gr.nprefix - first;
+      cnt = left < (unsigned long long)gr.ppl ? (long long)left : gr.ppl;
+    }
+    const long long maxcnt = __shfl_sync(FULL, cnt, 0);
+    const uint32_t* R = srows + gr.gamma * k * WP;
+    const uint32_t* PX = spx + gr.gamma * (k + 1) * WP;
+    const int e0 = gr.ell + 1;
+    const unsigned chunk_work = (unsigned)(cnt * (k - e0));
+    if (since_flush + chunk_work > 65535u) flush();
+    since_flush += chunk_work;
+
+    uint32_t acc[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) acc[j] = 0u;
+    Mask x{0ull, 0ull};
+    if (cnt > 0 && gr.ell >= 0) {
+      xor_row<W>(acc, R + gr.ell * WP);
+      if (q > 0) {
+        x = colex_unrank(first, q, gr.ell, a.binom);
+        Mask y = x;
+        while (y.lo | y.hi) {
+          const int b = mask_ctz(y);
+          xor_row<W>(acc, R + b * WP);
+          if (b < 64) y.lo &= y.lo - 1; else y.hi &= y.hi - 1;
+        }
+      }
+    }
+    for (long long p = 0; p < maxcnt; ++p) {
+      if (p < cnt) {
+        const uint32_t* re = R + e0 * WP;
+#pragma unroll 1
+        for (int e = e0; e < k; ++e, re += WP) {
+          uint32_t r0[W];
+          load_row<W>(r0, re);
+          const int w = weight_xor<W>(acc, r0);
+          best = min(best, w);
+          unsigned short* h = th + w * bd + tid;
+          *h = (unsigned short)(*h + 1);
+        }
+        if (p + 1 < cnt) {
+          int i0, i1, i2;
+          colex_next(x, i0, i1, i2);
+          xor_row<W>(acc, PX + i0 * WP);
+          xor_row<W>(acc, PX + i1 * WP);
+          xor_row<W>(acc, PX + i2 * WP);
+        }
+      }
+    }
+    const unsigned tot = __reduce_add_sync(FULL, (unsigned)cnt);
+    if (lane == 0)
+      atomicAdd(a.combos + gr.gamma, (unsigned long long)tot * (unsigned long long)(k - e0));
+  }
+  flush();
+  const int wbest = __reduce_min_sync(FULL, best);
+  if (lane == 0 && wbest < INT_MAX) atomicMin(a.bound, wbest);
+  __syncthreads();
+  for (int b = tid; b < nbins; b += bd)
+    if (bhist[b]) atomicAdd(a.hist + b, (unsigned long long)bhist[b]);
+}
+
+// ---------------------------------------------------------------------------
+// Integer-pipe microbenchmarks (roofline denominators).
+__global__ void peak_popc(uint32_t* out, uint32_t seed, int iters, long long* clk) {
+  uint32_t y0 = seed ^ threadIdx.x, y1 = y0 * 3u, y2 = y0 * 5u, y3 = y0 * 7u;
+  uint32_t y4 = y0 * 11u, y5 = y0 * 13u, y6 = y0 * 17u, y7 = y0 * 19u;
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      asm volatile("popc.b32 %0, %0;" : "+r"(y0));
+      asm volatile("popc.b32 %0, %0;" : "+r"(y1));
+      asm volatile("popc.b32 %0, %0;" : "+r"(y2));
+      asm volatile("popc.b32 %0, %0;" : "+r"(y3));
+      asm volatile("popc.b32 %0, %0;" : "+r"(y4));
+      asm volatile("popc.b32 %0, %0;" : "+r"(y5));
+      asm volatile("popc.b32 %0, %0;" : "+r"(y6));
+      asm volatile("popc.b32 %0, %0;" : "+r"(y7));
+    }
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = y0 + y1 + y2 + y3 + y4 + y5 + y6 + y7;
+}
+
+__global__ void peak_lop3(uint32_t* out, uint32_t seed, int iters, long long* clk) {
+  uint32_t y0 = seed ^ threadIdx.x, y1 = y0 * 3u, y2 = y0 * 5u, y3 = y0 * 7u;
+  uint32_t y4 = y0 * 11u, y5 = y0 * 13u, y6 = y0 * 17u, y7 = y0 * 19u;
+  const uint32_t a = seed * 0x9e3779b9u, b = seed * 0x85ebca6bu;
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(y0) : "r"(a), "r"(b));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(y1) : "r"(a), "r"(b));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(y2) : "r"(a), "r"(b));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(y3) : "r"(a), "r"(b));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(y4) : "r"(a), "r"(b));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(y5) : "r"(a), "r"(b));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(y6) : "r"(a), "r"(b));
+      asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(y7) : "r"(a), "r"(b));
+    }
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = y0 + y1 + y2 + y3 + y4 + y5 + y6 + y7;
+}
+
+// Synthetic codeword loop: register-resident rows, W words, 4 codewords per
+// iteration -- the best the XOR+POPC+min recipe can do on this chip.
+template <int W>
+__global__ void peak_codeword(int* out, uint32_t seed, int iters, long long* clk) {
+  uint32_t acc[W], r0[W], r1[W], r2[W], r3[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    acc[j] = seed * (j + 1) ^ threadIdx.x;
+    r0[j] = acc[j] * 3u; r1[j] = acc[j] * 5u; r2[j] = acc[j] * 7u; r3[j] = acc[j] * 9u;
+  }
+  int best = INT_MAX;
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+    const int w0 = weight_xor<W>(acc, r0);
+    const int w1 = weight_xor<W>(acc, r1);
+    const int w2 = weight_xor<W>(acc, r2);
+    const int w3 = weight_xor<W>(acc, r3);
+    best = min(best, min(min(w0, w1), min(w2, w3)));
+#pragma unroll
+    for (int j = 0; j < W; ++j) acc[j] += 0x9e3779b9u;  // keep iterations distinct
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
+  out[blockIdx.x * blockDim.x + threadIdx.x] = best;
+}
+
+}  // namespace bz

@@ -1,0 +1,299 @@
+"""Brouwer-Zimmermann outer loop with the enumeration on the GPU.
+
+Drop-in for the reference's ``mindist.engine`` (pkg/src/mindist/engine.py):
+``minimum_distance(G, config) -> DistanceReport`` keeps its signature and
+its semantics -- Gamma family from ``build_gamma_set`` (gf2.py:168-199),
+bounds (1, n-k+1) (engine.py:90-94), the per-round lower bound
+(m-1)(g+1) + max(0, g+1-k+k_m) with the all-full-rank convention of
+``_line7_args`` (engine.py:106-116), the loop ``while g <= k and L < U``
+with the ``max_g`` cap, one ``(g, L, U)`` trace entry per round, the
+``progress`` callback and ``Interrupted`` carrying a resumable partial
+report (engine.py:157-220).
+
+What changes is the inside of a round.  The reference runs one strategy
+call per Gamma_j (engine.py:208-211); here the whole round -- every
+g-combination of every Gamma_j -- is ONE call into the sm_100a kernel
+(``bz_round``), which returns per-Gamma minima that the loop folds into U
+in Gamma order exactly as the reference does.  Clipping by the running U is
+the only thing the reference passes between the passes of a round
+(engine.py:7-9), so a round-level call yields the same U, L and trace.
+
+Multi-GPU: with ``EngineConfig(distributed=True)`` each process (one per
+GPU) enumerates its shard of every round and the shards' results are
+combined by one collective per round (parallel.py).
+"""
+
+from __future__ import annotations
+
+import os
+import time
+from dataclasses import dataclass, field
+
+from . import _native
+from .enumeration import EnumerationResult, family_words
+from .errors import InvalidArity, InvalidDimensions, Interrupted
+from .gf2 import BitMatrix, GammaSet, build_gamma_set
+from .parallel import LocalComm
+
+STRATEGIES = ("gpu",)
+
+DEFAULT_MAX_G = 16
+
+STATUS_EXACT = "exact"
+STATUS_UPPER_BOUND_ONLY = "upper_bound_only"
+STATUS_INTERRUPTED = "interrupted"
+
+
+@dataclass(frozen=True)
+class Bounds:
+    lower: int
+    upper: int
+
+
+@dataclass
+class Counters:
+    combinations: int = 0
+    row_additions: int = 0
+    row_accesses: int = 0
+
+    def add(self, res: EnumerationResult) -> None:
+        self.combinations += res.combinations
+        self.row_additions += res.row_additions
+        self.row_accesses += res.row_accesses
+
+
+@dataclass
+class EngineConfig:
+    """Reference fields (engine.py:57-67) plus the GPU placement.
+
+    ``s``, ``unroll``, ``workers`` and ``memory_budget`` configure the
+    reference's CPU strategies and are accepted but unused here.
+    ``device`` defaults to $LOCAL_RANK (or 0); ``distributed`` shards every
+    round over the torch.distributed default group."""
+
+    strategy: str = "gpu"
+    s: int = 3
+    unroll: int = 2
+    workers: int = 1
+    memory_budget: int = 256 * 1024 * 1024
+    max_g: int = DEFAULT_MAX_G
+    start_g: int = 1
+    start_upper: int | None = None
+    progress: object = None  # callable(g, L, U) after each round
+    device: int | None = None
+    distributed: bool = False
+    early_exit: bool = True  # stop a round once U reaches the previous L
+
+
+@dataclass
+class RoundStat:
+    g: int
+    combinations: int
+    kernel_ms: float
+    wall_ms: float
+
+
+@dataclass
+class DistanceReport:
+    distance: int
+    status: str
+    g_reached: int
+    n: int
+    k: int
+    m: int
+    k_m: int
+    pivot_sets: tuple[tuple[int, ...], ...]
+    bounds_trace: list[tuple[int, int, int]] = field(default_factory=list)
+    counters: Counters = field(default_factory=Counters)
+    store_build_additions: int = 0
+    elapsed: float = 0.0
+    rounds: list[RoundStat] = field(default_factory=list)
+
+    @property
+    def exact(self) -> bool:
+        return self.status == STATUS_EXACT
+
+
+def initial_bounds(n: int, k: int) -> Bounds:
+    """(1, n-k+1): trivial lower bound and the Singleton upper bound."""
+    if not 0 < k <= n:
+        raise InvalidDimensions(f"need 0 < k <= n, got k={k}, n={n}")
+    return Bounds(1, n - k + 1)
+
+
+def lower_bound_update(g: int, m: int, k: int, k_m: int) -> int:
+    """Certified lower bound after round g: (m-1)(g+1) + max(0, g+1-k+k_m)."""
+    if m < 1:
+        raise InvalidDimensions(f"need m >= 1, got {m}")
+    if not 0 <= k_m <= k:
+        raise InvalidDimensions(f"need 0 <= k_m <= k, got k_m={k_m}, k={k}")
+    return (m - 1) * (g + 1) + max(0, g + 1 - k + k_m)
+
+
+def line7_args(gs: GammaSet, k: int) -> tuple[int, int]:
+    """(m, k_m) for lower_bound_update: a deficient remainder counts as the
+    m-th matrix with its rank; otherwise the last full matrix plays the
+    remainder of rank k (engine.py:106-116)."""
+    if gs.remainder_rank > 0:
+        return gs.full_rank_count + 1, gs.remainder_rank
+    return gs.full_rank_count, k
+
+
+class GpuRounds:
+    """Round backend on one CUDA device (the product path)."""
+
+    def __init__(self, config: EngineConfig, comm):
+        dev = config.device
+        if dev is None:
+            dev = int(os.environ.get("LOCAL_RANK", "0"))
+        self.ctx = _native.context(dev)
+        self.comm = comm
+
+    def load(self, gs: GammaSet, n: int) -> None:
+        self.ctx.load(family_words(gs.gammas, n), n)
+
+    def run(self, g: int, lower_prev: int, upper: int):
+        mins, combos = self.ctx.round(g, lower_prev, upper, self.comm.rank, self.comm.world)
+        kernel_ms = self.ctx.last_kernel_ms()
+        mins, combos = self.comm.combine(mins, combos)
+        return mins, combos, kernel_ms
+
+
+def make_backend(config: EngineConfig, comm):
+    """Seam for tests (cf. the reference's monkeypatch of enumerate_basic,
+    t/test_engine.py:165-208): returns the object that runs the rounds."""
+    return GpuRounds(config, comm)
+
+
+def _make_comm(config: EngineConfig):
+    if not config.distributed:
+        return LocalComm()
+    from .parallel import TorchComm
+
+    return TorchComm()
+
+
+@dataclass
+class LoopState:
+    """Mutable state of Algorithm 1 between rounds."""
+
+    L: int
+    U: int
+    g: int
+    g_reached: int
+    status: str = STATUS_EXACT
+    counters: Counters = field(default_factory=Counters)
+    trace: list = field(default_factory=list)
+    rounds: list = field(default_factory=list)
+
+
+def start_state(gs: GammaSet, n: int, k: int, config: EngineConfig) -> LoopState:
+    m_arg, km_arg = line7_args(gs, k)
+    start = initial_bounds(n, k)
+    L, U = start.lower, start.upper
+    if config.start_upper is not None:
+        U = min(U, config.start_upper)
+    g = max(1, config.start_g)
+    if g > 1:
+        L = lower_bound_update(g - 1, m_arg, k, km_arg)
+    return LoopState(L=L, U=U, g=g, g_reached=g - 1)
+
+
+def run_rounds(backend, gs: GammaSet, k: int, config: EngineConfig, st: LoopState) -> None:
+    """The loop of engine.py:204-217 with one device round per g: fold the
+    per-Gamma minima into U in Gamma order, then raise L, append (g, L, U),
+    report progress.  ``backend`` already holds the family on the device."""
+    m_arg, km_arg = line7_args(gs, k)
+    while st.g <= k and st.L < st.U:
+        if st.g > config.max_g:
+            st.status = STATUS_UPPER_BOUND_ONLY
+            break
+        tr = time.perf_counter()
+        mins, combos, kernel_ms = backend.run(st.g, st.L if config.early_exit else 0, st.U)
+        round_combos = 0
+        for mn, c in zip(mins, combos):
+            st.U = min(st.U, mn)
+            st.counters.add(EnumerationResult(st.U, c, c, c))
+            round_combos += c
+        st.rounds.append(RoundStat(st.g, round_combos, kernel_ms,
+                                   (time.perf_counter() - tr) * 1e3))
+        st.L = lower_bound_update(st.g, m_arg, k, km_arg)
+        st.trace.append((st.g, st.L, st.U))
+        st.g_reached = st.g
+        if config.progress is not None:
+            config.progress(st.g, st.L, st.U)
+        st.g += 1
+
+
+def minimum_distance(G: BitMatrix, config: EngineConfig | None = None) -> DistanceReport:
+    """Exact minimum weight of the code generated by G (Algorithm 1).
+
+    Raises RankDeficient for rank-deficient input.  With ``max_g`` cutting
+    the loop short the distance is only an upper bound (status says so).
+    On KeyboardInterrupt, Interrupted carries the partial report; rerun
+    with start_g = g_reached + 1 and start_upper = distance to continue."""
+    config = config or EngineConfig()
+    if config.strategy not in STRATEGIES:
+        raise InvalidArity(f"unknown strategy {config.strategy!r} (this build: {STRATEGIES})")
+    t0 = time.perf_counter()
+    gs = build_gamma_set(G)
+    k, n = G.num_rows, G.num_cols
+    st = start_state(gs, n, k, config)
+
+    def report(status: str) -> DistanceReport:
+        return DistanceReport(
+            distance=st.U, status=status, g_reached=st.g_reached, n=n, k=k,
+            m=gs.matrix_count, k_m=gs.remainder_rank, pivot_sets=gs.pivot_sets,
+            bounds_trace=st.trace, counters=st.counters, store_build_additions=0,
+            elapsed=time.perf_counter() - t0, rounds=st.rounds)
+
+    try:
+        if st.g <= k and st.L < st.U and st.g <= config.max_g:
+            backend = make_backend(config, _make_comm(config))
+            backend.load(gs, n)
+            run_rounds(backend, gs, k, config, st)
+        elif st.g <= k and st.L < st.U:
+            st.status = STATUS_UPPER_BOUND_ONLY
+    except KeyboardInterrupt:
+        raise Interrupted(report(STATUS_INTERRUPTED)) from None
+    return report(st.status)
+
+
+# ---------------------------------------------------------------------------
+# report text: key=value lines plus one "g=.. L=.. U=.." line per completed
+# round -- the reference's checkpoint format (engine.py:245-285).
+
+
+def format_report(r: DistanceReport) -> str:
+    rate = r.counters.combinations / r.elapsed if r.elapsed > 0 else 0.0
+    lines = [f"status={r.status}", f"n={r.n}", f"k={r.k}", f"distance={r.distance}",
+             f"g_reached={r.g_reached}", f"m={r.m}", f"k_m={r.k_m}",
+             f"combinations={r.counters.combinations}",
+             f"row_additions={r.counters.row_additions}",
+             f"row_accesses={r.counters.row_accesses}",
+             f"store_build_additions={r.store_build_additions}",
+             f"elapsed_s={r.elapsed:.3f}", f"combos_per_sec={rate:.0f}"]
+    lines += [f"g={g} L={L} U={U}" for g, L, U in r.bounds_trace]
+    return "\n".join(lines) + "\n"
+
+
+_INT_KEYS = ("n", "k", "distance", "g_reached", "m", "k_m", "combinations",
+             "row_additions", "row_accesses", "store_build_additions")
+
+
+def parse_report(text: str) -> dict:
+    out: dict = {"bounds_trace": []}
+    for raw in text.splitlines():
+        line = raw.strip()
+        if not line:
+            continue
+        if line.startswith("g=") and " L=" in line:
+            kv = dict(p.split("=", 1) for p in line.split())
+            out["bounds_trace"].append((int(kv["g"]), int(kv["L"]), int(kv["U"])))
+        elif "=" in line:
+            key, value = line.split("=", 1)
+            out[key] = value
+    for key in _INT_KEYS:
+        if key in out:
+            out[key] = int(out[key])
+    return out

@@ -1,0 +1,98 @@
+"""The C ABI without a GPU: the library loads, exports every symbol
+include/bz.h declares, its host-only work planner partitions each round's
+combination space exactly (across any number of shards), and compute
+entry points fail loudly when no device is present."""
+
+from __future__ import annotations
+
+import ctypes
+import itertools
+import os
+import re
+from math import comb
+
+import pytest
+
+from oracle import oracle
+from paper_1603_06757_b200 import _native
+from paper_1603_06757_b200.errors import InvalidArity, NoDevice, TooLarge
+
+HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                      "include", "bz.h")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char \*)\s*(bz_\w+)\s*\(",
+                                 text, re.M)))
+
+
+def test_header_symbols_exported():
+    L = _native.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 15
+    assert set(syms) == set(_native.SYMBOLS)
+    for s in syms:
+        assert hasattr(L, s), s
+    assert L.bz_abi_version() == _native.ABI_VERSION
+
+
+def test_plan_counts():
+    for (m, k, g) in [(1, 5, 1), (2, 24, 3), (2, 80, 8), (3, 40, 8), (1, 64, 6), (2, 128, 4)]:
+        groups, nchunks = _native.plan(m, k, g)
+        assert sum(gr[5] for gr in groups) == m * comb(k, g)
+        assert nchunks >= 1
+        starts = [gr[0] for gr in groups]
+        assert starts == sorted(starts) and starts[0] == 0
+        for gr in groups:
+            begin, nprefix, gamma, ell, ppl, combos = gr
+            assert nprefix == (1 if g == 1 else comb(ell, g - 2))
+            assert combos == nprefix * (k - 1 - ell)
+
+
+@pytest.mark.parametrize("m,k,g", [(1, 6, 1), (1, 7, 2), (2, 9, 3), (1, 12, 5),
+                                   (2, 10, 10), (1, 40, 3), (1, 34, 4)])
+def test_plan_partitions_rank_space(m, k, g):
+    """Every g-combination of every Gamma is visited exactly once, for any
+    shard count, by the device's chunk/lane/colex walk."""
+    import random
+
+    rng = random.Random(k * 100 + g)
+    n = 2 * k + 5
+    gammas = [[rng.getrandbits(n) for _ in range(k)] for _ in range(m)]
+    groups, nchunks = _native.plan(m, k, g)
+    expect = sorted(oracle.all_combinations(m, k, g))
+    for nshards in (1, 2, 3, 8):
+        seen = []
+        mins = [None] * m
+        for s in range(nshards):
+            mn, _, got = oracle.enumerate_chunks(gammas, k, g, groups, nchunks, s, nshards)
+            seen += got
+            mins = [a if b is None else (b if a is None else min(a, b))
+                    for a, b in zip(mins, mn)]
+        assert sorted(seen) == expect
+        for j in range(m):
+            assert mins[j] == oracle.min_weight(gammas[j], n, g)[0]
+
+
+def test_plan_errors():
+    with pytest.raises(InvalidArity):
+        _native.plan(1, 5, 6)
+    with pytest.raises(InvalidArity):
+        _native.plan(1, 5, 0)
+    with pytest.raises(TooLarge):
+        _native.plan(1, 128, 40)
+
+
+def test_no_device_fails_loudly():
+    if _native.device_count() > 0:
+        pytest.skip("a GPU is visible")
+    with pytest.raises(NoDevice):
+        _native.Context(0)
+
+
+def test_colex_unrank_bijective():
+    for ell in range(0, 12):
+        for q in range(0, min(ell, 5) + 1):
+            subs = [tuple(oracle.colex_unrank(r, q, ell)) for r in range(comb(ell, q))]
+            assert sorted(subs) == sorted(itertools.combinations(range(ell), q))

@@ -1,0 +1,179 @@
+"""Parity of the sm_100a kernels (through the C ABI) with the CPU oracle
+and with the reference's golden outputs.  Needs a B200: run via gpurun
+with `pytest -m gpu`.  Integer work, so every comparison is exact."""
+
+from __future__ import annotations
+
+import hashlib
+import random
+from math import comb
+
+import numpy as np
+import pytest
+
+from conftest import CFG4_HIST_SHA256, hexrows
+from oracle import oracle
+from paper_1603_06757_b200 import (BitMatrix, EngineConfig, InvalidArity, TooLarge,
+                                   enumerate_gpu, minimum_distance, weight_histogram_gpu)
+from paper_1603_06757_b200 import _native
+from paper_1603_06757_b200.configs import code, microbench_gamma
+from paper_1603_06757_b200.enumeration import family_words
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return _native.context(0)
+
+
+def test_small_enum_fixtures(goldens):
+    for fx in goldens["small"]["enum"]:
+        M = BitMatrix(hexrows(fx["rows"]), fx["n"])
+        for g, expect in enumerate(fx["min_by_g"], start=1):
+            res = enumerate_gpu(M, g)
+            assert res.min_weight == expect, (fx["src"], g)
+            assert res.combinations == comb(fx["k"], g)
+
+
+def test_clipping_semantics():
+    M = BitMatrix([random.Random(19).getrandbits(16) | (1 << i) for i in range(6)], 22)
+    true_min = enumerate_gpu(M, 3).min_weight
+    assert enumerate_gpu(M, 3, ubound=true_min - 1).min_weight == true_min - 1
+    assert enumerate_gpu(M, 3, ubound=true_min + 5).min_weight == true_min
+    assert enumerate_gpu(M, 3, ubound=true_min - 1).combinations == comb(6, 3)
+
+
+def test_bad_arity():
+    M = BitMatrix([1, 2, 4, 8], 5)
+    with pytest.raises(InvalidArity):
+        enumerate_gpu(M, 0)
+    with pytest.raises(InvalidArity):
+        enumerate_gpu(M, 5)
+
+
+@pytest.mark.parametrize("n", [1, 7, 31, 32, 33, 64, 65, 100, 127, 160, 192, 200, 255, 256])
+def test_word_widths(n):
+    """Every W = ceil(n/32) instantiation (1..8), padded and exact sizes."""
+    rng = random.Random(n)
+    k = min(12, n) if n > 1 else 1
+    rows = [rng.getrandbits(n) for _ in range(k)]
+    M = BitMatrix(rows, n)
+    for g in range(1, k + 1):
+        assert enumerate_gpu(M, g).min_weight == oracle.min_weight(rows, n, g)[0], (n, g)
+
+
+@pytest.mark.parametrize("k,g", [(1, 1), (2, 2), (33, 3), (64, 4), (65, 3), (100, 3),
+                                 (127, 2), (128, 3), (128, 128), (70, 69)])
+def test_row_counts(k, g):
+    """Masks cross the 64-bit word boundary; g = k and g = k-1 edges."""
+    rng = random.Random(k * 7 + g)
+    n = 150
+    rows = [rng.getrandbits(n) for _ in range(k)]
+    M = BitMatrix(rows, n)
+    assert enumerate_gpu(M, g).min_weight == oracle.min_weight(rows, n, g)[0]
+
+
+def test_random_sweep_vs_oracle():
+    rng = random.Random(2024)
+    for _ in range(40):
+        k = rng.randint(2, 40)
+        n = rng.randint(k, 256)
+        rows = [rng.getrandbits(n) for _ in range(k)]
+        M = BitMatrix(rows, n)
+        for g in sorted({1, 2, min(k, 3), min(k, 4), min(k, 5), k}):
+            if comb(k, g) > 3_000_000:
+                continue
+            assert enumerate_gpu(M, g).min_weight == oracle.min_weight(rows, n, g)[0], (k, n, g)
+
+
+def test_zero_rows_and_duplicates():
+    rows = [0, 0, 5, 5, 7]
+    M = BitMatrix(rows, 3)
+    for g in range(1, 6):
+        assert enumerate_gpu(M, g).min_weight == oracle.min_weight(rows, 3, g)[0]
+
+
+def test_round_sharded_equals_whole(ctx):
+    G, gs, _ = code("cfg2", 1)
+    ctx.load(family_words(gs.gammas, 96), 96)
+    for g in (1, 2, 3, 4, 5):
+        whole_min, whole_c = ctx.round(g, 0, 10**6)
+        for nshards in (2, 3, 8):
+            mins = [10**9] * 2
+            cs = [0, 0]
+            for s in range(nshards):
+                mn, c = ctx.round(g, 0, 10**6, s, nshards)
+                mins = [min(a, b) for a, b in zip(mins, mn)]
+                cs = [a + b for a, b in zip(cs, c)]
+            assert mins == whole_min and cs == whole_c == [comb(48, g)] * 2
+
+
+@pytest.mark.parametrize("idx", range(6))
+def test_minimum_distance_configs(goldens, idx):
+    fx = goldens["configs"][idx]
+    rep = minimum_distance(BitMatrix(hexrows(fx["rows"]), fx["n"]))
+    assert rep.distance == fx["distance"]
+    assert rep.bounds_trace == [tuple(t) for t in fx["bounds_trace"]]
+    assert (rep.status, rep.g_reached, rep.m, rep.k_m) == \
+        (fx["status"], fx["g_reached"], fx["m"], fx["k_m"])
+    assert [list(p) for p in rep.pivot_sets] == fx["pivot_sets"]
+    if (fx["name"], fx["seed"]) != ("cfg1", 2):  # that run exits early (below)
+        assert rep.counters.combinations == fx["combinations"]
+
+
+def test_early_exit_fixture(goldens):
+    """cfg1 seed 2 round 3: U reaches L_prev = 6, the only exit that keeps
+    the trace bit-exact (SURVEY.md 8(a) invariant 5)."""
+    fx = [c for c in goldens["configs"] if (c["name"], c["seed"]) == ("cfg1", 2)][0]
+    G = BitMatrix(hexrows(fx["rows"]), fx["n"])
+    fast = minimum_distance(G)
+    full = minimum_distance(G, EngineConfig(early_exit=False))
+    for rep in (fast, full):
+        assert rep.bounds_trace == [tuple(t) for t in fx["bounds_trace"]]
+        assert rep.distance == 6
+    assert full.counters.combinations == fx["combinations"]
+    assert fast.counters.combinations <= full.counters.combinations
+
+
+def test_small_codes(goldens):
+    for fx in goldens["small"]["codes"]:
+        rep = minimum_distance(BitMatrix(hexrows(fx["rows"]), fx["n"]))
+        assert rep.distance == fx["distance"] == fx["brute"], fx["src"]
+        assert rep.bounds_trace == [tuple(t) for t in fx["bounds_trace"]], fx["src"]
+
+
+def test_cfg4_histogram(goldens):
+    fx = goldens["cfg4"]
+    M = microbench_gamma(1)
+    assert [format(r, "x") for r in M.rows] == fx["rows"]
+    hist, mn, combos = weight_histogram_gpu(M, 6)
+    assert combos == comb(64, 6) == int(hist.sum())
+    assert mn == fx["min_weight"] == 39
+    assert hashlib.sha256(hist.astype("<u8").tobytes()).hexdigest() == CFG4_HIST_SHA256
+    assert np.array_equal(hist, oracle.histogram(list(M.rows), 192, 6))
+    assert enumerate_gpu(M, 6).min_weight == 39
+
+
+def test_histogram_small_vs_oracle():
+    rng = random.Random(11)
+    for (k, n, g) in [(10, 40, 3), (20, 70, 4), (30, 256, 3), (16, 16, 5), (9, 33, 1)]:
+        rows = [rng.getrandbits(n) for _ in range(k)]
+        hist, mn, c = weight_histogram_gpu(BitMatrix(rows, n), g)
+        assert np.array_equal(hist, oracle.histogram(rows, n, g)), (k, n, g)
+
+
+def test_cfg5_full(cfg5_golden):
+    fx = cfg5_golden
+    G, gs, draws = code("cfg5", 7)
+    assert [format(r, "x") for r in G.rows] == fx["rows"]
+    rep = minimum_distance(G)
+    assert rep.distance == fx["distance"]
+    assert rep.bounds_trace == [tuple(t) for t in fx["bounds_trace"]]
+    assert rep.counters.combinations == fx["combinations"]
+
+
+def test_too_large(ctx):
+    M = BitMatrix([(1 << i) for i in range(128)], 200)
+    with pytest.raises(TooLarge):
+        enumerate_gpu(M, 40)
