@@ -108,14 +108,15 @@ int bz_histogram(bz_ctx *ctx, int gamma, int g, int shard, int nshards,
                  uint64_t *out_hist, int32_t *out_min, uint64_t *out_combos);
 
 /* Host-only: the work plan bz_round uses for (m, k, g), for inspection and
- * for the CPU tests of the sharding logic.  Writes *out_ngroups groups of 6
+ * for the CPU tests of the sharding logic.  Writes *out_ngroups groups of 7
  * int64 each -- chunk_begin, nprefix, gamma, ell, prefixes_per_lane,
- * combinations -- into out (capacity `cap` groups; out may be NULL to query
- * the count) and the round's chunk count into *out_nchunks.  Chunk c of the
- * round belongs to shard c % nshards; within a chunk of group (gamma, ell),
- * lane l of the warp walks the colex ranks [(c_local*32 + l)*ppl, +ppl) of
- * the (g-2)-subsets of [0, ell), each extended by ell and then by every
- * suffix row e in (ell, k). */
+ * combinations, depth -- into out (capacity `cap` groups; out may be NULL to
+ * query the count) and the round's chunk count into *out_nchunks.  Chunk c
+ * of the round belongs to shard c % nshards; within a chunk of group
+ * (gamma, ell), lane l of the warp walks the colex ranks
+ * [(c_local*32 + l)*ppl, +ppl) of the (g-1-depth)-subsets of [0, ell), each
+ * extended by ell and then by every depth-subset of the suffix rows
+ * (ell, k).  depth = 2 for g >= 3, else 1 (g = 1: ell = -1, empty prefix). */
 int bz_plan(int m, int k, int g, int64_t *out, int cap, int *out_ngroups,
             uint64_t *out_nchunks);
 

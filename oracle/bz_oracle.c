@@ -34,7 +34,7 @@
 #include <unistd.h>
 
 #define BZO_MAXW 8
-#define BZO_MAXG 64
+#define BZO_MAXG 130
 
 /* Host threads usable by this process (sched affinity). */
 int bzo_max_threads(void) {

@@ -237,7 +237,8 @@ def enumerate_chunks(gammas: list[list[int]], k: int, g: int, groups, nchunks: i
                      shard: int, nshards: int, hist_bins: int | None = None):
     """Visit every combination of the chunks owned by `shard` exactly as the
     device kernel does (chunk c -> shard c % nshards; lane-major prefix
-    ranges of ppl colex ranks; suffix loop e in (ell, k)).  Returns
+    ranges of ppl colex ranks of (g-1-depth)-subsets of [0, ell), plus ell;
+    then every depth-subset of the suffix rows (ell, k)).  Returns
     (per-gamma minima, per-gamma combos, list of visited combos)."""
     m = len(gammas)
     mins = [None] * m
@@ -246,21 +247,24 @@ def enumerate_chunks(gammas: list[list[int]], k: int, g: int, groups, nchunks: i
     starts = [gr[0] for gr in groups]
     for chunk in range(shard, nchunks, nshards):
         gi = max(i for i, s in enumerate(starts) if s <= chunk)
-        begin, nprefix, gamma, ell, ppl = groups[gi][:5]
+        begin, nprefix, gamma, ell, ppl, _, depth = groups[gi]
         local = chunk - begin
         rows = gammas[gamma]
         for lane in range(32):
             first = (local * 32 + lane) * ppl
             for p in range(first, min(first + ppl, nprefix)):
-                prefix = [] if g == 1 else colex_unrank(p, g - 2, ell) + [ell]
+                prefix = [] if g == 1 else colex_unrank(p, g - 1 - depth, ell) + [ell]
                 acc = 0
                 for i in prefix:
                     acc ^= rows[i]
-                for e in range(ell + 1, k):
-                    w = (acc ^ rows[e]).bit_count()
+                for suf in itertools.combinations(range(ell + 1, k), depth):
+                    w = acc
+                    for e in suf:
+                        w ^= rows[e]
+                    w = w.bit_count()
                     mins[gamma] = w if mins[gamma] is None else min(mins[gamma], w)
                     cnt[gamma] += 1
-                    seen.append((gamma, tuple(prefix + [e])))
+                    seen.append((gamma, tuple(prefix + list(suf))))
     return mins, cnt, seen
 
 

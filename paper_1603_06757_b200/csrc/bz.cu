@@ -54,7 +54,11 @@ struct bz_ctx {
 
 namespace {
 
-constexpr long long kLaneTarget = 4096;  // codewords per lane per chunk
+// Codewords per lane per chunk: aim for ~40k chunks per round (dynamic
+// balance over 148 SMs x 32 warps), within [32, 4096].  Depends only on the
+// problem size, so every process computes the same plan.
+constexpr long long kChunksTarget = 40000;
+constexpr long long kLaneMin = 32, kLaneMax = 4096;
 
 int fail(bz_ctx* c, int code, const char* fmt, ...) {
   char buf[512];
@@ -108,16 +112,20 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, std::vector<Gro
   unsigned long long chunk = 0;
   const int j0 = gamma_only < 0 ? 0 : gamma_only;
   const int j1 = gamma_only < 0 ? m : gamma_only + 1;
+  const int depth = g >= 3 ? 2 : 1;
+  const unsigned long long total = binom_sat(k, g) * (unsigned long long)(j1 - j0);
+  long long lane_target = (long long)(total / (32ull * kChunksTarget));
+  lane_target = std::min(kLaneMax, std::max(kLaneMin, lane_target));
   for (int j = j0; j < j1; ++j) {
-    const int ell_lo = g == 1 ? -1 : g - 2;
-    const int ell_hi = g == 1 ? -1 : k - 2;
+    const int ell_lo = g == 1 ? -1 : g - 1 - depth;
+    const int ell_hi = g == 1 ? -1 : k - 1 - depth;
     for (int ell = ell_lo; ell <= ell_hi; ++ell) {
-      const unsigned long long np = g == 1 ? 1ull : binom_sat(ell, g - 2);
+      const unsigned long long np = g == 1 ? 1ull : binom_sat(ell, g - 1 - depth);
       if (np == 0) continue;
       if (np >= (1ull << 62))
-        return fail(ctx, BZ_ERR_TOO_LARGE, "C(%d,%d) prefixes exceed 2^62", ell, g - 2);
-      const long long looplen = k - 1 - ell;
-      long long ppl = std::max(1ll, kLaneTarget / looplen);
+        return fail(ctx, BZ_ERR_TOO_LARGE, "C(%d,%d) prefixes exceed 2^62", ell, g - 1 - depth);
+      const long long work = (long long)binom_sat(k - 1 - ell, depth);
+      long long ppl = std::max(1ll, lane_target / std::max(1ll, work));
       const long long spread = (long long)((np + 31) / 32);
       ppl = std::min(ppl, std::max(1ll, spread));
       Group gr{};
@@ -126,6 +134,7 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, std::vector<Gro
       gr.gamma = j;
       gr.ell = ell;
       gr.ppl = (int)ppl;
+      gr.depth = depth;
       const unsigned long long per_chunk = 32ull * (unsigned long long)ppl;
       chunk += (np + per_chunk - 1) / per_chunk;
       gs.push_back(gr);
@@ -159,8 +168,8 @@ int check_g(bz_ctx* ctx, int g) {
   return BZ_OK;
 }
 
-template <int W>
-int launch_w(bz_ctx* ctx, const RoundArgs& a, bool hist) {
+template <int W, int D>
+int launch_wd(bz_ctx* ctx, const RoundArgs& a, bool hist) {
   size_t smem = bz::smem_base_bytes<W>(a.m, a.k, a.ngroups);
   int threads = 256;
   if (hist) {
@@ -171,17 +180,17 @@ int launch_w(bz_ctx* ctx, const RoundArgs& a, bool hist) {
     while (threads > 32 && smem + (size_t)(a.n + 1) * threads * 2 > (size_t)dev_max / 2)
       threads /= 2;
     smem += (size_t)(a.n + 1) * threads * 2;
-    CK(cudaFuncSetAttribute(bz::k1h_histogram<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(bz::k1h_histogram<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
   } else {
-    CK(cudaFuncSetAttribute(bz::k1_round_min<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(bz::k1_round_min<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
   }
   int per_sm = 0;
   if (hist)
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bz::k1h_histogram<W>, threads, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bz::k1h_histogram<W, D>, threads, smem));
   else
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bz::k1_round_min<W>, threads, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bz::k1_round_min<W, D>, threads, smem));
   if (per_sm < 1) return fail(ctx, BZ_ERR_TOO_LARGE, "kernel does not fit on an SM (smem %zu)", smem);
   // persistent grid: one wave, but no more warps than chunks need
   unsigned long long warps_needed = (a.nchunks + a.nshards - 1) / a.nshards;
@@ -190,13 +199,18 @@ int launch_w(bz_ctx* ctx, const RoundArgs& a, bool hist) {
   blocks = std::max(1ll, std::min(blocks, need));
   CK(cudaEventRecord(ctx->ev_k0, ctx->stream));
   if (hist)
-    bz::k1h_histogram<W><<<(unsigned)blocks, threads, smem, ctx->stream>>>(a);
+    bz::k1h_histogram<W, D><<<(unsigned)blocks, threads, smem, ctx->stream>>>(a);
   else
-    bz::k1_round_min<W><<<(unsigned)blocks, threads, smem, ctx->stream>>>(a);
+    bz::k1_round_min<W, D><<<(unsigned)blocks, threads, smem, ctx->stream>>>(a);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
   ctx->launches += 1;
   return BZ_OK;
+}
+
+template <int W>
+int launch_w(bz_ctx* ctx, const RoundArgs& a, bool hist) {
+  return a.g >= 3 ? launch_wd<W, 2>(ctx, a, hist) : launch_wd<W, 1>(ctx, a, hist);
 }
 
 int launch(bz_ctx* ctx, const RoundArgs& a, bool hist) {
@@ -487,12 +501,14 @@ int bz_plan(int m, int k, int g, int64_t* out, int cap, int* out_ngroups,
   if (out) {
     if ((int)gs.size() > cap) return BZ_ERR_ARGUMENT;
     for (size_t i = 0; i < gs.size(); ++i) {
-      out[6 * i + 0] = (int64_t)gs[i].chunk_begin;
-      out[6 * i + 1] = (int64_t)gs[i].nprefix;
-      out[6 * i + 2] = gs[i].gamma;
-      out[6 * i + 3] = gs[i].ell;
-      out[6 * i + 4] = gs[i].ppl;
-      out[6 * i + 5] = (int64_t)gs[i].nprefix * (k - 1 - gs[i].ell);
+      out[7 * i + 0] = (int64_t)gs[i].chunk_begin;
+      out[7 * i + 1] = (int64_t)gs[i].nprefix;
+      out[7 * i + 2] = gs[i].gamma;
+      out[7 * i + 3] = gs[i].ell;
+      out[7 * i + 4] = gs[i].ppl;
+      out[7 * i + 5] = (int64_t)gs[i].nprefix *
+                       (int64_t)binom_sat(k - 1 - gs[i].ell, gs[i].depth);
+      out[7 * i + 6] = gs[i].depth;
     }
   }
   return BZ_OK;

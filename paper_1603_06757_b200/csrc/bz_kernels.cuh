@@ -44,7 +44,7 @@ struct Group {
   int gamma;                       // matrix index
   int ell;                         // last prefix element (-1 when g == 1)
   int ppl;                         // prefixes per lane per chunk
-  int pad;
+  int depth;                       // suffix depth D of the round (1 or 2)
 };
 
 struct RoundArgs {
@@ -66,6 +66,10 @@ struct RoundArgs {
 __host__ __device__ constexpr int padded_words(int w) {
   return w <= 1 ? 1 : (w <= 2 ? 2 : (w <= 4 ? 4 : 8));
 }
+
+// Prefix-XOR rows are read at lane-divergent indices; an odd row stride in
+// shared memory spreads them over distinct banks (scalar LDS per word).
+__host__ __device__ constexpr int px_stride(int w) { return (w & 1) ? w : w + 1; }
 
 // 128-bit subset mask over row indices [0, 128).
 struct Mask {
@@ -137,7 +141,17 @@ __device__ __forceinline__ Mask colex_unrank(unsigned long long r, int q, int el
 template <int W>
 __device__ __forceinline__ void load_row(uint32_t (&r)[W], const uint32_t* p) {
   constexpr int WP = padded_words(W);
-  if constexpr (WP >= 4) {
+  if constexpr (W == 5 || W == 6 || W == 7) {
+    const uint4 v = reinterpret_cast<const uint4*>(p)[0];
+    r[0] = v.x; r[1] = v.y; r[2] = v.z; r[3] = v.w;
+    if constexpr (W == 5) {
+      r[4 % W] = p[4];
+    } else {
+      const uint2 u = reinterpret_cast<const uint2*>(p)[2];
+      r[4 % W] = u.x; r[5 % W] = u.y;
+      if constexpr (W == 7) r[6 % W] = p[6];
+    }
+  } else if constexpr (WP >= 4) {
 #pragma unroll
     for (int j = 0; j < WP / 4; ++j) {
       const uint4 v = reinterpret_cast<const uint4*>(p)[j];
@@ -171,6 +185,49 @@ __device__ __forceinline__ int weight_xor(const uint32_t (&acc)[W], const uint32
   return w;
 }
 
+template <int W>
+__device__ __forceinline__ void xor_px(uint32_t (&acc)[W], const uint32_t* px, int i) {
+  constexpr int PS = px_stride(W);
+#pragma unroll
+  for (int j = 0; j < W; ++j) acc[j] ^= px[i * PS + j];
+}
+
+// One lane-private walker over consecutive colex ranks of the (g-2)-subsets
+// of [0, ell): subset mask + XOR of its rows and of row ell.
+template <int W>
+struct Walker {
+  Mask x;
+  uint32_t acc[W];
+
+  __device__ __forceinline__ void init(unsigned long long rank, int q, int ell,
+                                       const uint32_t* R, const unsigned long long* binom) {
+    constexpr int WP = padded_words(W);
+#pragma unroll
+    for (int j = 0; j < W; ++j) acc[j] = 0u;
+    x = Mask{0ull, 0ull};
+    if (ell < 0) return;
+    xor_row<W>(acc, R + ell * WP);
+    if (q > 0) {
+      x = colex_unrank(rank, q, ell, binom);
+      Mask y = x;
+      while (y.lo | y.hi) {
+        const int b = mask_ctz(y);
+        xor_row<W>(acc, R + b * WP);
+        if (b < 64) y.lo &= y.lo - 1; else y.hi &= y.hi - 1;
+      }
+    }
+  }
+
+  // colex successor; PX[0] = 0, so the third row only matters for runs > 1
+  __device__ __forceinline__ void step(const uint32_t* PX) {
+    int i0, i1, i2;
+    colex_next(x, i0, i1, i2);
+    xor_px<W>(acc, PX, i0);
+    xor_px<W>(acc, PX, i1);
+    if (i2 > 0) xor_px<W>(acc, PX, i2);
+  }
+};
+
 // Locate the group owning `chunk` (groups sorted by chunk_begin).
 __device__ __forceinline__ int find_group(const Group* sg, int ngroups,
                                           unsigned long long chunk) {
@@ -186,7 +243,8 @@ __device__ __forceinline__ int find_group(const Group* sg, int ngroups,
 template <int W>
 __host__ __device__ inline size_t smem_base_bytes(int m, int k, int ngroups) {
   constexpr int WP = padded_words(W);
-  size_t words = (size_t)m * k * WP + (size_t)m * (k + 1) * WP;
+  constexpr int PS = px_stride(W);
+  size_t words = (size_t)m * k * WP + (size_t)m * (k + 1) * PS;
   size_t bytes = words * 4;
   bytes = (bytes + 15) & ~size_t(15);
   return bytes + (size_t)ngroups * sizeof(Group);
@@ -197,14 +255,19 @@ __device__ __forceinline__ void stage(const RoundArgs& a, uint32_t*& srows,
                                       uint32_t*& spx, Group*& sgroups,
                                       unsigned char* smem) {
   constexpr int WP = padded_words(W);
+  constexpr int PS = px_stride(W);
   const int nrow_words = a.m * a.k * WP;
-  const int npx_words = a.m * (a.k + 1) * WP;
+  const int npx_rows = a.m * (a.k + 1);
+  const int npx_words = npx_rows * PS;
   srows = reinterpret_cast<uint32_t*>(smem);
   spx = srows + nrow_words;
   size_t off = ((size_t)(nrow_words + npx_words) * 4 + 15) & ~size_t(15);
   sgroups = reinterpret_cast<Group*>(smem + off);
   for (int i = threadIdx.x; i < nrow_words; i += blockDim.x) srows[i] = a.rows[i];
-  for (int i = threadIdx.x; i < npx_words; i += blockDim.x) spx[i] = a.px[i];
+  for (int i = threadIdx.x; i < npx_words; i += blockDim.x) {
+    const int r = i / PS, j = i - r * PS;
+    spx[i] = j < W ? a.px[r * WP + j] : 0u;
+  }
   const int gw = a.ngroups * (int)(sizeof(Group) / 4);
   const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(a.groups);
   uint32_t* gdst = reinterpret_cast<uint32_t*>(sgroups);
@@ -212,9 +275,79 @@ __device__ __forceinline__ void stage(const RoundArgs& a, uint32_t*& srows,
   __syncthreads();
 }
 
+// Suffix enumeration of one prefix (row sum `acc`, last element ell):
+//   D = 1: codewords acc ^ R[e]           for ell < e < k
+//   D = 2: codewords acc ^ R[e1] ^ R[e2]  for ell < e1 < e2 < k
+// Two prefixes (walkers A and B) share every broadcast row load.  `visit`
+// receives the weight of each codeword of A and of B.
+template <int W, int D, typename Visit>
+__device__ __forceinline__ void suffix_pair(const uint32_t (&a)[W], const uint32_t (&b)[W],
+                                            const uint32_t* R, int e0, int k, Visit&& visit) {
+  constexpr int WP = padded_words(W);
+  if constexpr (D == 1) {
+    const uint32_t* re = R + e0 * WP;
+#pragma unroll 2
+    for (int e = e0; e < k; ++e, re += WP) {
+      uint32_t r0[W];
+      load_row<W>(r0, re);
+      visit(weight_xor<W>(a, r0), weight_xor<W>(b, r0));
+    }
+  } else {
+    const uint32_t* r1p = R + e0 * WP;
+#pragma unroll 1
+    for (int e1 = e0; e1 < k - 1; ++e1, r1p += WP) {
+      uint32_t r1[W], a1[W], b1[W];
+      load_row<W>(r1, r1p);
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        a1[j] = a[j] ^ r1[j];
+        b1[j] = b[j] ^ r1[j];
+      }
+      const uint32_t* re = r1p + WP;
+#pragma unroll 2
+      for (int e2 = e1 + 1; e2 < k; ++e2, re += WP) {
+        uint32_t r0[W];
+        load_row<W>(r0, re);
+        visit(weight_xor<W>(a1, r0), weight_xor<W>(b1, r0));
+      }
+    }
+  }
+}
+
+template <int D>
+__device__ __forceinline__ unsigned long long suffix_count(int k, int e0) {
+  const unsigned long long t = (unsigned long long)(k - e0);
+  return D == 1 ? t : t * (t - 1) / 2;
+}
+
+// Shared prologue of a chunk: the lane's prefix range [first, first+cnt).
+struct ChunkView {
+  Group gr;
+  unsigned long long first;
+  long long cnt;
+};
+
+__device__ __forceinline__ ChunkView open_chunk(const Group* sg, int ngroups,
+                                                unsigned long long chunk, int lane) {
+  ChunkView v;
+  v.gr = sg[find_group(sg, ngroups, chunk)];
+  const unsigned long long local = chunk - v.gr.chunk_begin;
+  v.first = (local * 32ull + lane) * (unsigned long long)v.gr.ppl;
+  v.cnt = 0;
+  if (v.first < v.gr.nprefix) {
+    const unsigned long long left = v.gr.nprefix - v.first;
+    v.cnt = left < (unsigned long long)v.gr.ppl ? (long long)left : v.gr.ppl;
+  }
+  return v;
+}
+
 // ---------------------------------------------------------------------------
 // K1: minimum-weight enumeration of one round (all Gammas, one shard).
-template <int W>
+// Each lane runs two walkers over the two halves of its prefix range so that
+// every broadcast row load feeds two codewords (and two independent
+// XOR/POPC chains).  When the range is odd the second walker duplicates the
+// first on the last step -- harmless for a minimum.
+template <int W, int D>
 __global__ void __launch_bounds__(256)
 k1_round_min(const RoundArgs a) {
   constexpr int WP = padded_words(W);
@@ -225,7 +358,7 @@ k1_round_min(const RoundArgs a) {
 
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
-  const int k = a.k, q = a.g - 2;
+  const int k = a.k, q = a.g - 1 - D;
   volatile int* vbound = a.bound;
 
   while (true) {
@@ -236,75 +369,43 @@ k1_round_min(const RoundArgs a) {
     if (chunk >= a.nchunks) break;
     if (vbound[0] <= a.lower_prev) break;
 
-    const Group gr = sgroups[find_group(sgroups, a.ngroups, chunk)];
-    const unsigned long long local = chunk - gr.chunk_begin;
-    const unsigned long long first = (local * 32ull + lane) * (unsigned long long)gr.ppl;
-    long long cnt = 0;
-    if (first < gr.nprefix) {
-      const unsigned long long left = gr.nprefix - first;
-      cnt = left < (unsigned long long)gr.ppl ? (long long)left : gr.ppl;
-    }
-    const long long maxcnt = __shfl_sync(FULL, cnt, 0);
-    const uint32_t* R = srows + gr.gamma * k * WP;
-    const uint32_t* PX = spx + gr.gamma * (k + 1) * WP;
-    const int e0 = gr.ell + 1;
+    const ChunkView v = open_chunk(sgroups, a.ngroups, chunk, lane);
+    const long long ca = (v.cnt + 1) >> 1;  // walker A: [first, first+ca)
+    const long long cb = v.cnt - ca;        // walker B: [first+ca, first+cnt)
+    const long long maxca = __shfl_sync(FULL, ca, 0);
+    const uint32_t* R = srows + v.gr.gamma * k * WP;
+    const uint32_t* PX = spx + v.gr.gamma * (k + 1) * px_stride(W);
+    const int e0 = v.gr.ell + 1;
 
-    uint32_t acc[W];
-#pragma unroll
-    for (int j = 0; j < W; ++j) acc[j] = 0u;
-    Mask x{0ull, 0ull};
-    if (cnt > 0 && gr.ell >= 0) {
-      xor_row<W>(acc, R + gr.ell * WP);
-      if (q > 0) {
-        x = colex_unrank(first, q, gr.ell, a.binom);
-        Mask y = x;
-        while (y.lo | y.hi) {
-          const int b = mask_ctz(y);
-          xor_row<W>(acc, R + b * WP);
-          if (b < 64) y.lo &= y.lo - 1; else y.hi &= y.hi - 1;
-        }
-      }
-    }
+    Walker<W> A, B;
+    if (v.cnt > 0) A.init(v.first, q, v.gr.ell, R, a.binom);
+    if (cb > 0) B.init(v.first + ca, q, v.gr.ell, R, a.binom);
 
     int best = INT_MAX;
-    for (long long p = 0; p < maxcnt; ++p) {
-      if (p < cnt) {
-        int pb = INT_MAX;
-        const uint32_t* re = R + e0 * WP;
-        int e = e0;
-#pragma unroll 1
-        for (; e + 2 <= k; e += 2, re += 2 * WP) {
-          uint32_t r0[W], r1[W];
-          load_row<W>(r0, re);
-          load_row<W>(r1, re + WP);
-          const int w0 = weight_xor<W>(acc, r0);
-          const int w1 = weight_xor<W>(acc, r1);
-          pb = min(pb, min(w0, w1));
+    for (long long p = 0; p < maxca; ++p) {
+      if (p < ca) {
+        if (p >= cb) {
+#pragma unroll
+          for (int j = 0; j < W; ++j) B.acc[j] = A.acc[j];
         }
-        if (e < k) {
-          uint32_t r0[W];
-          load_row<W>(r0, re);
-          pb = min(pb, weight_xor<W>(acc, r0));
-        }
-        best = min(best, pb);
-        if (p + 1 < cnt) {
-          int i0, i1, i2;
-          colex_next(x, i0, i1, i2);
-          xor_row<W>(acc, PX + i0 * WP);
-          xor_row<W>(acc, PX + i1 * WP);
-          xor_row<W>(acc, PX + i2 * WP);
-        }
+        int pa = INT_MAX, pb = INT_MAX;
+        suffix_pair<W, D>(A.acc, B.acc, R, e0, k, [&](int wa, int wb) {
+          pa = min(pa, wa);
+          pb = min(pb, wb);
+        });
+        best = min(best, min(pa, pb));
+        if (p + 1 < ca) A.step(PX);
+        if (p + 1 < cb) B.step(PX);
       }
     }
 
     // chunk epilogue: warp min -> per-Gamma and round minima; combos count
     const int wbest = __reduce_min_sync(FULL, best);
-    const unsigned cnt_u = (unsigned)cnt;
-    const unsigned tot = __reduce_add_sync(FULL, cnt_u);
+    const unsigned tot = __reduce_add_sync(FULL, (unsigned)v.cnt);
     if (lane == 0) {
-      if (wbest < vbound[1 + gr.gamma]) atomicMin(a.bound + 1 + gr.gamma, wbest);
+      if (wbest < vbound[1 + v.gr.gamma]) atomicMin(a.bound + 1 + v.gr.gamma, wbest);
       if (wbest < vbound[0]) atomicMin(a.bound, wbest);
-      atomicAdd(a.combos + gr.gamma, (unsigned long long)tot * (unsigned long long)(k - e0));
+      atomicAdd(a.combos + v.gr.gamma, (unsigned long long)tot * suffix_count<D>(k, e0));
     }
   }
 }
@@ -313,8 +414,9 @@ k1_round_min(const RoundArgs a) {
 // K1h: weight histogram of one (Gamma, g) pass.  Each thread owns a private
 // u16 histogram column in shared memory (layout [bin][thread]: conflict-free
 // for any bin pattern), flushed into a block-wide u32 histogram before it
-// can overflow, and finally into the global u64 bins.
-template <int W>
+// can overflow, and finally into the global u64 bins.  Same two-walker
+// structure as K1; on an odd range the second walker's last step is masked.
+template <int W, int D>
 __global__ void __launch_bounds__(256)
 k1h_histogram(const RoundArgs a) {
   constexpr int WP = padded_words(W);
@@ -322,7 +424,6 @@ k1h_histogram(const RoundArgs a) {
   uint32_t *srows, *spx;
   Group* sgroups;
   const int nbins = a.n + 1;
-  // histogram region follows the staged data
   size_t base = smem_base_bytes<W>(a.m, a.k, a.ngroups);
   base = (base + 15) & ~size_t(15);
   unsigned int* bhist = reinterpret_cast<unsigned int*>(smem + base);
@@ -335,7 +436,7 @@ k1h_histogram(const RoundArgs a) {
   const int lane = threadIdx.x & 31;
   const int tid = threadIdx.x;
   const int bd = blockDim.x;
-  const int k = a.k, q = a.g - 2;
+  const int k = a.k, q = a.g - 1 - D;
   unsigned int since_flush = 0;
   int best = INT_MAX;
 
@@ -357,62 +458,40 @@ k1h_histogram(const RoundArgs a) {
     const unsigned long long chunk = c * (unsigned long long)a.nshards + a.shard;
     if (chunk >= a.nchunks) break;
 
-    const Group gr = sgroups[find_group(sgroups, a.ngroups, chunk)];
-    const unsigned long long local = chunk - gr.chunk_begin;
-    const unsigned long long first = (local * 32ull + lane) * (unsigned long long)gr.ppl;
-    long long cnt = 0;
-    if (first < gr.nprefix) {
-      const unsigned long long left = gr.nprefix - first;
-      cnt = left < (unsigned long long)gr.ppl ? (long long)left : gr.ppl;
-    }
-    const long long maxcnt = __shfl_sync(FULL, cnt, 0);
-    const uint32_t* R = srows + gr.gamma * k * WP;
-    const uint32_t* PX = spx + gr.gamma * (k + 1) * WP;
-    const int e0 = gr.ell + 1;
-    const unsigned chunk_work = (unsigned)(cnt * (k - e0));
+    const ChunkView v = open_chunk(sgroups, a.ngroups, chunk, lane);
+    const long long ca = (v.cnt + 1) >> 1;
+    const long long cb = v.cnt - ca;
+    const long long maxca = __shfl_sync(FULL, ca, 0);
+    const uint32_t* R = srows + v.gr.gamma * k * WP;
+    const uint32_t* PX = spx + v.gr.gamma * (k + 1) * px_stride(W);
+    const int e0 = v.gr.ell + 1;
+    const unsigned chunk_work = (unsigned)((unsigned long long)v.cnt * suffix_count<D>(k, e0));
     if (since_flush + chunk_work > 65535u) flush();
     since_flush += chunk_work;
 
-    uint32_t acc[W];
-#pragma unroll
-    for (int j = 0; j < W; ++j) acc[j] = 0u;
-    Mask x{0ull, 0ull};
-    if (cnt > 0 && gr.ell >= 0) {
-      xor_row<W>(acc, R + gr.ell * WP);
-      if (q > 0) {
-        x = colex_unrank(first, q, gr.ell, a.binom);
-        Mask y = x;
-        while (y.lo | y.hi) {
-          const int b = mask_ctz(y);
-          xor_row<W>(acc, R + b * WP);
-          if (b < 64) y.lo &= y.lo - 1; else y.hi &= y.hi - 1;
-        }
-      }
-    }
-    for (long long p = 0; p < maxcnt; ++p) {
-      if (p < cnt) {
-        const uint32_t* re = R + e0 * WP;
-#pragma unroll 1
-        for (int e = e0; e < k; ++e, re += WP) {
-          uint32_t r0[W];
-          load_row<W>(r0, re);
-          const int w = weight_xor<W>(acc, r0);
-          best = min(best, w);
-          unsigned short* h = th + w * bd + tid;
+    Walker<W> A, B;
+    if (v.cnt > 0) A.init(v.first, q, v.gr.ell, R, a.binom);
+    if (cb > 0) B.init(v.first + ca, q, v.gr.ell, R, a.binom);
+    for (long long p = 0; p < maxca; ++p) {
+      if (p < ca) {
+        const bool with_b = p < cb;
+        suffix_pair<W, D>(A.acc, B.acc, R, e0, k, [&](int wa, int wb) {
+          best = min(best, wa);
+          unsigned short* h = th + wa * bd + tid;
           *h = (unsigned short)(*h + 1);
-        }
-        if (p + 1 < cnt) {
-          int i0, i1, i2;
-          colex_next(x, i0, i1, i2);
-          xor_row<W>(acc, PX + i0 * WP);
-          xor_row<W>(acc, PX + i1 * WP);
-          xor_row<W>(acc, PX + i2 * WP);
-        }
+          if (with_b) {
+            best = min(best, wb);
+            unsigned short* hb = th + wb * bd + tid;
+            *hb = (unsigned short)(*hb + 1);
+          }
+        });
+        if (p + 1 < ca) A.step(PX);
+        if (p + 1 < cb) B.step(PX);
       }
     }
-    const unsigned tot = __reduce_add_sync(FULL, (unsigned)cnt);
+    const unsigned tot = __reduce_add_sync(FULL, (unsigned)v.cnt);
     if (lane == 0)
-      atomicAdd(a.combos + gr.gamma, (unsigned long long)tot * (unsigned long long)(k - e0));
+      atomicAdd(a.combos + v.gr.gamma, (unsigned long long)tot * suffix_count<D>(k, e0));
   }
   flush();
   const int wbest = __reduce_min_sync(FULL, best);

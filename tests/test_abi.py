@@ -45,9 +45,10 @@ def test_plan_counts():
         starts = [gr[0] for gr in groups]
         assert starts == sorted(starts) and starts[0] == 0
         for gr in groups:
-            begin, nprefix, gamma, ell, ppl, combos = gr
-            assert nprefix == (1 if g == 1 else comb(ell, g - 2))
-            assert combos == nprefix * (k - 1 - ell)
+            begin, nprefix, gamma, ell, ppl, combos, depth = gr
+            assert depth == (2 if g >= 3 else 1)
+            assert nprefix == (1 if g == 1 else comb(ell, g - 1 - depth))
+            assert combos == nprefix * comb(k - 1 - ell, depth)
 
 
 @pytest.mark.parametrize("m,k,g", [(1, 6, 1), (1, 7, 2), (2, 9, 3), (1, 12, 5),
