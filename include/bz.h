@@ -59,6 +59,11 @@ extern "C" {
 #define BZ_ERR_STATE 6              /* no Gamma loaded / bad gamma index         */
 #define BZ_ERR_ARGUMENT 7           /* null pointer, bad shard                   */
 
+/* enumeration engines (bz_set_engine) */
+#define BZ_ENGINE_AUTO 0 /* tensor-pipe K2 for g >= 4, POPC K1 otherwise */
+#define BZ_ENGINE_POPC 1 /* K1 only: XOR + POPC on the integer pipes       */
+#define BZ_ENGINE_IMMA 2 /* same as AUTO (K2 needs g >= 4)                  */
+
 typedef struct bz_ctx bz_ctx;
 
 /* Library / ABI version (BZ_ABI_VERSION). */
@@ -75,6 +80,10 @@ void bz_destroy(bz_ctx *ctx);
 
 /* Human-readable description of the last error on ctx (never NULL). */
 const char *bz_last_error(const bz_ctx *ctx);
+
+/* Select the enumeration engine for later calls (BZ_ENGINE_*).  Results
+ * are identical; only the kernel and the work plan differ. */
+int bz_set_engine(bz_ctx *ctx, int engine);
 
 /* Upload the m systematic matrices of one generator: `rows` holds
  * m*k*ceil(n/64) little-endian uint64 words, matrix-major then row-major
@@ -116,9 +125,10 @@ int bz_histogram(bz_ctx *ctx, int gamma, int g, int shard, int nshards,
  * (gamma, ell), lane l of the warp walks the colex ranks
  * [(c_local*32 + l)*ppl, +ppl) of the (g-1-depth)-subsets of [0, ell), each
  * extended by ell and then by every depth-subset of the suffix rows
- * (ell, k).  depth = 2 for g >= 3, else 1 (g = 1: ell = -1, empty prefix). */
-int bz_plan(int m, int k, int g, int64_t *out, int cap, int *out_ngroups,
-            uint64_t *out_nchunks);
+ * (ell, k).  depth = 3 for g >= 4 unless engine == BZ_ENGINE_POPC, else 2
+ * for g >= 3, else 1 (g = 1: ell = -1, empty prefix). */
+int bz_plan(int m, int k, int g, int engine, int64_t *out, int cap,
+            int *out_ngroups, uint64_t *out_nchunks);
 
 /* Device timing on the context's stream: bz_timer_start records a CUDA
  * event, bz_timer_stop records a second one, synchronises and returns the

@@ -33,7 +33,7 @@ _CODES = {
 
 # every symbol include/bz.h declares (checked by tests/test_abi.py)
 SYMBOLS = ("bz_abi_version", "bz_device_count", "bz_create", "bz_destroy",
-           "bz_last_error", "bz_load_gammas", "bz_round", "bz_enumerate",
+           "bz_last_error", "bz_set_engine", "bz_load_gammas", "bz_round", "bz_enumerate",
            "bz_histogram", "bz_plan", "bz_timer_start", "bz_timer_stop",
            "bz_last_kernel_ms", "bz_launch_count", "bz_measure_int_peaks")
 
@@ -62,11 +62,12 @@ def lib():
     L.bz_destroy.restype = None
     L.bz_last_error.argtypes = [vp]
     L.bz_last_error.restype = ctypes.c_char_p
+    L.bz_set_engine.argtypes = [vp, c_int]
     L.bz_load_gammas.argtypes = [vp, u64p, c_int, c_int, c_int]
     L.bz_round.argtypes = [vp, c_int, c_int, c_int, c_int, c_int, i32p, u64p]
     L.bz_enumerate.argtypes = [vp, c_int, c_int, c_int, c_int, i32p, u64p]
     L.bz_histogram.argtypes = [vp, c_int, c_int, c_int, c_int, u64p, i32p, u64p]
-    L.bz_plan.argtypes = [c_int, c_int, c_int, i64p, c_int, i32p, u64p]
+    L.bz_plan.argtypes = [c_int, c_int, c_int, c_int, i64p, c_int, i32p, u64p]
     L.bz_timer_start.argtypes = [vp]
     L.bz_timer_stop.argtypes = [vp, ctypes.POINTER(c_float)]
     L.bz_last_kernel_ms.argtypes = [vp, ctypes.POINTER(c_float)]
@@ -97,15 +98,19 @@ def device_count() -> int:
     return int(lib().bz_device_count())
 
 
-def plan(m: int, k: int, g: int):
+ENGINES = {"auto": 0, "popc": 1, "imma": 2}
+
+
+def plan(m: int, k: int, g: int, engine: str = "auto"):
     """The device work plan for one round (host-only; see bz_plan)."""
     L = lib()
+    e = ENGINES[engine]
     ng = np.zeros(1, dtype=np.int32)
     nc = np.zeros(1, dtype=np.uint64)
-    check(L.bz_plan(m, k, g, None, 0, _ptr(ng, ctypes.c_int32), _ptr(nc, ctypes.c_uint64)),
-          what="bz_plan")
+    check(L.bz_plan(m, k, g, e, None, 0, _ptr(ng, ctypes.c_int32),
+                    _ptr(nc, ctypes.c_uint64)), what="bz_plan")
     out = np.zeros((int(ng[0]), 7), dtype=np.int64)
-    check(L.bz_plan(m, k, g, _ptr(out, ctypes.c_int64), int(ng[0]),
+    check(L.bz_plan(m, k, g, e, _ptr(out, ctypes.c_int64), int(ng[0]),
                     _ptr(ng, ctypes.c_int32), _ptr(nc, ctypes.c_uint64)), what="bz_plan")
     return [tuple(int(v) for v in row) for row in out], int(nc[0])
 
@@ -125,6 +130,8 @@ class Context:
                 L.bz_destroy(h)
                 self._h = None
         self.device = device
+        self.engine = "auto"
+        self.loaded_key = None
         self.m = self.k = self.n = 0
 
     def close(self) -> None:
@@ -150,8 +157,17 @@ class Context:
             raise MindistError("context is closed")
         return self._h
 
-    def load(self, words: np.ndarray, n: int) -> None:
-        """words: (m, k, ceil(n/64)) uint64 row image of the family."""
+    def set_engine(self, engine: str) -> None:
+        """'auto' (tensor-pipe K2 for g >= 4), 'popc' (K1 only) or 'imma'."""
+        if engine not in ENGINES:
+            raise ValueError(f"unknown engine {engine!r}")
+        check(lib().bz_set_engine(self.handle, ENGINES[engine]), self.handle, "bz_set_engine")
+        self.engine = engine
+
+    def load(self, words: np.ndarray, n: int, key=None) -> None:
+        """words: (m, k, ceil(n/64)) uint64 row image of the family.  `key`
+        identifies the family for callers that cache what is loaded."""
+        self.loaded_key = None
         words = np.ascontiguousarray(words, dtype=np.uint64)
         if words.ndim != 3:
             raise InvalidDimensions("expected an (m, k, w64) array")
@@ -159,6 +175,7 @@ class Context:
         check(lib().bz_load_gammas(self.handle, _ptr(words, ctypes.c_uint64), m, k, n),
               self.handle, "bz_load_gammas")
         self.m, self.k, self.n = m, k, n
+        self.loaded_key = key
 
     def round(self, g: int, lower_prev: int, upper: int, shard: int = 0,
               nshards: int = 1):

@@ -18,6 +18,7 @@
 
 #include "../../include/bz.h"
 #include "bz_kernels.cuh"
+#include "bz_tc.cuh"
 
 using bz::Group;
 using bz::RoundArgs;
@@ -34,7 +35,9 @@ struct bz_ctx {
 
   // loaded family
   int m = 0, k = 0, n = 0, w32 = 0, wp = 0;
+  int engine = BZ_ENGINE_AUTO;
   uint32_t* d_rows = nullptr;   // m*k*wp
+  uint8_t* d_tbl = nullptr;     // m*(k+8) rows of 0/1 bytes (K2)
   uint32_t* d_px = nullptr;     // m*(k+1)*wp
   unsigned long long* d_binom = nullptr;
   // per-round scratch
@@ -106,13 +109,19 @@ int ensure_round_buffers(bz_ctx* ctx, int ngroups) {
 
 // Work plan of one round (host only): one Group per (Gamma, ell) with its
 // chunk range.  gamma_only < 0: all m Gammas.
-int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, std::vector<Group>& gs,
-               unsigned long long* out_nchunks) {
+// Suffix depth of a pass: K2 (tensor pipe) takes D = 3 for g >= 4; K1
+// (POPC) takes D = 2 for g >= 3, else 1.  The histogram always runs on K1.
+int pass_depth(int engine, int g, bool hist) {
+  if (!hist && engine != BZ_ENGINE_POPC && g >= 4) return 3;
+  return g >= 3 ? 2 : 1;
+}
+
+int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, int depth,
+               std::vector<Group>& gs, unsigned long long* out_nchunks) {
   gs.clear();
   unsigned long long chunk = 0;
   const int j0 = gamma_only < 0 ? 0 : gamma_only;
   const int j1 = gamma_only < 0 ? m : gamma_only + 1;
-  const int depth = g >= 3 ? 2 : 1;
   const unsigned long long total = binom_sat(k, g) * (unsigned long long)(j1 - j0);
   long long lane_target = (long long)(total / (32ull * kChunksTarget));
   lane_target = std::min(kLaneMax, std::max(kLaneMin, lane_target));
@@ -145,10 +154,10 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, std::vector<Gro
 }
 
 // Build the round's group table and upload it.
-int plan_round(bz_ctx* ctx, int g, int gamma_only, int* out_ngroups,
+int plan_round(bz_ctx* ctx, int g, int gamma_only, int depth, int* out_ngroups,
                unsigned long long* out_nchunks) {
   std::vector<Group> gs;
-  int rc = build_plan(ctx, ctx->m, ctx->k, g, gamma_only, gs, out_nchunks);
+  int rc = build_plan(ctx, ctx->m, ctx->k, g, gamma_only, depth, gs, out_nchunks);
   if (rc) return rc;
   rc = ensure_round_buffers(ctx, (int)gs.size());
   if (rc) return rc;
@@ -209,20 +218,42 @@ int launch_wd(bz_ctx* ctx, const RoundArgs& a, bool hist) {
 }
 
 template <int W>
-int launch_w(bz_ctx* ctx, const RoundArgs& a, bool hist) {
-  return a.g >= 3 ? launch_wd<W, 2>(ctx, a, hist) : launch_wd<W, 1>(ctx, a, hist);
+int launch_tc(bz_ctx* ctx, const RoundArgs& a) {
+  const size_t smem = bz::tc_smem_bytes<W>(a.m, a.k, a.ngroups);
+  const int threads = 256;
+  CK(cudaFuncSetAttribute(bz::k2_round_mma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bz::k2_round_mma<W>, threads, smem));
+  if (per_sm < 1) return fail(ctx, BZ_ERR_TOO_LARGE, "K2 does not fit on an SM (smem %zu)", smem);
+  unsigned long long warps_needed = (a.nchunks + a.nshards - 1) / a.nshards;
+  long long blocks = (long long)per_sm * ctx->sm_count;
+  long long need = (long long)((warps_needed + (threads / 32) - 1) / (threads / 32));
+  blocks = std::max(1ll, std::min(blocks, need));
+  CK(cudaEventRecord(ctx->ev_k0, ctx->stream));
+  bz::k2_round_mma<W><<<(unsigned)blocks, threads, smem, ctx->stream>>>(a, ctx->d_tbl);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
+  ctx->launches += 1;
+  return BZ_OK;
 }
 
-int launch(bz_ctx* ctx, const RoundArgs& a, bool hist) {
+template <int W>
+int launch_w(bz_ctx* ctx, const RoundArgs& a, bool hist, int depth) {
+  if (depth == 3) return launch_tc<W>(ctx, a);
+  return depth == 2 ? launch_wd<W, 2>(ctx, a, hist) : launch_wd<W, 1>(ctx, a, hist);
+}
+
+int launch(bz_ctx* ctx, const RoundArgs& a, bool hist, int depth) {
   switch (ctx->w32) {
-    case 1: return launch_w<1>(ctx, a, hist);
-    case 2: return launch_w<2>(ctx, a, hist);
-    case 3: return launch_w<3>(ctx, a, hist);
-    case 4: return launch_w<4>(ctx, a, hist);
-    case 5: return launch_w<5>(ctx, a, hist);
-    case 6: return launch_w<6>(ctx, a, hist);
-    case 7: return launch_w<7>(ctx, a, hist);
-    case 8: return launch_w<8>(ctx, a, hist);
+    case 1: return launch_w<1>(ctx, a, hist, depth);
+    case 2: return launch_w<2>(ctx, a, hist, depth);
+    case 3: return launch_w<3>(ctx, a, hist, depth);
+    case 4: return launch_w<4>(ctx, a, hist, depth);
+    case 5: return launch_w<5>(ctx, a, hist, depth);
+    case 6: return launch_w<6>(ctx, a, hist, depth);
+    case 7: return launch_w<7>(ctx, a, hist, depth);
+    case 8: return launch_w<8>(ctx, a, hist, depth);
     default: return fail(ctx, BZ_ERR_TOO_LARGE, "unsupported word count %d", ctx->w32);
   }
 }
@@ -236,7 +267,8 @@ int run_pass(bz_ctx* ctx, int g, int gamma_only, int lower_prev, int upper,
   if (rc) return rc;
   int ngroups = 0;
   unsigned long long nchunks = 0;
-  rc = plan_round(ctx, g, gamma_only, &ngroups, &nchunks);
+  const int depth = pass_depth(ctx->engine, g, hist);
+  rc = plan_round(ctx, g, gamma_only, depth, &ngroups, &nchunks);
   if (rc) return rc;
   const int m = ctx->m;
   for (int i = 0; i <= m; ++i) ctx->h_bound[i] = upper;
@@ -265,7 +297,7 @@ int run_pass(bz_ctx* ctx, int g, int gamma_only, int lower_prev, int upper,
   a.nshards = nshards;
   a.lower_prev = lower_prev;
   if (nchunks > 0 && (unsigned long long)shard < nchunks) {
-    rc = launch(ctx, a, hist);
+    rc = launch(ctx, a, hist, depth);
     if (rc) return rc;
   } else {
     CK(cudaEventRecord(ctx->ev_k0, ctx->stream));
@@ -345,6 +377,7 @@ void bz_destroy(bz_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     cudaFree(ctx->d_rows);
     cudaFree(ctx->d_px);
+    cudaFree(ctx->d_tbl);
     cudaFree(ctx->d_binom);
     cudaFree(ctx->d_groups);
     cudaFree(ctx->d_bound);
@@ -407,10 +440,23 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
         px[((size_t)j * (k + 1) + r + 1) * wp + w] =
             px[((size_t)j * (k + 1) + r) * wp + w] ^ img[((size_t)j * k + r) * wp + w];
   }
+  // 0/1 byte image for K2: row r, column c -> byte c (zero padding rows)
+  const int ts = bz::tc_stride(w32);
+  std::vector<uint8_t> tbl((size_t)m * (k + bz::kTcPadRows) * ts, 0u);
+  for (int j = 0; j < m; ++j)
+    for (int r = 0; r < k; ++r)
+      for (int col = 0; col < n; ++col) {
+        const uint32_t wv = img[((size_t)j * k + r) * wp + col / 32];
+        tbl[((size_t)j * (k + bz::kTcPadRows) + r) * ts + col] = (uint8_t)((wv >> (col % 32)) & 1u);
+      }
   cudaFree(ctx->d_rows);
   cudaFree(ctx->d_px);
+  cudaFree(ctx->d_tbl);
   ctx->d_rows = nullptr;
   ctx->d_px = nullptr;
+  ctx->d_tbl = nullptr;
+  CK(cudaMalloc(&ctx->d_tbl, tbl.size()));
+  CK(cudaMemcpy(ctx->d_tbl, tbl.data(), tbl.size(), cudaMemcpyHostToDevice));
   CK(cudaMalloc(&ctx->d_rows, img.size() * 4));
   CK(cudaMalloc(&ctx->d_px, px.size() * 4));
   CK(cudaMemcpy(ctx->d_rows, img.data(), img.size() * 4, cudaMemcpyHostToDevice));
@@ -485,7 +531,15 @@ int bz_histogram(bz_ctx* ctx, int gamma, int g, int shard, int nshards, uint64_t
   return BZ_OK;
 }
 
-int bz_plan(int m, int k, int g, int64_t* out, int cap, int* out_ngroups,
+int bz_set_engine(bz_ctx* ctx, int engine) {
+  if (!ctx) return BZ_ERR_ARGUMENT;
+  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_IMMA)
+    return fail(ctx, BZ_ERR_ARGUMENT, "unknown engine %d", engine);
+  ctx->engine = engine;
+  return BZ_OK;
+}
+
+int bz_plan(int m, int k, int g, int engine, int64_t* out, int cap, int* out_ngroups,
             uint64_t* out_nchunks) {
   if (!out_ngroups || !out_nchunks) return BZ_ERR_ARGUMENT;
   if (m < 1 || k < 1) return BZ_ERR_INVALID_DIMENSIONS;
@@ -494,7 +548,8 @@ int bz_plan(int m, int k, int g, int64_t* out, int cap, int* out_ngroups,
   if (binom_sat(k, g) >= (1ull << 62)) return BZ_ERR_TOO_LARGE;
   std::vector<Group> gs;
   unsigned long long nchunks = 0;
-  int rc = build_plan(nullptr, m, k, g, -1, gs, &nchunks);
+  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_IMMA) return BZ_ERR_ARGUMENT;
+  int rc = build_plan(nullptr, m, k, g, -1, pass_depth(engine, g, false), gs, &nchunks);
   if (rc) return rc;
   *out_ngroups = (int)gs.size();
   *out_nchunks = nchunks;

@@ -83,6 +83,7 @@ class EngineConfig:
     device: int | None = None
     distributed: bool = False
     early_exit: bool = True  # stop a round once U reaches the previous L
+    engine: str = "auto"     # "auto" | "popc" | "imma" (kernel choice; same results)
 
 
 @dataclass
@@ -147,6 +148,7 @@ class GpuRounds:
         if dev is None:
             dev = int(os.environ.get("LOCAL_RANK", "0"))
         self.ctx = _native.context(dev)
+        self.ctx.set_engine(config.engine)
         self.comm = comm
 
     def load(self, gs: GammaSet, n: int) -> None:

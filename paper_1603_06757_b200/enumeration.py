@@ -40,15 +40,11 @@ def family_words(gammas, n: int) -> np.ndarray:
     return np.ascontiguousarray(np.stack(mats, axis=0), dtype=np.uint64)
 
 
-_loaded: dict[int, tuple] = {}
-
-
 def _load_single(gamma: BitMatrix, device: int) -> _native.Context:
     ctx = _native.context(device)
-    key = (gamma.num_cols, gamma.rows)
-    if _loaded.get(device) != key:
-        ctx.load(family_words([gamma], gamma.num_cols), gamma.num_cols)
-        _loaded[device] = key
+    key = ("single", gamma.num_cols, gamma.rows)
+    if ctx.loaded_key != key:
+        ctx.load(family_words([gamma], gamma.num_cols), gamma.num_cols, key=key)
     return ctx
 
 
@@ -74,6 +70,3 @@ def weight_histogram_gpu(gamma: BitMatrix, g: int, device: int = 0):
     ctx = _load_single(gamma, device)
     return ctx.histogram(0, g)
 
-
-def invalidate_cache() -> None:
-    _loaded.clear()

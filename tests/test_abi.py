@@ -37,23 +37,26 @@ def test_header_symbols_exported():
     assert L.bz_abi_version() == _native.ABI_VERSION
 
 
-def test_plan_counts():
+@pytest.mark.parametrize("engine", ["auto", "popc"])
+def test_plan_counts(engine):
     for (m, k, g) in [(1, 5, 1), (2, 24, 3), (2, 80, 8), (3, 40, 8), (1, 64, 6), (2, 128, 4)]:
-        groups, nchunks = _native.plan(m, k, g)
+        groups, nchunks = _native.plan(m, k, g, engine)
         assert sum(gr[5] for gr in groups) == m * comb(k, g)
         assert nchunks >= 1
         starts = [gr[0] for gr in groups]
         assert starts == sorted(starts) and starts[0] == 0
         for gr in groups:
             begin, nprefix, gamma, ell, ppl, combos, depth = gr
-            assert depth == (2 if g >= 3 else 1)
+            want = 3 if (engine == "auto" and g >= 4) else (2 if g >= 3 else 1)
+            assert depth == want
             assert nprefix == (1 if g == 1 else comb(ell, g - 1 - depth))
             assert combos == nprefix * comb(k - 1 - ell, depth)
 
 
+@pytest.mark.parametrize("engine", ["auto", "popc"])
 @pytest.mark.parametrize("m,k,g", [(1, 6, 1), (1, 7, 2), (2, 9, 3), (1, 12, 5),
-                                   (2, 10, 10), (1, 40, 3), (1, 34, 4)])
-def test_plan_partitions_rank_space(m, k, g):
+                                   (2, 10, 10), (1, 40, 3), (1, 34, 4), (1, 20, 6)])
+def test_plan_partitions_rank_space(m, k, g, engine):
     """Every g-combination of every Gamma is visited exactly once, for any
     shard count, by the device's chunk/lane/colex walk."""
     import random
@@ -61,7 +64,7 @@ def test_plan_partitions_rank_space(m, k, g):
     rng = random.Random(k * 100 + g)
     n = 2 * k + 5
     gammas = [[rng.getrandbits(n) for _ in range(k)] for _ in range(m)]
-    groups, nchunks = _native.plan(m, k, g)
+    groups, nchunks = _native.plan(m, k, g, engine)
     expect = sorted(oracle.all_combinations(m, k, g))
     for nshards in (1, 2, 3, 8):
         seen = []

@@ -27,7 +27,15 @@ def ctx():
     return _native.context(0)
 
 
-def test_small_enum_fixtures(goldens):
+@pytest.fixture(params=["popc", "imma"])
+def engine(request):
+    """Both kernels: K1 (XOR+POPC) and K2 (tensor-pipe IMMA, g >= 4)."""
+    _native.context(0).set_engine(request.param)
+    yield request.param
+    _native.context(0).set_engine("auto")
+
+
+def test_small_enum_fixtures(goldens, engine):
     for fx in goldens["small"]["enum"]:
         M = BitMatrix(hexrows(fx["rows"]), fx["n"])
         for g, expect in enumerate(fx["min_by_g"], start=1):
@@ -53,7 +61,7 @@ def test_bad_arity():
 
 
 @pytest.mark.parametrize("n", [1, 7, 31, 32, 33, 64, 65, 100, 127, 160, 192, 200, 255, 256])
-def test_word_widths(n):
+def test_word_widths(n, engine):
     """Every W = ceil(n/32) instantiation (1..8), padded and exact sizes."""
     rng = random.Random(n)
     k = min(12, n) if n > 1 else 1
@@ -65,7 +73,7 @@ def test_word_widths(n):
 
 @pytest.mark.parametrize("k,g", [(1, 1), (2, 2), (33, 3), (64, 4), (65, 3), (100, 3),
                                  (127, 2), (128, 3), (128, 128), (70, 69)])
-def test_row_counts(k, g):
+def test_row_counts(k, g, engine):
     """Masks cross the 64-bit word boundary; g = k and g = k-1 edges."""
     rng = random.Random(k * 7 + g)
     n = 150
@@ -74,7 +82,7 @@ def test_row_counts(k, g):
     assert enumerate_gpu(M, g).min_weight == oracle.min_weight(rows, n, g)[0]
 
 
-def test_random_sweep_vs_oracle():
+def test_random_sweep_vs_oracle(engine):
     rng = random.Random(2024)
     for _ in range(40):
         k = rng.randint(2, 40)
@@ -87,17 +95,17 @@ def test_random_sweep_vs_oracle():
             assert enumerate_gpu(M, g).min_weight == oracle.min_weight(rows, n, g)[0], (k, n, g)
 
 
-def test_zero_rows_and_duplicates():
+def test_zero_rows_and_duplicates(engine):
     rows = [0, 0, 5, 5, 7]
     M = BitMatrix(rows, 3)
     for g in range(1, 6):
         assert enumerate_gpu(M, g).min_weight == oracle.min_weight(rows, 3, g)[0]
 
 
-def test_round_sharded_equals_whole(ctx):
+def test_round_sharded_equals_whole(ctx, engine):
     G, gs, _ = code("cfg2", 1)
     ctx.load(family_words(gs.gammas, 96), 96)
-    for g in (1, 2, 3, 4, 5):
+    for g in (1, 2, 3, 4, 5, 6):
         whole_min, whole_c = ctx.round(g, 0, 10**6)
         for nshards in (2, 3, 8):
             mins = [10**9] * 2
@@ -107,12 +115,13 @@ def test_round_sharded_equals_whole(ctx):
                 mins = [min(a, b) for a, b in zip(mins, mn)]
                 cs = [a + b for a, b in zip(cs, c)]
             assert mins == whole_min and cs == whole_c == [comb(48, g)] * 2
+        assert whole_min == [oracle.min_weight(list(gm.rows), 96, g)[0] for gm in gs.gammas]
 
 
 @pytest.mark.parametrize("idx", range(6))
-def test_minimum_distance_configs(goldens, idx):
+def test_minimum_distance_configs(goldens, idx, engine):
     fx = goldens["configs"][idx]
-    rep = minimum_distance(BitMatrix(hexrows(fx["rows"]), fx["n"]))
+    rep = minimum_distance(BitMatrix(hexrows(fx["rows"]), fx["n"]), EngineConfig(engine=engine))
     assert rep.distance == fx["distance"]
     assert rep.bounds_trace == [tuple(t) for t in fx["bounds_trace"]]
     assert (rep.status, rep.g_reached, rep.m, rep.k_m) == \
@@ -136,9 +145,9 @@ def test_early_exit_fixture(goldens):
     assert fast.counters.combinations <= full.counters.combinations
 
 
-def test_small_codes(goldens):
+def test_small_codes(goldens, engine):
     for fx in goldens["small"]["codes"]:
-        rep = minimum_distance(BitMatrix(hexrows(fx["rows"]), fx["n"]))
+        rep = minimum_distance(BitMatrix(hexrows(fx["rows"]), fx["n"]), EngineConfig(engine=engine))
         assert rep.distance == fx["distance"] == fx["brute"], fx["src"]
         assert rep.bounds_trace == [tuple(t) for t in fx["bounds_trace"]], fx["src"]
 
@@ -163,11 +172,11 @@ def test_histogram_small_vs_oracle():
         assert np.array_equal(hist, oracle.histogram(rows, n, g)), (k, n, g)
 
 
-def test_cfg5_full(cfg5_golden):
+def test_cfg5_full(cfg5_golden, engine):
     fx = cfg5_golden
     G, gs, draws = code("cfg5", 7)
     assert [format(r, "x") for r in G.rows] == fx["rows"]
-    rep = minimum_distance(G)
+    rep = minimum_distance(G, EngineConfig(engine=engine))
     assert rep.distance == fx["distance"]
     assert rep.bounds_trace == [tuple(t) for t in fx["bounds_trace"]]
     assert rep.counters.combinations == fx["combinations"]
