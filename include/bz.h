@@ -60,9 +60,9 @@ extern "C" {
 #define BZ_ERR_ARGUMENT 7           /* null pointer, bad shard                   */
 
 /* enumeration engines (bz_set_engine) */
-#define BZ_ENGINE_AUTO 0 /* tensor-pipe K2 for g >= 4, POPC K1 otherwise */
+#define BZ_ENGINE_AUTO 0 /* tensor-pipe K3 for g >= 4, POPC K1 otherwise */
 #define BZ_ENGINE_POPC 1 /* K1 only: XOR + POPC on the integer pipes       */
-#define BZ_ENGINE_IMMA 2 /* same as AUTO (K2 needs g >= 4)                  */
+#define BZ_ENGINE_IMMA 2 /* same as AUTO (K3 needs g >= 4)                  */
 
 typedef struct bz_ctx bz_ctx;
 
@@ -117,13 +117,14 @@ int bz_histogram(bz_ctx *ctx, int gamma, int g, int shard, int nshards,
                  uint64_t *out_hist, int32_t *out_min, uint64_t *out_combos);
 
 /* Host-only: the work plan bz_round uses for (m, k, g), for inspection and
- * for the CPU tests of the sharding logic.  Writes *out_ngroups groups of 7
+ * for the CPU tests of the sharding logic.  Writes *out_ngroups groups of 8
  * int64 each -- chunk_begin, nprefix, gamma, ell, prefixes_per_lane,
- * combinations, depth -- into out (capacity `cap` groups; out may be NULL to
- * query the count) and the round's chunk count into *out_nchunks.  Chunk c
- * of the round belongs to shard c % nshards; within a chunk of group
- * (gamma, ell), lane l of the warp walks the colex ranks
- * [(c_local*32 + l)*ppl, +ppl) of the (g-1-depth)-subsets of [0, ell), each
+ * combinations, depth, lanes_per_chunk -- into out (capacity `cap` groups;
+ * out may be NULL to query the count) and the round's chunk count into
+ * *out_nchunks.  Chunk c of the round belongs to shard c % nshards; within
+ * a chunk of group (gamma, ell), lane l (0 <= l < lanes_per_chunk: 32 for a
+ * warp of K1, 256 for a block of K3) walks the colex ranks
+ * [(c_local*lanes + l)*ppl, +ppl) of the (g-1-depth)-subsets of [0, ell), each
  * extended by ell and then by every depth-subset of the suffix rows
  * (ell, k).  depth = 3 for g >= 4 unless engine == BZ_ENGINE_POPC, else 2
  * for g >= 3, else 1 (g = 1: ell = -1, empty prefix). */

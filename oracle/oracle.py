@@ -247,11 +247,11 @@ def enumerate_chunks(gammas: list[list[int]], k: int, g: int, groups, nchunks: i
     starts = [gr[0] for gr in groups]
     for chunk in range(shard, nchunks, nshards):
         gi = max(i for i, s in enumerate(starts) if s <= chunk)
-        begin, nprefix, gamma, ell, ppl, _, depth = groups[gi]
+        begin, nprefix, gamma, ell, ppl, _, depth, lanes = groups[gi]
         local = chunk - begin
         rows = gammas[gamma]
-        for lane in range(32):
-            first = (local * 32 + lane) * ppl
+        for lane in range(lanes):
+            first = (local * lanes + lane) * ppl
             for p in range(first, min(first + ppl, nprefix)):
                 prefix = [] if g == 1 else colex_unrank(p, g - 1 - depth, ell) + [ell]
                 acc = 0

@@ -37,7 +37,8 @@ struct bz_ctx {
   int m = 0, k = 0, n = 0, w32 = 0, wp = 0;
   int engine = BZ_ENGINE_AUTO;
   uint32_t* d_rows = nullptr;   // m*k*wp
-  uint8_t* d_tbl = nullptr;     // m*(k+8) rows of 0/1 bytes (K2)
+  uint8_t* d_trip = nullptr;    // K3 triple tables: m x trip_rows rows of 0/1 bytes
+  size_t trip_rows = 0;         // rows per Gamma (C(k,3) + one tile of padding)
   uint32_t* d_px = nullptr;     // m*(k+1)*wp
   unsigned long long* d_binom = nullptr;
   // per-round scratch
@@ -135,7 +136,8 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, int depth,
         return fail(ctx, BZ_ERR_TOO_LARGE, "C(%d,%d) prefixes exceed 2^62", ell, g - 1 - depth);
       const long long work = (long long)binom_sat(k - 1 - ell, depth);
       long long ppl = std::max(1ll, lane_target / std::max(1ll, work));
-      const long long spread = (long long)((np + 31) / 32);
+      const long long lanes_ll = depth == 3 ? bz::kTcThreads : 32;
+      const long long spread = (long long)((np + lanes_ll - 1) / lanes_ll);
       ppl = std::min(ppl, std::max(1ll, spread));
       Group gr{};
       gr.chunk_begin = chunk;
@@ -144,7 +146,8 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, int depth,
       gr.ell = ell;
       gr.ppl = (int)ppl;
       gr.depth = depth;
-      const unsigned long long per_chunk = 32ull * (unsigned long long)ppl;
+      const unsigned long long lanes = depth == 3 ? (unsigned long long)bz::kTcThreads : 32ull;
+      const unsigned long long per_chunk = lanes * (unsigned long long)ppl;
       chunk += (np + per_chunk - 1) / per_chunk;
       gs.push_back(gr);
     }
@@ -219,23 +222,47 @@ int launch_wd(bz_ctx* ctx, const RoundArgs& a, bool hist) {
 
 template <int W>
 int launch_tc(bz_ctx* ctx, const RoundArgs& a) {
-  const size_t smem = bz::tc_smem_bytes<W>(a.m, a.k, a.ngroups);
-  const int threads = 256;
-  CK(cudaFuncSetAttribute(bz::k2_round_mma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = bz::k3_smem_bytes<W>(a.m, a.k, a.ngroups);
+  const int threads = bz::kTcThreads;
+  CK(cudaFuncSetAttribute(bz::k3_round_gemm<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)smem));
   int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bz::k2_round_mma<W>, threads, smem));
-  if (per_sm < 1) return fail(ctx, BZ_ERR_TOO_LARGE, "K2 does not fit on an SM (smem %zu)", smem);
-  unsigned long long warps_needed = (a.nchunks + a.nshards - 1) / a.nshards;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bz::k3_round_gemm<W>, threads, smem));
+  if (per_sm < 1) return fail(ctx, BZ_ERR_TOO_LARGE, "K3 does not fit on an SM (smem %zu)", smem);
+  const unsigned long long blocks_needed = (a.nchunks + a.nshards - 1) / a.nshards;
   long long blocks = (long long)per_sm * ctx->sm_count;
-  long long need = (long long)((warps_needed + (threads / 32) - 1) / (threads / 32));
-  blocks = std::max(1ll, std::min(blocks, need));
+  blocks = std::max(1ll, std::min(blocks, (long long)blocks_needed));
   CK(cudaEventRecord(ctx->ev_k0, ctx->stream));
-  bz::k2_round_mma<W><<<(unsigned)blocks, threads, smem, ctx->stream>>>(a, ctx->d_tbl);
+  bz::k3_round_gemm<W><<<(unsigned)blocks, threads, smem, ctx->stream>>>(a, ctx->d_trip,
+                                                                         ctx->trip_rows);
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
   ctx->launches += 1;
   return BZ_OK;
+}
+
+template <int W>
+int build_triples_w(bz_ctx* ctx) {
+  dim3 grid(ctx->k, ctx->m);
+  bz::k_build_triples<W><<<grid, 256, 0, ctx->stream>>>(ctx->d_rows, ctx->d_trip, ctx->k,
+                                                        ctx->trip_rows);
+  CK(cudaGetLastError());
+  ctx->launches += 1;
+  return BZ_OK;
+}
+
+int build_triples(bz_ctx* ctx) {
+  switch (ctx->w32) {
+    case 1: return build_triples_w<1>(ctx);
+    case 2: return build_triples_w<2>(ctx);
+    case 3: return build_triples_w<3>(ctx);
+    case 4: return build_triples_w<4>(ctx);
+    case 5: return build_triples_w<5>(ctx);
+    case 6: return build_triples_w<6>(ctx);
+    case 7: return build_triples_w<7>(ctx);
+    case 8: return build_triples_w<8>(ctx);
+    default: return fail(ctx, BZ_ERR_TOO_LARGE, "unsupported word count %d", ctx->w32);
+  }
 }
 
 template <int W>
@@ -377,7 +404,7 @@ void bz_destroy(bz_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     cudaFree(ctx->d_rows);
     cudaFree(ctx->d_px);
-    cudaFree(ctx->d_tbl);
+    cudaFree(ctx->d_trip);
     cudaFree(ctx->d_binom);
     cudaFree(ctx->d_groups);
     cudaFree(ctx->d_bound);
@@ -440,27 +467,24 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
         px[((size_t)j * (k + 1) + r + 1) * wp + w] =
             px[((size_t)j * (k + 1) + r) * wp + w] ^ img[((size_t)j * k + r) * wp + w];
   }
-  // 0/1 byte image for K2: row r, column c -> byte c (zero padding rows)
-  const int ts = bz::tc_stride(w32);
-  std::vector<uint8_t> tbl((size_t)m * (k + bz::kTcPadRows) * ts, 0u);
-  for (int j = 0; j < m; ++j)
-    for (int r = 0; r < k; ++r)
-      for (int col = 0; col < n; ++col) {
-        const uint32_t wv = img[((size_t)j * k + r) * wp + col / 32];
-        tbl[((size_t)j * (k + bz::kTcPadRows) + r) * ts + col] = (uint8_t)((wv >> (col % 32)) & 1u);
-      }
   cudaFree(ctx->d_rows);
   cudaFree(ctx->d_px);
-  cudaFree(ctx->d_tbl);
+  cudaFree(ctx->d_trip);
   ctx->d_rows = nullptr;
   ctx->d_px = nullptr;
-  ctx->d_tbl = nullptr;
-  CK(cudaMalloc(&ctx->d_tbl, tbl.size()));
-  CK(cudaMemcpy(ctx->d_tbl, tbl.data(), tbl.size(), cudaMemcpyHostToDevice));
+  ctx->d_trip = nullptr;
+  ctx->trip_rows = 0;
   CK(cudaMalloc(&ctx->d_rows, img.size() * 4));
   CK(cudaMalloc(&ctx->d_px, px.size() * 4));
   CK(cudaMemcpy(ctx->d_rows, img.data(), img.size() * 4, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ctx->d_px, px.data(), px.size() * 4, cudaMemcpyHostToDevice));
+  // K3 triple tables (device-built): every 3-subset of the rows, 0/1 bytes
+  if (k >= 4) {
+    const size_t rows3 = (size_t)k * (k - 1) * (k - 2) / 6 + bz::kTileRows;
+    CK(cudaMalloc(&ctx->d_trip, (size_t)m * rows3 * bz::tc_stride(w32)));
+    CK(cudaMemsetAsync(ctx->d_trip, 0, (size_t)m * rows3 * bz::tc_stride(w32), ctx->stream));
+    ctx->trip_rows = rows3;
+  }
   if (m + 1 > ctx->bound_cap) {
     cudaFree(ctx->d_bound);
     cudaFree(ctx->d_combos);
@@ -482,6 +506,11 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
   ctx->n = n;
   ctx->w32 = w32;
   ctx->wp = wp;
+  if (ctx->d_trip) {
+    int rc = build_triples(ctx);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(ctx->stream));
+  }
   return BZ_OK;
 }
 
@@ -556,14 +585,15 @@ int bz_plan(int m, int k, int g, int engine, int64_t* out, int cap, int* out_ngr
   if (out) {
     if ((int)gs.size() > cap) return BZ_ERR_ARGUMENT;
     for (size_t i = 0; i < gs.size(); ++i) {
-      out[7 * i + 0] = (int64_t)gs[i].chunk_begin;
-      out[7 * i + 1] = (int64_t)gs[i].nprefix;
-      out[7 * i + 2] = gs[i].gamma;
-      out[7 * i + 3] = gs[i].ell;
-      out[7 * i + 4] = gs[i].ppl;
-      out[7 * i + 5] = (int64_t)gs[i].nprefix *
+      out[8 * i + 0] = (int64_t)gs[i].chunk_begin;
+      out[8 * i + 1] = (int64_t)gs[i].nprefix;
+      out[8 * i + 2] = gs[i].gamma;
+      out[8 * i + 3] = gs[i].ell;
+      out[8 * i + 4] = gs[i].ppl;
+      out[8 * i + 5] = (int64_t)gs[i].nprefix *
                        (int64_t)binom_sat(k - 1 - gs[i].ell, gs[i].depth);
-      out[7 * i + 6] = gs[i].depth;
+      out[8 * i + 6] = gs[i].depth;
+      out[8 * i + 7] = gs[i].depth == 3 ? bz::kTcThreads : 32;
     }
   }
   return BZ_OK;

@@ -1,40 +1,50 @@
-// bz_tc.cuh -- K2: the round on the tensor pipe (legacy warp-level IMMA,
-// mma.sync.m16n8k32 s8 x s8 -> s32, native on sm_100a).
+// bz_tc.cuh -- K3: the round as a GEMM on the tensor pipe (legacy
+// warp-level IMMA, mma.sync.m16n8k32 s8 x s8 -> s32, native on sm_100a).
 //
 // The weight of a codeword P ^ S over GF(2) is an integer dot product:
 //     w(P ^ S) = w(P) + sum_j (1 - 2 P_j) * S_j ,
 // so with the prefix P encoded as +-1 bytes (A operand, 16 rows per m-tile)
 // and the suffix sum S encoded as 0/1 bytes (B operand, 8 columns per
-// n-tile), one IMMA chain over the n columns (K = 32 per instruction) with
-// the accumulator initialised to w(P) yields the exact weights of 16 x 8
-// codewords.  Every weight is exact (|values| <= 256 in s32).
+// n-tile), one IMMA chain over the n columns (K = 32 per instruction)
+// started from the accumulator w(P) yields the exact weights of 16 x 8
+// codewords (|values| <= 256: exact in s32).
 //
-// Work decomposition (same chunk/lane plan as K1, suffix depth D = 3):
-//   combination = prefix {(g-4)-subset of [0, ell)} + ell  (lane-owned
-//   walker, one prefix per lane per step)  +  suffix e1 < e2 < e3 in (ell, k).
-//   The 32 lanes' current prefixes form the A operand (two m16 tiles); the
-//   warp walks e1 < e2 uniformly, forms the fragment of R[e1] ^ R[e2] in
-//   registers, and streams e3 in n8 tiles through ldmatrix from a 0/1 byte
-//   image of the rows in shared memory; B = ldmatrix ^ (R[e1]^R[e2]).
-//   Tail columns (e3 >= k) read a zero row and are masked in the epilogue;
-//   lanes without a prefix duplicate a valid one (harmless for a minimum).
+// Decomposition (suffix depth D = 3, g >= 4): a g-combination is
+//   prefix = {(g-4)-subset of [0, ell)} + ell      (A side, lane walkers)
+//   suffix = {e1 < e2 < e3} with e1 > ell          (B side, a table row)
+// For each Gamma the device holds the TRIPLE TABLE: every 3-subset of the
+// rows as a 0/1 byte row, ordered by smallest element descending, so the
+// suffixes valid for ell -- all triples above ell -- are exactly its first
+// C(k-1-ell, 3) rows.  A (Gamma, ell) group is then a dense GEMM
+//   [C(ell, g-4) prefixes] x [C(k-1-ell, 3) triples] x [n columns]
+// with a min-reduction epilogue.  A block (8 warps = 256 prefixes, one per
+// lane) streams that slice of the table from L2 through shared memory in
+// double-buffered cp.async tiles of 64 triples; every warp multiplies its
+// two m16 tiles of prefixes against each n8 sub-tile (ldmatrix, no ALU work
+// on the B side), so the inner loop is 3 ldmatrix + 2W IMMA + 8 min.
 #pragma once
 
 #include "bz_kernels.cuh"
 
 namespace bz {
 
-// Byte stride of one row of the 0/1 image: 32 bytes per 32-column block plus
+// Byte stride of one row of a 0/1 table: 32 bytes per 32-column block plus
 // 16, so 8 consecutive rows hit 8 distinct 16-byte bank groups (ldmatrix is
 // conflict-free).
 __host__ __device__ constexpr int tc_stride(int w) { return 32 * w + 16; }
-constexpr int kTcPadRows = 8;  // zero rows after the k rows of each Gamma
+constexpr int kTileRows = 64;    // triples per cp.async tile
+constexpr int kTcThreads = 256;  // 8 warps, one prefix per lane
 
 // +-1 bytes of the 4 bits of `word` at `shift`: bit 0 -> 0x01, bit 1 -> 0xff.
 __device__ __forceinline__ uint32_t pm1_nibble(uint32_t word, int shift) {
   const uint32_t x = (word >> shift) & 0xFu;
   const uint32_t m = (x * 0x00204081u) & 0x01010101u;
   return m * 0xFEu + 0x01010101u;
+}
+
+// 0/1 bytes of the 4 bits of `word` at `shift`.
+__device__ __forceinline__ uint32_t bit_nibble(uint32_t word, int shift) {
+  return (((word >> shift) & 0xFu) * 0x00204081u) & 0x01010101u;
 }
 
 __device__ __forceinline__ void imma16832(int (&d)[4], const uint32_t (&a)[4], uint32_t b0,
@@ -58,70 +68,129 @@ __device__ __forceinline__ void ldsm_x2(uint32_t& r0, uint32_t& r1, uint32_t add
                : "r"(addr));
 }
 
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;"); }
+
+// ---------------------------------------------------------------------------
+// Triple table: row index of {a < b < c} = C(k-1-a, 3) + (lex rank of (b, c)
+// among the pairs of (a, k)).  Built on the device at load time; one block
+// per (Gamma, a), threads over (pair, 32-column word).
 template <int W>
-__host__ __device__ inline size_t tc_smem_bytes(int m, int k, int ngroups) {
-  size_t base = (smem_base_bytes<W>(m, k, ngroups) + 15) & ~size_t(15);
-  return base + (size_t)m * (k + kTcPadRows) * tc_stride(W);
+__global__ void k_build_triples(const uint32_t* __restrict__ rows, uint8_t* __restrict__ trip,
+                                int k, size_t gamma_stride_rows) {
+  constexpr int WP = padded_words(W);
+  constexpr int TS = tc_stride(W);
+  const int j = blockIdx.y, a = blockIdx.x;
+  if (a > k - 3) return;
+  const uint32_t* R = rows + (size_t)j * k * WP;
+  const long long base = (long long)(k - 1 - a) * (k - 2 - a) * (k - 3 - a) / 6;
+  const int span = k - 1 - a;  // candidates for b, c
+  const int npairs = span * (span - 1) / 2;
+  uint8_t* out = trip + (size_t)j * gamma_stride_rows * TS;
+  for (int t = threadIdx.x; t < npairs * W; t += blockDim.x) {
+    const int pi = t / W, w = t - pi * W;
+    // lex pair index pi -> (b, c) over (a, k)
+    int b = a + 1, rem = pi;
+    while (rem >= k - 1 - b) { rem -= k - 1 - b; ++b; }
+    const int c = b + 1 + rem;
+    const uint32_t v = R[a * WP + w] ^ R[b * WP + w] ^ R[c * WP + w];
+    uint32_t* dst = reinterpret_cast<uint32_t*>(out + (size_t)(base + pi) * TS + 32 * w);
+#pragma unroll
+    for (int s = 0; s < 8; ++s) dst[s] = bit_nibble(v, 4 * s);
+  }
 }
 
 template <int W>
-__global__ void __launch_bounds__(256)
-k2_round_mma(const RoundArgs a, const uint8_t* __restrict__ tbl) {
+__host__ __device__ inline size_t k3_smem_bytes(int m, int k, int ngroups) {
+  const size_t base = (smem_base_bytes<W>(m, k, ngroups) + 127) & ~size_t(127);
+  return base + 2 * (size_t)kTileRows * tc_stride(W) + 16;
+}
+
+template <int W>
+__global__ void __launch_bounds__(kTcThreads, 2)
+k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_stride_rows) {
   constexpr int TS = tc_stride(W);
   constexpr int WP = padded_words(W);
-  extern __shared__ __align__(16) unsigned char smem[];
-  // 0/1 byte image first (its copy overlaps the staging below)
-  const size_t tbase = (smem_base_bytes<W>(a.m, a.k, a.ngroups) + 15) & ~size_t(15);
-  unsigned char* stbl = smem + tbase;
-  {
-    const int n16 = a.m * (a.k + kTcPadRows) * TS / 16;
-    const uint4* src = reinterpret_cast<const uint4*>(tbl);
-    uint4* dst = reinterpret_cast<uint4*>(stbl);
-    for (int i = threadIdx.x; i < n16; i += blockDim.x) dst[i] = src[i];
-  }
+  constexpr int TILE_BYTES = kTileRows * TS;
+  constexpr int N16 = TILE_BYTES / 16;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const size_t bbase = (smem_base_bytes<W>(a.m, a.k, a.ngroups) + 127) & ~size_t(127);
+  unsigned char* sbuf = smem + bbase;                      // 2 tiles
+  int* sctl = reinterpret_cast<int*>(sbuf + 2 * TILE_BYTES);  // chunk broadcast
   uint32_t *srows, *spx;
   Group* sgroups;
   stage<W>(a, srows, spx, sgroups, smem);  // ends with __syncthreads
 
   const unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const int gid = lane >> 2, t0 = lane & 3;
   const int k = a.k, q = a.g - 4;
   volatile int* vbound = a.bound;
-  const uint32_t stbl_s = (uint32_t)__cvta_generic_to_shared(stbl);
-  // this lane's ldmatrix row offset inside an 8-row tile and its 16-byte half
-  const int ld_row = lane & 7;
-  const int ld_off = (lane >> 4) * 32 + ((lane >> 3) & 1) * 16;
+  const uint32_t sbuf_s = (uint32_t)__cvta_generic_to_shared(sbuf);
+  // this lane's ldmatrix row inside an 8-row sub-tile and its 16-byte half
+  const uint32_t ld_off = (uint32_t)((lane & 7) * TS + (lane >> 4) * 32 + ((lane >> 3) & 1) * 16);
 
   while (true) {
-    unsigned long long c = 0;
-    if (lane == 0) c = atomicAdd(a.counter, 1ull);
-    c = __shfl_sync(FULL, c, 0);
-    const unsigned long long chunk = c * (unsigned long long)a.nshards + a.shard;
-    if (chunk >= a.nchunks) break;
-    if (vbound[0] <= a.lower_prev) break;
+    if (tid == 0) {
+      const unsigned long long c = atomicAdd(a.counter, 1ull);
+      const unsigned long long chunk = c * (unsigned long long)a.nshards + a.shard;
+      const bool stop = chunk >= a.nchunks || vbound[0] <= a.lower_prev;
+      sctl[0] = stop ? -1 : find_group(sgroups, a.ngroups, chunk);
+      reinterpret_cast<unsigned long long*>(sctl)[1] = chunk;
+    }
+    __syncthreads();
+    const int gi = sctl[0];
+    const unsigned long long chunk = reinterpret_cast<unsigned long long*>(sctl)[1];
+    __syncthreads();
+    if (gi < 0) break;
 
-    const ChunkView v = open_chunk(sgroups, a.ngroups, chunk, lane);
-    const long long maxcnt = __shfl_sync(FULL, v.cnt, 0);
-    const unsigned long long first0 = __shfl_sync(FULL, v.first, 0);
-    const uint32_t* R = srows + v.gr.gamma * k * WP;
-    const uint32_t* PX = spx + v.gr.gamma * (k + 1) * px_stride(W);
-    const uint32_t tg = stbl_s + (uint32_t)(v.gr.gamma * (k + kTcPadRows) * TS);
-    const unsigned char* tgp = stbl + v.gr.gamma * (k + kTcPadRows) * TS;
-    const int e0 = v.gr.ell + 1;
+    const Group gr = sgroups[gi];
+    const unsigned long long local = chunk - gr.chunk_begin;
+    const unsigned long long bfirst = local * (unsigned long long)kTcThreads * gr.ppl;
+    const unsigned long long first = bfirst + (unsigned long long)tid * gr.ppl;
+    long long cnt = 0;
+    if (first < gr.nprefix) {
+      const unsigned long long left = gr.nprefix - first;
+      cnt = left < (unsigned long long)gr.ppl ? (long long)left : gr.ppl;
+    }
+    const unsigned long long bleft = gr.nprefix - bfirst;
+    const long long maxcnt = bleft < (unsigned long long)gr.ppl ? (long long)bleft : gr.ppl;
+    const uint32_t* R = srows + gr.gamma * k * WP;
+    const uint32_t* PX = spx + gr.gamma * (k + 1) * px_stride(W);
+    const int e0 = gr.ell + 1;
+    const long long t = k - e0;
+    const int slice = (int)(t * (t - 1) * (t - 2) / 6);  // triples above ell
+    const int ntiles = (slice + kTileRows - 1) / kTileRows;
+    const uint8_t* tsrc = trip + (size_t)gr.gamma * gamma_stride_rows * TS;
 
-    // lanes without prefixes duplicate lane 0's first prefix
+    // lanes without prefixes duplicate the block's first prefix
     Walker<W> wk;
-    wk.init(v.cnt > 0 ? v.first : first0, q, v.gr.ell, R, a.binom);
+    wk.init(cnt > 0 ? first : bfirst, q, gr.ell, R, a.binom);
+
+    auto load_tile = [&](int tile, int buf) {
+      const uint8_t* src = tsrc + (size_t)tile * TILE_BYTES;
+      const uint32_t dst = sbuf_s + (uint32_t)(buf * TILE_BYTES);
+      for (int i = tid; i < N16; i += kTcThreads) cp_async16(dst + 16 * i, src + 16 * i);
+      cp_async_commit();
+    };
 
     int best = INT_MAX;
+    uint32_t A[2][W][4];
+    int C0[4], C1[4];
+    long long s = 0;                         // flat (prefix step, tile) index
+    const long long nsteps = maxcnt * ntiles;
+    load_tile(0, 0);
     for (long long p = 0; p < maxcnt; ++p) {
-      // ---- A operand: the 32 lanes' prefixes as +-1 bytes; C init = w(P)
+      if (p > 0 && p < cnt) wk.step(PX);     // exhausted lanes keep a duplicate
+      // ---- A operand (+-1 prefix bytes) and C init (prefix weight)
       int wt = 0;
 #pragma unroll
       for (int j = 0; j < W; ++j) wt += __popc(wk.acc[j]);
-      uint32_t A[2][W][4];
-      int C0[4], C1[4];
 #pragma unroll
       for (int mt = 0; mt < 2; ++mt) {
         const int r0 = gid + 16 * mt, r1 = r0 + 8;
@@ -139,77 +208,62 @@ k2_round_mma(const RoundArgs a, const uint8_t* __restrict__ tbl) {
         else         { C1[0] = C1[1] = c0; C1[2] = C1[3] = c1; }
       }
 
-      // ---- suffixes e1 < e2 < e3 above ell
-#pragma unroll 1
-      for (int e1 = e0; e1 < k - 2; ++e1) {
-        uint32_t f1[W][2];
-        const unsigned char* p1 = tgp + e1 * TS + 4 * t0;
-#pragma unroll
-        for (int j = 0; j < W; ++j) {
-          f1[j][0] = *reinterpret_cast<const uint32_t*>(p1 + 32 * j);
-          f1[j][1] = *reinterpret_cast<const uint32_t*>(p1 + 32 * j + 16);
+      for (int tile = 0; tile < ntiles; ++tile, ++s) {
+        // prefetch the next tile into the other buffer (freed by the sync at
+        // the end of the previous step), then wait for this one
+        if (s + 1 < nsteps) {
+          const int nt = tile + 1 < ntiles ? tile + 1 : 0;
+          load_tile(nt, (int)((s + 1) & 1));
+          cp_async_wait1();
+        } else {
+          cp_async_wait0();
         }
-#pragma unroll 1
-        for (int e2 = e1 + 1; e2 < k - 1; ++e2) {
-          uint32_t f12[W][2];
-          const unsigned char* p2 = tgp + e2 * TS + 4 * t0;
+        __syncthreads();
+
+        // ---- 8 n8 sub-tiles of this 64-triple tile
+        const uint32_t tb = sbuf_s + (uint32_t)((s & 1) * TILE_BYTES) + ld_off;
+        const int col0 = tile * kTileRows;
+#pragma unroll 2
+        for (int sub = 0; sub < kTileRows / 8; ++sub) {
+          if (col0 + 8 * sub >= slice) break;
+          const uint32_t addr = tb + (uint32_t)(sub * 8 * TS);
+          uint32_t B[W][2];
 #pragma unroll
-          for (int j = 0; j < W; ++j) {
-            f12[j][0] = f1[j][0] ^ *reinterpret_cast<const uint32_t*>(p2 + 32 * j);
-            f12[j][1] = f1[j][1] ^ *reinterpret_cast<const uint32_t*>(p2 + 32 * j + 16);
+          for (int j = 0; j + 1 < W; j += 2) {
+            uint32_t r[4];
+            ldsm_x4(r, addr + 32 * j);
+            B[j][0] = r[0]; B[j][1] = r[1]; B[j + 1][0] = r[2]; B[j + 1][1] = r[3];
           }
-#pragma unroll 1
-          for (int e3 = e2 + 1; e3 < k; e3 += 8) {
-            const int row = min(e3 + ld_row, k);  // row k is all zero
-            const uint32_t addr = tg + (uint32_t)(row * TS + ld_off);
-            uint32_t B[W][2];
+          if constexpr (W & 1) ldsm_x2(B[W - 1][0], B[W - 1][1], addr + 32 * (W - 1));
+          int d0[4], d1[4];
+          imma16832(d0, A[0][0], B[0][0], B[0][1], C0);
+          imma16832(d1, A[1][0], B[0][0], B[0][1], C1);
 #pragma unroll
-            for (int j = 0; j + 1 < W; j += 2) {
-              uint32_t r[4];
-              ldsm_x4(r, addr + 32 * j);
-              B[j][0] = r[0] ^ f12[j][0];
-              B[j][1] = r[1] ^ f12[j][1];
-              B[j + 1][0] = r[2] ^ f12[j + 1][0];
-              B[j + 1][1] = r[3] ^ f12[j + 1][1];
-            }
-            if constexpr (W & 1) {
-              uint32_t r0, r1;
-              ldsm_x2(r0, r1, addr + 32 * (W - 1));
-              B[W - 1][0] = r0 ^ f12[W - 1][0];
-              B[W - 1][1] = r1 ^ f12[W - 1][1];
-            }
-            int d0[4], d1[4];
-            imma16832(d0, A[0][0], B[0][0], B[0][1], C0);
-            imma16832(d1, A[1][0], B[0][0], B[0][1], C1);
-#pragma unroll
-            for (int j = 1; j < W; ++j) {
-              imma16832(d0, A[0][j], B[j][0], B[j][1], d0);
-              imma16832(d1, A[1][j], B[j][0], B[j][1], d1);
-            }
-            if (e3 + 8 <= k) {
-              best = min(best, min(min(min(d0[0], d0[1]), min(d0[2], d0[3])),
-                                   min(min(d1[0], d1[1]), min(d1[2], d1[3]))));
-            } else {
-              const int col = e3 + 2 * t0;
-              const int m0 = col < k ? 0 : 0x3fffffff;
-              const int m1 = col + 1 < k ? 0 : 0x3fffffff;
-              best = min(best, min(min(d0[0] + m0, d0[1] + m1), min(d0[2] + m0, d0[3] + m1)));
-              best = min(best, min(min(d1[0] + m0, d1[1] + m1), min(d1[2] + m0, d1[3] + m1)));
-            }
+          for (int j = 1; j < W; ++j) {
+            imma16832(d0, A[0][j], B[j][0], B[j][1], d0);
+            imma16832(d1, A[1][j], B[j][0], B[j][1], d1);
+          }
+          if (col0 + 8 * sub + 8 <= slice) {
+            best = min(best, min(min(min(d0[0], d0[1]), min(d0[2], d0[3])),
+                                 min(min(d1[0], d1[1]), min(d1[2], d1[3]))));
+          } else {
+            const int col = col0 + 8 * sub + 2 * t0;
+            const int m0 = col < slice ? 0 : 0x3fffffff;
+            const int m1 = col + 1 < slice ? 0 : 0x3fffffff;
+            best = min(best, min(min(d0[0] + m0, d0[1] + m1), min(d0[2] + m0, d0[3] + m1)));
+            best = min(best, min(min(d1[0] + m0, d1[1] + m1), min(d1[2] + m0, d1[3] + m1)));
           }
         }
+        __syncthreads();  // buffer (s & 1) may be refilled by step s + 1's prefetch
       }
-      if (p + 1 < v.cnt) wk.step(PX);
     }
 
     const int wbest = __reduce_min_sync(FULL, best);
-    const unsigned tot = __reduce_add_sync(FULL, (unsigned)v.cnt);
+    const unsigned tot = __reduce_add_sync(FULL, (unsigned)cnt);
     if (lane == 0) {
-      if (wbest < vbound[1 + v.gr.gamma]) atomicMin(a.bound + 1 + v.gr.gamma, wbest);
+      if (wbest < vbound[1 + gr.gamma]) atomicMin(a.bound + 1 + gr.gamma, wbest);
       if (wbest < vbound[0]) atomicMin(a.bound, wbest);
-      const unsigned long long t = (unsigned long long)(k - e0);
-      atomicAdd(a.combos + v.gr.gamma,
-                (unsigned long long)tot * (t * (t - 1) * (t - 2) / 6));
+      if (tot) atomicAdd(a.combos + gr.gamma, (unsigned long long)tot * (unsigned long long)slice);
     }
   }
 }
