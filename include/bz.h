@@ -117,16 +117,19 @@ int bz_histogram(bz_ctx *ctx, int gamma, int g, int shard, int nshards,
                  uint64_t *out_hist, int32_t *out_min, uint64_t *out_combos);
 
 /* Host-only: the work plan bz_round uses for (m, k, g), for inspection and
- * for the CPU tests of the sharding logic.  Writes *out_ngroups groups of 8
+ * for the CPU tests of the sharding logic.  Writes *out_ngroups groups of 10
  * int64 each -- chunk_begin, nprefix, gamma, ell, prefixes_per_lane,
- * combinations, depth, lanes_per_chunk -- into out (capacity `cap` groups;
- * out may be NULL to query the count) and the round's chunk count into
- * *out_nchunks.  Chunk c of the round belongs to shard c % nshards; within
- * a chunk of group (gamma, ell), lane l (0 <= l < lanes_per_chunk: 32 for a
- * warp of K1, 256 for a block of K3) walks the colex ranks
- * [(c_local*lanes + l)*ppl, +ppl) of the (g-1-depth)-subsets of [0, ell), each
+ * combinations, depth, lanes_per_chunk, suffixes_per_chunk, suffix_blocks --
+ * into out (capacity `cap` groups; out may be NULL to query the count) and
+ * the round's chunk count into *out_nchunks.  Chunk c of the round belongs
+ * to shard c % nshards.  Within group (gamma, ell), local chunk index
+ * c_local = pb * suffix_blocks + sb: lane l (0 <= l < lanes_per_chunk: 32
+ * for a warp of K1, 256 for a block of K3) walks the colex ranks
+ * [(pb*lanes + l)*ppl, +ppl) of the (g-1-depth)-subsets of [0, ell), each
  * extended by ell and then by every depth-subset of the suffix rows
- * (ell, k).  depth = 3 for g >= 4 unless engine == BZ_ENGINE_POPC, else 2
+ * (ell, k) -- for depth 3 only those with index in [sb*S, (sb+1)*S) of the
+ * triple order (smallest element descending, then lex), S =
+ * suffixes_per_chunk.  depth = 3 for g >= 4 unless engine == BZ_ENGINE_POPC, else 2
  * for g >= 3, else 1 (g = 1: ell = -1, empty prefix). */
 int bz_plan(int m, int k, int g, int engine, int64_t *out, int cap,
             int *out_ngroups, uint64_t *out_nchunks);

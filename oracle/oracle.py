@@ -247,17 +247,21 @@ def enumerate_chunks(gammas: list[list[int]], k: int, g: int, groups, nchunks: i
     starts = [gr[0] for gr in groups]
     for chunk in range(shard, nchunks, nshards):
         gi = max(i for i, s in enumerate(starts) if s <= chunk)
-        begin, nprefix, gamma, ell, ppl, _, depth, lanes = groups[gi]
+        begin, nprefix, gamma, ell, ppl, _, depth, lanes, spc, nsb = groups[gi]
         local = chunk - begin
+        pb, sb = divmod(local, nsb)
         rows = gammas[gamma]
+        sufs = suffix_order(ell, k, depth)
+        if depth == 3:
+            sufs = sufs[sb * spc:(sb + 1) * spc]
         for lane in range(lanes):
-            first = (local * lanes + lane) * ppl
+            first = (pb * lanes + lane) * ppl
             for p in range(first, min(first + ppl, nprefix)):
                 prefix = [] if g == 1 else colex_unrank(p, g - 1 - depth, ell) + [ell]
                 acc = 0
                 for i in prefix:
                     acc ^= rows[i]
-                for suf in itertools.combinations(range(ell + 1, k), depth):
+                for suf in sufs:
                     w = acc
                     for e in suf:
                         w ^= rows[e]
@@ -266,6 +270,17 @@ def enumerate_chunks(gammas: list[list[int]], k: int, g: int, groups, nchunks: i
                     cnt[gamma] += 1
                     seen.append((gamma, tuple(prefix + list(suf))))
     return mins, cnt, seen
+
+
+def suffix_order(ell: int, k: int, depth: int):
+    """Suffixes above ell in device order: lex for depth 1-2; for depth 3
+    the triple-table order (smallest element descending, then (b, c) lex)."""
+    if depth < 3:
+        return list(itertools.combinations(range(ell + 1, k), depth))
+    out = []
+    for a in range(k - 3, ell, -1):
+        out += [(a, b, c) for b, c in itertools.combinations(range(a + 1, k), 2)]
+    return out
 
 
 def all_combinations(m: int, k: int, g: int):

@@ -63,6 +63,7 @@ namespace {
 // problem size, so every process computes the same plan.
 constexpr long long kChunksTarget = 40000;
 constexpr long long kLaneMin = 32, kLaneMax = 4096;
+constexpr int kPlanCols = 10;  // int64 columns per group in bz_plan
 
 int fail(bz_ctx* c, int code, const char* fmt, ...) {
   char buf[512];
@@ -135,10 +136,17 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, int depth,
       if (np >= (1ull << 62))
         return fail(ctx, BZ_ERR_TOO_LARGE, "C(%d,%d) prefixes exceed 2^62", ell, g - 1 - depth);
       const long long work = (long long)binom_sat(k - 1 - ell, depth);
-      long long ppl = std::max(1ll, lane_target / std::max(1ll, work));
       const long long lanes_ll = depth == 3 ? bz::kTcThreads : 32;
       const long long spread = (long long)((np + lanes_ll - 1) / lanes_ll);
+      long long ppl = std::max(1ll, lane_target / std::max(1ll, work));
       ppl = std::min(ppl, std::max(1ll, spread));
+      // D = 3: a chunk is 256 prefixes x ppl steps x tpc tiles of 64
+      // triples; a slice too large for one chunk is split into tile blocks
+      long long ntiles = (work + bz::kTileRows - 1) / bz::kTileRows;
+      long long tpc = ntiles;
+      if (depth == 3 && work > lane_target)
+        tpc = std::max(1ll, lane_target / bz::kTileRows);
+      const long long ntb = depth == 3 ? (ntiles + tpc - 1) / tpc : 1;
       Group gr{};
       gr.chunk_begin = chunk;
       gr.nprefix = np;
@@ -146,9 +154,10 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, int depth,
       gr.ell = ell;
       gr.ppl = (int)ppl;
       gr.depth = depth;
-      const unsigned long long lanes = depth == 3 ? (unsigned long long)bz::kTcThreads : 32ull;
-      const unsigned long long per_chunk = lanes * (unsigned long long)ppl;
-      chunk += (np + per_chunk - 1) / per_chunk;
+      gr.tpc = (int)tpc;
+      gr.ntb = (int)ntb;
+      const unsigned long long per_chunk = (unsigned long long)lanes_ll * (unsigned long long)ppl;
+      chunk += (np + per_chunk - 1) / per_chunk * (unsigned long long)ntb;
       gs.push_back(gr);
     }
   }
@@ -585,15 +594,17 @@ int bz_plan(int m, int k, int g, int engine, int64_t* out, int cap, int* out_ngr
   if (out) {
     if ((int)gs.size() > cap) return BZ_ERR_ARGUMENT;
     for (size_t i = 0; i < gs.size(); ++i) {
-      out[8 * i + 0] = (int64_t)gs[i].chunk_begin;
-      out[8 * i + 1] = (int64_t)gs[i].nprefix;
-      out[8 * i + 2] = gs[i].gamma;
-      out[8 * i + 3] = gs[i].ell;
-      out[8 * i + 4] = gs[i].ppl;
-      out[8 * i + 5] = (int64_t)gs[i].nprefix *
-                       (int64_t)binom_sat(k - 1 - gs[i].ell, gs[i].depth);
-      out[8 * i + 6] = gs[i].depth;
-      out[8 * i + 7] = gs[i].depth == 3 ? bz::kTcThreads : 32;
+      int64_t* o = out + (size_t)kPlanCols * i;
+      o[0] = (int64_t)gs[i].chunk_begin;
+      o[1] = (int64_t)gs[i].nprefix;
+      o[2] = gs[i].gamma;
+      o[3] = gs[i].ell;
+      o[4] = gs[i].ppl;
+      o[5] = (int64_t)gs[i].nprefix * (int64_t)binom_sat(k - 1 - gs[i].ell, gs[i].depth);
+      o[6] = gs[i].depth;
+      o[7] = gs[i].depth == 3 ? bz::kTcThreads : 32;
+      o[8] = gs[i].depth == 3 ? (int64_t)gs[i].tpc * bz::kTileRows : 0;
+      o[9] = gs[i].ntb;
     }
   }
   return BZ_OK;

@@ -40,11 +40,13 @@ constexpr int kBinomDim = kMaxK + 1;  // C(p, q) for 0 <= p, q <= 128
 
 struct Group {
   unsigned long long chunk_begin;  // first global chunk index of the group
-  unsigned long long nprefix;      // C(ell, g-2) prefixes in the group
+  unsigned long long nprefix;      // C(ell, g-1-D) prefixes in the group
   int gamma;                       // matrix index
   int ell;                         // last prefix element (-1 when g == 1)
   int ppl;                         // prefixes per lane per chunk
-  int depth;                       // suffix depth D of the round (1 or 2)
+  int depth;                       // suffix depth D of the round (1, 2 or 3)
+  int tpc;                         // D = 3: suffix tiles per chunk
+  int ntb;                         // D = 3: tile blocks per prefix block
 };
 
 struct RoundArgs {

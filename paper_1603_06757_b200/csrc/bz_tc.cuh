@@ -151,7 +151,9 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
 
     const Group gr = sgroups[gi];
     const unsigned long long local = chunk - gr.chunk_begin;
-    const unsigned long long bfirst = local * (unsigned long long)kTcThreads * gr.ppl;
+    const unsigned long long pb = local / (unsigned long long)gr.ntb;
+    const int tb = (int)(local - pb * (unsigned long long)gr.ntb);
+    const unsigned long long bfirst = pb * (unsigned long long)kTcThreads * gr.ppl;
     const unsigned long long first = bfirst + (unsigned long long)tid * gr.ppl;
     long long cnt = 0;
     if (first < gr.nprefix) {
@@ -166,6 +168,9 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
     const long long t = k - e0;
     const int slice = (int)(t * (t - 1) * (t - 2) / 6);  // triples above ell
     const int ntiles = (slice + kTileRows - 1) / kTileRows;
+    const int tile_lo = tb * gr.tpc;
+    const int tile_hi = min(ntiles, tile_lo + gr.tpc);
+    const int nt = tile_hi - tile_lo;  // tiles per prefix step
     const uint8_t* tsrc = trip + (size_t)gr.gamma * gamma_stride_rows * TS;
 
     // lanes without prefixes duplicate the block's first prefix
@@ -182,11 +187,17 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
     int best = INT_MAX;
     uint32_t A[2][W][4];
     int C0[4], C1[4];
-    long long s = 0;                         // flat (prefix step, tile) index
-    const long long nsteps = maxcnt * ntiles;
-    load_tile(0, 0);
+    // one tile per step: it stays resident for every prefix step
+    const bool resident = nt == 1;
+    long long s = 0;  // flat (prefix step, tile) index: buffer = s & 1
+    const long long nsteps = maxcnt * nt;
+    load_tile(tile_lo, 0);
+    if (resident) {
+      cp_async_wait0();
+      __syncthreads();
+    }
     for (long long p = 0; p < maxcnt; ++p) {
-      if (p > 0 && p < cnt) wk.step(PX);     // exhausted lanes keep a duplicate
+      if (p > 0 && p < cnt) wk.step(PX);  // exhausted lanes keep a duplicate
       // ---- A operand (+-1 prefix bytes) and C init (prefix weight)
       int wt = 0;
 #pragma unroll
@@ -208,25 +219,26 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
         else         { C1[0] = C1[1] = c0; C1[2] = C1[3] = c1; }
       }
 
-      for (int tile = 0; tile < ntiles; ++tile, ++s) {
-        // prefetch the next tile into the other buffer (freed by the sync at
-        // the end of the previous step), then wait for this one
-        if (s + 1 < nsteps) {
-          const int nt = tile + 1 < ntiles ? tile + 1 : 0;
-          load_tile(nt, (int)((s + 1) & 1));
-          cp_async_wait1();
-        } else {
-          cp_async_wait0();
+      for (int tile = tile_lo; tile < tile_hi; ++tile, ++s) {
+        if (!resident) {
+          // prefetch the next tile into the other buffer (freed by the sync
+          // at the end of the previous step), then wait for this one
+          if (s + 1 < nsteps) {
+            load_tile(tile + 1 < tile_hi ? tile + 1 : tile_lo, (int)((s + 1) & 1));
+            cp_async_wait1();
+          } else {
+            cp_async_wait0();
+          }
+          __syncthreads();
         }
-        __syncthreads();
 
         // ---- 8 n8 sub-tiles of this 64-triple tile
-        const uint32_t tb = sbuf_s + (uint32_t)((s & 1) * TILE_BYTES) + ld_off;
+        const uint32_t tbuf = sbuf_s + (uint32_t)((resident ? 0 : (s & 1)) * TILE_BYTES) + ld_off;
         const int col0 = tile * kTileRows;
 #pragma unroll 2
         for (int sub = 0; sub < kTileRows / 8; ++sub) {
           if (col0 + 8 * sub >= slice) break;
-          const uint32_t addr = tb + (uint32_t)(sub * 8 * TS);
+          const uint32_t addr = tbuf + (uint32_t)(sub * 8 * TS);
           uint32_t B[W][2];
 #pragma unroll
           for (int j = 0; j + 1 < W; j += 2) {
@@ -254,16 +266,21 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
             best = min(best, min(min(d1[0] + m0, d1[1] + m1), min(d1[2] + m0, d1[3] + m1)));
           }
         }
-        __syncthreads();  // buffer (s & 1) may be refilled by step s + 1's prefetch
+        if (!resident) __syncthreads();  // buffer (s & 1) is refilled at step s + 1
       }
     }
+    if (resident) __syncthreads();  // the next chunk reloads buffer 0
 
+    // visited combinations: this chunk's prefixes x its triples
+    const long long col_lo = (long long)tile_lo * kTileRows;
+    const long long col_hi = min((long long)tile_hi * kTileRows, (long long)slice);
+    const unsigned long long ncols = (unsigned long long)(col_hi - col_lo);
     const int wbest = __reduce_min_sync(FULL, best);
     const unsigned tot = __reduce_add_sync(FULL, (unsigned)cnt);
     if (lane == 0) {
       if (wbest < vbound[1 + gr.gamma]) atomicMin(a.bound + 1 + gr.gamma, wbest);
       if (wbest < vbound[0]) atomicMin(a.bound, wbest);
-      if (tot) atomicAdd(a.combos + gr.gamma, (unsigned long long)tot * (unsigned long long)slice);
+      if (tot) atomicAdd(a.combos + gr.gamma, (unsigned long long)tot * ncols);
     }
   }
 }

@@ -46,7 +46,8 @@ def test_plan_counts(engine):
         starts = [gr[0] for gr in groups]
         assert starts == sorted(starts) and starts[0] == 0
         for gr in groups:
-            begin, nprefix, gamma, ell, ppl, combos, depth, lanes = gr
+            begin, nprefix, gamma, ell, ppl, combos, depth, lanes, spc, nsb = gr
+            assert nsb >= 1 and (depth != 3 or spc * nsb >= comb(k - 1 - ell, 3))
             assert lanes == (256 if depth == 3 else 32)
             want = 3 if (engine == "auto" and g >= 4) else (2 if g >= 3 else 1)
             assert depth == want
