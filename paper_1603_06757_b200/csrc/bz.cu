@@ -138,7 +138,11 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, int depth,
       const long long work = (long long)binom_sat(k - 1 - ell, depth);
       const long long lanes_ll = depth == 3 ? bz::kTcThreads : 32;
       const long long spread = (long long)((np + lanes_ll - 1) / lanes_ll);
-      long long ppl = std::max(1ll, lane_target / std::max(1ll, work));
+      // D = 3: every prefix step also rebuilds the A operand (about as much
+      // issue time as 256 codewords per lane), which bounds chunk duration
+      // for the tiny slices near ell = k - 4
+      const long long step_cost = depth == 3 ? work + 256 : work;
+      long long ppl = std::max(1ll, lane_target / std::max(1ll, step_cost));
       ppl = std::min(ppl, std::max(1ll, spread));
       // D = 3: a chunk is 256 prefixes x ppl steps x tpc tiles of 64
       // triples; a slice too large for one chunk is split into tile blocks

@@ -186,7 +186,7 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
 
     int best = INT_MAX;
     uint32_t A[2][W][4];
-    int C0[4], C1[4];
+    int wrow[4];  // prefix weights of this thread's rows g, g+8, g+16, g+24
     // one tile per step: it stays resident for every prefix step
     const bool resident = nt == 1;
     long long s = 0;  // flat (prefix step, tile) index: buffer = s & 1
@@ -214,10 +214,12 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
           A[mt][j][2] = pm1_nibble(w0, 16 + 4 * t0);
           A[mt][j][3] = pm1_nibble(w1, 16 + 4 * t0);
         }
-        const int c0 = __shfl_sync(FULL, wt, r0), c1 = __shfl_sync(FULL, wt, r1);
-        if (mt == 0) { C0[0] = C0[1] = c0; C0[2] = C0[3] = c1; }
-        else         { C1[0] = C1[1] = c0; C1[2] = C1[3] = c1; }
+        wrow[2 * mt] = __shfl_sync(FULL, wt, r0);
+        wrow[2 * mt + 1] = __shfl_sync(FULL, wt, r1);
       }
+      // running minima of sum_j (1 - 2 P_j) S_j per row; w(P) is added once
+      // per prefix step (min over columns commutes with the row constant)
+      int rmin[4] = {INT_MAX / 2, INT_MAX / 2, INT_MAX / 2, INT_MAX / 2};
 
       for (int tile = tile_lo; tile < tile_hi; ++tile, ++s) {
         if (!resident) {
@@ -247,27 +249,50 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
             B[j][0] = r[0]; B[j][1] = r[1]; B[j + 1][0] = r[2]; B[j + 1][1] = r[3];
           }
           if constexpr (W & 1) ldsm_x2(B[W - 1][0], B[W - 1][1], addr + 32 * (W - 1));
-          int d0[4], d1[4];
-          imma16832(d0, A[0][0], B[0][0], B[0][1], C0);
-          imma16832(d1, A[1][0], B[0][0], B[0][1], C1);
+          // two independent K-chains per m-tile (words [0, H) and [H, W))
+          constexpr int H = (W + 1) / 2;
+          const int zero4[4] = {0, 0, 0, 0};
+          int d0[4], d1[4], e0v[4], e1v[4];
+          imma16832(d0, A[0][0], B[0][0], B[0][1], zero4);
+          imma16832(d1, A[1][0], B[0][0], B[0][1], zero4);
+          if constexpr (W > 1) {
+            imma16832(e0v, A[0][H], B[H][0], B[H][1], zero4);
+            imma16832(e1v, A[1][H], B[H][0], B[H][1], zero4);
+          }
 #pragma unroll
-          for (int j = 1; j < W; ++j) {
+          for (int j = 1; j < H; ++j) {
             imma16832(d0, A[0][j], B[j][0], B[j][1], d0);
             imma16832(d1, A[1][j], B[j][0], B[j][1], d1);
           }
+#pragma unroll
+          for (int j = H + 1; j < W; ++j) {
+            imma16832(e0v, A[0][j], B[j][0], B[j][1], e0v);
+            imma16832(e1v, A[1][j], B[j][0], B[j][1], e1v);
+          }
+          if constexpr (W == 1) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) { e0v[i] = 0; e1v[i] = 0; }
+          }
+          // c0,c1: row g (cols 2t0, 2t0+1); c2,c3: row g+8
           if (col0 + 8 * sub + 8 <= slice) {
-            best = min(best, min(min(min(d0[0], d0[1]), min(d0[2], d0[3])),
-                                 min(min(d1[0], d1[1]), min(d1[2], d1[3]))));
+            rmin[0] = min(rmin[0], min(d0[0] + e0v[0], d0[1] + e0v[1]));
+            rmin[1] = min(rmin[1], min(d0[2] + e0v[2], d0[3] + e0v[3]));
+            rmin[2] = min(rmin[2], min(d1[0] + e1v[0], d1[1] + e1v[1]));
+            rmin[3] = min(rmin[3], min(d1[2] + e1v[2], d1[3] + e1v[3]));
           } else {
             const int col = col0 + 8 * sub + 2 * t0;
             const int m0 = col < slice ? 0 : 0x3fffffff;
             const int m1 = col + 1 < slice ? 0 : 0x3fffffff;
-            best = min(best, min(min(d0[0] + m0, d0[1] + m1), min(d0[2] + m0, d0[3] + m1)));
-            best = min(best, min(min(d1[0] + m0, d1[1] + m1), min(d1[2] + m0, d1[3] + m1)));
+            rmin[0] = min(rmin[0], min(d0[0] + e0v[0] + m0, d0[1] + e0v[1] + m1));
+            rmin[1] = min(rmin[1], min(d0[2] + e0v[2] + m0, d0[3] + e0v[3] + m1));
+            rmin[2] = min(rmin[2], min(d1[0] + e1v[0] + m0, d1[1] + e1v[1] + m1));
+            rmin[3] = min(rmin[3], min(d1[2] + e1v[2] + m0, d1[3] + e1v[3] + m1));
           }
         }
         if (!resident) __syncthreads();  // buffer (s & 1) is refilled at step s + 1
       }
+      best = min(best, min(min(rmin[0] + wrow[0], rmin[1] + wrow[1]),
+                           min(rmin[2] + wrow[2], rmin[3] + wrow[3])));
     }
     if (resident) __syncthreads();  // the next chunk reloads buffer 0
 
