@@ -104,18 +104,6 @@ __global__ void k_build_triples(const uint32_t* __restrict__ rows, uint8_t* __re
   }
 }
 
-// B fragments (W k-blocks) of one n8 sub-tile: 0/1 bytes of 8 table rows.
-template <int W>
-__device__ __forceinline__ void load_b(uint32_t (&B)[W][2], uint32_t addr) {
-#pragma unroll
-  for (int j = 0; j + 1 < W; j += 2) {
-    uint32_t r[4];
-    ldsm_x4(r, addr + 32 * j);
-    B[j][0] = r[0]; B[j][1] = r[1]; B[j + 1][0] = r[2]; B[j + 1][1] = r[3];
-  }
-  if constexpr (W & 1) ldsm_x2(B[W - 1][0], B[W - 1][1], addr + 32 * (W - 1));
-}
-
 template <int W>
 __host__ __device__ inline size_t k3_smem_bytes(int m, int k, int ngroups) {
   const size_t base = (smem_base_bytes<W>(m, k, ngroups) + 127) & ~size_t(127);
@@ -246,18 +234,21 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
           __syncthreads();
         }
 
-        // ---- the n8 sub-tiles of this 64-triple tile.  B fragments of the
-        // next sub-tile are loaded before the IMMAs of the current one, and
-        // the epilogue is branch-free (tail columns masked by +2^30).
+        // ---- 8 n8 sub-tiles of this 64-triple tile
         const uint32_t tbuf = sbuf_s + (uint32_t)((resident ? 0 : (s & 1)) * TILE_BYTES) + ld_off;
         const int col0 = tile * kTileRows;
-        const int nsub = min(kTileRows / 8, (slice - col0 + 7) / 8);
-        uint32_t B[W][2];
-        load_b<W>(B, tbuf);
-#pragma unroll 1
-        for (int sub = 0; sub < nsub; ++sub) {
-          uint32_t Bn[W][2];
-          if (sub + 1 < nsub) load_b<W>(Bn, tbuf + (uint32_t)((sub + 1) * 8 * TS));
+#pragma unroll 2
+        for (int sub = 0; sub < kTileRows / 8; ++sub) {
+          if (col0 + 8 * sub >= slice) break;
+          const uint32_t addr = tbuf + (uint32_t)(sub * 8 * TS);
+          uint32_t B[W][2];
+#pragma unroll
+          for (int j = 0; j + 1 < W; j += 2) {
+            uint32_t r[4];
+            ldsm_x4(r, addr + 32 * j);
+            B[j][0] = r[0]; B[j][1] = r[1]; B[j + 1][0] = r[2]; B[j + 1][1] = r[3];
+          }
+          if constexpr (W & 1) ldsm_x2(B[W - 1][0], B[W - 1][1], addr + 32 * (W - 1));
           // two independent K-chains per m-tile (words [0, H) and [H, W))
           constexpr int H = (W + 1) / 2;
           const int zero4[4] = {0, 0, 0, 0};
@@ -267,9 +258,6 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
           if constexpr (W > 1) {
             imma16832(e0v, A[0][H], B[H][0], B[H][1], zero4);
             imma16832(e1v, A[1][H], B[H][0], B[H][1], zero4);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 4; ++i) { e0v[i] = 0; e1v[i] = 0; }
           }
 #pragma unroll
           for (int j = 1; j < H; ++j) {
@@ -281,17 +269,24 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
             imma16832(e0v, A[0][j], B[j][0], B[j][1], e0v);
             imma16832(e1v, A[1][j], B[j][0], B[j][1], e1v);
           }
-          // c0,c1: row g (cols 2t0, 2t0+1); c2,c3: row g+8
-          const int col = col0 + 8 * sub + 2 * t0;
-          const int m0 = col < slice ? 0 : 0x3fffffff;
-          const int m1 = col + 1 < slice ? 0 : 0x3fffffff;
-          rmin[0] = min(rmin[0], min(d0[0] + e0v[0] + m0, d0[1] + e0v[1] + m1));
-          rmin[1] = min(rmin[1], min(d0[2] + e0v[2] + m0, d0[3] + e0v[3] + m1));
-          rmin[2] = min(rmin[2], min(d1[0] + e1v[0] + m0, d1[1] + e1v[1] + m1));
-          rmin[3] = min(rmin[3], min(d1[2] + e1v[2] + m0, d1[3] + e1v[3] + m1));
-          if (sub + 1 < nsub) {
+          if constexpr (W == 1) {
 #pragma unroll
-            for (int j = 0; j < W; ++j) { B[j][0] = Bn[j][0]; B[j][1] = Bn[j][1]; }
+            for (int i = 0; i < 4; ++i) { e0v[i] = 0; e1v[i] = 0; }
+          }
+          // c0,c1: row g (cols 2t0, 2t0+1); c2,c3: row g+8
+          if (col0 + 8 * sub + 8 <= slice) {
+            rmin[0] = min(rmin[0], min(d0[0] + e0v[0], d0[1] + e0v[1]));
+            rmin[1] = min(rmin[1], min(d0[2] + e0v[2], d0[3] + e0v[3]));
+            rmin[2] = min(rmin[2], min(d1[0] + e1v[0], d1[1] + e1v[1]));
+            rmin[3] = min(rmin[3], min(d1[2] + e1v[2], d1[3] + e1v[3]));
+          } else {
+            const int col = col0 + 8 * sub + 2 * t0;
+            const int m0 = col < slice ? 0 : 0x3fffffff;
+            const int m1 = col + 1 < slice ? 0 : 0x3fffffff;
+            rmin[0] = min(rmin[0], min(d0[0] + e0v[0] + m0, d0[1] + e0v[1] + m1));
+            rmin[1] = min(rmin[1], min(d0[2] + e0v[2] + m0, d0[3] + e0v[3] + m1));
+            rmin[2] = min(rmin[2], min(d1[0] + e1v[0] + m0, d1[1] + e1v[1] + m1));
+            rmin[3] = min(rmin[3], min(d1[2] + e1v[2] + m0, d1[3] + e1v[3] + m1));
           }
         }
         if (!resident) __syncthreads();  // buffer (s & 1) is refilled at step s + 1
