@@ -237,9 +237,9 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
         // ---- 8 n8 sub-tiles of this 64-triple tile
         const uint32_t tbuf = sbuf_s + (uint32_t)((resident ? 0 : (s & 1)) * TILE_BYTES) + ld_off;
         const int col0 = tile * kTileRows;
-        const int nsub = min(kTileRows / 8, (slice - col0 + 7) / 8);
 #pragma unroll 2
-        for (int sub = 0; sub < nsub; ++sub) {
+        for (int sub = 0; sub < kTileRows / 8; ++sub) {
+          if (col0 + 8 * sub >= slice) break;
           const uint32_t addr = tbuf + (uint32_t)(sub * 8 * TS);
           uint32_t B[W][2];
 #pragma unroll
@@ -273,15 +273,21 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
 #pragma unroll
             for (int i = 0; i < 4; ++i) { e0v[i] = 0; e1v[i] = 0; }
           }
-          // c0,c1: row g (cols 2t0, 2t0+1); c2,c3: row g+8; branch-free
-          // epilogue, tail columns masked by +2^30
-          const int col = col0 + 8 * sub + 2 * t0;
-          const int m0 = col < slice ? 0 : 0x3fffffff;
-          const int m1 = col + 1 < slice ? 0 : 0x3fffffff;
-          rmin[0] = min(rmin[0], min(d0[0] + e0v[0] + m0, d0[1] + e0v[1] + m1));
-          rmin[1] = min(rmin[1], min(d0[2] + e0v[2] + m0, d0[3] + e0v[3] + m1));
-          rmin[2] = min(rmin[2], min(d1[0] + e1v[0] + m0, d1[1] + e1v[1] + m1));
-          rmin[3] = min(rmin[3], min(d1[2] + e1v[2] + m0, d1[3] + e1v[3] + m1));
+          // c0,c1: row g (cols 2t0, 2t0+1); c2,c3: row g+8
+          if (col0 + 8 * sub + 8 <= slice) {
+            rmin[0] = min(rmin[0], min(d0[0] + e0v[0], d0[1] + e0v[1]));
+            rmin[1] = min(rmin[1], min(d0[2] + e0v[2], d0[3] + e0v[3]));
+            rmin[2] = min(rmin[2], min(d1[0] + e1v[0], d1[1] + e1v[1]));
+            rmin[3] = min(rmin[3], min(d1[2] + e1v[2], d1[3] + e1v[3]));
+          } else {
+            const int col = col0 + 8 * sub + 2 * t0;
+            const int m0 = col < slice ? 0 : 0x3fffffff;
+            const int m1 = col + 1 < slice ? 0 : 0x3fffffff;
+            rmin[0] = min(rmin[0], min(d0[0] + e0v[0] + m0, d0[1] + e0v[1] + m1));
+            rmin[1] = min(rmin[1], min(d0[2] + e0v[2] + m0, d0[3] + e0v[3] + m1));
+            rmin[2] = min(rmin[2], min(d1[0] + e1v[0] + m0, d1[1] + e1v[1] + m1));
+            rmin[3] = min(rmin[3], min(d1[2] + e1v[2] + m0, d1[3] + e1v[3] + m1));
+          }
         }
         if (!resident) __syncthreads();  // buffer (s & 1) is refilled at step s + 1
       }
