@@ -152,7 +152,9 @@ int bz_launch_count(bz_ctx *ctx, uint64_t *out);
  * second, out[2] = SM clock in MHz during the run, out[3] = SM count,
  * out[4] = POPC per clock per SM, out[5] = LOP3 per clock per SM,
  * out[6] = codewords/s of a synthetic W-word XOR+POPC+min loop (w_words
- * selects W, 1..8), out[7] = its codewords per clock per SM. */
+ * selects W, 1..8), out[7] = its codewords per clock per SM, out[8] = s8
+ * IMMA (mma.sync m16n8k32) multiply-accumulates per second, out[9] = IMMA
+ * MACs per clock per SM.  `out` must hold 10 doubles. */
 int bz_measure_int_peaks(bz_ctx *ctx, int w_words, double *out);
 
 #ifdef __cplusplus

@@ -660,7 +660,10 @@ int bz_measure_int_peaks(bz_ctx* ctx, int w_words, double* out) {
                  double* mhz) -> int {
     for (int rep = 0; rep < 2; ++rep) {  // first pass warms up clocks
       CK(cudaEventRecord(ctx->ev_a, ctx->stream));
-      if (which == 0)
+      if (which == 3)
+        bz::peak_imma<<<blocks, threads, 0, ctx->stream>>>(reinterpret_cast<int*>(d_out), 9u,
+                                                           iters, d_clk);
+      else if (which == 0)
         bz::peak_popc<<<blocks, threads, 0, ctx->stream>>>(d_out, 12345u, iters, d_clk);
       else if (which == 1)
         bz::peak_lop3<<<blocks, threads, 0, ctx->stream>>>(d_out, 12345u, iters, d_clk);
@@ -687,7 +690,10 @@ int bz_measure_int_peaks(bz_ctx* ctx, int w_words, double* out) {
     CK(cudaMemcpy(clk.data(), d_clk, sizeof(long long) * blocks, cudaMemcpyDeviceToHost));
     double max_clk = 0;
     for (long long c : clk) max_clk = std::max(max_clk, (double)c);
-    const double per_thread = which == 2 ? 4.0 * iters : 128.0 * iters;
+    // ops per thread: codewords (2), MACs (3: 4 chains x 16*8*32 MACs per
+    // warp-level MMA = 512 per lane), or single instructions (0, 1)
+    const double per_thread = which == 2 ? 4.0 * iters
+                            : which == 3 ? 4.0 * 512.0 * iters : 128.0 * iters;
     const double total = per_thread * threads * blocks;
     *ops_per_s = total / (ms * 1e-3);
     // per clock per SM: blocks resident concurrently (per_sm per SM)
@@ -695,10 +701,11 @@ int bz_measure_int_peaks(bz_ctx* ctx, int w_words, double* out) {
     *mhz = max_clk / (ms * 1e-3) / 1e6;
     return BZ_OK;
   };
-  double popc_s, popc_clk, lop_s, lop_clk, cw_s, cw_clk, mhz0, mhz1, mhz2;
+  double popc_s, popc_clk, lop_s, lop_clk, cw_s, cw_clk, mma_s, mma_clk, mhz0, mhz1, mhz2, mhz3;
   int rc = run(0, 2048, &popc_s, &popc_clk, &mhz0);
   if (!rc) rc = run(1, 2048, &lop_s, &lop_clk, &mhz1);
   if (!rc) rc = run(2, 16384, &cw_s, &cw_clk, &mhz2);
+  if (!rc) rc = run(3, 4096, &mma_s, &mma_clk, &mhz3);
   cudaFree(d_out);
   cudaFree(d_clk);
   if (rc) return rc;
@@ -710,6 +717,8 @@ int bz_measure_int_peaks(bz_ctx* ctx, int w_words, double* out) {
   out[5] = lop_clk;
   out[6] = cw_s;
   out[7] = cw_clk;
+  out[8] = mma_s;
+  out[9] = mma_clk;
   return BZ_OK;
 }
 

@@ -353,7 +353,7 @@ template <int W, int D>
 __global__ void __launch_bounds__(256)
 k1_round_min(const RoundArgs a) {
   constexpr int WP = padded_words(W);
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   uint32_t *srows, *spx;
   Group* sgroups;
   stage<W>(a, srows, spx, sgroups, smem);
@@ -422,7 +422,7 @@ template <int W, int D>
 __global__ void __launch_bounds__(256)
 k1h_histogram(const RoundArgs a) {
   constexpr int WP = padded_words(W);
-  extern __shared__ __align__(16) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   uint32_t *srows, *spx;
   Group* sgroups;
   const int nbins = a.n + 1;
@@ -548,6 +548,29 @@ __global__ void peak_lop3(uint32_t* out, uint32_t seed, int iters, long long* cl
   const long long t1 = clock64();
   if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
   out[blockIdx.x * blockDim.x + threadIdx.x] = y0 + y1 + y2 + y3 + y4 + y5 + y6 + y7;
+}
+
+// Legacy warp-level IMMA (mma.sync m16n8k32 s8) throughput: 4 independent
+// accumulator chains per warp -- the denominator of K3's tensor roofline.
+__global__ void peak_imma(int* out, uint32_t seed, int iters, long long* clk) {
+  uint32_t a0 = seed ^ threadIdx.x, a1 = a0 * 3u, a2 = a0 * 5u, a3 = a0 * 7u;
+  uint32_t b0 = a0 * 11u, b1 = a0 * 13u;
+  int c[4][4] = {};
+  const long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int ch = 0; ch < 4; ++ch)
+      asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, "
+                   "{%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                   : "+r"(c[ch][0]), "+r"(c[ch][1]), "+r"(c[ch][2]), "+r"(c[ch][3])
+                   : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0) clk[blockIdx.x] = t1 - t0;
+  int s = 0;
+#pragma unroll
+  for (int ch = 0; ch < 4; ++ch) s += c[ch][0] + c[ch][1] + c[ch][2] + c[ch][3];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
 // Synthetic codeword loop: register-resident rows, W words, 4 codewords per

@@ -127,7 +127,7 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
 
   const unsigned FULL = 0xffffffffu;
   const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
+  const int lane = tid & 31;
   const int gid = lane >> 2, t0 = lane & 3;
   const int k = a.k, q = a.g - 4;
   volatile int* vbound = a.bound;
