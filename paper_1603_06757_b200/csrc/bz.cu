@@ -691,9 +691,9 @@ int bz_measure_int_peaks(bz_ctx* ctx, int w_words, double* out) {
     double max_clk = 0;
     for (long long c : clk) max_clk = std::max(max_clk, (double)c);
     // ops per thread: codewords (2), MACs (3: 4 chains x 16*8*32 MACs per
-    // warp-level MMA = 512 per lane), or single instructions (0, 1)
+    // warp-level MMA = 128 per lane), or single instructions (0, 1)
     const double per_thread = which == 2 ? 4.0 * iters
-                            : which == 3 ? 4.0 * 512.0 * iters : 128.0 * iters;
+                            : which == 3 ? 4.0 * 128.0 * iters : 128.0 * iters;
     const double total = per_thread * threads * blocks;
     *ops_per_s = total / (ms * 1e-3);
     // per clock per SM: blocks resident concurrently (per_sm per SM)
