@@ -60,9 +60,10 @@ extern "C" {
 #define BZ_ERR_ARGUMENT 7           /* null pointer, bad shard                   */
 
 /* enumeration engines (bz_set_engine) */
-#define BZ_ENGINE_AUTO 0 /* tensor-pipe K3 for g >= 4, POPC K1 otherwise */
+#define BZ_ENGINE_AUTO 0 /* K4 for g >= 4, K1 otherwise                     */
 #define BZ_ENGINE_POPC 1 /* K1 only: XOR + POPC on the integer pipes       */
-#define BZ_ENGINE_IMMA 2 /* same as AUTO (K3 needs g >= 4)                  */
+#define BZ_ENGINE_IMMA 2 /* K3 (legacy warp-level IMMA) for g >= 4        */
+#define BZ_ENGINE_UMMA 3 /* K4 (tcgen05.mma kind::i8, TMEM) for g >= 4     */
 
 typedef struct bz_ctx bz_ctx;
 
@@ -129,7 +130,8 @@ int bz_histogram(bz_ctx *ctx, int gamma, int g, int shard, int nshards,
  * extended by ell and then by every depth-subset of the suffix rows
  * (ell, k) -- for depth 3 only those with index in [sb*S, (sb+1)*S) of the
  * triple order (smallest element descending, then lex), S =
- * suffixes_per_chunk.  depth = 3 for g >= 4 unless engine == BZ_ENGINE_POPC, else 2
+ * suffixes_per_chunk.  lanes_per_chunk: 32 (K1 warp), 256 (K3 block), 128
+ * (K4 block).  depth = 3 for g >= 4 unless engine == BZ_ENGINE_POPC, else 2
  * for g >= 3, else 1 (g = 1: ell = -1, empty prefix). */
 int bz_plan(int m, int k, int g, int engine, int64_t *out, int cap,
             int *out_ngroups, uint64_t *out_nchunks);

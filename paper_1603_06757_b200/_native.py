@@ -98,7 +98,7 @@ def device_count() -> int:
     return int(lib().bz_device_count())
 
 
-ENGINES = {"auto": 0, "popc": 1, "imma": 2}
+ENGINES = {"auto": 0, "popc": 1, "imma": 2, "umma": 3}
 
 
 def plan(m: int, k: int, g: int, engine: str = "auto"):
@@ -158,7 +158,8 @@ class Context:
         return self._h
 
     def set_engine(self, engine: str) -> None:
-        """'auto' (tensor-pipe K2 for g >= 4), 'popc' (K1 only) or 'imma'."""
+        """'auto' (= 'umma': tcgen05 K4 for g >= 4), 'popc' (K1 only) or
+        'imma' (legacy-IMMA K3 for g >= 4)."""
         if engine not in ENGINES:
             raise ValueError(f"unknown engine {engine!r}")
         check(lib().bz_set_engine(self.handle, ENGINES[engine]), self.handle, "bz_set_engine")

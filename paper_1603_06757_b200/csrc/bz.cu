@@ -19,6 +19,7 @@
 #include "../../include/bz.h"
 #include "bz_kernels.cuh"
 #include "bz_tc.cuh"
+#include "bz_umma.cuh"
 
 using bz::Group;
 using bz::RoundArgs;
@@ -39,6 +40,8 @@ struct bz_ctx {
   uint32_t* d_rows = nullptr;   // m*k*wp
   uint8_t* d_trip = nullptr;    // K3 triple tables: m x trip_rows rows of 0/1 bytes
   size_t trip_rows = 0;         // rows per Gamma (C(k,3) + one tile of padding)
+  uint8_t* d_trip4 = nullptr;   // K4 triple tables (UMMA core-matrix layout)
+  size_t trip4_rows = 0;        // rows per Gamma (C(k,3) rounded up to a tile, + a tile)
   uint32_t* d_px = nullptr;     // m*(k+1)*wp
   unsigned long long* d_binom = nullptr;
   // per-round scratch
@@ -111,15 +114,25 @@ int ensure_round_buffers(bz_ctx* ctx, int ngroups) {
 
 // Work plan of one round (host only): one Group per (Gamma, ell) with its
 // chunk range.  gamma_only < 0: all m Gammas.
-// Suffix depth of a pass: K2 (tensor pipe) takes D = 3 for g >= 4; K1
-// (POPC) takes D = 2 for g >= 3, else 1.  The histogram always runs on K1.
-int pass_depth(int engine, int g, bool hist) {
-  if (!hist && engine != BZ_ENGINE_POPC && g >= 4) return 3;
-  return g >= 3 ? 2 : 1;
+// Shape of a pass: suffix depth D, prefixes walked in parallel per chunk,
+// triples per tile.  K4 (tcgen05) and K3 (legacy IMMA) take D = 3 for
+// g >= 4; K1 (POPC) takes D = 2 for g >= 3, else 1.  Histograms run on K1.
+struct PlanShape {
+  int depth, lanes, tile_rows, kernel;  // kernel: 1 = K1, 3 = K3, 4 = K4
+};
+
+PlanShape pass_shape(int engine, int g, bool hist) {
+  if (!hist && g >= 4) {
+    if (engine == BZ_ENGINE_IMMA) return {3, bz::kTcThreads, bz::kTileRows, 3};
+    if (engine == BZ_ENGINE_AUTO || engine == BZ_ENGINE_UMMA)
+      return {3, bz::kUmmaM, bz::kUmmaN, 4};
+  }
+  return {g >= 3 ? 2 : 1, 32, 0, 1};
 }
 
-int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, int depth,
+int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape,
                std::vector<Group>& gs, unsigned long long* out_nchunks) {
+  const int depth = shape.depth;
   gs.clear();
   unsigned long long chunk = 0;
   const int j0 = gamma_only < 0 ? 0 : gamma_only;
@@ -136,20 +149,21 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, int depth,
       if (np >= (1ull << 62))
         return fail(ctx, BZ_ERR_TOO_LARGE, "C(%d,%d) prefixes exceed 2^62", ell, g - 1 - depth);
       const long long work = (long long)binom_sat(k - 1 - ell, depth);
-      const long long lanes_ll = depth == 3 ? bz::kTcThreads : 32;
+      const long long lanes_ll = shape.lanes;
       const long long spread = (long long)((np + lanes_ll - 1) / lanes_ll);
-      // D = 3: every prefix step also rebuilds the A operand (about as much
-      // issue time as 256 codewords per lane), which bounds chunk duration
-      // for the tiny slices near ell = k - 4
-      const long long step_cost = depth == 3 ? work + 256 : work;
+      // D = 3: every prefix step also rebuilds the A operand and streams at
+      // least one whole tile, which bounds chunk duration for the tiny
+      // slices near ell = k - 4
+      const long long step_cost = depth == 3 ? std::max(work, (long long)shape.tile_rows) + 256 : work;
       long long ppl = std::max(1ll, lane_target / std::max(1ll, step_cost));
       ppl = std::min(ppl, std::max(1ll, spread));
       // D = 3: a chunk is 256 prefixes x ppl steps x tpc tiles of 64
       // triples; a slice too large for one chunk is split into tile blocks
-      long long ntiles = (work + bz::kTileRows - 1) / bz::kTileRows;
+      const long long trows = depth == 3 ? shape.tile_rows : 1;
+      long long ntiles = (work + trows - 1) / trows;
       long long tpc = ntiles;
       if (depth == 3 && work > lane_target)
-        tpc = std::max(1ll, lane_target / bz::kTileRows);
+        tpc = std::max(1ll, lane_target / trows);
       const long long ntb = depth == 3 ? (ntiles + tpc - 1) / tpc : 1;
       Group gr{};
       gr.chunk_begin = chunk;
@@ -160,6 +174,8 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, int depth,
       gr.depth = depth;
       gr.tpc = (int)tpc;
       gr.ntb = (int)ntb;
+      gr.lanes = shape.lanes;
+      gr.tile_rows = shape.tile_rows;
       const unsigned long long per_chunk = (unsigned long long)lanes_ll * (unsigned long long)ppl;
       chunk += (np + per_chunk - 1) / per_chunk * (unsigned long long)ntb;
       gs.push_back(gr);
@@ -170,10 +186,10 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, int depth,
 }
 
 // Build the round's group table and upload it.
-int plan_round(bz_ctx* ctx, int g, int gamma_only, int depth, int* out_ngroups,
+int plan_round(bz_ctx* ctx, int g, int gamma_only, PlanShape shape, int* out_ngroups,
                unsigned long long* out_nchunks) {
   std::vector<Group> gs;
-  int rc = build_plan(ctx, ctx->m, ctx->k, g, gamma_only, depth, gs, out_nchunks);
+  int rc = build_plan(ctx, ctx->m, ctx->k, g, gamma_only, shape, gs, out_nchunks);
   if (rc) return rc;
   rc = ensure_round_buffers(ctx, (int)gs.size());
   if (rc) return rc;
@@ -255,12 +271,31 @@ int launch_tc(bz_ctx* ctx, const RoundArgs& a) {
 }
 
 template <int W>
+int launch_umma(bz_ctx* ctx, const RoundArgs& a) {
+  const size_t smem = bz::k4_smem_bytes<W>(a.m, a.k, a.ngroups);
+  CK(cudaFuncSetAttribute(bz::k4_round_umma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  const unsigned long long mine = (a.nchunks + a.nshards - 1 - a.shard) / a.nshards;
+  long long blocks = std::max(1ll, std::min((long long)ctx->sm_count, (long long)mine));
+  CK(cudaEventRecord(ctx->ev_k0, ctx->stream));
+  bz::k4_round_umma<W><<<(unsigned)blocks, bz::kK4Threads, smem, ctx->stream>>>(
+      a, ctx->d_trip4, ctx->trip4_rows);
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
+  ctx->launches += 1;
+  return BZ_OK;
+}
+
+template <int W>
 int build_triples_w(bz_ctx* ctx) {
   dim3 grid(ctx->k, ctx->m);
   bz::k_build_triples<W><<<grid, 256, 0, ctx->stream>>>(ctx->d_rows, ctx->d_trip, ctx->k,
                                                         ctx->trip_rows);
   CK(cudaGetLastError());
-  ctx->launches += 1;
+  bz::k_build_triples_umma<W><<<grid, 256, 0, ctx->stream>>>(ctx->d_rows, ctx->d_trip4, ctx->k,
+                                                             ctx->trip4_rows);
+  CK(cudaGetLastError());
+  ctx->launches += 2;
   return BZ_OK;
 }
 
@@ -279,12 +314,13 @@ int build_triples(bz_ctx* ctx) {
 }
 
 template <int W>
-int launch_w(bz_ctx* ctx, const RoundArgs& a, bool hist, int depth) {
-  if (depth == 3) return launch_tc<W>(ctx, a);
-  return depth == 2 ? launch_wd<W, 2>(ctx, a, hist) : launch_wd<W, 1>(ctx, a, hist);
+int launch_w(bz_ctx* ctx, const RoundArgs& a, bool hist, const PlanShape& shape) {
+  if (shape.kernel == 4) return launch_umma<W>(ctx, a);
+  if (shape.kernel == 3) return launch_tc<W>(ctx, a);
+  return shape.depth == 2 ? launch_wd<W, 2>(ctx, a, hist) : launch_wd<W, 1>(ctx, a, hist);
 }
 
-int launch(bz_ctx* ctx, const RoundArgs& a, bool hist, int depth) {
+int launch(bz_ctx* ctx, const RoundArgs& a, bool hist, const PlanShape& depth) {
   switch (ctx->w32) {
     case 1: return launch_w<1>(ctx, a, hist, depth);
     case 2: return launch_w<2>(ctx, a, hist, depth);
@@ -307,7 +343,7 @@ int run_pass(bz_ctx* ctx, int g, int gamma_only, int lower_prev, int upper,
   if (rc) return rc;
   int ngroups = 0;
   unsigned long long nchunks = 0;
-  const int depth = pass_depth(ctx->engine, g, hist);
+  const PlanShape depth = pass_shape(ctx->engine, g, hist);
   rc = plan_round(ctx, g, gamma_only, depth, &ngroups, &nchunks);
   if (rc) return rc;
   const int m = ctx->m;
@@ -418,6 +454,7 @@ void bz_destroy(bz_ctx* ctx) {
     cudaFree(ctx->d_rows);
     cudaFree(ctx->d_px);
     cudaFree(ctx->d_trip);
+    cudaFree(ctx->d_trip4);
     cudaFree(ctx->d_binom);
     cudaFree(ctx->d_groups);
     cudaFree(ctx->d_bound);
@@ -483,10 +520,13 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
   cudaFree(ctx->d_rows);
   cudaFree(ctx->d_px);
   cudaFree(ctx->d_trip);
+  cudaFree(ctx->d_trip4);
   ctx->d_rows = nullptr;
   ctx->d_px = nullptr;
   ctx->d_trip = nullptr;
+  ctx->d_trip4 = nullptr;
   ctx->trip_rows = 0;
+  ctx->trip4_rows = 0;
   CK(cudaMalloc(&ctx->d_rows, img.size() * 4));
   CK(cudaMalloc(&ctx->d_px, px.size() * 4));
   CK(cudaMemcpy(ctx->d_rows, img.data(), img.size() * 4, cudaMemcpyHostToDevice));
@@ -497,6 +537,12 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
     CK(cudaMalloc(&ctx->d_trip, (size_t)m * rows3 * bz::tc_stride(w32)));
     CK(cudaMemsetAsync(ctx->d_trip, 0, (size_t)m * rows3 * bz::tc_stride(w32), ctx->stream));
     ctx->trip_rows = rows3;
+    const size_t n3 = (size_t)k * (k - 1) * (k - 2) / 6;
+    const size_t rows4 = (n3 + bz::kUmmaN - 1) / bz::kUmmaN * bz::kUmmaN + bz::kUmmaN;
+    const size_t bytes4 = (size_t)m * rows4 * 32 * w32;
+    CK(cudaMalloc(&ctx->d_trip4, bytes4));
+    CK(cudaMemsetAsync(ctx->d_trip4, 0, bytes4, ctx->stream));
+    ctx->trip4_rows = rows4;
   }
   if (m + 1 > ctx->bound_cap) {
     cudaFree(ctx->d_bound);
@@ -575,7 +621,7 @@ int bz_histogram(bz_ctx* ctx, int gamma, int g, int shard, int nshards, uint64_t
 
 int bz_set_engine(bz_ctx* ctx, int engine) {
   if (!ctx) return BZ_ERR_ARGUMENT;
-  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_IMMA)
+  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_UMMA)
     return fail(ctx, BZ_ERR_ARGUMENT, "unknown engine %d", engine);
   ctx->engine = engine;
   return BZ_OK;
@@ -590,8 +636,8 @@ int bz_plan(int m, int k, int g, int engine, int64_t* out, int cap, int* out_ngr
   if (binom_sat(k, g) >= (1ull << 62)) return BZ_ERR_TOO_LARGE;
   std::vector<Group> gs;
   unsigned long long nchunks = 0;
-  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_IMMA) return BZ_ERR_ARGUMENT;
-  int rc = build_plan(nullptr, m, k, g, -1, pass_depth(engine, g, false), gs, &nchunks);
+  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_UMMA) return BZ_ERR_ARGUMENT;
+  int rc = build_plan(nullptr, m, k, g, -1, pass_shape(engine, g, false), gs, &nchunks);
   if (rc) return rc;
   *out_ngroups = (int)gs.size();
   *out_nchunks = nchunks;
@@ -606,8 +652,8 @@ int bz_plan(int m, int k, int g, int engine, int64_t* out, int cap, int* out_ngr
       o[4] = gs[i].ppl;
       o[5] = (int64_t)gs[i].nprefix * (int64_t)binom_sat(k - 1 - gs[i].ell, gs[i].depth);
       o[6] = gs[i].depth;
-      o[7] = gs[i].depth == 3 ? bz::kTcThreads : 32;
-      o[8] = gs[i].depth == 3 ? (int64_t)gs[i].tpc * bz::kTileRows : 0;
+      o[7] = gs[i].lanes;
+      o[8] = gs[i].depth == 3 ? (int64_t)gs[i].tpc * gs[i].tile_rows : 0;
       o[9] = gs[i].ntb;
     }
   }

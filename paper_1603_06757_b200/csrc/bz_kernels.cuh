@@ -47,6 +47,8 @@ struct Group {
   int depth;                       // suffix depth D of the round (1, 2 or 3)
   int tpc;                         // D = 3: suffix tiles per chunk
   int ntb;                         // D = 3: tile blocks per prefix block
+  int lanes;                       // prefixes walked in parallel per chunk
+  int tile_rows;                   // D = 3: triples per suffix tile
 };
 
 struct RoundArgs {

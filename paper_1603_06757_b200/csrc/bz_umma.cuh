@@ -1,0 +1,423 @@
+// bz_umma.cuh -- K4: the round as an integer GEMM on the Blackwell 5th-gen
+// tensor cores (tcgen05.mma kind::i8, accumulators in TMEM).
+//
+// Same algebra as K3 (bz_tc.cuh): w(P ^ S) = w(P) + sum_j (1 - 2 P_j) S_j,
+// prefixes P as +-1 bytes (A, M = 128 rows), triples S as 0/1 bytes (B,
+// N = 256 columns), K = the 32*W padded code columns (W MMAs of K = 32).
+// A (Gamma, ell) group is the GEMM [C(ell,g-4) prefixes] x [C(k-1-ell,3)
+// triples]; D[r][c] + w(P_r) is the weight of codeword (prefix r, triple c)
+// and only its minimum is kept.
+//
+// One CTA per SM (persistent, static chunk striding), warp-specialised:
+//   warps 0-3  producer + epilogue: thread r owns prefix row r of the tile.
+//              It walks its prefixes (colex walker), writes its A row (+-1
+//              bytes, UMMA K-major core-matrix layout) into one of two A
+//              buffers, and later reads its row of the accumulator from TMEM
+//              (tcgen05.ld 32x32b, warp w <-> TMEM lanes 32w..32w+31) and
+//              min-reduces it.
+//   warp 4     TMEM allocator + MMA issuer (one thread): per tile W x
+//              tcgen05.mma into one of two 256-column accumulators, then
+//              tcgen05.commit to the barriers that free the B stage and
+//              publish the accumulator.
+//   warp 5     loader (one thread): 1-D TMA bulk copies (cp.async.bulk) of
+//              contiguous triple-table tiles into a ring of B stages.
+// All synchronisation is mbarrier-based; every role walks the same chunk
+// sequence, so the pipeline counters agree without extra signalling.
+//
+// Triple table (device-built at load time): all C(k,3) row triples in the
+// K3 order (smallest element descending, then lex), stored directly in the
+// UMMA SWIZZLE_NONE K-major canonical layout -- 8-row x 16-byte core
+// matrices, the 2W 16-byte K chunks of an 8-row group contiguous -- so a
+// 256-row tile is one contiguous byte range and the TMA copy lands it in
+// exactly the layout the smem descriptor describes.
+#pragma once
+
+#include "bz_tc.cuh"
+
+namespace bz {
+
+constexpr int kUmmaM = 128;       // prefixes per tile = producer threads
+constexpr int kUmmaN = 256;       // triples per tile
+constexpr int kK4Threads = 192;   // 4 producer/epilogue warps, MMA warp, loader warp
+constexpr int kTmemCols = 512;    // two 256-column s32 accumulators
+
+__host__ __device__ constexpr int umma_tile_bytes_b(int w) { return kUmmaN * 32 * w; }
+__host__ __device__ constexpr int umma_tile_bytes_a(int w) { return kUmmaM * 32 * w; }
+__host__ __device__ constexpr int umma_stages(int w) { return w <= 6 ? 3 : 2; }
+
+// byte offset of (row, 16-byte chunk kc) in a K-major no-swizzle UMMA tile
+__host__ __device__ constexpr uint32_t umma_off(int row, int kc, int w) {
+  return (uint32_t)((row >> 3) * (2 * w * 128) + kc * 128 + (row & 7) * 16);
+}
+
+// tcgen05 shared-memory matrix descriptor, SWIZZLE_NONE, K-major:
+// LBO = distance between the two 16-byte K chunks of one MMA (128 B here),
+// SBO = distance between 8-row core-matrix groups (2W * 128 B).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version 1 (sm_100)
+  return d;                // base offset 0, lbo mode 0, layout SWIZZLE_NONE
+}
+
+// instruction descriptor: D = s32, A = s8, B = s8, both K-major, N, M
+constexpr uint32_t kUmmaIdesc = (2u << 4) | (1u << 7) | (1u << 10) |
+                                ((uint32_t)(kUmmaN >> 3) << 17) |
+                                ((uint32_t)(kUmmaM >> 4) << 24);
+
+// ---- mbarrier / TMA / tcgen05 primitives
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+          bar),
+      "r"(bytes)
+      : "memory");
+}
+// wait for the phase of parity `parity` to complete; traps instead of
+// hanging forever if the pipeline is ever wedged
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (unsigned long long spin = 0;; ++spin) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (spin > (1ull << 26)) __trap();
+  }
+}
+__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld_wait() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Triple table in UMMA layout: one block per (Gamma, a).
+template <int W>
+__global__ void k_build_triples_umma(const uint32_t* __restrict__ rows,
+                                     uint8_t* __restrict__ trip, int k,
+                                     size_t gamma_stride_rows) {
+  constexpr int WP = padded_words(W);
+  const int j = blockIdx.y, a = blockIdx.x;
+  if (a > k - 3) return;
+  const uint32_t* R = rows + (size_t)j * k * WP;
+  const long long base = (long long)(k - 1 - a) * (k - 2 - a) * (k - 3 - a) / 6;
+  const int span = k - 1 - a;
+  const int npairs = span * (span - 1) / 2;
+  uint8_t* out = trip + (size_t)j * gamma_stride_rows * 32 * W;
+  for (int t = threadIdx.x; t < npairs * W; t += blockDim.x) {
+    const int pi = t / W, w = t - pi * W;
+    int b = a + 1, rem = pi;
+    while (rem >= k - 1 - b) { rem -= k - 1 - b; ++b; }
+    const int c = b + 1 + rem;
+    const uint32_t v = R[a * WP + w] ^ R[b * WP + w] ^ R[c * WP + w];
+    const long long row = base + pi;
+    // 32 bytes of word w = K chunks 2w and 2w+1 of this row
+    uint8_t* tile = out + (size_t)(row >> 3) * (2 * W * 128);
+    uint4 lo, hi;
+    lo.x = bit_nibble(v, 0);  lo.y = bit_nibble(v, 4);  lo.z = bit_nibble(v, 8);  lo.w = bit_nibble(v, 12);
+    hi.x = bit_nibble(v, 16); hi.y = bit_nibble(v, 20); hi.z = bit_nibble(v, 24); hi.w = bit_nibble(v, 28);
+    *reinterpret_cast<uint4*>(tile + (2 * w) * 128 + (row & 7) * 16) = lo;
+    *reinterpret_cast<uint4*>(tile + (2 * w + 1) * 128 + (row & 7) * 16) = hi;
+  }
+}
+
+template <int W>
+__host__ __device__ inline size_t k4_smem_bytes(int m, int k, int ngroups) {
+  size_t off = (smem_base_bytes<W>(m, k, ngroups) + 1023) & ~size_t(1023);
+  off += (size_t)umma_stages(W) * umma_tile_bytes_b(W);
+  off += 2 * (size_t)umma_tile_bytes_a(W);
+  off += 16 * 8 + 16;  // barriers + TMEM base
+  return off;
+}
+
+// Decoded chunk: identical on every role.
+struct K4Chunk {
+  Group gr;
+  unsigned long long bfirst;
+  long long maxcnt;
+  int slice, tile_lo, tile_hi;
+};
+
+__device__ __forceinline__ K4Chunk k4_decode(const Group* sg, int ngroups,
+                                             unsigned long long chunk, int k) {
+  K4Chunk c;
+  c.gr = sg[find_group(sg, ngroups, chunk)];
+  const unsigned long long local = chunk - c.gr.chunk_begin;
+  const unsigned long long pb = local / (unsigned long long)c.gr.ntb;
+  const int tb = (int)(local - pb * (unsigned long long)c.gr.ntb);
+  c.bfirst = pb * (unsigned long long)kUmmaM * c.gr.ppl;
+  const unsigned long long bleft = c.gr.nprefix - c.bfirst;
+  c.maxcnt = bleft < (unsigned long long)c.gr.ppl ? (long long)bleft : c.gr.ppl;
+  const long long t = k - 1 - c.gr.ell;
+  c.slice = (int)(t * (t - 1) * (t - 2) / 6);
+  const int ntiles = (c.slice + kUmmaN - 1) / kUmmaN;
+  c.tile_lo = tb * c.gr.tpc;
+  c.tile_hi = min(ntiles, c.tile_lo + c.gr.tpc);
+  return c;
+}
+
+template <int W>
+__global__ void __launch_bounds__(kK4Threads, 1)
+k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_stride_rows) {
+  constexpr int WP = padded_words(W);
+  constexpr int S = umma_stages(W);
+  constexpr uint32_t TB = umma_tile_bytes_b(W);
+  constexpr uint32_t TA = umma_tile_bytes_a(W);
+  extern __shared__ __align__(128) unsigned char smem[];
+  const size_t base = (smem_base_bytes<W>(a.m, a.k, a.ngroups) + 1023) & ~size_t(1023);
+  unsigned char* sB = smem + base;
+  unsigned char* sA = sB + S * TB;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(sA + 2 * TA);
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 16);
+  const uint32_t sB_s = (uint32_t)__cvta_generic_to_shared(sB);
+  const uint32_t sA_s = (uint32_t)__cvta_generic_to_shared(sA);
+  const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
+  // barrier slots: bfull[0..S), bempty[3..3+S), afull 6,7  aempty 8,9
+  //                accfull 10,11  accempty 12,13
+  auto bfull = [&](int i) { return bar_s + 8u * i; };
+  auto bempty = [&](int i) { return bar_s + 8u * (3 + i); };
+  auto afull = [&](int i) { return bar_s + 8u * (6 + i); };
+  auto aempty = [&](int i) { return bar_s + 8u * (8 + i); };
+  auto accfull = [&](int i) { return bar_s + 8u * (10 + i); };
+  auto accempty = [&](int i) { return bar_s + 8u * (12 + i); };
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) { mbar_init(bfull(i), 1); mbar_init(bempty(i), 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(afull(i), kUmmaM);
+      mbar_init(aempty(i), 1);
+      mbar_init(accfull(i), 1);
+      mbar_init(accempty(i), kUmmaM);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_proxy_async();
+  }
+  if (warp == 4) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(s_tmem)),
+                 "r"(kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  uint32_t *srows, *spx;
+  Group* sgroups;
+  tc_fence_before();
+  stage<W>(a, srows, spx, sgroups, smem);  // ends with __syncthreads
+  tc_fence_after();
+  const uint32_t tmem = *s_tmem;
+  const int k = a.k, q = a.g - 4;
+  const unsigned long long my_chunks =
+      a.nchunks > (unsigned long long)a.shard
+          ? (a.nchunks - a.shard + a.nshards - 1) / a.nshards
+          : 0ull;
+
+  if (warp < 4) {
+    // ================= producer + epilogue (thread r <-> prefix row r)
+    const int r = tid;
+    uint32_t step = 0, tcount = 0;
+    for (unsigned long long ci = blockIdx.x; ci < my_chunks; ci += gridDim.x) {
+      const unsigned long long chunk = ci * a.nshards + a.shard;
+      const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
+      const unsigned long long first = c.bfirst + (unsigned long long)r * c.gr.ppl;
+      long long cnt = 0;
+      if (first < c.gr.nprefix) {
+        const unsigned long long left = c.gr.nprefix - first;
+        cnt = left < (unsigned long long)c.gr.ppl ? (long long)left : c.gr.ppl;
+      }
+      const uint32_t* R = srows + c.gr.gamma * k * WP;
+      const uint32_t* PX = spx + c.gr.gamma * (k + 1) * px_stride(W);
+      Walker<W> wk;
+      wk.init(cnt > 0 ? first : c.bfirst, q, c.gr.ell, R, a.binom);
+
+      auto produce = [&](uint32_t st) {
+        const int ab = st & 1;
+        mbar_wait(aempty(ab), ((st >> 1) & 1) ^ 1);
+        unsigned char* dst = sA + ab * TA;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          uint4 lo, hi;
+          const uint32_t v = wk.acc[j];
+          lo.x = pm1_nibble(v, 0);  lo.y = pm1_nibble(v, 4);
+          lo.z = pm1_nibble(v, 8);  lo.w = pm1_nibble(v, 12);
+          hi.x = pm1_nibble(v, 16); hi.y = pm1_nibble(v, 20);
+          hi.z = pm1_nibble(v, 24); hi.w = pm1_nibble(v, 28);
+          *reinterpret_cast<uint4*>(dst + umma_off(r, 2 * j, W)) = lo;
+          *reinterpret_cast<uint4*>(dst + umma_off(r, 2 * j + 1, W)) = hi;
+        }
+        fence_proxy_async();  // generic-proxy writes -> tensor-core reads
+        mbar_arrive(afull(ab));
+      };
+
+      int best = INT_MAX;
+      int wt = 0;
+#pragma unroll
+      for (int j = 0; j < W; ++j) wt += __popc(wk.acc[j]);
+      produce(step);
+      for (long long p = 0; p < c.maxcnt; ++p) {
+        const int wt_cur = wt;
+        if (p + 1 < c.maxcnt) {  // next step's A overlaps this step's MMAs
+          if (p + 1 < cnt) wk.step(PX);
+          wt = 0;
+#pragma unroll
+          for (int j = 0; j < W; ++j) wt += __popc(wk.acc[j]);
+          produce(step + 1);
+        }
+        int rmin = INT_MAX / 2;
+        for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount) {
+          const int buf = tcount & 1;
+          mbar_wait(accfull(buf), (tcount >> 1) & 1);
+          tc_fence_after();
+          const int valid = min(kUmmaN, c.slice - t * kUmmaN);
+          const uint32_t tb = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(buf * kUmmaN);
+#pragma unroll 1
+          for (int cc = 0; cc < kUmmaN / 32; ++cc) {
+            uint32_t v[32];
+            tmem_ld32(tb + 32 * cc, v);
+            tmem_ld_wait();
+            if (32 * cc + 32 <= valid) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 2) rmin = min(rmin, min((int)v[i], (int)v[i + 1]));
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (32 * cc + i < valid) rmin = min(rmin, (int)v[i]);
+            }
+          }
+          tc_fence_before();
+          mbar_arrive(accempty(buf));
+        }
+        best = min(best, rmin + wt_cur);
+        ++step;
+      }
+      // chunk epilogue
+      const unsigned FULL = 0xffffffffu;
+      const int wbest = __reduce_min_sync(FULL, best);
+      const unsigned tot = __reduce_add_sync(FULL, (unsigned)cnt);
+      if (lane == 0) {
+        volatile int* vb = a.bound;
+        if (wbest < vb[1 + c.gr.gamma]) atomicMin(a.bound + 1 + c.gr.gamma, wbest);
+        if (wbest < vb[0]) atomicMin(a.bound, wbest);
+        const long long cols = min((long long)c.tile_hi * kUmmaN, (long long)c.slice) -
+                               (long long)c.tile_lo * kUmmaN;
+        if (tot) atomicAdd(a.combos + c.gr.gamma, (unsigned long long)tot * (unsigned long long)cols);
+      }
+    }
+  } else if (warp == 4) {
+    // ================= MMA issuer
+    if (lane == 0) {
+      uint32_t step = 0, tcount = 0, bcount = 0;
+      for (unsigned long long ci = blockIdx.x; ci < my_chunks; ci += gridDim.x) {
+        const unsigned long long chunk = ci * a.nshards + a.shard;
+        const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
+        for (long long p = 0; p < c.maxcnt; ++p, ++step) {
+          const int ab = step & 1;
+          mbar_wait(afull(ab), (step >> 1) & 1);
+          tc_fence_after();
+          for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount, ++bcount) {
+            const int stg = bcount % S;
+            mbar_wait(bfull(stg), (bcount / S) & 1);
+            const int buf = tcount & 1;
+            mbar_wait(accempty(buf), ((tcount >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t d = tmem + (uint32_t)(buf * kUmmaN);
+#pragma unroll
+            for (int kb = 0; kb < W; ++kb) {
+              const uint64_t ad = umma_desc(sA_s + ab * TA + kb * 256, 128, 2 * W * 128);
+              const uint64_t bd = umma_desc(sB_s + stg * TB + kb * 256, 128, 2 * W * 128);
+              umma_i8(d, ad, bd, kUmmaIdesc, kb > 0 ? 1u : 0u);
+            }
+            umma_commit(bempty(stg));
+            umma_commit(accfull(buf));
+          }
+          umma_commit(aempty(ab));
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ================= loader: TMA bulk copies of triple tiles
+    if (lane == 0) {
+      uint32_t bcount = 0;
+      for (unsigned long long ci = blockIdx.x; ci < my_chunks; ci += gridDim.x) {
+        const unsigned long long chunk = ci * a.nshards + a.shard;
+        const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
+        const uint8_t* tsrc = trip + (size_t)c.gr.gamma * gamma_stride_rows * 32 * W;
+        for (long long p = 0; p < c.maxcnt; ++p) {
+          for (int t = c.tile_lo; t < c.tile_hi; ++t, ++bcount) {
+            const int stg = bcount % S;
+            mbar_wait(bempty(stg), ((bcount / S) & 1) ^ 1);
+            // only the rows this tile needs (8-row granularity); the rest of
+            // the stage keeps stale rows whose columns the epilogue masks
+            const int valid = min(kUmmaN, c.slice - t * kUmmaN);
+            const uint32_t bytes = (uint32_t)((valid + 7) / 8) * (2 * W * 128);
+            mbar_arrive_tx(bfull(stg), bytes);
+            tma_load_1d(sB_s + stg * TB, tsrc + (size_t)t * TB, bytes, bfull(stg));
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 4) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(kTmemCols));
+  }
+}
+
+}  // namespace bz

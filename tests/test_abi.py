@@ -37,7 +37,7 @@ def test_header_symbols_exported():
     assert L.bz_abi_version() == _native.ABI_VERSION
 
 
-@pytest.mark.parametrize("engine", ["auto", "popc"])
+@pytest.mark.parametrize("engine", ["auto", "popc", "imma", "umma"])
 def test_plan_counts(engine):
     for (m, k, g) in [(1, 5, 1), (2, 24, 3), (2, 80, 8), (3, 40, 8), (1, 64, 6), (2, 128, 4)]:
         groups, nchunks = _native.plan(m, k, g, engine)
@@ -48,14 +48,14 @@ def test_plan_counts(engine):
         for gr in groups:
             begin, nprefix, gamma, ell, ppl, combos, depth, lanes, spc, nsb = gr
             assert nsb >= 1 and (depth != 3 or spc * nsb >= comb(k - 1 - ell, 3))
-            assert lanes == (256 if depth == 3 else 32)
-            want = 3 if (engine == "auto" and g >= 4) else (2 if g >= 3 else 1)
+            assert lanes == ({"imma": 256}.get(engine, 128) if depth == 3 else 32)
+            want = 3 if (engine != "popc" and g >= 4) else (2 if g >= 3 else 1)
             assert depth == want
             assert nprefix == (1 if g == 1 else comb(ell, g - 1 - depth))
             assert combos == nprefix * comb(k - 1 - ell, depth)
 
 
-@pytest.mark.parametrize("engine", ["auto", "popc"])
+@pytest.mark.parametrize("engine", ["auto", "popc", "imma"])
 @pytest.mark.parametrize("m,k,g", [(1, 6, 1), (1, 7, 2), (2, 9, 3), (1, 12, 5),
                                    (2, 10, 10), (1, 40, 3), (1, 34, 4), (1, 20, 6)])
 def test_plan_partitions_rank_space(m, k, g, engine):

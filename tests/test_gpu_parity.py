@@ -27,9 +27,10 @@ def ctx():
     return _native.context(0)
 
 
-@pytest.fixture(params=["popc", "imma"])
+@pytest.fixture(params=["popc", "imma", "umma"])
 def engine(request):
-    """Both kernels: K1 (XOR+POPC) and K2 (tensor-pipe IMMA, g >= 4)."""
+    """Every kernel: K1 (XOR+POPC), K3 (legacy IMMA, g >= 4) and K4
+    (tcgen05 + TMEM, g >= 4)."""
     _native.context(0).set_engine(request.param)
     yield request.param
     _native.context(0).set_engine("auto")
