@@ -141,6 +141,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// Ties 32 loaded registers to a point after tcgen05.wait::ld, so no use of
+// them can be scheduled before the wait.
+__device__ __forceinline__ void tmem_regs_after_wait(uint32_t* v) {
+  asm volatile(""
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                 "+r"(v[6]), "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]),
+                 "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15]), "+r"(v[16]), "+r"(v[17]),
+                 "+r"(v[18]), "+r"(v[19]), "+r"(v[20]), "+r"(v[21]), "+r"(v[22]), "+r"(v[23]),
+                 "+r"(v[24]), "+r"(v[25]), "+r"(v[26]), "+r"(v[27]), "+r"(v[28]), "+r"(v[29]),
+                 "+r"(v[30]), "+r"(v[31])
+               :
+               : "memory");
+}
 
 // ---------------------------------------------------------------------------
 // Triple table in UMMA layout: one block per (Gamma, a).
@@ -321,19 +334,31 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
           tc_fence_after();
           const int valid = min(kUmmaN, c.slice - t * kUmmaN);
           const uint32_t tb = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(buf * kUmmaN);
+          // two halves of 128 columns: four loads in flight, one wait, then
+          // a min tree (independent partial minima, no serial chain)
 #pragma unroll 1
-          for (int cc = 0; cc < kUmmaN / 32; ++cc) {
-            uint32_t v[32];
-            tmem_ld32(tb + 32 * cc, v);
+          for (int h = 0; h < kUmmaN / 128; ++h) {
+            uint32_t v[128];
+            tmem_ld32(tb + 128 * h + 0, *reinterpret_cast<uint32_t(*)[32]>(v + 0));
+            tmem_ld32(tb + 128 * h + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
+            tmem_ld32(tb + 128 * h + 64, *reinterpret_cast<uint32_t(*)[32]>(v + 64));
+            tmem_ld32(tb + 128 * h + 96, *reinterpret_cast<uint32_t(*)[32]>(v + 96));
             tmem_ld_wait();
-            if (32 * cc + 32 <= valid) {
+            tmem_regs_after_wait(v + 0);
+            tmem_regs_after_wait(v + 32);
+            tmem_regs_after_wait(v + 64);
+            tmem_regs_after_wait(v + 96);
+            const int lim = valid - 128 * h;  // columns of this half that count
+            if (lim < 128) {
 #pragma unroll
-              for (int i = 0; i < 32; i += 2) rmin = min(rmin, min((int)v[i], (int)v[i + 1]));
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (32 * cc + i < valid) rmin = min(rmin, (int)v[i]);
+              for (int i = 0; i < 128; ++i)
+                if (i >= lim) v[i] = 0x3fffffffu;
             }
+#pragma unroll
+            for (int w2 = 64; w2 >= 1; w2 >>= 1)
+#pragma unroll
+              for (int i = 0; i < w2; ++i) v[i] = (uint32_t)min((int)v[i], (int)v[i + w2]);
+            rmin = min(rmin, (int)v[0]);
           }
           tc_fence_before();
           mbar_arrive(accempty(buf));
