@@ -140,6 +140,12 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
   const unsigned long long total = binom_sat(k, g) * (unsigned long long)(j1 - j0);
   long long lane_target = (long long)(total / (32ull * kChunksTarget));
   lane_target = std::min(kLaneMax, std::max(kLaneMin, lane_target));
+  if (shape.kernel == 4) {
+    // K4: one persistent CTA per SM walks ~16 chunks; a chunk costs a walker
+    // unrank per producer thread, so chunks are large
+    lane_target = (long long)(total / ((unsigned long long)shape.lanes * 148ull * 16ull));
+    lane_target = std::min(1ll << 20, std::max(4096ll, lane_target));
+  }
   for (int j = j0; j < j1; ++j) {
     const int ell_lo = g == 1 ? -1 : g - 1 - depth;
     const int ell_hi = g == 1 ? -1 : k - 1 - depth;
