@@ -38,7 +38,14 @@ namespace bz {
 
 constexpr int kUmmaM = 128;       // prefixes per tile = producer threads
 constexpr int kUmmaN = 256;       // triples per tile
-constexpr int kK4Threads = 192;   // 4 producer/epilogue warps, MMA warp, loader warp
+// warp roles: 0-15 epilogue (TMEM lane quarter = warp % 4, 64-column slice
+// = warp / 4), 16 MMA issuer + TMEM owner, 17 TMA loader, 18-21 producers
+constexpr int kK4EpiWarps = 16;
+constexpr int kK4EpiCols = kUmmaN / (kK4EpiWarps / 4);  // columns per epilogue warp
+constexpr int kK4MmaWarp = 16;
+constexpr int kK4LoadWarp = 17;
+constexpr int kK4ProdWarp0 = 18;
+constexpr int kK4Threads = 32 * 22;
 constexpr int kTmemCols = 512;    // two 256-column s32 accumulators
 
 __host__ __device__ constexpr int umma_tile_bytes_b(int w) { return kUmmaN * 32 * w; }
@@ -191,7 +198,8 @@ __host__ __device__ inline size_t k4_smem_bytes(int m, int k, int ngroups) {
   size_t off = (smem_base_bytes<W>(m, k, ngroups) + 1023) & ~size_t(1023);
   off += (size_t)umma_stages(W) * umma_tile_bytes_b(W);
   off += 2 * (size_t)umma_tile_bytes_a(W);
-  off += 16 * 8 + 16;  // barriers + TMEM base
+  off += 16 * 8 + 16;            // barriers + TMEM base
+  off += 2 * kUmmaM * sizeof(int);  // prefix weights of the two A buffers
   return off;
 }
 
@@ -234,6 +242,7 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   unsigned char* sA = sB + S * TB;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(sA + 2 * TA);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 16);
+  int* s_wt = reinterpret_cast<int*>(s_tmem + 4);  // [2][kUmmaM] prefix weights
   const uint32_t sB_s = (uint32_t)__cvta_generic_to_shared(sB);
   const uint32_t sA_s = (uint32_t)__cvta_generic_to_shared(sA);
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
@@ -250,15 +259,15 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   if (tid == 0) {
     for (int i = 0; i < S; ++i) { mbar_init(bfull(i), 1); mbar_init(bempty(i), 1); }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(afull(i), kUmmaM);
-      mbar_init(aempty(i), 1);
-      mbar_init(accfull(i), 1);
-      mbar_init(accempty(i), kUmmaM);
+      mbar_init(afull(i), kUmmaM);               // every producer thread
+      mbar_init(aempty(i), 1 + kK4EpiWarps);     // MMA commit + each epilogue warp
+      mbar_init(accfull(i), 1);                  // MMA commit
+      mbar_init(accempty(i), kK4EpiWarps);       // each epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async();
   }
-  if (warp == 4) {
+  if (warp == kK4MmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(s_tmem)),
                  "r"(kTmemCols));
@@ -275,11 +284,66 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
       a.nchunks > (unsigned long long)a.shard
           ? (a.nchunks - a.shard + a.nshards - 1) / a.nshards
           : 0ull;
+  const unsigned FULL = 0xffffffffu;
 
-  if (warp < 4) {
-    // ================= producer + epilogue (thread r <-> prefix row r)
-    const int r = tid;
+  if (warp < kK4EpiWarps) {
+    // ================= epilogue: warp e reads TMEM lanes 32(e%4).. (rows),
+    // columns [kK4EpiCols*(e/4), +kK4EpiCols) of each 256-column accumulator
+    const int quarter = warp & 3, slice_id = warp >> 2;
+    const int r = 32 * quarter + lane;
     uint32_t step = 0, tcount = 0;
+    for (unsigned long long ci = blockIdx.x; ci < my_chunks; ci += gridDim.x) {
+      const unsigned long long chunk = ci * a.nshards + a.shard;
+      const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
+      int best = INT_MAX;
+      for (long long p = 0; p < c.maxcnt; ++p, ++step) {
+        const int ab = step & 1;
+        mbar_wait(afull(ab), (step >> 1) & 1);
+        const int wt = s_wt[ab * kUmmaM + r];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(aempty(ab));
+        int rmin = INT_MAX / 2;
+        for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount) {
+          const int buf = tcount & 1;
+          mbar_wait(accfull(buf), (tcount >> 1) & 1);
+          tc_fence_after();
+          const int lim = min(kUmmaN, c.slice - t * kUmmaN) - kK4EpiCols * slice_id;
+          const uint32_t tb = tmem + ((uint32_t)(32 * quarter) << 16) +
+                              (uint32_t)(buf * kUmmaN + kK4EpiCols * slice_id);
+          uint32_t v[kK4EpiCols];
+#pragma unroll
+          for (int cc = 0; cc < kK4EpiCols / 32; ++cc)
+            tmem_ld32(tb + 32 * cc, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * cc));
+          tmem_ld_wait();
+#pragma unroll
+          for (int cc = 0; cc < kK4EpiCols / 32; ++cc) tmem_regs_after_wait(v + 32 * cc);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(accempty(buf));  // accumulator is in registers
+          if (lim < kK4EpiCols) {
+#pragma unroll
+            for (int i = 0; i < kK4EpiCols; ++i)
+              if (i >= lim) v[i] = 0x3fffffffu;
+          }
+#pragma unroll
+          for (int w2 = kK4EpiCols / 2; w2 >= 1; w2 >>= 1)
+#pragma unroll
+            for (int i = 0; i < w2; ++i) v[i] = (uint32_t)min((int)v[i], (int)v[i + w2]);
+          rmin = min(rmin, (int)v[0]);
+        }
+        best = min(best, rmin + wt);
+      }
+      const int wbest = __reduce_min_sync(FULL, best);
+      if (lane == 0) {
+        volatile int* vb = a.bound;
+        if (wbest < vb[1 + c.gr.gamma]) atomicMin(a.bound + 1 + c.gr.gamma, wbest);
+        if (wbest < vb[0]) atomicMin(a.bound, wbest);
+      }
+    }
+  } else if (warp >= kK4ProdWarp0) {
+    // ================= producers: thread r walks prefix row r
+    const int r = tid - 32 * kK4ProdWarp0;
+    uint32_t step = 0;
     for (unsigned long long ci = blockIdx.x; ci < my_chunks; ci += gridDim.x) {
       const unsigned long long chunk = ci * a.nshards + a.shard;
       const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
@@ -292,16 +356,19 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
       const uint32_t* R = srows + c.gr.gamma * k * WP;
       const uint32_t* PX = spx + c.gr.gamma * (k + 1) * px_stride(W);
       Walker<W> wk;
+      // rows without prefixes duplicate the block's first prefix
       wk.init(cnt > 0 ? first : c.bfirst, q, c.gr.ell, R, a.binom);
-
-      auto produce = [&](uint32_t st) {
-        const int ab = st & 1;
-        mbar_wait(aempty(ab), ((st >> 1) & 1) ^ 1);
+      for (long long p = 0; p < c.maxcnt; ++p, ++step) {
+        if (p > 0 && p < cnt) wk.step(PX);
+        const int ab = step & 1;
+        mbar_wait(aempty(ab), ((step >> 1) & 1) ^ 1);
         unsigned char* dst = sA + ab * TA;
+        int wt = 0;
 #pragma unroll
         for (int j = 0; j < W; ++j) {
           uint4 lo, hi;
           const uint32_t v = wk.acc[j];
+          wt += __popc(v);
           lo.x = pm1_nibble(v, 0);  lo.y = pm1_nibble(v, 4);
           lo.z = pm1_nibble(v, 8);  lo.w = pm1_nibble(v, 12);
           hi.x = pm1_nibble(v, 16); hi.y = pm1_nibble(v, 20);
@@ -309,77 +376,19 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
           *reinterpret_cast<uint4*>(dst + umma_off(r, 2 * j, W)) = lo;
           *reinterpret_cast<uint4*>(dst + umma_off(r, 2 * j + 1, W)) = hi;
         }
+        s_wt[ab * kUmmaM + r] = wt;
         fence_proxy_async();  // generic-proxy writes -> tensor-core reads
         mbar_arrive(afull(ab));
-      };
-
-      int best = INT_MAX;
-      int wt = 0;
-#pragma unroll
-      for (int j = 0; j < W; ++j) wt += __popc(wk.acc[j]);
-      produce(step);
-      for (long long p = 0; p < c.maxcnt; ++p) {
-        const int wt_cur = wt;
-        if (p + 1 < c.maxcnt) {  // next step's A overlaps this step's MMAs
-          if (p + 1 < cnt) wk.step(PX);
-          wt = 0;
-#pragma unroll
-          for (int j = 0; j < W; ++j) wt += __popc(wk.acc[j]);
-          produce(step + 1);
-        }
-        int rmin = INT_MAX / 2;
-        for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount) {
-          const int buf = tcount & 1;
-          mbar_wait(accfull(buf), (tcount >> 1) & 1);
-          tc_fence_after();
-          const int valid = min(kUmmaN, c.slice - t * kUmmaN);
-          const uint32_t tb = tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(buf * kUmmaN);
-          // two halves of 128 columns: four loads in flight, one wait, then
-          // a min tree (independent partial minima, no serial chain)
-#pragma unroll 1
-          for (int h = 0; h < kUmmaN / 128; ++h) {
-            uint32_t v[128];
-            tmem_ld32(tb + 128 * h + 0, *reinterpret_cast<uint32_t(*)[32]>(v + 0));
-            tmem_ld32(tb + 128 * h + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-            tmem_ld32(tb + 128 * h + 64, *reinterpret_cast<uint32_t(*)[32]>(v + 64));
-            tmem_ld32(tb + 128 * h + 96, *reinterpret_cast<uint32_t(*)[32]>(v + 96));
-            tmem_ld_wait();
-            tmem_regs_after_wait(v + 0);
-            tmem_regs_after_wait(v + 32);
-            tmem_regs_after_wait(v + 64);
-            tmem_regs_after_wait(v + 96);
-            const int lim = valid - 128 * h;  // columns of this half that count
-            if (lim < 128) {
-#pragma unroll
-              for (int i = 0; i < 128; ++i)
-                if (i >= lim) v[i] = 0x3fffffffu;
-            }
-#pragma unroll
-            for (int w2 = 64; w2 >= 1; w2 >>= 1)
-#pragma unroll
-              for (int i = 0; i < w2; ++i) v[i] = (uint32_t)min((int)v[i], (int)v[i + w2]);
-            rmin = min(rmin, (int)v[0]);
-          }
-          tc_fence_before();
-          mbar_arrive(accempty(buf));
-        }
-        best = min(best, rmin + wt_cur);
-        ++step;
       }
-      // chunk epilogue
-      const unsigned FULL = 0xffffffffu;
-      const int wbest = __reduce_min_sync(FULL, best);
+      // visited combinations of this chunk
       const unsigned tot = __reduce_add_sync(FULL, (unsigned)cnt);
-      if (lane == 0) {
-        volatile int* vb = a.bound;
-        if (wbest < vb[1 + c.gr.gamma]) atomicMin(a.bound + 1 + c.gr.gamma, wbest);
-        if (wbest < vb[0]) atomicMin(a.bound, wbest);
+      if (lane == 0 && tot) {
         const long long cols = min((long long)c.tile_hi * kUmmaN, (long long)c.slice) -
                                (long long)c.tile_lo * kUmmaN;
-        if (tot) atomicAdd(a.combos + c.gr.gamma, (unsigned long long)tot * (unsigned long long)cols);
+        atomicAdd(a.combos + c.gr.gamma, (unsigned long long)tot * (unsigned long long)cols);
       }
     }
-  } else if (warp == 4) {
+  } else if (warp == kK4MmaWarp) {
     // ================= MMA issuer
     if (lane == 0) {
       uint32_t step = 0, tcount = 0, bcount = 0;
@@ -438,7 +447,7 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 4) {
+  if (warp == kK4MmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(kTmemCols));
