@@ -36,21 +36,22 @@
 
 namespace bz {
 
-constexpr int kUmmaM = 128;       // prefixes per tile = producer threads
-constexpr int kUmmaN = 256;       // triples per tile
+constexpr int kUmmaM = 128;       // prefixes per A tile = producer threads
+constexpr int kUmmaN = 128;       // triples per B tile
+constexpr int kUmmaMA = 2;        // A tiles (consecutive prefix steps) per B tile
 // warp roles: 0-15 epilogue (TMEM lane quarter = warp % 4, 64-column slice
 // = warp / 4), 16 MMA issuer + TMEM owner, 17 TMA loader, 18-21 producers
 constexpr int kK4EpiWarps = 16;
-constexpr int kK4EpiCols = kUmmaN / (kK4EpiWarps / 4);  // columns per epilogue warp
+constexpr int kK4EpiCols = kUmmaN / (kK4EpiWarps / 4);  // columns per epilogue warp and A tile
 constexpr int kK4MmaWarp = 16;
 constexpr int kK4LoadWarp = 17;
 constexpr int kK4ProdWarp0 = 18;
 constexpr int kK4Threads = 32 * 22;
-constexpr int kTmemCols = 512;    // two 256-column s32 accumulators
+constexpr int kTmemCols = 512;    // 2 buffers x kUmmaMA accumulators x kUmmaN columns
 
 __host__ __device__ constexpr int umma_tile_bytes_b(int w) { return kUmmaN * 32 * w; }
 __host__ __device__ constexpr int umma_tile_bytes_a(int w) { return kUmmaM * 32 * w; }
-__host__ __device__ constexpr int umma_stages(int w) { return w <= 6 ? 3 : 2; }
+__host__ __device__ constexpr int umma_stages(int w) { return w <= 6 ? 4 : 2; }
 
 // byte offset of (row, 16-byte chunk kc) in a K-major no-swizzle UMMA tile
 __host__ __device__ constexpr uint32_t umma_off(int row, int kc, int w) {
@@ -197,9 +198,9 @@ template <int W>
 __host__ __device__ inline size_t k4_smem_bytes(int m, int k, int ngroups) {
   size_t off = (smem_base_bytes<W>(m, k, ngroups) + 1023) & ~size_t(1023);
   off += (size_t)umma_stages(W) * umma_tile_bytes_b(W);
-  off += 2 * (size_t)umma_tile_bytes_a(W);
+  off += 2 * (size_t)kUmmaMA * umma_tile_bytes_a(W);
   off += 16 * 8 + 16;            // barriers + TMEM base
-  off += 2 * kUmmaM * sizeof(int);  // prefix weights of the two A buffers
+  off += 2 * kUmmaMA * kUmmaM * sizeof(int);  // prefix weights of the A buffers
   return off;
 }
 
@@ -240,20 +241,20 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   const size_t base = (smem_base_bytes<W>(a.m, a.k, a.ngroups) + 1023) & ~size_t(1023);
   unsigned char* sB = smem + base;
   unsigned char* sA = sB + S * TB;
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(sA + 2 * TA);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(sA + 2 * kUmmaMA * TA);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 16);
-  int* s_wt = reinterpret_cast<int*>(s_tmem + 4);  // [2][kUmmaM] prefix weights
+  int* s_wt = reinterpret_cast<int*>(s_tmem + 4);  // [2][kUmmaMA][kUmmaM] prefix weights
   const uint32_t sB_s = (uint32_t)__cvta_generic_to_shared(sB);
   const uint32_t sA_s = (uint32_t)__cvta_generic_to_shared(sA);
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
-  // barrier slots: bfull[0..S), bempty[3..3+S), afull 6,7  aempty 8,9
-  //                accfull 10,11  accempty 12,13
+  // barrier slots: bfull[0..S), bempty[4..4+S), afull 8,9  aempty 10,11
+  //                accfull 12,13  accempty 14,15
   auto bfull = [&](int i) { return bar_s + 8u * i; };
-  auto bempty = [&](int i) { return bar_s + 8u * (3 + i); };
-  auto afull = [&](int i) { return bar_s + 8u * (6 + i); };
-  auto aempty = [&](int i) { return bar_s + 8u * (8 + i); };
-  auto accfull = [&](int i) { return bar_s + 8u * (10 + i); };
-  auto accempty = [&](int i) { return bar_s + 8u * (12 + i); };
+  auto bempty = [&](int i) { return bar_s + 8u * (4 + i); };
+  auto afull = [&](int i) { return bar_s + 8u * (8 + i); };
+  auto aempty = [&](int i) { return bar_s + 8u * (10 + i); };
+  auto accfull = [&](int i) { return bar_s + 8u * (12 + i); };
+  auto accempty = [&](int i) { return bar_s + 8u * (14 + i); };
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -288,50 +289,62 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
 
   if (warp < kK4EpiWarps) {
     // ================= epilogue: warp e reads TMEM lanes 32(e%4).. (rows),
-    // columns [kK4EpiCols*(e/4), +kK4EpiCols) of each 256-column accumulator
+    // columns [kK4EpiCols*(e/4), +kK4EpiCols) of each accumulator
     const int quarter = warp & 3, slice_id = warp >> 2;
     const int r = 32 * quarter + lane;
-    uint32_t step = 0, tcount = 0;
+    uint32_t grp = 0, tcount = 0;
     for (unsigned long long ci = blockIdx.x; ci < my_chunks; ci += gridDim.x) {
       const unsigned long long chunk = ci * a.nshards + a.shard;
       const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
       int best = INT_MAX;
-      for (long long p = 0; p < c.maxcnt; ++p, ++step) {
-        const int ab = step & 1;
-        mbar_wait(afull(ab), (step >> 1) & 1);
-        const int wt = s_wt[ab * kUmmaM + r];
+      for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
+        const int ab = grp & 1;
+        mbar_wait(afull(ab), (grp >> 1) & 1);
+        int wt[kUmmaMA];
+#pragma unroll
+        for (int j = 0; j < kUmmaMA; ++j) wt[j] = s_wt[(ab * kUmmaMA + j) * kUmmaM + r];
         __syncwarp();
         if (lane == 0) mbar_arrive(aempty(ab));
-        int rmin = INT_MAX / 2;
+        int rmin[kUmmaMA];
+#pragma unroll
+        for (int j = 0; j < kUmmaMA; ++j) rmin[j] = INT_MAX / 2;
         for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount) {
           const int buf = tcount & 1;
           mbar_wait(accfull(buf), (tcount >> 1) & 1);
           tc_fence_after();
           const int lim = min(kUmmaN, c.slice - t * kUmmaN) - kK4EpiCols * slice_id;
           const uint32_t tb = tmem + ((uint32_t)(32 * quarter) << 16) +
-                              (uint32_t)(buf * kUmmaN + kK4EpiCols * slice_id);
-          uint32_t v[kK4EpiCols];
+                              (uint32_t)(buf * kUmmaMA * kUmmaN + kK4EpiCols * slice_id);
+          uint32_t v[kUmmaMA][kK4EpiCols];
 #pragma unroll
-          for (int cc = 0; cc < kK4EpiCols / 32; ++cc)
-            tmem_ld32(tb + 32 * cc, *reinterpret_cast<uint32_t(*)[32]>(v + 32 * cc));
+          for (int j = 0; j < kUmmaMA; ++j)
+#pragma unroll
+            for (int cc = 0; cc < kK4EpiCols / 32; ++cc)
+              tmem_ld32(tb + j * kUmmaN + 32 * cc, *reinterpret_cast<uint32_t(*)[32]>(&v[j][32 * cc]));
           tmem_ld_wait();
 #pragma unroll
-          for (int cc = 0; cc < kK4EpiCols / 32; ++cc) tmem_regs_after_wait(v + 32 * cc);
+          for (int j = 0; j < kUmmaMA; ++j)
+#pragma unroll
+            for (int cc = 0; cc < kK4EpiCols / 32; ++cc) tmem_regs_after_wait(&v[j][32 * cc]);
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(accempty(buf));  // accumulator is in registers
-          if (lim < kK4EpiCols) {
+          if (lane == 0) mbar_arrive(accempty(buf));  // accumulators are in registers
 #pragma unroll
-            for (int i = 0; i < kK4EpiCols; ++i)
-              if (i >= lim) v[i] = 0x3fffffffu;
+          for (int j = 0; j < kUmmaMA; ++j) {
+            if (lim < kK4EpiCols) {
+#pragma unroll
+              for (int i = 0; i < kK4EpiCols; ++i)
+                if (i >= lim) v[j][i] = 0x3fffffffu;
+            }
+#pragma unroll
+            for (int w2 = kK4EpiCols / 2; w2 >= 1; w2 >>= 1)
+#pragma unroll
+              for (int i = 0; i < w2; ++i) v[j][i] = (uint32_t)min((int)v[j][i], (int)v[j][i + w2]);
+            rmin[j] = min(rmin[j], (int)v[j][0]);
           }
-#pragma unroll
-          for (int w2 = kK4EpiCols / 2; w2 >= 1; w2 >>= 1)
-#pragma unroll
-            for (int i = 0; i < w2; ++i) v[i] = (uint32_t)min((int)v[i], (int)v[i + w2]);
-          rmin = min(rmin, (int)v[0]);
         }
-        best = min(best, rmin + wt);
+#pragma unroll
+        for (int j = 0; j < kUmmaMA; ++j) best = min(best, rmin[j] + wt[j]);
       }
       const int wbest = __reduce_min_sync(FULL, best);
       if (lane == 0) {
@@ -343,7 +356,7 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   } else if (warp >= kK4ProdWarp0) {
     // ================= producers: thread r walks prefix row r
     const int r = tid - 32 * kK4ProdWarp0;
-    uint32_t step = 0;
+    uint32_t grp = 0;
     for (unsigned long long ci = blockIdx.x; ci < my_chunks; ci += gridDim.x) {
       const unsigned long long chunk = ci * a.nshards + a.shard;
       const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
@@ -358,25 +371,29 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
       Walker<W> wk;
       // rows without prefixes duplicate the block's first prefix
       wk.init(cnt > 0 ? first : c.bfirst, q, c.gr.ell, R, a.binom);
-      for (long long p = 0; p < c.maxcnt; ++p, ++step) {
-        if (p > 0 && p < cnt) wk.step(PX);
-        const int ab = step & 1;
-        mbar_wait(aempty(ab), ((step >> 1) & 1) ^ 1);
-        unsigned char* dst = sA + ab * TA;
-        int wt = 0;
+      for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
+        const int ab = grp & 1;
+        mbar_wait(aempty(ab), ((grp >> 1) & 1) ^ 1);
+#pragma unroll 1
+        for (int j = 0; j < kUmmaMA; ++j) {
+          // step j of the group; past this row's range the last prefix repeats
+          if (p + j > 0 && p + j < cnt) wk.step(PX);
+          unsigned char* dst = sA + (ab * kUmmaMA + j) * TA;
+          int wt = 0;
 #pragma unroll
-        for (int j = 0; j < W; ++j) {
-          uint4 lo, hi;
-          const uint32_t v = wk.acc[j];
-          wt += __popc(v);
-          lo.x = pm1_nibble(v, 0);  lo.y = pm1_nibble(v, 4);
-          lo.z = pm1_nibble(v, 8);  lo.w = pm1_nibble(v, 12);
-          hi.x = pm1_nibble(v, 16); hi.y = pm1_nibble(v, 20);
-          hi.z = pm1_nibble(v, 24); hi.w = pm1_nibble(v, 28);
-          *reinterpret_cast<uint4*>(dst + umma_off(r, 2 * j, W)) = lo;
-          *reinterpret_cast<uint4*>(dst + umma_off(r, 2 * j + 1, W)) = hi;
+          for (int jj = 0; jj < W; ++jj) {
+            uint4 lo, hi;
+            const uint32_t v = wk.acc[jj];
+            wt += __popc(v);
+            lo.x = pm1_nibble(v, 0);  lo.y = pm1_nibble(v, 4);
+            lo.z = pm1_nibble(v, 8);  lo.w = pm1_nibble(v, 12);
+            hi.x = pm1_nibble(v, 16); hi.y = pm1_nibble(v, 20);
+            hi.z = pm1_nibble(v, 24); hi.w = pm1_nibble(v, 28);
+            *reinterpret_cast<uint4*>(dst + umma_off(r, 2 * jj, W)) = lo;
+            *reinterpret_cast<uint4*>(dst + umma_off(r, 2 * jj + 1, W)) = hi;
+          }
+          s_wt[(ab * kUmmaMA + j) * kUmmaM + r] = wt;
         }
-        s_wt[ab * kUmmaM + r] = wt;
         fence_proxy_async();  // generic-proxy writes -> tensor-core reads
         mbar_arrive(afull(ab));
       }
@@ -391,13 +408,13 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   } else if (warp == kK4MmaWarp) {
     // ================= MMA issuer
     if (lane == 0) {
-      uint32_t step = 0, tcount = 0, bcount = 0;
+      uint32_t grp = 0, tcount = 0, bcount = 0;
       for (unsigned long long ci = blockIdx.x; ci < my_chunks; ci += gridDim.x) {
         const unsigned long long chunk = ci * a.nshards + a.shard;
         const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
-        for (long long p = 0; p < c.maxcnt; ++p, ++step) {
-          const int ab = step & 1;
-          mbar_wait(afull(ab), (step >> 1) & 1);
+        for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
+          const int ab = grp & 1;
+          mbar_wait(afull(ab), (grp >> 1) & 1);
           tc_fence_after();
           for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount, ++bcount) {
             const int stg = bcount % S;
@@ -405,12 +422,16 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
             const int buf = tcount & 1;
             mbar_wait(accempty(buf), ((tcount >> 1) & 1) ^ 1);
             tc_fence_after();
-            const uint32_t d = tmem + (uint32_t)(buf * kUmmaN);
 #pragma unroll
-            for (int kb = 0; kb < W; ++kb) {
-              const uint64_t ad = umma_desc(sA_s + ab * TA + kb * 256, 128, 2 * W * 128);
-              const uint64_t bd = umma_desc(sB_s + stg * TB + kb * 256, 128, 2 * W * 128);
-              umma_i8(d, ad, bd, kUmmaIdesc, kb > 0 ? 1u : 0u);
+            for (int j = 0; j < kUmmaMA; ++j) {
+              const uint32_t d = tmem + (uint32_t)((buf * kUmmaMA + j) * kUmmaN);
+#pragma unroll
+              for (int kb = 0; kb < W; ++kb) {
+                const uint64_t ad =
+                    umma_desc(sA_s + (ab * kUmmaMA + j) * TA + kb * 256, 128, 2 * W * 128);
+                const uint64_t bd = umma_desc(sB_s + stg * TB + kb * 256, 128, 2 * W * 128);
+                umma_i8(d, ad, bd, kUmmaIdesc, kb > 0 ? 1u : 0u);
+              }
             }
             umma_commit(bempty(stg));
             umma_commit(accfull(buf));
@@ -428,7 +449,7 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
         const unsigned long long chunk = ci * a.nshards + a.shard;
         const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
         const uint8_t* tsrc = trip + (size_t)c.gr.gamma * gamma_stride_rows * 32 * W;
-        for (long long p = 0; p < c.maxcnt; ++p) {
+        for (long long p = 0; p < c.maxcnt; p += kUmmaMA) {
           for (int t = c.tile_lo; t < c.tile_hi; ++t, ++bcount) {
             const int stg = bcount % S;
             mbar_wait(bempty(stg), ((bcount / S) & 1) ^ 1);
