@@ -156,7 +156,9 @@ int bz_launch_count(bz_ctx *ctx, uint64_t *out);
  * out[6] = codewords/s of a synthetic W-word XOR+POPC+min loop (w_words
  * selects W, 1..8), out[7] = its codewords per clock per SM, out[8] = s8
  * IMMA (mma.sync m16n8k32) multiply-accumulates per second, out[9] = IMMA
- * MACs per clock per SM.  `out` must hold 10 doubles. */
+ * MACs per clock per SM, out[10] = tcgen05.mma kind::i8 (M=128, N=256,
+ * K=32, operands in shared memory, one CTA per SM) MACs per second,
+ * out[11] = its MACs per clock per SM.  `out` must hold 12 doubles. */
 int bz_measure_int_peaks(bz_ctx *ctx, int w_words, double *out);
 
 #ifdef __cplusplus

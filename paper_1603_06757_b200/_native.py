@@ -224,12 +224,12 @@ class Context:
         return int(v[0])
 
     def measure_int_peaks(self, w_words: int) -> dict:
-        out = (c_double * 10)()
+        out = (c_double * 12)()
         check(lib().bz_measure_int_peaks(self.handle, w_words, out), self.handle,
               "bz_measure_int_peaks")
         keys = ("popc_per_s", "lop3_per_s", "sm_mhz", "sm_count", "popc_per_clk_sm",
                 "lop3_per_clk_sm", "codeword_per_s", "codeword_per_clk_sm", "imma_mac_per_s",
-                "imma_mac_per_clk_sm")
+                "imma_mac_per_clk_sm", "umma_mac_per_s", "umma_mac_per_clk_sm")
         return dict(zip(keys, (float(v) for v in out)))
 
 

@@ -753,11 +753,37 @@ int bz_measure_int_peaks(bz_ctx* ctx, int w_words, double* out) {
     *mhz = max_clk / (ms * 1e-3) / 1e6;
     return BZ_OK;
   };
+  // tcgen05 kind::i8 M=128 x N=256 x K=32 from shared memory, one CTA per SM
+  auto run_umma = [&](double* macs_per_s, double* macs_per_clk_sm) -> int {
+    const int iters = 20000;
+    const size_t smem = 128 * 32 + 256 * 32 + 1024;
+    CK(cudaFuncSetAttribute(bz::peak_umma_i8<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+    for (int rep = 0; rep < 2; ++rep) {
+      CK(cudaEventRecord(ctx->ev_a, ctx->stream));
+      bz::peak_umma_i8<256><<<ctx->sm_count, 128, smem, ctx->stream>>>(iters, d_clk);
+      CK(cudaGetLastError());
+      CK(cudaEventRecord(ctx->ev_b, ctx->stream));
+      ctx->launches += 1;
+      CK(cudaEventSynchronize(ctx->ev_b));
+    }
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ctx->ev_a, ctx->ev_b));
+    CK(cudaMemcpy(clk.data(), d_clk, sizeof(long long) * ctx->sm_count, cudaMemcpyDeviceToHost));
+    double max_clk = 0;
+    for (int i = 0; i < ctx->sm_count; ++i) max_clk = std::max(max_clk, (double)clk[i]);
+    const double macs = (double)iters * 128.0 * 256.0 * 32.0 * ctx->sm_count;
+    *macs_per_s = macs / (ms * 1e-3);
+    *macs_per_clk_sm = macs / ((double)ctx->sm_count * max_clk);
+    return BZ_OK;
+  };
+  double umma_s = 0, umma_clk = 0;
   double popc_s, popc_clk, lop_s, lop_clk, cw_s, cw_clk, mma_s, mma_clk, mhz0, mhz1, mhz2, mhz3;
   int rc = run(0, 2048, &popc_s, &popc_clk, &mhz0);
   if (!rc) rc = run(1, 2048, &lop_s, &lop_clk, &mhz1);
   if (!rc) rc = run(2, 16384, &cw_s, &cw_clk, &mhz2);
   if (!rc) rc = run(3, 4096, &mma_s, &mma_clk, &mhz3);
+  if (!rc) rc = run_umma(&umma_s, &umma_clk);
   cudaFree(d_out);
   cudaFree(d_clk);
   if (rc) return rc;
@@ -771,6 +797,8 @@ int bz_measure_int_peaks(bz_ctx* ctx, int w_words, double* out) {
   out[7] = cw_clk;
   out[8] = mma_s;
   out[9] = mma_clk;
+  out[10] = umma_s;
+  out[11] = umma_clk;
   return BZ_OK;
 }
 

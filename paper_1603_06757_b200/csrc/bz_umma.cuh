@@ -475,4 +475,52 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   }
 }
 
+// ---------------------------------------------------------------------------
+// tcgen05 kind::i8 throughput probe (roofline denominator of K4): one CTA per
+// SM issues `iters` back-to-back M=128 x N x K=32 MMAs from shared memory
+// into TMEM (operand contents are irrelevant), then waits for completion.
+template <int N>
+__global__ void __launch_bounds__(128, 1) peak_umma_i8(int iters, long long* clk) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  __shared__ __align__(8) unsigned long long bar;
+  __shared__ uint32_t s_tmem;
+  const int warp = threadIdx.x >> 5;
+  const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(&bar);
+  if (threadIdx.x == 0) {
+    mbar_init(bar_s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_tmem)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem);
+  constexpr uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
+                             ((uint32_t)(128 >> 4) << 24);
+  long long t0 = 0, t1 = 0;
+  if (threadIdx.x == 0) {
+    const uint64_t ad = umma_desc(base, 128, 256);
+    const uint64_t bd = umma_desc(base + 128 * 32, 128, 256);
+    t0 = clock64();
+    for (int i = 0; i < iters; ++i)
+      umma_i8(tmem + (uint32_t)((i & 1) * N), ad, bd, idesc, (i & 2) ? 1u : 0u);
+    umma_commit(bar_s);
+    mbar_wait(bar_s, 0);
+    t1 = clock64();
+    clk[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
 }  // namespace bz
