@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -378,6 +379,12 @@ int run_pass(bz_ctx* ctx, int g, int gamma_only, int lower_prev, int upper,
   a.shard = shard;
   a.nshards = nshards;
   a.lower_prev = lower_prev;
+  {
+    // timing experiments on K4 (results are NOT valid when set): bit 0 skips
+    // the epilogue's TMEM reads, bit 1 the TMA tile loads, bit 2 the MMAs
+    const char* dbg = getenv("BZ_K4_DEBUG");
+    a.debug = dbg ? atoi(dbg) : 0;
+  }
   if (nchunks > 0 && (unsigned long long)shard < nchunks) {
     rc = launch(ctx, a, hist, depth);
     if (rc) return rc;

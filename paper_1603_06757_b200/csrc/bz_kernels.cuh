@@ -65,6 +65,7 @@ struct RoundArgs {
   int m, k, g, n;
   int shard, nshards;
   int lower_prev;              // early exit once bound[0] <= lower_prev
+  int debug;                   // K4 timing experiments only (see BZ_K4_DEBUG)
 };
 
 __host__ __device__ constexpr int padded_words(int w) {

@@ -38,7 +38,7 @@ namespace bz {
 
 constexpr int kUmmaM = 128;       // prefixes per A tile = producer threads
 constexpr int kUmmaN = 128;       // triples per B tile
-constexpr int kUmmaMA = 2;        // A tiles (consecutive prefix steps) per B tile
+constexpr int kUmmaMA = 1;        // A tiles (consecutive prefix steps) per B tile
 // warp roles: 0-15 epilogue (TMEM lane quarter = warp % 4, 64-column slice
 // = warp / 4), 16 MMA issuer + TMEM owner, 17 TMA loader, 18-21 producers
 constexpr int kK4EpiWarps = 16;
@@ -47,7 +47,9 @@ constexpr int kK4MmaWarp = 16;
 constexpr int kK4LoadWarp = 17;
 constexpr int kK4ProdWarp0 = 18;
 constexpr int kK4Threads = 32 * 22;
-constexpr int kTmemCols = 512;    // 2 buffers x kUmmaMA accumulators x kUmmaN columns
+constexpr int kTmemCols = 512;    // kAccBufs buffers x kUmmaMA accumulators x kUmmaN columns
+constexpr int kAccBufs = kTmemCols / (kUmmaMA * kUmmaN);  // accumulator ring depth
+constexpr int kBarSlots = 12 + 2 * kAccBufs;
 
 __host__ __device__ constexpr int umma_tile_bytes_b(int w) { return kUmmaN * 32 * w; }
 __host__ __device__ constexpr int umma_tile_bytes_a(int w) { return kUmmaM * 32 * w; }
@@ -199,7 +201,7 @@ __host__ __device__ inline size_t k4_smem_bytes(int m, int k, int ngroups) {
   size_t off = (smem_base_bytes<W>(m, k, ngroups) + 1023) & ~size_t(1023);
   off += (size_t)umma_stages(W) * umma_tile_bytes_b(W);
   off += 2 * (size_t)kUmmaMA * umma_tile_bytes_a(W);
-  off += 16 * 8 + 16;            // barriers + TMEM base
+  off += kBarSlots * 8 + 16;     // barriers + TMEM base
   off += 2 * kUmmaMA * kUmmaM * sizeof(int);  // prefix weights of the A buffers
   return off;
 }
@@ -242,19 +244,19 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   unsigned char* sB = smem + base;
   unsigned char* sA = sB + S * TB;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(sA + 2 * kUmmaMA * TA);
-  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + 16);
+  uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + kBarSlots);
   int* s_wt = reinterpret_cast<int*>(s_tmem + 4);  // [2][kUmmaMA][kUmmaM] prefix weights
   const uint32_t sB_s = (uint32_t)__cvta_generic_to_shared(sB);
   const uint32_t sA_s = (uint32_t)__cvta_generic_to_shared(sA);
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
   // barrier slots: bfull[0..S), bempty[4..4+S), afull 8,9  aempty 10,11
-  //                accfull 12,13  accempty 14,15
+  //                accfull[12..12+kAccBufs)  accempty[12+kAccBufs..)
   auto bfull = [&](int i) { return bar_s + 8u * i; };
   auto bempty = [&](int i) { return bar_s + 8u * (4 + i); };
   auto afull = [&](int i) { return bar_s + 8u * (8 + i); };
   auto aempty = [&](int i) { return bar_s + 8u * (10 + i); };
   auto accfull = [&](int i) { return bar_s + 8u * (12 + i); };
-  auto accempty = [&](int i) { return bar_s + 8u * (14 + i); };
+  auto accempty = [&](int i) { return bar_s + 8u * (12 + kAccBufs + i); };
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -262,6 +264,8 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
     for (int i = 0; i < 2; ++i) {
       mbar_init(afull(i), kUmmaM);               // every producer thread
       mbar_init(aempty(i), 1 + kK4EpiWarps);     // MMA commit + each epilogue warp
+    }
+    for (int i = 0; i < kAccBufs; ++i) {
       mbar_init(accfull(i), 1);                  // MMA commit
       mbar_init(accempty(i), kK4EpiWarps);       // each epilogue warp
     }
@@ -309,13 +313,18 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
 #pragma unroll
         for (int j = 0; j < kUmmaMA; ++j) rmin[j] = INT_MAX / 2;
         for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount) {
-          const int buf = tcount & 1;
-          mbar_wait(accfull(buf), (tcount >> 1) & 1);
+          const int buf = tcount % kAccBufs;
+          mbar_wait(accfull(buf), (tcount / kAccBufs) & 1);
           tc_fence_after();
           const int lim = min(kUmmaN, c.slice - t * kUmmaN) - kK4EpiCols * slice_id;
           const uint32_t tb = tmem + ((uint32_t)(32 * quarter) << 16) +
                               (uint32_t)(buf * kUmmaMA * kUmmaN + kK4EpiCols * slice_id);
           uint32_t v[kUmmaMA][kK4EpiCols];
+          if (a.debug & 1) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(accempty(buf));
+            continue;
+          }
 #pragma unroll
           for (int j = 0; j < kUmmaMA; ++j)
 #pragma unroll
@@ -408,6 +417,8 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   } else if (warp == kK4MmaWarp) {
     // ================= MMA issuer
     if (lane == 0) {
+      const uint64_t a_desc0 = umma_desc(sA_s, 128, 2 * W * 128);
+      const uint64_t b_desc0 = umma_desc(sB_s, 128, 2 * W * 128);
       uint32_t grp = 0, tcount = 0, bcount = 0;
       for (unsigned long long ci = blockIdx.x; ci < my_chunks; ci += gridDim.x) {
         const unsigned long long chunk = ci * a.nshards + a.shard;
@@ -419,19 +430,20 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
           for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount, ++bcount) {
             const int stg = bcount % S;
             mbar_wait(bfull(stg), (bcount / S) & 1);
-            const int buf = tcount & 1;
-            mbar_wait(accempty(buf), ((tcount >> 1) & 1) ^ 1);
+            const int buf = tcount % kAccBufs;
+            mbar_wait(accempty(buf), ((tcount / kAccBufs) & 1) ^ 1);
             tc_fence_after();
 #pragma unroll
             for (int j = 0; j < kUmmaMA; ++j) {
+              if (a.debug & 4) break;
               const uint32_t d = tmem + (uint32_t)((buf * kUmmaMA + j) * kUmmaN);
+              // K step kb advances both start addresses by 256 B (16 in the
+              // 16-byte-granular address field)
+              const uint64_t ad0 = a_desc0 + (uint64_t)((ab * kUmmaMA + j) * (TA >> 4));
+              const uint64_t bd0 = b_desc0 + (uint64_t)(stg * (TB >> 4));
 #pragma unroll
-              for (int kb = 0; kb < W; ++kb) {
-                const uint64_t ad =
-                    umma_desc(sA_s + (ab * kUmmaMA + j) * TA + kb * 256, 128, 2 * W * 128);
-                const uint64_t bd = umma_desc(sB_s + stg * TB + kb * 256, 128, 2 * W * 128);
-                umma_i8(d, ad, bd, kUmmaIdesc, kb > 0 ? 1u : 0u);
-              }
+              for (int kb = 0; kb < W; ++kb)
+                umma_i8(d, ad0 + 16u * kb, bd0 + 16u * kb, kUmmaIdesc, kb > 0 ? 1u : 0u);
             }
             umma_commit(bempty(stg));
             umma_commit(accfull(buf));
@@ -457,8 +469,12 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
             // the stage keeps stale rows whose columns the epilogue masks
             const int valid = min(kUmmaN, c.slice - t * kUmmaN);
             const uint32_t bytes = (uint32_t)((valid + 7) / 8) * (2 * W * 128);
-            mbar_arrive_tx(bfull(stg), bytes);
-            tma_load_1d(sB_s + stg * TB, tsrc + (size_t)t * TB, bytes, bfull(stg));
+            if (a.debug & 2) {
+              mbar_arrive(bfull(stg));
+            } else {
+              mbar_arrive_tx(bfull(stg), bytes);
+              tma_load_1d(sB_s + stg * TB, tsrc + (size_t)t * TB, bytes, bfull(stg));
+            }
           }
         }
       }
