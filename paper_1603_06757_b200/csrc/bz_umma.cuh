@@ -37,7 +37,7 @@
 namespace bz {
 
 constexpr int kUmmaM = 128;       // prefixes per A tile = producer threads
-constexpr int kUmmaN = 128;       // triples per B tile
+constexpr int kUmmaN = 256;       // triples per B tile
 constexpr int kUmmaMA = 1;        // A tiles (consecutive prefix steps) per B tile
 // warp roles: 0-15 epilogue (TMEM lane quarter = warp % 4, 64-column slice
 // = warp / 4), 16 MMA issuer + TMEM owner, 17 TMA loader, 18-21 producers
@@ -49,11 +49,12 @@ constexpr int kK4ProdWarp0 = 18;
 constexpr int kK4Threads = 32 * 22;
 constexpr int kTmemCols = 512;    // kAccBufs buffers x kUmmaMA accumulators x kUmmaN columns
 constexpr int kAccBufs = kTmemCols / (kUmmaMA * kUmmaN);  // accumulator ring depth
-constexpr int kBarSlots = 12 + 2 * kAccBufs;
+constexpr int kBarSlots = 4 + 3 * kAccBufs;
 
 __host__ __device__ constexpr int umma_tile_bytes_b(int w) { return kUmmaN * 32 * w; }
 __host__ __device__ constexpr int umma_tile_bytes_a(int w) { return kUmmaM * 32 * w; }
-__host__ __device__ constexpr int umma_stages(int w) { return w <= 6 ? 4 : 2; }
+// one ring of kAccBufs slots: B stage s feeds accumulator s (see K4 notes)
+__host__ __device__ constexpr int umma_stages(int) { return kAccBufs; }
 
 // byte offset of (row, 16-byte chunk kc) in a K-major no-swizzle UMMA tile
 __host__ __device__ constexpr uint32_t umma_off(int row, int kc, int w) {
@@ -249,18 +250,23 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   const uint32_t sB_s = (uint32_t)__cvta_generic_to_shared(sB);
   const uint32_t sA_s = (uint32_t)__cvta_generic_to_shared(sA);
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
-  // barrier slots: bfull[0..S), bempty[4..4+S), afull 8,9  aempty 10,11
-  //                accfull[12..12+kAccBufs)  accempty[12+kAccBufs..)
-  auto bfull = [&](int i) { return bar_s + 8u * i; };
-  auto bempty = [&](int i) { return bar_s + 8u * (4 + i); };
-  auto afull = [&](int i) { return bar_s + 8u * (8 + i); };
-  auto aempty = [&](int i) { return bar_s + 8u * (10 + i); };
-  auto accfull = [&](int i) { return bar_s + 8u * (12 + i); };
-  auto accempty = [&](int i) { return bar_s + 8u * (12 + kAccBufs + i); };
+  // One ring of kAccBufs slots: tile t uses B stage and accumulator t % R.
+  //   loader : wait accempty(slot) -> TMA -> bfull(slot)
+  //   MMA    : wait bfull(slot) -> W x tcgen05.mma -> commit accfull(slot)
+  //   epilogue: wait accfull(slot) -> tcgen05.ld -> arrive accempty(slot)
+  // (epilogue done implies MMA done, so the stage is free too): one wait and
+  // one commit per tile on the single MMA-issuing thread.
+  // barrier slots: afull 0,1  aempty 2,3  bfull[4..4+R)  accfull[4+R..)
+  //                accempty[4+2R..)
+  auto afull = [&](int i) { return bar_s + 8u * (0 + i); };
+  auto aempty = [&](int i) { return bar_s + 8u * (2 + i); };
+  auto bfull = [&](int i) { return bar_s + 8u * (4 + i); };
+  auto accfull = [&](int i) { return bar_s + 8u * (4 + kAccBufs + i); };
+  auto accempty = [&](int i) { return bar_s + 8u * (4 + 2 * kAccBufs + i); };
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int i = 0; i < S; ++i) { mbar_init(bfull(i), 1); mbar_init(bempty(i), 1); }
+    for (int i = 0; i < S; ++i) mbar_init(bfull(i), 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(afull(i), kUmmaM);               // every producer thread
       mbar_init(aempty(i), 1 + kK4EpiWarps);     // MMA commit + each epilogue warp
@@ -429,9 +435,8 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
           tc_fence_after();
           for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount, ++bcount) {
             const int stg = bcount % S;
-            mbar_wait(bfull(stg), (bcount / S) & 1);
-            const int buf = tcount % kAccBufs;
-            mbar_wait(accempty(buf), ((tcount / kAccBufs) & 1) ^ 1);
+            const int buf = stg;
+            mbar_wait(bfull(stg), (bcount / S) & 1);  // implies accumulator free
             tc_fence_after();
 #pragma unroll
             for (int j = 0; j < kUmmaMA; ++j) {
@@ -445,7 +450,6 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
               for (int kb = 0; kb < W; ++kb)
                 umma_i8(d, ad0 + 16u * kb, bd0 + 16u * kb, kUmmaIdesc, kb > 0 ? 1u : 0u);
             }
-            umma_commit(bempty(stg));
             umma_commit(accfull(buf));
           }
           umma_commit(aempty(ab));
@@ -464,7 +468,7 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
         for (long long p = 0; p < c.maxcnt; p += kUmmaMA) {
           for (int t = c.tile_lo; t < c.tile_hi; ++t, ++bcount) {
             const int stg = bcount % S;
-            mbar_wait(bempty(stg), ((bcount / S) & 1) ^ 1);
+            mbar_wait(accempty(stg), ((bcount / S) & 1) ^ 1);
             // only the rows this tile needs (8-row granularity); the rest of
             // the stage keeps stale rows whose columns the epilogue masks
             const int valid = min(kUmmaN, c.slice - t * kUmmaN);
