@@ -384,6 +384,15 @@ int run_pass(bz_ctx* ctx, int g, int gamma_only, int lower_prev, int upper,
     // the epilogue's TMEM reads, bit 1 the TMA tile loads, bit 2 the MMAs
     const char* dbg = getenv("BZ_K4_DEBUG");
     a.debug = dbg ? atoi(dbg) : 0;
+    a.trace = nullptr;
+    if (a.debug & 8) {
+      static long long* d_trace = nullptr;
+      if (!d_trace) {
+        CK(cudaMalloc(&d_trace, 8 * 256 * sizeof(long long)));
+      }
+      CK(cudaMemsetAsync(d_trace, 0, 8 * 256 * sizeof(long long), ctx->stream));
+      a.trace = d_trace;
+    }
   }
   if (nchunks > 0 && (unsigned long long)shard < nchunks) {
     rc = launch(ctx, a, hist, depth);
@@ -401,6 +410,15 @@ int run_pass(bz_ctx* ctx, int g, int gamma_only, int lower_prev, int upper,
                        cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaEventElapsedTime(&ctx->last_kernel_ms, ctx->ev_k0, ctx->ev_k1));
+  if (a.trace) {
+    std::vector<long long> h(8 * 256);
+    CK(cudaMemcpy(h.data(), a.trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+    const long long t0 = h[0];
+    fprintf(stderr, "tile loader_go mma_go epi_go epi_released commit\n");
+    for (int t = 0; t < 48; ++t)
+      fprintf(stderr, "%3d %8lld %8lld %8lld %8lld %8lld\n", t, h[t] - t0, h[256 + t] - t0,
+              h[512 + t] - t0, h[768 + t] - t0, h[1024 + t] - t0);
+  }
   return BZ_OK;
 }
 

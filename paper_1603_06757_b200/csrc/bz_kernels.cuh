@@ -66,6 +66,7 @@ struct RoundArgs {
   int shard, nshards;
   int lower_prev;              // early exit once bound[0] <= lower_prev
   int debug;                   // K4 timing experiments only (see BZ_K4_DEBUG)
+  long long* trace;            // K4 debug timeline (BZ_K4_DEBUG & 8), else null
 };
 
 __host__ __device__ constexpr int padded_words(int w) {

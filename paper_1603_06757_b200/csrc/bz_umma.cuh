@@ -49,12 +49,14 @@ constexpr int kK4ProdWarp0 = 18;
 constexpr int kK4Threads = 32 * 22;
 constexpr int kTmemCols = 512;    // kAccBufs buffers x kUmmaMA accumulators x kUmmaN columns
 constexpr int kAccBufs = kTmemCols / (kUmmaMA * kUmmaN);  // accumulator ring depth
-constexpr int kBarSlots = 4 + 3 * kAccBufs;
+constexpr int kMaxStages = 4;
+constexpr int kBarSlots = 4 + 2 * kMaxStages + 2 * kAccBufs;
+constexpr int kTmaPieces = 4;     // parallel bulk copies per B tile
 
 __host__ __device__ constexpr int umma_tile_bytes_b(int w) { return kUmmaN * 32 * w; }
 __host__ __device__ constexpr int umma_tile_bytes_a(int w) { return kUmmaM * 32 * w; }
-// one ring of kAccBufs slots: B stage s feeds accumulator s (see K4 notes)
-__host__ __device__ constexpr int umma_stages(int) { return kAccBufs; }
+// B-tile ring depth (shared memory: S x 8 KB x W plus 2 A tiles)
+__host__ __device__ constexpr int umma_stages(int w) { return w <= 5 ? 4 : (w <= 6 ? 3 : 2); }
 
 // byte offset of (row, 16-byte chunk kc) in a K-major no-swizzle UMMA tile
 __host__ __device__ constexpr uint32_t umma_off(int row, int kc, int w) {
@@ -250,23 +252,20 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   const uint32_t sB_s = (uint32_t)__cvta_generic_to_shared(sB);
   const uint32_t sA_s = (uint32_t)__cvta_generic_to_shared(sA);
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
-  // One ring of kAccBufs slots: tile t uses B stage and accumulator t % R.
-  //   loader : wait accempty(slot) -> TMA -> bfull(slot)
-  //   MMA    : wait bfull(slot) -> W x tcgen05.mma -> commit accfull(slot)
-  //   epilogue: wait accfull(slot) -> tcgen05.ld -> arrive accempty(slot)
-  // (epilogue done implies MMA done, so the stage is free too): one wait and
-  // one commit per tile on the single MMA-issuing thread.
-  // barrier slots: afull 0,1  aempty 2,3  bfull[4..4+R)  accfull[4+R..)
-  //                accempty[4+2R..)
+  // Rings: B stages (loader -> MMA: bfull; MMA commit -> loader: bempty),
+  // accumulators (MMA commit -> epilogue: accfull; epilogue -> MMA:
+  // accempty), A buffers (producers -> MMA, epilogue: afull; MMA commit +
+  // epilogue -> producers: aempty).
   auto afull = [&](int i) { return bar_s + 8u * (0 + i); };
   auto aempty = [&](int i) { return bar_s + 8u * (2 + i); };
   auto bfull = [&](int i) { return bar_s + 8u * (4 + i); };
-  auto accfull = [&](int i) { return bar_s + 8u * (4 + kAccBufs + i); };
-  auto accempty = [&](int i) { return bar_s + 8u * (4 + 2 * kAccBufs + i); };
+  auto bempty = [&](int i) { return bar_s + 8u * (4 + kMaxStages + i); };
+  auto accfull = [&](int i) { return bar_s + 8u * (4 + 2 * kMaxStages + i); };
+  auto accempty = [&](int i) { return bar_s + 8u * (4 + 2 * kMaxStages + kAccBufs + i); };
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
-    for (int i = 0; i < S; ++i) mbar_init(bfull(i), 1);
+    for (int i = 0; i < S; ++i) { mbar_init(bfull(i), 1); mbar_init(bempty(i), 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(afull(i), kUmmaM);               // every producer thread
       mbar_init(aempty(i), 1 + kK4EpiWarps);     // MMA commit + each epilogue warp
@@ -322,6 +321,8 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
           const int buf = tcount % kAccBufs;
           mbar_wait(accfull(buf), (tcount / kAccBufs) & 1);
           tc_fence_after();
+          if (a.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && tcount < 256)
+            a.trace[2 * 256 + tcount] = clock64();
           const int lim = min(kUmmaN, c.slice - t * kUmmaN) - kK4EpiCols * slice_id;
           const uint32_t tb = tmem + ((uint32_t)(32 * quarter) << 16) +
                               (uint32_t)(buf * kUmmaMA * kUmmaN + kK4EpiCols * slice_id);
@@ -422,39 +423,63 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
     }
   } else if (warp == kK4MmaWarp) {
     // ================= MMA issuer
+    // tcgen05.mma issue blocks while the tensor pipe is busy, so the waits
+    // for tile t+1 are placed *before* the last MMA of tile t: the pipe then
+    // still holds queued work while this thread does its barrier handshakes.
     if (lane == 0) {
       const uint64_t a_desc0 = umma_desc(sA_s, 128, 2 * W * 128);
       const uint64_t b_desc0 = umma_desc(sB_s, 128, 2 * W * 128);
       uint32_t grp = 0, tcount = 0, bcount = 0;
+      // the held-back last MMA of the previous tile and its commits
+      bool pend = false;
+      uint32_t pd = 0, pstg = 0, pbuf = 0, pab = 0;
+      uint64_t pad = 0, pbd = 0;
+      bool pend_group_end = false;
+      auto flush = [&]() {
+        if (!pend) return;
+        if (!(a.debug & 4)) umma_i8(pd, pad, pbd, kUmmaIdesc, W > 1 ? 1u : 0u);
+        umma_commit(bempty(pstg));
+        umma_commit(accfull(pbuf));
+        if (pend_group_end) umma_commit(aempty(pab));
+        pend = false;
+      };
       for (unsigned long long ci = blockIdx.x; ci < my_chunks; ci += gridDim.x) {
         const unsigned long long chunk = ci * a.nshards + a.shard;
         const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
         for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
           const int ab = grp & 1;
           mbar_wait(afull(ab), (grp >> 1) & 1);
-          tc_fence_after();
           for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount, ++bcount) {
             const int stg = bcount % S;
-            const int buf = stg;
-            mbar_wait(bfull(stg), (bcount / S) & 1);  // implies accumulator free
+            const int buf = tcount % kAccBufs;
+            mbar_wait(accempty(buf), ((tcount / kAccBufs) & 1) ^ 1);
+            mbar_wait(bfull(stg), (bcount / S) & 1);
             tc_fence_after();
+            flush();  // previous tile's last MMA + commits
+            if (a.trace && blockIdx.x == 0 && tcount < 256) a.trace[1 * 256 + tcount] = clock64();
+            const uint32_t d = tmem + (uint32_t)(buf * kUmmaN);
+            // K step kb advances both start addresses by 256 B (16 in the
+            // 16-byte-granular address field)
+            const uint64_t ad0 = a_desc0 + (uint64_t)(ab * (TA >> 4));
+            const uint64_t bd0 = b_desc0 + (uint64_t)(stg * (TB >> 4));
+            if (!(a.debug & 4)) {
 #pragma unroll
-            for (int j = 0; j < kUmmaMA; ++j) {
-              if (a.debug & 4) break;
-              const uint32_t d = tmem + (uint32_t)((buf * kUmmaMA + j) * kUmmaN);
-              // K step kb advances both start addresses by 256 B (16 in the
-              // 16-byte-granular address field)
-              const uint64_t ad0 = a_desc0 + (uint64_t)((ab * kUmmaMA + j) * (TA >> 4));
-              const uint64_t bd0 = b_desc0 + (uint64_t)(stg * (TB >> 4));
-#pragma unroll
-              for (int kb = 0; kb < W; ++kb)
+              for (int kb = 0; kb + 1 < W; ++kb)
                 umma_i8(d, ad0 + 16u * kb, bd0 + 16u * kb, kUmmaIdesc, kb > 0 ? 1u : 0u);
             }
-            umma_commit(accfull(buf));
+            pend = true;
+            pd = d;
+            pad = ad0 + 16u * (W - 1);
+            pbd = bd0 + 16u * (W - 1);
+            pstg = stg;
+            pbuf = buf;
+            pab = ab;
+            pend_group_end = (t + 1 == c.tile_hi);
+            if (a.trace && blockIdx.x == 0 && tcount < 256) a.trace[4 * 256 + tcount] = clock64();
           }
-          umma_commit(aempty(ab));
         }
       }
+      flush();
     }
     __syncwarp();
   } else {
@@ -468,7 +493,8 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
         for (long long p = 0; p < c.maxcnt; p += kUmmaMA) {
           for (int t = c.tile_lo; t < c.tile_hi; ++t, ++bcount) {
             const int stg = bcount % S;
-            mbar_wait(accempty(stg), ((bcount / S) & 1) ^ 1);
+            mbar_wait(bempty(stg), ((bcount / S) & 1) ^ 1);
+            if (a.trace && blockIdx.x == 0 && bcount < 256) a.trace[0 * 256 + bcount] = clock64();
             // only the rows this tile needs (8-row granularity); the rest of
             // the stage keeps stale rows whose columns the epilogue masks
             const int valid = min(kUmmaN, c.slice - t * kUmmaN);
@@ -477,7 +503,16 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
               mbar_arrive(bfull(stg));
             } else {
               mbar_arrive_tx(bfull(stg), bytes);
-              tma_load_1d(sB_s + stg * TB, tsrc + (size_t)t * TB, bytes, bfull(stg));
+              // a few bulk copies in flight per tile (one per 8-row groups
+              // slice) keep more of the L2->SMEM path busy
+              const uint32_t groups8 = (uint32_t)((valid + 7) / 8);
+              const uint32_t per = (groups8 + kTmaPieces - 1) / kTmaPieces;
+              for (uint32_t g0 = 0; g0 < groups8; g0 += per) {
+                const uint32_t gn = min(per, groups8 - g0);
+                const uint32_t off = g0 * (2 * W * 128);
+                tma_load_1d(sB_s + stg * TB + off, tsrc + (size_t)t * TB + off,
+                            gn * (2 * W * 128), bfull(stg));
+              }
             }
           }
         }
