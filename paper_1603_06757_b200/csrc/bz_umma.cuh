@@ -151,6 +151,25 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
 }
+// 32 columns of s32 accumulators as 16 registers of two s16 each (the low
+// halves of adjacent columns; |values| <= 256 so nothing is lost)
+__device__ __forceinline__ void tmem_ld16p(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
+      "%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_regs16_after_wait(uint32_t* v) {
+  asm volatile(""
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                 "+r"(v[6]), "+r"(v[7]), "+r"(v[8]), "+r"(v[9]), "+r"(v[10]), "+r"(v[11]),
+                 "+r"(v[12]), "+r"(v[13]), "+r"(v[14]), "+r"(v[15])
+               :
+               : "memory");
+}
 __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -326,38 +345,38 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
           const int lim = min(kUmmaN, c.slice - t * kUmmaN) - kK4EpiCols * slice_id;
           const uint32_t tb = tmem + ((uint32_t)(32 * quarter) << 16) +
                               (uint32_t)(buf * kUmmaMA * kUmmaN + kK4EpiCols * slice_id);
-          uint32_t v[kUmmaMA][kK4EpiCols];
+          // kK4EpiCols columns as packed s16 pairs: 3-input SIMD minima
+          constexpr int NP = kK4EpiCols / 2;
+          uint32_t v[NP];
           if (a.debug & 1) {
             __syncwarp();
             if (lane == 0) mbar_arrive(accempty(buf));
             continue;
           }
 #pragma unroll
-          for (int j = 0; j < kUmmaMA; ++j)
-#pragma unroll
-            for (int cc = 0; cc < kK4EpiCols / 32; ++cc)
-              tmem_ld32(tb + j * kUmmaN + 32 * cc, *reinterpret_cast<uint32_t(*)[32]>(&v[j][32 * cc]));
+          for (int cc = 0; cc < kK4EpiCols / 32; ++cc) tmem_ld16p(tb + 32 * cc, v + 16 * cc);
           tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < kUmmaMA; ++j)
-#pragma unroll
-            for (int cc = 0; cc < kK4EpiCols / 32; ++cc) tmem_regs_after_wait(&v[j][32 * cc]);
+          for (int cc = 0; cc < kK4EpiCols / 32; ++cc) tmem_regs16_after_wait(v + 16 * cc);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(accempty(buf));  // accumulators are in registers
+          if (a.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && tcount < 256)
+            a.trace[3 * 256 + tcount] = clock64();
+          if (lim < kK4EpiCols) {
 #pragma unroll
-          for (int j = 0; j < kUmmaMA; ++j) {
-            if (lim < kK4EpiCols) {
-#pragma unroll
-              for (int i = 0; i < kK4EpiCols; ++i)
-                if (i >= lim) v[j][i] = 0x3fffffffu;
+            for (int i = 0; i < NP; ++i) {
+              if (2 * i >= lim) v[i] |= 0x00007fffu, v[i] &= 0xffff7fffu;
+              if (2 * i + 1 >= lim) v[i] = (v[i] & 0x0000ffffu) | 0x7fff0000u;
             }
-#pragma unroll
-            for (int w2 = kK4EpiCols / 2; w2 >= 1; w2 >>= 1)
-#pragma unroll
-              for (int i = 0; i < w2; ++i) v[j][i] = (uint32_t)min((int)v[j][i], (int)v[j][i + w2]);
-            rmin[j] = min(rmin[j], (int)v[j][0]);
           }
+          // 32 -> 11 -> 4 -> 2 -> 1 packed registers
+          uint32_t m = __vimin3_s16x2(v[0], v[1], v[2]);
+#pragma unroll
+          for (int i = 3; i + 1 < NP; i += 2) m = __vimin3_s16x2(m, v[i], v[i + 1]);
+          if (NP % 2 == 0) m = __vmins2(m, v[NP - 1]);
+          const int lo = (int)(short)(m & 0xffffu), hi = (int)(short)(m >> 16);
+          rmin[0] = min(rmin[0], min(lo, hi));
         }
 #pragma unroll
         for (int j = 0; j < kUmmaMA; ++j) best = min(best, rmin[j] + wt[j]);
