@@ -305,149 +305,6 @@ def main():
         with open(prof) as fh:
             traffic = json.load(fh).get("dram_bytes_per_launch")
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": WORKLOAD if args.config == "cfg5" else args.config,
-                   "sample": f"rounds g<={sample_max_g} per step"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"oracle/bz_oracle.c BZ rounds g<={sample_max_g} of "
-                                   f"{args.config} ({rep['combinations']} combinations/step)"},
-        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
-
-
-def main():
-    args = parse()
-    if args.impl == "reference":
-        reference_arm(args)
-        return
-
-    rank, world, local = dist_env()
-    import torch
-
-    distributed = world > 1
-    if distributed:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_1603_06757_b200 import EngineConfig, _native, engine, minimum_distance
-    from paper_1603_06757_b200.configs import code
-    from paper_1603_06757_b200.enumeration import family_words
-
-    G, gs, _ = code(args.config, args.seed)
-    k, n, m = G.num_rows, G.num_cols, gs.matrix_count
-    w32 = -(-n // 32)
-    cfg = EngineConfig(device=local, distributed=distributed)
-    comm = engine._make_comm(cfg)
-    backend = engine.make_backend(cfg, comm)
-    backend.load(gs, n)
-    ctx = backend.ctx
-
-    def barrier():
-        if distributed:
-            comm.barrier()
-        torch.cuda.synchronize(local)
-
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
-
-    def step():
-        st = engine.start_state(gs, n, k, cfg)
-        engine.run_rounds(backend, gs, k, cfg, st)
-        return st
-
-    # warm-up
-    for _ in range(max(args.warmup, 3)):
-        st = step()
-    ref_trace = st.trace
-
-    # ---- value: device-resident rounds, CUDA events on the library stream
-    launches0 = ctx.launch_count()
-    dev_ms, combos_total, g_top_ms, g_top_combos = 0.0, 0, [], 0
-    with ClockSampler(local) as clocks:
-        for _ in range(args.steps):
-            flush.zero_()
-            barrier()
-            ctx.timer_start()
-            st = step()
-            dev_ms += ctx.timer_stop()
-            combos_total += st.counters.combinations
-            top = max(st.rounds, key=lambda r: r.combinations)
-            g_top_ms.append(top.kernel_ms)
-            g_top_combos = top.combinations
-            assert st.trace == ref_trace
-    launches = ctx.launch_count() - launches0
-    clock = clocks.summary()
-
-    # max over ranks of the time; the counters are already whole-job sums
-    # (every round's all-gather adds the shards' combination counts)
-    dev_ms_max = dev_ms
-    if distributed:
-        import torch.distributed as dist
-
-        t_max = torch.tensor([dev_ms], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-        dev_ms_max = float(t_max.item())
-    combos_all = float(combos_total)
-    value = combos_all / (dev_ms_max * 1e-3)
-
-    # ---- e2e: public API from a host matrix
-    e2e_times = []
-    for _ in range(args.steps):
-        barrier()
-        t0 = time.perf_counter()
-        rep = minimum_distance(G, cfg)
-        barrier()
-        e2e_times.append(time.perf_counter() - t0)
-        assert rep.bounds_trace == ref_trace
-    e2e_s = statistics.median(e2e_times)
-    if distributed:
-        import torch.distributed as dist
-
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e_value = rep.counters.combinations / e2e_s
-    wp = 1 if w32 <= 1 else 2 if w32 <= 2 else 4 if w32 <= 4 else 8
-    h2d = m * k * wp * 4 + m * (k + 1) * wp * 4  # padded rows + prefix-XOR table
-    d2h = 0
-    for (g, L, U) in rep.bounds_trace:
-        groups, _ = _native.plan(m, k, g)
-        h2d += len(groups) * 32 + (m + 1) * 4  # work plan + bound init
-        d2h += (m + 1) * 4 + m * 8             # minima + counters
-
-    if rank != 0:
-        if distributed:
-            import torch.distributed as dist
-
-            dist.destroy_process_group()
-        return
-
-    # ---- roofline of the dominant kernel (largest round)
-    peaks = ctx.measure_int_peaks(w32)
-    top_ms = statistics.median(g_top_ms)
-    achieved = (g_top_combos / world) / (top_ms * 1e-3)
-    macs_per_combo = 32 * w32  # K of the weight GEMM: the full codeword
-    tensor_peak = peaks["imma_mac_per_s"] / macs_per_combo
-    popc_peak = peaks["popc_per_s"] / w32
-    g_top = max(st.rounds, key=lambda r: r.combinations).g
-    # the XOR+POPC kernel K1 on the same launch, for the integer roofline
-    ctx.set_engine("popc")
-    k1_ms = []
-    for _ in range(2):
-        ctx.round(g_top, 0, 1 << 30, local, world)
-        k1_ms.append(ctx.last_kernel_ms())
-    ctx.set_engine(cfg.engine)
-    k1_achieved = (g_top_combos / world) / (min(k1_ms) * 1e-3)
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
-    if os.path.exists(prof):
-        with open(prof) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
-    line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
