@@ -43,6 +43,9 @@ struct bz_ctx {
   size_t trip_rows = 0;         // rows per Gamma (C(k,3) + one tile of padding)
   uint8_t* d_trip4 = nullptr;   // K4 triple tables (UMMA core-matrix layout)
   size_t trip4_rows = 0;        // rows per Gamma (C(k,3) rounded up to a tile, + a tile)
+  // grow-only capacities (bytes) so repeated loads do not reallocate
+  size_t rows_cap = 0, px_cap = 0, trip_cap = 0, trip4_cap = 0;
+  bool trip_built = false, trip4_built = false;  // tables are built on first use
   uint32_t* d_px = nullptr;     // m*(k+1)*wp
   unsigned long long* d_binom = nullptr;
   // per-round scratch
@@ -97,6 +100,17 @@ unsigned long long binom_sat(int p, int q) {
     if (r > (unsigned __int128)~0ull) return ~0ull;
   }
   return (unsigned long long)r;
+}
+
+// grow-only device buffer
+cudaError_t grow(bz_ctx*, void** p, size_t* cap, size_t bytes) {
+  if (bytes <= *cap && *p) return cudaSuccess;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  cudaError_t e = cudaMalloc(p, std::max<size_t>(bytes, 256));
+  if (e == cudaSuccess) *cap = std::max<size_t>(bytes, 256);
+  return e;
 }
 
 int ensure_round_buffers(bz_ctx* ctx, int ngroups) {
@@ -294,30 +308,49 @@ int launch_umma(bz_ctx* ctx, const RoundArgs& a) {
 }
 
 template <int W>
-int build_triples_w(bz_ctx* ctx) {
+int build_triples_w(bz_ctx* ctx, int which) {
   dim3 grid(ctx->k, ctx->m);
-  bz::k_build_triples<W><<<grid, 256, 0, ctx->stream>>>(ctx->d_rows, ctx->d_trip, ctx->k,
-                                                        ctx->trip_rows);
+  if (which == 3) {
+    bz::k_build_triples<W><<<grid, 256, 0, ctx->stream>>>(ctx->d_rows, ctx->d_trip, ctx->k,
+                                                          ctx->trip_rows);
+  } else {
+    bz::k_build_triples_umma<W><<<grid, 256, 0, ctx->stream>>>(ctx->d_rows, ctx->d_trip4,
+                                                               ctx->k, ctx->trip4_rows);
+  }
   CK(cudaGetLastError());
-  bz::k_build_triples_umma<W><<<grid, 256, 0, ctx->stream>>>(ctx->d_rows, ctx->d_trip4, ctx->k,
-                                                             ctx->trip4_rows);
-  CK(cudaGetLastError());
-  ctx->launches += 2;
+  ctx->launches += 1;
   return BZ_OK;
 }
 
-int build_triples(bz_ctx* ctx) {
+// Build (once per loaded family) the triple table kernel `which` (3: K3
+// layout, 4: K4 UMMA layout) reads.  Tables are not zero-filled: padding rows
+// are only ever read into columns the kernels mask.
+int ensure_triples(bz_ctx* ctx, int which) {
+  bool& built = which == 3 ? ctx->trip_built : ctx->trip4_built;
+  if (built) return BZ_OK;
+  if (ctx->k < 4) return fail(ctx, BZ_ERR_STATE, "triple tables need k >= 4");
+  const size_t bytes = which == 3
+                           ? (size_t)ctx->m * ctx->trip_rows * bz::tc_stride(ctx->w32)
+                           : (size_t)ctx->m * ctx->trip4_rows * 32 * ctx->w32;
+  if (which == 3)
+    CK(grow(ctx, (void**)&ctx->d_trip, &ctx->trip_cap, bytes));
+  else
+    CK(grow(ctx, (void**)&ctx->d_trip4, &ctx->trip4_cap, bytes));
+  int rc;
   switch (ctx->w32) {
-    case 1: return build_triples_w<1>(ctx);
-    case 2: return build_triples_w<2>(ctx);
-    case 3: return build_triples_w<3>(ctx);
-    case 4: return build_triples_w<4>(ctx);
-    case 5: return build_triples_w<5>(ctx);
-    case 6: return build_triples_w<6>(ctx);
-    case 7: return build_triples_w<7>(ctx);
-    case 8: return build_triples_w<8>(ctx);
+    case 1: rc = build_triples_w<1>(ctx, which); break;
+    case 2: rc = build_triples_w<2>(ctx, which); break;
+    case 3: rc = build_triples_w<3>(ctx, which); break;
+    case 4: rc = build_triples_w<4>(ctx, which); break;
+    case 5: rc = build_triples_w<5>(ctx, which); break;
+    case 6: rc = build_triples_w<6>(ctx, which); break;
+    case 7: rc = build_triples_w<7>(ctx, which); break;
+    case 8: rc = build_triples_w<8>(ctx, which); break;
     default: return fail(ctx, BZ_ERR_TOO_LARGE, "unsupported word count %d", ctx->w32);
   }
+  if (rc) return rc;
+  built = true;
+  return BZ_OK;
 }
 
 template <int W>
@@ -351,6 +384,10 @@ int run_pass(bz_ctx* ctx, int g, int gamma_only, int lower_prev, int upper,
   int ngroups = 0;
   unsigned long long nchunks = 0;
   const PlanShape depth = pass_shape(ctx->engine, g, hist);
+  if (depth.kernel == 3 || depth.kernel == 4) {
+    rc = ensure_triples(ctx, depth.kernel);
+    if (rc) return rc;
+  }
   rc = plan_round(ctx, g, gamma_only, depth, &ngroups, &nchunks);
   if (rc) return rc;
   const int m = ctx->m;
@@ -548,32 +585,21 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
         px[((size_t)j * (k + 1) + r + 1) * wp + w] =
             px[((size_t)j * (k + 1) + r) * wp + w] ^ img[((size_t)j * k + r) * wp + w];
   }
-  cudaFree(ctx->d_rows);
-  cudaFree(ctx->d_px);
-  cudaFree(ctx->d_trip);
-  cudaFree(ctx->d_trip4);
-  ctx->d_rows = nullptr;
-  ctx->d_px = nullptr;
-  ctx->d_trip = nullptr;
-  ctx->d_trip4 = nullptr;
-  ctx->trip_rows = 0;
-  ctx->trip4_rows = 0;
-  CK(cudaMalloc(&ctx->d_rows, img.size() * 4));
-  CK(cudaMalloc(&ctx->d_px, px.size() * 4));
-  CK(cudaMemcpy(ctx->d_rows, img.data(), img.size() * 4, cudaMemcpyHostToDevice));
-  CK(cudaMemcpy(ctx->d_px, px.data(), px.size() * 4, cudaMemcpyHostToDevice));
-  // K3 triple tables (device-built): every 3-subset of the rows, 0/1 bytes
+  CK(grow(ctx, (void**)&ctx->d_rows, &ctx->rows_cap, img.size() * 4));
+  CK(grow(ctx, (void**)&ctx->d_px, &ctx->px_cap, px.size() * 4));
+  CK(cudaMemcpyAsync(ctx->d_rows, img.data(), img.size() * 4, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaMemcpyAsync(ctx->d_px, px.data(), px.size() * 4, cudaMemcpyHostToDevice,
+                     ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
+  // triple tables (K3, K4) are sized here and built lazily by the first
+  // round that needs them
+  ctx->trip_built = ctx->trip4_built = false;
+  ctx->trip_rows = ctx->trip4_rows = 0;
   if (k >= 4) {
-    const size_t rows3 = (size_t)k * (k - 1) * (k - 2) / 6 + bz::kTileRows;
-    CK(cudaMalloc(&ctx->d_trip, (size_t)m * rows3 * bz::tc_stride(w32)));
-    CK(cudaMemsetAsync(ctx->d_trip, 0, (size_t)m * rows3 * bz::tc_stride(w32), ctx->stream));
-    ctx->trip_rows = rows3;
     const size_t n3 = (size_t)k * (k - 1) * (k - 2) / 6;
-    const size_t rows4 = (n3 + bz::kUmmaN - 1) / bz::kUmmaN * bz::kUmmaN + bz::kUmmaN;
-    const size_t bytes4 = (size_t)m * rows4 * 32 * w32;
-    CK(cudaMalloc(&ctx->d_trip4, bytes4));
-    CK(cudaMemsetAsync(ctx->d_trip4, 0, bytes4, ctx->stream));
-    ctx->trip4_rows = rows4;
+    ctx->trip_rows = n3 + bz::kTileRows;
+    ctx->trip4_rows = (n3 + bz::kUmmaN - 1) / bz::kUmmaN * bz::kUmmaN + bz::kUmmaN;
   }
   if (m + 1 > ctx->bound_cap) {
     cudaFree(ctx->d_bound);
@@ -596,11 +622,6 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
   ctx->n = n;
   ctx->w32 = w32;
   ctx->wp = wp;
-  if (ctx->d_trip) {
-    int rc = build_triples(ctx);
-    if (rc) return rc;
-    CK(cudaStreamSynchronize(ctx->stream));
-  }
   return BZ_OK;
 }
 
