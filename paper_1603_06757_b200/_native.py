@@ -17,7 +17,7 @@ from .errors import (DeviceError, InvalidArity, InvalidDimensions, MindistError,
                      NoDevice, TooLarge)
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libbz.so")
+LIB_PATH = os.environ.get("BZ_LIB") or os.path.join(PKG_DIR, "libbz.so")
 ABI_VERSION = 1
 
 BZ_OK = 0

@@ -39,14 +39,17 @@ namespace bz {
 constexpr int kUmmaM = 128;       // prefixes per A tile = producer threads
 constexpr int kUmmaN = 256;       // triples per B tile
 constexpr int kUmmaMA = 1;        // A tiles (consecutive prefix steps) per B tile
-// warp roles: 0-15 epilogue (TMEM lane quarter = warp % 4, 64-column slice
-// = warp / 4), 16 MMA issuer + TMEM owner, 17 TMA loader, 18-21 producers
-constexpr int kK4EpiWarps = 16;
+// warp roles: [0, E) epilogue (TMEM lane quarter = warp % 4, column slice
+// = warp / 4), E MMA issuer + TMEM owner, E+1 TMA loader, E+2..E+5 producers
+#ifndef BZ_K4_EPI_WARPS
+#define BZ_K4_EPI_WARPS 16
+#endif
+constexpr int kK4EpiWarps = BZ_K4_EPI_WARPS;
 constexpr int kK4EpiCols = kUmmaN / (kK4EpiWarps / 4);  // columns per epilogue warp and A tile
-constexpr int kK4MmaWarp = 16;
-constexpr int kK4LoadWarp = 17;
-constexpr int kK4ProdWarp0 = 18;
-constexpr int kK4Threads = 32 * 22;
+constexpr int kK4MmaWarp = kK4EpiWarps;
+constexpr int kK4LoadWarp = kK4EpiWarps + 1;
+constexpr int kK4ProdWarp0 = kK4EpiWarps + 2;
+constexpr int kK4Threads = 32 * (kK4EpiWarps + 6);
 constexpr int kTmemCols = 512;    // kAccBufs buffers x kUmmaMA accumulators x kUmmaN columns
 constexpr int kAccBufs = kTmemCols / (kUmmaMA * kUmmaN);  // accumulator ring depth
 constexpr int kMaxStages = 4;
@@ -109,6 +112,24 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (done) return;
     if (spin > (1ull << 26)) __trap();
   }
+}
+// Tight wait (loop inside PTX; labels are local to the braces): used on the
+// MMA-issuing warp, where every cycle of handshake latency idles the pipe.
+__device__ __forceinline__ void mbar_wait_fast(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
 }
 __device__ __forceinline__ void tma_load_1d(uint32_t dst, const void* src, uint32_t bytes,
                                             uint32_t bar) {
@@ -445,7 +466,9 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
     // tcgen05.mma issue blocks while the tensor pipe is busy, so the waits
     // for tile t+1 are placed *before* the last MMA of tile t: the pipe then
     // still holds queued work while this thread does its barrier handshakes.
-    if (lane == 0) {
+    // the whole warp runs the loop (warp-uniform values stay in uniform
+    // registers); one elected lane issues the MMAs and commits
+    {
       const uint64_t a_desc0 = umma_desc(sA_s, 128, 2 * W * 128);
       const uint64_t b_desc0 = umma_desc(sB_s, 128, 2 * W * 128);
       uint32_t grp = 0, tcount = 0, bcount = 0;
@@ -456,10 +479,13 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
       bool pend_group_end = false;
       auto flush = [&]() {
         if (!pend) return;
-        if (!(a.debug & 4)) umma_i8(pd, pad, pbd, kUmmaIdesc, W > 1 ? 1u : 0u);
-        umma_commit(bempty(pstg));
-        umma_commit(accfull(pbuf));
-        if (pend_group_end) umma_commit(aempty(pab));
+        if (elect_one()) {
+          if (!(a.debug & 4)) umma_i8(pd, pad, pbd, kUmmaIdesc, W > 1 ? 1u : 0u);
+          umma_commit(bempty(pstg));
+          umma_commit(accfull(pbuf));
+          if (pend_group_end) umma_commit(aempty(pab));
+        }
+        __syncwarp();
         pend = false;
       };
       for (unsigned long long ci = blockIdx.x; ci < my_chunks; ci += gridDim.x) {
@@ -467,24 +493,28 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
         const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
         for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
           const int ab = grp & 1;
-          mbar_wait(afull(ab), (grp >> 1) & 1);
+          mbar_wait_fast(afull(ab), (grp >> 1) & 1);
           for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount, ++bcount) {
             const int stg = bcount % S;
             const int buf = tcount % kAccBufs;
-            mbar_wait(accempty(buf), ((tcount / kAccBufs) & 1) ^ 1);
-            mbar_wait(bfull(stg), (bcount / S) & 1);
+            mbar_wait_fast(accempty(buf), ((tcount / kAccBufs) & 1) ^ 1);
+            mbar_wait_fast(bfull(stg), (bcount / S) & 1);
             tc_fence_after();
             flush();  // previous tile's last MMA + commits
-            if (a.trace && blockIdx.x == 0 && tcount < 256) a.trace[1 * 256 + tcount] = clock64();
+            if (a.trace && blockIdx.x == 0 && lane == 0 && tcount < 256)
+              a.trace[1 * 256 + tcount] = clock64();
             const uint32_t d = tmem + (uint32_t)(buf * kUmmaN);
             // K step kb advances both start addresses by 256 B (16 in the
             // 16-byte-granular address field)
             const uint64_t ad0 = a_desc0 + (uint64_t)(ab * (TA >> 4));
             const uint64_t bd0 = b_desc0 + (uint64_t)(stg * (TB >> 4));
             if (!(a.debug & 4)) {
+              if (elect_one()) {
 #pragma unroll
-              for (int kb = 0; kb + 1 < W; ++kb)
-                umma_i8(d, ad0 + 16u * kb, bd0 + 16u * kb, kUmmaIdesc, kb > 0 ? 1u : 0u);
+                for (int kb = 0; kb + 1 < W; ++kb)
+                  umma_i8(d, ad0 + 16u * kb, bd0 + 16u * kb, kUmmaIdesc, kb > 0 ? 1u : 0u);
+              }
+              __syncwarp();
             }
             pend = true;
             pd = d;
@@ -494,7 +524,8 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
             pbuf = buf;
             pab = ab;
             pend_group_end = (t + 1 == c.tile_hi);
-            if (a.trace && blockIdx.x == 0 && tcount < 256) a.trace[4 * 256 + tcount] = clock64();
+            if (a.trace && blockIdx.x == 0 && lane == 0 && tcount < 256)
+              a.trace[4 * 256 + tcount] = clock64();
           }
         }
       }
