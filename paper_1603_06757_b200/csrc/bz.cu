@@ -451,10 +451,11 @@ int run_pass(bz_ctx* ctx, int g, int gamma_only, int lower_prev, int upper,
     std::vector<long long> h(8 * 256);
     CK(cudaMemcpy(h.data(), a.trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
     const long long t0 = h[0];
-    fprintf(stderr, "tile loader_go mma_go epi_go epi_released commit\n");
+    fprintf(stderr, "tile loader_go mma_pre mma_accok mma_go(bfull+flush) issued epi0_go epi0_rel epiL_go\n");
     for (int t = 0; t < 48; ++t)
-      fprintf(stderr, "%3d %8lld %8lld %8lld %8lld %8lld\n", t, h[t] - t0, h[256 + t] - t0,
-              h[512 + t] - t0, h[768 + t] - t0, h[1024 + t] - t0);
+      fprintf(stderr, "%3d %8lld %8lld %8lld %8lld %8lld %8lld %8lld %8lld\n", t, h[t] - t0,
+              h[1280 + t] - t0, h[1536 + t] - t0, h[256 + t] - t0, h[1024 + t] - t0,
+              h[512 + t] - t0, h[768 + t] - t0, h[1792 + t] - t0);
   }
   return BZ_OK;
 }

@@ -37,12 +37,22 @@
 namespace bz {
 
 constexpr int kUmmaM = 128;       // prefixes per A tile = producer threads
-constexpr int kUmmaN = 256;       // triples per B tile
-constexpr int kUmmaMA = 1;        // A tiles (consecutive prefix steps) per B tile
+#ifndef BZ_K4_N
+#define BZ_K4_N 256
+#endif
+#ifndef BZ_K4_MA
+#define BZ_K4_MA 1
+#endif
+#ifndef BZ_K4_HOLDBACK
+#define BZ_K4_HOLDBACK 0
+#endif
+constexpr bool kHoldBack = BZ_K4_HOLDBACK != 0;  // last MMA of a tile waits for the next tile's barriers
+constexpr int kUmmaN = BZ_K4_N;   // triples per B tile
+constexpr int kUmmaMA = BZ_K4_MA; // A tiles (consecutive prefix steps) per B tile
 // warp roles: [0, E) epilogue (TMEM lane quarter = warp % 4, column slice
 // = warp / 4), E MMA issuer + TMEM owner, E+1 TMA loader, E+2..E+5 producers
 #ifndef BZ_K4_EPI_WARPS
-#define BZ_K4_EPI_WARPS 16
+#define BZ_K4_EPI_WARPS 8
 #endif
 constexpr int kK4EpiWarps = BZ_K4_EPI_WARPS;
 constexpr int kK4EpiCols = kUmmaN / (kK4EpiWarps / 4);  // columns per epilogue warp and A tile
@@ -54,7 +64,10 @@ constexpr int kTmemCols = 512;    // kAccBufs buffers x kUmmaMA accumulators x k
 constexpr int kAccBufs = kTmemCols / (kUmmaMA * kUmmaN);  // accumulator ring depth
 constexpr int kMaxStages = 4;
 constexpr int kBarSlots = 4 + 2 * kMaxStages + 2 * kAccBufs;
-constexpr int kTmaPieces = 4;     // parallel bulk copies per B tile
+#ifndef BZ_K4_TMA_PIECES
+#define BZ_K4_TMA_PIECES 1
+#endif
+constexpr int kTmaPieces = BZ_K4_TMA_PIECES;  // parallel bulk copies per B tile
 
 __host__ __device__ constexpr int umma_tile_bytes_b(int w) { return kUmmaN * 32 * w; }
 __host__ __device__ constexpr int umma_tile_bytes_a(int w) { return kUmmaM * 32 * w; }
@@ -363,41 +376,51 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
           tc_fence_after();
           if (a.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && tcount < 256)
             a.trace[2 * 256 + tcount] = clock64();
+          if (a.trace && blockIdx.x == 0 && warp == kK4EpiWarps - 1 && lane == 0 && tcount < 256)
+            a.trace[7 * 256 + tcount] = clock64();
           const int lim = min(kUmmaN, c.slice - t * kUmmaN) - kK4EpiCols * slice_id;
           const uint32_t tb = tmem + ((uint32_t)(32 * quarter) << 16) +
                               (uint32_t)(buf * kUmmaMA * kUmmaN + kK4EpiCols * slice_id);
           // kK4EpiCols columns as packed s16 pairs: 3-input SIMD minima
           constexpr int NP = kK4EpiCols / 2;
-          uint32_t v[NP];
+          uint32_t v[kUmmaMA][NP];
           if (a.debug & 1) {
             __syncwarp();
             if (lane == 0) mbar_arrive(accempty(buf));
             continue;
           }
 #pragma unroll
-          for (int cc = 0; cc < kK4EpiCols / 32; ++cc) tmem_ld16p(tb + 32 * cc, v + 16 * cc);
+          for (int j = 0; j < kUmmaMA; ++j)
+#pragma unroll
+            for (int cc = 0; cc < kK4EpiCols / 32; ++cc)
+              tmem_ld16p(tb + j * kUmmaN + 32 * cc, &v[j][16 * cc]);
           tmem_ld_wait();
 #pragma unroll
-          for (int cc = 0; cc < kK4EpiCols / 32; ++cc) tmem_regs16_after_wait(v + 16 * cc);
+          for (int j = 0; j < kUmmaMA; ++j)
+#pragma unroll
+            for (int cc = 0; cc < kK4EpiCols / 32; ++cc) tmem_regs16_after_wait(&v[j][16 * cc]);
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(accempty(buf));  // accumulators are in registers
           if (a.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && tcount < 256)
             a.trace[3 * 256 + tcount] = clock64();
-          if (lim < kK4EpiCols) {
 #pragma unroll
-            for (int i = 0; i < NP; ++i) {
-              if (2 * i >= lim) v[i] |= 0x00007fffu, v[i] &= 0xffff7fffu;
-              if (2 * i + 1 >= lim) v[i] = (v[i] & 0x0000ffffu) | 0x7fff0000u;
+          for (int j = 0; j < kUmmaMA; ++j) {
+            if (lim < kK4EpiCols) {
+#pragma unroll
+              for (int i = 0; i < NP; ++i) {
+                if (2 * i >= lim) v[j][i] = (v[j][i] & 0xffff0000u) | 0x00007fffu;
+                if (2 * i + 1 >= lim) v[j][i] = (v[j][i] & 0x0000ffffu) | 0x7fff0000u;
+              }
             }
-          }
-          // 32 -> 11 -> 4 -> 2 -> 1 packed registers
-          uint32_t m = __vimin3_s16x2(v[0], v[1], v[2]);
+            // packed s16 pairs: 3-input SIMD minima down to one register
+            uint32_t m = __vimin3_s16x2(v[j][0], v[j][1], v[j][2]);
 #pragma unroll
-          for (int i = 3; i + 1 < NP; i += 2) m = __vimin3_s16x2(m, v[i], v[i + 1]);
-          if (NP % 2 == 0) m = __vmins2(m, v[NP - 1]);
-          const int lo = (int)(short)(m & 0xffffu), hi = (int)(short)(m >> 16);
-          rmin[0] = min(rmin[0], min(lo, hi));
+            for (int i = 3; i + 1 < NP; i += 2) m = __vimin3_s16x2(m, v[j][i], v[j][i + 1]);
+            if (NP % 2 == 0) m = __vmins2(m, v[j][NP - 1]);
+            const int lo = (int)(short)(m & 0xffffu), hi = (int)(short)(m >> 16);
+            rmin[j] = min(rmin[j], min(lo, hi));
+          }
         }
 #pragma unroll
         for (int j = 0; j < kUmmaMA; ++j) best = min(best, rmin[j] + wt[j]);
@@ -497,26 +520,46 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
           for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount, ++bcount) {
             const int stg = bcount % S;
             const int buf = tcount % kAccBufs;
+            if (a.trace && blockIdx.x == 0 && lane == 0 && tcount < 256)
+              a.trace[5 * 256 + tcount] = clock64();
             mbar_wait_fast(accempty(buf), ((tcount / kAccBufs) & 1) ^ 1);
+            if (a.trace && blockIdx.x == 0 && lane == 0 && tcount < 256)
+              a.trace[6 * 256 + tcount] = clock64();
             mbar_wait_fast(bfull(stg), (bcount / S) & 1);
             tc_fence_after();
             flush();  // previous tile's last MMA + commits
             if (a.trace && blockIdx.x == 0 && lane == 0 && tcount < 256)
               a.trace[1 * 256 + tcount] = clock64();
-            const uint32_t d = tmem + (uint32_t)(buf * kUmmaN);
             // K step kb advances both start addresses by 256 B (16 in the
             // 16-byte-granular address field)
-            const uint64_t ad0 = a_desc0 + (uint64_t)(ab * (TA >> 4));
             const uint64_t bd0 = b_desc0 + (uint64_t)(stg * (TB >> 4));
             if (!(a.debug & 4)) {
               if (elect_one()) {
 #pragma unroll
-                for (int kb = 0; kb + 1 < W; ++kb)
-                  umma_i8(d, ad0 + 16u * kb, bd0 + 16u * kb, kUmmaIdesc, kb > 0 ? 1u : 0u);
+                for (int j = 0; j < kUmmaMA; ++j) {
+                  const uint32_t dj = tmem + (uint32_t)((buf * kUmmaMA + j) * kUmmaN);
+                  const uint64_t adj = a_desc0 + (uint64_t)((ab * kUmmaMA + j) * (TA >> 4));
+#pragma unroll
+                  for (int kb = 0; kb < W; ++kb) {
+                    if (kHoldBack && j == kUmmaMA - 1 && kb == W - 1) break;  // held back
+                    umma_i8(dj, adj + 16u * kb, bd0 + 16u * kb, kUmmaIdesc, kb > 0 ? 1u : 0u);
+                  }
+                }
               }
               __syncwarp();
             }
+            const uint32_t d = tmem + (uint32_t)((buf * kUmmaMA + kUmmaMA - 1) * kUmmaN);
+            const uint64_t ad0 = a_desc0 + (uint64_t)((ab * kUmmaMA + kUmmaMA - 1) * (TA >> 4));
             pend = true;
+            if (!kHoldBack) {  // everything issued: commit right away
+              if (elect_one()) {
+                umma_commit(bempty(stg));
+                umma_commit(accfull(buf));
+                if (t + 1 == c.tile_hi) umma_commit(aempty(ab));
+              }
+              __syncwarp();
+              pend = false;
+            }
             pd = d;
             pad = ad0 + 16u * (W - 1);
             pbd = bd0 + 16u * (W - 1);
