@@ -117,7 +117,7 @@ int bz_enumerate(bz_ctx *ctx, int gamma, int g, int shard, int nshards,
 int bz_histogram(bz_ctx *ctx, int gamma, int g, int shard, int nshards,
                  uint64_t *out_hist, int32_t *out_min, uint64_t *out_combos);
 
-/* Host-only: the work plan bz_round uses for (m, k, g), for inspection and
+/* Host-only: the work plan bz_round uses for (m, k, g, nshards), for inspection and
  * for the CPU tests of the sharding logic.  Writes *out_ngroups groups of 10
  * int64 each -- chunk_begin, nprefix, gamma, ell, prefixes_per_lane,
  * combinations, depth, lanes_per_chunk, suffixes_per_chunk, suffix_blocks --
@@ -133,7 +133,7 @@ int bz_histogram(bz_ctx *ctx, int gamma, int g, int shard, int nshards,
  * suffixes_per_chunk.  lanes_per_chunk: 32 (K1 warp), 256 (K3 block), 128
  * (K4 block).  depth = 3 for g >= 4 unless engine == BZ_ENGINE_POPC, else 2
  * for g >= 3, else 1 (g = 1: ell = -1, empty prefix). */
-int bz_plan(int m, int k, int g, int engine, int64_t *out, int cap,
+int bz_plan(int m, int k, int g, int engine, int nshards, int64_t *out, int cap,
             int *out_ngroups, uint64_t *out_nchunks);
 
 /* Device timing on the context's stream: bz_timer_start records a CUDA

@@ -67,7 +67,7 @@ def lib():
     L.bz_round.argtypes = [vp, c_int, c_int, c_int, c_int, c_int, i32p, u64p]
     L.bz_enumerate.argtypes = [vp, c_int, c_int, c_int, c_int, i32p, u64p]
     L.bz_histogram.argtypes = [vp, c_int, c_int, c_int, c_int, u64p, i32p, u64p]
-    L.bz_plan.argtypes = [c_int, c_int, c_int, c_int, i64p, c_int, i32p, u64p]
+    L.bz_plan.argtypes = [c_int, c_int, c_int, c_int, c_int, i64p, c_int, i32p, u64p]
     L.bz_timer_start.argtypes = [vp]
     L.bz_timer_stop.argtypes = [vp, ctypes.POINTER(c_float)]
     L.bz_last_kernel_ms.argtypes = [vp, ctypes.POINTER(c_float)]
@@ -101,16 +101,16 @@ def device_count() -> int:
 ENGINES = {"auto": 0, "popc": 1, "imma": 2, "umma": 3}
 
 
-def plan(m: int, k: int, g: int, engine: str = "auto"):
+def plan(m: int, k: int, g: int, engine: str = "auto", nshards: int = 1):
     """The device work plan for one round (host-only; see bz_plan)."""
     L = lib()
     e = ENGINES[engine]
     ng = np.zeros(1, dtype=np.int32)
     nc = np.zeros(1, dtype=np.uint64)
-    check(L.bz_plan(m, k, g, e, None, 0, _ptr(ng, ctypes.c_int32),
+    check(L.bz_plan(m, k, g, e, nshards, None, 0, _ptr(ng, ctypes.c_int32),
                     _ptr(nc, ctypes.c_uint64)), what="bz_plan")
     out = np.zeros((int(ng[0]), 10), dtype=np.int64)
-    check(L.bz_plan(m, k, g, e, _ptr(out, ctypes.c_int64), int(ng[0]),
+    check(L.bz_plan(m, k, g, e, nshards, _ptr(out, ctypes.c_int64), int(ng[0]),
                     _ptr(ng, ctypes.c_int32), _ptr(nc, ctypes.c_uint64)), what="bz_plan")
     return [tuple(int(v) for v in row) for row in out], int(nc[0])
 

@@ -145,7 +145,7 @@ PlanShape pass_shape(int engine, int g, bool hist) {
   return {g >= 3 ? 2 : 1, 32, 0, 1};
 }
 
-int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape,
+int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape, int nshards,
                std::vector<Group>& gs, unsigned long long* out_nchunks) {
   const int depth = shape.depth;
   gs.clear();
@@ -158,7 +158,8 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
   if (shape.kernel == 4) {
     // K4: one persistent CTA per SM walks ~16 chunks; a chunk costs a walker
     // unrank per producer thread, so chunks are large
-    lane_target = (long long)(total / ((unsigned long long)shape.lanes * 148ull * 16ull));
+    lane_target = (long long)(total / ((unsigned long long)shape.lanes * 148ull * 16ull *
+                                       (unsigned long long)std::max(1, nshards)));
     lane_target = std::min(1ll << 20, std::max(4096ll, lane_target));
   }
   for (int j = j0; j < j1; ++j) {
@@ -207,10 +208,10 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
 }
 
 // Build the round's group table and upload it.
-int plan_round(bz_ctx* ctx, int g, int gamma_only, PlanShape shape, int* out_ngroups,
-               unsigned long long* out_nchunks) {
+int plan_round(bz_ctx* ctx, int g, int gamma_only, PlanShape shape, int nshards,
+               int* out_ngroups, unsigned long long* out_nchunks) {
   std::vector<Group> gs;
-  int rc = build_plan(ctx, ctx->m, ctx->k, g, gamma_only, shape, gs, out_nchunks);
+  int rc = build_plan(ctx, ctx->m, ctx->k, g, gamma_only, shape, nshards, gs, out_nchunks);
   if (rc) return rc;
   rc = ensure_round_buffers(ctx, (int)gs.size());
   if (rc) return rc;
@@ -388,7 +389,7 @@ int run_pass(bz_ctx* ctx, int g, int gamma_only, int lower_prev, int upper,
     rc = ensure_triples(ctx, depth.kernel);
     if (rc) return rc;
   }
-  rc = plan_round(ctx, g, gamma_only, depth, &ngroups, &nchunks);
+  rc = plan_round(ctx, g, gamma_only, depth, nshards, &ngroups, &nchunks);
   if (rc) return rc;
   const int m = ctx->m;
   for (int i = 0; i <= m; ++i) ctx->h_bound[i] = upper;
@@ -680,8 +681,8 @@ int bz_set_engine(bz_ctx* ctx, int engine) {
   return BZ_OK;
 }
 
-int bz_plan(int m, int k, int g, int engine, int64_t* out, int cap, int* out_ngroups,
-            uint64_t* out_nchunks) {
+int bz_plan(int m, int k, int g, int engine, int nshards, int64_t* out, int cap,
+            int* out_ngroups, uint64_t* out_nchunks) {
   if (!out_ngroups || !out_nchunks) return BZ_ERR_ARGUMENT;
   if (m < 1 || k < 1) return BZ_ERR_INVALID_DIMENSIONS;
   if (k > BZ_MAX_K) return BZ_ERR_TOO_LARGE;
@@ -690,7 +691,8 @@ int bz_plan(int m, int k, int g, int engine, int64_t* out, int cap, int* out_ngr
   std::vector<Group> gs;
   unsigned long long nchunks = 0;
   if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_UMMA) return BZ_ERR_ARGUMENT;
-  int rc = build_plan(nullptr, m, k, g, -1, pass_shape(engine, g, false), gs, &nchunks);
+  if (nshards < 1) return BZ_ERR_ARGUMENT;
+  int rc = build_plan(nullptr, m, k, g, -1, pass_shape(engine, g, false), nshards, gs, &nchunks);
   if (rc) return rc;
   *out_ngroups = (int)gs.size();
   *out_nchunks = nchunks;

@@ -63,7 +63,8 @@ constexpr int kK4Threads = 32 * (kK4EpiWarps + 6);
 constexpr int kTmemCols = 512;    // kAccBufs buffers x kUmmaMA accumulators x kUmmaN columns
 constexpr int kAccBufs = kTmemCols / (kUmmaMA * kUmmaN);  // accumulator ring depth
 constexpr int kMaxStages = 4;
-constexpr int kBarSlots = 4 + 2 * kMaxStages + 2 * kAccBufs;
+constexpr int kChunkQ = 4;         // depth of the loader -> roles chunk queue
+constexpr int kBarSlots = 4 + 2 * kMaxStages + 2 * kAccBufs + 2 * kChunkQ;
 #ifndef BZ_K4_TMA_PIECES
 #define BZ_K4_TMA_PIECES 1
 #endif
@@ -259,6 +260,7 @@ __host__ __device__ inline size_t k4_smem_bytes(int m, int k, int ngroups) {
   off += 2 * (size_t)kUmmaMA * umma_tile_bytes_a(W);
   off += kBarSlots * 8 + 16;     // barriers + TMEM base
   off += 2 * kUmmaMA * kUmmaM * sizeof(int);  // prefix weights of the A buffers
+  off += kChunkQ * sizeof(long long) + 16;    // chunk queue
   return off;
 }
 
@@ -302,6 +304,8 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(sA + 2 * kUmmaMA * TA);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + kBarSlots);
   int* s_wt = reinterpret_cast<int*>(s_tmem + 4);  // [2][kUmmaMA][kUmmaM] prefix weights
+  volatile long long* s_q = reinterpret_cast<volatile long long*>(
+      (reinterpret_cast<uintptr_t>(s_wt + 2 * kUmmaMA * kUmmaM) + 15) & ~uintptr_t(15));
   const uint32_t sB_s = (uint32_t)__cvta_generic_to_shared(sB);
   const uint32_t sA_s = (uint32_t)__cvta_generic_to_shared(sA);
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
@@ -315,6 +319,12 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   auto bempty = [&](int i) { return bar_s + 8u * (4 + kMaxStages + i); };
   auto accfull = [&](int i) { return bar_s + 8u * (4 + 2 * kMaxStages + i); };
   auto accempty = [&](int i) { return bar_s + 8u * (4 + 2 * kMaxStages + kAccBufs + i); };
+  // chunk queue: the loader draws chunks from the round's global counter
+  // (dynamic balance across CTAs) and publishes them to every other role
+  auto qfull = [&](int i) { return bar_s + 8u * (4 + 2 * kMaxStages + 2 * kAccBufs + i); };
+  auto qempty = [&](int i) {
+    return bar_s + 8u * (4 + 2 * kMaxStages + 2 * kAccBufs + kChunkQ + i);
+  };
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
@@ -326,6 +336,10 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
     for (int i = 0; i < kAccBufs; ++i) {
       mbar_init(accfull(i), 1);                  // MMA commit
       mbar_init(accempty(i), kK4EpiWarps);       // each epilogue warp
+    }
+    for (int i = 0; i < kChunkQ; ++i) {
+      mbar_init(qfull(i), 1);                    // loader
+      mbar_init(qempty(i), kK4EpiWarps + 5);     // epilogue, producer and MMA warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async();
@@ -343,10 +357,6 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
   const int k = a.k, q = a.g - 4;
-  const unsigned long long my_chunks =
-      a.nchunks > (unsigned long long)a.shard
-          ? (a.nchunks - a.shard + a.nshards - 1) / a.nshards
-          : 0ull;
   const unsigned FULL = 0xffffffffu;
 
   if (warp < kK4EpiWarps) {
@@ -355,8 +365,14 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
     const int quarter = warp & 3, slice_id = warp >> 2;
     const int r = 32 * quarter + lane;
     uint32_t grp = 0, tcount = 0;
-    for (unsigned long long ci = blockIdx.x; ci < my_chunks; ci += gridDim.x) {
-      const unsigned long long chunk = ci * a.nshards + a.shard;
+    for (uint32_t qi = 0;; ++qi) {
+      const int qs = qi % kChunkQ;
+      mbar_wait(qfull(qs), (qi / kChunkQ) & 1);
+      const long long qchunk = s_q[qs];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qempty(qs));
+      if (qchunk < 0) break;
+      const unsigned long long chunk = (unsigned long long)qchunk;
       const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
       int best = INT_MAX;
       for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
@@ -436,8 +452,14 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
     // ================= producers: thread r walks prefix row r
     const int r = tid - 32 * kK4ProdWarp0;
     uint32_t grp = 0;
-    for (unsigned long long ci = blockIdx.x; ci < my_chunks; ci += gridDim.x) {
-      const unsigned long long chunk = ci * a.nshards + a.shard;
+    for (uint32_t qi = 0;; ++qi) {
+      const int qs = qi % kChunkQ;
+      mbar_wait(qfull(qs), (qi / kChunkQ) & 1);
+      const long long qchunk = s_q[qs];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(qempty(qs));
+      if (qchunk < 0) break;
+      const unsigned long long chunk = (unsigned long long)qchunk;
       const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
       const unsigned long long first = c.bfirst + (unsigned long long)r * c.gr.ppl;
       long long cnt = 0;
@@ -511,8 +533,14 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
         __syncwarp();
         pend = false;
       };
-      for (unsigned long long ci = blockIdx.x; ci < my_chunks; ci += gridDim.x) {
-        const unsigned long long chunk = ci * a.nshards + a.shard;
+      for (uint32_t qi = 0;; ++qi) {
+        const int qs = qi % kChunkQ;
+        mbar_wait_fast(qfull(qs), (qi / kChunkQ) & 1);
+        const long long qchunk = s_q[qs];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(qempty(qs));
+        if (qchunk < 0) break;
+        const unsigned long long chunk = (unsigned long long)qchunk;
         const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
         for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
           const int ab = grp & 1;
@@ -579,8 +607,18 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
     // ================= loader: TMA bulk copies of triple tiles
     if (lane == 0) {
       uint32_t bcount = 0;
-      for (unsigned long long ci = blockIdx.x; ci < my_chunks; ci += gridDim.x) {
-        const unsigned long long chunk = ci * a.nshards + a.shard;
+      volatile int* vb = a.bound;
+      for (uint32_t qi = 0;; ++qi) {
+        const int qs = qi % kChunkQ;
+        mbar_wait(qempty(qs), ((qi / kChunkQ) & 1) ^ 1);
+        // next chunk of this shard, or -1 (done, or U reached L_prev)
+        const unsigned long long cidx = atomicAdd(a.counter, 1ull);
+        const unsigned long long ch = cidx * (unsigned long long)a.nshards + a.shard;
+        const long long qchunk = (ch < a.nchunks && vb[0] > a.lower_prev) ? (long long)ch : -1;
+        s_q[qs] = qchunk;
+        mbar_arrive(qfull(qs));
+        if (qchunk < 0) break;
+        const unsigned long long chunk = (unsigned long long)qchunk;
         const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
         const uint8_t* tsrc = trip + (size_t)c.gr.gamma * gamma_stride_rows * 32 * W;
         for (long long p = 0; p < c.maxcnt; p += kUmmaMA) {
@@ -629,7 +667,7 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
 // into TMEM (operand contents are irrelevant), then waits for completion.
 template <int N>
 __global__ void __launch_bounds__(128, 1) peak_umma_i8(int iters, long long* clk) {
-  extern __shared__ __align__(1024) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) unsigned long long bar;
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5;

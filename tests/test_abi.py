@@ -66,9 +66,9 @@ def test_plan_partitions_rank_space(m, k, g, engine):
     rng = random.Random(k * 100 + g)
     n = 2 * k + 5
     gammas = [[rng.getrandbits(n) for _ in range(k)] for _ in range(m)]
-    groups, nchunks = _native.plan(m, k, g, engine)
     expect = sorted(oracle.all_combinations(m, k, g))
     for nshards in (1, 2, 3, 8):
+        groups, nchunks = _native.plan(m, k, g, engine, nshards)
         seen = []
         mins = [None] * m
         for s in range(nshards):

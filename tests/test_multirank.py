@@ -44,7 +44,8 @@ def _worker(rank, world, port, rows_hex, n, out_path):
             self.k = gs.gammas[0].num_rows
 
         def run(self, g, lower_prev, upper):
-            groups, nchunks = _native.plan(len(self.gammas), self.k, g)
+            groups, nchunks = _native.plan(len(self.gammas), self.k, g,
+                                           nshards=self.comm.world)
             mins, combos, _ = oracle.enumerate_chunks(self.gammas, self.k, g, groups,
                                                       nchunks, self.comm.rank,
                                                       self.comm.world)
