@@ -187,3 +187,42 @@ def test_too_large(ctx):
     M = BitMatrix([(1 << i) for i in range(128)], 200)
     with pytest.raises(TooLarge):
         enumerate_gpu(M, 40)
+
+
+@pytest.mark.parametrize("k,n,g", [(4, 9, 4), (5, 40, 4), (128, 256, 4), (100, 200, 5),
+                                   (40, 224, 6), (30, 33, 7)])
+def test_tensor_engine_shapes(k, n, g, engine):
+    """K3/K4 edge shapes: smallest triple tables (k = 4, 5), the 2-stage
+    shared-memory path (W = 7, 8), slices smaller than one tile."""
+    rng = random.Random(k * 1000 + n + g)
+    rows = [rng.getrandbits(n) for _ in range(k)]
+    M = BitMatrix(rows, n)
+    if comb(k, g) > 20_000_000:
+        pytest.skip("oracle too slow")
+    assert enumerate_gpu(M, g).min_weight == oracle.min_weight(rows, n, g)[0], (k, n, g)
+
+
+def test_round_many_shards(ctx, engine):
+    G, gs, _ = code("cfg2", 2)
+    ctx.load(family_words(gs.gammas, 96), 96)
+    for g in (4, 5, 6):
+        whole_min, whole_c = ctx.round(g, 0, 10**6)
+        mins, cs = [10**9] * 2, [0, 0]
+        for s in range(5):
+            mn, c = ctx.round(g, 0, 10**6, s, 5)
+            mins = [min(a, b) for a, b in zip(mins, mn)]
+            cs = [a + b for a, b in zip(cs, c)]
+        assert mins == whole_min and cs == whole_c == [comb(48, g)] * 2
+
+
+def test_early_exit_all_engines(ctx, engine):
+    """Once the running minimum reaches lower_prev the round stops; its
+    result is then exactly lower_prev and fewer combinations are visited."""
+    G, gs, _ = code("cfg2", 1)
+    ctx.load(family_words(gs.gammas, 96), 96)
+    for g in (4, 5):
+        full_min, full_c = ctx.round(g, 0, 10**6)
+        true_min = min(full_min)
+        mins, combos = ctx.round(g, true_min, 10**6)
+        assert min(mins) == true_min
+        assert sum(combos) <= sum(full_c)
