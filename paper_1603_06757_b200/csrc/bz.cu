@@ -49,17 +49,22 @@ struct bz_ctx {
   uint32_t* d_px = nullptr;     // m*(k+1)*wp
   unsigned long long* d_binom = nullptr;
   // per-round scratch
+  // per-round I/O block (one H2D and one D2H per round):
+  //   [counter u64][combos m x u64][bound (m+1) x int32][pad][groups]
+  unsigned char* d_io = nullptr;
+  unsigned char* h_io = nullptr;  // pinned mirror
+  size_t io_cap = 0;
   Group* d_groups = nullptr;
-  int groups_cap = 0;
   int* d_bound = nullptr;                  // 1 + m
   unsigned long long* d_combos = nullptr;  // m
   unsigned long long* d_counter = nullptr;
   unsigned long long* d_hist = nullptr;    // BZ_MAX_N + 1
-  int bound_cap = 0;
-  // pinned staging
+  // pinned staging (views into h_io, and the histogram)
   Group* h_groups = nullptr;
   int* h_bound = nullptr;
   unsigned long long* h_combos = nullptr;
+  unsigned long long* h_counter = nullptr;
+  size_t io_in_bytes = 0, io_out_bytes = 0;
   unsigned long long* h_hist = nullptr;
 };
 
@@ -113,17 +118,32 @@ cudaError_t grow(bz_ctx*, void** p, size_t* cap, size_t bytes) {
   return e;
 }
 
-int ensure_round_buffers(bz_ctx* ctx, int ngroups) {
-  if (ngroups > ctx->groups_cap) {
-    if (ctx->d_groups) cudaFree(ctx->d_groups);
-    if (ctx->h_groups) cudaFreeHost(ctx->h_groups);
-    ctx->d_groups = nullptr;
-    ctx->h_groups = nullptr;
-    int cap = std::max(ngroups, 1024);
-    CK(cudaMalloc(&ctx->d_groups, sizeof(Group) * cap));
-    CK(cudaMallocHost(&ctx->h_groups, sizeof(Group) * cap));
-    ctx->groups_cap = cap;
+// Lay out (and grow) the per-round I/O block for m Gammas and ngroups groups.
+int ensure_io(bz_ctx* ctx, int m, int ngroups) {
+  const size_t off_combos = 8;
+  const size_t off_bound = off_combos + 8 * (size_t)m;
+  const size_t off_groups = (off_bound + 4 * (size_t)(m + 1) + 15) & ~size_t(15);
+  const size_t total = off_groups + sizeof(Group) * (size_t)std::max(ngroups, 1);
+  if (total > ctx->io_cap) {
+    if (ctx->d_io) cudaFree(ctx->d_io);
+    if (ctx->h_io) cudaFreeHost(ctx->h_io);
+    ctx->d_io = ctx->h_io = nullptr;
+    ctx->io_cap = 0;
+    const size_t cap = std::max<size_t>(total * 2, 64 * 1024);
+    CK(cudaMalloc(&ctx->d_io, cap));
+    CK(cudaMallocHost(&ctx->h_io, cap));
+    ctx->io_cap = cap;
   }
+  ctx->d_counter = reinterpret_cast<unsigned long long*>(ctx->d_io);
+  ctx->d_combos = reinterpret_cast<unsigned long long*>(ctx->d_io + off_combos);
+  ctx->d_bound = reinterpret_cast<int*>(ctx->d_io + off_bound);
+  ctx->d_groups = reinterpret_cast<Group*>(ctx->d_io + off_groups);
+  ctx->h_counter = reinterpret_cast<unsigned long long*>(ctx->h_io);
+  ctx->h_combos = reinterpret_cast<unsigned long long*>(ctx->h_io + off_combos);
+  ctx->h_bound = reinterpret_cast<int*>(ctx->h_io + off_bound);
+  ctx->h_groups = reinterpret_cast<Group*>(ctx->h_io + off_groups);
+  ctx->io_in_bytes = total;
+  ctx->io_out_bytes = off_bound + 4 * (size_t)(m + 1);
   return BZ_OK;
 }
 
@@ -131,7 +151,7 @@ int ensure_round_buffers(bz_ctx* ctx, int ngroups) {
 // chunk range.  gamma_only < 0: all m Gammas.
 // Shape of a pass: suffix depth D, prefixes walked in parallel per chunk,
 // triples per tile.  K4 (tcgen05) and K3 (legacy IMMA) take D = 3 for
-// g >= 4; K1 (POPC) takes D = 2 for g >= 3, else 1.  Histograms run on K1.
+// g >= 4; K1 (POPC) takes D = 2 for g >= 4, else 1.  Histograms run on K1.
 struct PlanShape {
   int depth, lanes, tile_rows, kernel;  // kernel: 1 = K1, 3 = K3, 4 = K4
 };
@@ -142,7 +162,9 @@ PlanShape pass_shape(int engine, int g, bool hist) {
     if (engine == BZ_ENGINE_AUTO || engine == BZ_ENGINE_UMMA)
       return {3, bz::kUmmaM, bz::kUmmaN, 4};
   }
-  return {g >= 3 ? 2 : 1, 32, 0, 1};
+  // D = 2 needs enough (g-3)-prefixes per group to fill a warp; at g = 3
+  // every group would hold one prefix, so g <= 3 keeps D = 1
+  return {g >= 4 ? 2 : 1, 32, 0, 1};
 }
 
 int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape, int nshards,
@@ -207,17 +229,16 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
   return BZ_OK;
 }
 
-// Build the round's group table and upload it.
+// Build the round's group table into the pinned I/O block (uploaded by
+// run_pass together with the bounds and counters).
 int plan_round(bz_ctx* ctx, int g, int gamma_only, PlanShape shape, int nshards,
                int* out_ngroups, unsigned long long* out_nchunks) {
   std::vector<Group> gs;
   int rc = build_plan(ctx, ctx->m, ctx->k, g, gamma_only, shape, nshards, gs, out_nchunks);
   if (rc) return rc;
-  rc = ensure_round_buffers(ctx, (int)gs.size());
+  rc = ensure_io(ctx, ctx->m, (int)gs.size());
   if (rc) return rc;
   std::memcpy(ctx->h_groups, gs.data(), gs.size() * sizeof(Group));
-  CK(cudaMemcpyAsync(ctx->d_groups, ctx->h_groups, gs.size() * sizeof(Group),
-                     cudaMemcpyHostToDevice, ctx->stream));
   *out_ngroups = (int)gs.size();
   return BZ_OK;
 }
@@ -392,11 +413,12 @@ int run_pass(bz_ctx* ctx, int g, int gamma_only, int lower_prev, int upper,
   rc = plan_round(ctx, g, gamma_only, depth, nshards, &ngroups, &nchunks);
   if (rc) return rc;
   const int m = ctx->m;
+  *ctx->h_counter = 0ull;
+  for (int i = 0; i < m; ++i) ctx->h_combos[i] = 0ull;
   for (int i = 0; i <= m; ++i) ctx->h_bound[i] = upper;
-  CK(cudaMemcpyAsync(ctx->d_bound, ctx->h_bound, sizeof(int) * (m + 1),
-                     cudaMemcpyHostToDevice, ctx->stream));
-  CK(cudaMemsetAsync(ctx->d_combos, 0, sizeof(unsigned long long) * m, ctx->stream));
-  CK(cudaMemsetAsync(ctx->d_counter, 0, sizeof(unsigned long long), ctx->stream));
+  // counter, counters, bounds and the work plan: one copy
+  CK(cudaMemcpyAsync(ctx->d_io, ctx->h_io, ctx->io_in_bytes, cudaMemcpyHostToDevice,
+                     ctx->stream));
   if (hist)
     CK(cudaMemsetAsync(ctx->d_hist, 0, sizeof(unsigned long long) * (ctx->n + 1), ctx->stream));
   RoundArgs a{};
@@ -439,10 +461,8 @@ int run_pass(bz_ctx* ctx, int g, int gamma_only, int lower_prev, int upper,
     CK(cudaEventRecord(ctx->ev_k0, ctx->stream));
     CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
   }
-  CK(cudaMemcpyAsync(ctx->h_bound, ctx->d_bound, sizeof(int) * (m + 1),
-                     cudaMemcpyDeviceToHost, ctx->stream));
-  CK(cudaMemcpyAsync(ctx->h_combos, ctx->d_combos, sizeof(unsigned long long) * m,
-                     cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->h_io, ctx->d_io, ctx->io_out_bytes, cudaMemcpyDeviceToHost,
+                     ctx->stream));
   if (hist)
     CK(cudaMemcpyAsync(ctx->h_hist, ctx->d_hist, sizeof(unsigned long long) * (ctx->n + 1),
                        cudaMemcpyDeviceToHost, ctx->stream));
@@ -509,7 +529,6 @@ int bz_create(int device, bz_ctx** out) {
   CK(cudaMalloc(&ctx->d_binom, tab.size() * sizeof(unsigned long long)));
   CK(cudaMemcpy(ctx->d_binom, tab.data(), tab.size() * sizeof(unsigned long long),
                 cudaMemcpyHostToDevice));
-  CK(cudaMalloc(&ctx->d_counter, sizeof(unsigned long long)));
   CK(cudaMalloc(&ctx->d_hist, sizeof(unsigned long long) * (BZ_MAX_N + 1)));
   CK(cudaMallocHost(&ctx->h_hist, sizeof(unsigned long long) * (BZ_MAX_N + 1)));
   ctx->err.clear();
@@ -526,14 +545,9 @@ void bz_destroy(bz_ctx* ctx) {
     cudaFree(ctx->d_trip);
     cudaFree(ctx->d_trip4);
     cudaFree(ctx->d_binom);
-    cudaFree(ctx->d_groups);
-    cudaFree(ctx->d_bound);
-    cudaFree(ctx->d_combos);
-    cudaFree(ctx->d_counter);
+    cudaFree(ctx->d_io);
     cudaFree(ctx->d_hist);
-    if (ctx->h_groups) cudaFreeHost(ctx->h_groups);
-    if (ctx->h_bound) cudaFreeHost(ctx->h_bound);
-    if (ctx->h_combos) cudaFreeHost(ctx->h_combos);
+    if (ctx->h_io) cudaFreeHost(ctx->h_io);
     if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
     if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
     if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
@@ -603,21 +617,9 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
     ctx->trip_rows = n3 + bz::kTileRows;
     ctx->trip4_rows = (n3 + bz::kUmmaN - 1) / bz::kUmmaN * bz::kUmmaN + bz::kUmmaN;
   }
-  if (m + 1 > ctx->bound_cap) {
-    cudaFree(ctx->d_bound);
-    cudaFree(ctx->d_combos);
-    if (ctx->h_bound) cudaFreeHost(ctx->h_bound);
-    if (ctx->h_combos) cudaFreeHost(ctx->h_combos);
-    ctx->d_bound = nullptr;
-    ctx->d_combos = nullptr;
-    ctx->h_bound = nullptr;
-    ctx->h_combos = nullptr;
-    const int cap = std::max(m + 1, 64);
-    CK(cudaMalloc(&ctx->d_bound, sizeof(int) * cap));
-    CK(cudaMalloc(&ctx->d_combos, sizeof(unsigned long long) * cap));
-    CK(cudaMallocHost(&ctx->h_bound, sizeof(int) * cap));
-    CK(cudaMallocHost(&ctx->h_combos, sizeof(unsigned long long) * cap));
-    ctx->bound_cap = cap;
+  {
+    int rc = ensure_io(ctx, m, 1);
+    if (rc) return rc;
   }
   ctx->m = m;
   ctx->k = k;

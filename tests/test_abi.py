@@ -49,7 +49,7 @@ def test_plan_counts(engine):
             begin, nprefix, gamma, ell, ppl, combos, depth, lanes, spc, nsb = gr
             assert nsb >= 1 and (depth != 3 or spc * nsb >= comb(k - 1 - ell, 3))
             assert lanes == ({"imma": 256}.get(engine, 128) if depth == 3 else 32)
-            want = 3 if (engine != "popc" and g >= 4) else (2 if g >= 3 else 1)
+            want = 3 if (engine != "popc" and g >= 4) else (2 if g >= 4 else 1)
             assert depth == want
             assert nprefix == (1 if g == 1 else comb(ell, g - 1 - depth))
             assert combos == nprefix * comb(k - 1 - ell, depth)
