@@ -132,7 +132,7 @@ int bz_histogram(bz_ctx *ctx, int gamma, int g, int shard, int nshards,
  * triple order (smallest element descending, then lex), S =
  * suffixes_per_chunk.  lanes_per_chunk: 32 (K1 warp), 256 (K3 block), 128
  * (K4 block).  depth = 3 for g >= 4 unless engine == BZ_ENGINE_POPC, else 2
- * for g >= 3, else 1 (g = 1: ell = -1, empty prefix). */
+ * for g >= 4, else 1 (g = 1: ell = -1, empty prefix). */
 int bz_plan(int m, int k, int g, int engine, int nshards, int64_t *out, int cap,
             int *out_ngroups, uint64_t *out_nchunks);
 
