@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define BZ_ABI_VERSION 1
+#define BZ_ABI_VERSION 2
 
 /* limits of the device kernels */
 #define BZ_MAX_K 128 /* rows per Gamma (prefix masks are 128-bit)      */
@@ -106,6 +106,15 @@ int bz_load_gammas(bz_ctx *ctx, const uint64_t *rows, int m, int k, int n);
  * combine by min (out_min) and sum (out_combos). */
 int bz_round(bz_ctx *ctx, int g, int lower_prev, int upper, int shard,
              int nshards, int32_t *out_min, uint64_t *out_combos);
+
+/* Rounds g0 .. g0+count-1 in one call: planned together, launched back to
+ * back, one synchronisation -- for the short early rounds, where launch and
+ * synchronisation latency dominate.  lower_prev[i] is round g0+i's early
+ * exit threshold; every round starts from `upper` (the caller folds the
+ * rounds into its bounds in order and may discard rounds past termination).
+ * out_min / out_combos hold count x m values, round-major. */
+int bz_rounds(bz_ctx *ctx, int g0, int count, const int32_t *lower_prev, int upper,
+              int shard, int nshards, int32_t *out_min, uint64_t *out_combos);
 
 /* One (Gamma_gamma, g) pass without early exit; out_min is the unclipped
  * minimum weight (INT32_MAX when the shard is empty). */

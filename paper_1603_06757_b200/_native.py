@@ -18,7 +18,7 @@ from .errors import (DeviceError, InvalidArity, InvalidDimensions, MindistError,
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BZ_LIB") or os.path.join(PKG_DIR, "libbz.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 BZ_OK = 0
 _CODES = {
@@ -33,7 +33,8 @@ _CODES = {
 
 # every symbol include/bz.h declares (checked by tests/test_abi.py)
 SYMBOLS = ("bz_abi_version", "bz_device_count", "bz_create", "bz_destroy",
-           "bz_last_error", "bz_set_engine", "bz_load_gammas", "bz_round", "bz_enumerate",
+           "bz_last_error", "bz_set_engine", "bz_load_gammas", "bz_round", "bz_rounds",
+           "bz_enumerate",
            "bz_histogram", "bz_plan", "bz_timer_start", "bz_timer_stop",
            "bz_last_kernel_ms", "bz_launch_count", "bz_measure_int_peaks")
 
@@ -65,6 +66,7 @@ def lib():
     L.bz_set_engine.argtypes = [vp, c_int]
     L.bz_load_gammas.argtypes = [vp, u64p, c_int, c_int, c_int]
     L.bz_round.argtypes = [vp, c_int, c_int, c_int, c_int, c_int, i32p, u64p]
+    L.bz_rounds.argtypes = [vp, c_int, c_int, i32p, c_int, c_int, c_int, i32p, u64p]
     L.bz_enumerate.argtypes = [vp, c_int, c_int, c_int, c_int, i32p, u64p]
     L.bz_histogram.argtypes = [vp, c_int, c_int, c_int, c_int, u64p, i32p, u64p]
     L.bz_plan.argtypes = [c_int, c_int, c_int, c_int, c_int, i64p, c_int, i32p, u64p]
@@ -186,6 +188,22 @@ class Context:
                              _ptr(mins, ctypes.c_int32), _ptr(combos, ctypes.c_uint64)),
               self.handle, f"bz_round(g={g})")
         return [int(v) for v in mins[:self.m]], [int(v) for v in combos[:self.m]]
+
+    def rounds(self, g0: int, lower_prev: list[int], upper: int, shard: int = 0,
+               nshards: int = 1):
+        """Rounds g0 .. g0+len(lower_prev)-1 in one call (see bz_rounds);
+        returns [(mins, combos)] per round."""
+        count = len(lower_prev)
+        lp = np.ascontiguousarray(lower_prev, dtype=np.int32)
+        mins = np.zeros(count * max(self.m, 1), dtype=np.int32)
+        combos = np.zeros(count * max(self.m, 1), dtype=np.uint64)
+        check(lib().bz_rounds(self.handle, g0, count, _ptr(lp, ctypes.c_int32), upper, shard,
+                              nshards, _ptr(mins, ctypes.c_int32),
+                              _ptr(combos, ctypes.c_uint64)),
+              self.handle, f"bz_rounds(g0={g0}, count={count})")
+        m = self.m
+        return [([int(v) for v in mins[i * m:(i + 1) * m]],
+                 [int(v) for v in combos[i * m:(i + 1) * m]]) for i in range(count)]
 
     def enumerate(self, gamma: int, g: int, shard: int = 0, nshards: int = 1):
         mn = np.zeros(1, dtype=np.int32)

@@ -49,22 +49,12 @@ struct bz_ctx {
   uint32_t* d_px = nullptr;     // m*(k+1)*wp
   unsigned long long* d_binom = nullptr;
   // per-round scratch
-  // per-round I/O block (one H2D and one D2H per round):
-  //   [counter u64][combos m x u64][bound (m+1) x int32][pad][groups]
+  // per-round I/O slots (io_layout): one H2D and one D2H per batch
   unsigned char* d_io = nullptr;
   unsigned char* h_io = nullptr;  // pinned mirror
   size_t io_cap = 0;
-  Group* d_groups = nullptr;
-  int* d_bound = nullptr;                  // 1 + m
-  unsigned long long* d_combos = nullptr;  // m
-  unsigned long long* d_counter = nullptr;
   unsigned long long* d_hist = nullptr;    // BZ_MAX_N + 1
-  // pinned staging (views into h_io, and the histogram)
-  Group* h_groups = nullptr;
-  int* h_bound = nullptr;
-  unsigned long long* h_combos = nullptr;
-  unsigned long long* h_counter = nullptr;
-  size_t io_in_bytes = 0, io_out_bytes = 0;
+  // pinned histogram staging
   unsigned long long* h_hist = nullptr;
 };
 
@@ -118,33 +108,43 @@ cudaError_t grow(bz_ctx*, void** p, size_t* cap, size_t bytes) {
   return e;
 }
 
-// Lay out (and grow) the per-round I/O block for m Gammas and ngroups groups.
-int ensure_io(bz_ctx* ctx, int m, int ngroups) {
-  const size_t off_combos = 8;
-  const size_t off_bound = off_combos + 8 * (size_t)m;
-  const size_t off_groups = (off_bound + 4 * (size_t)(m + 1) + 15) & ~size_t(15);
-  const size_t total = off_groups + sizeof(Group) * (size_t)std::max(ngroups, 1);
+// Per-round I/O slot: [counter u64][combos m x u64][bound (m+1) x int32]
+// [pad][groups].  A batch of rounds uses consecutive slots; the whole block
+// goes to the device in one copy and comes back in one copy.
+struct IoSlot {
+  size_t off_combos, off_bound, off_groups, size;
+};
+
+IoSlot io_layout(int m, int k) {
+  IoSlot l;
+  l.off_combos = 8;
+  l.off_bound = l.off_combos + 8 * (size_t)m;
+  l.off_groups = (l.off_bound + 4 * (size_t)(m + 1) + 15) & ~size_t(15);
+  const size_t max_groups = (size_t)m * (size_t)(k + 2) + 1;
+  l.size = (l.off_groups + sizeof(Group) * max_groups + 255) & ~size_t(255);
+  return l;
+}
+
+int ensure_io(bz_ctx* ctx, int nslots) {
+  const IoSlot l = io_layout(ctx->m, ctx->k);
+  const size_t total = l.size * (size_t)std::max(nslots, 1);
   if (total > ctx->io_cap) {
     if (ctx->d_io) cudaFree(ctx->d_io);
     if (ctx->h_io) cudaFreeHost(ctx->h_io);
     ctx->d_io = ctx->h_io = nullptr;
     ctx->io_cap = 0;
-    const size_t cap = std::max<size_t>(total * 2, 64 * 1024);
+    const size_t cap = std::max<size_t>(total, 64 * 1024);
     CK(cudaMalloc(&ctx->d_io, cap));
     CK(cudaMallocHost(&ctx->h_io, cap));
     ctx->io_cap = cap;
   }
-  ctx->d_counter = reinterpret_cast<unsigned long long*>(ctx->d_io);
-  ctx->d_combos = reinterpret_cast<unsigned long long*>(ctx->d_io + off_combos);
-  ctx->d_bound = reinterpret_cast<int*>(ctx->d_io + off_bound);
-  ctx->d_groups = reinterpret_cast<Group*>(ctx->d_io + off_groups);
-  ctx->h_counter = reinterpret_cast<unsigned long long*>(ctx->h_io);
-  ctx->h_combos = reinterpret_cast<unsigned long long*>(ctx->h_io + off_combos);
-  ctx->h_bound = reinterpret_cast<int*>(ctx->h_io + off_bound);
-  ctx->h_groups = reinterpret_cast<Group*>(ctx->h_io + off_groups);
-  ctx->io_in_bytes = total;
-  ctx->io_out_bytes = off_bound + 4 * (size_t)(m + 1);
   return BZ_OK;
+}
+
+// host / device views of slot i
+template <typename T>
+T* slot_ptr(unsigned char* base, const IoSlot& l, int i, size_t off) {
+  return reinterpret_cast<T*>(base + l.size * (size_t)i + off);
 }
 
 // Work plan of one round (host only): one Group per (Gamma, ell) with its
@@ -229,16 +229,15 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
   return BZ_OK;
 }
 
-// Build the round's group table into the pinned I/O block (uploaded by
-// run_pass together with the bounds and counters).
-int plan_round(bz_ctx* ctx, int g, int gamma_only, PlanShape shape, int nshards,
+// Build the round's group table into I/O slot `slot` (host side).
+int plan_round(bz_ctx* ctx, int g, int gamma_only, PlanShape shape, int nshards, int slot,
                int* out_ngroups, unsigned long long* out_nchunks) {
   std::vector<Group> gs;
   int rc = build_plan(ctx, ctx->m, ctx->k, g, gamma_only, shape, nshards, gs, out_nchunks);
   if (rc) return rc;
-  rc = ensure_io(ctx, ctx->m, (int)gs.size());
-  if (rc) return rc;
-  std::memcpy(ctx->h_groups, gs.data(), gs.size() * sizeof(Group));
+  const IoSlot l = io_layout(ctx->m, ctx->k);
+  std::memcpy(slot_ptr<Group>(ctx->h_io, l, slot, l.off_groups), gs.data(),
+              gs.size() * sizeof(Group));
   *out_ngroups = (int)gs.size();
   return BZ_OK;
 }
@@ -281,13 +280,11 @@ int launch_wd(bz_ctx* ctx, const RoundArgs& a, bool hist) {
   long long blocks = (long long)per_sm * ctx->sm_count;
   long long need = (long long)((warps_needed + (threads / 32) - 1) / (threads / 32));
   blocks = std::max(1ll, std::min(blocks, need));
-  CK(cudaEventRecord(ctx->ev_k0, ctx->stream));
   if (hist)
     bz::k1h_histogram<W, D><<<(unsigned)blocks, threads, smem, ctx->stream>>>(a);
   else
     bz::k1_round_min<W, D><<<(unsigned)blocks, threads, smem, ctx->stream>>>(a);
   CK(cudaGetLastError());
-  CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
   ctx->launches += 1;
   return BZ_OK;
 }
@@ -304,11 +301,9 @@ int launch_tc(bz_ctx* ctx, const RoundArgs& a) {
   const unsigned long long blocks_needed = (a.nchunks + a.nshards - 1) / a.nshards;
   long long blocks = (long long)per_sm * ctx->sm_count;
   blocks = std::max(1ll, std::min(blocks, (long long)blocks_needed));
-  CK(cudaEventRecord(ctx->ev_k0, ctx->stream));
   bz::k3_round_gemm<W><<<(unsigned)blocks, threads, smem, ctx->stream>>>(a, ctx->d_trip,
                                                                          ctx->trip_rows);
   CK(cudaGetLastError());
-  CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
   ctx->launches += 1;
   return BZ_OK;
 }
@@ -320,11 +315,9 @@ int launch_umma(bz_ctx* ctx, const RoundArgs& a) {
                           (int)smem));
   const unsigned long long mine = (a.nchunks + a.nshards - 1 - a.shard) / a.nshards;
   long long blocks = std::max(1ll, std::min((long long)ctx->sm_count, (long long)mine));
-  CK(cudaEventRecord(ctx->ev_k0, ctx->stream));
   bz::k4_round_umma<W><<<(unsigned)blocks, bz::kK4Threads, smem, ctx->stream>>>(
       a, ctx->d_trip4, ctx->trip4_rows);
   CK(cudaGetLastError());
-  CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
   ctx->launches += 1;
   return BZ_OK;
 }
@@ -396,81 +389,106 @@ int launch(bz_ctx* ctx, const RoundArgs& a, bool hist, const PlanShape& depth) {
   }
 }
 
-// Shared body of bz_round / bz_enumerate / bz_histogram.
-int run_pass(bz_ctx* ctx, int g, int gamma_only, int lower_prev, int upper,
-             int shard, int nshards, bool hist) {
+// Shared body of bz_round / bz_rounds / bz_enumerate / bz_histogram: rounds
+// g0 .. g0+count-1 (each over all Gammas, or only `gamma_only`) planned on
+// the host, one H2D of their I/O slots, the launches back to back on the
+// stream, one D2H, one synchronisation.  lower_prev[i] is round i's early
+// exit threshold; every round starts from the same `upper`.
+int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_prev,
+              int upper, int shard, int nshards, bool hist) {
   if (nshards < 1 || shard < 0 || shard >= nshards)
     return fail(ctx, BZ_ERR_ARGUMENT, "bad shard %d of %d", shard, nshards);
-  int rc = check_g(ctx, g);
-  if (rc) return rc;
-  int ngroups = 0;
-  unsigned long long nchunks = 0;
-  const PlanShape depth = pass_shape(ctx->engine, g, hist);
-  if (depth.kernel == 3 || depth.kernel == 4) {
-    rc = ensure_triples(ctx, depth.kernel);
+  if (count < 1 || (hist && count != 1)) return fail(ctx, BZ_ERR_ARGUMENT, "bad count %d", count);
+  for (int i = 0; i < count; ++i) {
+    int rc = check_g(ctx, g0 + i);
     if (rc) return rc;
   }
-  rc = plan_round(ctx, g, gamma_only, depth, nshards, &ngroups, &nchunks);
+  int rc = ensure_io(ctx, count);
   if (rc) return rc;
+  const IoSlot l = io_layout(ctx->m, ctx->k);
   const int m = ctx->m;
-  *ctx->h_counter = 0ull;
-  for (int i = 0; i < m; ++i) ctx->h_combos[i] = 0ull;
-  for (int i = 0; i <= m; ++i) ctx->h_bound[i] = upper;
-  // counter, counters, bounds and the work plan: one copy
-  CK(cudaMemcpyAsync(ctx->d_io, ctx->h_io, ctx->io_in_bytes, cudaMemcpyHostToDevice,
-                     ctx->stream));
-  if (hist)
-    CK(cudaMemsetAsync(ctx->d_hist, 0, sizeof(unsigned long long) * (ctx->n + 1), ctx->stream));
-  RoundArgs a{};
-  a.rows = ctx->d_rows;
-  a.px = ctx->d_px;
-  a.groups = ctx->d_groups;
-  a.binom = ctx->d_binom;
-  a.bound = ctx->d_bound;
-  a.combos = ctx->d_combos;
-  a.counter = ctx->d_counter;
-  a.hist = ctx->d_hist;
-  a.nchunks = nchunks;
-  a.ngroups = ngroups;
-  a.m = m;
-  a.k = ctx->k;
-  a.g = g;
-  a.n = ctx->n;
-  a.shard = shard;
-  a.nshards = nshards;
-  a.lower_prev = lower_prev;
+  struct Pending {
+    RoundArgs a;
+    PlanShape shape;
+    bool run;
+  };
+  std::vector<Pending> todo(count);
+  long long* trace = nullptr;
+  int debug = 0;
   {
     // timing experiments on K4 (results are NOT valid when set): bit 0 skips
-    // the epilogue's TMEM reads, bit 1 the TMA tile loads, bit 2 the MMAs
+    // the epilogue's TMEM reads, bit 1 the TMA tile loads, bit 2 the MMAs,
+    // bit 3 records a per-tile timeline of block 0
     const char* dbg = getenv("BZ_K4_DEBUG");
-    a.debug = dbg ? atoi(dbg) : 0;
-    a.trace = nullptr;
-    if (a.debug & 8) {
+    debug = dbg ? atoi(dbg) : 0;
+    if (debug & 8) {
       static long long* d_trace = nullptr;
-      if (!d_trace) {
-        CK(cudaMalloc(&d_trace, 8 * 256 * sizeof(long long)));
-      }
+      if (!d_trace) CK(cudaMalloc(&d_trace, 8 * 256 * sizeof(long long)));
       CK(cudaMemsetAsync(d_trace, 0, 8 * 256 * sizeof(long long), ctx->stream));
-      a.trace = d_trace;
+      trace = d_trace;
     }
   }
-  if (nchunks > 0 && (unsigned long long)shard < nchunks) {
-    rc = launch(ctx, a, hist, depth);
+  for (int i = 0; i < count; ++i) {
+    const int g = g0 + i;
+    const PlanShape shape = pass_shape(ctx->engine, g, hist);
+    if (shape.kernel == 3 || shape.kernel == 4) {
+      rc = ensure_triples(ctx, shape.kernel);
+      if (rc) return rc;
+    }
+    int ngroups = 0;
+    unsigned long long nchunks = 0;
+    rc = plan_round(ctx, g, gamma_only, shape, nshards, i, &ngroups, &nchunks);
     if (rc) return rc;
-  } else {
-    CK(cudaEventRecord(ctx->ev_k0, ctx->stream));
-    CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
+    *slot_ptr<unsigned long long>(ctx->h_io, l, i, 0) = 0ull;
+    unsigned long long* hc = slot_ptr<unsigned long long>(ctx->h_io, l, i, l.off_combos);
+    int* hb = slot_ptr<int>(ctx->h_io, l, i, l.off_bound);
+    for (int j = 0; j < m; ++j) hc[j] = 0ull;
+    for (int j = 0; j <= m; ++j) hb[j] = upper;
+    RoundArgs& a = todo[i].a;
+    a = RoundArgs{};
+    a.rows = ctx->d_rows;
+    a.px = ctx->d_px;
+    a.groups = slot_ptr<Group>(ctx->d_io, l, i, l.off_groups);
+    a.binom = ctx->d_binom;
+    a.bound = slot_ptr<int>(ctx->d_io, l, i, l.off_bound);
+    a.combos = slot_ptr<unsigned long long>(ctx->d_io, l, i, l.off_combos);
+    a.counter = slot_ptr<unsigned long long>(ctx->d_io, l, i, 0);
+    a.hist = ctx->d_hist;
+    a.nchunks = nchunks;
+    a.ngroups = ngroups;
+    a.m = m;
+    a.k = ctx->k;
+    a.g = g;
+    a.n = ctx->n;
+    a.shard = shard;
+    a.nshards = nshards;
+    a.lower_prev = lower_prev ? lower_prev[i] : 0;
+    a.debug = debug;
+    a.trace = (i == count - 1) ? trace : nullptr;
+    todo[i].shape = shape;
+    todo[i].run = nchunks > 0 && (unsigned long long)shard < nchunks;
   }
-  CK(cudaMemcpyAsync(ctx->h_io, ctx->d_io, ctx->io_out_bytes, cudaMemcpyDeviceToHost,
+  if (hist)
+    CK(cudaMemsetAsync(ctx->d_hist, 0, sizeof(unsigned long long) * (ctx->n + 1), ctx->stream));
+  CK(cudaMemcpyAsync(ctx->d_io, ctx->h_io, l.size * (size_t)count, cudaMemcpyHostToDevice,
                      ctx->stream));
+  CK(cudaEventRecord(ctx->ev_k0, ctx->stream));
+  for (int i = 0; i < count; ++i) {
+    if (!todo[i].run) continue;
+    rc = launch(ctx, todo[i].a, hist, todo[i].shape);
+    if (rc) return rc;
+  }
+  CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->h_io, ctx->d_io, l.size * (size_t)(count - 1) + l.off_groups,
+                     cudaMemcpyDeviceToHost, ctx->stream));
   if (hist)
     CK(cudaMemcpyAsync(ctx->h_hist, ctx->d_hist, sizeof(unsigned long long) * (ctx->n + 1),
                        cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaEventElapsedTime(&ctx->last_kernel_ms, ctx->ev_k0, ctx->ev_k1));
-  if (a.trace) {
+  if (trace) {
     std::vector<long long> h(8 * 256);
-    CK(cudaMemcpy(h.data(), a.trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
     const long long t0 = h[0];
     fprintf(stderr, "tile loader_go mma_pre mma_accok mma_go(bfull+flush) issued epi0_go epi0_rel epiL_go\n");
     for (int t = 0; t < 48; ++t)
@@ -479,6 +497,16 @@ int run_pass(bz_ctx* ctx, int g, int gamma_only, int lower_prev, int upper,
               h[512 + t] - t0, h[768 + t] - t0, h[1792 + t] - t0);
   }
   return BZ_OK;
+}
+
+// results of slot i after run_batch
+const int* slot_bound(bz_ctx* ctx, int i) {
+  const IoSlot l = io_layout(ctx->m, ctx->k);
+  return slot_ptr<int>(ctx->h_io, l, i, l.off_bound);
+}
+const unsigned long long* slot_combos(bz_ctx* ctx, int i) {
+  const IoSlot l = io_layout(ctx->m, ctx->k);
+  return slot_ptr<unsigned long long>(ctx->h_io, l, i, l.off_combos);
 }
 
 }  // namespace
@@ -617,10 +645,7 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
     ctx->trip_rows = n3 + bz::kTileRows;
     ctx->trip4_rows = (n3 + bz::kUmmaN - 1) / bz::kUmmaN * bz::kUmmaN + bz::kUmmaN;
   }
-  {
-    int rc = ensure_io(ctx, m, 1);
-    if (rc) return rc;
-  }
+
   ctx->m = m;
   ctx->k = k;
   ctx->n = n;
@@ -635,12 +660,29 @@ int bz_round(bz_ctx* ctx, int g, int lower_prev, int upper, int shard, int nshar
   if (!out_min || !out_combos) return fail(ctx, BZ_ERR_ARGUMENT, "null output");
   if (ctx->device < 0) return fail(ctx, BZ_ERR_NO_DEVICE, "context has no device");
   CK(cudaSetDevice(ctx->device));
-  int rc = run_pass(ctx, g, -1, lower_prev, upper, shard, nshards, false);
+  int rc = run_batch(ctx, g, 1, -1, &lower_prev, upper, shard, nshards, false);
   if (rc) return rc;
   for (int j = 0; j < ctx->m; ++j) {
-    out_min[j] = std::min(ctx->h_bound[1 + j], upper);
-    out_combos[j] = ctx->h_combos[j];
+    out_min[j] = std::min(slot_bound(ctx, 0)[1 + j], upper);
+    out_combos[j] = slot_combos(ctx, 0)[j];
   }
+  return BZ_OK;
+}
+
+int bz_rounds(bz_ctx* ctx, int g0, int count, const int32_t* lower_prev, int upper,
+              int shard, int nshards, int32_t* out_min, uint64_t* out_combos) {
+  if (!ctx) return BZ_ERR_ARGUMENT;
+  if (!out_min || !out_combos || !lower_prev) return fail(ctx, BZ_ERR_ARGUMENT, "null argument");
+  if (ctx->device < 0) return fail(ctx, BZ_ERR_NO_DEVICE, "context has no device");
+  CK(cudaSetDevice(ctx->device));
+  std::vector<int> lp(lower_prev, lower_prev + std::max(count, 0));
+  int rc = run_batch(ctx, g0, count, -1, lp.data(), upper, shard, nshards, false);
+  if (rc) return rc;
+  for (int i = 0; i < count; ++i)
+    for (int j = 0; j < ctx->m; ++j) {
+      out_min[(size_t)i * ctx->m + j] = std::min(slot_bound(ctx, i)[1 + j], upper);
+      out_combos[(size_t)i * ctx->m + j] = slot_combos(ctx, i)[j];
+    }
   return BZ_OK;
 }
 
@@ -652,10 +694,11 @@ int bz_enumerate(bz_ctx* ctx, int gamma, int g, int shard, int nshards, int32_t*
   if (gamma < 0 || gamma >= ctx->m)
     return fail(ctx, BZ_ERR_STATE, "gamma %d not in 0..%d", gamma, ctx->m - 1);
   CK(cudaSetDevice(ctx->device));
-  int rc = run_pass(ctx, g, gamma, 0, INT32_MAX, shard, nshards, false);
+  const int zero = 0;
+  int rc = run_batch(ctx, g, 1, gamma, &zero, INT32_MAX, shard, nshards, false);
   if (rc) return rc;
-  *out_min = ctx->h_bound[1 + gamma];
-  *out_combos = ctx->h_combos[gamma];
+  *out_min = slot_bound(ctx, 0)[1 + gamma];
+  *out_combos = slot_combos(ctx, 0)[gamma];
   return BZ_OK;
 }
 
@@ -667,11 +710,12 @@ int bz_histogram(bz_ctx* ctx, int gamma, int g, int shard, int nshards, uint64_t
   if (gamma < 0 || gamma >= ctx->m)
     return fail(ctx, BZ_ERR_STATE, "gamma %d not in 0..%d", gamma, ctx->m - 1);
   CK(cudaSetDevice(ctx->device));
-  int rc = run_pass(ctx, g, gamma, 0, INT32_MAX, shard, nshards, true);
+  const int zero = 0;
+  int rc = run_batch(ctx, g, 1, gamma, &zero, INT32_MAX, shard, nshards, true);
   if (rc) return rc;
   for (int b = 0; b <= ctx->n; ++b) out_hist[b] = ctx->h_hist[b];
-  *out_min = ctx->h_bound[0];
-  *out_combos = ctx->h_combos[gamma];
+  *out_min = slot_bound(ctx, 0)[0];
+  *out_combos = slot_combos(ctx, 0)[gamma];
   return BZ_OK;
 }
 

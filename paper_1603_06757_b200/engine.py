@@ -28,6 +28,7 @@ from __future__ import annotations
 import os
 import time
 from dataclasses import dataclass, field
+from math import comb
 
 from . import _native
 from .enumeration import EnumerationResult, family_words
@@ -83,6 +84,10 @@ class EngineConfig:
     device: int | None = None
     distributed: bool = False
     early_exit: bool = True  # stop a round once U reaches the previous L
+    # consecutive rounds with at most this many combinations in total run as
+    # one batch (one launch sequence, one synchronisation; replicated, not
+    # sharded, across ranks); 0 disables batching
+    batch_combinations: int = 2_000_000_000
     engine: str = "auto"     # "auto" | "popc" | "imma" (kernel choice; same results)
 
 
@@ -160,6 +165,12 @@ class GpuRounds:
         mins, combos = self.comm.combine(mins, combos)
         return mins, combos, kernel_ms
 
+    def run_batch(self, g0: int, lower_prevs: list[int], upper: int):
+        """Rounds g0.. in one call, computed whole on every rank (no
+        exchange): [(mins, combos)] per round and the batch's kernel ms."""
+        res = self.ctx.rounds(g0, lower_prevs, upper)
+        return res, self.ctx.last_kernel_ms()
+
 
 def make_backend(config: EngineConfig, comm):
     """Seam for tests (cf. the reference's monkeypatch of enumerate_basic,
@@ -206,12 +217,35 @@ def run_rounds(backend, gs: GammaSet, k: int, config: EngineConfig, st: LoopStat
     per-Gamma minima into U in Gamma order, then raise L, append (g, L, U),
     report progress.  ``backend`` already holds the family on the device."""
     m_arg, km_arg = line7_args(gs, k)
+    m = gs.matrix_count
+    batch_ok = config.batch_combinations > 0 and hasattr(backend, "run_batch")
+    queued: list = []  # precomputed (g, mins, combos, kernel_ms) of a batch
     while st.g <= k and st.L < st.U:
         if st.g > config.max_g:
             st.status = STATUS_UPPER_BOUND_ONLY
             break
         tr = time.perf_counter()
-        mins, combos, kernel_ms = backend.run(st.g, st.L if config.early_exit else 0, st.U)
+        if not queued and batch_ok:
+            # the next rounds whose total size fits the batch budget
+            count, total = 0, 0
+            while (st.g + count <= min(k, config.max_g)
+                   and total + m * comb(k, st.g + count) <= config.batch_combinations):
+                total += m * comb(k, st.g + count)
+                count += 1
+            if count >= 2:
+                lps = [st.L if config.early_exit else 0]
+                for i in range(1, count):
+                    lps.append(lower_bound_update(st.g + i - 1, m_arg, k, km_arg)
+                               if config.early_exit else 0)
+                res, batch_ms = backend.run_batch(st.g, lps, st.U)
+                for i, (mn, cb) in enumerate(res):
+                    share = (m * comb(k, st.g + i)) / total if total else 0.0
+                    queued.append((st.g + i, mn, cb, batch_ms * share))
+        if queued and queued[0][0] == st.g:
+            _, mins, combos, kernel_ms = queued.pop(0)
+        else:
+            queued.clear()
+            mins, combos, kernel_ms = backend.run(st.g, st.L if config.early_exit else 0, st.U)
         round_combos = 0
         for mn, c in zip(mins, combos):
             st.U = min(st.U, mn)

@@ -163,3 +163,32 @@ def test_report_roundtrip(oracle_backend):
 
 def test_configs_table():
     assert CONFIGS["cfg5"].k == 80 and CONFIGS["cfg5"].n == 160
+
+
+class OracleBatchRounds(OracleRounds):
+    """Adds the batched-rounds seam (GpuRounds.run_batch) on the oracle."""
+
+    batches: list = []
+
+    def run_batch(self, g0, lower_prevs, upper):
+        OracleBatchRounds.batches.append((g0, len(lower_prevs)))
+        out = []
+        for i in range(len(lower_prevs)):
+            res = [oracle.min_weight(rows, self.n, g0 + i, threads=2) for rows in self.gammas]
+            out.append(([min(mn, upper) for mn, _ in res], [c for _, c in res]))
+        return out, 0.0
+
+
+@pytest.mark.parametrize("idx", range(6))
+def test_engine_batched_rounds(goldens, monkeypatch, idx):
+    """Rounds batched ahead of the bound check give the reference's trace,
+    status and combination count (rounds past termination are dropped)."""
+    OracleBatchRounds.batches = []
+    monkeypatch.setattr(engine, "make_backend", lambda cfg, comm: OracleBatchRounds(cfg, comm))
+    fx = goldens["configs"][idx]
+    rep = minimum_distance(BitMatrix(hexrows(fx["rows"]), fx["n"]),
+                           EngineConfig(batch_combinations=10**9))
+    assert rep.distance == fx["distance"]
+    assert rep.bounds_trace == [tuple(t) for t in fx["bounds_trace"]]
+    assert rep.counters.combinations == fx["combinations"]
+    assert OracleBatchRounds.batches and OracleBatchRounds.batches[0][0] == 1
