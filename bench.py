@@ -282,9 +282,13 @@ def main():
     peaks = ctx.measure_int_peaks(w32)
     top_ms = statistics.median(g_top_ms)
     achieved = (g_top_combos / world) / (top_ms * 1e-3)
-    macs_per_combo = 32 * w32  # K of the weight GEMM: the full padded codeword
-    umma_peak = peaks["umma_mac_per_s"] / macs_per_combo
-    imma_peak = peaks["imma_mac_per_s"] / macs_per_combo
+    # MACs per combination: the K of the weight GEMM, i.e. the padded
+    # codeword -- K4 (kind::i8) 32 per word, K5 (kind::mxf4) K = 64 steps
+    macs_i8 = 32 * w32
+    macs_f4 = 64 * ((w32 + 1) // 2)
+    mxf4_peak = peaks["mxf4_mac_per_s"] / macs_f4
+    umma_peak = peaks["umma_mac_per_s"] / macs_i8
+    imma_peak = peaks["imma_mac_per_s"] / macs_i8
     popc_peak = peaks["popc_per_s"] / w32
     g_top = max(st.rounds, key=lambda r: r.combinations).g
 
@@ -299,6 +303,7 @@ def main():
 
     k1_achieved = engine_rate("popc")
     k3_achieved = engine_rate("imma")
+    k4_achieved = engine_rate("umma")
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
@@ -308,7 +313,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "s8 tensor / u32", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "e2m1 tensor (fp32 acc) / u32", "data": "synthetic",
         "config": {"workload": WORKLOAD if args.config == "cfg5" else args.config,
                    "k": k, "n": n, "m": m, "d": rep.distance, "g_final": rep.g_reached,
                    "combinations_per_step": int(combos_all / args.steps),
@@ -321,21 +326,28 @@ def main():
                 "d2h_bytes_per_step": d2h, "wall_s": e2e_s},
         "gpu_launches": launches,
         "clocks": clock,
-        "roofline": {"bound": "tensor", "achieved": achieved / 1e9, "peak": umma_peak / 1e9,
-                     "unit": "Gcombinations/s", "frac": achieved / umma_peak,
+        "roofline": {"bound": "tensor", "achieved": achieved / 1e9, "peak": mxf4_peak / 1e9,
+                     "unit": "Gcombinations/s", "frac": achieved / mxf4_peak,
                      "traffic": traffic,
-                     "kernel": f"k4_round_umma<{w32}> round g={g_top} (tcgen05.mma kind::i8)",
-                     "peak_source": f"live microbenchmark: tcgen05.mma kind::i8 M128xN256xK32 "
-                                    f"{peaks['umma_mac_per_clk_sm']:.0f} MACs/clk/SM, "
-                                    f"{peaks['umma_mac_per_s'] / 1e15:.2f} PMAC/s / "
-                                    f"{macs_per_combo} MACs per combination",
+                     "kernel": f"k4_round_umma<{w32},true> = K5, round g={g_top} "
+                               f"(tcgen05.mma kind::mxf4, unit block scales)",
+                     "peak_source": f"live microbenchmark: tcgen05.mma kind::mxf4 M128xN240xK64 "
+                                    f"{peaks['mxf4_mac_per_clk_sm']:.0f} MACs/clk/SM, "
+                                    f"{peaks['mxf4_mac_per_s'] / 1e15:.2f} PMAC/s / "
+                                    f"{macs_f4} MACs per combination (K padded to 64)",
                      "popc_roofline": popc_peak / 1e9,
                      "frac_of_popc_roofline": achieved / popc_peak},
+        "k4_umma_i8": {"kernel": f"k4_round_umma<{w32},false> round g={g_top} "
+                                 f"(tcgen05.mma kind::i8)",
+                       "achieved": k4_achieved / 1e9, "peak": umma_peak / 1e9,
+                       "unit": "Gcombinations/s", "frac": k4_achieved / umma_peak,
+                       "peak_source": f"live microbenchmark: {peaks['umma_mac_per_clk_sm']:.0f} "
+                                      f"MACs/clk/SM / {macs_i8} MACs per combination"},
         "k3_imma": {"kernel": f"k3_round_gemm<{w32}> round g={g_top} (legacy mma.sync s8)",
                     "achieved": k3_achieved / 1e9, "peak": imma_peak / 1e9,
                     "unit": "Gcombinations/s", "frac": k3_achieved / imma_peak,
                     "peak_source": f"live microbenchmark: {peaks['imma_mac_per_clk_sm']:.0f} "
-                                   f"IMMA MACs/clk/SM / {macs_per_combo} MACs per combination"},
+                                   f"IMMA MACs/clk/SM / {macs_i8} MACs per combination"},
         "k1_popc": {"kernel": f"k1_round_min<{w32},2> round g={g_top} (XOR+POPC)",
                     "achieved": k1_achieved / 1e9, "peak": popc_peak / 1e9,
                     "unit": "Gcombinations/s", "frac": k1_achieved / popc_peak,

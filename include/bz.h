@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define BZ_ABI_VERSION 2
+#define BZ_ABI_VERSION 3
 
 /* limits of the device kernels */
 #define BZ_MAX_K 128 /* rows per Gamma (prefix masks are 128-bit)      */
@@ -60,10 +60,11 @@ extern "C" {
 #define BZ_ERR_ARGUMENT 7           /* null pointer, bad shard                   */
 
 /* enumeration engines (bz_set_engine) */
-#define BZ_ENGINE_AUTO 0 /* K4 for g >= 4, K1 otherwise                     */
+#define BZ_ENGINE_AUTO 0 /* K5 for g >= 4, K1 otherwise                     */
 #define BZ_ENGINE_POPC 1 /* K1 only: XOR + POPC on the integer pipes       */
 #define BZ_ENGINE_IMMA 2 /* K3 (legacy warp-level IMMA) for g >= 4        */
 #define BZ_ENGINE_UMMA 3 /* K4 (tcgen05.mma kind::i8, TMEM) for g >= 4     */
+#define BZ_ENGINE_MXF4 4 /* K5 (tcgen05.mma kind::mxf4, unit scales) g >= 4 */
 
 typedef struct bz_ctx bz_ctx;
 
@@ -140,7 +141,7 @@ int bz_histogram(bz_ctx *ctx, int gamma, int g, int shard, int nshards,
  * (ell, k) -- for depth 3 only those with index in [sb*S, (sb+1)*S) of the
  * triple order (smallest element descending, then lex), S =
  * suffixes_per_chunk.  lanes_per_chunk: 32 (K1 warp), 256 (K3 block), 128
- * (K4 block).  depth = 3 for g >= 4 unless engine == BZ_ENGINE_POPC, else 2
+ * (K4 / K5 block).  depth = 3 for g >= 4 unless engine == BZ_ENGINE_POPC, else 2
  * for g >= 4, else 1 (g = 1: ell = -1, empty prefix). */
 int bz_plan(int m, int k, int g, int engine, int nshards, int64_t *out, int cap,
             int *out_ngroups, uint64_t *out_nchunks);
@@ -167,7 +168,9 @@ int bz_launch_count(bz_ctx *ctx, uint64_t *out);
  * IMMA (mma.sync m16n8k32) multiply-accumulates per second, out[9] = IMMA
  * MACs per clock per SM, out[10] = tcgen05.mma kind::i8 (M=128, N=256,
  * K=32, operands in shared memory, one CTA per SM) MACs per second,
- * out[11] = its MACs per clock per SM.  `out` must hold 12 doubles. */
+ * out[11] = its MACs per clock per SM, out[12] = tcgen05.mma kind::mxf4
+ * (M=128, N=240, K=64, unit block scales) MACs per second, out[13] = its
+ * MACs per clock per SM.  `out` must hold 14 doubles. */
 int bz_measure_int_peaks(bz_ctx *ctx, int w_words, double *out);
 
 #ifdef __cplusplus

@@ -18,7 +18,7 @@ from .errors import (DeviceError, InvalidArity, InvalidDimensions, MindistError,
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BZ_LIB") or os.path.join(PKG_DIR, "libbz.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 BZ_OK = 0
 _CODES = {
@@ -100,7 +100,7 @@ def device_count() -> int:
     return int(lib().bz_device_count())
 
 
-ENGINES = {"auto": 0, "popc": 1, "imma": 2, "umma": 3}
+ENGINES = {"auto": 0, "popc": 1, "imma": 2, "umma": 3, "mxf4": 4}
 
 
 def plan(m: int, k: int, g: int, engine: str = "auto", nshards: int = 1):
@@ -160,8 +160,8 @@ class Context:
         return self._h
 
     def set_engine(self, engine: str) -> None:
-        """'auto' (= 'umma': tcgen05 K4 for g >= 4), 'popc' (K1 only) or
-        'imma' (legacy-IMMA K3 for g >= 4)."""
+        """'auto' (= 'mxf4': tcgen05 kind::mxf4 K5 for g >= 4), 'umma'
+        (tcgen05 kind::i8 K4), 'imma' (legacy-IMMA K3) or 'popc' (K1 only)."""
         if engine not in ENGINES:
             raise ValueError(f"unknown engine {engine!r}")
         check(lib().bz_set_engine(self.handle, ENGINES[engine]), self.handle, "bz_set_engine")
@@ -242,12 +242,13 @@ class Context:
         return int(v[0])
 
     def measure_int_peaks(self, w_words: int) -> dict:
-        out = (c_double * 12)()
+        out = (c_double * 14)()
         check(lib().bz_measure_int_peaks(self.handle, w_words, out), self.handle,
               "bz_measure_int_peaks")
         keys = ("popc_per_s", "lop3_per_s", "sm_mhz", "sm_count", "popc_per_clk_sm",
                 "lop3_per_clk_sm", "codeword_per_s", "codeword_per_clk_sm", "imma_mac_per_s",
-                "imma_mac_per_clk_sm", "umma_mac_per_s", "umma_mac_per_clk_sm")
+                "imma_mac_per_clk_sm", "umma_mac_per_s", "umma_mac_per_clk_sm",
+                "mxf4_mac_per_s", "mxf4_mac_per_clk_sm")
         return dict(zip(keys, (float(v) for v in out)))
 
 

@@ -41,11 +41,14 @@ struct bz_ctx {
   uint32_t* d_rows = nullptr;   // m*k*wp
   uint8_t* d_trip = nullptr;    // K3 triple tables: m x trip_rows rows of 0/1 bytes
   size_t trip_rows = 0;         // rows per Gamma (C(k,3) + one tile of padding)
-  uint8_t* d_trip4 = nullptr;   // K4 triple tables (UMMA core-matrix layout)
+  uint8_t* d_trip4 = nullptr;   // K4 triple tables (UMMA core-matrix layout, s8)
   size_t trip4_rows = 0;        // rows per Gamma (C(k,3) rounded up to a tile, + a tile)
+  uint8_t* d_trip5 = nullptr;   // K5 triple tables (UMMA core-matrix layout, e2m1)
+  size_t trip5_rows = 0;
   // grow-only capacities (bytes) so repeated loads do not reallocate
-  size_t rows_cap = 0, px_cap = 0, trip_cap = 0, trip4_cap = 0;
-  bool trip_built = false, trip4_built = false;  // tables are built on first use
+  size_t rows_cap = 0, px_cap = 0, trip_cap = 0, trip4_cap = 0, trip5_cap = 0;
+  // tables are built on first use
+  bool trip_built = false, trip4_built = false, trip5_built = false;
   uint32_t* d_px = nullptr;     // m*(k+1)*wp
   unsigned long long* d_binom = nullptr;
   // per-round scratch
@@ -159,8 +162,9 @@ struct PlanShape {
 PlanShape pass_shape(int engine, int g, bool hist) {
   if (!hist && g >= 4) {
     if (engine == BZ_ENGINE_IMMA) return {3, bz::kTcThreads, bz::kTileRows, 3};
-    if (engine == BZ_ENGINE_AUTO || engine == BZ_ENGINE_UMMA)
-      return {3, bz::kUmmaM, bz::kUmmaN, 4};
+    if (engine == BZ_ENGINE_UMMA) return {3, bz::kUmmaM, bz::kUmmaN, 4};
+    if (engine == BZ_ENGINE_AUTO || engine == BZ_ENGINE_MXF4)
+      return {3, bz::kUmmaM, bz::kUmmaN4, 5};
   }
   // D = 2 needs enough (g-3)-prefixes per group to fill a warp; at g = 3
   // every group would hold one prefix, so g <= 3 keeps D = 1
@@ -177,8 +181,8 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
   const unsigned long long total = binom_sat(k, g) * (unsigned long long)(j1 - j0);
   long long lane_target = (long long)(total / (32ull * kChunksTarget));
   lane_target = std::min(kLaneMax, std::max(kLaneMin, lane_target));
-  if (shape.kernel == 4) {
-    // K4: one persistent CTA per SM walks ~16 chunks; a chunk costs a walker
+  if (shape.kernel >= 4) {
+    // K4 / K5: one persistent CTA per SM walks ~16 chunks; a chunk costs a walker
     // unrank per producer thread, so chunks are large
     lane_target = (long long)(total / ((unsigned long long)shape.lanes * 148ull * 16ull *
                                        (unsigned long long)std::max(1, nshards)));
@@ -308,15 +312,17 @@ int launch_tc(bz_ctx* ctx, const RoundArgs& a) {
   return BZ_OK;
 }
 
-template <int W>
+template <int W, bool F4>
 int launch_umma(bz_ctx* ctx, const RoundArgs& a) {
-  const size_t smem = bz::k4_smem_bytes<W>(a.m, a.k, a.ngroups);
-  CK(cudaFuncSetAttribute(bz::k4_round_umma<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  const size_t smem = bz::k4_smem_bytes<W, F4>(a.m, a.k, a.ngroups);
+  if (smem > 232448)
+    return fail(ctx, BZ_ERR_TOO_LARGE, "K%d does not fit on an SM (smem %zu)", F4 ? 5 : 4, smem);
+  CK(cudaFuncSetAttribute(bz::k4_round_umma<W, F4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)smem));
   const unsigned long long mine = (a.nchunks + a.nshards - 1 - a.shard) / a.nshards;
   long long blocks = std::max(1ll, std::min((long long)ctx->sm_count, (long long)mine));
-  bz::k4_round_umma<W><<<(unsigned)blocks, bz::kK4Threads, smem, ctx->stream>>>(
-      a, ctx->d_trip4, ctx->trip4_rows);
+  bz::k4_round_umma<W, F4><<<(unsigned)blocks, bz::K4Roles<F4>::THREADS, smem, ctx->stream>>>(
+      a, F4 ? ctx->d_trip5 : ctx->d_trip4, F4 ? ctx->trip5_rows : ctx->trip4_rows);
   CK(cudaGetLastError());
   ctx->launches += 1;
   return BZ_OK;
@@ -328,9 +334,12 @@ int build_triples_w(bz_ctx* ctx, int which) {
   if (which == 3) {
     bz::k_build_triples<W><<<grid, 256, 0, ctx->stream>>>(ctx->d_rows, ctx->d_trip, ctx->k,
                                                           ctx->trip_rows);
+  } else if (which == 4) {
+    bz::k_build_triples_umma<W, false><<<grid, 256, 0, ctx->stream>>>(
+        ctx->d_rows, ctx->d_trip4, ctx->k, ctx->trip4_rows);
   } else {
-    bz::k_build_triples_umma<W><<<grid, 256, 0, ctx->stream>>>(ctx->d_rows, ctx->d_trip4,
-                                                               ctx->k, ctx->trip4_rows);
+    bz::k_build_triples_umma<W, true><<<grid, 256, 0, ctx->stream>>>(
+        ctx->d_rows, ctx->d_trip5, ctx->k, ctx->trip5_rows);
   }
   CK(cudaGetLastError());
   ctx->launches += 1;
@@ -338,19 +347,22 @@ int build_triples_w(bz_ctx* ctx, int which) {
 }
 
 // Build (once per loaded family) the triple table kernel `which` (3: K3
-// layout, 4: K4 UMMA layout) reads.  Tables are not zero-filled: padding rows
+// layout, 4: K4 s8 UMMA layout, 5: K5 e2m1 UMMA layout) reads.  Tables are not zero-filled: padding rows
 // are only ever read into columns the kernels mask.
 int ensure_triples(bz_ctx* ctx, int which) {
-  bool& built = which == 3 ? ctx->trip_built : ctx->trip4_built;
+  bool& built = which == 3 ? ctx->trip_built : (which == 4 ? ctx->trip4_built : ctx->trip5_built);
   if (built) return BZ_OK;
   if (ctx->k < 4) return fail(ctx, BZ_ERR_STATE, "triple tables need k >= 4");
   const size_t bytes = which == 3
                            ? (size_t)ctx->m * ctx->trip_rows * bz::tc_stride(ctx->w32)
-                           : (size_t)ctx->m * ctx->trip4_rows * 32 * ctx->w32;
+                           : which == 4 ? (size_t)ctx->m * ctx->trip4_rows * 32 * ctx->w32
+                                        : (size_t)ctx->m * ctx->trip5_rows * 16 * ctx->w32;
   if (which == 3)
     CK(grow(ctx, (void**)&ctx->d_trip, &ctx->trip_cap, bytes));
-  else
+  else if (which == 4)
     CK(grow(ctx, (void**)&ctx->d_trip4, &ctx->trip4_cap, bytes));
+  else
+    CK(grow(ctx, (void**)&ctx->d_trip5, &ctx->trip5_cap, bytes));
   int rc;
   switch (ctx->w32) {
     case 1: rc = build_triples_w<1>(ctx, which); break;
@@ -370,7 +382,8 @@ int ensure_triples(bz_ctx* ctx, int which) {
 
 template <int W>
 int launch_w(bz_ctx* ctx, const RoundArgs& a, bool hist, const PlanShape& shape) {
-  if (shape.kernel == 4) return launch_umma<W>(ctx, a);
+  if (shape.kernel == 5) return launch_umma<W, true>(ctx, a);
+  if (shape.kernel == 4) return launch_umma<W, false>(ctx, a);
   if (shape.kernel == 3) return launch_tc<W>(ctx, a);
   return shape.depth == 2 ? launch_wd<W, 2>(ctx, a, hist) : launch_wd<W, 1>(ctx, a, hist);
 }
@@ -418,7 +431,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   {
     // timing experiments on K4 (results are NOT valid when set): bit 0 skips
     // the epilogue's TMEM reads, bit 1 the TMA tile loads, bit 2 the MMAs,
-    // bit 3 records a per-tile timeline of block 0
+    // bit 3 records a per-tile timeline of block 0, bit 4 skips the producers' A rows
     const char* dbg = getenv("BZ_K4_DEBUG");
     debug = dbg ? atoi(dbg) : 0;
     if (debug & 8) {
@@ -431,7 +444,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   for (int i = 0; i < count; ++i) {
     const int g = g0 + i;
     const PlanShape shape = pass_shape(ctx->engine, g, hist);
-    if (shape.kernel == 3 || shape.kernel == 4) {
+    if (shape.kernel >= 3) {
       rc = ensure_triples(ctx, shape.kernel);
       if (rc) return rc;
     }
@@ -465,6 +478,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     a.lower_prev = lower_prev ? lower_prev[i] : 0;
     a.debug = debug;
     a.trace = (i == count - 1) ? trace : nullptr;
+    a.trace_from = getenv("BZ_K4_TRACE_FROM") ? atoi(getenv("BZ_K4_TRACE_FROM")) : 0;
     todo[i].shape = shape;
     todo[i].run = nchunks > 0 && (unsigned long long)shard < nchunks;
   }
@@ -490,8 +504,8 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     std::vector<long long> h(8 * 256);
     CK(cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
     const long long t0 = h[0];
-    fprintf(stderr, "tile loader_go mma_pre mma_accok mma_go(bfull+flush) issued epi0_go epi0_rel epiL_go\n");
-    for (int t = 0; t < 48; ++t)
+    fprintf(stderr, "tile loader_go mma_pre mma_accok mma_go(bfull) issued epi0_go epi0_done epiL_go\n");
+    for (int t = 0; t < 64; ++t)
       fprintf(stderr, "%3d %8lld %8lld %8lld %8lld %8lld %8lld %8lld %8lld\n", t, h[t] - t0,
               h[1280 + t] - t0, h[1536 + t] - t0, h[256 + t] - t0, h[1024 + t] - t0,
               h[512 + t] - t0, h[768 + t] - t0, h[1792 + t] - t0);
@@ -572,6 +586,7 @@ void bz_destroy(bz_ctx* ctx) {
     cudaFree(ctx->d_px);
     cudaFree(ctx->d_trip);
     cudaFree(ctx->d_trip4);
+    cudaFree(ctx->d_trip5);
     cudaFree(ctx->d_binom);
     cudaFree(ctx->d_io);
     cudaFree(ctx->d_hist);
@@ -638,12 +653,13 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
   CK(cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
   // triple tables (K3, K4) are sized here and built lazily by the first
   // round that needs them
-  ctx->trip_built = ctx->trip4_built = false;
-  ctx->trip_rows = ctx->trip4_rows = 0;
+  ctx->trip_built = ctx->trip4_built = ctx->trip5_built = false;
+  ctx->trip_rows = ctx->trip4_rows = ctx->trip5_rows = 0;
   if (k >= 4) {
     const size_t n3 = (size_t)k * (k - 1) * (k - 2) / 6;
     ctx->trip_rows = n3 + bz::kTileRows;
     ctx->trip4_rows = (n3 + bz::kUmmaN - 1) / bz::kUmmaN * bz::kUmmaN + bz::kUmmaN;
+    ctx->trip5_rows = (n3 + bz::kUmmaN4 - 1) / bz::kUmmaN4 * bz::kUmmaN4 + bz::kUmmaN4;
   }
 
   ctx->m = m;
@@ -721,7 +737,7 @@ int bz_histogram(bz_ctx* ctx, int gamma, int g, int shard, int nshards, uint64_t
 
 int bz_set_engine(bz_ctx* ctx, int engine) {
   if (!ctx) return BZ_ERR_ARGUMENT;
-  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_UMMA)
+  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4)
     return fail(ctx, BZ_ERR_ARGUMENT, "unknown engine %d", engine);
   ctx->engine = engine;
   return BZ_OK;
@@ -736,7 +752,7 @@ int bz_plan(int m, int k, int g, int engine, int nshards, int64_t* out, int cap,
   if (binom_sat(k, g) >= (1ull << 62)) return BZ_ERR_TOO_LARGE;
   std::vector<Group> gs;
   unsigned long long nchunks = 0;
-  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_UMMA) return BZ_ERR_ARGUMENT;
+  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4) return BZ_ERR_ARGUMENT;
   if (nshards < 1) return BZ_ERR_ARGUMENT;
   int rc = build_plan(nullptr, m, k, g, -1, pass_shape(engine, g, false), nshards, gs, &nchunks);
   if (rc) return rc;
@@ -848,15 +864,23 @@ int bz_measure_int_peaks(bz_ctx* ctx, int w_words, double* out) {
     *mhz = max_clk / (ms * 1e-3) / 1e6;
     return BZ_OK;
   };
-  // tcgen05 kind::i8 M=128 x N=256 x K=32 from shared memory, one CTA per SM
-  auto run_umma = [&](double* macs_per_s, double* macs_per_clk_sm) -> int {
+  // tcgen05 kind::i8 M=128 x N=256 x K=32 (f4 = false) or kind::mxf4
+  // M=128 x N=240 x K=64 (f4 = true) from shared memory, one CTA per SM
+  auto run_umma = [&](bool f4, double* macs_per_s, double* macs_per_clk_sm) -> int {
     const int iters = 20000;
     const size_t smem = 128 * 32 + 256 * 32 + 1024;
-    CK(cudaFuncSetAttribute(bz::peak_umma_i8<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
+    if (f4)
+      CK(cudaFuncSetAttribute(bz::peak_umma_mxf4, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem));
+    else
+      CK(cudaFuncSetAttribute(bz::peak_umma_i8<256>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     for (int rep = 0; rep < 2; ++rep) {
       CK(cudaEventRecord(ctx->ev_a, ctx->stream));
-      bz::peak_umma_i8<256><<<ctx->sm_count, 128, smem, ctx->stream>>>(iters, d_clk);
+      if (f4)
+        bz::peak_umma_mxf4<<<ctx->sm_count, 128, smem, ctx->stream>>>(iters, d_clk);
+      else
+        bz::peak_umma_i8<256><<<ctx->sm_count, 128, smem, ctx->stream>>>(iters, d_clk);
       CK(cudaGetLastError());
       CK(cudaEventRecord(ctx->ev_b, ctx->stream));
       ctx->launches += 1;
@@ -867,18 +891,20 @@ int bz_measure_int_peaks(bz_ctx* ctx, int w_words, double* out) {
     CK(cudaMemcpy(clk.data(), d_clk, sizeof(long long) * ctx->sm_count, cudaMemcpyDeviceToHost));
     double max_clk = 0;
     for (int i = 0; i < ctx->sm_count; ++i) max_clk = std::max(max_clk, (double)clk[i]);
-    const double macs = (double)iters * 128.0 * 256.0 * 32.0 * ctx->sm_count;
+    const double per_mma = f4 ? 128.0 * bz::kUmmaN4 * 64.0 : 128.0 * 256.0 * 32.0;
+    const double macs = (double)iters * per_mma * ctx->sm_count;
     *macs_per_s = macs / (ms * 1e-3);
     *macs_per_clk_sm = macs / ((double)ctx->sm_count * max_clk);
     return BZ_OK;
   };
-  double umma_s = 0, umma_clk = 0;
+  double umma_s = 0, umma_clk = 0, mxf4_s = 0, mxf4_clk = 0;
   double popc_s, popc_clk, lop_s, lop_clk, cw_s, cw_clk, mma_s, mma_clk, mhz0, mhz1, mhz2, mhz3;
   int rc = run(0, 2048, &popc_s, &popc_clk, &mhz0);
   if (!rc) rc = run(1, 2048, &lop_s, &lop_clk, &mhz1);
   if (!rc) rc = run(2, 16384, &cw_s, &cw_clk, &mhz2);
   if (!rc) rc = run(3, 4096, &mma_s, &mma_clk, &mhz3);
-  if (!rc) rc = run_umma(&umma_s, &umma_clk);
+  if (!rc) rc = run_umma(false, &umma_s, &umma_clk);
+  if (!rc) rc = run_umma(true, &mxf4_s, &mxf4_clk);
   cudaFree(d_out);
   cudaFree(d_clk);
   if (rc) return rc;
@@ -894,6 +920,8 @@ int bz_measure_int_peaks(bz_ctx* ctx, int w_words, double* out) {
   out[9] = mma_clk;
   out[10] = umma_s;
   out[11] = umma_clk;
+  out[12] = mxf4_s;
+  out[13] = mxf4_clk;
   return BZ_OK;
 }
 

@@ -67,6 +67,7 @@ struct RoundArgs {
   int lower_prev;              // early exit once bound[0] <= lower_prev
   int debug;                   // K4 timing experiments only (see BZ_K4_DEBUG)
   long long* trace;            // K4 debug timeline (BZ_K4_DEBUG & 8), else null
+  int trace_from;              // first traced tile (BZ_K4_TRACE_FROM)
 };
 
 __host__ __device__ constexpr int padded_words(int w) {

@@ -1,35 +1,43 @@
-// bz_umma.cuh -- K4: the round as an integer GEMM on the Blackwell 5th-gen
-// tensor cores (tcgen05.mma kind::i8, accumulators in TMEM).
+// bz_umma.cuh -- K4 / K5: the round as a GEMM on the Blackwell 5th-gen
+// tensor cores (tcgen05.mma, accumulators in TMEM).
 //
 // Same algebra as K3 (bz_tc.cuh): w(P ^ S) = w(P) + sum_j (1 - 2 P_j) S_j,
-// prefixes P as +-1 bytes (A, M = 128 rows), triples S as 0/1 bytes (B,
-// N = 256 columns), K = the 32*W padded code columns (W MMAs of K = 32).
-// A (Gamma, ell) group is the GEMM [C(ell,g-4) prefixes] x [C(k-1-ell,3)
-// triples]; D[r][c] + w(P_r) is the weight of codeword (prefix r, triple c)
-// and only its minimum is kept.
+// prefixes P as +-1 (A, M = 128 rows), triples S as 0/1 (B, N columns), K =
+// the padded code columns.  A (Gamma, ell) group is the GEMM
+// [C(ell,g-4) prefixes] x [C(k-1-ell,3) triples]; D[r][c] + w(P_r) is the
+// weight of codeword (prefix r, triple c) and only its minimum is kept.
 //
-// One CTA per SM (persistent, static chunk striding), warp-specialised:
-//   warps 0-3  producer + epilogue: thread r owns prefix row r of the tile.
-//              It walks its prefixes (colex walker), writes its A row (+-1
-//              bytes, UMMA K-major core-matrix layout) into one of two A
-//              buffers, and later reads its row of the accumulator from TMEM
-//              (tcgen05.ld 32x32b, warp w <-> TMEM lanes 32w..32w+31) and
-//              min-reduces it.
-//   warp 4     TMEM allocator + MMA issuer (one thread): per tile W x
-//              tcgen05.mma into one of two 256-column accumulators, then
-//              tcgen05.commit to the barriers that free the B stage and
-//              publish the accumulator.
-//   warp 5     loader (one thread): 1-D TMA bulk copies (cp.async.bulk) of
-//              contiguous triple-table tiles into a ring of B stages.
-// All synchronisation is mbarrier-based; every role walks the same chunk
-// sequence, so the pipeline counters agree without extra signalling.
+//   K4  kind::i8: s8 operands (32 K per byte-pair chunk), N = 256, s32
+//       accumulators read back as packed s16 pairs.  W MMAs of K = 32.
+//   K5  kind::mxf4 with every block scale 1.0: +-1 and 0/1 are exact e2m1
+//       values, so the products and their fp32 sums are the same integers,
+//       at twice the i8 MAC rate from half the operand bytes.  N = 240
+//       (2 x 240 accumulator columns + the scale-factor columns fill TMEM),
+//       ceil(W/2) MMAs of K = 64; for odd W the last MMA reads one 16-byte
+//       chunk past the B row, which the A row's zero padding chunk cancels
+//       (every e2m1 code is finite).
 //
-// Triple table (device-built at load time): all C(k,3) row triples in the
+// One persistent CTA per SM, warp-specialised, every hand-off an mbarrier:
+//   warps [0, E)   epilogue: warp e reads TMEM lanes 32(e%4).. (its prefix
+//                  rows) of column slice e/4 of each accumulator
+//                  (tcgen05.ld), min-reduces, and releases the buffer.
+//   warp E         TMEM allocator + MMA issuer (one elected lane): per tile
+//                  the K passes into one of two accumulators, then
+//                  tcgen05.commit to the barriers that free the B stage,
+//                  publish the accumulator and (last tile) free the A tile.
+//   warp E+1       loader: draws chunks from the round's global counter,
+//                  publishes them to the other roles through a small smem
+//                  queue, and streams each chunk's triple tiles with 1-D TMA
+//                  bulk copies (cp.async.bulk) into a ring of B stages.
+//   warps E+2..+5  producers: thread r walks prefix row r (colex walker) and
+//                  writes its A row into one of two A buffers.
+//
+// Triple tables (device-built at load time): all C(k,3) row triples in the
 // K3 order (smallest element descending, then lex), stored directly in the
 // UMMA SWIZZLE_NONE K-major canonical layout -- 8-row x 16-byte core
-// matrices, the 2W 16-byte K chunks of an 8-row group contiguous -- so a
-// 256-row tile is one contiguous byte range and the TMA copy lands it in
-// exactly the layout the smem descriptor describes.
+// matrices, the K chunks of an 8-row group contiguous -- so a tile is one
+// contiguous byte range and the TMA copy lands it in exactly the layout the
+// smem descriptor describes.
 #pragma once
 
 #include "bz_tc.cuh"
@@ -43,41 +51,85 @@ constexpr int kUmmaM = 128;       // prefixes per A tile = producer threads
 #ifndef BZ_K4_MA
 #define BZ_K4_MA 1
 #endif
-#ifndef BZ_K4_HOLDBACK
-#define BZ_K4_HOLDBACK 0
-#endif
-constexpr bool kHoldBack = BZ_K4_HOLDBACK != 0;  // last MMA of a tile waits for the next tile's barriers
-constexpr int kUmmaN = BZ_K4_N;   // triples per B tile
-constexpr int kUmmaMA = BZ_K4_MA; // A tiles (consecutive prefix steps) per B tile
-// warp roles: [0, E) epilogue (TMEM lane quarter = warp % 4, column slice
-// = warp / 4), E MMA issuer + TMEM owner, E+1 TMA loader, E+2..E+5 producers
 #ifndef BZ_K4_EPI_WARPS
 #define BZ_K4_EPI_WARPS 8
 #endif
-constexpr int kK4EpiWarps = BZ_K4_EPI_WARPS;
-constexpr int kK4EpiCols = kUmmaN / (kK4EpiWarps / 4);  // columns per epilogue warp and A tile
-constexpr int kK4MmaWarp = kK4EpiWarps;
-constexpr int kK4LoadWarp = kK4EpiWarps + 1;
-constexpr int kK4ProdWarp0 = kK4EpiWarps + 2;
-constexpr int kK4Threads = 32 * (kK4EpiWarps + 6);
-constexpr int kTmemCols = 512;    // kAccBufs buffers x kUmmaMA accumulators x kUmmaN columns
-constexpr int kAccBufs = kTmemCols / (kUmmaMA * kUmmaN);  // accumulator ring depth
-constexpr int kMaxStages = 4;
-constexpr int kChunkQ = 4;         // depth of the loader -> roles chunk queue
-constexpr int kBarSlots = 4 + 2 * kMaxStages + 2 * kAccBufs + 2 * kChunkQ;
-#ifndef BZ_K4_TMA_PIECES
-#define BZ_K4_TMA_PIECES 1
+#ifndef BZ_K5_EPI_WARPS
+#define BZ_K5_EPI_WARPS 16
 #endif
-constexpr int kTmaPieces = BZ_K4_TMA_PIECES;  // parallel bulk copies per B tile
+#ifndef BZ_K5_BUFS
+#define BZ_K5_BUFS 2
+#endif
+constexpr int kUmmaN = BZ_K4_N;   // K4 triples per B tile
+constexpr int kUmmaMA = BZ_K4_MA; // K4 A tiles (consecutive prefix steps) per B tile
+constexpr int kTmemCols = 512;    // accumulators (+ K5 scale factors)
+constexpr int kSfCol = 480;       // K5 scale-factor columns [480, 512)
+constexpr int kUmmaN4 = kSfCol / BZ_K5_BUFS;  // K5 triples per B tile (240 / 120)
+constexpr int kMaxStages = 8;
+constexpr int kMaxAcc = 4;
+constexpr int kMaxABuf = 4;
+constexpr int kChunkQ = 4;         // depth of the loader -> roles chunk queue
+constexpr int kBarSlots = 2 * kMaxABuf + 2 * kMaxStages + 2 * kMaxAcc + 2 * kChunkQ;
 
-__host__ __device__ constexpr int umma_tile_bytes_b(int w) { return kUmmaN * 32 * w; }
-__host__ __device__ constexpr int umma_tile_bytes_a(int w) { return kUmmaM * 32 * w; }
-// B-tile ring depth (shared memory: S x 8 KB x W plus 2 A tiles)
-__host__ __device__ constexpr int umma_stages(int w) { return w <= 5 ? 4 : (w <= 6 ? 3 : 2); }
+// Warp roles of K4 (F4 = false) / K5 (F4 = true):
+//   [0, E)            epilogue
+//   [E, E + ACC)      MMA issuers: warp E + b owns accumulator buffer b and
+//                     issues every tile t with t % ACC == b (a second issuer
+//                     hides one issuer's barrier handshakes behind the other's
+//                     MMAs: tcgen05.mma issue stalls while the pipe is busy)
+//   E + ACC           loader
+//   E + ACC + 1 .. 4  producers (thread r <-> prefix row r)
+template <bool F4>
+struct K4Roles {
+  static constexpr int E = F4 ? BZ_K5_EPI_WARPS : BZ_K4_EPI_WARPS;
+  static constexpr int ACC = F4 ? BZ_K5_BUFS : kTmemCols / (kUmmaMA * kUmmaN);
+  static constexpr int MMA0 = E;
+  static constexpr int LOAD = E + ACC;
+  static constexpr int PROD0 = E + ACC + 1;
+  static constexpr int THREADS = 32 * (E + ACC + 5);
+  static_assert(E % 4 == 0 && ACC <= kMaxAcc, "roles");
+};
 
-// byte offset of (row, 16-byte chunk kc) in a K-major no-swizzle UMMA tile
-__host__ __device__ constexpr uint32_t umma_off(int row, int kc, int w) {
-  return (uint32_t)((row >> 3) * (2 * w * 128) + kc * 128 + (row & 7) * 16);
+template <bool F4> __host__ __device__ constexpr int k4_n() { return F4 ? kUmmaN4 : kUmmaN; }
+// bytes per table (B) row: K4 one byte per column, K5 one nibble
+template <bool F4> __host__ __device__ constexpr int k4_row_bytes(int w) { return F4 ? 16 * w : 32 * w; }
+// 16-byte K chunks per A row (K5 pads to whole K = 64 MMAs)
+template <bool F4> __host__ __device__ constexpr int k4_a_chunks(int w) {
+  return F4 ? 2 * ((w + 1) / 2) : 2 * w;
+}
+template <bool F4> __host__ __device__ constexpr int k4_passes(int w) { return k4_a_chunks<F4>(w) / 2; }
+template <bool F4> __host__ __device__ constexpr uint32_t k4_tile_b(int w) {
+  return (uint32_t)(k4_n<F4>() * k4_row_bytes<F4>(w));
+}
+template <bool F4> __host__ __device__ constexpr uint32_t k4_tile_a(int w) {
+  return (uint32_t)(kUmmaM * 16 * k4_a_chunks<F4>(w));
+}
+// A-tile ring depth (producers run that many prefix steps ahead)
+template <bool F4> __host__ __device__ constexpr int k4_abufs() { return F4 ? 4 : 2; }
+// B-tile ring depth: K5 ~150 KB of stages, K4 4 x 40 KB at W = 5
+template <bool F4> __host__ __device__ constexpr int k4_stages(int w) {
+  return F4 ? (150000 / (int)k4_tile_b<true>(w) < kMaxStages ? 150000 / (int)k4_tile_b<true>(w)
+                                                              : kMaxStages)
+            : (w <= 5 ? 4 : (w <= 6 ? 3 : 2));
+}
+
+// byte offset of (row, 16-byte chunk kc) in a K-major no-swizzle tile of
+// `chunks` chunks per row
+__host__ __device__ constexpr uint32_t umma_off_c(int row, int kc, int chunks) {
+  return (uint32_t)((row >> 3) * (chunks * 128) + kc * 128 + (row & 7) * 16);
+}
+
+// K5 operand encoding of one 32-bit code word into 16 bytes = 32 e2m1
+// nibbles, as 4 words: nibble q of word j holds bit 4q + j (a fixed K
+// permutation, the same on both operands, so dot products are unchanged).
+// B: 0 / 1.0 (0x2); A: +1.0 (0x2) for a 0 bit, -1.0 (0xA) for a 1 bit.
+__host__ __device__ __forceinline__ uint4 e2m1_bits01(uint32_t v) {
+  return make_uint4((v << 1) & 0x22222222u, v & 0x22222222u, (v >> 1) & 0x22222222u,
+                    (v >> 2) & 0x22222222u);
+}
+__host__ __device__ __forceinline__ uint4 e2m1_pm1(uint32_t v) {
+  return make_uint4(((v << 3) & 0x88888888u) | 0x22222222u, ((v << 2) & 0x88888888u) | 0x22222222u,
+                    ((v << 1) & 0x88888888u) | 0x22222222u, (v & 0x88888888u) | 0x22222222u);
 }
 
 // tcgen05 shared-memory matrix descriptor, SWIZZLE_NONE, K-major:
@@ -96,6 +148,10 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 constexpr uint32_t kUmmaIdesc = (2u << 4) | (1u << 7) | (1u << 10) |
                                 ((uint32_t)(kUmmaN >> 3) << 17) |
                                 ((uint32_t)(kUmmaM >> 4) << 24);
+// block-scaled: A = B = e2m1 (format 1), K-major, N, scale type ue8m0
+// (bit 23), M, K = 64 (bit 31 clear), scale-factor ids 0
+constexpr uint32_t kMxf4Idesc = (1u << 7) | (1u << 10) | ((uint32_t)(kUmmaN4 >> 3) << 17) |
+                                (1u << 23) | ((uint32_t)(kUmmaM >> 4) << 24);
 
 // ---- mbarrier / TMA / tcgen05 primitives
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -170,6 +226,58 @@ __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t a_desc, uint64
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// D (f32) [+]= A . B with per-32-K block scales read from TMEM (sfa, sfb)
+__device__ __forceinline__ void umma_mxf4(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate, uint32_t sfa,
+                                          uint32_t sfb) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], "
+      "p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
+      : "memory");
+}
+__device__ __forceinline__ float fmin3f(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, uint32_t v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(v)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                 "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_regs4_after_wait(uint32_t* v) {
+  asm volatile("" : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]) : : "memory");
+}
+__device__ __forceinline__ void tmem_regs8_after_wait(uint32_t* v) {
+  asm volatile(""
+               : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]),
+                 "+r"(v[6]), "+r"(v[7])
+               :
+               : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    bar)
@@ -222,20 +330,41 @@ __device__ __forceinline__ void tmem_regs_after_wait(uint32_t* v) {
                : "memory");
 }
 
+// C consecutive 32-bit columns of this warp's 32 TMEM lanes into v[0, C)
+// (C a multiple of 4, at most 128): x32 / x16 / x8 / x4 loads, no wait.
+template <int C>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t* v) {
+  if constexpr (C >= 32) {
+    tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(v));
+    tmem_ld_cols<C - 32>(taddr + 32, v + 32);
+  } else if constexpr (C >= 16) {
+    tmem_ld16(taddr, v);
+    tmem_ld_cols<C - 16>(taddr + 16, v + 16);
+  } else if constexpr (C >= 8) {
+    tmem_ld8(taddr, *reinterpret_cast<uint32_t(*)[8]>(v));
+    tmem_ld_cols<C - 8>(taddr + 8, v + 8);
+  } else if constexpr (C >= 4) {
+    tmem_ld4(taddr, v);
+  }
+}
+
 // ---------------------------------------------------------------------------
-// Triple table in UMMA layout: one block per (Gamma, a).
-template <int W>
+// Triple tables, one block per (Gamma, a).  K4: 0/1 bytes (kind::i8), 2W
+// 16-byte K chunks per row.  K5: e2m1 nibbles 0x0 / 0x2 (kind::mxf4), W
+// 16-byte chunks per row (chunk w = code word w: 32 columns).
+template <int W, bool F4>
 __global__ void k_build_triples_umma(const uint32_t* __restrict__ rows,
                                      uint8_t* __restrict__ trip, int k,
                                      size_t gamma_stride_rows) {
   constexpr int WP = padded_words(W);
+  constexpr int RB = k4_row_bytes<F4>(W);  // bytes per table row
   const int j = blockIdx.y, a = blockIdx.x;
   if (a > k - 3) return;
   const uint32_t* R = rows + (size_t)j * k * WP;
   const long long base = (long long)(k - 1 - a) * (k - 2 - a) * (k - 3 - a) / 6;
   const int span = k - 1 - a;
   const int npairs = span * (span - 1) / 2;
-  uint8_t* out = trip + (size_t)j * gamma_stride_rows * 32 * W;
+  uint8_t* out = trip + (size_t)j * gamma_stride_rows * RB;
   for (int t = threadIdx.x; t < npairs * W; t += blockDim.x) {
     const int pi = t / W, w = t - pi * W;
     int b = a + 1, rem = pi;
@@ -243,25 +372,36 @@ __global__ void k_build_triples_umma(const uint32_t* __restrict__ rows,
     const int c = b + 1 + rem;
     const uint32_t v = R[a * WP + w] ^ R[b * WP + w] ^ R[c * WP + w];
     const long long row = base + pi;
-    // 32 bytes of word w = K chunks 2w and 2w+1 of this row
-    uint8_t* tile = out + (size_t)(row >> 3) * (2 * W * 128);
-    uint4 lo, hi;
-    lo.x = bit_nibble(v, 0);  lo.y = bit_nibble(v, 4);  lo.z = bit_nibble(v, 8);  lo.w = bit_nibble(v, 12);
-    hi.x = bit_nibble(v, 16); hi.y = bit_nibble(v, 20); hi.z = bit_nibble(v, 24); hi.w = bit_nibble(v, 28);
-    *reinterpret_cast<uint4*>(tile + (2 * w) * 128 + (row & 7) * 16) = lo;
-    *reinterpret_cast<uint4*>(tile + (2 * w + 1) * 128 + (row & 7) * 16) = hi;
+    uint8_t* grp = out + (size_t)(row >> 3) * (8 * RB);
+    if constexpr (F4) {
+      *reinterpret_cast<uint4*>(grp + w * 128 + (row & 7) * 16) = e2m1_bits01(v);
+    } else {
+      // 32 bytes of word w = K chunks 2w and 2w+1 of this row
+      uint4 lo, hi;
+      lo.x = bit_nibble(v, 0);  lo.y = bit_nibble(v, 4);  lo.z = bit_nibble(v, 8);  lo.w = bit_nibble(v, 12);
+      hi.x = bit_nibble(v, 16); hi.y = bit_nibble(v, 20); hi.z = bit_nibble(v, 24); hi.w = bit_nibble(v, 28);
+      *reinterpret_cast<uint4*>(grp + (2 * w) * 128 + (row & 7) * 16) = lo;
+      *reinterpret_cast<uint4*>(grp + (2 * w + 1) * 128 + (row & 7) * 16) = hi;
+    }
   }
 }
 
-template <int W>
+template <int W, bool F4>
 __host__ __device__ inline size_t k4_smem_bytes(int m, int k, int ngroups) {
   size_t off = (smem_base_bytes<W>(m, k, ngroups) + 1023) & ~size_t(1023);
-  off += (size_t)umma_stages(W) * umma_tile_bytes_b(W);
-  off += 2 * (size_t)kUmmaMA * umma_tile_bytes_a(W);
+  off += (size_t)k4_stages<F4>(W) * k4_tile_b<F4>(W);
+  off += (size_t)k4_abufs<F4>() * kUmmaMA * k4_tile_a<F4>(W);
   off += kBarSlots * 8 + 16;     // barriers + TMEM base
-  off += 2 * kUmmaMA * kUmmaM * sizeof(int);  // prefix weights of the A buffers
+  off += k4_abufs<F4>() * kUmmaMA * kUmmaM * sizeof(int);  // prefix weights of the A buffers
   off += kChunkQ * sizeof(long long) + 16;    // chunk queue
   return off;
+}
+
+// debug timeline (BZ_K4_DEBUG & 8): block 0, tiles [trace_from, +256)
+__device__ __forceinline__ void k4_trace(const RoundArgs& a, int slot, uint32_t tile) {
+  if (!a.trace || blockIdx.x != 0) return;
+  const uint32_t i = tile - (uint32_t)a.trace_from;
+  if (i < 256) a.trace[slot * 256 + i] = clock64();
 }
 
 // Decoded chunk: identical on every role.
@@ -272,6 +412,7 @@ struct K4Chunk {
   int slice, tile_lo, tile_hi;
 };
 
+template <int N>
 __device__ __forceinline__ K4Chunk k4_decode(const Group* sg, int ngroups,
                                              unsigned long long chunk, int k) {
   K4Chunk c;
@@ -284,28 +425,44 @@ __device__ __forceinline__ K4Chunk k4_decode(const Group* sg, int ngroups,
   c.maxcnt = bleft < (unsigned long long)c.gr.ppl ? (long long)bleft : c.gr.ppl;
   const long long t = k - 1 - c.gr.ell;
   c.slice = (int)(t * (t - 1) * (t - 2) / 6);
-  const int ntiles = (c.slice + kUmmaN - 1) / kUmmaN;
+  const int ntiles = (c.slice + N - 1) / N;
   c.tile_lo = tb * c.gr.tpc;
   c.tile_hi = min(ntiles, c.tile_lo + c.gr.tpc);
   return c;
 }
 
-template <int W>
-__global__ void __launch_bounds__(kK4Threads, 1)
+// K4 (F4 = false, tcgen05.mma kind::i8) and K5 (F4 = true, kind::mxf4 with
+// unit block scales): one persistent CTA per SM, warp-specialised (see the
+// file comment).  The two differ only in operand encoding, MMA kind,
+// accumulator type (s32 read as packed s16 / f32) and tile geometry.
+template <int W, bool F4>
+__global__ void __launch_bounds__(K4Roles<F4>::THREADS, 1)
 k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_stride_rows) {
-  constexpr int WP = padded_words(W);
-  constexpr int S = umma_stages(W);
-  constexpr uint32_t TB = umma_tile_bytes_b(W);
-  constexpr uint32_t TA = umma_tile_bytes_a(W);
+  static_assert(!F4 || kUmmaMA == 1, "K5 runs one A tile per B tile");
+  constexpr int N = k4_n<F4>();
+  constexpr int S = k4_stages<F4>(W);
+  constexpr int P = k4_passes<F4>(W);        // MMAs per tile (K = 32 bytes each)
+  constexpr int CA = k4_a_chunks<F4>(W);     // 16-byte K chunks per A row
+  constexpr int CB = k4_row_bytes<F4>(W) / 16;  // ... per B row
+  constexpr uint32_t TB = k4_tile_b<F4>(W);
+  constexpr uint32_t TA = k4_tile_a<F4>(W);
+  using RL = K4Roles<F4>;
+  constexpr int ACC = RL::ACC;
+  constexpr int E = RL::E;
+  constexpr int EC = N / (E / 4);  // columns per epilogue warp and A tile
+  constexpr uint32_t IDESC = F4 ? kMxf4Idesc : kUmmaIdesc;
+  static_assert(S <= kMaxStages, "barrier slots");
+  static_assert(EC * (E / 4) == N && (F4 ? EC % 4 == 0 && EC <= 128 : EC % 32 == 0), "epilogue");
   extern __shared__ __align__(128) unsigned char smem[];
   const size_t base = (smem_base_bytes<W>(a.m, a.k, a.ngroups) + 1023) & ~size_t(1023);
   unsigned char* sB = smem + base;
   unsigned char* sA = sB + S * TB;
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(sA + 2 * kUmmaMA * TA);
+  constexpr int NA = k4_abufs<F4>();
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(sA + NA * kUmmaMA * TA);
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + kBarSlots);
   int* s_wt = reinterpret_cast<int*>(s_tmem + 4);  // [2][kUmmaMA][kUmmaM] prefix weights
   volatile long long* s_q = reinterpret_cast<volatile long long*>(
-      (reinterpret_cast<uintptr_t>(s_wt + 2 * kUmmaMA * kUmmaM) + 15) & ~uintptr_t(15));
+      (reinterpret_cast<uintptr_t>(s_wt + NA * kUmmaMA * kUmmaM) + 15) & ~uintptr_t(15));
   const uint32_t sB_s = (uint32_t)__cvta_generic_to_shared(sB);
   const uint32_t sA_s = (uint32_t)__cvta_generic_to_shared(sA);
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
@@ -313,38 +470,39 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   // accumulators (MMA commit -> epilogue: accfull; epilogue -> MMA:
   // accempty), A buffers (producers -> MMA, epilogue: afull; MMA commit +
   // epilogue -> producers: aempty).
+  constexpr uint32_t B0 = 2 * kMaxABuf;  // first B-stage barrier slot
   auto afull = [&](int i) { return bar_s + 8u * (0 + i); };
-  auto aempty = [&](int i) { return bar_s + 8u * (2 + i); };
-  auto bfull = [&](int i) { return bar_s + 8u * (4 + i); };
-  auto bempty = [&](int i) { return bar_s + 8u * (4 + kMaxStages + i); };
-  auto accfull = [&](int i) { return bar_s + 8u * (4 + 2 * kMaxStages + i); };
-  auto accempty = [&](int i) { return bar_s + 8u * (4 + 2 * kMaxStages + kAccBufs + i); };
+  auto aempty = [&](int i) { return bar_s + 8u * (kMaxABuf + i); };
+  auto bfull = [&](int i) { return bar_s + 8u * (B0 + i); };
+  auto bempty = [&](int i) { return bar_s + 8u * (B0 + kMaxStages + i); };
+  auto accfull = [&](int i) { return bar_s + 8u * (B0 + 2 * kMaxStages + i); };
+  auto accempty = [&](int i) { return bar_s + 8u * (B0 + 2 * kMaxStages + kMaxAcc + i); };
   // chunk queue: the loader draws chunks from the round's global counter
   // (dynamic balance across CTAs) and publishes them to every other role
-  auto qfull = [&](int i) { return bar_s + 8u * (4 + 2 * kMaxStages + 2 * kAccBufs + i); };
+  auto qfull = [&](int i) { return bar_s + 8u * (B0 + 2 * kMaxStages + 2 * kMaxAcc + i); };
   auto qempty = [&](int i) {
-    return bar_s + 8u * (4 + 2 * kMaxStages + 2 * kAccBufs + kChunkQ + i);
+    return bar_s + 8u * (B0 + 2 * kMaxStages + 2 * kMaxAcc + kChunkQ + i);
   };
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     for (int i = 0; i < S; ++i) { mbar_init(bfull(i), 1); mbar_init(bempty(i), 1); }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NA; ++i) {
       mbar_init(afull(i), kUmmaM);               // every producer thread
-      mbar_init(aempty(i), 1 + kK4EpiWarps);     // MMA commit + each epilogue warp
+      mbar_init(aempty(i), ACC + E);             // each MMA warp's commit + epilogue warp
     }
-    for (int i = 0; i < kAccBufs; ++i) {
+    for (int i = 0; i < ACC; ++i) {
       mbar_init(accfull(i), 1);                  // MMA commit
-      mbar_init(accempty(i), kK4EpiWarps);       // each epilogue warp
+      mbar_init(accempty(i), E);                 // each epilogue warp
     }
     for (int i = 0; i < kChunkQ; ++i) {
       mbar_init(qfull(i), 1);                    // loader
-      mbar_init(qempty(i), kK4EpiWarps + 5);     // epilogue, producer and MMA warps
+      mbar_init(qempty(i), E + ACC + 4);         // epilogue, MMA and producer warps
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async();
   }
-  if (warp == kK4MmaWarp) {
+  if (warp == RL::MMA0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(s_tmem)),
                  "r"(kTmemCols));
@@ -356,12 +514,30 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   stage<W>(a, srows, spx, sgroups, smem);  // ends with __syncthreads
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
+  if constexpr (F4) {
+    // unit block scales (ue8m0 0x7F = 2^0) in TMEM columns [kSfCol, 512);
+    // the zero K-padding chunk of both A buffers (odd W)
+    if (warp < 4) {
+      for (int c = 0; c < 512 - kSfCol; c += 8)
+        tmem_st8(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(kSfCol + c), 0x7F7F7F7Fu);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    if (CA > W && warp >= RL::PROD0) {
+      const int r = tid - 32 * RL::PROD0;
+      for (int ab = 0; ab < NA; ++ab)
+        *reinterpret_cast<uint4*>(sA + ab * TA + umma_off_c(r, W, CA)) = make_uint4(0, 0, 0, 0);
+      fence_proxy_async();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+  }
   const int k = a.k, q = a.g - 4;
   const unsigned FULL = 0xffffffffu;
 
-  if (warp < kK4EpiWarps) {
+  if (warp < E) {
     // ================= epilogue: warp e reads TMEM lanes 32(e%4).. (rows),
-    // columns [kK4EpiCols*(e/4), +kK4EpiCols) of each accumulator
+    // columns [EC*(e/4), +EC) of each accumulator
     const int quarter = warp & 3, slice_id = warp >> 2;
     const int r = 32 * quarter + lane;
     uint32_t grp = 0, tcount = 0;
@@ -373,11 +549,11 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
       if (lane == 0) mbar_arrive(qempty(qs));
       if (qchunk < 0) break;
       const unsigned long long chunk = (unsigned long long)qchunk;
-      const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
+      const K4Chunk c = k4_decode<N>(sgroups, a.ngroups, chunk, k);
       int best = INT_MAX;
       for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
-        const int ab = grp & 1;
-        mbar_wait(afull(ab), (grp >> 1) & 1);
+        const int ab = grp % NA;
+        mbar_wait(afull(ab), (grp / NA) & 1);
         int wt[kUmmaMA];
 #pragma unroll
         for (int j = 0; j < kUmmaMA; ++j) wt[j] = s_wt[(ab * kUmmaMA + j) * kUmmaM + r];
@@ -386,57 +562,90 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
         int rmin[kUmmaMA];
 #pragma unroll
         for (int j = 0; j < kUmmaMA; ++j) rmin[j] = INT_MAX / 2;
+        float fmin_acc = __int_as_float(0x7f800000);  // K5: +inf
         for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount) {
-          const int buf = tcount % kAccBufs;
-          mbar_wait(accfull(buf), (tcount / kAccBufs) & 1);
+          const int buf = tcount % ACC;
+          mbar_wait(accfull(buf), (tcount / ACC) & 1);
           tc_fence_after();
-          if (a.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && tcount < 256)
-            a.trace[2 * 256 + tcount] = clock64();
-          if (a.trace && blockIdx.x == 0 && warp == kK4EpiWarps - 1 && lane == 0 && tcount < 256)
-            a.trace[7 * 256 + tcount] = clock64();
-          const int lim = min(kUmmaN, c.slice - t * kUmmaN) - kK4EpiCols * slice_id;
+          if (warp == 0 && lane == 0) k4_trace(a, 2, tcount);
+          if (warp == E - 1 && lane == 0) k4_trace(a, 7, tcount);
+          const int lim = min(N, c.slice - t * N) - EC * slice_id;
           const uint32_t tb = tmem + ((uint32_t)(32 * quarter) << 16) +
-                              (uint32_t)(buf * kUmmaMA * kUmmaN + kK4EpiCols * slice_id);
-          // kK4EpiCols columns as packed s16 pairs: 3-input SIMD minima
-          constexpr int NP = kK4EpiCols / 2;
-          uint32_t v[kUmmaMA][NP];
+                              (uint32_t)(buf * kUmmaMA * N + EC * slice_id);
           if (a.debug & 1) {
             __syncwarp();
             if (lane == 0) mbar_arrive(accempty(buf));
             continue;
           }
+          if constexpr (F4) {
+            // EC f32 accumulators: every load, one wait, release the buffer,
+            // then 3-input float minima
+            uint32_t v[EC];
+            tmem_ld_cols<EC>(tb, v);
+            tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < kUmmaMA; ++j)
+            for (int i = 0; i < EC; i += 4) tmem_regs4_after_wait(v + i);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(accempty(buf));  // accumulators are in registers
+            if (lim < EC) {
 #pragma unroll
-            for (int cc = 0; cc < kK4EpiCols / 32; ++cc)
-              tmem_ld16p(tb + j * kUmmaN + 32 * cc, &v[j][16 * cc]);
-          tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < kUmmaMA; ++j)
-#pragma unroll
-            for (int cc = 0; cc < kK4EpiCols / 32; ++cc) tmem_regs16_after_wait(&v[j][16 * cc]);
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(accempty(buf));  // accumulators are in registers
-          if (a.trace && blockIdx.x == 0 && warp == 0 && lane == 0 && tcount < 256)
-            a.trace[3 * 256 + tcount] = clock64();
-#pragma unroll
-          for (int j = 0; j < kUmmaMA; ++j) {
-            if (lim < kK4EpiCols) {
-#pragma unroll
-              for (int i = 0; i < NP; ++i) {
-                if (2 * i >= lim) v[j][i] = (v[j][i] & 0xffff0000u) | 0x00007fffu;
-                if (2 * i + 1 >= lim) v[j][i] = (v[j][i] & 0x0000ffffu) | 0x7fff0000u;
-              }
+              for (int i = 0; i < EC; ++i)
+                if (i >= lim) v[i] = 0x7f800000u;
             }
-            // packed s16 pairs: 3-input SIMD minima down to one register
-            uint32_t m = __vimin3_s16x2(v[j][0], v[j][1], v[j][2]);
+            // four independent 3-input chains, then combine
+            float m0 = fmin_acc, m1 = __uint_as_float(v[0]), m2 = __uint_as_float(v[1]),
+                  m3 = __uint_as_float(v[2]);
 #pragma unroll
-            for (int i = 3; i + 1 < NP; i += 2) m = __vimin3_s16x2(m, v[j][i], v[j][i + 1]);
-            if (NP % 2 == 0) m = __vmins2(m, v[j][NP - 1]);
-            const int lo = (int)(short)(m & 0xffffu), hi = (int)(short)(m >> 16);
-            rmin[j] = min(rmin[j], min(lo, hi));
+            for (int i = 3; i + 7 < EC; i += 8) {
+              m0 = fmin3f(m0, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+              m1 = fmin3f(m1, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+              m2 = fmin3f(m2, __uint_as_float(v[i + 4]), __uint_as_float(v[i + 5]));
+              m3 = fmin3f(m3, __uint_as_float(v[i + 6]), __uint_as_float(v[i + 7]));
+            }
+#pragma unroll
+            for (int i = 3 + ((EC - 3) / 8) * 8; i < EC; ++i) m0 = fminf(m0, __uint_as_float(v[i]));
+            fmin_acc = fmin3f(fminf(m0, m1), m2, m3);
+          } else {
+            // EC columns as packed s16 pairs: 3-input SIMD minima
+            constexpr int NP = EC / 2;
+            uint32_t v[kUmmaMA][NP];
+#pragma unroll
+            for (int j = 0; j < kUmmaMA; ++j)
+#pragma unroll
+              for (int cc = 0; cc < EC / 32; ++cc)
+                tmem_ld16p(tb + j * N + 32 * cc, &v[j][16 * cc]);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < kUmmaMA; ++j)
+#pragma unroll
+              for (int cc = 0; cc < EC / 32; ++cc) tmem_regs16_after_wait(&v[j][16 * cc]);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(accempty(buf));  // accumulators are in registers
+#pragma unroll
+            for (int j = 0; j < kUmmaMA; ++j) {
+              if (lim < EC) {
+#pragma unroll
+                for (int i = 0; i < NP; ++i) {
+                  if (2 * i >= lim) v[j][i] = (v[j][i] & 0xffff0000u) | 0x00007fffu;
+                  if (2 * i + 1 >= lim) v[j][i] = (v[j][i] & 0x0000ffffu) | 0x7fff0000u;
+                }
+              }
+              uint32_t m = __vimin3_s16x2(v[j][0], v[j][1], v[j][2]);
+#pragma unroll
+              for (int i = 3; i + 1 < NP; i += 2) m = __vimin3_s16x2(m, v[j][i], v[j][i + 1]);
+              if (NP % 2 == 0) m = __vmins2(m, v[j][NP - 1]);
+              const int lo = (int)(short)(m & 0xffffu), hi = (int)(short)(m >> 16);
+              rmin[j] = min(rmin[j], min(lo, hi));
+            }
           }
+          if (warp == 0 && lane == 0) k4_trace(a, 3, tcount);
+        }
+        if constexpr (F4) {
+          // |D| <= n, so a finite minimum converts exactly; +inf (every
+          // column of this slice masked) stays out of the way
+          if (fmin_acc < 1.0e6f) rmin[0] = (int)fmin_acc;
         }
 #pragma unroll
         for (int j = 0; j < kUmmaMA; ++j) best = min(best, rmin[j] + wt[j]);
@@ -448,9 +657,9 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
         if (wbest < vb[0]) atomicMin(a.bound, wbest);
       }
     }
-  } else if (warp >= kK4ProdWarp0) {
+  } else if (warp >= RL::PROD0) {
     // ================= producers: thread r walks prefix row r
-    const int r = tid - 32 * kK4ProdWarp0;
+    const int r = tid - 32 * RL::PROD0;
     uint32_t grp = 0;
     for (uint32_t qi = 0;; ++qi) {
       const int qs = qi % kChunkQ;
@@ -460,38 +669,44 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
       if (lane == 0) mbar_arrive(qempty(qs));
       if (qchunk < 0) break;
       const unsigned long long chunk = (unsigned long long)qchunk;
-      const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
+      const K4Chunk c = k4_decode<N>(sgroups, a.ngroups, chunk, k);
       const unsigned long long first = c.bfirst + (unsigned long long)r * c.gr.ppl;
       long long cnt = 0;
       if (first < c.gr.nprefix) {
         const unsigned long long left = c.gr.nprefix - first;
         cnt = left < (unsigned long long)c.gr.ppl ? (long long)left : c.gr.ppl;
       }
-      const uint32_t* R = srows + c.gr.gamma * k * WP;
+      const uint32_t* R = srows + c.gr.gamma * k * padded_words(W);
       const uint32_t* PX = spx + c.gr.gamma * (k + 1) * px_stride(W);
       Walker<W> wk;
       // rows without prefixes duplicate the block's first prefix
       wk.init(cnt > 0 ? first : c.bfirst, q, c.gr.ell, R, a.binom);
       for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
-        const int ab = grp & 1;
-        mbar_wait(aempty(ab), ((grp >> 1) & 1) ^ 1);
+        const int ab = grp % NA;
+        mbar_wait(aempty(ab), ((grp / NA) & 1) ^ 1);
 #pragma unroll 1
         for (int j = 0; j < kUmmaMA; ++j) {
           // step j of the group; past this row's range the last prefix repeats
           if (p + j > 0 && p + j < cnt) wk.step(PX);
           unsigned char* dst = sA + (ab * kUmmaMA + j) * TA;
           int wt = 0;
+          if (a.debug & 16) continue;  // timing experiment: no A rows
 #pragma unroll
           for (int jj = 0; jj < W; ++jj) {
-            uint4 lo, hi;
             const uint32_t v = wk.acc[jj];
             wt += __popc(v);
-            lo.x = pm1_nibble(v, 0);  lo.y = pm1_nibble(v, 4);
-            lo.z = pm1_nibble(v, 8);  lo.w = pm1_nibble(v, 12);
-            hi.x = pm1_nibble(v, 16); hi.y = pm1_nibble(v, 20);
-            hi.z = pm1_nibble(v, 24); hi.w = pm1_nibble(v, 28);
-            *reinterpret_cast<uint4*>(dst + umma_off(r, 2 * jj, W)) = lo;
-            *reinterpret_cast<uint4*>(dst + umma_off(r, 2 * jj + 1, W)) = hi;
+            if constexpr (F4) {
+              // e2m1 +1 (0x2) for a 0 bit, -1 (0xA) for a 1 bit
+              *reinterpret_cast<uint4*>(dst + umma_off_c(r, jj, CA)) = e2m1_pm1(v);
+            } else {
+              uint4 lo, hi;
+              lo.x = pm1_nibble(v, 0);  lo.y = pm1_nibble(v, 4);
+              lo.z = pm1_nibble(v, 8);  lo.w = pm1_nibble(v, 12);
+              hi.x = pm1_nibble(v, 16); hi.y = pm1_nibble(v, 20);
+              hi.z = pm1_nibble(v, 24); hi.w = pm1_nibble(v, 28);
+              *reinterpret_cast<uint4*>(dst + umma_off_c(r, 2 * jj, CA)) = lo;
+              *reinterpret_cast<uint4*>(dst + umma_off_c(r, 2 * jj + 1, CA)) = hi;
+            }
           }
           s_wt[(ab * kUmmaMA + j) * kUmmaM + r] = wt;
         }
@@ -501,38 +716,22 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
       // visited combinations of this chunk
       const unsigned tot = __reduce_add_sync(FULL, (unsigned)cnt);
       if (lane == 0 && tot) {
-        const long long cols = min((long long)c.tile_hi * kUmmaN, (long long)c.slice) -
-                               (long long)c.tile_lo * kUmmaN;
+        const long long cols = min((long long)c.tile_hi * N, (long long)c.slice) -
+                               (long long)c.tile_lo * N;
         atomicAdd(a.combos + c.gr.gamma, (unsigned long long)tot * (unsigned long long)cols);
       }
     }
-  } else if (warp == kK4MmaWarp) {
-    // ================= MMA issuer
-    // tcgen05.mma issue blocks while the tensor pipe is busy, so the waits
-    // for tile t+1 are placed *before* the last MMA of tile t: the pipe then
-    // still holds queued work while this thread does its barrier handshakes.
-    // the whole warp runs the loop (warp-uniform values stay in uniform
-    // registers); one elected lane issues the MMAs and commits
+  } else if (warp < RL::LOAD) {
+    // ================= MMA issuers: warp MMA0 + mb owns accumulator buffer
+    // mb.  The whole warp runs the loop (warp-uniform values stay in uniform
+    // registers); one elected lane issues the MMAs and commits.
+    const int mb = warp - RL::MMA0;
     {
-      const uint64_t a_desc0 = umma_desc(sA_s, 128, 2 * W * 128);
-      const uint64_t b_desc0 = umma_desc(sB_s, 128, 2 * W * 128);
-      uint32_t grp = 0, tcount = 0, bcount = 0;
-      // the held-back last MMA of the previous tile and its commits
-      bool pend = false;
-      uint32_t pd = 0, pstg = 0, pbuf = 0, pab = 0;
-      uint64_t pad = 0, pbd = 0;
-      bool pend_group_end = false;
-      auto flush = [&]() {
-        if (!pend) return;
-        if (elect_one()) {
-          if (!(a.debug & 4)) umma_i8(pd, pad, pbd, kUmmaIdesc, W > 1 ? 1u : 0u);
-          umma_commit(bempty(pstg));
-          umma_commit(accfull(pbuf));
-          if (pend_group_end) umma_commit(aempty(pab));
-        }
-        __syncwarp();
-        pend = false;
-      };
+      const uint64_t a_desc0 = umma_desc(sA_s, 128, CA * 128);
+      const uint64_t b_desc0 = umma_desc(sB_s, 128, CB * 128);
+      const uint32_t sfa = tmem + kSfCol, sfb = tmem + kSfCol + 8;
+      const uint32_t dbase = tmem + (uint32_t)(mb * kUmmaMA * N);
+      uint32_t grp = 0, tcount = 0;
       for (uint32_t qi = 0;; ++qi) {
         const int qs = qi % kChunkQ;
         mbar_wait_fast(qfull(qs), (qi / kChunkQ) & 1);
@@ -541,66 +740,59 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
         if (lane == 0) mbar_arrive(qempty(qs));
         if (qchunk < 0) break;
         const unsigned long long chunk = (unsigned long long)qchunk;
-        const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
+        const K4Chunk c = k4_decode<N>(sgroups, a.ngroups, chunk, k);
+        const int ntile = c.tile_hi - c.tile_lo;
         for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
-          const int ab = grp & 1;
-          mbar_wait_fast(afull(ab), (grp >> 1) & 1);
-          for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount, ++bcount) {
-            const int stg = bcount % S;
-            const int buf = tcount % kAccBufs;
-            if (a.trace && blockIdx.x == 0 && lane == 0 && tcount < 256)
-              a.trace[5 * 256 + tcount] = clock64();
-            mbar_wait_fast(accempty(buf), ((tcount / kAccBufs) & 1) ^ 1);
-            if (a.trace && blockIdx.x == 0 && lane == 0 && tcount < 256)
-              a.trace[6 * 256 + tcount] = clock64();
-            mbar_wait_fast(bfull(stg), (bcount / S) & 1);
+          const int ab = grp % NA;
+          // first tile of this step that falls to this issuer
+          // (every issuer waits for every step, so no issuer's arrivals run
+          // ahead into a later phase of the A-buffer barriers)
+          const int t0 = (int)((mb - (int)(tcount % ACC) + ACC) % ACC);
+          mbar_wait_fast(afull(ab), (grp / NA) & 1);
+          for (int i = t0; i < ntile; i += ACC) {
+            const uint32_t tc = tcount + (uint32_t)i;  // global tile number
+            const int stg = (int)(tc % S);
+            // the B stage is normally long loaded: wait for it first, so the
+            // accumulator hand-back (the critical loop) is the last wait
+            // before the MMAs
+            if (lane == 0) k4_trace(a, 5, tc);
+            mbar_wait_fast(bfull(stg), (tc / S) & 1);
+            if (lane == 0) k4_trace(a, 6, tc);
+            mbar_wait_fast(accempty(mb), ((tc / ACC) & 1) ^ 1);
             tc_fence_after();
-            flush();  // previous tile's last MMA + commits
-            if (a.trace && blockIdx.x == 0 && lane == 0 && tcount < 256)
-              a.trace[1 * 256 + tcount] = clock64();
-            // K step kb advances both start addresses by 256 B (16 in the
-            // 16-byte-granular address field)
+            if (lane == 0) k4_trace(a, 1, tc);
+            // pass kb advances both start addresses by 32 bytes of K per
+            // row = two core matrices = 256 B (16 in the 16-byte-granular
+            // address field)
             const uint64_t bd0 = b_desc0 + (uint64_t)(stg * (TB >> 4));
-            if (!(a.debug & 4)) {
-              if (elect_one()) {
+            if (elect_one()) {
+              if (!(a.debug & 4)) {
 #pragma unroll
                 for (int j = 0; j < kUmmaMA; ++j) {
-                  const uint32_t dj = tmem + (uint32_t)((buf * kUmmaMA + j) * kUmmaN);
+                  const uint32_t dj = dbase + (uint32_t)(j * N);
                   const uint64_t adj = a_desc0 + (uint64_t)((ab * kUmmaMA + j) * (TA >> 4));
 #pragma unroll
-                  for (int kb = 0; kb < W; ++kb) {
-                    if (kHoldBack && j == kUmmaMA - 1 && kb == W - 1) break;  // held back
-                    umma_i8(dj, adj + 16u * kb, bd0 + 16u * kb, kUmmaIdesc, kb > 0 ? 1u : 0u);
+                  for (int kb = 0; kb < P; ++kb) {
+                    if constexpr (F4)
+                      umma_mxf4(dj, adj + 16u * kb, bd0 + 16u * kb, IDESC, kb > 0 ? 1u : 0u,
+                                sfa, sfb);
+                    else
+                      umma_i8(dj, adj + 16u * kb, bd0 + 16u * kb, IDESC, kb > 0 ? 1u : 0u);
                   }
                 }
               }
-              __syncwarp();
+              umma_commit(bempty(stg));
+              umma_commit(accfull(mb));
             }
-            const uint32_t d = tmem + (uint32_t)((buf * kUmmaMA + kUmmaMA - 1) * kUmmaN);
-            const uint64_t ad0 = a_desc0 + (uint64_t)((ab * kUmmaMA + kUmmaMA - 1) * (TA >> 4));
-            pend = true;
-            if (!kHoldBack) {  // everything issued: commit right away
-              if (elect_one()) {
-                umma_commit(bempty(stg));
-                umma_commit(accfull(buf));
-                if (t + 1 == c.tile_hi) umma_commit(aempty(ab));
-              }
-              __syncwarp();
-              pend = false;
-            }
-            pd = d;
-            pad = ad0 + 16u * (W - 1);
-            pbd = bd0 + 16u * (W - 1);
-            pstg = stg;
-            pbuf = buf;
-            pab = ab;
-            pend_group_end = (t + 1 == c.tile_hi);
-            if (a.trace && blockIdx.x == 0 && lane == 0 && tcount < 256)
-              a.trace[4 * 256 + tcount] = clock64();
+            __syncwarp();
+            if (lane == 0) k4_trace(a, 4, tc);
           }
+          // the A buffer is free once every issuer's MMAs on it completed
+          if (elect_one()) umma_commit(aempty(ab));
+          __syncwarp();
+          tcount += (uint32_t)ntile;
         }
       }
-      flush();
     }
     __syncwarp();
   } else {
@@ -619,31 +811,22 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
         mbar_arrive(qfull(qs));
         if (qchunk < 0) break;
         const unsigned long long chunk = (unsigned long long)qchunk;
-        const K4Chunk c = k4_decode(sgroups, a.ngroups, chunk, k);
-        const uint8_t* tsrc = trip + (size_t)c.gr.gamma * gamma_stride_rows * 32 * W;
+        const K4Chunk c = k4_decode<N>(sgroups, a.ngroups, chunk, k);
+        const uint8_t* tsrc = trip + (size_t)c.gr.gamma * gamma_stride_rows * (CB * 16);
         for (long long p = 0; p < c.maxcnt; p += kUmmaMA) {
           for (int t = c.tile_lo; t < c.tile_hi; ++t, ++bcount) {
             const int stg = bcount % S;
             mbar_wait(bempty(stg), ((bcount / S) & 1) ^ 1);
-            if (a.trace && blockIdx.x == 0 && bcount < 256) a.trace[0 * 256 + bcount] = clock64();
+            k4_trace(a, 0, bcount);
             // only the rows this tile needs (8-row granularity); the rest of
             // the stage keeps stale rows whose columns the epilogue masks
-            const int valid = min(kUmmaN, c.slice - t * kUmmaN);
-            const uint32_t bytes = (uint32_t)((valid + 7) / 8) * (2 * W * 128);
+            const int valid = min(N, c.slice - t * N);
+            const uint32_t bytes = (uint32_t)((valid + 7) / 8) * (CB * 128);
             if (a.debug & 2) {
               mbar_arrive(bfull(stg));
             } else {
               mbar_arrive_tx(bfull(stg), bytes);
-              // a few bulk copies in flight per tile (one per 8-row groups
-              // slice) keep more of the L2->SMEM path busy
-              const uint32_t groups8 = (uint32_t)((valid + 7) / 8);
-              const uint32_t per = (groups8 + kTmaPieces - 1) / kTmaPieces;
-              for (uint32_t g0 = 0; g0 < groups8; g0 += per) {
-                const uint32_t gn = min(per, groups8 - g0);
-                const uint32_t off = g0 * (2 * W * 128);
-                tma_load_1d(sB_s + stg * TB + off, tsrc + (size_t)t * TB + off,
-                            gn * (2 * W * 128), bfull(stg));
-              }
+              tma_load_1d(sB_s + stg * TB, tsrc + (size_t)t * TB, bytes, bfull(stg));
             }
           }
         }
@@ -654,7 +837,7 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
 
   tc_fence_before();
   __syncthreads();
-  if (warp == kK4MmaWarp) {
+  if (warp == RL::MMA0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
                  "r"(kTmemCols));
@@ -700,6 +883,55 @@ __global__ void __launch_bounds__(128, 1) peak_umma_i8(int iters, long long* clk
     mbar_wait(bar_s, 0);
     t1 = clock64();
     clk[blockIdx.x] = t1 - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// tcgen05 kind::mxf4 throughput probe (roofline denominator of K5): one CTA
+// per SM issues `iters` back-to-back M=128 x N=240 x K=64 block-scaled MMAs
+// (unit scales in TMEM) alternating between the two accumulators.
+__global__ void __launch_bounds__(128, 1) peak_umma_mxf4(int iters, long long* clk) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) unsigned long long bar;
+  __shared__ uint32_t s_tmem;
+  const int warp = threadIdx.x >> 5;
+  const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(&bar);
+  if (threadIdx.x == 0) {
+    mbar_init(bar_s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&s_tmem)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = s_tmem;
+  for (int c = 0; c < 512 - kSfCol; c += 8)
+    tmem_st8(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(kSfCol + c), 0x7F7F7F7Fu);
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem);
+  if (threadIdx.x == 0) {
+    const uint64_t ad = umma_desc(base, 128, 256);
+    const uint64_t bd = umma_desc(base + 128 * 32, 128, 256);
+    const long long t0 = clock64();
+    for (int i = 0; i < iters; ++i)
+      umma_mxf4(tmem + (uint32_t)((i & 1) * kUmmaN4), ad, bd, kMxf4Idesc, (i & 2) ? 1u : 0u,
+                tmem + kSfCol, tmem + kSfCol + 8);
+    umma_commit(bar_s);
+    mbar_wait(bar_s, 0);
+    clk[blockIdx.x] = clock64() - t0;
   }
   tc_fence_before();
   __syncthreads();

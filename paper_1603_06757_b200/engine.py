@@ -88,7 +88,7 @@ class EngineConfig:
     # one batch (one launch sequence, one synchronisation; replicated, not
     # sharded, across ranks); 0 disables batching
     batch_combinations: int = 2_000_000_000
-    engine: str = "auto"     # "auto" | "popc" | "imma" (kernel choice; same results)
+    engine: str = "auto"     # "auto" | "mxf4" | "umma" | "imma" | "popc" (kernel; same results)
 
 
 @dataclass

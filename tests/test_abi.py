@@ -37,7 +37,7 @@ def test_header_symbols_exported():
     assert L.bz_abi_version() == _native.ABI_VERSION
 
 
-@pytest.mark.parametrize("engine", ["auto", "popc", "imma", "umma"])
+@pytest.mark.parametrize("engine", ["auto", "popc", "imma", "umma", "mxf4"])
 def test_plan_counts(engine):
     for (m, k, g) in [(1, 5, 1), (2, 24, 3), (2, 80, 8), (3, 40, 8), (1, 64, 6), (2, 128, 4)]:
         groups, nchunks = _native.plan(m, k, g, engine)
@@ -55,7 +55,7 @@ def test_plan_counts(engine):
             assert combos == nprefix * comb(k - 1 - ell, depth)
 
 
-@pytest.mark.parametrize("engine", ["auto", "popc", "imma"])
+@pytest.mark.parametrize("engine", ["auto", "popc", "imma", "umma", "mxf4"])
 @pytest.mark.parametrize("m,k,g", [(1, 6, 1), (1, 7, 2), (2, 9, 3), (1, 12, 5),
                                    (2, 10, 10), (1, 40, 3), (1, 34, 4), (1, 20, 6)])
 def test_plan_partitions_rank_space(m, k, g, engine):

@@ -27,7 +27,7 @@ def ctx():
     return _native.context(0)
 
 
-@pytest.fixture(params=["popc", "imma", "umma"])
+@pytest.fixture(params=["popc", "imma", "umma", "mxf4"])
 def engine(request):
     """Every kernel: K1 (XOR+POPC), K3 (legacy IMMA, g >= 4) and K4
     (tcgen05 + TMEM, g >= 4)."""

@@ -1,7 +1,7 @@
 """One enumeration launch for ncu: the dominant round (g = 8) of the cfg5
 workload, or any (config, g) given on the command line.
 
-    python tools/profile_round.py [config] [g] [--hist]
+    python tools/profile_round.py [config] [g] [--hist] [--engine=NAME]
 """
 
 from __future__ import annotations
@@ -22,6 +22,9 @@ def main():
     name = args[0] if args else "cfg5"
     g = int(args[1]) if len(args) > 1 else 8
     ctx = _native.context(0)
+    for a in sys.argv[1:]:
+        if a.startswith("--engine="):
+            ctx.set_engine(a.split("=", 1)[1])
     if name == "cfg4":
         gm = microbench_gamma(1)
         ctx.load(family_words([gm], 192), 192)
