@@ -128,21 +128,24 @@ int bz_histogram(bz_ctx *ctx, int gamma, int g, int shard, int nshards,
                  uint64_t *out_hist, int32_t *out_min, uint64_t *out_combos);
 
 /* Host-only: the work plan bz_round uses for (m, k, g, nshards), for inspection and
- * for the CPU tests of the sharding logic.  Writes *out_ngroups groups of 10
+ * for the CPU tests of the sharding logic.  Writes *out_ngroups groups of 11
  * int64 each -- chunk_begin, nprefix, gamma, ell, prefixes_per_lane,
- * combinations, depth, lanes_per_chunk, suffixes_per_chunk, suffix_blocks --
- * into out (capacity `cap` groups; out may be NULL to query the count) and
- * the round's chunk count into *out_nchunks.  Chunk c of the round belongs
- * to shard c % nshards.  Within group (gamma, ell), local chunk index
- * c_local = pb * suffix_blocks + sb: lane l (0 <= l < lanes_per_chunk: 32
- * for a warp of K1, 256 for a block of K3) walks the colex ranks
- * [(pb*lanes + l)*ppl, +ppl) of the (g-1-depth)-subsets of [0, ell), each
- * extended by ell and then by every depth-subset of the suffix rows
- * (ell, k) -- for depth 3 only those with index in [sb*S, (sb+1)*S) of the
- * triple order (smallest element descending, then lex), S =
- * suffixes_per_chunk.  lanes_per_chunk: 32 (K1 warp), 256 (K3 block), 128
- * (K4 / K5 block).  depth = 3 for g >= 4 unless engine == BZ_ENGINE_POPC, else 2
- * for g >= 4, else 1 (g = 1: ell = -1, empty prefix). */
+ * combinations, depth, lanes_per_chunk, suffixes_per_chunk, suffix_blocks,
+ * suffix_floor -- into out (capacity `cap` groups; out may be NULL to query
+ * the count) and the round's chunk count into *out_nchunks.  Chunk c of the
+ * round belongs to shard c % nshards.  Within group (gamma, ell, depth),
+ * local chunk index c_local = pb * suffix_blocks + sb: lane l (0 <= l <
+ * lanes_per_chunk: 32 for a warp of K1, 256 for a block of K3, 128 for K4 /
+ * K5) walks the colex ranks [(pb*lanes + l)*ppl, +ppl) of the
+ * (g-1-depth)-subsets of [0, ell), each extended by ell and then by every
+ * depth-subset of the suffix rows [suffix_floor, k) -- for depth >= 3 only
+ * those with index in [sb*S, (sb+1)*S) of the table order (smallest element
+ * descending, then the rest lex), S = suffixes_per_chunk.  suffix_floor is
+ * ell + 1 except in K5's deeper levels (depth 4, 5), which take the
+ * combinations whose top `depth` elements all lie in rows >= a level floor.
+ * depth = 3..5 (K5) or 3 (K3, K4) for g >= 4 unless engine ==
+ * BZ_ENGINE_POPC, else 2 for g >= 4, else 1 (g = 1: ell = -1, empty
+ * prefix). */
 int bz_plan(int m, int k, int g, int engine, int nshards, int64_t *out, int cap,
             int *out_ngroups, uint64_t *out_nchunks);
 

@@ -238,7 +238,7 @@ def enumerate_chunks(gammas: list[list[int]], k: int, g: int, groups, nchunks: i
     """Visit every combination of the chunks owned by `shard` exactly as the
     device kernel does (chunk c -> shard c % nshards; lane-major prefix
     ranges of ppl colex ranks of (g-1-depth)-subsets of [0, ell), plus ell;
-    then every depth-subset of the suffix rows (ell, k)).  Returns
+    then every depth-subset of the suffix rows [suffix_floor, k)).  Returns
     (per-gamma minima, per-gamma combos, list of visited combos)."""
     m = len(gammas)
     mins = [None] * m
@@ -247,12 +247,12 @@ def enumerate_chunks(gammas: list[list[int]], k: int, g: int, groups, nchunks: i
     starts = [gr[0] for gr in groups]
     for chunk in range(shard, nchunks, nshards):
         gi = max(i for i, s in enumerate(starts) if s <= chunk)
-        begin, nprefix, gamma, ell, ppl, _, depth, lanes, spc, nsb = groups[gi]
+        begin, nprefix, gamma, ell, ppl, _, depth, lanes, spc, nsb, sfloor = groups[gi]
         local = chunk - begin
         pb, sb = divmod(local, nsb)
         rows = gammas[gamma]
-        sufs = suffix_order(ell, k, depth)
-        if depth == 3:
+        sufs = suffix_order(ell, k, depth, sfloor)
+        if depth >= 3:
             sufs = sufs[sb * spc:(sb + 1) * spc]
         for lane in range(lanes):
             first = (pb * lanes + lane) * ppl
@@ -272,14 +272,16 @@ def enumerate_chunks(gammas: list[list[int]], k: int, g: int, groups, nchunks: i
     return mins, cnt, seen
 
 
-def suffix_order(ell: int, k: int, depth: int):
-    """Suffixes above ell in device order: lex for depth 1-2; for depth 3
-    the triple-table order (smallest element descending, then (b, c) lex)."""
+def suffix_order(ell: int, k: int, depth: int, floor: int | None = None):
+    """Suffixes of rows >= floor (default ell + 1) in device order: lex for
+    depth 1-2; for depth >= 3 the table order (smallest element descending,
+    then the other depth-1 elements lex)."""
+    lo = ell + 1 if floor is None else floor
     if depth < 3:
-        return list(itertools.combinations(range(ell + 1, k), depth))
+        return list(itertools.combinations(range(lo, k), depth))
     out = []
-    for a in range(k - 3, ell, -1):
-        out += [(a, b, c) for b, c in itertools.combinations(range(a + 1, k), 2)]
+    for a in range(k - depth, lo - 1, -1):
+        out += [(a,) + rest for rest in itertools.combinations(range(a + 1, k), depth - 1)]
     return out
 
 

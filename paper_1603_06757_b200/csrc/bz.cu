@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -43,12 +44,17 @@ struct bz_ctx {
   size_t trip_rows = 0;         // rows per Gamma (C(k,3) + one tile of padding)
   uint8_t* d_trip4 = nullptr;   // K4 triple tables (UMMA core-matrix layout, s8)
   size_t trip4_rows = 0;        // rows per Gamma (C(k,3) rounded up to a tile, + a tile)
-  uint8_t* d_trip5 = nullptr;   // K5 triple tables (UMMA core-matrix layout, e2m1)
-  size_t trip5_rows = 0;
+  // K5 suffix tables, level D = 3 + i (UMMA core-matrix layout, e2m1):
+  // all D-subsets of rows >= lvl_floor[i] (-1: not built), lvl_rows[i] rows
+  // per Gamma
+  uint8_t* d_lvl[3] = {nullptr, nullptr, nullptr};
+  size_t lvl_cap[3] = {0, 0, 0};
+  size_t lvl_rows[3] = {0, 0, 0};
+  int lvl_floor[3] = {-1, -1, -1};
   // grow-only capacities (bytes) so repeated loads do not reallocate
-  size_t rows_cap = 0, px_cap = 0, trip_cap = 0, trip4_cap = 0, trip5_cap = 0;
+  size_t rows_cap = 0, px_cap = 0, trip_cap = 0, trip4_cap = 0;
   // tables are built on first use
-  bool trip_built = false, trip4_built = false, trip5_built = false;
+  bool trip_built = false, trip4_built = false;
   uint32_t* d_px = nullptr;     // m*(k+1)*wp
   unsigned long long* d_binom = nullptr;
   // per-round scratch
@@ -68,7 +74,7 @@ namespace {
 // problem size, so every process computes the same plan.
 constexpr long long kChunksTarget = 40000;
 constexpr long long kLaneMin = 32, kLaneMax = 4096;
-constexpr int kPlanCols = 10;  // int64 columns per group in bz_plan
+constexpr int kPlanCols = 11;  // int64 columns per group in bz_plan
 
 int fail(bz_ctx* c, int code, const char* fmt, ...) {
   char buf[512];
@@ -123,7 +129,7 @@ IoSlot io_layout(int m, int k) {
   l.off_combos = 8;
   l.off_bound = l.off_combos + 8 * (size_t)m;
   l.off_groups = (l.off_bound + 4 * (size_t)(m + 1) + 15) & ~size_t(15);
-  const size_t max_groups = (size_t)m * (size_t)(k + 2) + 1;
+  const size_t max_groups = (size_t)m * (size_t)(3 * k + 6) + 1;  // K5: up to 3 levels
   l.size = (l.off_groups + sizeof(Group) * max_groups + 255) & ~size_t(255);
   return l;
 }
@@ -171,9 +177,88 @@ PlanShape pass_shape(int engine, int g, bool hist) {
   return {g >= 4 ? 2 : 1, 32, 0, 1};
 }
 
+// K5 suffix levels.  Level D (3..5) owns the combinations whose top D
+// elements all lie in rows >= floor[D] and whose (D+1)-th largest element
+// ell is below floor[D+1]; its groups are (ell, D) with prefixes = the
+// (g-1-D)-subsets of [0, ell) plus ell, and suffixes = the D-subsets of
+// rows >= max(ell + 1, floor[D]) -- a prefix of that level's table (all
+// D-subsets of rows >= floor[D], smallest element descending).  Deeper
+// levels turn the many one-tile prefix steps of the small slices near
+// ell = k - 4 into few steps over large slices; the floors are chosen by a
+// cost model fitted to K5 (clocks per tile and per prefix step), with every
+// table capped at kLevelRowCap rows per Gamma.
+constexpr int kMaxLevel = 5;
+constexpr unsigned long long kLevelRowCap = 1ull << 20;
+
+struct Levels {
+  int dmax = 3;                  // deepest level (3: plain triples)
+  int floor[kMaxLevel + 2] = {}; // floor[D] for D in 3..dmax; floor[dmax+1] = k
+};
+
+double k5_cost(int k, int g, const Levels& lv) {
+  const double kTile = 727.0, kStep = 1271.0;  // K5 clocks (cfg5, B200)
+  double cost = 0;
+  for (int D = 3; D <= lv.dmax; ++D) {
+    const int hi = std::min(lv.floor[D + 1] - 1, k - 1 - D);
+    for (int ell = g - 1 - D; ell <= hi; ++ell) {
+      const double np = (double)binom_sat(ell, g - 1 - D);
+      const int f = std::max(ell + 1, lv.floor[D]);
+      const double slice = (double)binom_sat(k - f, D);
+      if (np == 0 || slice == 0) continue;
+      const double steps = std::ceil(np / bz::kUmmaM);
+      cost += steps * (std::ceil(slice / bz::kUmmaN4) * kTile + kStep);
+    }
+  }
+  return cost;
+}
+
+Levels k5_levels(int k, int g) {
+  Levels best;
+  best.floor[3] = 0;
+  best.floor[4] = k;
+  if (g < 5) return best;  // a level-D prefix needs g - 1 - D >= 0
+  if (const char* env = getenv("BZ_K5_FLOORS")) {
+    // test hook: force the level floors "t1[,t2]" (clamped to valid ranges)
+    int t1 = k, t2 = k;
+    if (sscanf(env, "%d,%d", &t1, &t2) >= 1 && t1 >= 0 && t1 <= k - 4) {
+      best.dmax = 4;
+      best.floor[4] = t1;
+      best.floor[5] = k;
+      if (g >= 6 && t2 > t1 && t2 <= k - 5) {
+        best.dmax = 5;
+        best.floor[5] = t2;
+        best.floor[6] = k;
+      }
+    }
+    return best;
+  }
+  double best_cost = k5_cost(k, g, best);
+  // one extra level (D = 4), then optionally D = 5 above it
+  for (int t1 = 1; t1 <= k - 4; ++t1) {
+    if (binom_sat(k - t1, 4) > kLevelRowCap) continue;
+    Levels lv;
+    lv.dmax = 4;
+    lv.floor[3] = 0;
+    lv.floor[4] = t1;
+    lv.floor[5] = k;
+    const double c4 = k5_cost(k, g, lv);
+    if (c4 < best_cost) { best_cost = c4; best = lv; }
+    if (g < 6) continue;
+    for (int t2 = t1 + 1; t2 <= k - 5; ++t2) {
+      if (binom_sat(k - t2, 5) > kLevelRowCap) continue;
+      Levels l5 = lv;
+      l5.dmax = 5;
+      l5.floor[5] = t2;
+      l5.floor[6] = k;
+      const double c5 = k5_cost(k, g, l5);
+      if (c5 < best_cost) { best_cost = c5; best = l5; }
+    }
+  }
+  return best;
+}
+
 int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape, int nshards,
                std::vector<Group>& gs, unsigned long long* out_nchunks) {
-  const int depth = shape.depth;
   gs.clear();
   unsigned long long chunk = 0;
   const int j0 = gamma_only < 0 ? 0 : gamma_only;
@@ -188,45 +273,60 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
                                        (unsigned long long)std::max(1, nshards)));
     lane_target = std::min(1ll << 20, std::max(4096ll, lane_target));
   }
+  // suffix levels: K5 may split the round over depths 3..5, every other
+  // kernel runs one depth with floor ell + 1
+  Levels lv;
+  lv.dmax = shape.depth;
+  lv.floor[shape.depth] = 0;
+  lv.floor[shape.depth + 1] = k;
+  if (shape.kernel == 5) lv = k5_levels(k, g);
+  const int dmin = shape.depth;
   for (int j = j0; j < j1; ++j) {
-    const int ell_lo = g == 1 ? -1 : g - 1 - depth;
-    const int ell_hi = g == 1 ? -1 : k - 1 - depth;
-    for (int ell = ell_lo; ell <= ell_hi; ++ell) {
-      const unsigned long long np = g == 1 ? 1ull : binom_sat(ell, g - 1 - depth);
-      if (np == 0) continue;
-      if (np >= (1ull << 62))
-        return fail(ctx, BZ_ERR_TOO_LARGE, "C(%d,%d) prefixes exceed 2^62", ell, g - 1 - depth);
-      const long long work = (long long)binom_sat(k - 1 - ell, depth);
-      const long long lanes_ll = shape.lanes;
-      const long long spread = (long long)((np + lanes_ll - 1) / lanes_ll);
-      // D = 3: every prefix step also rebuilds the A operand and streams at
-      // least one whole tile, which bounds chunk duration for the tiny
-      // slices near ell = k - 4
-      const long long step_cost = depth == 3 ? std::max(work, (long long)shape.tile_rows) + 256 : work;
-      long long ppl = std::max(1ll, lane_target / std::max(1ll, step_cost));
-      ppl = std::min(ppl, std::max(1ll, spread));
-      // D = 3: a chunk is 256 prefixes x ppl steps x tpc tiles of 64
-      // triples; a slice too large for one chunk is split into tile blocks
-      const long long trows = depth == 3 ? shape.tile_rows : 1;
-      long long ntiles = (work + trows - 1) / trows;
-      long long tpc = ntiles;
-      if (depth == 3 && work > lane_target)
-        tpc = std::max(1ll, lane_target / trows);
-      const long long ntb = depth == 3 ? (ntiles + tpc - 1) / tpc : 1;
-      Group gr{};
-      gr.chunk_begin = chunk;
-      gr.nprefix = np;
-      gr.gamma = j;
-      gr.ell = ell;
-      gr.ppl = (int)ppl;
-      gr.depth = depth;
-      gr.tpc = (int)tpc;
-      gr.ntb = (int)ntb;
-      gr.lanes = shape.lanes;
-      gr.tile_rows = shape.tile_rows;
-      const unsigned long long per_chunk = (unsigned long long)lanes_ll * (unsigned long long)ppl;
-      chunk += (np + per_chunk - 1) / per_chunk * (unsigned long long)ntb;
-      gs.push_back(gr);
+    for (int depth = dmin; depth <= lv.dmax; ++depth) {
+      const int ell_lo = g == 1 ? -1 : g - 1 - depth;
+      const int ell_hi = g == 1 ? -1 : std::min(k - 1 - depth, lv.floor[depth + 1] - 1);
+      for (int ell = ell_lo; ell <= ell_hi; ++ell) {
+        const unsigned long long np = g == 1 ? 1ull : binom_sat(ell, g - 1 - depth);
+        if (np == 0) continue;
+        if (np >= (1ull << 62))
+          return fail(ctx, BZ_ERR_TOO_LARGE, "C(%d,%d) prefixes exceed 2^62", ell, g - 1 - depth);
+        const int sfloor = std::max(ell + 1, lv.floor[depth]);
+        const long long work = (long long)binom_sat(k - sfloor, depth);
+        if (work == 0) continue;
+        const bool tiled = depth >= 3;
+        const long long lanes_ll = shape.lanes;
+        const long long spread = (long long)((np + lanes_ll - 1) / lanes_ll);
+        // D >= 3: every prefix step also rebuilds the A operand and streams
+        // at least one whole tile, which bounds chunk duration for the tiny
+        // slices near ell = k - 4
+        const long long step_cost =
+            tiled ? std::max(work, (long long)shape.tile_rows) + 256 : work;
+        long long ppl = std::max(1ll, lane_target / std::max(1ll, step_cost));
+        ppl = std::min(ppl, std::max(1ll, spread));
+        // D >= 3: a chunk is lanes prefixes x ppl steps x tpc tiles; a slice
+        // too large for one chunk is split into tile blocks
+        const long long trows = tiled ? shape.tile_rows : 1;
+        long long ntiles = (work + trows - 1) / trows;
+        long long tpc = ntiles;
+        if (tiled && work > lane_target) tpc = std::max(1ll, lane_target / trows);
+        const long long ntb = tiled ? (ntiles + tpc - 1) / tpc : 1;
+        Group gr{};
+        gr.chunk_begin = chunk;
+        gr.nprefix = np;
+        gr.gamma = j;
+        gr.ell = ell;
+        gr.ppl = (int)ppl;
+        gr.depth = depth;
+        gr.tpc = (int)tpc;
+        gr.ntb = (int)ntb;
+        gr.lanes = shape.lanes;
+        gr.tile_rows = shape.tile_rows;
+        gr.slice = (int)work;
+        gr.sfloor = sfloor;
+        const unsigned long long per_chunk = (unsigned long long)lanes_ll * (unsigned long long)ppl;
+        chunk += (np + per_chunk - 1) / per_chunk * (unsigned long long)ntb;
+        gs.push_back(gr);
+      }
     }
   }
   *out_nchunks = chunk;
@@ -321,8 +421,18 @@ int launch_umma(bz_ctx* ctx, const RoundArgs& a) {
                           (int)smem));
   const unsigned long long mine = (a.nchunks + a.nshards - 1 - a.shard) / a.nshards;
   long long blocks = std::max(1ll, std::min((long long)ctx->sm_count, (long long)mine));
+  bz::K4Tables tabs{};
+  if (F4) {
+    for (int i = 0; i < 3; ++i) {
+      tabs.t[i] = ctx->d_lvl[i];
+      tabs.stride_rows[i] = ctx->lvl_rows[i];
+    }
+  } else {
+    tabs.t[0] = ctx->d_trip4;
+    tabs.stride_rows[0] = ctx->trip4_rows;
+  }
   bz::k4_round_umma<W, F4><<<(unsigned)blocks, bz::K4Roles<F4>::THREADS, smem, ctx->stream>>>(
-      a, F4 ? ctx->d_trip5 : ctx->d_trip4, F4 ? ctx->trip5_rows : ctx->trip4_rows);
+      a, tabs);
   CK(cudaGetLastError());
   ctx->launches += 1;
   return BZ_OK;
@@ -334,35 +444,69 @@ int build_triples_w(bz_ctx* ctx, int which) {
   if (which == 3) {
     bz::k_build_triples<W><<<grid, 256, 0, ctx->stream>>>(ctx->d_rows, ctx->d_trip, ctx->k,
                                                           ctx->trip_rows);
-  } else if (which == 4) {
+  } else {
     bz::k_build_triples_umma<W, false><<<grid, 256, 0, ctx->stream>>>(
         ctx->d_rows, ctx->d_trip4, ctx->k, ctx->trip4_rows);
-  } else {
-    bz::k_build_triples_umma<W, true><<<grid, 256, 0, ctx->stream>>>(
-        ctx->d_rows, ctx->d_trip5, ctx->k, ctx->trip5_rows);
   }
   CK(cudaGetLastError());
   ctx->launches += 1;
   return BZ_OK;
 }
 
+template <int W>
+int build_level_w(bz_ctx* ctx, int D, int floor) {
+  dim3 grid(ctx->k - D - floor + 1, ctx->m);
+  bz::k_build_subsets_mxf4<W><<<grid, 256, 0, ctx->stream>>>(
+      ctx->d_rows, ctx->d_lvl[D - 3], ctx->k, D, floor, ctx->lvl_rows[D - 3], ctx->d_binom);
+  CK(cudaGetLastError());
+  ctx->launches += 1;
+  return BZ_OK;
+}
+
+// K5 suffix table of level D covering every D-subset of rows >= floor
+// (grow-only: a table built for a lower floor already holds these subsets
+// as its first rows).  Not zero-filled: padding rows are only ever read into
+// columns the kernel masks.
+int ensure_level(bz_ctx* ctx, int D, int floor) {
+  const int i = D - 3;
+  if (ctx->lvl_floor[i] >= 0 && ctx->lvl_floor[i] <= floor) return BZ_OK;
+  if (ctx->k - floor < D) return BZ_OK;  // no subsets: nothing reads it
+  const size_t n = (size_t)binom_sat(ctx->k - floor, D);
+  const size_t N = bz::kUmmaN4;
+  ctx->lvl_rows[i] = (n + N - 1) / N * N + N;
+  const size_t bytes = (size_t)ctx->m * ctx->lvl_rows[i] * 16 * ctx->w32;
+  CK(grow(ctx, (void**)&ctx->d_lvl[i], &ctx->lvl_cap[i], bytes));
+  int rc;
+  switch (ctx->w32) {
+    case 1: rc = build_level_w<1>(ctx, D, floor); break;
+    case 2: rc = build_level_w<2>(ctx, D, floor); break;
+    case 3: rc = build_level_w<3>(ctx, D, floor); break;
+    case 4: rc = build_level_w<4>(ctx, D, floor); break;
+    case 5: rc = build_level_w<5>(ctx, D, floor); break;
+    case 6: rc = build_level_w<6>(ctx, D, floor); break;
+    case 7: rc = build_level_w<7>(ctx, D, floor); break;
+    case 8: rc = build_level_w<8>(ctx, D, floor); break;
+    default: return fail(ctx, BZ_ERR_TOO_LARGE, "unsupported word count %d", ctx->w32);
+  }
+  if (rc) return rc;
+  ctx->lvl_floor[i] = floor;
+  return BZ_OK;
+}
+
 // Build (once per loaded family) the triple table kernel `which` (3: K3
-// layout, 4: K4 s8 UMMA layout, 5: K5 e2m1 UMMA layout) reads.  Tables are not zero-filled: padding rows
-// are only ever read into columns the kernels mask.
+// layout, 4: K4 s8 UMMA layout) reads.  Tables are not zero-filled: padding
+// rows are only ever read into columns the kernels mask.
 int ensure_triples(bz_ctx* ctx, int which) {
-  bool& built = which == 3 ? ctx->trip_built : (which == 4 ? ctx->trip4_built : ctx->trip5_built);
+  bool& built = which == 3 ? ctx->trip_built : ctx->trip4_built;
   if (built) return BZ_OK;
   if (ctx->k < 4) return fail(ctx, BZ_ERR_STATE, "triple tables need k >= 4");
   const size_t bytes = which == 3
                            ? (size_t)ctx->m * ctx->trip_rows * bz::tc_stride(ctx->w32)
-                           : which == 4 ? (size_t)ctx->m * ctx->trip4_rows * 32 * ctx->w32
-                                        : (size_t)ctx->m * ctx->trip5_rows * 16 * ctx->w32;
+                           : (size_t)ctx->m * ctx->trip4_rows * 32 * ctx->w32;
   if (which == 3)
     CK(grow(ctx, (void**)&ctx->d_trip, &ctx->trip_cap, bytes));
-  else if (which == 4)
-    CK(grow(ctx, (void**)&ctx->d_trip4, &ctx->trip4_cap, bytes));
   else
-    CK(grow(ctx, (void**)&ctx->d_trip5, &ctx->trip5_cap, bytes));
+    CK(grow(ctx, (void**)&ctx->d_trip4, &ctx->trip4_cap, bytes));
   int rc;
   switch (ctx->w32) {
     case 1: rc = build_triples_w<1>(ctx, which); break;
@@ -427,24 +571,31 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   };
   std::vector<Pending> todo(count);
   long long* trace = nullptr;
+  long long* ctrace = nullptr;
   int debug = 0;
   {
     // timing experiments on K4 (results are NOT valid when set): bit 0 skips
     // the epilogue's TMEM reads, bit 1 the TMA tile loads, bit 2 the MMAs,
-    // bit 3 records a per-tile timeline of block 0, bit 4 skips the producers' A rows
+    // bit 3 records a per-tile timeline of block 0, bit 4 skips the producers' A rows, bit 5 records per-chunk times
     const char* dbg = getenv("BZ_K4_DEBUG");
     debug = dbg ? atoi(dbg) : 0;
     if (debug & 8) {
       static long long* d_trace = nullptr;
-      if (!d_trace) CK(cudaMalloc(&d_trace, 8 * 256 * sizeof(long long)));
-      CK(cudaMemsetAsync(d_trace, 0, 8 * 256 * sizeof(long long), ctx->stream));
+      if (!d_trace) CK(cudaMalloc(&d_trace, 16 * 256 * sizeof(long long)));
+      CK(cudaMemsetAsync(d_trace, 0, 16 * 256 * sizeof(long long), ctx->stream));
       trace = d_trace;
+    }
+    if (debug & 32) {
+      static long long* d_ct = nullptr;
+      if (!d_ct) CK(cudaMalloc(&d_ct, 1024 * 64 * 4 * sizeof(long long)));
+      CK(cudaMemsetAsync(d_ct, 0xff, 1024 * 64 * 4 * sizeof(long long), ctx->stream));
+      ctrace = d_ct;
     }
   }
   for (int i = 0; i < count; ++i) {
     const int g = g0 + i;
     const PlanShape shape = pass_shape(ctx->engine, g, hist);
-    if (shape.kernel >= 3) {
+    if (shape.kernel == 3 || shape.kernel == 4) {
       rc = ensure_triples(ctx, shape.kernel);
       if (rc) return rc;
     }
@@ -452,6 +603,18 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     unsigned long long nchunks = 0;
     rc = plan_round(ctx, g, gamma_only, shape, nshards, i, &ngroups, &nchunks);
     if (rc) return rc;
+    if (shape.kernel == 5) {
+      // the suffix tables this round's levels read
+      int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX};
+      const Group* gp = slot_ptr<Group>(ctx->h_io, l, i, l.off_groups);
+      for (int q = 0; q < ngroups; ++q)
+        lo[gp[q].depth - 3] = std::min(lo[gp[q].depth - 3], gp[q].sfloor);
+      for (int D = 3; D <= 5; ++D)
+        if (lo[D - 3] != INT32_MAX) {
+          rc = ensure_level(ctx, D, D == 3 ? 0 : lo[D - 3]);
+          if (rc) return rc;
+        }
+    }
     *slot_ptr<unsigned long long>(ctx->h_io, l, i, 0) = 0ull;
     unsigned long long* hc = slot_ptr<unsigned long long>(ctx->h_io, l, i, l.off_combos);
     int* hb = slot_ptr<int>(ctx->h_io, l, i, l.off_bound);
@@ -479,6 +642,8 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     a.debug = debug;
     a.trace = (i == count - 1) ? trace : nullptr;
     a.trace_from = getenv("BZ_K4_TRACE_FROM") ? atoi(getenv("BZ_K4_TRACE_FROM")) : 0;
+    a.ctrace = (i == count - 1) ? ctrace : nullptr;
+    a.trace_ell = getenv("BZ_K4_TRACE_ELL") ? atoi(getenv("BZ_K4_TRACE_ELL")) : -1;
     todo[i].shape = shape;
     todo[i].run = nchunks > 0 && (unsigned long long)shard < nchunks;
   }
@@ -500,15 +665,25 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
                        cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaEventElapsedTime(&ctx->last_kernel_ms, ctx->ev_k0, ctx->ev_k1));
+  if (ctrace) {
+    // BZ_K4_DEBUG & 32: per-chunk timeline to $BZ_K4_CTRACE (raw int64)
+    std::vector<long long> h(1024 * 64 * 4);
+    CK(cudaMemcpy(h.data(), ctrace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+    const char* path = getenv("BZ_K4_CTRACE");
+    if (FILE* f = fopen(path ? path : "bz_ctrace.bin", "wb")) {
+      fwrite(h.data(), sizeof(long long), h.size(), f);
+      fclose(f);
+    }
+  }
   if (trace) {
-    std::vector<long long> h(8 * 256);
+    // 16 timeline slots x 256 tiles (clock64 of block 0) to $BZ_K4_TRACE_OUT
+    std::vector<long long> h(16 * 256);
     CK(cudaMemcpy(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
-    const long long t0 = h[0];
-    fprintf(stderr, "tile loader_go mma_pre mma_accok mma_go(bfull) issued epi0_go epi0_done epiL_go\n");
-    for (int t = 0; t < 64; ++t)
-      fprintf(stderr, "%3d %8lld %8lld %8lld %8lld %8lld %8lld %8lld %8lld\n", t, h[t] - t0,
-              h[1280 + t] - t0, h[1536 + t] - t0, h[256 + t] - t0, h[1024 + t] - t0,
-              h[512 + t] - t0, h[768 + t] - t0, h[1792 + t] - t0);
+    const char* path = getenv("BZ_K4_TRACE_OUT");
+    if (FILE* f = fopen(path ? path : "bz_trace.bin", "wb")) {
+      fwrite(h.data(), sizeof(long long), h.size(), f);
+      fclose(f);
+    }
   }
   return BZ_OK;
 }
@@ -586,7 +761,7 @@ void bz_destroy(bz_ctx* ctx) {
     cudaFree(ctx->d_px);
     cudaFree(ctx->d_trip);
     cudaFree(ctx->d_trip4);
-    cudaFree(ctx->d_trip5);
+    for (int i = 0; i < 3; ++i) cudaFree(ctx->d_lvl[i]);
     cudaFree(ctx->d_binom);
     cudaFree(ctx->d_io);
     cudaFree(ctx->d_hist);
@@ -653,13 +828,13 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
   CK(cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
   // triple tables (K3, K4) are sized here and built lazily by the first
   // round that needs them
-  ctx->trip_built = ctx->trip4_built = ctx->trip5_built = false;
-  ctx->trip_rows = ctx->trip4_rows = ctx->trip5_rows = 0;
+  ctx->trip_built = ctx->trip4_built = false;
+  ctx->trip_rows = ctx->trip4_rows = 0;
+  for (int i = 0; i < 3; ++i) ctx->lvl_floor[i] = -1;
   if (k >= 4) {
     const size_t n3 = (size_t)k * (k - 1) * (k - 2) / 6;
     ctx->trip_rows = n3 + bz::kTileRows;
     ctx->trip4_rows = (n3 + bz::kUmmaN - 1) / bz::kUmmaN * bz::kUmmaN + bz::kUmmaN;
-    ctx->trip5_rows = (n3 + bz::kUmmaN4 - 1) / bz::kUmmaN4 * bz::kUmmaN4 + bz::kUmmaN4;
   }
 
   ctx->m = m;
@@ -767,11 +942,12 @@ int bz_plan(int m, int k, int g, int engine, int nshards, int64_t* out, int cap,
       o[2] = gs[i].gamma;
       o[3] = gs[i].ell;
       o[4] = gs[i].ppl;
-      o[5] = (int64_t)gs[i].nprefix * (int64_t)binom_sat(k - 1 - gs[i].ell, gs[i].depth);
+      o[5] = (int64_t)gs[i].nprefix * (int64_t)gs[i].slice;
       o[6] = gs[i].depth;
       o[7] = gs[i].lanes;
-      o[8] = gs[i].depth == 3 ? (int64_t)gs[i].tpc * gs[i].tile_rows : 0;
+      o[8] = gs[i].depth >= 3 ? (int64_t)gs[i].tpc * gs[i].tile_rows : 0;
       o[9] = gs[i].ntb;
+      o[10] = gs[i].sfloor;
     }
   }
   return BZ_OK;

@@ -44,11 +44,13 @@ struct Group {
   int gamma;                       // matrix index
   int ell;                         // last prefix element (-1 when g == 1)
   int ppl;                         // prefixes per lane per chunk
-  int depth;                       // suffix depth D of the round (1, 2 or 3)
+  int depth;                       // suffix depth D (1, 2 or 3; K5 levels 3..5)
   int tpc;                         // D = 3: suffix tiles per chunk
   int ntb;                         // D = 3: tile blocks per prefix block
   int lanes;                       // prefixes walked in parallel per chunk
-  int tile_rows;                   // D = 3: triples per suffix tile
+  int tile_rows;                   // D >= 3: suffixes per table tile
+  int slice;                       // suffixes per prefix: C(k - sfloor, D)
+  int sfloor;                      // smallest suffix row: max(ell + 1, level floor)
 };
 
 struct RoundArgs {
@@ -68,6 +70,8 @@ struct RoundArgs {
   int debug;                   // K4 timing experiments only (see BZ_K4_DEBUG)
   long long* trace;            // K4 debug timeline (BZ_K4_DEBUG & 8), else null
   int trace_from;              // first traced tile (BZ_K4_TRACE_FROM)
+  int trace_ell;               // or: from the first chunk with ell >= this (BZ_K4_TRACE_ELL)
+  long long* ctrace;           // K4/K5 per-chunk timeline (BZ_K4_DEBUG & 32), else null
 };
 
 __host__ __device__ constexpr int padded_words(int w) {

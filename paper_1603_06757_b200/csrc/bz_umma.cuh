@@ -55,18 +55,31 @@ constexpr int kUmmaM = 128;       // prefixes per A tile = producer threads
 #define BZ_K4_EPI_WARPS 8
 #endif
 #ifndef BZ_K5_EPI_WARPS
-#define BZ_K5_EPI_WARPS 16
+#define BZ_K5_EPI_WARPS 8
 #endif
 #ifndef BZ_K5_BUFS
 #define BZ_K5_BUFS 2
 #endif
+#ifndef BZ_K5_SPLIT
+#define BZ_K5_SPLIT 1
+#endif
+#ifndef BZ_K5_MAGIC
+#define BZ_K5_MAGIC 1
+#endif
+// K5 accumulators start at 1.5 * 2^23 (one extra MMA per part from two tiny
+// constant operands): the fp32 sum then carries the integer dot product in
+// its low 16 bits, so the epilogue reads them with .pack::16b (half the
+// register traffic) and reduces packed s16 pairs, like K4.
+constexpr bool kK5Magic = BZ_K5_MAGIC != 0;
+constexpr int kSfColMagic = 496;  // ue8m0 2^23 scale columns of the magic MMA
+constexpr uint32_t kMagicBytes = 512;  // A and B magic operands (K = 64, SBO = 0)
 constexpr int kUmmaN = BZ_K4_N;   // K4 triples per B tile
 constexpr int kUmmaMA = BZ_K4_MA; // K4 A tiles (consecutive prefix steps) per B tile
 constexpr int kTmemCols = 512;    // accumulators (+ K5 scale factors)
 constexpr int kSfCol = 480;       // K5 scale-factor columns [480, 512)
 constexpr int kUmmaN4 = kSfCol / BZ_K5_BUFS;  // K5 triples per B tile (240 / 120)
 constexpr int kMaxStages = 8;
-constexpr int kMaxAcc = 4;
+constexpr int kMaxAcc = 8;
 constexpr int kMaxABuf = 4;
 constexpr int kChunkQ = 4;         // depth of the loader -> roles chunk queue
 constexpr int kBarSlots = 2 * kMaxABuf + 2 * kMaxStages + 2 * kMaxAcc + 2 * kChunkQ;
@@ -87,7 +100,11 @@ struct K4Roles {
   static constexpr int LOAD = E + ACC;
   static constexpr int PROD0 = E + ACC + 1;
   static constexpr int THREADS = 32 * (E + ACC + 5);
-  static_assert(E % 4 == 0 && ACC <= kMaxAcc, "roles");
+  // column parts of each accumulator with their own full/empty barriers:
+  // the epilogue drains part 0 while the MMAs of part 1 still run, and the
+  // next tile's part-0 MMAs start as soon as part 0 is drained
+  static constexpr int SPLIT = F4 ? BZ_K5_SPLIT : 1;
+  static_assert(E % 4 == 0 && ACC * SPLIT <= kMaxAcc && (E / 4) % SPLIT == 0, "roles");
 };
 
 template <bool F4> __host__ __device__ constexpr int k4_n() { return F4 ? kUmmaN4 : kUmmaN; }
@@ -105,10 +122,12 @@ template <bool F4> __host__ __device__ constexpr uint32_t k4_tile_a(int w) {
   return (uint32_t)(kUmmaM * 16 * k4_a_chunks<F4>(w));
 }
 // A-tile ring depth (producers run that many prefix steps ahead)
-template <bool F4> __host__ __device__ constexpr int k4_abufs() { return F4 ? 4 : 2; }
-// B-tile ring depth: K5 ~150 KB of stages, K4 4 x 40 KB at W = 5
+template <bool F4> __host__ __device__ constexpr int k4_abufs(int w) {
+  return F4 && w <= 6 ? 4 : 2;
+}
+// B-tile ring depth: K5 ~136 KB of stages, K4 4 x 40 KB at W = 5
 template <bool F4> __host__ __device__ constexpr int k4_stages(int w) {
-  return F4 ? (150000 / (int)k4_tile_b<true>(w) < kMaxStages ? 150000 / (int)k4_tile_b<true>(w)
+  return F4 ? (136000 / (int)k4_tile_b<true>(w) < kMaxStages ? 136000 / (int)k4_tile_b<true>(w)
                                                               : kMaxStages)
             : (w <= 5 ? 4 : (w <= 6 ? 3 : 2));
 }
@@ -150,8 +169,11 @@ constexpr uint32_t kUmmaIdesc = (2u << 4) | (1u << 7) | (1u << 10) |
                                 ((uint32_t)(kUmmaM >> 4) << 24);
 // block-scaled: A = B = e2m1 (format 1), K-major, N, scale type ue8m0
 // (bit 23), M, K = 64 (bit 31 clear), scale-factor ids 0
-constexpr uint32_t kMxf4Idesc = (1u << 7) | (1u << 10) | ((uint32_t)(kUmmaN4 >> 3) << 17) |
-                                (1u << 23) | ((uint32_t)(kUmmaM >> 4) << 24);
+__host__ __device__ constexpr uint32_t mxf4_idesc(int n) {
+  return (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | (1u << 23) |
+         ((uint32_t)(kUmmaM >> 4) << 24);
+}
+constexpr uint32_t kMxf4Idesc = mxf4_idesc(kUmmaN4);
 
 // ---- mbarrier / TMA / tcgen05 primitives
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
@@ -330,6 +352,40 @@ __device__ __forceinline__ void tmem_regs_after_wait(uint32_t* v) {
                : "memory");
 }
 
+// C consecutive 32-bit columns of this warp's 32 TMEM lanes as packed
+// 16-bit pairs (low halves) into v[0, C/2) (C a multiple of 4, at most 128)
+__device__ __forceinline__ void tmem_ld8p(uint32_t taddr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                 "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld4p(uint32_t taddr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.pack::16b.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld2p(uint32_t taddr, uint32_t* v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.pack::16b.b32 {%0,%1}, [%2];"
+               : "=r"(v[0]), "=r"(v[1])
+               : "r"(taddr));
+}
+template <int C>
+__device__ __forceinline__ void tmem_ld_cols_p(uint32_t taddr, uint32_t* v) {
+  if constexpr (C >= 32) {
+    tmem_ld16p(taddr, v);
+    tmem_ld_cols_p<C - 32>(taddr + 32, v + 16);
+  } else if constexpr (C >= 16) {
+    tmem_ld8p(taddr, v);
+    tmem_ld_cols_p<C - 16>(taddr + 16, v + 8);
+  } else if constexpr (C >= 8) {
+    tmem_ld4p(taddr, v);
+    tmem_ld_cols_p<C - 8>(taddr + 8, v + 4);
+  } else if constexpr (C >= 4) {
+    tmem_ld2p(taddr, v);
+  }
+}
+
 // C consecutive 32-bit columns of this warp's 32 TMEM lanes into v[0, C)
 // (C a multiple of 4, at most 128): x32 / x16 / x8 / x4 loads, no wait.
 template <int C>
@@ -345,6 +401,54 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t* v) {
     tmem_ld_cols<C - 8>(taddr + 8, v + 8);
   } else if constexpr (C >= 4) {
     tmem_ld4(taddr, v);
+  }
+}
+
+// Suffix tables of one round: level D = 3 + i at t[i], stride_rows[i] rows
+// per Gamma (K4 uses t[0] only).
+struct K4Tables {
+  const uint8_t* t[3];
+  unsigned long long stride_rows[3];
+};
+
+// K5 suffix table of level D: every D-subset of rows [floor, k), smallest
+// element a descending (so the subsets with smallest element >= f are the
+// first C(k - f, D) rows), then the other D - 1 elements lex.  One block per
+// (a, Gamma), one thread per subset; rows stored as e2m1 0 / 1.0 nibbles in
+// the UMMA K-major no-swizzle layout (W 16-byte chunks per row).
+template <int W>
+__global__ void k_build_subsets_mxf4(const uint32_t* __restrict__ rows,
+                                     uint8_t* __restrict__ out, int k, int D, int floor,
+                                     size_t gamma_stride_rows,
+                                     const unsigned long long* __restrict__ binom) {
+  constexpr int WP = padded_words(W);
+  const int j = blockIdx.y, a = floor + blockIdx.x;
+  if (a > k - D) return;
+  const uint32_t* R = rows + (size_t)j * k * WP;
+  const unsigned long long base = binom[(k - 1 - a) * kBinomDim + D];
+  const unsigned long long cnt = binom[(k - 1 - a) * kBinomDim + (D - 1)];
+  uint8_t* tab = out + (size_t)j * gamma_stride_rows * (16 * W);
+  for (unsigned long long t = threadIdx.x; t < cnt; t += blockDim.x) {
+    uint32_t v[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) v[w] = R[a * WP + w];
+    // lex unrank of t among the (D-1)-subsets of [a+1, k)
+    unsigned long long r = t;
+    int e = a + 1;
+    for (int i = D - 1; i >= 1; --i) {
+      for (;; ++e) {
+        const unsigned long long c = binom[(k - 1 - e) * kBinomDim + (i - 1)];
+        if (r < c) break;
+        r -= c;
+      }
+#pragma unroll
+      for (int w = 0; w < W; ++w) v[w] ^= R[e * WP + w];
+      ++e;
+    }
+    const unsigned long long row = base + t;
+    uint8_t* grp = tab + (size_t)(row >> 3) * (8 * 16 * W) + (row & 7) * 16;
+#pragma unroll
+    for (int w = 0; w < W; ++w) *reinterpret_cast<uint4*>(grp + w * 128) = e2m1_bits01(v[w]);
   }
 }
 
@@ -390,18 +494,44 @@ template <int W, bool F4>
 __host__ __device__ inline size_t k4_smem_bytes(int m, int k, int ngroups) {
   size_t off = (smem_base_bytes<W>(m, k, ngroups) + 1023) & ~size_t(1023);
   off += (size_t)k4_stages<F4>(W) * k4_tile_b<F4>(W);
-  off += (size_t)k4_abufs<F4>() * kUmmaMA * k4_tile_a<F4>(W);
+  off += (size_t)k4_abufs<F4>(W) * kUmmaMA * k4_tile_a<F4>(W);
+  off += F4 ? kMagicBytes : 0;   // K5 magic operands
   off += kBarSlots * 8 + 16;     // barriers + TMEM base
-  off += k4_abufs<F4>() * kUmmaMA * kUmmaM * sizeof(int);  // prefix weights of the A buffers
+  off += k4_abufs<F4>(W) * kUmmaMA * kUmmaM * sizeof(int);  // prefix weights of the A buffers
   off += kChunkQ * sizeof(long long) + 16;    // chunk queue
   return off;
 }
 
 // debug timeline (BZ_K4_DEBUG & 8): block 0, tiles [trace_from, +256)
-__device__ __forceinline__ void k4_trace(const RoundArgs& a, int slot, uint32_t tile) {
-  if (!a.trace || blockIdx.x != 0) return;
-  const uint32_t i = tile - (uint32_t)a.trace_from;
+// (BZ_K4_TRACE_ELL = L >= 0 instead traces from the first chunk with ell >= L;
+// every role tracks that tile offset in `toff`)
+constexpr uint32_t kNoTrace = 0xF0000000u;
+__device__ __forceinline__ uint32_t k4_trace_off(const RoundArgs& a) {
+  return a.trace_ell >= 0 ? kNoTrace : (uint32_t)a.trace_from;
+}
+__device__ __forceinline__ void k4_trace_chunk(const RoundArgs& a, uint32_t& toff, int ell,
+                                               uint32_t tile) {
+  if (a.trace_ell >= 0 && toff == kNoTrace && ell >= a.trace_ell) toff = tile;
+}
+#ifndef BZ_K4_TRACE
+#define BZ_K4_TRACE 0  // build with -DBZ_K4_TRACE=1 for the BZ_K4_DEBUG & 8 timeline
+#endif
+__device__ __forceinline__ void k4_trace(const RoundArgs& a, int slot, uint32_t tile,
+                                         uint32_t toff) {
+  if (!BZ_K4_TRACE || !a.trace || blockIdx.x != 0) return;
+  const uint32_t i = tile - toff;
   if (i < 256) a.trace[slot * 256 + i] = clock64();
+}
+
+// debug per-chunk timeline (BZ_K4_DEBUG & 32): per block, the first 64
+// chunks as {chunk, dequeued (clock64), done (clock64), done (globaltimer)}
+__device__ __forceinline__ long long* k4_ctrace(const RoundArgs& a, uint32_t qi) {
+  return (a.ctrace && qi < 64) ? a.ctrace + ((size_t)blockIdx.x * 64 + qi) * 4 : nullptr;
+}
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
 }
 
 // Decoded chunk: identical on every role.
@@ -423,8 +553,7 @@ __device__ __forceinline__ K4Chunk k4_decode(const Group* sg, int ngroups,
   c.bfirst = pb * (unsigned long long)kUmmaM * c.gr.ppl;
   const unsigned long long bleft = c.gr.nprefix - c.bfirst;
   c.maxcnt = bleft < (unsigned long long)c.gr.ppl ? (long long)bleft : c.gr.ppl;
-  const long long t = k - 1 - c.gr.ell;
-  c.slice = (int)(t * (t - 1) * (t - 2) / 6);
+  c.slice = c.gr.slice;
   const int ntiles = (c.slice + N - 1) / N;
   c.tile_lo = tb * c.gr.tpc;
   c.tile_hi = min(ntiles, c.tile_lo + c.gr.tpc);
@@ -437,7 +566,7 @@ __device__ __forceinline__ K4Chunk k4_decode(const Group* sg, int ngroups,
 // accumulator type (s32 read as packed s16 / f32) and tile geometry.
 template <int W, bool F4>
 __global__ void __launch_bounds__(K4Roles<F4>::THREADS, 1)
-k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_stride_rows) {
+k4_round_umma(const RoundArgs a, const K4Tables tabs) {
   static_assert(!F4 || kUmmaMA == 1, "K5 runs one A tile per B tile");
   constexpr int N = k4_n<F4>();
   constexpr int S = k4_stages<F4>(W);
@@ -450,15 +579,20 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   constexpr int ACC = RL::ACC;
   constexpr int E = RL::E;
   constexpr int EC = N / (E / 4);  // columns per epilogue warp and A tile
-  constexpr uint32_t IDESC = F4 ? kMxf4Idesc : kUmmaIdesc;
+  constexpr int SPLIT = RL::SPLIT;
+  constexpr int NH = N / SPLIT;  // accumulator columns per part
+  static_assert(NH % 8 == 0, "parts are whole 8-row groups of the B tile");
+  constexpr uint32_t IDESC = F4 ? mxf4_idesc(NH) : kUmmaIdesc;
   static_assert(S <= kMaxStages, "barrier slots");
   static_assert(EC * (E / 4) == N && (F4 ? EC % 4 == 0 && EC <= 128 : EC % 32 == 0), "epilogue");
   extern __shared__ __align__(128) unsigned char smem[];
   const size_t base = (smem_base_bytes<W>(a.m, a.k, a.ngroups) + 1023) & ~size_t(1023);
   unsigned char* sB = smem + base;
   unsigned char* sA = sB + S * TB;
-  constexpr int NA = k4_abufs<F4>();
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(sA + NA * kUmmaMA * TA);
+  constexpr int NA = k4_abufs<F4>(W);
+  unsigned char* sMagic = sA + NA * kUmmaMA * TA;  // K5: A, B magic core matrices
+  unsigned long long* bars =
+      reinterpret_cast<unsigned long long*>(sMagic + (F4 ? kMagicBytes : 0));
   uint32_t* s_tmem = reinterpret_cast<uint32_t*>(bars + kBarSlots);
   int* s_wt = reinterpret_cast<int*>(s_tmem + 4);  // [2][kUmmaMA][kUmmaM] prefix weights
   volatile long long* s_q = reinterpret_cast<volatile long long*>(
@@ -488,12 +622,12 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   if (tid == 0) {
     for (int i = 0; i < S; ++i) { mbar_init(bfull(i), 1); mbar_init(bempty(i), 1); }
     for (int i = 0; i < NA; ++i) {
-      mbar_init(afull(i), kUmmaM);               // every producer thread
+      mbar_init(afull(i), 4);                    // each producer warp
       mbar_init(aempty(i), ACC + E);             // each MMA warp's commit + epilogue warp
     }
-    for (int i = 0; i < ACC; ++i) {
+    for (int i = 0; i < ACC * SPLIT; ++i) {
       mbar_init(accfull(i), 1);                  // MMA commit
-      mbar_init(accempty(i), E);                 // each epilogue warp
+      mbar_init(accempty(i), E / SPLIT);         // each epilogue warp of the part
     }
     for (int i = 0; i < kChunkQ; ++i) {
       mbar_init(qfull(i), 1);                    // loader
@@ -519,8 +653,19 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
     // the zero K-padding chunk of both A buffers (odd W)
     if (warp < 4) {
       for (int c = 0; c < 512 - kSfCol; c += 8)
-        tmem_st8(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(kSfCol + c), 0x7F7F7F7Fu);
+        tmem_st8(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(kSfCol + c),
+                 kSfCol + c == kSfColMagic ? 0x96969696u : 0x7F7F7F7Fu);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    if (kK5Magic && tid < (int)kMagicBytes / 16) {
+      // two K-chunks x 8 rows x 16 B per operand; element 0 of every row:
+      // A = 1.5 (0x3), B = 1.0 (0x2); scaled by 2^23 the product is the
+      // 1.5 * 2^23 the accumulators start from
+      const int op = tid / 16, row16 = tid % 16;  // row16 < 8: chunk 0
+      uint4 z = make_uint4(0, 0, 0, 0);
+      if (row16 < 8) z.x = op == 0 ? 0x3u : 0x2u;
+      *reinterpret_cast<uint4*>(sMagic + op * 256 + row16 * 16) = z;
+      fence_proxy_async();
     }
     if (CA > W && warp >= RL::PROD0) {
       const int r = tid - 32 * RL::PROD0;
@@ -532,15 +677,16 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
     __syncthreads();
     tc_fence_after();
   }
-  const int k = a.k, q = a.g - 4;
+  const int k = a.k;
   const unsigned FULL = 0xffffffffu;
 
   if (warp < E) {
     // ================= epilogue: warp e reads TMEM lanes 32(e%4).. (rows),
     // columns [EC*(e/4), +EC) of each accumulator
     const int quarter = warp & 3, slice_id = warp >> 2;
+    const int part = slice_id / ((E / 4) / SPLIT);  // accumulator part this warp drains
     const int r = 32 * quarter + lane;
-    uint32_t grp = 0, tcount = 0;
+    uint32_t grp = 0, tcount = 0, toff = k4_trace_off(a);
     for (uint32_t qi = 0;; ++qi) {
       const int qs = qi % kChunkQ;
       mbar_wait(qfull(qs), (qi / kChunkQ) & 1);
@@ -550,6 +696,7 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
       if (qchunk < 0) break;
       const unsigned long long chunk = (unsigned long long)qchunk;
       const K4Chunk c = k4_decode<N>(sgroups, a.ngroups, chunk, k);
+      k4_trace_chunk(a, toff, c.gr.ell, tcount);
       int best = INT_MAX;
       for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
         const int ab = grp % NA;
@@ -565,19 +712,59 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
         float fmin_acc = __int_as_float(0x7f800000);  // K5: +inf
         for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount) {
           const int buf = tcount % ACC;
-          mbar_wait(accfull(buf), (tcount / ACC) & 1);
+          const int hb = buf * SPLIT + part;
+          if (warp == 0 && lane == 0) k4_trace(a, 8, tcount, toff);
+          mbar_wait(accfull(hb), (tcount / ACC) & 1);
+          if (warp == 0 && lane == 0) k4_trace(a, 9, tcount, toff);
           tc_fence_after();
-          if (warp == 0 && lane == 0) k4_trace(a, 2, tcount);
-          if (warp == E - 1 && lane == 0) k4_trace(a, 7, tcount);
+          if (warp == 0 && lane == 0) k4_trace(a, 2, tcount, toff);
+          if (warp == E - 1 && lane == 0) k4_trace(a, 7, tcount, toff);
           const int lim = min(N, c.slice - t * N) - EC * slice_id;
           const uint32_t tb = tmem + ((uint32_t)(32 * quarter) << 16) +
                               (uint32_t)(buf * kUmmaMA * N + EC * slice_id);
           if (a.debug & 1) {
             __syncwarp();
-            if (lane == 0) mbar_arrive(accempty(buf));
+            if (lane == 0) mbar_arrive(accempty(hb));
             continue;
           }
-          if constexpr (F4) {
+          if constexpr (F4 && kK5Magic) {
+            // EC accumulators as packed s16 pairs (low halves of 1.5*2^23 + D)
+            constexpr int NP = EC / 2;
+            uint32_t v[NP];
+            tmem_ld_cols_p<EC>(tb, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i + 1 < NP; i += 2) {
+              asm volatile("" : "+r"(v[i]), "+r"(v[i + 1]) : : "memory");
+            }
+            if (NP % 2) asm volatile("" : "+r"(v[NP - 1]) : : "memory");
+            if (warp == 0 && lane == 0) k4_trace(a, 10, tcount, toff);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(accempty(hb));  // accumulators are in registers
+            if (warp == 0 && lane == 0) k4_trace(a, 11, tcount, toff);
+            if (warp == E - 1 && lane == 0) k4_trace(a, 14, tcount, toff);
+            if (lim < EC) {
+#pragma unroll
+              for (int i = 0; i < NP; ++i) {
+                if (2 * i >= lim) v[i] = (v[i] & 0xffff0000u) | 0x00007fffu;
+                if (2 * i + 1 >= lim) v[i] = (v[i] & 0x0000ffffu) | 0x7fff0000u;
+              }
+            }
+            // two independent 3-input SIMD chains
+            uint32_t m0 = __vimin3_s16x2(v[0], v[1], v[2]);
+            uint32_t m1 = NP > 5 ? __vimin3_s16x2(v[3], v[4], v[5]) : v[0];
+#pragma unroll
+            for (int i = 6; i + 3 < NP; i += 4) {
+              m0 = __vimin3_s16x2(m0, v[i], v[i + 1]);
+              m1 = __vimin3_s16x2(m1, v[i + 2], v[i + 3]);
+            }
+#pragma unroll
+            for (int i = 6 + ((NP - 6) / 4) * 4; i < NP; ++i) m0 = __vmins2(m0, v[i]);
+            const uint32_t m = __vmins2(m0, m1);
+            const int lo = (int)(short)(m & 0xffffu), hi = (int)(short)(m >> 16);
+            rmin[0] = min(rmin[0], min(lo, hi));
+          } else if constexpr (F4) {
             // EC f32 accumulators: every load, one wait, release the buffer,
             // then 3-input float minima
             uint32_t v[EC];
@@ -585,9 +772,12 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
             tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < EC; i += 4) tmem_regs4_after_wait(v + i);
+            if (warp == 0 && lane == 0) k4_trace(a, 10, tcount, toff);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(accempty(buf));  // accumulators are in registers
+            if (lane == 0) mbar_arrive(accempty(hb));  // accumulators are in registers
+            if (warp == 0 && lane == 0) k4_trace(a, 11, tcount, toff);
+            if (warp == E - 1 && lane == 0) k4_trace(a, 14, tcount, toff);
             if (lim < EC) {
 #pragma unroll
               for (int i = 0; i < EC; ++i)
@@ -622,7 +812,7 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
               for (int cc = 0; cc < EC / 32; ++cc) tmem_regs16_after_wait(&v[j][16 * cc]);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(accempty(buf));  // accumulators are in registers
+            if (lane == 0) mbar_arrive(accempty(hb));  // accumulators are in registers
 #pragma unroll
             for (int j = 0; j < kUmmaMA; ++j) {
               if (lim < EC) {
@@ -640,9 +830,9 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
               rmin[j] = min(rmin[j], min(lo, hi));
             }
           }
-          if (warp == 0 && lane == 0) k4_trace(a, 3, tcount);
+          if (warp == 0 && lane == 0) k4_trace(a, 3, tcount, toff);
         }
-        if constexpr (F4) {
+        if constexpr (F4 && !kK5Magic) {
           // |D| <= n, so a finite minimum converts exactly; +inf (every
           // column of this slice masked) stays out of the way
           if (fmin_acc < 1.0e6f) rmin[0] = (int)fmin_acc;
@@ -655,6 +845,8 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
         volatile int* vb = a.bound;
         if (wbest < vb[1 + c.gr.gamma]) atomicMin(a.bound + 1 + c.gr.gamma, wbest);
         if (wbest < vb[0]) atomicMin(a.bound, wbest);
+        long long* ct = k4_ctrace(a, qi);
+        if (ct && warp == 0) { ct[2] = clock64(); ct[3] = global_ns(); }
       }
     }
   } else if (warp >= RL::PROD0) {
@@ -680,7 +872,7 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
       const uint32_t* PX = spx + c.gr.gamma * (k + 1) * px_stride(W);
       Walker<W> wk;
       // rows without prefixes duplicate the block's first prefix
-      wk.init(cnt > 0 ? first : c.bfirst, q, c.gr.ell, R, a.binom);
+      wk.init(cnt > 0 ? first : c.bfirst, a.g - 1 - c.gr.depth, c.gr.ell, R, a.binom);
       for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
         const int ab = grp % NA;
         mbar_wait(aempty(ab), ((grp / NA) & 1) ^ 1);
@@ -711,7 +903,8 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
           s_wt[(ab * kUmmaMA + j) * kUmmaM + r] = wt;
         }
         fence_proxy_async();  // generic-proxy writes -> tensor-core reads
-        mbar_arrive(afull(ab));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(afull(ab));
       }
       // visited combinations of this chunk
       const unsigned tot = __reduce_add_sync(FULL, (unsigned)cnt);
@@ -729,9 +922,13 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
     {
       const uint64_t a_desc0 = umma_desc(sA_s, 128, CA * 128);
       const uint64_t b_desc0 = umma_desc(sB_s, 128, CB * 128);
-      const uint32_t sfa = tmem + kSfCol, sfb = tmem + kSfCol + 8;
+      const uint32_t sfa = tmem + kSfCol, sfb = tmem + kSfCol + 8, sfm = tmem + kSfColMagic;
+      // magic operands: one core matrix per K chunk, SBO = 0 (every 8-row
+      // group reads the same 8 rows)
+      const uint32_t sM = (uint32_t)__cvta_generic_to_shared(sMagic);
+      const uint64_t magic_a = umma_desc(sM, 128, 0), magic_b = umma_desc(sM + 256, 128, 0);
       const uint32_t dbase = tmem + (uint32_t)(mb * kUmmaMA * N);
-      uint32_t grp = 0, tcount = 0;
+      uint32_t grp = 0, tcount = 0, toff = k4_trace_off(a);
       for (uint32_t qi = 0;; ++qi) {
         const int qs = qi % kChunkQ;
         mbar_wait_fast(qfull(qs), (qi / kChunkQ) & 1);
@@ -741,6 +938,7 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
         if (qchunk < 0) break;
         const unsigned long long chunk = (unsigned long long)qchunk;
         const K4Chunk c = k4_decode<N>(sgroups, a.ngroups, chunk, k);
+        k4_trace_chunk(a, toff, c.gr.ell, tcount);
         const int ntile = c.tile_hi - c.tile_lo;
         for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
           const int ab = grp % NA;
@@ -755,37 +953,48 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
             // the B stage is normally long loaded: wait for it first, so the
             // accumulator hand-back (the critical loop) is the last wait
             // before the MMAs
-            if (lane == 0) k4_trace(a, 5, tc);
+            if (lane == 0) k4_trace(a, 5, tc, toff);
             mbar_wait_fast(bfull(stg), (tc / S) & 1);
-            if (lane == 0) k4_trace(a, 6, tc);
-            mbar_wait_fast(accempty(mb), ((tc / ACC) & 1) ^ 1);
-            tc_fence_after();
-            if (lane == 0) k4_trace(a, 1, tc);
-            // pass kb advances both start addresses by 32 bytes of K per
-            // row = two core matrices = 256 B (16 in the 16-byte-granular
-            // address field)
-            const uint64_t bd0 = b_desc0 + (uint64_t)(stg * (TB >> 4));
-            if (elect_one()) {
-              if (!(a.debug & 4)) {
+            if (lane == 0) k4_trace(a, 6, tc, toff);
+            const int valid = min(N, c.slice - (c.tile_lo + i) * N);
 #pragma unroll
-                for (int j = 0; j < kUmmaMA; ++j) {
-                  const uint32_t dj = dbase + (uint32_t)(j * N);
-                  const uint64_t adj = a_desc0 + (uint64_t)((ab * kUmmaMA + j) * (TA >> 4));
+            for (int h = 0; h < SPLIT; ++h) {
+              mbar_wait_fast(accempty(mb * SPLIT + h), ((tc / ACC) & 1) ^ 1);
+              if (lane == 0 && h == 1) k4_trace(a, 13, tc, toff);
+              tc_fence_after();
+              if (lane == 0 && h == 0) k4_trace(a, 1, tc, toff);
+              // pass kb advances both start addresses by 32 bytes of K per
+              // row = two core matrices = 256 B (16 in the 16-byte-granular
+              // address field); part h starts NH/8 row groups into the tile
+              const uint64_t bd0 =
+                  b_desc0 + (uint64_t)(stg * (TB >> 4)) + (uint64_t)(h * (NH / 8) * CB * 8);
+              if (elect_one()) {
+                // a part holding no valid suffix is only committed (its
+                // columns are masked anyway)
+                if (!(a.debug & 4) && valid > h * NH) {
 #pragma unroll
-                  for (int kb = 0; kb < P; ++kb) {
-                    if constexpr (F4)
-                      umma_mxf4(dj, adj + 16u * kb, bd0 + 16u * kb, IDESC, kb > 0 ? 1u : 0u,
-                                sfa, sfb);
-                    else
-                      umma_i8(dj, adj + 16u * kb, bd0 + 16u * kb, IDESC, kb > 0 ? 1u : 0u);
+                  for (int j = 0; j < kUmmaMA; ++j) {
+                    const uint32_t dj = dbase + (uint32_t)(j * N + h * NH);
+                    const uint64_t adj = a_desc0 + (uint64_t)((ab * kUmmaMA + j) * (TA >> 4));
+                    if constexpr (F4 && kK5Magic)
+                      umma_mxf4(dj, magic_a, magic_b, IDESC, 0u, sfm, sfb);
+#pragma unroll
+                    for (int kb = 0; kb < P; ++kb) {
+                      if constexpr (F4)
+                        umma_mxf4(dj, adj + 16u * kb, bd0 + 16u * kb, IDESC,
+                                  (kb > 0 || kK5Magic) ? 1u : 0u, sfa, sfb);
+                      else
+                        umma_i8(dj, adj + 16u * kb, bd0 + 16u * kb, IDESC, kb > 0 ? 1u : 0u);
+                    }
                   }
                 }
+                umma_commit(accfull(mb * SPLIT + h));
+                if (h == SPLIT - 1) umma_commit(bempty(stg));
               }
-              umma_commit(bempty(stg));
-              umma_commit(accfull(mb));
+              __syncwarp();
+              if (lane == 0 && h == 0) k4_trace(a, 12, tc, toff);
             }
-            __syncwarp();
-            if (lane == 0) k4_trace(a, 4, tc);
+            if (lane == 0) k4_trace(a, 4, tc, toff);
           }
           // the A buffer is free once every issuer's MMAs on it completed
           if (elect_one()) umma_commit(aempty(ab));
@@ -798,7 +1007,7 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   } else {
     // ================= loader: TMA bulk copies of triple tiles
     if (lane == 0) {
-      uint32_t bcount = 0;
+      uint32_t bcount = 0, toff = k4_trace_off(a);
       volatile int* vb = a.bound;
       for (uint32_t qi = 0;; ++qi) {
         const int qs = qi % kChunkQ;
@@ -808,16 +1017,21 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
         const unsigned long long ch = cidx * (unsigned long long)a.nshards + a.shard;
         const long long qchunk = (ch < a.nchunks && vb[0] > a.lower_prev) ? (long long)ch : -1;
         s_q[qs] = qchunk;
+        long long* ct = k4_ctrace(a, qi);
+        if (ct) { ct[0] = qchunk; ct[1] = clock64(); }
         mbar_arrive(qfull(qs));
         if (qchunk < 0) break;
         const unsigned long long chunk = (unsigned long long)qchunk;
         const K4Chunk c = k4_decode<N>(sgroups, a.ngroups, chunk, k);
-        const uint8_t* tsrc = trip + (size_t)c.gr.gamma * gamma_stride_rows * (CB * 16);
+        k4_trace_chunk(a, toff, c.gr.ell, bcount);
+        const int lvl = c.gr.depth - 3;  // suffix table of this group's level
+        const uint8_t* tsrc =
+            tabs.t[lvl] + (size_t)c.gr.gamma * tabs.stride_rows[lvl] * (CB * 16);
         for (long long p = 0; p < c.maxcnt; p += kUmmaMA) {
           for (int t = c.tile_lo; t < c.tile_hi; ++t, ++bcount) {
             const int stg = bcount % S;
             mbar_wait(bempty(stg), ((bcount / S) & 1) ^ 1);
-            k4_trace(a, 0, bcount);
+            k4_trace(a, 0, bcount, toff);
             // only the rows this tile needs (8-row granularity); the rest of
             // the stage keeps stale rows whose columns the epilogue masks
             const int valid = min(N, c.slice - t * N);
@@ -827,6 +1041,7 @@ k4_round_umma(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
             } else {
               mbar_arrive_tx(bfull(stg), bytes);
               tma_load_1d(sB_s + stg * TB, tsrc + (size_t)t * TB, bytes, bfull(stg));
+              k4_trace(a, 15, bcount, toff);
             }
           }
         }

@@ -46,13 +46,17 @@ def test_plan_counts(engine):
         starts = [gr[0] for gr in groups]
         assert starts == sorted(starts) and starts[0] == 0
         for gr in groups:
-            begin, nprefix, gamma, ell, ppl, combos, depth, lanes, spc, nsb = gr
-            assert nsb >= 1 and (depth != 3 or spc * nsb >= comb(k - 1 - ell, 3))
-            assert lanes == ({"imma": 256}.get(engine, 128) if depth == 3 else 32)
+            begin, nprefix, gamma, ell, ppl, combos, depth, lanes, spc, nsb, sfloor = gr
+            assert nsb >= 1 and (depth < 3 or spc * nsb >= comb(k - sfloor, depth))
+            assert lanes == ({"imma": 256}.get(engine, 128) if depth >= 3 else 32)
             want = 3 if (engine != "popc" and g >= 4) else (2 if g >= 4 else 1)
-            assert depth == want
+            if engine in ("auto", "mxf4") and g >= 4:
+                # K5 suffix levels: depth 3..5, floors above ell + 1
+                assert 3 <= depth <= min(5, g - 1) and sfloor >= ell + 1
+            else:
+                assert depth == want and sfloor == ell + 1
             assert nprefix == (1 if g == 1 else comb(ell, g - 1 - depth))
-            assert combos == nprefix * comb(k - 1 - ell, depth)
+            assert combos == nprefix * comb(k - sfloor, depth)
 
 
 @pytest.mark.parametrize("engine", ["auto", "popc", "imma", "umma", "mxf4"])
@@ -102,3 +106,36 @@ def test_colex_unrank_bijective():
         for q in range(0, min(ell, 5) + 1):
             subs = [tuple(oracle.colex_unrank(r, q, ell)) for r in range(comb(ell, q))]
             assert sorted(subs) == sorted(itertools.combinations(range(ell), q))
+
+
+@pytest.mark.parametrize("m,k,g,floors", [(1, 12, 6, "4,7"), (2, 10, 7, "4"), (1, 14, 8, "5,9"),
+                                          (1, 12, 5, "6"), (1, 11, 9, "0,3")])
+def test_plan_levels_partition(monkeypatch, m, k, g, floors):
+    """K5 suffix levels (forced floors): the depth-3/4/5 groups still visit
+    every g-combination exactly once, for any shard count."""
+    import collections
+    import random
+
+    monkeypatch.setenv("BZ_K5_FLOORS", floors)
+    rng = random.Random(k * 31 + g)
+    n = 2 * k + 3
+    gammas = [[rng.getrandbits(n) for _ in range(k)] for _ in range(m)]
+    expect = sorted(oracle.all_combinations(m, k, g))
+    groups, _ = _native.plan(m, k, g, "mxf4")
+    assert max(collections.Counter(int(gr[6]) for gr in groups)) > 3  # deeper levels in use
+    for nshards in (1, 3):
+        groups, nchunks = _native.plan(m, k, g, "mxf4", nshards)
+        seen = []
+        for s in range(nshards):
+            _, _, got = oracle.enumerate_chunks(gammas, k, g, groups, nchunks, s, nshards)
+            seen += got
+        assert sorted(seen) == expect
+
+
+def test_plan_levels_auto_cfg5():
+    """The cost model splits the cfg5 top round into levels and keeps the
+    combination count exact."""
+    groups, _ = _native.plan(2, 80, 8, "mxf4")
+    depths = {int(gr[6]) for gr in groups}
+    assert depths >= {3, 4}
+    assert sum(int(gr[5]) for gr in groups) == 2 * comb(80, 8)

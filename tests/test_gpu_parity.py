@@ -226,3 +226,24 @@ def test_early_exit_all_engines(ctx, engine):
         mins, combos = ctx.round(g, true_min, 10**6)
         assert min(mins) == true_min
         assert sum(combos) <= sum(full_c)
+
+
+@pytest.mark.parametrize("k,g,floors", [(12, 6, "4,7"), (14, 8, "5,9"), (12, 5, "6"),
+                                        (20, 7, "8,13"), (11, 9, "0,3")])
+@pytest.mark.parametrize("n", [37, 160, 230])
+def test_mxf4_levels(monkeypatch, ctx, k, g, floors, n):
+    """K5 with forced suffix levels (depth-4/5 tables): exact minima and
+    combination counts per Gamma against the oracle."""
+    monkeypatch.setenv("BZ_K5_FLOORS", floors)
+    rng = random.Random(k * 1000 + g * 10 + n)
+    gammas = [[rng.getrandbits(n) for _ in range(k)] for _ in range(2)]
+    ctx.set_engine("mxf4")
+    try:
+        ctx.load(family_words([BitMatrix(r, n) for r in gammas], n), n)
+        mins, combos = ctx.round(g, -1, 1 << 30)
+    finally:
+        ctx.set_engine("auto")
+    for j in range(2):
+        want = oracle.min_weight(gammas[j], n, g)[0]
+        assert mins[j] == want, (j, mins, want)
+        assert combos[j] == comb(k, g)

@@ -86,6 +86,29 @@ __global__ void __launch_bounds__(128, 1) probe(int mode, int gap, long long* ou
     mbar_wait(warp ? bar2 : bar_s, 0);
     o[warp] = clock64() - t0;
   }
+  if (mode == 6 && threadIdx.x == 0) {
+    // commit latency: (a) no MMA pending, (b) after one MMA, (c) after 3 chained
+    uint32_t ph = 0;
+    for (int rep = 0; rep < 3; ++rep) {
+      long long t0 = clock64();
+      umma_commit(bar_s);
+      mbar_wait(bar_s, ph); ph ^= 1;
+      o[3 * rep + 0] = clock64() - t0;
+      t0 = clock64();
+      umma_mxf4(tmem, ad, bd, kMxf4Idesc, 0u, tmem + kSfCol, tmem + kSfCol + 8);
+      const long long ti = clock64();
+      umma_commit(bar_s);
+      mbar_wait(bar_s, ph); ph ^= 1;
+      o[3 * rep + 1] = clock64() - t0;
+      o[20 + rep] = ti - t0;
+      t0 = clock64();
+      for (int i = 0; i < 3; ++i)
+        umma_mxf4(tmem, ad, bd, kMxf4Idesc, i ? 1u : 0u, tmem + kSfCol, tmem + kSfCol + 8);
+      umma_commit(bar_s);
+      mbar_wait(bar_s, ph); ph ^= 1;
+      o[3 * rep + 2] = clock64() - t0;
+    }
+  }
   if (mode == 3 && warp == 0) {
     // already-complete barrier: phase 0 completed by one arrive
     if (threadIdx.x == 0) mbar_arrive(bar2);
@@ -145,6 +168,12 @@ int main() {
     cudaError_t e = run(5, gap);
     printf("mode F (2 issuing warps x 12) gap %3d: %6lld / %6lld clk (%.1f per MMA) (%s)\n", gap,
            h[0], h[1], (h[0] > h[1] ? h[0] : h[1]) / 24.0, cudaGetErrorString(e));
+  }
+  {
+    cudaError_t e = run(6, 0);
+    printf("mode G: commit->wait: none %lld / 1 MMA %lld (issue returned at %lld) / 3 MMAs %lld clk;"
+           " rep2: %lld %lld %lld (%s)\n", h[6], h[7], h[22], h[8], h[3], h[4], h[5],
+           cudaGetErrorString(e));
   }
   cudaError_t e = run(3, 0);
   printf("mode D: satisfied try_wait 32 lanes %lld clk, 1 lane %lld clk (%s)\n", h[0], h[1],

@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(128, 1) check(const uint8_t* gA, const uint8_t
 // ---- 2. throughput: warp 0 issues `iters` MMA pairs; warps 1..8 optionally
 // stream tcgen05.ld over columns [256, 480) while it runs
 template <int KIND, int N>
-__global__ void __launch_bounds__(32 * 17, 1) thr(int iters, int readers, long long* clk) {
+__global__ void __launch_bounds__(32 * 17, 1) thr(int iters, int readers, int packed, long long* clk) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ __align__(8) unsigned long long bar;
   __shared__ uint32_t s_tmem;
@@ -145,7 +145,10 @@ __global__ void __launch_bounds__(32 * 17, 1) thr(int iters, int readers, long l
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem);
   if (threadIdx.x == 0) {
     const long long t0 = clock64();
-    if (KIND == 0) {  // kind::i8, K-chains of 5 x K=32 (K=160)
+    if (iters < 0) {  // no MMAs: readers alone for -iters clocks
+      while (clock64() - t0 < -(long long)iters) {
+      }
+    } else if (KIND == 0) {  // kind::i8, K-chains of 5 x K=32 (K=160)
       const uint64_t ad = umma_desc(base, 128, 1280), bd = umma_desc(base + 20480, 128, 1280);
       for (int i = 0; i < iters; ++i)
         for (int kb = 0; kb < 5; ++kb)
@@ -173,13 +176,24 @@ __global__ void __launch_bounds__(32 * 17, 1) thr(int iters, int readers, long l
     // (inside accumulator 1, which the MMAs do not touch), 4 loads per wait
     while (!s_done) {
       uint32_t v[64];
-      tmem_ld16(tq + 240 + 32 * (((warp - 1) / 4) % 4), v);
-      tmem_ld16(tq + 256 + 32 * (((warp - 1) / 4) % 4), v + 16);
-      tmem_ld16(tq + 240 + 32 * (((warp - 1) / 4) % 4) + 8, v + 32);
-      tmem_ld16(tq + 256 + 32 * (((warp - 1) / 4) % 4) + 8, v + 48);
-      tmem_ld_wait();
-      for (int j = 0; j < 64; ++j) acc ^= v[j];
-      loads += 2;  // 64 columns = two 32-column units
+      if (packed) {
+        // 4 x (32 columns as 16 packed registers): 128 columns per wait
+        tmem_ld16p(tq + 240 + 32 * (((warp - 1) / 4) % 4), v);
+        tmem_ld16p(tq + 272 + 32 * (((warp - 1) / 4) % 4), v + 16);
+        tmem_ld16p(tq + 240 + 32 * (((warp - 1) / 4) % 4) + 8, v + 32);
+        tmem_ld16p(tq + 272 + 32 * (((warp - 1) / 4) % 4) + 8, v + 48);
+        tmem_ld_wait();
+        for (int j = 0; j < 64; ++j) acc ^= v[j];
+        loads += 4;
+      } else {
+        tmem_ld16(tq + 240 + 32 * (((warp - 1) / 4) % 4), v);
+        tmem_ld16(tq + 256 + 32 * (((warp - 1) / 4) % 4), v + 16);
+        tmem_ld16(tq + 240 + 32 * (((warp - 1) / 4) % 4) + 8, v + 32);
+        tmem_ld16(tq + 256 + 32 * (((warp - 1) / 4) % 4) + 8, v + 48);
+        tmem_ld_wait();
+        for (int j = 0; j < 64; ++j) acc ^= v[j];
+        loads += 2;  // 64 columns = two 32-column units
+      }
     }
     if ((threadIdx.x & 31) == 0) atomicAdd((unsigned long long*)&clk[2 * blockIdx.x + 1], loads);
     if (acc == 0x12345678u) clk[0] = 0;
@@ -258,16 +272,16 @@ bool run_check() {
 }
 
 template <int KIND, int N>
-void run_thr(int readers) {
+void run_thr(int readers, int packed = 0, int iters_arg = 4000) {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   long long* clk;
   cudaMalloc(&clk, sizeof(long long) * 2 * sms);
-  const int smem = 64 * 1024, iters = 4000;
+  const int smem = 64 * 1024, iters = iters_arg;
   cudaFuncSetAttribute(thr<KIND, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   for (int rep = 0; rep < 2; ++rep) {
     cudaMemset(clk, 0, sizeof(long long) * 2 * sms);
-    thr<KIND, N><<<sms, 32 * 17, smem>>>(iters, readers, clk);
+    thr<KIND, N><<<sms, 32 * 17, smem>>>(iters, readers, packed, clk);
   }
   cudaError_t e = cudaDeviceSynchronize();
   std::vector<long long> h(2 * sms);
@@ -277,9 +291,9 @@ void run_thr(int readers) {
     mx = h[2 * i] > mx ? h[2 * i] : mx;
     loads += h[2 * i + 1];
   }
-  const double macs = (double)iters * 128 * N * (KIND ? 192 : 160);
-  printf("%s N=%d readers=%d: %7.0f MACs/clk/SM, %6.1f clk per K=160 tile, tcgen05.ld %6.0f B/clk/SM (%s)\n",
-         KIND ? "mxf4" : "i8  ", N, readers, macs / mx, (double)mx / iters,
+  const double macs = iters < 0 ? 0.0 : (double)iters * 128 * N * (KIND ? 192 : 160);
+  printf("%s N=%d readers=%d packed=%d: %7.0f MACs/clk/SM, %6.1f clk per K=160 tile, tcgen05.ld %6.0f B/clk/SM (%s)\n",
+         KIND ? "mxf4" : "i8  ", N, readers, packed, macs / mx, (double)mx / iters,
          (double)loads * 32 * 32 * 4 / sms / mx, cudaGetErrorString(e));
   cudaFree(clk);
 }
@@ -287,6 +301,8 @@ void run_thr(int readers) {
 int main() {
   run_check<256>();
   run_check<240>();
-  for (int readers : {0, 4, 8, 12, 16}) run_thr<1, 240>(readers);
+  for (int readers : {0, 8, 16}) run_thr<1, 240>(readers, 0);
+  for (int readers : {8, 16}) run_thr<1, 240>(readers, 1);
+  for (int packed : {0, 1}) run_thr<1, 240>(16, packed, -2000000);
   return 0;
 }
