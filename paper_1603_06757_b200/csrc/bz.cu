@@ -474,7 +474,8 @@ int ensure_level(bz_ctx* ctx, int D, int floor) {
   const size_t n = (size_t)binom_sat(ctx->k - floor, D);
   const size_t N = bz::kUmmaN4;
   ctx->lvl_rows[i] = (n + N - 1) / N * N + N;
-  const size_t bytes = (size_t)ctx->m * ctx->lvl_rows[i] * 16 * ctx->w32;
+  const size_t row_bytes = 16 * (size_t)(bz::k5_padmagic(ctx->w32) ? ctx->w32 + 1 : ctx->w32);
+  const size_t bytes = (size_t)ctx->m * ctx->lvl_rows[i] * row_bytes;
   CK(grow(ctx, (void**)&ctx->d_lvl[i], &ctx->lvl_cap[i], bytes));
   int rc;
   switch (ctx->w32) {

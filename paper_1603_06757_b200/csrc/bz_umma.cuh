@@ -70,8 +70,13 @@ constexpr int kUmmaM = 128;       // prefixes per A tile = producer threads
 // constant operands): the fp32 sum then carries the integer dot product in
 // its low 16 bits, so the epilogue reads them with .pack::16b (half the
 // register traffic) and reduces packed s16 pairs, like K4.
+// For odd W the offset rides on the zero K padding chunk instead: the last
+// real MMA's padding block gets A = 1.5, B = 1.0 (every table row carries
+// the extra chunk) and an A scale of 2^23 for that block only, so no extra
+// MMA is issued.
 constexpr bool kK5Magic = BZ_K5_MAGIC != 0;
 constexpr int kSfColMagic = 496;  // ue8m0 2^23 scale columns of the magic MMA
+constexpr int kSfColPad = 504;    // A scales (1, 2^23): block 0 = chunk W-1, block 1 = pad
 constexpr uint32_t kMagicBytes = 512;  // A and B magic operands (K = 64, SBO = 0)
 constexpr int kUmmaN = BZ_K4_N;   // K4 triples per B tile
 constexpr int kUmmaMA = BZ_K4_MA; // K4 A tiles (consecutive prefix steps) per B tile
@@ -109,7 +114,11 @@ struct K4Roles {
 
 template <bool F4> __host__ __device__ constexpr int k4_n() { return F4 ? kUmmaN4 : kUmmaN; }
 // bytes per table (B) row: K4 one byte per column, K5 one nibble
-template <bool F4> __host__ __device__ constexpr int k4_row_bytes(int w) { return F4 ? 16 * w : 32 * w; }
+// K5 with the padding-chunk offset (odd W): tables carry the pad chunk
+__host__ __device__ constexpr bool k5_padmagic(int w) { return kK5Magic && (w & 1); }
+template <bool F4> __host__ __device__ constexpr int k4_row_bytes(int w) {
+  return F4 ? 16 * (k5_padmagic(w) ? w + 1 : w) : 32 * w;
+}
 // 16-byte K chunks per A row (K5 pads to whole K = 64 MMAs)
 template <bool F4> __host__ __device__ constexpr int k4_a_chunks(int w) {
   return F4 ? 2 * ((w + 1) / 2) : 2 * w;
@@ -427,7 +436,7 @@ __global__ void k_build_subsets_mxf4(const uint32_t* __restrict__ rows,
   const uint32_t* R = rows + (size_t)j * k * WP;
   const unsigned long long base = binom[(k - 1 - a) * kBinomDim + D];
   const unsigned long long cnt = binom[(k - 1 - a) * kBinomDim + (D - 1)];
-  uint8_t* tab = out + (size_t)j * gamma_stride_rows * (16 * W);
+  uint8_t* tab = out + (size_t)j * gamma_stride_rows * k4_row_bytes<true>(W);
   for (unsigned long long t = threadIdx.x; t < cnt; t += blockDim.x) {
     uint32_t v[W];
 #pragma unroll
@@ -445,10 +454,13 @@ __global__ void k_build_subsets_mxf4(const uint32_t* __restrict__ rows,
       for (int w = 0; w < W; ++w) v[w] ^= R[e * WP + w];
       ++e;
     }
+    constexpr int C = k4_row_bytes<true>(W) / 16;  // chunks per row (+ pad chunk)
     const unsigned long long row = base + t;
-    uint8_t* grp = tab + (size_t)(row >> 3) * (8 * 16 * W) + (row & 7) * 16;
+    uint8_t* grp = tab + (size_t)(row >> 3) * (8 * 16 * C) + (row & 7) * 16;
 #pragma unroll
     for (int w = 0; w < W; ++w) *reinterpret_cast<uint4*>(grp + w * 128) = e2m1_bits01(v[w]);
+    if constexpr (C > W)  // offset chunk: 1.0 at element 0
+      *reinterpret_cast<uint4*>(grp + W * 128) = make_uint4(0x2u, 0u, 0u, 0u);
   }
 }
 
@@ -654,7 +666,8 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
     if (warp < 4) {
       for (int c = 0; c < 512 - kSfCol; c += 8)
         tmem_st8(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(kSfCol + c),
-                 kSfCol + c == kSfColMagic ? 0x96969696u : 0x7F7F7F7Fu);
+                 kSfCol + c == kSfColMagic ? 0x96969696u
+                                           : (kSfCol + c == kSfColPad ? 0x7F7F967Fu : 0x7F7F7F7Fu));
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
     if (kK5Magic && tid < (int)kMagicBytes / 16) {
@@ -668,9 +681,11 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       fence_proxy_async();
     }
     if (CA > W && warp >= RL::PROD0) {
+      // the A padding chunk: zero, or 1.5 at element 0 (padding-chunk offset)
       const int r = tid - 32 * RL::PROD0;
       for (int ab = 0; ab < NA; ++ab)
-        *reinterpret_cast<uint4*>(sA + ab * TA + umma_off_c(r, W, CA)) = make_uint4(0, 0, 0, 0);
+        *reinterpret_cast<uint4*>(sA + ab * TA + umma_off_c(r, W, CA)) =
+            make_uint4(k5_padmagic(W) ? 0x3u : 0u, 0u, 0u, 0u);
       fence_proxy_async();
     }
     tc_fence_before();
@@ -923,6 +938,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       const uint64_t a_desc0 = umma_desc(sA_s, 128, CA * 128);
       const uint64_t b_desc0 = umma_desc(sB_s, 128, CB * 128);
       const uint32_t sfa = tmem + kSfCol, sfb = tmem + kSfCol + 8, sfm = tmem + kSfColMagic;
+      const uint32_t sfp = tmem + kSfColPad;
       // magic operands: one core matrix per K chunk, SBO = 0 (every 8-row
       // group reads the same 8 rows)
       const uint32_t sM = (uint32_t)__cvta_generic_to_shared(sMagic);
@@ -976,13 +992,14 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
                   for (int j = 0; j < kUmmaMA; ++j) {
                     const uint32_t dj = dbase + (uint32_t)(j * N + h * NH);
                     const uint64_t adj = a_desc0 + (uint64_t)((ab * kUmmaMA + j) * (TA >> 4));
-                    if constexpr (F4 && kK5Magic)
-                      umma_mxf4(dj, magic_a, magic_b, IDESC, 0u, sfm, sfb);
+                    constexpr bool kExtra = F4 && kK5Magic && !k5_padmagic(W);
+                    if constexpr (kExtra) umma_mxf4(dj, magic_a, magic_b, IDESC, 0u, sfm, sfb);
 #pragma unroll
                     for (int kb = 0; kb < P; ++kb) {
                       if constexpr (F4)
                         umma_mxf4(dj, adj + 16u * kb, bd0 + 16u * kb, IDESC,
-                                  (kb > 0 || kK5Magic) ? 1u : 0u, sfa, sfb);
+                                  (kb > 0 || kExtra) ? 1u : 0u,
+                                  (k5_padmagic(W) && kb == P - 1) ? sfp : sfa, sfb);
                       else
                         umma_i8(dj, adj + 16u * kb, bd0 + 16u * kb, IDESC, kb > 0 ? 1u : 0u);
                     }
