@@ -15,6 +15,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -195,15 +197,31 @@ struct Levels {
   int floor[kMaxLevel + 2] = {}; // floor[D] for D in 3..dmax; floor[dmax+1] = k
 };
 
+// C(p, q) as double for 0 <= p, q <= BZ_MAX_K (cost model only)
+double binom_d(int p, int q) {
+  static const std::vector<double> t = [] {
+    std::vector<double> v((BZ_MAX_K + 1) * (BZ_MAX_K + 1), 0.0);
+    for (int a = 0; a <= BZ_MAX_K; ++a) {
+      v[a * (BZ_MAX_K + 1)] = 1.0;
+      for (int b = 1; b <= a; ++b)
+        v[a * (BZ_MAX_K + 1) + b] = v[(a - 1) * (BZ_MAX_K + 1) + b - 1] +
+                                    (b <= a - 1 ? v[(a - 1) * (BZ_MAX_K + 1) + b] : 0.0);
+    }
+    return v;
+  }();
+  if (p < 0 || q < 0 || q > p || p > BZ_MAX_K) return 0.0;
+  return t[p * (BZ_MAX_K + 1) + q];
+}
+
 double k5_cost(int k, int g, const Levels& lv) {
   const double kTile = 727.0, kStep = 1271.0;  // K5 clocks (cfg5, B200)
   double cost = 0;
   for (int D = 3; D <= lv.dmax; ++D) {
     const int hi = std::min(lv.floor[D + 1] - 1, k - 1 - D);
     for (int ell = g - 1 - D; ell <= hi; ++ell) {
-      const double np = (double)binom_sat(ell, g - 1 - D);
+      const double np = binom_d(ell, g - 1 - D);
       const int f = std::max(ell + 1, lv.floor[D]);
-      const double slice = (double)binom_sat(k - f, D);
+      const double slice = binom_d(k - f, D);
       if (np == 0 || slice == 0) continue;
       const double steps = std::ceil(np / bz::kUmmaM);
       cost += steps * (std::ceil(slice / bz::kUmmaN4) * kTile + kStep);
@@ -212,7 +230,24 @@ double k5_cost(int k, int g, const Levels& lv) {
   return cost;
 }
 
+Levels k5_levels_search(int k, int g);
+
+// memoised per (k, g, BZ_K5_FLOORS): the search costs milliseconds and every
+// round's plan (every process the same) asks for it
 Levels k5_levels(int k, int g) {
+  static std::mutex mu;
+  static std::map<std::string, Levels> memo;
+  const char* env = getenv("BZ_K5_FLOORS");
+  const std::string key = std::to_string(k) + "/" + std::to_string(g) + "/" + (env ? env : "");
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = memo.find(key);
+  if (it != memo.end()) return it->second;
+  const Levels lv = k5_levels_search(k, g);
+  memo.emplace(key, lv);
+  return lv;
+}
+
+Levels k5_levels_search(int k, int g) {
   Levels best;
   best.floor[3] = 0;
   best.floor[4] = k;
@@ -455,9 +490,10 @@ int build_triples_w(bz_ctx* ctx, int which) {
 
 template <int W>
 int build_level_w(bz_ctx* ctx, int D, int floor) {
-  dim3 grid(ctx->k - D - floor + 1, ctx->m);
+  const unsigned long long n = binom_sat(ctx->k - floor, D);
+  dim3 grid((unsigned)((n + 255) / 256), ctx->m);
   bz::k_build_subsets_mxf4<W><<<grid, 256, 0, ctx->stream>>>(
-      ctx->d_rows, ctx->d_lvl[D - 3], ctx->k, D, floor, ctx->lvl_rows[D - 3], ctx->d_binom);
+      ctx->d_rows, ctx->d_lvl[D - 3], ctx->k, D, n, ctx->lvl_rows[D - 3], ctx->d_binom);
   CK(cudaGetLastError());
   ctx->launches += 1;
   return BZ_OK;

@@ -422,46 +422,47 @@ struct K4Tables {
 
 // K5 suffix table of level D: every D-subset of rows [floor, k), smallest
 // element a descending (so the subsets with smallest element >= f are the
-// first C(k - f, D) rows), then the other D - 1 elements lex.  One block per
-// (a, Gamma), one thread per subset; rows stored as e2m1 0 / 1.0 nibbles in
-// the UMMA K-major no-swizzle layout (W 16-byte chunks per row).
+// first C(k - f, D) rows), then the other D - 1 elements lex.  One thread per
+// table row (grid.y = Gamma); rows stored as e2m1 0 / 1.0 nibbles in the
+// UMMA K-major no-swizzle layout (+ the offset chunk for odd W).
 template <int W>
 __global__ void k_build_subsets_mxf4(const uint32_t* __restrict__ rows,
-                                     uint8_t* __restrict__ out, int k, int D, int floor,
-                                     size_t gamma_stride_rows,
+                                     uint8_t* __restrict__ out, int k, int D,
+                                     unsigned long long nrows, size_t gamma_stride_rows,
                                      const unsigned long long* __restrict__ binom) {
   constexpr int WP = padded_words(W);
-  const int j = blockIdx.y, a = floor + blockIdx.x;
-  if (a > k - D) return;
+  constexpr int C = k4_row_bytes<true>(W) / 16;  // chunks per row (+ offset chunk)
+  const unsigned long long row = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= nrows) return;
+  const int j = blockIdx.y;
   const uint32_t* R = rows + (size_t)j * k * WP;
-  const unsigned long long base = binom[(k - 1 - a) * kBinomDim + D];
-  const unsigned long long cnt = binom[(k - 1 - a) * kBinomDim + (D - 1)];
-  uint8_t* tab = out + (size_t)j * gamma_stride_rows * k4_row_bytes<true>(W);
-  for (unsigned long long t = threadIdx.x; t < cnt; t += blockDim.x) {
-    uint32_t v[W];
+  // smallest element a: rows of a start at C(k-1-a, D); x = k-1-a is the
+  // largest x with C(x, D) <= row
+  int x = D - 1;  // C(D-1, D) = 0: row 0 is the subset {k-D, ..., k-1}
+  while (x + 1 <= k - 1 && binom[(x + 1) * kBinomDim + D] <= row) ++x;
+  const int a = k - 1 - x;
+  unsigned long long r = row - binom[x * kBinomDim + D];
+  uint32_t v[W];
 #pragma unroll
-    for (int w = 0; w < W; ++w) v[w] = R[a * WP + w];
-    // lex unrank of t among the (D-1)-subsets of [a+1, k)
-    unsigned long long r = t;
-    int e = a + 1;
-    for (int i = D - 1; i >= 1; --i) {
-      for (;; ++e) {
-        const unsigned long long c = binom[(k - 1 - e) * kBinomDim + (i - 1)];
-        if (r < c) break;
-        r -= c;
-      }
-#pragma unroll
-      for (int w = 0; w < W; ++w) v[w] ^= R[e * WP + w];
-      ++e;
+  for (int w = 0; w < W; ++w) v[w] = R[a * WP + w];
+  // lex unrank of r among the (D-1)-subsets of [a+1, k)
+  int e = a + 1;
+  for (int i = D - 1; i >= 1; --i) {
+    for (;; ++e) {
+      const unsigned long long c = binom[(k - 1 - e) * kBinomDim + (i - 1)];
+      if (r < c) break;
+      r -= c;
     }
-    constexpr int C = k4_row_bytes<true>(W) / 16;  // chunks per row (+ pad chunk)
-    const unsigned long long row = base + t;
-    uint8_t* grp = tab + (size_t)(row >> 3) * (8 * 16 * C) + (row & 7) * 16;
 #pragma unroll
-    for (int w = 0; w < W; ++w) *reinterpret_cast<uint4*>(grp + w * 128) = e2m1_bits01(v[w]);
-    if constexpr (C > W)  // offset chunk: 1.0 at element 0
-      *reinterpret_cast<uint4*>(grp + W * 128) = make_uint4(0x2u, 0u, 0u, 0u);
+    for (int w = 0; w < W; ++w) v[w] ^= R[e * WP + w];
+    ++e;
   }
+  uint8_t* grp = out + (size_t)j * gamma_stride_rows * (16 * C) + (size_t)(row >> 3) * (8 * 16 * C) +
+                 (row & 7) * 16;
+#pragma unroll
+  for (int w = 0; w < W; ++w) *reinterpret_cast<uint4*>(grp + w * 128) = e2m1_bits01(v[w]);
+  if constexpr (C > W)  // offset chunk: 1.0 at element 0
+    *reinterpret_cast<uint4*>(grp + W * 128) = make_uint4(0x2u, 0u, 0u, 0u);
 }
 
 // ---------------------------------------------------------------------------
