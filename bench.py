@@ -262,7 +262,11 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_value = rep.counters.combinations / e2e_s
-    wp = 1 if w32 <= 1 else 2 if w32 <= 2 else 4 if w32 <= 4 else 8
+    # the device stores only the kept columns (identity-column elision)
+    mask = ctx.elided()
+    n_eff = max((n - k) if (mask >> j) & 1 else n for j in range(m))
+    w_eff = (max(n_eff, 1) + 31) // 32
+    wp = 1 if w_eff <= 1 else 2 if w_eff <= 2 else 4 if w_eff <= 4 else 8
     h2d = m * k * wp * 4 + m * (k + 1) * wp * 4  # padded rows + prefix-XOR table
     d2h = 0
     for (g, L, U) in rep.bounds_trace:
@@ -279,17 +283,22 @@ def main():
 
     # ---- roofline of the dominant kernel (largest round), and the other two
     # kernels on the same launch for comparison
-    peaks = ctx.measure_int_peaks(w32)
+    # words per stored row: identity-column elision drops k columns of every
+    # Gamma that has a unit column per row (all of them for config 5), so the
+    # kernels run on W_eff = ceil((n - k) / 32) words -- the rooflines below
+    # use that as their own denominator
+    peaks = ctx.measure_int_peaks(w_eff)
     top_ms = statistics.median(g_top_ms)
     achieved = (g_top_combos / world) / (top_ms * 1e-3)
-    # MACs per combination: the K of the weight GEMM, i.e. the padded
-    # codeword -- K4 (kind::i8) 32 per word, K5 (kind::mxf4) K = 64 steps
-    macs_i8 = 32 * w32
-    macs_f4 = 64 * ((w32 + 1) // 2)
+    # MACs per combination: the K of the weight GEMM, i.e. the padded stored
+    # row -- K4 (kind::i8) 32 per word, K5 (kind::mxf4) K = 64 steps
+    macs_i8 = 32 * w_eff
+    macs_f4 = 64 * ((w_eff + 1) // 2)
+    macs_f4_full = 64 * ((w32 + 1) // 2)
     mxf4_peak = peaks["mxf4_mac_per_s"] / macs_f4
     umma_peak = peaks["umma_mac_per_s"] / macs_i8
     imma_peak = peaks["imma_mac_per_s"] / macs_i8
-    popc_peak = peaks["popc_per_s"] / w32
+    popc_peak = peaks["popc_per_s"] / w_eff
     g_top = max(st.rounds, key=lambda r: r.combinations).g
 
     def engine_rate(engine):
@@ -304,6 +313,12 @@ def main():
     k1_achieved = engine_rate("popc")
     k3_achieved = engine_rate("imma")
     k4_achieved = engine_rate("umma")
+    # the same K5 launch without elision (full n-column rows)
+    ctx.set_elision(False)
+    backend.load(gs, n)
+    k5_full = engine_rate(cfg.engine)
+    ctx.set_elision(True)
+    backend.load(gs, n)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
@@ -318,6 +333,7 @@ def main():
                    "k": k, "n": n, "m": m, "d": rep.distance, "g_final": rep.g_reached,
                    "combinations_per_step": int(combos_all / args.steps),
                    "engine": cfg.engine,
+                   "identity_elision": bool(mask),
                    "parallelism": f"rank-space shards x{world}",
                    "l2": "flushed (256 MiB memset) before every timed step; working set "
                          "(rows, prefix table, triple tables) is L2/shared-memory resident"},
@@ -329,31 +345,43 @@ def main():
         "roofline": {"bound": "tensor", "achieved": achieved / 1e9, "peak": mxf4_peak / 1e9,
                      "unit": "Gcombinations/s", "frac": achieved / mxf4_peak,
                      "traffic": traffic,
-                     "kernel": f"k4_round_umma<{w32},true> = K5, round g={g_top} "
+                     "kernel": f"k4_round_umma<{w_eff},true> = K5, round g={g_top} "
                                f"(tcgen05.mma kind::mxf4, unit block scales)",
                      "peak_source": f"live microbenchmark: tcgen05.mma kind::mxf4 M128xN240xK64 "
                                     f"{peaks['mxf4_mac_per_clk_sm']:.0f} MACs/clk/SM, "
                                     f"{peaks['mxf4_mac_per_s'] / 1e15:.2f} PMAC/s / "
-                                    f"{macs_f4} MACs per combination (K padded to 64)",
+                                    f"{macs_f4} MACs per combination (stored K = "
+                                    f"{32 * w_eff} padded to 64)",
                      "popc_roofline": popc_peak / 1e9,
-                     "frac_of_popc_roofline": achieved / popc_peak},
-        "k4_umma_i8": {"kernel": f"k4_round_umma<{w32},false> round g={g_top} "
+                     "frac_of_popc_roofline": achieved / popc_peak,
+                     "identity_elision": {
+                         "on": bool(mask), "gamma_mask": mask, "stored_columns": n_eff,
+                         "words": w_eff,
+                         "note": "rows of Gammas with a unit column per row are stored without "
+                                 "those k columns and every weight gets +g (exact); rooflines "
+                                 "use the stored K as their denominator"},
+                     "without_elision": {
+                         "achieved": k5_full / 1e9,
+                         "peak": peaks["mxf4_mac_per_s"] / macs_f4_full / 1e9,
+                         "frac": k5_full / (peaks["mxf4_mac_per_s"] / macs_f4_full),
+                         "macs_per_combination": macs_f4_full}},
+        "k4_umma_i8": {"kernel": f"k4_round_umma<{w_eff},false> round g={g_top} "
                                  f"(tcgen05.mma kind::i8)",
                        "achieved": k4_achieved / 1e9, "peak": umma_peak / 1e9,
                        "unit": "Gcombinations/s", "frac": k4_achieved / umma_peak,
                        "peak_source": f"live microbenchmark: {peaks['umma_mac_per_clk_sm']:.0f} "
                                       f"MACs/clk/SM / {macs_i8} MACs per combination"},
-        "k3_imma": {"kernel": f"k3_round_gemm<{w32}> round g={g_top} (legacy mma.sync s8)",
+        "k3_imma": {"kernel": f"k3_round_gemm<{w_eff}> round g={g_top} (legacy mma.sync s8)",
                     "achieved": k3_achieved / 1e9, "peak": imma_peak / 1e9,
                     "unit": "Gcombinations/s", "frac": k3_achieved / imma_peak,
                     "peak_source": f"live microbenchmark: {peaks['imma_mac_per_clk_sm']:.0f} "
                                    f"IMMA MACs/clk/SM / {macs_i8} MACs per combination"},
-        "k1_popc": {"kernel": f"k1_round_min<{w32},2> round g={g_top} (XOR+POPC)",
+        "k1_popc": {"kernel": f"k1_round_min<{w_eff},2> round g={g_top} (XOR+POPC)",
                     "achieved": k1_achieved / 1e9, "peak": popc_peak / 1e9,
                     "unit": "Gcombinations/s", "frac": k1_achieved / popc_peak,
                     "peak_source": f"live microbenchmark: {peaks['popc_per_clk_sm']:.1f} POPC/clk/SM"
-                                   f" / {w32} POPC per combination",
-                    "alu_peak": peaks["lop3_per_s"] / (2 * w32) / 1e9},
+                                   f" / {w_eff} POPC per combination",
+                    "alu_peak": peaks["lop3_per_s"] / (2 * w_eff) / 1e9},
     }
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(G, gs, args.cpu_sample_g)

@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define BZ_ABI_VERSION 3
+#define BZ_ABI_VERSION 4
 
 /* limits of the device kernels */
 #define BZ_MAX_K 128 /* rows per Gamma (prefix masks are 128-bit)      */
@@ -82,6 +82,18 @@ void bz_destroy(bz_ctx *ctx);
 
 /* Human-readable description of the last error on ctx (never NULL). */
 const char *bz_last_error(const bz_ctx *ctx);
+
+/* Identity-column elision (default on; applies from the next
+ * bz_load_gammas): a Gamma with one unit column per row -- every full-rank
+ * information set from build_gamma_set (m/gf2.py:133-199) -- is stored
+ * without those k columns and its weights get + g, which is exact because
+ * each chosen row carries exactly one of them.  The remainder Gamma (rank <
+ * k) keeps all n columns.  Results are identical either way. */
+int bz_set_elision(bz_ctx *ctx, int on);
+
+/* Bit j set: Gamma j of the loaded family was stored with its identity
+ * columns dropped. */
+int bz_elided(bz_ctx *ctx, uint64_t *out_mask);
 
 /* Select the enumeration engine for later calls (BZ_ENGINE_*).  Results
  * are identical; only the kernel and the work plan differ. */

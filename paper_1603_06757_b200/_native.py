@@ -18,7 +18,7 @@ from .errors import (DeviceError, InvalidArity, InvalidDimensions, MindistError,
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BZ_LIB") or os.path.join(PKG_DIR, "libbz.so")
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 BZ_OK = 0
 _CODES = {
@@ -33,7 +33,8 @@ _CODES = {
 
 # every symbol include/bz.h declares (checked by tests/test_abi.py)
 SYMBOLS = ("bz_abi_version", "bz_device_count", "bz_create", "bz_destroy",
-           "bz_last_error", "bz_set_engine", "bz_load_gammas", "bz_round", "bz_rounds",
+           "bz_last_error", "bz_set_engine", "bz_set_elision", "bz_elided", "bz_load_gammas",
+           "bz_round", "bz_rounds",
            "bz_enumerate",
            "bz_histogram", "bz_plan", "bz_timer_start", "bz_timer_stop",
            "bz_last_kernel_ms", "bz_launch_count", "bz_measure_int_peaks")
@@ -64,6 +65,8 @@ def lib():
     L.bz_last_error.argtypes = [vp]
     L.bz_last_error.restype = ctypes.c_char_p
     L.bz_set_engine.argtypes = [vp, c_int]
+    L.bz_set_elision.argtypes = [vp, c_int]
+    L.bz_elided.argtypes = [vp, u64p]
     L.bz_load_gammas.argtypes = [vp, u64p, c_int, c_int, c_int]
     L.bz_round.argtypes = [vp, c_int, c_int, c_int, c_int, c_int, i32p, u64p]
     L.bz_rounds.argtypes = [vp, c_int, c_int, i32p, c_int, c_int, c_int, i32p, u64p]
@@ -133,6 +136,7 @@ class Context:
                 self._h = None
         self.device = device
         self.engine = "auto"
+        self.elision = True
         self.loaded_key = None
         self.m = self.k = self.n = 0
 
@@ -166,6 +170,19 @@ class Context:
             raise ValueError(f"unknown engine {engine!r}")
         check(lib().bz_set_engine(self.handle, ENGINES[engine]), self.handle, "bz_set_engine")
         self.engine = engine
+
+    def set_elision(self, on: bool) -> None:
+        """Identity-column elision for the next load (see bz_set_elision);
+        results are identical either way."""
+        check(lib().bz_set_elision(self.handle, 1 if on else 0), self.handle, "bz_set_elision")
+        self.elision = bool(on)
+        self.loaded_key = None
+
+    def elided(self) -> int:
+        """Bit mask of the loaded Gammas stored without identity columns."""
+        v = np.zeros(1, dtype=np.uint64)
+        check(lib().bz_elided(self.handle, _ptr(v, ctypes.c_uint64)), self.handle, "bz_elided")
+        return int(v[0])
 
     def load(self, words: np.ndarray, n: int, key=None) -> None:
         """words: (m, k, ceil(n/64)) uint64 row image of the family.  `key`

@@ -41,6 +41,8 @@ struct bz_ctx {
   // loaded family
   int m = 0, k = 0, n = 0, w32 = 0, wp = 0;
   int engine = BZ_ENGINE_AUTO;
+  int elision = 1;                   // bz_set_elision (applies at the next load)
+  unsigned long long elide_mask = 0; // Gammas loaded with identity columns dropped
   uint32_t* d_rows = nullptr;   // m*k*wp
   uint8_t* d_trip = nullptr;    // K3 triple tables: m x trip_rows rows of 0/1 bytes
   size_t trip_rows = 0;         // rows per Gamma (C(k,3) + one tile of padding)
@@ -676,6 +678,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     a.shard = shard;
     a.nshards = nshards;
     a.lower_prev = lower_prev ? lower_prev[i] : 0;
+    a.elide = ctx->elide_mask;
     a.debug = debug;
     a.trace = (i == count - 1) ? trace : nullptr;
     a.trace_from = getenv("BZ_K4_TRACE_FROM") ? atoi(getenv("BZ_K4_TRACE_FROM")) : 0;
@@ -828,28 +831,55 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
   if (n > BZ_MAX_N) return fail(ctx, BZ_ERR_TOO_LARGE, "n=%d exceeds %d", n, BZ_MAX_N);
   CK(cudaSetDevice(ctx->device));
   const int w64 = (n + 63) / 64;
-  const int w32 = (n + 31) / 32;
+  // validate padding
+  for (int j = 0; j < m; ++j)
+    for (int r = 0; r < k; ++r) {
+      const uint64_t* src = rows + ((size_t)j * k + r) * w64;
+      const int keep = n - 64 * (w64 - 1);
+      const uint64_t mask = keep >= 64 ? ~0ull : ((1ull << keep) - 1ull);
+      if (src[w64 - 1] & ~mask)
+        return fail(ctx, BZ_ERR_INVALID_DIMENSIONS,
+                    "Gamma %d row %d has bits outside columns 0..%d", j, r, n - 1);
+    }
+  auto bit = [&](int j, int r, int c) -> int {
+    return (int)((rows[((size_t)j * k + r) * w64 + (c >> 6)] >> (c & 63)) & 1ull);
+  };
+  // Identity-column elision: a Gamma with one unit column per row (every
+  // full-rank information set, m/gf2.py:133-199) has exactly one 1 of those
+  // columns in each chosen row, so the weight of any g-combination is
+  // g + the weight of its other n - k columns.  Those columns are dropped
+  // here and the kernels add g back (RoundArgs::elide).
+  std::vector<std::vector<int>> keep_cols(m);
+  unsigned long long elide = 0;
+  int n_eff = 1;
+  for (int j = 0; j < m; ++j) {
+    std::vector<char> drop(n, 0);
+    bool ok = ctx->elision && m <= 64 && k < n;
+    for (int r = 0; ok && r < k; ++r) {
+      int unit = -1;
+      for (int c = 0; c < n && unit < 0; ++c) {
+        if (!bit(j, r, c)) continue;
+        int ones = 0;
+        for (int rr = 0; rr < k && ones < 2; ++rr) ones += bit(j, rr, c);
+        if (ones == 1) unit = c;
+      }
+      if (unit < 0) ok = false; else drop[unit] = 1;
+    }
+    for (int c = 0; c < n; ++c)
+      if (!(ok && drop[c])) keep_cols[j].push_back(c);
+    if (ok) elide |= 1ull << j;
+    n_eff = std::max(n_eff, (int)keep_cols[j].size());
+  }
+  const int w32 = (n_eff + 31) / 32;
   const int wp = bz::padded_words(w32);
-  // validate padding, repack to padded 32-bit rows, build prefix-XOR tables
+  // repack the kept columns to padded 32-bit rows, build prefix-XOR tables
   std::vector<uint32_t> img((size_t)m * k * wp, 0u);
   std::vector<uint32_t> px((size_t)m * (k + 1) * wp, 0u);
   for (int j = 0; j < m; ++j) {
     for (int r = 0; r < k; ++r) {
-      const uint64_t* src = rows + ((size_t)j * k + r) * w64;
-      for (int w = 0; w < w64; ++w) {
-        uint64_t v = src[w];
-        const int lo_bit = 64 * w;
-        if (lo_bit + 64 > n) {
-          const int keep = n - lo_bit;
-          const uint64_t mask = keep >= 64 ? ~0ull : ((1ull << keep) - 1ull);
-          if (v & ~mask)
-            return fail(ctx, BZ_ERR_INVALID_DIMENSIONS,
-                        "Gamma %d row %d has bits outside columns 0..%d", j, r, n - 1);
-        }
-        const int w0 = 2 * w, w1 = 2 * w + 1;
-        if (w0 < w32) img[((size_t)j * k + r) * wp + w0] = (uint32_t)v;
-        if (w1 < w32) img[((size_t)j * k + r) * wp + w1] = (uint32_t)(v >> 32);
-      }
+      uint32_t* dst = img.data() + ((size_t)j * k + r) * wp;
+      for (size_t i = 0; i < keep_cols[j].size(); ++i)
+        if (bit(j, r, keep_cols[j][i])) dst[i >> 5] |= 1u << (i & 31);
     }
     for (int r = 0; r < k; ++r)
       for (int w = 0; w < wp; ++w)
@@ -879,6 +909,7 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
   ctx->n = n;
   ctx->w32 = w32;
   ctx->wp = wp;
+  ctx->elide_mask = elide;
   return BZ_OK;
 }
 
@@ -944,6 +975,18 @@ int bz_histogram(bz_ctx* ctx, int gamma, int g, int shard, int nshards, uint64_t
   for (int b = 0; b <= ctx->n; ++b) out_hist[b] = ctx->h_hist[b];
   *out_min = slot_bound(ctx, 0)[0];
   *out_combos = slot_combos(ctx, 0)[gamma];
+  return BZ_OK;
+}
+
+int bz_set_elision(bz_ctx* ctx, int on) {
+  if (!ctx) return BZ_ERR_ARGUMENT;
+  ctx->elision = on ? 1 : 0;
+  return BZ_OK;
+}
+
+int bz_elided(bz_ctx* ctx, uint64_t* out_mask) {
+  if (!ctx || !out_mask) return BZ_ERR_ARGUMENT;
+  *out_mask = ctx->elide_mask;
   return BZ_OK;
 }
 

@@ -67,6 +67,8 @@ struct RoundArgs {
   int m, k, g, n;
   int shard, nshards;
   int lower_prev;              // early exit once bound[0] <= lower_prev
+  unsigned long long elide;    // bit j: Gamma j's identity columns were dropped at load
+                               // time, so its codeword weights get + g (see bz_load_gammas)
   int debug;                   // K4 timing experiments only (see BZ_K4_DEBUG)
   long long* trace;            // K4 debug timeline (BZ_K4_DEBUG & 8), else null
   int trace_from;              // first traced tile (BZ_K4_TRACE_FROM)
@@ -238,6 +240,12 @@ struct Walker {
     if (i2 > 0) xor_px<W>(acc, PX, i2);
   }
 };
+
+// Weight of the dropped identity columns of Gamma j: every chosen row has
+// exactly one of them set.
+__device__ __forceinline__ int gamma_woff(const RoundArgs& a, int gamma) {
+  return (gamma < 64 && ((a.elide >> gamma) & 1ull)) ? a.g : 0;
+}
 
 // Locate the group owning `chunk` (groups sorted by chunk_begin).
 __device__ __forceinline__ int find_group(const Group* sg, int ngroups,
@@ -411,7 +419,8 @@ k1_round_min(const RoundArgs a) {
     }
 
     // chunk epilogue: warp min -> per-Gamma and round minima; combos count
-    const int wbest = __reduce_min_sync(FULL, best);
+    int wbest = __reduce_min_sync(FULL, best);
+    if (wbest != INT_MAX) wbest += gamma_woff(a, v.gr.gamma);
     const unsigned tot = __reduce_add_sync(FULL, (unsigned)v.cnt);
     if (lane == 0) {
       if (wbest < vbound[1 + v.gr.gamma]) atomicMin(a.bound + 1 + v.gr.gamma, wbest);
@@ -505,11 +514,14 @@ k1h_histogram(const RoundArgs a) {
       atomicAdd(a.combos + v.gr.gamma, (unsigned long long)tot * suffix_count<D>(k, e0));
   }
   flush();
+  // the pass is one Gamma (all groups share it): shift by its dropped
+  // identity weight
+  const int off = a.ngroups > 0 ? gamma_woff(a, sgroups[0].gamma) : 0;
   const int wbest = __reduce_min_sync(FULL, best);
-  if (lane == 0 && wbest < INT_MAX) atomicMin(a.bound, wbest);
+  if (lane == 0 && wbest < INT_MAX) atomicMin(a.bound, wbest + off);
   __syncthreads();
-  for (int b = tid; b < nbins; b += bd)
-    if (bhist[b]) atomicAdd(a.hist + b, (unsigned long long)bhist[b]);
+  for (int b = tid; b + off < nbins; b += bd)
+    if (bhist[b]) atomicAdd(a.hist + b + off, (unsigned long long)bhist[b]);
 }
 
 // ---------------------------------------------------------------------------

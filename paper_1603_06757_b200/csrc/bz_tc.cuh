@@ -300,7 +300,8 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
     const long long col_lo = (long long)tile_lo * kTileRows;
     const long long col_hi = min((long long)tile_hi * kTileRows, (long long)slice);
     const unsigned long long ncols = (unsigned long long)(col_hi - col_lo);
-    const int wbest = __reduce_min_sync(FULL, best);
+    int wbest = __reduce_min_sync(FULL, best);
+    if (wbest < INT_MAX / 2) wbest += gamma_woff(a, gr.gamma);
     const unsigned tot = __reduce_add_sync(FULL, (unsigned)cnt);
     if (lane == 0) {
       if (wbest < vbound[1 + gr.gamma]) atomicMin(a.bound + 1 + gr.gamma, wbest);

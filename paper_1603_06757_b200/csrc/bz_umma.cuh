@@ -63,6 +63,9 @@ constexpr int kUmmaM = 128;       // prefixes per A tile = producer threads
 #ifndef BZ_K5_SPLIT
 #define BZ_K5_SPLIT 1
 #endif
+#ifndef BZ_K5_EPI_GROUPS
+#define BZ_K5_EPI_GROUPS 1
+#endif
 #ifndef BZ_K5_MAGIC
 #define BZ_K5_MAGIC 1
 #endif
@@ -109,7 +112,15 @@ struct K4Roles {
   // the epilogue drains part 0 while the MMAs of part 1 still run, and the
   // next tile's part-0 MMAs start as soon as part 0 is drained
   static constexpr int SPLIT = F4 ? BZ_K5_SPLIT : 1;
-  static_assert(E % 4 == 0 && ACC * SPLIT <= kMaxAcc && (E / 4) % SPLIT == 0, "roles");
+  // epilogue groups: group q drains the tiles t with t % EGRP == q (each
+  // group covers the whole accumulator), so a group has EGRP tile periods
+  // for its loads and reductions while the other groups take the tiles in
+  // between
+  static constexpr int EGRP = F4 ? BZ_K5_EPI_GROUPS : 1;
+  static constexpr int EW = E / EGRP;  // warps per group
+  static_assert(E % 4 == 0 && ACC * SPLIT <= kMaxAcc && EW % 4 == 0 && (EW / 4) % SPLIT == 0 &&
+                    ACC % EGRP == 0,
+                "roles");
 };
 
 template <bool F4> __host__ __device__ constexpr int k4_n() { return F4 ? kUmmaN4 : kUmmaN; }
@@ -591,13 +602,15 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
   using RL = K4Roles<F4>;
   constexpr int ACC = RL::ACC;
   constexpr int E = RL::E;
-  constexpr int EC = N / (E / 4);  // columns per epilogue warp and A tile
+  constexpr int EGRP = RL::EGRP;
+  constexpr int EC = N / (RL::EW / 4);  // columns per epilogue warp and A tile
   constexpr int SPLIT = RL::SPLIT;
   constexpr int NH = N / SPLIT;  // accumulator columns per part
   static_assert(NH % 8 == 0, "parts are whole 8-row groups of the B tile");
   constexpr uint32_t IDESC = F4 ? mxf4_idesc(NH) : kUmmaIdesc;
   static_assert(S <= kMaxStages, "barrier slots");
-  static_assert(EC * (E / 4) == N && (F4 ? EC % 4 == 0 && EC <= 128 : EC % 32 == 0), "epilogue");
+  static_assert(EC * (RL::EW / 4) == N && (F4 ? EC % 4 == 0 && EC <= 128 : EC % 32 == 0),
+                "epilogue");
   extern __shared__ __align__(128) unsigned char smem[];
   const size_t base = (smem_base_bytes<W>(a.m, a.k, a.ngroups) + 1023) & ~size_t(1023);
   unsigned char* sB = smem + base;
@@ -640,7 +653,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
     }
     for (int i = 0; i < ACC * SPLIT; ++i) {
       mbar_init(accfull(i), 1);                  // MMA commit
-      mbar_init(accempty(i), E / SPLIT);         // each epilogue warp of the part
+      mbar_init(accempty(i), RL::EW / SPLIT);    // each epilogue warp of the part
     }
     for (int i = 0; i < kChunkQ; ++i) {
       mbar_init(qfull(i), 1);                    // loader
@@ -699,8 +712,9 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
   if (warp < E) {
     // ================= epilogue: warp e reads TMEM lanes 32(e%4).. (rows),
     // columns [EC*(e/4), +EC) of each accumulator
-    const int quarter = warp & 3, slice_id = warp >> 2;
-    const int part = slice_id / ((E / 4) / SPLIT);  // accumulator part this warp drains
+    const int egroup = warp / RL::EW;  // this warp drains tiles t % EGRP == egroup
+    const int quarter = warp & 3, slice_id = (warp % RL::EW) >> 2;
+    const int part = slice_id / ((RL::EW / 4) / SPLIT);  // accumulator part this warp drains
     const int r = 32 * quarter + lane;
     uint32_t grp = 0, tcount = 0, toff = k4_trace_off(a);
     for (uint32_t qi = 0;; ++qi) {
@@ -727,6 +741,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
         for (int j = 0; j < kUmmaMA; ++j) rmin[j] = INT_MAX / 2;
         float fmin_acc = __int_as_float(0x7f800000);  // K5: +inf
         for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount) {
+          if (EGRP > 1 && (int)(tcount % EGRP) != egroup) continue;
           const int buf = tcount % ACC;
           const int hb = buf * SPLIT + part;
           if (warp == 0 && lane == 0) k4_trace(a, 8, tcount, toff);
@@ -856,7 +871,8 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
 #pragma unroll
         for (int j = 0; j < kUmmaMA; ++j) best = min(best, rmin[j] + wt[j]);
       }
-      const int wbest = __reduce_min_sync(FULL, best);
+      int wbest = __reduce_min_sync(FULL, best);
+      if (wbest < INT_MAX / 2) wbest += gamma_woff(a, c.gr.gamma);
       if (lane == 0) {
         volatile int* vb = a.bound;
         if (wbest < vb[1 + c.gr.gamma]) atomicMin(a.bound + 1 + c.gr.gamma, wbest);

@@ -89,6 +89,7 @@ class EngineConfig:
     # sharded, across ranks); 0 disables batching
     batch_combinations: int = 2_000_000_000
     engine: str = "auto"     # "auto" | "mxf4" | "umma" | "imma" | "popc" (kernel; same results)
+    elide_identity: bool = True  # drop each full-rank Gamma's identity columns (+g; exact)
 
 
 @dataclass
@@ -154,6 +155,8 @@ class GpuRounds:
             dev = int(os.environ.get("LOCAL_RANK", "0"))
         self.ctx = _native.context(dev)
         self.ctx.set_engine(config.engine)
+        if self.ctx.elision != config.elide_identity:
+            self.ctx.set_elision(config.elide_identity)
         self.comm = comm
 
     def load(self, gs: GammaSet, n: int) -> None:

@@ -247,3 +247,43 @@ def test_mxf4_levels(monkeypatch, ctx, k, g, floors, n):
         want = oracle.min_weight(gammas[j], n, g)[0]
         assert mins[j] == want, (j, mins, want)
         assert combos[j] == comb(k, g)
+
+
+@pytest.mark.parametrize("name,seed,mask", [("cfg1", 2, 0b11), ("cfg2", 1, 0b11),
+                                            ("cfg3", 1, 0b111), ("cfg3", 2, 0b111)])
+def test_identity_elision(ctx, name, seed, mask):
+    """Gammas with a unit column per row are stored without those columns
+    (+g on every weight).  That includes cfg3's remainder: k_m counts its new
+    pivots, but like every Gamma it spans the full row space and keeps the
+    earlier pivots' unit columns.  The whole BZ run is identical with
+    elision on and off, for every engine."""
+    G, gs, _ = code(name, seed)
+    reports = {}
+    for elide in (True, False):
+        for eng in ("auto", "umma", "popc"):
+            rep = minimum_distance(G, EngineConfig(engine=eng, elide_identity=elide))
+            if elide:
+                assert ctx.elided() == mask
+            reports[(elide, eng)] = (rep.distance, tuple(map(tuple, rep.bounds_trace)),
+                                     rep.counters.combinations)
+    assert len(set(reports.values())) == 1, reports
+    _native.context(0).set_elision(True)
+
+
+def test_identity_elision_systematic_histogram(ctx):
+    """[I | A] (cfg4's generator): elided min and histogram equal the
+    un-elided ones, bin for bin (the histogram is shifted by g)."""
+    gm = microbench_gamma(3)  # random_systematic_matrix(64, 192, 3)
+    out = {}
+    for elide in (True, False):
+        ctx.set_elision(elide)
+        words = family_words([gm], gm.num_cols)
+        ctx.load(words, gm.num_cols)
+        assert ctx.elided() == (1 if elide else 0)
+        for g in (3, 4):
+            hist, mn, c = ctx.histogram(0, g)
+            out[(elide, g)] = (list(hist), mn, c)
+    ctx.set_elision(True)
+    for g in (3, 4):
+        assert out[(True, g)] == out[(False, g)]
+        assert out[(True, g)][1] == min(i for i, v in enumerate(out[(True, g)][0]) if v)
