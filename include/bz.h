@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define BZ_ABI_VERSION 4
+#define BZ_ABI_VERSION 5
 
 /* limits of the device kernels */
 #define BZ_MAX_K 128 /* rows per Gamma (prefix masks are 128-bit)      */
@@ -82,6 +82,15 @@ void bz_destroy(bz_ctx *ctx);
 
 /* Human-readable description of the last error on ctx (never NULL). */
 const char *bz_last_error(const bz_ctx *ctx);
+
+/* Host-only Gauss-Jordan (reduce_on_columns, m/gf2.py:133-161): reduce the
+ * k x n matrix `rows` (row-major, ceil(n/64) u64 words per row, bit j =
+ * column j) in place, taking pivots from `cols` in the given order (leftmost
+ * available row, swapped to the top, eliminated from every other row).
+ * Writes the pivot columns to out_pivots (capacity k, may be NULL) and the
+ * rank to *out_rank.  Needs no device. */
+int bz_reduce_on_columns(uint64_t *rows, int k, int n, const int32_t *cols, int ncols,
+                         int32_t *out_pivots, int *out_rank);
 
 /* Identity-column elision (default on; applies from the next
  * bz_load_gammas): a Gamma with one unit column per row -- every full-rank

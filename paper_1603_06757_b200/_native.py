@@ -18,7 +18,7 @@ from .errors import (DeviceError, InvalidArity, InvalidDimensions, MindistError,
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BZ_LIB") or os.path.join(PKG_DIR, "libbz.so")
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 BZ_OK = 0
 _CODES = {
@@ -33,7 +33,8 @@ _CODES = {
 
 # every symbol include/bz.h declares (checked by tests/test_abi.py)
 SYMBOLS = ("bz_abi_version", "bz_device_count", "bz_create", "bz_destroy",
-           "bz_last_error", "bz_set_engine", "bz_set_elision", "bz_elided", "bz_load_gammas",
+           "bz_last_error", "bz_set_engine", "bz_set_elision", "bz_elided",
+           "bz_reduce_on_columns", "bz_load_gammas",
            "bz_round", "bz_rounds",
            "bz_enumerate",
            "bz_histogram", "bz_plan", "bz_timer_start", "bz_timer_stop",
@@ -66,6 +67,7 @@ def lib():
     L.bz_last_error.restype = ctypes.c_char_p
     L.bz_set_engine.argtypes = [vp, c_int]
     L.bz_set_elision.argtypes = [vp, c_int]
+    L.bz_reduce_on_columns.argtypes = [u64p, c_int, c_int, i32p, c_int, i32p, ctypes.POINTER(c_int)]
     L.bz_elided.argtypes = [vp, u64p]
     L.bz_load_gammas.argtypes = [vp, u64p, c_int, c_int, c_int]
     L.bz_round.argtypes = [vp, c_int, c_int, c_int, c_int, c_int, i32p, u64p]

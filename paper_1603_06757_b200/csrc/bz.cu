@@ -855,14 +855,14 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
   for (int j = 0; j < m; ++j) {
     std::vector<char> drop(n, 0);
     bool ok = ctx->elision && m <= 64 && k < n;
+    // column weights, then each row's first column of weight 1
+    std::vector<int> ones(n, 0);
+    for (int r = 0; ok && r < k; ++r)
+      for (int c = 0; c < n; ++c) ones[c] += bit(j, r, c);
     for (int r = 0; ok && r < k; ++r) {
       int unit = -1;
-      for (int c = 0; c < n && unit < 0; ++c) {
-        if (!bit(j, r, c)) continue;
-        int ones = 0;
-        for (int rr = 0; rr < k && ones < 2; ++rr) ones += bit(j, rr, c);
-        if (ones == 1) unit = c;
-      }
+      for (int c = 0; c < n && unit < 0; ++c)
+        if (ones[c] == 1 && bit(j, r, c)) unit = c;
       if (unit < 0) ok = false; else drop[unit] = 1;
     }
     for (int c = 0; c < n; ++c)
@@ -975,6 +975,35 @@ int bz_histogram(bz_ctx* ctx, int gamma, int g, int shard, int nshards, uint64_t
   for (int b = 0; b <= ctx->n; ++b) out_hist[b] = ctx->h_hist[b];
   *out_min = slot_bound(ctx, 0)[0];
   *out_combos = slot_combos(ctx, 0)[gamma];
+  return BZ_OK;
+}
+
+int bz_reduce_on_columns(uint64_t* rows, int k, int n, const int32_t* cols, int ncols,
+                         int32_t* out_pivots, int* out_rank) {
+  if (!rows || !out_rank || (ncols > 0 && !cols)) return BZ_ERR_ARGUMENT;
+  if (k < 1 || n < 1 || k > 4096 || n > 65536) return BZ_ERR_INVALID_DIMENSIONS;
+  const int w = (n + 63) / 64;
+  std::vector<uint64_t> tmp(w);
+  int top = 0;
+  for (int i = 0; i < ncols && top < k; ++i) {
+    const int col = cols[i];
+    if (col < 0 || col >= n) return BZ_ERR_INVALID_DIMENSIONS;
+    const int cw = col >> 6;
+    const uint64_t cb = 1ull << (col & 63);
+    int hit = -1;
+    for (int r = top; r < k; ++r)
+      if (rows[(size_t)r * w + cw] & cb) { hit = r; break; }
+    if (hit < 0) continue;
+    if (hit != top)
+      for (int x = 0; x < w; ++x) std::swap(rows[(size_t)hit * w + x], rows[(size_t)top * w + x]);
+    const uint64_t* pr = rows + (size_t)top * w;
+    for (int r = 0; r < k; ++r)
+      if (r != top && (rows[(size_t)r * w + cw] & cb))
+        for (int x = 0; x < w; ++x) rows[(size_t)r * w + x] ^= pr[x];
+    if (out_pivots) out_pivots[top] = col;
+    ++top;
+  }
+  *out_rank = top;
   return BZ_OK;
 }
 
