@@ -34,7 +34,7 @@ from . import _native
 from .enumeration import EnumerationResult, family_words
 from .errors import InvalidArity, InvalidDimensions, Interrupted
 from .gf2 import BitMatrix, GammaSet, build_gamma_set
-from .parallel import LocalComm
+from .parallel import LocalComm, combine_rounds
 
 STRATEGIES = ("gpu",)
 
@@ -169,10 +169,12 @@ class GpuRounds:
         return mins, combos, kernel_ms
 
     def run_batch(self, g0: int, lower_prevs: list[int], upper: int):
-        """Rounds g0.. in one call, computed whole on every rank (no
-        exchange): [(mins, combos)] per round and the batch's kernel ms."""
-        res = self.ctx.rounds(g0, lower_prevs, upper)
-        return res, self.ctx.last_kernel_ms()
+        """Rounds g0.. in one call, each sharded over the ranks like a single
+        round, then one exchange for all of them: [(mins, combos)] per round
+        and the batch's kernel ms."""
+        res = self.ctx.rounds(g0, lower_prevs, upper, self.comm.rank, self.comm.world)
+        ms = self.ctx.last_kernel_ms()
+        return combine_rounds(self.comm, res), ms
 
 
 def make_backend(config: EngineConfig, comm):
@@ -229,10 +231,13 @@ def run_rounds(backend, gs: GammaSet, k: int, config: EngineConfig, st: LoopStat
             break
         tr = time.perf_counter()
         if not queued and batch_ok:
-            # the next rounds whose total size fits the batch budget
+            # the next rounds whose total size fits the batch budget (per
+            # rank: a batch is sharded like a round)
+            world = getattr(getattr(backend, "comm", None), "world", 1)
+            budget = config.batch_combinations * world
             count, total = 0, 0
             while (st.g + count <= min(k, config.max_g)
-                   and total + m * comb(k, st.g + count) <= config.batch_combinations):
+                   and total + m * comb(k, st.g + count) <= budget):
                 total += m * comb(k, st.g + count)
                 count += 1
             if count >= 2:

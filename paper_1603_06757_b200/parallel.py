@@ -67,3 +67,15 @@ class TorchComm:
 
     def barrier(self) -> None:
         self._dist.barrier(group=self.group)
+
+
+def combine_rounds(comm, res):
+    """Combine several rounds' per-rank (mins, combos) with ONE exchange:
+    the vectors are concatenated, reduced (min / sum) and split again."""
+    if comm.world == 1 or not res:
+        return [(list(mn), list(cb)) for mn, cb in res]
+    m = len(res[0][0])
+    mins, combos = comm.combine([v for mn, _ in res for v in mn],
+                                [v for _, cb in res for v in cb])
+    return [(mins[i * m:(i + 1) * m], combos[i * m:(i + 1) * m]) for i in range(len(res))]
+
