@@ -318,6 +318,11 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
   lv.floor[shape.depth + 1] = k;
   if (shape.kernel == 5) lv = k5_levels(k, g);
   const int dmin = shape.depth;
+  // K4/K5: the round's last ~15 % of combinations (in chunk order, which is
+  // the order the CTAs draw them in) go in chunks 8x finer, so the SMs
+  // finish together instead of waiting on a few large last chunks
+  const unsigned long long fine_from = total - total / 7;
+  unsigned long long done = 0;
   for (int j = j0; j < j1; ++j) {
     for (int depth = dmin; depth <= lv.dmax; ++depth) {
       const int ell_lo = g == 1 ? -1 : g - 1 - depth;
@@ -331,6 +336,9 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
         const long long work = (long long)binom_sat(k - sfloor, depth);
         if (work == 0) continue;
         const bool tiled = depth >= 3;
+        const long long lt =
+            (shape.kernel >= 4 && done >= fine_from) ? std::max(4096ll, lane_target / 8) : lane_target;
+        done += np * (unsigned long long)work;
         const long long lanes_ll = shape.lanes;
         const long long spread = (long long)((np + lanes_ll - 1) / lanes_ll);
         // D >= 3: every prefix step also rebuilds the A operand and streams
@@ -338,14 +346,14 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
         // slices near ell = k - 4
         const long long step_cost =
             tiled ? std::max(work, (long long)shape.tile_rows) + 256 : work;
-        long long ppl = std::max(1ll, lane_target / std::max(1ll, step_cost));
+        long long ppl = std::max(1ll, lt / std::max(1ll, step_cost));
         ppl = std::min(ppl, std::max(1ll, spread));
         // D >= 3: a chunk is lanes prefixes x ppl steps x tpc tiles; a slice
         // too large for one chunk is split into tile blocks
         const long long trows = tiled ? shape.tile_rows : 1;
         long long ntiles = (work + trows - 1) / trows;
         long long tpc = ntiles;
-        if (tiled && work > lane_target) tpc = std::max(1ll, lane_target / trows);
+        if (tiled && work > lt) tpc = std::max(1ll, lt / trows);
         const long long ntb = tiled ? (ntiles + tpc - 1) / tpc : 1;
         Group gr{};
         gr.chunk_begin = chunk;
