@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define BZ_ABI_VERSION 5
+#define BZ_ABI_VERSION 6
 
 /* limits of the device kernels */
 #define BZ_MAX_K 128 /* rows per Gamma (prefix masks are 128-bit)      */
@@ -82,6 +82,15 @@ void bz_destroy(bz_ctx *ctx);
 
 /* Human-readable description of the last error on ctx (never NULL). */
 const char *bz_last_error(const bz_ctx *ctx);
+
+/* GPU brute force (brute_force_distance, m/engine.py:223-237): the minimum
+ * weight over all 2^k - 1 nonzero messages of the k x n generator `rows`
+ * (ceil(n/64) u64 words per row, bit j = column j), Gray-code order, one
+ * row XOR per codeword.  k <= min(max_k, 48) else BZ_ERR_TOO_LARGE.
+ * Zero-weight codewords (rank-deficient G) give 0, as in the reference;
+ * *out_codewords = 2^k - 1. */
+int bz_brute_force(bz_ctx *ctx, const uint64_t *rows, int k, int n, int max_k,
+                   int32_t *out_distance, uint64_t *out_codewords);
 
 /* Host-only Gauss-Jordan (reduce_on_columns, m/gf2.py:133-161): reduce the
  * k x n matrix `rows` (row-major, ceil(n/64) u64 words per row, bit j =

@@ -18,7 +18,7 @@ from .errors import (DeviceError, InvalidArity, InvalidDimensions, MindistError,
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BZ_LIB") or os.path.join(PKG_DIR, "libbz.so")
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 BZ_OK = 0
 _CODES = {
@@ -34,7 +34,7 @@ _CODES = {
 # every symbol include/bz.h declares (checked by tests/test_abi.py)
 SYMBOLS = ("bz_abi_version", "bz_device_count", "bz_create", "bz_destroy",
            "bz_last_error", "bz_set_engine", "bz_set_elision", "bz_elided",
-           "bz_reduce_on_columns", "bz_load_gammas",
+           "bz_reduce_on_columns", "bz_brute_force", "bz_load_gammas",
            "bz_round", "bz_rounds",
            "bz_enumerate",
            "bz_histogram", "bz_plan", "bz_timer_start", "bz_timer_stop",
@@ -67,6 +67,7 @@ def lib():
     L.bz_last_error.restype = ctypes.c_char_p
     L.bz_set_engine.argtypes = [vp, c_int]
     L.bz_set_elision.argtypes = [vp, c_int]
+    L.bz_brute_force.argtypes = [vp, u64p, c_int, c_int, c_int, i32p, u64p]
     L.bz_reduce_on_columns.argtypes = [u64p, c_int, c_int, i32p, c_int, i32p, ctypes.POINTER(c_int)]
     L.bz_elided.argtypes = [vp, u64p]
     L.bz_load_gammas.argtypes = [vp, u64p, c_int, c_int, c_int]
@@ -185,6 +186,17 @@ class Context:
         v = np.zeros(1, dtype=np.uint64)
         check(lib().bz_elided(self.handle, _ptr(v, ctypes.c_uint64)), self.handle, "bz_elided")
         return int(v[0])
+
+    def brute_force(self, words: np.ndarray, n: int, max_k: int):
+        """(distance, codewords) over all 2^k - 1 messages (bz_brute_force)."""
+        words = np.ascontiguousarray(words, dtype=np.uint64)
+        d = np.zeros(1, dtype=np.int32)
+        c = np.zeros(1, dtype=np.uint64)
+        check(lib().bz_brute_force(self.handle, _ptr(words, ctypes.c_uint64), words.shape[0],
+                                   n, max_k, _ptr(d, ctypes.c_int32),
+                                   _ptr(c, ctypes.c_uint64)),
+              self.handle, "bz_brute_force")
+        return int(d[0]), int(c[0])
 
     def load(self, words: np.ndarray, n: int, key=None) -> None:
         """words: (m, k, ceil(n/64)) uint64 row image of the family.  `key`

@@ -24,6 +24,7 @@
 #include "bz_kernels.cuh"
 #include "bz_tc.cuh"
 #include "bz_umma.cuh"
+#include "bz_brute.cuh"
 
 using bz::Group;
 using bz::RoundArgs;
@@ -748,6 +749,23 @@ const unsigned long long* slot_combos(bz_ctx* ctx, int i) {
 
 }  // namespace
 
+namespace {
+template <int W>
+int launch_brute(bz_ctx* ctx, const uint32_t* d_rows, int k, unsigned long long nranges,
+                 unsigned long long* d_counter, int* d_best) {
+  int per_sm = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bz::k6_brute<W>, 256, 0));
+  const unsigned long long want = (nranges + 255) / 256;
+  const long long blocks =
+      std::max(1ll, std::min((long long)std::max(per_sm, 1) * ctx->sm_count, (long long)want));
+  bz::k6_brute<W><<<(unsigned)blocks, 256, 0, ctx->stream>>>(d_rows, k, nranges, d_counter,
+                                                             d_best);
+  CK(cudaGetLastError());
+  ctx->launches += 1;
+  return BZ_OK;
+}
+}  // namespace
+
 extern "C" {
 
 int bz_abi_version(void) { return BZ_ABI_VERSION; }
@@ -983,6 +1001,62 @@ int bz_histogram(bz_ctx* ctx, int gamma, int g, int shard, int nshards, uint64_t
   for (int b = 0; b <= ctx->n; ++b) out_hist[b] = ctx->h_hist[b];
   *out_min = slot_bound(ctx, 0)[0];
   *out_combos = slot_combos(ctx, 0)[gamma];
+  return BZ_OK;
+}
+
+
+int bz_brute_force(bz_ctx* ctx, const uint64_t* rows, int k, int n, int max_k,
+                   int32_t* out_distance, uint64_t* out_codewords) {
+  if (!ctx) return BZ_ERR_ARGUMENT;
+  if (ctx->device < 0) return fail(ctx, BZ_ERR_NO_DEVICE, "context has no device");
+  if (!rows || !out_distance) return fail(ctx, BZ_ERR_ARGUMENT, "null argument");
+  if (k < 1 || n < 1) return fail(ctx, BZ_ERR_INVALID_DIMENSIONS, "need k, n >= 1");
+  if (n > BZ_MAX_N) return fail(ctx, BZ_ERR_TOO_LARGE, "n=%d exceeds %d", n, BZ_MAX_N);
+  const int cap = std::min(max_k, bz::kBruteMaxK);
+  if (k > cap)
+    return fail(ctx, BZ_ERR_TOO_LARGE, "brute force limited to k <= %d (got %d)", cap, k);
+  CK(cudaSetDevice(ctx->device));
+  const int w64 = (n + 63) / 64, w32 = (n + 31) / 32, wp = bz::padded_words(w32);
+  std::vector<uint32_t> img((size_t)k * wp, 0u);
+  for (int r = 0; r < k; ++r)
+    for (int w = 0; w < w64; ++w) {
+      const uint64_t v = rows[(size_t)r * w64 + w];
+      if (2 * w < w32) img[(size_t)r * wp + 2 * w] = (uint32_t)v;
+      if (2 * w + 1 < w32) img[(size_t)r * wp + 2 * w + 1] = (uint32_t)(v >> 32);
+    }
+  const size_t bytes = img.size() * 4 + 16;
+  unsigned char* d = nullptr;
+  CK(cudaMallocAsync((void**)&d, bytes, ctx->stream));
+  unsigned long long* d_counter = reinterpret_cast<unsigned long long*>(d);
+  int* d_best = reinterpret_cast<int*>(d + 8);
+  uint32_t* d_rows = reinterpret_cast<uint32_t*>(d + 16);
+  const int init[2] = {0, INT32_MAX};
+  CK(cudaMemsetAsync(d_counter, 0, 8, ctx->stream));
+  CK(cudaMemcpyAsync(d_best, &init[1], 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(d_rows, img.data(), img.size() * 4, cudaMemcpyHostToDevice, ctx->stream));
+  const unsigned long long total = 1ull << k;
+  const unsigned long long nranges = (total + bz::kBruteSpan - 1) / bz::kBruteSpan;
+  CK(cudaEventRecord(ctx->ev_k0, ctx->stream));
+  int rc;
+  switch (w32) {
+    case 1: rc = launch_brute<1>(ctx, d_rows, k, nranges, d_counter, d_best); break;
+    case 2: rc = launch_brute<2>(ctx, d_rows, k, nranges, d_counter, d_best); break;
+    case 3: rc = launch_brute<3>(ctx, d_rows, k, nranges, d_counter, d_best); break;
+    case 4: rc = launch_brute<4>(ctx, d_rows, k, nranges, d_counter, d_best); break;
+    case 5: rc = launch_brute<5>(ctx, d_rows, k, nranges, d_counter, d_best); break;
+    case 6: rc = launch_brute<6>(ctx, d_rows, k, nranges, d_counter, d_best); break;
+    case 7: rc = launch_brute<7>(ctx, d_rows, k, nranges, d_counter, d_best); break;
+    default: rc = launch_brute<8>(ctx, d_rows, k, nranges, d_counter, d_best); break;
+  }
+  if (rc) return rc;
+  CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
+  int best = 0;
+  CK(cudaMemcpyAsync(&best, d_best, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaFreeAsync(d, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaEventElapsedTime(&ctx->last_kernel_ms, ctx->ev_k0, ctx->ev_k1));
+  *out_distance = best;  // INT32_MAX: every message maps to the zero word
+  if (out_codewords) *out_codewords = total - 1;
   return BZ_OK;
 }
 

@@ -30,9 +30,11 @@ import time
 from dataclasses import dataclass, field
 from math import comb
 
+import numpy as np
+
 from . import _native
 from .enumeration import EnumerationResult, family_words
-from .errors import InvalidArity, InvalidDimensions, Interrupted
+from .errors import InvalidArity, InvalidDimensions, Interrupted, TooLarge
 from .gf2 import BitMatrix, GammaSet, build_gamma_set
 from .parallel import LocalComm, combine_rounds
 
@@ -306,6 +308,21 @@ def minimum_distance(G: BitMatrix, config: EngineConfig | None = None) -> Distan
 # ---------------------------------------------------------------------------
 # report text: key=value lines plus one "g=.. L=.. U=.." line per completed
 # round -- the reference's checkpoint format (engine.py:245-285).
+
+
+def brute_force_distance(G: BitMatrix, max_k: int = 28, device: int | None = None) -> int:
+    """Minimum weight over all 2^k - 1 nonzero codewords (engine.py:223-237),
+    on the GPU (bz_brute_force: Gray-code order, one row XOR per message).
+    Same cap semantics as the reference (TooLarge above max_k); the device
+    kernel lifts the practical limit to k = 48."""
+    k = G.num_rows
+    if k > max_k:
+        raise TooLarge(f"k={k} exceeds brute-force cap {max_k}")
+    dev = device if device is not None else int(os.environ.get("LOCAL_RANK", "0"))
+    ctx = _native.context(dev)
+    words = np.ascontiguousarray(G.with_word_width(64).to_numpy(), dtype=np.uint64)
+    d, _ = ctx.brute_force(words, G.num_cols, max_k)
+    return d
 
 
 def format_report(r: DistanceReport) -> str:

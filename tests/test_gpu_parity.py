@@ -287,3 +287,45 @@ def test_identity_elision_systematic_histogram(ctx):
     for g in (3, 4):
         assert out[(True, g)] == out[(False, g)]
         assert out[(True, g)][1] == min(i for i, v in enumerate(out[(True, g)][0]) if v)
+
+
+def test_brute_force_goldens(goldens):
+    """GPU brute force (bz_brute_force) against the reference's
+    brute_force_distance on every golden code that has one."""
+    from paper_1603_06757_b200 import brute_force_distance
+
+    n_checked = 0
+    for fx in goldens["small"]["codes"]:
+        if "brute" in fx:
+            M = BitMatrix(hexrows(fx["rows"]), fx["n"])
+            assert brute_force_distance(M) == fx["brute"], fx["src"]
+            n_checked += 1
+    for fx in goldens["configs"]:
+        if fx["name"] == "cfg1":
+            M = BitMatrix(hexrows(fx["rows"]), fx["n"])
+            assert brute_force_distance(M) == fx["distance"]
+            n_checked += 1
+    assert n_checked >= 3
+
+
+@pytest.mark.parametrize("k,n", [(1, 5), (7, 31), (12, 33), (20, 100), (29, 64), (30, 256)])
+def test_brute_force_vs_oracle(k, n):
+    """Word widths 1..8; k = 29, 30 are beyond the reference's default cap
+    (max_k raised), checked against the C oracle's Gray walk."""
+    from paper_1603_06757_b200 import brute_force_distance
+
+    rng = random.Random(k * 1000 + n)
+    rows = [rng.getrandbits(n) for _ in range(k)]
+    M = BitMatrix(rows, n)
+    want = oracle.brute_distance(rows, n)
+    assert brute_force_distance(M, max_k=40) == want
+    if k > 28:
+        with pytest.raises(TooLarge):
+            brute_force_distance(M)
+
+
+def test_brute_force_rank_deficient():
+    from paper_1603_06757_b200 import brute_force_distance
+
+    M = BitMatrix([0b1011, 0b0110, 0b1101], 4)  # row 3 = row 1 ^ row 2
+    assert brute_force_distance(M) == 0
