@@ -66,6 +66,9 @@ constexpr int kUmmaM = 128;       // prefixes per A tile = producer threads
 #ifndef BZ_K5_EPI_GROUPS
 #define BZ_K5_EPI_GROUPS 1
 #endif
+#ifndef BZ_K5_NOFENCE
+#define BZ_K5_NOFENCE 0  // timing experiment only: drops the per-tile tcgen05 fences
+#endif
 #ifndef BZ_K5_MAGIC
 #define BZ_K5_MAGIC 1
 #endif
@@ -747,7 +750,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
           if (warp == 0 && lane == 0) k4_trace(a, 8, tcount, toff);
           mbar_wait(accfull(hb), (tcount / ACC) & 1);
           if (warp == 0 && lane == 0) k4_trace(a, 9, tcount, toff);
-          tc_fence_after();
+          if (!BZ_K5_NOFENCE) tc_fence_after();
           if (warp == 0 && lane == 0) k4_trace(a, 2, tcount, toff);
           if (warp == E - 1 && lane == 0) k4_trace(a, 7, tcount, toff);
           const int lim = min(N, c.slice - t * N) - EC * slice_id;
@@ -770,7 +773,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
             }
             if (NP % 2) asm volatile("" : "+r"(v[NP - 1]) : : "memory");
             if (warp == 0 && lane == 0) k4_trace(a, 10, tcount, toff);
-            tc_fence_before();
+            if (!BZ_K5_NOFENCE) tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(accempty(hb));  // accumulators are in registers
             if (warp == 0 && lane == 0) k4_trace(a, 11, tcount, toff);
@@ -804,7 +807,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
 #pragma unroll
             for (int i = 0; i < EC; i += 4) tmem_regs4_after_wait(v + i);
             if (warp == 0 && lane == 0) k4_trace(a, 10, tcount, toff);
-            tc_fence_before();
+            if (!BZ_K5_NOFENCE) tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(accempty(hb));  // accumulators are in registers
             if (warp == 0 && lane == 0) k4_trace(a, 11, tcount, toff);
@@ -994,7 +997,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
             for (int h = 0; h < SPLIT; ++h) {
               mbar_wait_fast(accempty(mb * SPLIT + h), ((tc / ACC) & 1) ^ 1);
               if (lane == 0 && h == 1) k4_trace(a, 13, tc, toff);
-              tc_fence_after();
+              if (!BZ_K5_NOFENCE) tc_fence_after();
               if (lane == 0 && h == 0) k4_trace(a, 1, tc, toff);
               // pass kb advances both start addresses by 32 bytes of K per
               // row = two core matrices = 256 B (16 in the 16-byte-granular
