@@ -491,7 +491,7 @@ int build_triples_w(bz_ctx* ctx, int which) {
     bz::k_build_triples<W><<<grid, 256, 0, ctx->stream>>>(ctx->d_rows, ctx->d_trip, ctx->k,
                                                           ctx->trip_rows);
   } else {
-    bz::k_build_triples_umma<W, false><<<grid, 256, 0, ctx->stream>>>(
+    bz::k_build_triples_umma<W><<<grid, 256, 0, ctx->stream>>>(
         ctx->d_rows, ctx->d_trip4, ctx->k, ctx->trip4_rows);
   }
   CK(cudaGetLastError());

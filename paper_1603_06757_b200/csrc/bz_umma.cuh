@@ -2,42 +2,47 @@
 // tensor cores (tcgen05.mma, accumulators in TMEM).
 //
 // Same algebra as K3 (bz_tc.cuh): w(P ^ S) = w(P) + sum_j (1 - 2 P_j) S_j,
-// prefixes P as +-1 (A, M = 128 rows), triples S as 0/1 (B, N columns), K =
-// the padded code columns.  A (Gamma, ell) group is the GEMM
-// [C(ell,g-4) prefixes] x [C(k-1-ell,3) triples]; D[r][c] + w(P_r) is the
-// weight of codeword (prefix r, triple c) and only its minimum is kept.
+// prefixes P as +-1 (A, M = 128 rows), suffixes S as 0/1 (B, N columns), K =
+// the padded stored code columns.  A (Gamma, ell, D) group is the GEMM
+// [C(ell, g-1-D) prefixes] x [its suffix slice]; D[r][c] + w(P_r) is the
+// weight of codeword (prefix r, suffix c) and only its minimum is kept.
 //
 //   K4  kind::i8: s8 operands (32 K per byte-pair chunk), N = 256, s32
 //       accumulators read back as packed s16 pairs.  W MMAs of K = 32.
-//   K5  kind::mxf4 with every block scale 1.0: +-1 and 0/1 are exact e2m1
+//       Triple table only (depth 3).
+//   K5  kind::mxf4 with unit block scales: +-1 and 0/1 are exact e2m1
 //       values, so the products and their fp32 sums are the same integers,
 //       at twice the i8 MAC rate from half the operand bytes.  N = 240
-//       (2 x 240 accumulator columns + the scale-factor columns fill TMEM),
-//       ceil(W/2) MMAs of K = 64; for odd W the last MMA reads one 16-byte
-//       chunk past the B row, which the A row's zero padding chunk cancels
-//       (every e2m1 code is finite).
+//       (2 x 240 accumulator columns + 32 scale-factor columns fill TMEM),
+//       ceil(W/2) MMAs of K = 64; suffix tables of depth 3, 4 and 5 (host
+//       level plan).  The accumulators start at 1.5 * 2^23 (on the K padding
+//       chunk for odd W, else one extra MMA), so their low 16 bits are the
+//       integer result and the epilogue reads packed s16 pairs.
 //
-// One persistent CTA per SM, warp-specialised, every hand-off an mbarrier:
-//   warps [0, E)   epilogue: warp e reads TMEM lanes 32(e%4).. (its prefix
-//                  rows) of column slice e/4 of each accumulator
-//                  (tcgen05.ld), min-reduces, and releases the buffer.
-//   warp E         TMEM allocator + MMA issuer (one elected lane): per tile
-//                  the K passes into one of two accumulators, then
-//                  tcgen05.commit to the barriers that free the B stage,
-//                  publish the accumulator and (last tile) free the A tile.
-//   warp E+1       loader: draws chunks from the round's global counter,
-//                  publishes them to the other roles through a small smem
-//                  queue, and streams each chunk's triple tiles with 1-D TMA
-//                  bulk copies (cp.async.bulk) into a ring of B stages.
-//   warps E+2..+5  producers: thread r walks prefix row r (colex walker) and
-//                  writes its A row into one of two A buffers.
+// One persistent CTA per SM, warp-specialised, every hand-off an mbarrier
+// (K4Roles):
+//   warps [0, E)        epilogue: warp e reads TMEM lanes 32(e%4).. (its
+//                       prefix rows) of one column slice of each accumulator
+//                       (tcgen05.ld), releases the buffer, min-reduces.
+//   warps E, E+1        MMA issuers (one elected lane each): issuer b owns
+//                       accumulator b and issues every other tile, then
+//                       tcgen05.commit to the barriers that free the B stage,
+//                       publish the accumulator and free the A tile.  Two
+//                       issuers hide each other's handshakes (a tcgen05.mma
+//                       issue stalls while the pipe is busy).
+//   warp E+2            loader: draws chunks from the round's global counter,
+//                       publishes them to the other roles through a small
+//                       smem queue, and streams each chunk's suffix tiles
+//                       with 1-D TMA bulk copies into a ring of B stages.
+//   warps E+3 .. E+6    producers: thread r walks prefix row r (colex
+//                       walker) and writes its A row into an A ring.
 //
-// Triple tables (device-built at load time): all C(k,3) row triples in the
-// K3 order (smallest element descending, then lex), stored directly in the
-// UMMA SWIZZLE_NONE K-major canonical layout -- 8-row x 16-byte core
-// matrices, the K chunks of an 8-row group contiguous -- so a tile is one
-// contiguous byte range and the TMA copy lands it in exactly the layout the
-// smem descriptor describes.
+// Suffix tables (device-built on first use): every D-subset of the rows
+// above a floor, smallest element descending, stored directly in the UMMA
+// SWIZZLE_NONE K-major canonical layout -- 8-row x 16-byte core matrices,
+// the K chunks of an 8-row group contiguous -- so a tile is one contiguous
+// byte range and the TMA copy lands it in exactly the layout the smem
+// descriptor describes.
 #pragma once
 
 #include "bz_tc.cuh"
@@ -480,15 +485,14 @@ __global__ void k_build_subsets_mxf4(const uint32_t* __restrict__ rows,
 }
 
 // ---------------------------------------------------------------------------
-// Triple tables, one block per (Gamma, a).  K4: 0/1 bytes (kind::i8), 2W
-// 16-byte K chunks per row.  K5: e2m1 nibbles 0x0 / 0x2 (kind::mxf4), W
-// 16-byte chunks per row (chunk w = code word w: 32 columns).
-template <int W, bool F4>
+// K4 triple table, one block per (Gamma, a): 0/1 bytes (kind::i8), 2W
+// 16-byte K chunks per row.  (K5's tables come from k_build_subsets_mxf4.)
+template <int W>
 __global__ void k_build_triples_umma(const uint32_t* __restrict__ rows,
                                      uint8_t* __restrict__ trip, int k,
                                      size_t gamma_stride_rows) {
   constexpr int WP = padded_words(W);
-  constexpr int RB = k4_row_bytes<F4>(W);  // bytes per table row
+  constexpr int RB = k4_row_bytes<false>(W);  // bytes per table row
   const int j = blockIdx.y, a = blockIdx.x;
   if (a > k - 3) return;
   const uint32_t* R = rows + (size_t)j * k * WP;
@@ -504,16 +508,12 @@ __global__ void k_build_triples_umma(const uint32_t* __restrict__ rows,
     const uint32_t v = R[a * WP + w] ^ R[b * WP + w] ^ R[c * WP + w];
     const long long row = base + pi;
     uint8_t* grp = out + (size_t)(row >> 3) * (8 * RB);
-    if constexpr (F4) {
-      *reinterpret_cast<uint4*>(grp + w * 128 + (row & 7) * 16) = e2m1_bits01(v);
-    } else {
-      // 32 bytes of word w = K chunks 2w and 2w+1 of this row
-      uint4 lo, hi;
-      lo.x = bit_nibble(v, 0);  lo.y = bit_nibble(v, 4);  lo.z = bit_nibble(v, 8);  lo.w = bit_nibble(v, 12);
-      hi.x = bit_nibble(v, 16); hi.y = bit_nibble(v, 20); hi.z = bit_nibble(v, 24); hi.w = bit_nibble(v, 28);
-      *reinterpret_cast<uint4*>(grp + (2 * w) * 128 + (row & 7) * 16) = lo;
-      *reinterpret_cast<uint4*>(grp + (2 * w + 1) * 128 + (row & 7) * 16) = hi;
-    }
+    // 32 bytes of word w = K chunks 2w and 2w+1 of this row
+    uint4 lo, hi;
+    lo.x = bit_nibble(v, 0);  lo.y = bit_nibble(v, 4);  lo.z = bit_nibble(v, 8);  lo.w = bit_nibble(v, 12);
+    hi.x = bit_nibble(v, 16); hi.y = bit_nibble(v, 20); hi.z = bit_nibble(v, 24); hi.w = bit_nibble(v, 28);
+    *reinterpret_cast<uint4*>(grp + (2 * w) * 128 + (row & 7) * 16) = lo;
+    *reinterpret_cast<uint4*>(grp + (2 * w + 1) * 128 + (row & 7) * 16) = hi;
   }
 }
 
