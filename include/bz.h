@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define BZ_ABI_VERSION 6
+#define BZ_ABI_VERSION 7
 
 /* limits of the device kernels */
 #define BZ_MAX_K 128 /* rows per Gamma (prefix masks are 128-bit)      */
@@ -60,11 +60,13 @@ extern "C" {
 #define BZ_ERR_ARGUMENT 7           /* null pointer, bad shard                   */
 
 /* enumeration engines (bz_set_engine) */
-#define BZ_ENGINE_AUTO 0 /* K5 for g >= 4, K1 otherwise                     */
+#define BZ_ENGINE_AUTO 0 /* K5p (W = 1, 3) or K5 for g >= 4, K1 otherwise   */
 #define BZ_ENGINE_POPC 1 /* K1 only: XOR + POPC on the integer pipes       */
 #define BZ_ENGINE_IMMA 2 /* K3 (legacy warp-level IMMA) for g >= 4        */
 #define BZ_ENGINE_UMMA 3 /* K4 (tcgen05.mma kind::i8, TMEM) for g >= 4     */
 #define BZ_ENGINE_MXF4 4 /* K5 (tcgen05.mma kind::mxf4, unit scales) g >= 4 */
+#define BZ_ENGINE_MXF4P 5 /* K5p: K5 with two codewords per accumulator     \
+                             column (stored words W = 1 or 3; else K5)     */
 
 typedef struct bz_ctx bz_ctx;
 

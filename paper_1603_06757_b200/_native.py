@@ -18,7 +18,7 @@ from .errors import (DeviceError, InvalidArity, InvalidDimensions, MindistError,
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BZ_LIB") or os.path.join(PKG_DIR, "libbz.so")
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 BZ_OK = 0
 _CODES = {
@@ -106,7 +106,7 @@ def device_count() -> int:
     return int(lib().bz_device_count())
 
 
-ENGINES = {"auto": 0, "popc": 1, "imma": 2, "umma": 3, "mxf4": 4}
+ENGINES = {"auto": 0, "popc": 1, "imma": 2, "umma": 3, "mxf4": 4, "mxf4p": 5}
 
 
 def plan(m: int, k: int, g: int, engine: str = "auto", nshards: int = 1):

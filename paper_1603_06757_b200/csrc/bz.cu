@@ -167,14 +167,22 @@ T* slot_ptr(unsigned char* base, const IoSlot& l, int i, size_t off) {
 // triples per tile.  K4 (tcgen05) and K3 (legacy IMMA) take D = 3 for
 // g >= 4; K1 (POPC) takes D = 2 for g >= 4, else 1.  Histograms run on K1.
 struct PlanShape {
-  int depth, lanes, tile_rows, kernel;  // kernel: 1 = K1, 3 = K3, 4 = K4
+  int depth, lanes, tile_rows, kernel;  // kernel: 1 = K1, 3 = K3, 4 = K4, 5 = K5, 6 = K5p
 };
 
-PlanShape pass_shape(int engine, int g, bool hist) {
+// K5p (two codewords per accumulator column) needs odd W <= 3 stored words
+bool k5p_ok(int w32) { return w32 == 1 || w32 == 3; }
+
+// w32: stored words of the loaded family (0 = unknown, host-only plans):
+// AUTO takes K5p where it applies, else K5
+PlanShape pass_shape(int engine, int g, bool hist, int w32 = 0) {
   if (!hist && g >= 4) {
     if (engine == BZ_ENGINE_IMMA) return {3, bz::kTcThreads, bz::kTileRows, 3};
     if (engine == BZ_ENGINE_UMMA) return {3, bz::kUmmaM, bz::kUmmaN, 4};
-    if (engine == BZ_ENGINE_AUTO || engine == BZ_ENGINE_MXF4)
+    const bool pair = (engine == BZ_ENGINE_MXF4P && (w32 == 0 || k5p_ok(w32))) ||
+                      (engine == BZ_ENGINE_AUTO && k5p_ok(w32));
+    if (pair) return {3, bz::kUmmaM, bz::k4_tile_rows<true, true>(), 6};
+    if (engine == BZ_ENGINE_AUTO || engine == BZ_ENGINE_MXF4 || engine == BZ_ENGINE_MXF4P)
       return {3, bz::kUmmaM, bz::kUmmaN4, 5};
   }
   // D = 2 needs enough (g-3)-prefixes per group to fill a warp; at g = 3
@@ -216,8 +224,11 @@ double binom_d(int p, int q) {
   return t[p * (BZ_MAX_K + 1) + q];
 }
 
-double k5_cost(int k, int g, const Levels& lv) {
-  const double kTile = 727.0, kStep = 1271.0;  // K5 clocks (cfg5, B200)
+double k5_cost(int k, int g, const Levels& lv, int tile_rows) {
+  // K5 clocks per tile / per prefix step (cfg5, B200); K5p tiles hold twice
+  // the rows for ~1.2x the time
+  const bool pair = tile_rows > bz::kUmmaN4;
+  const double kTile = pair ? 880.0 : 727.0, kStep = 1271.0;
   double cost = 0;
   for (int D = 3; D <= lv.dmax; ++D) {
     const int hi = std::min(lv.floor[D + 1] - 1, k - 1 - D);
@@ -227,30 +238,31 @@ double k5_cost(int k, int g, const Levels& lv) {
       const double slice = binom_d(k - f, D);
       if (np == 0 || slice == 0) continue;
       const double steps = std::ceil(np / bz::kUmmaM);
-      cost += steps * (std::ceil(slice / bz::kUmmaN4) * kTile + kStep);
+      cost += steps * (std::ceil(slice / tile_rows) * kTile + kStep);
     }
   }
   return cost;
 }
 
-Levels k5_levels_search(int k, int g);
+Levels k5_levels_search(int k, int g, int tile_rows);
 
-// memoised per (k, g, BZ_K5_FLOORS): the search costs milliseconds and every
-// round's plan (every process the same) asks for it
-Levels k5_levels(int k, int g) {
+// memoised per (k, g, tile rows, BZ_K5_FLOORS): the search costs
+// milliseconds and every round's plan (every process the same) asks for it
+Levels k5_levels(int k, int g, int tile_rows) {
   static std::mutex mu;
   static std::map<std::string, Levels> memo;
   const char* env = getenv("BZ_K5_FLOORS");
-  const std::string key = std::to_string(k) + "/" + std::to_string(g) + "/" + (env ? env : "");
+  const std::string key = std::to_string(k) + "/" + std::to_string(g) + "/" +
+                          std::to_string(tile_rows) + "/" + (env ? env : "");
   std::lock_guard<std::mutex> lock(mu);
   auto it = memo.find(key);
   if (it != memo.end()) return it->second;
-  const Levels lv = k5_levels_search(k, g);
+  const Levels lv = k5_levels_search(k, g, tile_rows);
   memo.emplace(key, lv);
   return lv;
 }
 
-Levels k5_levels_search(int k, int g) {
+Levels k5_levels_search(int k, int g, int tile_rows) {
   Levels best;
   best.floor[3] = 0;
   best.floor[4] = k;
@@ -270,7 +282,7 @@ Levels k5_levels_search(int k, int g) {
     }
     return best;
   }
-  double best_cost = k5_cost(k, g, best);
+  double best_cost = k5_cost(k, g, best, tile_rows);
   // one extra level (D = 4), then optionally D = 5 above it
   for (int t1 = 1; t1 <= k - 4; ++t1) {
     if (binom_sat(k - t1, 4) > kLevelRowCap) continue;
@@ -279,7 +291,7 @@ Levels k5_levels_search(int k, int g) {
     lv.floor[3] = 0;
     lv.floor[4] = t1;
     lv.floor[5] = k;
-    const double c4 = k5_cost(k, g, lv);
+    const double c4 = k5_cost(k, g, lv, tile_rows);
     if (c4 < best_cost) { best_cost = c4; best = lv; }
     if (g < 6) continue;
     for (int t2 = t1 + 1; t2 <= k - 5; ++t2) {
@@ -288,7 +300,7 @@ Levels k5_levels_search(int k, int g) {
       l5.dmax = 5;
       l5.floor[5] = t2;
       l5.floor[6] = k;
-      const double c5 = k5_cost(k, g, l5);
+      const double c5 = k5_cost(k, g, l5, tile_rows);
       if (c5 < best_cost) { best_cost = c5; best = l5; }
     }
   }
@@ -317,7 +329,7 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
   lv.dmax = shape.depth;
   lv.floor[shape.depth] = 0;
   lv.floor[shape.depth + 1] = k;
-  if (shape.kernel == 5) lv = k5_levels(k, g);
+  if (shape.kernel >= 5) lv = k5_levels(k, g, shape.tile_rows);
   const int dmin = shape.depth;
   // K4/K5: the round's last ~15 % of combinations (in chunk order, which is
   // the order the CTAs draw them in) go in chunks 8x finer, so the SMs
@@ -458,12 +470,12 @@ int launch_tc(bz_ctx* ctx, const RoundArgs& a) {
   return BZ_OK;
 }
 
-template <int W, bool F4>
+template <int W, bool F4, bool PR = false>
 int launch_umma(bz_ctx* ctx, const RoundArgs& a) {
-  const size_t smem = bz::k4_smem_bytes<W, F4>(a.m, a.k, a.ngroups);
+  const size_t smem = bz::k4_smem_bytes<W, F4, PR>(a.m, a.k, a.ngroups);
   if (smem > 232448)
     return fail(ctx, BZ_ERR_TOO_LARGE, "K%d does not fit on an SM (smem %zu)", F4 ? 5 : 4, smem);
-  CK(cudaFuncSetAttribute(bz::k4_round_umma<W, F4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CK(cudaFuncSetAttribute(bz::k4_round_umma<W, F4, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)smem));
   const unsigned long long mine = (a.nchunks + a.nshards - 1 - a.shard) / a.nshards;
   long long blocks = std::max(1ll, std::min((long long)ctx->sm_count, (long long)mine));
@@ -477,7 +489,7 @@ int launch_umma(bz_ctx* ctx, const RoundArgs& a) {
     tabs.t[0] = ctx->d_trip4;
     tabs.stride_rows[0] = ctx->trip4_rows;
   }
-  bz::k4_round_umma<W, F4><<<(unsigned)blocks, bz::K4Roles<F4>::THREADS, smem, ctx->stream>>>(
+  bz::k4_round_umma<W, F4, PR><<<(unsigned)blocks, bz::K4Roles<F4>::THREADS, smem, ctx->stream>>>(
       a, tabs);
   CK(cudaGetLastError());
   ctx->launches += 1;
@@ -502,7 +514,8 @@ int build_triples_w(bz_ctx* ctx, int which) {
 template <int W>
 int build_level_w(bz_ctx* ctx, int D, int floor) {
   const unsigned long long n = binom_sat(ctx->k - floor, D);
-  dim3 grid((unsigned)((n + 255) / 256), ctx->m);
+  // every row of the Gamma's stride: the subsets, then the empty-subset tail
+  dim3 grid((unsigned)((ctx->lvl_rows[D - 3] + 255) / 256), ctx->m);
   bz::k_build_subsets_mxf4<W><<<grid, 256, 0, ctx->stream>>>(
       ctx->d_rows, ctx->d_lvl[D - 3], ctx->k, D, n, ctx->lvl_rows[D - 3], ctx->d_binom);
   CK(cudaGetLastError());
@@ -519,7 +532,8 @@ int ensure_level(bz_ctx* ctx, int D, int floor) {
   if (ctx->lvl_floor[i] >= 0 && ctx->lvl_floor[i] <= floor) return BZ_OK;
   if (ctx->k - floor < D) return BZ_OK;  // no subsets: nothing reads it
   const size_t n = (size_t)binom_sat(ctx->k - floor, D);
-  const size_t N = bz::kUmmaN4;
+  // whole K5p tiles (two accumulator widths) plus one tile of slack
+  const size_t N = bz::k4_tile_rows<true, true>();
   ctx->lvl_rows[i] = (n + N - 1) / N * N + N;
   const size_t row_bytes = 16 * (size_t)(bz::k5_padmagic(ctx->w32) ? ctx->w32 + 1 : ctx->w32);
   const size_t bytes = (size_t)ctx->m * ctx->lvl_rows[i] * row_bytes;
@@ -574,6 +588,9 @@ int ensure_triples(bz_ctx* ctx, int which) {
 
 template <int W>
 int launch_w(bz_ctx* ctx, const RoundArgs& a, bool hist, const PlanShape& shape) {
+  if constexpr (W == 1 || W == 3)
+    if (shape.kernel == 6) return launch_umma<W, true, true>(ctx, a);
+  if (shape.kernel == 6) return fail(ctx, BZ_ERR_STATE, "K5p needs W = 1 or 3, not %d", W);
   if (shape.kernel == 5) return launch_umma<W, true>(ctx, a);
   if (shape.kernel == 4) return launch_umma<W, false>(ctx, a);
   if (shape.kernel == 3) return launch_tc<W>(ctx, a);
@@ -642,7 +659,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   }
   for (int i = 0; i < count; ++i) {
     const int g = g0 + i;
-    const PlanShape shape = pass_shape(ctx->engine, g, hist);
+    const PlanShape shape = pass_shape(ctx->engine, g, hist, ctx->w32);
     if (shape.kernel == 3 || shape.kernel == 4) {
       rc = ensure_triples(ctx, shape.kernel);
       if (rc) return rc;
@@ -651,7 +668,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     unsigned long long nchunks = 0;
     rc = plan_round(ctx, g, gamma_only, shape, nshards, i, &ngroups, &nchunks);
     if (rc) return rc;
-    if (shape.kernel == 5) {
+    if (shape.kernel >= 5) {
       // the suffix tables this round's levels read
       int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX};
       const Group* gp = slot_ptr<Group>(ctx->h_io, l, i, l.off_groups);
@@ -1103,7 +1120,7 @@ int bz_elided(bz_ctx* ctx, uint64_t* out_mask) {
 
 int bz_set_engine(bz_ctx* ctx, int engine) {
   if (!ctx) return BZ_ERR_ARGUMENT;
-  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4)
+  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4P)
     return fail(ctx, BZ_ERR_ARGUMENT, "unknown engine %d", engine);
   ctx->engine = engine;
   return BZ_OK;
@@ -1118,7 +1135,7 @@ int bz_plan(int m, int k, int g, int engine, int nshards, int64_t* out, int cap,
   if (binom_sat(k, g) >= (1ull << 62)) return BZ_ERR_TOO_LARGE;
   std::vector<Group> gs;
   unsigned long long nchunks = 0;
-  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4) return BZ_ERR_ARGUMENT;
+  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4P) return BZ_ERR_ARGUMENT;
   if (nshards < 1) return BZ_ERR_ARGUMENT;
   int rc = build_plan(nullptr, m, k, g, -1, pass_shape(engine, g, false), nshards, gs, &nchunks);
   if (rc) return rc;

@@ -138,25 +138,32 @@ __host__ __device__ constexpr bool k5_padmagic(int w) { return kK5Magic && (w & 
 template <bool F4> __host__ __device__ constexpr int k4_row_bytes(int w) {
   return F4 ? 16 * (k5_padmagic(w) ? w + 1 : w) : 32 * w;
 }
-// 16-byte K chunks per A row (K5 pads to whole K = 64 MMAs)
-template <bool F4> __host__ __device__ constexpr int k4_a_chunks(int w) {
-  return F4 ? 2 * ((w + 1) / 2) : 2 * w;
+// 16-byte K chunks per A row (K5 pads to whole K = 64 MMAs; the pair form
+// K5p carries two offset chunks, W data chunks + 2)
+template <bool F4, bool PR = false> __host__ __device__ constexpr int k4_a_chunks(int w) {
+  return PR ? w + 2 : (F4 ? 2 * ((w + 1) / 2) : 2 * w);
 }
+// MMAs per tile (per half for K5p)
 template <bool F4> __host__ __device__ constexpr int k4_passes(int w) { return k4_a_chunks<F4>(w) / 2; }
-template <bool F4> __host__ __device__ constexpr uint32_t k4_tile_b(int w) {
-  return (uint32_t)(k4_n<F4>() * k4_row_bytes<F4>(w));
+// table rows per B tile: K5p pairs two rows per accumulator column
+template <bool F4, bool PR = false> __host__ __device__ constexpr int k4_tile_rows() {
+  return PR ? 2 * k4_n<F4>() : k4_n<F4>();
 }
-template <bool F4> __host__ __device__ constexpr uint32_t k4_tile_a(int w) {
-  return (uint32_t)(kUmmaM * 16 * k4_a_chunks<F4>(w));
+template <bool F4, bool PR = false> __host__ __device__ constexpr uint32_t k4_tile_b(int w) {
+  return (uint32_t)(k4_tile_rows<F4, PR>() * k4_row_bytes<F4>(w));
+}
+template <bool F4, bool PR = false> __host__ __device__ constexpr uint32_t k4_tile_a(int w) {
+  return (uint32_t)(kUmmaM * 16 * k4_a_chunks<F4, PR>(w));
 }
 // A-tile ring depth (producers run that many prefix steps ahead)
 template <bool F4> __host__ __device__ constexpr int k4_abufs(int w) {
   return F4 && w <= 6 ? 4 : 2;
 }
 // B-tile ring depth: K5 ~136 KB of stages, K4 4 x 40 KB at W = 5
-template <bool F4> __host__ __device__ constexpr int k4_stages(int w) {
-  return F4 ? (136000 / (int)k4_tile_b<true>(w) < kMaxStages ? 136000 / (int)k4_tile_b<true>(w)
-                                                              : kMaxStages)
+template <bool F4, bool PR = false> __host__ __device__ constexpr int k4_stages(int w) {
+  return F4 ? (136000 / (int)k4_tile_b<true, PR>(w) < kMaxStages
+                   ? 136000 / (int)k4_tile_b<true, PR>(w)
+                   : kMaxStages)
             : (w <= 5 ? 4 : (w <= 6 ? 3 : 2));
 }
 
@@ -177,6 +184,25 @@ __host__ __device__ __forceinline__ uint4 e2m1_bits01(uint32_t v) {
 __host__ __device__ __forceinline__ uint4 e2m1_pm1(uint32_t v) {
   return make_uint4(((v << 3) & 0x88888888u) | 0x22222222u, ((v << 2) & 0x88888888u) | 0x22222222u,
                     ((v << 1) & 0x88888888u) | 0x22222222u, (v & 0x88888888u) | 0x22222222u);
+}
+
+// K5 table offset chunk: elements 0..15 = 1.0, 16..31 = 4.0 (bytes 0..7 /
+// 8..15).  K5 pairs it with an A chunk holding 1.5 at element 0 only; K5p
+// with k5p_offset_chunk(T), whose dot product with it is exactly T.
+__host__ __device__ __forceinline__ uint4 k5_table_offset_chunk() {
+  return make_uint4(0x22222222u, 0x22222222u, 0x66666666u, 0x66666666u);
+}
+// e2m1 nibbles whose dot product with k5_table_offset_chunk() is T
+// (0 <= T <= 4 * 16 * 6 + 3): T & 3 at element 0 (x1.0), T >> 2 as 6.0s
+// plus a remainder on elements 16.. (x4.0)
+__device__ __forceinline__ uint4 k5p_offset_chunk(int T) {
+  // e2m1 nibble of 0, 1, 2, 3, 4, 4 (+ 1.0 on the next element for 5)
+  constexpr uint32_t kSmall = 0x665420u;
+  const int r = T & 3, q = T >> 2, q6 = q / 6, qr = q - 6 * q6;
+  unsigned long long x = q6 ? (0x7777777777777777ull >> (64 - 4 * q6)) : 0ull;
+  x |= (unsigned long long)((kSmall >> (4 * qr)) & 0xFu) << (4 * q6);
+  x |= (unsigned long long)(qr == 5 ? 0x2u : 0u) << (4 * q6 + 4);
+  return make_uint4((kSmall >> (4 * r)) & 0xFu, 0u, (uint32_t)x, (uint32_t)(x >> 32));
 }
 
 // tcgen05 shared-memory matrix descriptor, SWIZZLE_NONE, K-major:
@@ -452,8 +478,18 @@ __global__ void k_build_subsets_mxf4(const uint32_t* __restrict__ rows,
   constexpr int WP = padded_words(W);
   constexpr int C = k4_row_bytes<true>(W) / 16;  // chunks per row (+ offset chunk)
   const unsigned long long row = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= nrows) return;
+  if (row >= gamma_stride_rows) return;
   const int j = blockIdx.y;
+  uint8_t* grp = out + (size_t)j * gamma_stride_rows * (16 * C) + (size_t)(row >> 3) * (8 * 16 * C) +
+                 (row & 7) * 16;
+  if (row >= nrows) {
+    // tail rows (read by whole-tile copies, their columns masked): the
+    // empty subset, so every column a K5p tile pairs stays in range
+#pragma unroll
+    for (int w = 0; w < W; ++w) *reinterpret_cast<uint4*>(grp + w * 128) = make_uint4(0u, 0u, 0u, 0u);
+    if constexpr (C > W) *reinterpret_cast<uint4*>(grp + W * 128) = k5_table_offset_chunk();
+    return;
+  }
   const uint32_t* R = rows + (size_t)j * k * WP;
   // smallest element a: rows of a start at C(k-1-a, D); x = k-1-a is the
   // largest x with C(x, D) <= row
@@ -476,12 +512,10 @@ __global__ void k_build_subsets_mxf4(const uint32_t* __restrict__ rows,
     for (int w = 0; w < W; ++w) v[w] ^= R[e * WP + w];
     ++e;
   }
-  uint8_t* grp = out + (size_t)j * gamma_stride_rows * (16 * C) + (size_t)(row >> 3) * (8 * 16 * C) +
-                 (row & 7) * 16;
 #pragma unroll
   for (int w = 0; w < W; ++w) *reinterpret_cast<uint4*>(grp + w * 128) = e2m1_bits01(v[w]);
-  if constexpr (C > W)  // offset chunk: 1.0 at element 0
-    *reinterpret_cast<uint4*>(grp + W * 128) = make_uint4(0x2u, 0u, 0u, 0u);
+  if constexpr (C > W)  // offset chunk
+    *reinterpret_cast<uint4*>(grp + W * 128) = k5_table_offset_chunk();
 }
 
 // ---------------------------------------------------------------------------
@@ -517,11 +551,11 @@ __global__ void k_build_triples_umma(const uint32_t* __restrict__ rows,
   }
 }
 
-template <int W, bool F4>
+template <int W, bool F4, bool PR = false>
 __host__ __device__ inline size_t k4_smem_bytes(int m, int k, int ngroups) {
   size_t off = (smem_base_bytes<W>(m, k, ngroups) + 1023) & ~size_t(1023);
-  off += (size_t)k4_stages<F4>(W) * k4_tile_b<F4>(W);
-  off += (size_t)k4_abufs<F4>(W) * kUmmaMA * k4_tile_a<F4>(W);
+  off += (size_t)k4_stages<F4, PR>(W) * k4_tile_b<F4, PR>(W);
+  off += (size_t)k4_abufs<F4>(W) * kUmmaMA * k4_tile_a<F4, PR>(W);
   off += F4 ? kMagicBytes : 0;   // K5 magic operands
   off += kBarSlots * 8 + 16;     // barriers + TMEM base
   off += k4_abufs<F4>(W) * kUmmaMA * kUmmaM * sizeof(int);  // prefix weights of the A buffers
@@ -591,17 +625,21 @@ __device__ __forceinline__ K4Chunk k4_decode(const Group* sg, int ngroups,
 // unit block scales): one persistent CTA per SM, warp-specialised (see the
 // file comment).  The two differ only in operand encoding, MMA kind,
 // accumulator type (s32 read as packed s16 / f32) and tile geometry.
-template <int W, bool F4>
+template <int W, bool F4, bool PR>
 __global__ void __launch_bounds__(K4Roles<F4>::THREADS, 1)
 k4_round_umma(const RoundArgs a, const K4Tables tabs) {
   static_assert(!F4 || kUmmaMA == 1, "K5 runs one A tile per B tile");
+  static_assert(!PR || (F4 && kK5Magic && (W & 1) && W <= 3 && BZ_K5_SPLIT == 1 &&
+                        BZ_K5_EPI_GROUPS == 1),
+                "K5p: odd W <= 3 (stored weights <= 127 fit the 7-bit high field)");
   constexpr int N = k4_n<F4>();
-  constexpr int S = k4_stages<F4>(W);
-  constexpr int P = k4_passes<F4>(W);        // MMAs per tile (K = 32 bytes each)
-  constexpr int CA = k4_a_chunks<F4>(W);     // 16-byte K chunks per A row
+  constexpr int TR = k4_tile_rows<F4, PR>();  // table rows per B tile
+  constexpr int S = k4_stages<F4, PR>(W);
+  constexpr int P = k4_passes<F4>(W);        // MMAs per tile (K5p: per half)
+  constexpr int CA = k4_a_chunks<F4, PR>(W); // 16-byte K chunks per A row
   constexpr int CB = k4_row_bytes<F4>(W) / 16;  // ... per B row
-  constexpr uint32_t TB = k4_tile_b<F4>(W);
-  constexpr uint32_t TA = k4_tile_a<F4>(W);
+  constexpr uint32_t TB = k4_tile_b<F4, PR>(W);
+  constexpr uint32_t TA = k4_tile_a<F4, PR>(W);
   using RL = K4Roles<F4>;
   constexpr int ACC = RL::ACC;
   constexpr int E = RL::E;
@@ -683,7 +721,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
     if (warp < 4) {
       for (int c = 0; c < 512 - kSfCol; c += 8)
         tmem_st8(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(kSfCol + c),
-                 kSfCol + c == kSfColMagic ? 0x96969696u
+                 kSfCol + c == kSfColMagic ? (PR ? 0x8F8F8F8Fu : 0x96969696u)
                                            : (kSfCol + c == kSfColPad ? 0x7F7F967Fu : 0x7F7F7F7Fu));
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
@@ -697,7 +735,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       *reinterpret_cast<uint4*>(sMagic + op * 256 + row16 * 16) = z;
       fence_proxy_async();
     }
-    if (CA > W && warp >= RL::PROD0) {
+    if (!PR && CA > W && warp >= RL::PROD0) {
       // the A padding chunk: zero, or 1.5 at element 0 (padding-chunk offset)
       const int r = tid - 32 * RL::PROD0;
       for (int ab = 0; ab < NA; ++ab)
@@ -728,7 +766,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       if (lane == 0) mbar_arrive(qempty(qs));
       if (qchunk < 0) break;
       const unsigned long long chunk = (unsigned long long)qchunk;
-      const K4Chunk c = k4_decode<N>(sgroups, a.ngroups, chunk, k);
+      const K4Chunk c = k4_decode<TR>(sgroups, a.ngroups, chunk, k);
       k4_trace_chunk(a, toff, c.gr.ell, tcount);
       int best = INT_MAX;
       for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
@@ -753,7 +791,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
           if (!BZ_K5_NOFENCE) tc_fence_after();
           if (warp == 0 && lane == 0) k4_trace(a, 2, tcount, toff);
           if (warp == E - 1 && lane == 0) k4_trace(a, 7, tcount, toff);
-          const int lim = min(N, c.slice - t * N) - EC * slice_id;
+          const int lim = min(N, c.slice - t * TR) - EC * slice_id;
           const uint32_t tb = tmem + ((uint32_t)(32 * quarter) << 16) +
                               (uint32_t)(buf * kUmmaMA * N + EC * slice_id);
           if (a.debug & 1) {
@@ -761,7 +799,46 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
             if (lane == 0) mbar_arrive(accempty(hb));
             continue;
           }
-          if constexpr (F4 && kK5Magic) {
+          if constexpr (PR) {
+            // K5p: every column holds two codewords, 2^23 + wt_a + 2^16 wt_b
+            // (stored weights <= 96): bits 0..15 = wt_a, bits 16..31 =
+            // 0x4B00 + wt_b, so one s16x2 minimum serves both.  Two loads of
+            // EC/2 columns (register budget), then the buffer is released.
+            constexpr int H = EC / 2;
+            const int la = c.slice - t * TR - EC * slice_id;  // half-a columns < la valid
+            const int lb = la - N;                             // half-b columns < lb valid
+            uint32_t m0 = 0x7FFF7FFFu, m1 = 0x7FFF7FFFu;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              uint32_t v[H];
+              tmem_ld_cols<H>(tb + hh * H, v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < H; i += 4) tmem_regs4_after_wait(v + i);
+              if (hh == 1) {
+                if (!BZ_K5_NOFENCE) tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(accempty(hb));  // accumulators are in registers
+              }
+              if (lb < EC) {
+#pragma unroll
+                for (int i = 0; i < H; ++i) {
+                  if (hh * H + i >= la) v[i] = (v[i] & 0xffff0000u) | 0x00007fffu;
+                  if (hh * H + i >= lb) v[i] = (v[i] & 0x0000ffffu) | 0x7fff0000u;
+                }
+              }
+#pragma unroll
+              for (int i = 0; i + 3 < H; i += 4) {
+                m0 = __vimin3_s16x2(m0, v[i], v[i + 1]);
+                m1 = __vimin3_s16x2(m1, v[i + 2], v[i + 3]);
+              }
+#pragma unroll
+              for (int i = (H / 4) * 4; i < H; ++i) m0 = __vmins2(m0, v[i]);
+            }
+            const uint32_t m = __vmins2(m0, m1);
+            const int lo = (int)(m & 0xffffu), hi = (int)(m >> 16) - 0x4B00;
+            rmin[0] = min(rmin[0], min(lo, hi));
+          } else if constexpr (F4 && kK5Magic) {
             // EC accumulators as packed s16 pairs (low halves of 1.5*2^23 + D)
             constexpr int NP = EC / 2;
             uint32_t v[NP];
@@ -871,8 +948,10 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
           // column of this slice masked) stays out of the way
           if (fmin_acc < 1.0e6f) rmin[0] = (int)fmin_acc;
         }
+        // K5p minima are whole stored weights (the prefix weight rode on the
+        // offset chunks)
 #pragma unroll
-        for (int j = 0; j < kUmmaMA; ++j) best = min(best, rmin[j] + wt[j]);
+        for (int j = 0; j < kUmmaMA; ++j) best = min(best, rmin[j] + (PR ? 0 : wt[j]));
       }
       int wbest = __reduce_min_sync(FULL, best);
       if (wbest < INT_MAX / 2) wbest += gamma_woff(a, c.gr.gamma);
@@ -896,7 +975,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       if (lane == 0) mbar_arrive(qempty(qs));
       if (qchunk < 0) break;
       const unsigned long long chunk = (unsigned long long)qchunk;
-      const K4Chunk c = k4_decode<N>(sgroups, a.ngroups, chunk, k);
+      const K4Chunk c = k4_decode<TR>(sgroups, a.ngroups, chunk, k);
       const unsigned long long first = c.bfirst + (unsigned long long)r * c.gr.ppl;
       long long cnt = 0;
       if (first < c.gr.nprefix) {
@@ -935,6 +1014,12 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
               *reinterpret_cast<uint4*>(dst + umma_off_c(r, 2 * jj + 1, CA)) = hi;
             }
           }
+          if constexpr (PR) {
+            // offset chunks: w(P) (half a, scale 1) and w(P) + 128 (half b,
+            // scale 2^16, which also supplies the 2^23 offset)
+            *reinterpret_cast<uint4*>(dst + umma_off_c(r, W, CA)) = k5p_offset_chunk(wt);
+            *reinterpret_cast<uint4*>(dst + umma_off_c(r, W + 1, CA)) = k5p_offset_chunk(wt + 128);
+          }
           s_wt[(ab * kUmmaMA + j) * kUmmaM + r] = wt;
         }
         fence_proxy_async();  // generic-proxy writes -> tensor-core reads
@@ -944,8 +1029,8 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       // visited combinations of this chunk
       const unsigned tot = __reduce_add_sync(FULL, (unsigned)cnt);
       if (lane == 0 && tot) {
-        const long long cols = min((long long)c.tile_hi * N, (long long)c.slice) -
-                               (long long)c.tile_lo * N;
+        const long long cols = min((long long)c.tile_hi * TR, (long long)c.slice) -
+                               (long long)c.tile_lo * TR;
         atomicAdd(a.combos + c.gr.gamma, (unsigned long long)tot * (unsigned long long)cols);
       }
     }
@@ -973,7 +1058,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
         if (lane == 0) mbar_arrive(qempty(qs));
         if (qchunk < 0) break;
         const unsigned long long chunk = (unsigned long long)qchunk;
-        const K4Chunk c = k4_decode<N>(sgroups, a.ngroups, chunk, k);
+        const K4Chunk c = k4_decode<TR>(sgroups, a.ngroups, chunk, k);
         k4_trace_chunk(a, toff, c.gr.ell, tcount);
         const int ntile = c.tile_hi - c.tile_lo;
         for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
@@ -992,7 +1077,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
             if (lane == 0) k4_trace(a, 5, tc, toff);
             mbar_wait_fast(bfull(stg), (tc / S) & 1);
             if (lane == 0) k4_trace(a, 6, tc, toff);
-            const int valid = min(N, c.slice - (c.tile_lo + i) * N);
+            const int valid = min(N, c.slice - (c.tile_lo + i) * TR);
 #pragma unroll
             for (int h = 0; h < SPLIT; ++h) {
               mbar_wait_fast(accempty(mb * SPLIT + h), ((tc / ACC) & 1) ^ 1);
@@ -1007,7 +1092,22 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
               if (elect_one()) {
                 // a part holding no valid suffix is only committed (its
                 // columns are masked anyway)
-                if (!(a.debug & 4) && valid > h * NH) {
+                if (PR && !(a.debug & 4)) {
+                  // K5p: half a (table rows [0, N) of the stage, unit scales),
+                  // then half b (rows [N, 2N), B scale 2^16); the last half-b
+                  // MMA reads A chunks W-1 and W+1 (LBO 256 B) so it meets
+                  // the second offset chunk
+                  const uint32_t dj = dbase;
+                  const uint64_t adj = a_desc0 + (uint64_t)(ab * (TA >> 4));
+                  const uint64_t bd1 = bd0 + (uint64_t)((N / 8) * CB * 8);
+#pragma unroll
+                  for (int kb = 0; kb < P; ++kb)
+                    umma_mxf4(dj, adj + 16u * kb, bd0 + 16u * kb, IDESC, kb > 0 ? 1u : 0u, sfa, sfb);
+#pragma unroll
+                  for (int kb = 0; kb < P; ++kb)
+                    umma_mxf4(dj, adj + 16u * kb + (kb == P - 1 ? (uint64_t)8 << 16 : 0ull),
+                              bd1 + 16u * kb, IDESC, 1u, sfa, sfm);
+                } else if (!(a.debug & 4) && valid > h * NH) {
 #pragma unroll
                   for (int j = 0; j < kUmmaMA; ++j) {
                     const uint32_t dj = dbase + (uint32_t)(j * N + h * NH);
@@ -1059,7 +1159,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
         mbar_arrive(qfull(qs));
         if (qchunk < 0) break;
         const unsigned long long chunk = (unsigned long long)qchunk;
-        const K4Chunk c = k4_decode<N>(sgroups, a.ngroups, chunk, k);
+        const K4Chunk c = k4_decode<TR>(sgroups, a.ngroups, chunk, k);
         k4_trace_chunk(a, toff, c.gr.ell, bcount);
         const int lvl = c.gr.depth - 3;  // suffix table of this group's level
         const uint8_t* tsrc =
@@ -1071,8 +1171,10 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
             k4_trace(a, 0, bcount, toff);
             // only the rows this tile needs (8-row granularity); the rest of
             // the stage keeps stale rows whose columns the epilogue masks
-            const int valid = min(N, c.slice - t * N);
-            const uint32_t bytes = (uint32_t)((valid + 7) / 8) * (CB * 128);
+            // (K5p: always the whole tile -- both halves of a column must
+            // hold in-range table rows, which the zeroed table tail provides)
+            const int valid = min(TR, c.slice - t * TR);
+            const uint32_t bytes = PR ? TB : (uint32_t)((valid + 7) / 8) * (CB * 128);
             if (a.debug & 2) {
               mbar_arrive(bfull(stg));
             } else {

@@ -27,10 +27,11 @@ def ctx():
     return _native.context(0)
 
 
-@pytest.fixture(params=["popc", "imma", "umma", "mxf4"])
+@pytest.fixture(params=["popc", "imma", "umma", "mxf4", "mxf4p"])
 def engine(request):
-    """Every kernel: K1 (XOR+POPC), K3 (legacy IMMA, g >= 4) and K4
-    (tcgen05 + TMEM, g >= 4)."""
+    """Every kernel: K1 (XOR+POPC), K3 (legacy IMMA, g >= 4), K4 (tcgen05
+    kind::i8), K5 (kind::mxf4) and K5p (two codewords per accumulator
+    column; W = 1, 3 -- other widths run K5)."""
     _native.context(0).set_engine(request.param)
     yield request.param
     _native.context(0).set_engine("auto")
@@ -230,14 +231,16 @@ def test_early_exit_all_engines(ctx, engine):
 
 @pytest.mark.parametrize("k,g,floors", [(12, 6, "4,7"), (14, 8, "5,9"), (12, 5, "6"),
                                         (20, 7, "8,13"), (11, 9, "0,3")])
-@pytest.mark.parametrize("n", [37, 160, 230])
-def test_mxf4_levels(monkeypatch, ctx, k, g, floors, n):
-    """K5 with forced suffix levels (depth-4/5 tables): exact minima and
-    combination counts per Gamma against the oracle."""
+@pytest.mark.parametrize("n", [20, 37, 70, 96, 160, 230])
+@pytest.mark.parametrize("kernel", ["mxf4", "mxf4p"])
+def test_mxf4_levels(monkeypatch, ctx, k, g, floors, n, kernel):
+    """K5 / K5p with forced suffix levels (depth-4/5 tables): exact minima and
+    combination counts per Gamma against the oracle (K5p runs at n = 20, 70,
+    96; the other widths fall back to K5)."""
     monkeypatch.setenv("BZ_K5_FLOORS", floors)
     rng = random.Random(k * 1000 + g * 10 + n)
     gammas = [[rng.getrandbits(n) for _ in range(k)] for _ in range(2)]
-    ctx.set_engine("mxf4")
+    ctx.set_engine(kernel)
     try:
         ctx.load(family_words([BitMatrix(r, n) for r in gammas], n), n)
         mins, combos = ctx.round(g, -1, 1 << 30)
@@ -329,3 +332,45 @@ def test_brute_force_rank_deficient():
 
     M = BitMatrix([0b1011, 0b0110, 0b1101], 4)  # row 3 = row 1 ^ row 2
     assert brute_force_distance(M) == 0
+
+
+@pytest.mark.parametrize("n", [1, 17, 32, 33, 64, 80, 95, 96])
+@pytest.mark.parametrize("density", [0.05, 0.5, 0.97])
+def test_mxf4p_weight_range(ctx, n, density):
+    """K5p packs two stored weights into one fp32 accumulator (bits 0..15 and
+    16..22): every weight from 0 to n <= 96 must come back exact, including
+    all-zero and all-one codewords, slices crossing the 480-row tile and
+    both halves of a column."""
+    rng = random.Random(n * 100 + int(density * 100))
+    k = 24
+    rows = [sum(1 << b for b in range(n) if rng.random() < density) for _ in range(k)]
+    rows[3] = rows[4]                      # a zero codeword at every even g >= 2
+    rows[5] = (1 << n) - 1                 # an all-ones row
+    ctx.set_engine("mxf4p")
+    try:
+        ctx.load(family_words([BitMatrix(rows, n), BitMatrix(rows[::-1], n)], n), n)
+        for g in (4, 5, 6, 7):
+            mins, combos = ctx.round(g, -1, 1 << 30)
+            want = oracle.min_weight(rows, n, g)[0]
+            assert mins == [want, want] and combos == [comb(k, g)] * 2, (g, mins, want)
+    finally:
+        ctx.set_engine("auto")
+
+
+@pytest.mark.parametrize("n", [40, 96])
+def test_mxf4p_all_heavy(ctx, n):
+    """Every codeword heavy (odd g over identical all-ones rows: weight n),
+    so the minimum is the largest value the packed fields carry."""
+    k = 15
+    rows = [(1 << n) - 1] * k
+    ctx.set_engine("mxf4p")
+    try:
+        ctx.load(family_words([BitMatrix(rows, n)], n), n)
+        for g in (5, 7, 9):
+            mins, _ = ctx.round(g, -1, 1 << 30)
+            assert mins == [n], (g, mins)
+        for g in (4, 6):
+            mins, _ = ctx.round(g, -1, 1 << 30)
+            assert mins == [0], (g, mins)
+    finally:
+        ctx.set_engine("auto")
