@@ -13,11 +13,12 @@ the random binary [160,80] code of seed 7 (SURVEY.md Appendix A generator,
             from a host BitMatrix: Gamma construction, H2D of the rows and
             of every round's work plan, all rounds, D2H of every round's
             minima and counters, timed by the host clock.
-  roofline -- the dominant kernel (the g = 8 round, K4 = tcgen05.mma
-            kind::i8 with TMEM accumulators): achieved combos/s vs the live
-            tcgen05 i8 MAC rate / (32*W32) MACs per combination; "k3_imma" and
-            "k1_popc" report the legacy-IMMA kernel K3 and the XOR+POPC kernel
-            K1 on the same launch against their own live rooflines.
+  roofline -- the dominant kernel (the g = 8 round, K5q = tcgen05.mma
+            kind::mxf4nvf4, two codewords as bytes of one fp32 TMEM
+            accumulator): achieved combos/s vs the live fp4 MAC rate /
+            (64*ceil(W/2)) MACs per combination; "k5p_mxf4", "k5_mxf4",
+            "k4_umma_i8", "k3_imma" and "k1_popc" report the other kernels on
+            the same launch against their own live rooflines.
   cpu_baseline -- the C oracle (oracle/, a restatement of the reference's
             enumerate_stack) on all host cores over a bounded sample.
 
@@ -310,6 +311,8 @@ def main():
         ctx.set_engine(cfg.engine)
         return (g_top_combos / world) / (min(ms) * 1e-3)
 
+    k5_achieved = engine_rate("mxf4")
+    k5p_achieved = engine_rate("mxf4p")
     k1_achieved = engine_rate("popc")
     k3_achieved = engine_rate("imma")
     k4_achieved = engine_rate("umma")
@@ -317,6 +320,8 @@ def main():
     ctx.set_elision(False)
     backend.load(gs, n)
     k5_full = engine_rate(cfg.engine)
+    w_full = w32  # without elision: K5p only for odd W <= 3, else K5
+    full_kernel = "K5q" if w_full in (1, 3) else "K5"
     ctx.set_elision(True)
     backend.load(gs, n)
     traffic = None
@@ -345,8 +350,12 @@ def main():
         "roofline": {"bound": "tensor", "achieved": achieved / 1e9, "peak": mxf4_peak / 1e9,
                      "unit": "Gcombinations/s", "frac": achieved / mxf4_peak,
                      "traffic": traffic,
-                     "kernel": f"k4_round_umma<{w_eff},true> = K5, round g={g_top} "
-                               f"(tcgen05.mma kind::mxf4, unit block scales)",
+                     "kernel": (f"k4_round_umma<{w_eff},true,4> = K5q, round g={g_top} "
+                                f"(tcgen05.mma kind::mxf4nvf4 block16, two codewords as bytes "
+                                f"of one fp32 accumulator)"
+                                if w_eff in (1, 3) else
+                                f"k4_round_umma<{w_eff},true,1> = K5, round g={g_top} "
+                                f"(tcgen05.mma kind::mxf4, unit block scales)"),
                      "peak_source": f"live microbenchmark: tcgen05.mma kind::mxf4 M128xN240xK64 "
                                     f"{peaks['mxf4_mac_per_clk_sm']:.0f} MACs/clk/SM, "
                                     f"{peaks['mxf4_mac_per_s'] / 1e15:.2f} PMAC/s / "
@@ -361,10 +370,19 @@ def main():
                                  "those k columns and every weight gets +g (exact); rooflines "
                                  "use the stored K as their denominator"},
                      "without_elision": {
+                         "kernel": full_kernel,
                          "achieved": k5_full / 1e9,
                          "peak": peaks["mxf4_mac_per_s"] / macs_f4_full / 1e9,
                          "frac": k5_full / (peaks["mxf4_mac_per_s"] / macs_f4_full),
                          "macs_per_combination": macs_f4_full}},
+        "k5p_mxf4": {"kernel": f"k4_round_umma<{w_eff},true,2> round g={g_top} "
+                               f"(kind::mxf4, two codewords as 16-bit fields)",
+                     "achieved": k5p_achieved / 1e9, "peak": mxf4_peak / 1e9,
+                     "unit": "Gcombinations/s", "frac": k5p_achieved / mxf4_peak},
+        "k5_mxf4": {"kernel": f"k4_round_umma<{w_eff},true,1> round g={g_top} "
+                              f"(tcgen05.mma kind::mxf4, one codeword per accumulator)",
+                    "achieved": k5_achieved / 1e9, "peak": mxf4_peak / 1e9,
+                    "unit": "Gcombinations/s", "frac": k5_achieved / mxf4_peak},
         "k4_umma_i8": {"kernel": f"k4_round_umma<{w_eff},false> round g={g_top} "
                                  f"(tcgen05.mma kind::i8)",
                        "achieved": k4_achieved / 1e9, "peak": umma_peak / 1e9,

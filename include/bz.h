@@ -60,13 +60,15 @@ extern "C" {
 #define BZ_ERR_ARGUMENT 7           /* null pointer, bad shard                   */
 
 /* enumeration engines (bz_set_engine) */
-#define BZ_ENGINE_AUTO 0 /* K5p (W = 1, 3) or K5 for g >= 4, K1 otherwise   */
+#define BZ_ENGINE_AUTO 0 /* K5q (W = 1, 3) or K5 for g >= 4, K1 otherwise   */
 #define BZ_ENGINE_POPC 1 /* K1 only: XOR + POPC on the integer pipes       */
 #define BZ_ENGINE_IMMA 2 /* K3 (legacy warp-level IMMA) for g >= 4        */
 #define BZ_ENGINE_UMMA 3 /* K4 (tcgen05.mma kind::i8, TMEM) for g >= 4     */
 #define BZ_ENGINE_MXF4 4 /* K5 (tcgen05.mma kind::mxf4, unit scales) g >= 4 */
 #define BZ_ENGINE_MXF4P 5 /* K5p: K5 with two codewords per accumulator     \
                              column (stored words W = 1 or 3; else K5)     */
+#define BZ_ENGINE_MXF4T 6 /* K5t: three codewords per column (W = 1, 3)     */
+#define BZ_ENGINE_MXF4Q 7 /* K5q: two codewords as bytes (mxf4nvf4, W = 1, 3) */
 
 typedef struct bz_ctx bz_ctx;
 
@@ -143,8 +145,11 @@ int bz_round(bz_ctx *ctx, int g, int lower_prev, int upper, int shard,
 /* Rounds g0 .. g0+count-1 in one call: planned together, launched back to
  * back, one synchronisation -- for the short early rounds, where launch and
  * synchronisation latency dominate.  lower_prev[i] is round g0+i's early
- * exit threshold; every round starts from `upper` (the caller folds the
- * rounds into its bounds in order and may discard rounds past termination).
+ * exit threshold.  Round g0 starts from `upper`, each later round from the
+ * U its predecessor ended with (min of `upper` and that round's minima) --
+ * the running U the reference clips with (m/engine.py:209-211); the caller
+ * folds the rounds into its bounds in order and discards rounds past
+ * termination (those exit at once: their start U is already <= lower_prev).
  * out_min / out_combos hold count x m values, round-major. */
 int bz_rounds(bz_ctx *ctx, int g0, int count, const int32_t *lower_prev, int upper,
               int shard, int nshards, int32_t *out_min, uint64_t *out_combos);

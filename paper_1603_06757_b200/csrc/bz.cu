@@ -174,15 +174,19 @@ struct PlanShape {
 bool k5p_ok(int w32) { return w32 == 1 || w32 == 3; }
 
 // w32: stored words of the loaded family (0 = unknown, host-only plans):
-// AUTO takes K5p where it applies, else K5
+// AUTO takes K5q where it applies (odd W <= 3), else K5
 PlanShape pass_shape(int engine, int g, bool hist, int w32 = 0) {
   if (!hist && g >= 4) {
     if (engine == BZ_ENGINE_IMMA) return {3, bz::kTcThreads, bz::kTileRows, 3};
     if (engine == BZ_ENGINE_UMMA) return {3, bz::kUmmaM, bz::kUmmaN, 4};
-    const bool pair = (engine == BZ_ENGINE_MXF4P && (w32 == 0 || k5p_ok(w32))) ||
-                      (engine == BZ_ENGINE_AUTO && k5p_ok(w32));
-    if (pair) return {3, bz::kUmmaM, bz::k4_tile_rows<true, true>(), 6};
-    if (engine == BZ_ENGINE_AUTO || engine == BZ_ENGINE_MXF4 || engine == BZ_ENGINE_MXF4P)
+    const bool packed_ok = w32 == 0 || k5p_ok(w32);
+    if (engine == BZ_ENGINE_MXF4T && packed_ok) return {3, bz::kUmmaM, bz::k4_tile_rows<true, 3>(), 7};
+    if (engine == BZ_ENGINE_MXF4Q && packed_ok) return {3, bz::kUmmaM, bz::k4_tile_rows<true, 4>(), 8};
+    if (engine == BZ_ENGINE_AUTO && k5p_ok(w32))
+      return {3, bz::kUmmaM, bz::k4_tile_rows<true, 4>(), 8};  // K5q
+    if (engine == BZ_ENGINE_MXF4P && packed_ok) return {3, bz::kUmmaM, bz::k4_tile_rows<true, 2>(), 6};
+    if (engine == BZ_ENGINE_AUTO || engine == BZ_ENGINE_MXF4 || engine == BZ_ENGINE_MXF4P ||
+        engine == BZ_ENGINE_MXF4T || engine == BZ_ENGINE_MXF4Q)
       return {3, bz::kUmmaM, bz::kUmmaN4, 5};
   }
   // D = 2 needs enough (g-3)-prefixes per group to fill a warp; at g = 3
@@ -225,8 +229,8 @@ double binom_d(int p, int q) {
 }
 
 double k5_cost(int k, int g, const Levels& lv, int tile_rows) {
-  // K5 clocks per tile / per prefix step (cfg5, B200); K5p tiles hold twice
-  // the rows for ~1.2x the time
+  // K5 clocks per tile / per prefix step (cfg5, B200); K5p/K5q tiles hold
+  // twice the rows for ~1.2x the time
   const bool pair = tile_rows > bz::kUmmaN4;
   const double kTile = pair ? 880.0 : 727.0, kStep = 1271.0;
   double cost = 0;
@@ -470,12 +474,12 @@ int launch_tc(bz_ctx* ctx, const RoundArgs& a) {
   return BZ_OK;
 }
 
-template <int W, bool F4, bool PR = false>
+template <int W, bool F4, int CW = 1>
 int launch_umma(bz_ctx* ctx, const RoundArgs& a) {
-  const size_t smem = bz::k4_smem_bytes<W, F4, PR>(a.m, a.k, a.ngroups);
+  const size_t smem = bz::k4_smem_bytes<W, F4, CW>(a.m, a.k, a.ngroups);
   if (smem > 232448)
     return fail(ctx, BZ_ERR_TOO_LARGE, "K%d does not fit on an SM (smem %zu)", F4 ? 5 : 4, smem);
-  CK(cudaFuncSetAttribute(bz::k4_round_umma<W, F4, PR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CK(cudaFuncSetAttribute(bz::k4_round_umma<W, F4, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)smem));
   const unsigned long long mine = (a.nchunks + a.nshards - 1 - a.shard) / a.nshards;
   long long blocks = std::max(1ll, std::min((long long)ctx->sm_count, (long long)mine));
@@ -489,7 +493,7 @@ int launch_umma(bz_ctx* ctx, const RoundArgs& a) {
     tabs.t[0] = ctx->d_trip4;
     tabs.stride_rows[0] = ctx->trip4_rows;
   }
-  bz::k4_round_umma<W, F4, PR><<<(unsigned)blocks, bz::K4Roles<F4>::THREADS, smem, ctx->stream>>>(
+  bz::k4_round_umma<W, F4, CW><<<(unsigned)blocks, bz::K4Roles<F4, CW>::THREADS, smem, ctx->stream>>>(
       a, tabs);
   CK(cudaGetLastError());
   ctx->launches += 1;
@@ -532,8 +536,9 @@ int ensure_level(bz_ctx* ctx, int D, int floor) {
   if (ctx->lvl_floor[i] >= 0 && ctx->lvl_floor[i] <= floor) return BZ_OK;
   if (ctx->k - floor < D) return BZ_OK;  // no subsets: nothing reads it
   const size_t n = (size_t)binom_sat(ctx->k - floor, D);
-  // whole K5p tiles (two accumulator widths) plus one tile of slack
-  const size_t N = bz::k4_tile_rows<true, true>();
+  // whole K5t tiles (three accumulator widths; also covers K5p's two) plus
+  // one tile of slack
+  const size_t N = bz::k4_tile_rows<true, 3>();
   ctx->lvl_rows[i] = (n + N - 1) / N * N + N;
   const size_t row_bytes = 16 * (size_t)(bz::k5_padmagic(ctx->w32) ? ctx->w32 + 1 : ctx->w32);
   const size_t bytes = (size_t)ctx->m * ctx->lvl_rows[i] * row_bytes;
@@ -588,9 +593,12 @@ int ensure_triples(bz_ctx* ctx, int which) {
 
 template <int W>
 int launch_w(bz_ctx* ctx, const RoundArgs& a, bool hist, const PlanShape& shape) {
-  if constexpr (W == 1 || W == 3)
-    if (shape.kernel == 6) return launch_umma<W, true, true>(ctx, a);
-  if (shape.kernel == 6) return fail(ctx, BZ_ERR_STATE, "K5p needs W = 1 or 3, not %d", W);
+  if constexpr (W == 1 || W == 3) {
+    if (shape.kernel == 6) return launch_umma<W, true, 2>(ctx, a);
+    if (shape.kernel == 7) return launch_umma<W, true, 3>(ctx, a);
+    if (shape.kernel == 8) return launch_umma<W, true, 4>(ctx, a);
+  }
+  if (shape.kernel >= 6) return fail(ctx, BZ_ERR_STATE, "K5p/K5t need W = 1 or 3, not %d", W);
   if (shape.kernel == 5) return launch_umma<W, true>(ctx, a);
   if (shape.kernel == 4) return launch_umma<W, false>(ctx, a);
   if (shape.kernel == 3) return launch_tc<W>(ctx, a);
@@ -710,6 +718,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     a.trace_from = getenv("BZ_K4_TRACE_FROM") ? atoi(getenv("BZ_K4_TRACE_FROM")) : 0;
     a.ctrace = (i == count - 1) ? ctrace : nullptr;
     a.trace_ell = getenv("BZ_K4_TRACE_ELL") ? atoi(getenv("BZ_K4_TRACE_ELL")) : -1;
+    a.chain = i > 0 ? todo[i - 1].a.bound : nullptr;
     todo[i].shape = shape;
     todo[i].run = nchunks > 0 && (unsigned long long)shard < nchunks;
   }
@@ -1120,7 +1129,7 @@ int bz_elided(bz_ctx* ctx, uint64_t* out_mask) {
 
 int bz_set_engine(bz_ctx* ctx, int engine) {
   if (!ctx) return BZ_ERR_ARGUMENT;
-  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4P)
+  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4Q)
     return fail(ctx, BZ_ERR_ARGUMENT, "unknown engine %d", engine);
   ctx->engine = engine;
   return BZ_OK;
@@ -1135,7 +1144,7 @@ int bz_plan(int m, int k, int g, int engine, int nshards, int64_t* out, int cap,
   if (binom_sat(k, g) >= (1ull << 62)) return BZ_ERR_TOO_LARGE;
   std::vector<Group> gs;
   unsigned long long nchunks = 0;
-  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4P) return BZ_ERR_ARGUMENT;
+  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4Q) return BZ_ERR_ARGUMENT;
   if (nshards < 1) return BZ_ERR_ARGUMENT;
   int rc = build_plan(nullptr, m, k, g, -1, pass_shape(engine, g, false), nshards, gs, &nchunks);
   if (rc) return rc;

@@ -74,6 +74,8 @@ struct RoundArgs {
   int trace_from;              // first traced tile (BZ_K4_TRACE_FROM)
   int trace_ell;               // or: from the first chunk with ell >= this (BZ_K4_TRACE_ELL)
   long long* ctrace;           // K4/K5 per-chunk timeline (BZ_K4_DEBUG & 32), else null
+  const int* chain;            // batched rounds: the previous round's bounds (its U
+                               // after the round tightens this round's start), or null
 };
 
 __host__ __device__ constexpr int padded_words(int w) {
@@ -374,6 +376,11 @@ k1_round_min(const RoundArgs a) {
   uint32_t *srows, *spx;
   Group* sgroups;
   stage<W>(a, srows, spx, sgroups, smem);
+  if (a.chain && threadIdx.x == 0) {
+    // batched round: start from the U the previous round ended with
+    const int u = ((volatile const int*)a.chain)[0];
+    for (int j = 0; j <= a.m; ++j) atomicMin(a.bound + j, u);
+  }
 
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;

@@ -124,6 +124,11 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   uint32_t *srows, *spx;
   Group* sgroups;
   stage<W>(a, srows, spx, sgroups, smem);  // ends with __syncthreads
+  if (a.chain && threadIdx.x == 0) {
+    // batched round: start from the U the previous round ended with
+    const int u = ((volatile const int*)a.chain)[0];
+    for (int j = 0; j <= a.m; ++j) atomicMin(a.bound + j, u);
+  }
 
   const unsigned FULL = 0xffffffffu;
   const int tid = threadIdx.x;

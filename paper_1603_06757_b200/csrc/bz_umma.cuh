@@ -77,6 +77,14 @@ constexpr int kUmmaM = 128;       // prefixes per A tile = producer threads
 #ifndef BZ_K5_MAGIC
 #define BZ_K5_MAGIC 1
 #endif
+// K5p geometry: accumulator buffers (= MMA issuer warps; N = 480 / BUFS
+// columns each) and epilogue warps
+#ifndef BZ_K5P_BUFS
+#define BZ_K5P_BUFS 2
+#endif
+#ifndef BZ_K5P_EPI_WARPS
+#define BZ_K5P_EPI_WARPS 16
+#endif
 // K5 accumulators start at 1.5 * 2^23 (one extra MMA per part from two tiny
 // constant operands): the fp32 sum then carries the integer dot product in
 // its low 16 bits, so the epilogue reads them with .pack::16b (half the
@@ -94,6 +102,7 @@ constexpr int kUmmaMA = BZ_K4_MA; // K4 A tiles (consecutive prefix steps) per B
 constexpr int kTmemCols = 512;    // accumulators (+ K5 scale factors)
 constexpr int kSfCol = 480;       // K5 scale-factor columns [480, 512)
 constexpr int kUmmaN4 = kSfCol / BZ_K5_BUFS;  // K5 triples per B tile (240 / 120)
+constexpr int kUmmaN4P = kSfCol / BZ_K5P_BUFS;  // K5p accumulator columns per tile
 constexpr int kMaxStages = 8;
 constexpr int kMaxAcc = 8;
 constexpr int kMaxABuf = 4;
@@ -108,10 +117,10 @@ constexpr int kBarSlots = 2 * kMaxABuf + 2 * kMaxStages + 2 * kMaxAcc + 2 * kChu
 //                     MMAs: tcgen05.mma issue stalls while the pipe is busy)
 //   E + ACC           loader
 //   E + ACC + 1 .. 4  producers (thread r <-> prefix row r)
-template <bool F4>
+template <bool F4, int CW = 1>
 struct K4Roles {
-  static constexpr int E = F4 ? BZ_K5_EPI_WARPS : BZ_K4_EPI_WARPS;
-  static constexpr int ACC = F4 ? BZ_K5_BUFS : kTmemCols / (kUmmaMA * kUmmaN);
+  static constexpr int E = CW > 1 ? BZ_K5P_EPI_WARPS : (F4 ? BZ_K5_EPI_WARPS : BZ_K4_EPI_WARPS);
+  static constexpr int ACC = CW > 1 ? BZ_K5P_BUFS : (F4 ? BZ_K5_BUFS : kTmemCols / (kUmmaMA * kUmmaN));
   static constexpr int MMA0 = E;
   static constexpr int LOAD = E + ACC;
   static constexpr int PROD0 = E + ACC + 1;
@@ -131,38 +140,47 @@ struct K4Roles {
                 "roles");
 };
 
-template <bool F4> __host__ __device__ constexpr int k4_n() { return F4 ? kUmmaN4 : kUmmaN; }
+template <bool F4, int CW = 1> __host__ __device__ constexpr int k4_n() {
+  return CW > 1 ? kUmmaN4P : (F4 ? kUmmaN4 : kUmmaN);
+}
 // bytes per table (B) row: K4 one byte per column, K5 one nibble
 // K5 with the padding-chunk offset (odd W): tables carry the pad chunk
 __host__ __device__ constexpr bool k5_padmagic(int w) { return kK5Magic && (w & 1); }
 template <bool F4> __host__ __device__ constexpr int k4_row_bytes(int w) {
   return F4 ? 16 * (k5_padmagic(w) ? w + 1 : w) : 32 * w;
 }
-// 16-byte K chunks per A row (K5 pads to whole K = 64 MMAs; the pair form
-// K5p carries two offset chunks, W data chunks + 2)
-template <bool F4, bool PR = false> __host__ __device__ constexpr int k4_a_chunks(int w) {
-  return PR ? w + 2 : (F4 ? 2 * ((w + 1) / 2) : 2 * w);
+// 16-byte K chunks per A row (K5 pads to whole K = 64 MMAs; K5p / K5t with
+// CW codewords per accumulator column carry CW offset chunks after the W
+// data chunks)
+// codewords per accumulator column of kernel form CW (1 = K5, 2 = K5p,
+// 3 = K5t, 4 = K5q: two codewords as bytes)
+__host__ __device__ constexpr int k5_ncw(int cw) { return cw == 4 ? 2 : cw; }
+template <bool F4, int CW = 1> __host__ __device__ constexpr int k4_a_chunks(int w) {
+  return CW > 1 ? w + k5_ncw(CW) : (F4 ? 2 * ((w + 1) / 2) : 2 * w);
 }
 // MMAs per tile (per half for K5p)
 template <bool F4> __host__ __device__ constexpr int k4_passes(int w) { return k4_a_chunks<F4>(w) / 2; }
 // table rows per B tile: K5p pairs two rows per accumulator column
-template <bool F4, bool PR = false> __host__ __device__ constexpr int k4_tile_rows() {
-  return PR ? 2 * k4_n<F4>() : k4_n<F4>();
+template <bool F4, int CW = 1> __host__ __device__ constexpr int k4_tile_rows() {
+  return k5_ncw(CW) * k4_n<F4, CW>();
 }
-template <bool F4, bool PR = false> __host__ __device__ constexpr uint32_t k4_tile_b(int w) {
-  return (uint32_t)(k4_tile_rows<F4, PR>() * k4_row_bytes<F4>(w));
+template <bool F4, int CW = 1> __host__ __device__ constexpr uint32_t k4_tile_b(int w) {
+  return (uint32_t)(k4_tile_rows<F4, CW>() * k4_row_bytes<F4>(w));
 }
-template <bool F4, bool PR = false> __host__ __device__ constexpr uint32_t k4_tile_a(int w) {
-  return (uint32_t)(kUmmaM * 16 * k4_a_chunks<F4, PR>(w));
+template <bool F4, int CW = 1> __host__ __device__ constexpr uint32_t k4_tile_a(int w) {
+  return (uint32_t)(kUmmaM * 16 * k4_a_chunks<F4, CW>(w));
 }
 // A-tile ring depth (producers run that many prefix steps ahead)
 template <bool F4> __host__ __device__ constexpr int k4_abufs(int w) {
   return F4 && w <= 6 ? 4 : 2;
 }
 // B-tile ring depth: K5 ~136 KB of stages, K4 4 x 40 KB at W = 5
-template <bool F4, bool PR = false> __host__ __device__ constexpr int k4_stages(int w) {
-  return F4 ? (136000 / (int)k4_tile_b<true, PR>(w) < kMaxStages
-                   ? 136000 / (int)k4_tile_b<true, PR>(w)
+#ifndef BZ_K5P_STAGE_BYTES
+#define BZ_K5P_STAGE_BYTES 160000
+#endif
+template <bool F4, int CW = 1> __host__ __device__ constexpr int k4_stages(int w) {
+  return F4 ? ((CW > 1 ? BZ_K5P_STAGE_BYTES : 136000) / (int)k4_tile_b<true, CW>(w) < kMaxStages
+                   ? (CW > 1 ? BZ_K5P_STAGE_BYTES : 136000) / (int)k4_tile_b<true, CW>(w)
                    : kMaxStages)
             : (w <= 5 ? 4 : (w <= 6 ? 3 : 2));
 }
@@ -186,24 +204,37 @@ __host__ __device__ __forceinline__ uint4 e2m1_pm1(uint32_t v) {
                     ((v << 1) & 0x88888888u) | 0x22222222u, (v & 0x88888888u) | 0x22222222u);
 }
 
-// K5 table offset chunk: elements 0..15 = 1.0, 16..31 = 4.0 (bytes 0..7 /
-// 8..15).  K5 pairs it with an A chunk holding 1.5 at element 0 only; K5p
-// with k5p_offset_chunk(T), whose dot product with it is exactly T.
+// K5 table offset chunk (the extra K chunk of every table row for odd W):
+// in each 16-element block (bytes 0..7 / 8..15) elements 0..7 = 4.0 and
+// 8..15 = 1.0.  The A side picks what it adds with its own offset chunk:
+// K5 1.5 at element 8 (block scale 2^23), K5p / K5t pad_chunk(T, 0) = T,
+// K5q pad_chunk(X, 128) with per-block scales.
 __host__ __device__ __forceinline__ uint4 k5_table_offset_chunk() {
-  return make_uint4(0x22222222u, 0x22222222u, 0x66666666u, 0x66666666u);
+  return make_uint4(0x66666666u, 0x22222222u, 0x66666666u, 0x22222222u);
 }
-// e2m1 nibbles whose dot product with k5_table_offset_chunk() is T
-// (0 <= T <= 4 * 16 * 6 + 3): T & 3 at element 0 (x1.0), T >> 2 as 6.0s
-// plus a remainder on elements 16.. (x4.0)
-__device__ __forceinline__ uint4 k5p_offset_chunk(int T) {
-  // e2m1 nibble of 0, 1, 2, 3, 4, 4 (+ 1.0 on the next element for 5)
+// v (0 <= v <= 46, or 48) as 8 e2m1 nibbles: 6.0s, then the remainder
+__host__ __device__ __forceinline__ uint32_t e2m1_sum8(int v) {
+  // e2m1 nibble of 0, 1, 2, 3, 4, 4 (+ 1.0 on the next nibble for 5)
   constexpr uint32_t kSmall = 0x665420u;
-  const int r = T & 3, q = T >> 2, q6 = q / 6, qr = q - 6 * q6;
-  unsigned long long x = q6 ? (0x7777777777777777ull >> (64 - 4 * q6)) : 0ull;
-  x |= (unsigned long long)((kSmall >> (4 * qr)) & 0xFu) << (4 * q6);
-  x |= (unsigned long long)(qr == 5 ? 0x2u : 0u) << (4 * q6 + 4);
-  return make_uint4((kSmall >> (4 * r)) & 0xFu, 0u, (uint32_t)x, (uint32_t)(x >> 32));
+  const int n6 = v / 6, rem = v - 6 * n6;
+  uint32_t x = n6 ? (0x77777777u >> (32 - 4 * n6)) : 0u;
+  if (n6 < 8) x |= ((kSmall >> (4 * rem)) & 0xFu) << (4 * n6);
+  if (rem == 5) x |= 0x2u << (4 * n6 + 4);
+  return x;
 }
+// one 16-element A block whose dot product with a table offset block is T
+// (0 <= T <= 238): 6.0s on the 4.0 elements (24 each), the rest on the 1.0s
+__host__ __device__ __forceinline__ unsigned long long e2m1_block(int T) {
+  const int k = min(8, T / 24);
+  const uint32_t lo = k ? (0x77777777u >> (32 - 4 * k)) : 0u;
+  return (unsigned long long)lo | ((unsigned long long)e2m1_sum8(T - 24 * k) << 32);
+}
+// A offset chunk: T0 on block 0, T1 on block 1
+__host__ __device__ __forceinline__ uint4 pad_chunk(int T0, int T1) {
+  const unsigned long long b0 = e2m1_block(T0), b1 = T1 ? e2m1_block(T1) : 0ull;
+  return make_uint4((uint32_t)b0, (uint32_t)(b0 >> 32), (uint32_t)b1, (uint32_t)(b1 >> 32));
+}
+__host__ __device__ __forceinline__ uint4 k5p_offset_chunk(int T) { return pad_chunk(T, 0); }
 
 // tcgen05 shared-memory matrix descriptor, SWIZZLE_NONE, K-major:
 // LBO = distance between the two 16-byte K chunks of one MMA (128 B here),
@@ -259,6 +290,33 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (spin > (1ull << 26)) __trap();
   }
 }
+// Sleeping wait: try_wait with a suspend-time hint, so a warp that waits
+// long (producers between chunks, the loader behind a full ring) sleeps in
+// the barrier instead of spinning through issue slots and ALU ops.
+#ifndef BZ_K5_SLEEPMASK
+#define BZ_K5_SLEEPMASK 37  // non-critical waits sleep (chunk queue, A ring, loader)
+#endif
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  for (uint32_t spin = 0;; ++spin) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity), "r"(20000u)
+        : "memory");
+    if (done) return;
+    if (spin > (1u << 20)) __trap();
+  }
+}
+template <int BIT>
+__device__ __forceinline__ void mbar_wait_sel(uint32_t bar, uint32_t parity) {
+  if constexpr ((BZ_K5_SLEEPMASK & BIT) != 0) mbar_wait_sleep(bar, parity);
+  else mbar_wait(bar, parity);
+}
+template <int BIT>
+__device__ __forceinline__ void mbar_wait_fast_sel(uint32_t bar, uint32_t parity);
+
 // Tight wait (loop inside PTX; labels are local to the braces): used on the
 // MMA-issuing warp, where every cycle of handshake latency idles the pipe.
 __device__ __forceinline__ void mbar_wait_fast(uint32_t bar, uint32_t parity) {
@@ -269,6 +327,11 @@ __device__ __forceinline__ void mbar_wait_fast(uint32_t bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(bar),
       "r"(parity)
       : "memory");
+}
+template <int BIT>
+__device__ __forceinline__ void mbar_wait_fast_sel(uint32_t bar, uint32_t parity) {
+  if constexpr ((BZ_K5_SLEEPMASK & BIT) != 0) mbar_wait_sleep(bar, parity);
+  else mbar_wait_fast(bar, parity);
 }
 __device__ __forceinline__ bool elect_one() {
   uint32_t pred = 0;
@@ -309,6 +372,17 @@ __device__ __forceinline__ void umma_mxf4(uint32_t d_tmem, uint64_t a_desc, uint
   asm volatile(
       "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%5], [%6], "
+      "p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
+      : "memory");
+}
+// kind::mxf4nvf4: e2m1 operands, ue4m3 scales per 16-element block
+__device__ __forceinline__ void umma_nvf4(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate, uint32_t sfa,
+                                          uint32_t sfb) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf4nvf4.block_scale.block16 [%0], %1, %2, %3, [%5], [%6], "
       "p;\n\t}" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
       : "memory");
@@ -551,11 +625,11 @@ __global__ void k_build_triples_umma(const uint32_t* __restrict__ rows,
   }
 }
 
-template <int W, bool F4, bool PR = false>
+template <int W, bool F4, int CW = 1>
 __host__ __device__ inline size_t k4_smem_bytes(int m, int k, int ngroups) {
   size_t off = (smem_base_bytes<W>(m, k, ngroups) + 1023) & ~size_t(1023);
-  off += (size_t)k4_stages<F4, PR>(W) * k4_tile_b<F4, PR>(W);
-  off += (size_t)k4_abufs<F4>(W) * kUmmaMA * k4_tile_a<F4, PR>(W);
+  off += (size_t)k4_stages<F4, CW>(W) * k4_tile_b<F4, CW>(W);
+  off += (size_t)k4_abufs<F4>(W) * kUmmaMA * k4_tile_a<F4, CW>(W);
   off += F4 ? kMagicBytes : 0;   // K5 magic operands
   off += kBarSlots * 8 + 16;     // barriers + TMEM base
   off += k4_abufs<F4>(W) * kUmmaMA * kUmmaM * sizeof(int);  // prefix weights of the A buffers
@@ -625,22 +699,26 @@ __device__ __forceinline__ K4Chunk k4_decode(const Group* sg, int ngroups,
 // unit block scales): one persistent CTA per SM, warp-specialised (see the
 // file comment).  The two differ only in operand encoding, MMA kind,
 // accumulator type (s32 read as packed s16 / f32) and tile geometry.
-template <int W, bool F4, bool PR>
-__global__ void __launch_bounds__(K4Roles<F4>::THREADS, 1)
+template <int W, bool F4, int CW>
+__global__ void __launch_bounds__(K4Roles<F4, CW>::THREADS, 1)
 k4_round_umma(const RoundArgs a, const K4Tables tabs) {
+  constexpr bool PR = CW > 1;  // K5p (CW = 2) / K5t (CW = 3) / K5q (CW = 4)
+  constexpr bool Q = CW == 4;  // K5q: two codewords as bytes, block16 scales
+  constexpr int NC = k5_ncw(CW);  // codewords per accumulator column
   static_assert(!F4 || kUmmaMA == 1, "K5 runs one A tile per B tile");
+  static_assert(CW >= 1 && CW <= 4, "kernel form");
   static_assert(!PR || (F4 && kK5Magic && (W & 1) && W <= 3 && BZ_K5_SPLIT == 1 &&
                         BZ_K5_EPI_GROUPS == 1),
-                "K5p: odd W <= 3 (stored weights <= 127 fit the 7-bit high field)");
-  constexpr int N = k4_n<F4>();
-  constexpr int TR = k4_tile_rows<F4, PR>();  // table rows per B tile
-  constexpr int S = k4_stages<F4, PR>(W);
+                "K5p/K5t: odd W <= 3 (stored weights <= 127 fit the 7-bit fields)");
+  constexpr int N = k4_n<F4, CW>();
+  constexpr int TR = k4_tile_rows<F4, CW>();  // table rows per B tile
+  constexpr int S = k4_stages<F4, CW>(W);
   constexpr int P = k4_passes<F4>(W);        // MMAs per tile (K5p: per half)
-  constexpr int CA = k4_a_chunks<F4, PR>(W); // 16-byte K chunks per A row
+  constexpr int CA = k4_a_chunks<F4, CW>(W); // 16-byte K chunks per A row
   constexpr int CB = k4_row_bytes<F4>(W) / 16;  // ... per B row
-  constexpr uint32_t TB = k4_tile_b<F4, PR>(W);
-  constexpr uint32_t TA = k4_tile_a<F4, PR>(W);
-  using RL = K4Roles<F4>;
+  constexpr uint32_t TB = k4_tile_b<F4, CW>(W);
+  constexpr uint32_t TA = k4_tile_a<F4, CW>(W);
+  using RL = K4Roles<F4, CW>;
   constexpr int ACC = RL::ACC;
   constexpr int E = RL::E;
   constexpr int EGRP = RL::EGRP;
@@ -648,7 +726,9 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
   constexpr int SPLIT = RL::SPLIT;
   constexpr int NH = N / SPLIT;  // accumulator columns per part
   static_assert(NH % 8 == 0, "parts are whole 8-row groups of the B tile");
-  constexpr uint32_t IDESC = F4 ? mxf4_idesc(NH) : kUmmaIdesc;
+  // K5q: kind::mxf4nvf4 with ue4m3 block16 scales (scale-format bit 23 clear)
+  constexpr uint32_t IDESC =
+      F4 ? (Q ? mxf4_idesc(NH) & ~(1u << 23) : mxf4_idesc(NH)) : kUmmaIdesc;
   static_assert(S <= kMaxStages, "barrier slots");
   static_assert(EC * (RL::EW / 4) == N && (F4 ? EC % 4 == 0 && EC <= 128 : EC % 32 == 0),
                 "epilogue");
@@ -715,14 +795,27 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
   stage<W>(a, srows, spx, sgroups, smem);  // ends with __syncthreads
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
+  if (a.chain && tid == 0) {
+    // a batched round starts from the U its predecessor ended with (the
+    // running U the reference clips with, m/engine.py:209-211); atomicMin
+    // keeps it race-free against blocks already lowering the bound
+    const int u = ((volatile const int*)a.chain)[0];
+    for (int j = 0; j <= a.m; ++j) atomicMin(a.bound + j, u);
+  }
   if constexpr (F4) {
     // unit block scales (ue8m0 0x7F = 2^0) in TMEM columns [kSfCol, 512);
     // the zero K-padding chunk of both A buffers (odd W)
     if (warp < 4) {
       for (int c = 0; c < 512 - kSfCol; c += 8)
         tmem_st8(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(kSfCol + c),
-                 kSfCol + c == kSfColMagic ? (PR ? 0x8F8F8F8Fu : 0x96969696u)
-                                           : (kSfCol + c == kSfColPad ? 0x7F7F967Fu : 0x7F7F7F7Fu));
+                 Q ? (kSfCol + c == kSfColMagic ? 0x78787878u   // ue4m3 256: half b
+                      : kSfCol + c == kSfColPad ? 0x78383838u  // A: 256 on block 3
+                                                : 0x38383838u) // ue4m3 1.0
+                 : kSfCol + c == kSfColMagic
+                     ? (PR ? 0x8F8F8F8Fu : 0x96969696u)                       // 2^16 | 2^23
+                     : (kSfCol + c == kSfColPad ? (CW == 3 ? 0x87878787u      // 2^8
+                                                           : 0x7F7F967Fu)
+                                                : 0x7F7F7F7Fu));
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
     if (kK5Magic && tid < (int)kMagicBytes / 16) {
@@ -736,11 +829,11 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       fence_proxy_async();
     }
     if (!PR && CA > W && warp >= RL::PROD0) {
-      // the A padding chunk: zero, or 1.5 at element 0 (padding-chunk offset)
+      // the A padding chunk: zero, or 1.5 at element 8 (padding-chunk offset)
       const int r = tid - 32 * RL::PROD0;
       for (int ab = 0; ab < NA; ++ab)
         *reinterpret_cast<uint4*>(sA + ab * TA + umma_off_c(r, W, CA)) =
-            make_uint4(k5_padmagic(W) ? 0x3u : 0u, 0u, 0u, 0u);
+            make_uint4(0u, k5_padmagic(W) ? 0x3u : 0u, 0u, 0u);  // 1.5 at element 8
       fence_proxy_async();
     }
     tc_fence_before();
@@ -760,7 +853,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
     uint32_t grp = 0, tcount = 0, toff = k4_trace_off(a);
     for (uint32_t qi = 0;; ++qi) {
       const int qs = qi % kChunkQ;
-      mbar_wait(qfull(qs), (qi / kChunkQ) & 1);
+      mbar_wait_sel<1>(qfull(qs), (qi / kChunkQ) & 1);
       const long long qchunk = s_q[qs];
       __syncwarp();
       if (lane == 0) mbar_arrive(qempty(qs));
@@ -769,9 +862,13 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       const K4Chunk c = k4_decode<TR>(sgroups, a.ngroups, chunk, k);
       k4_trace_chunk(a, toff, c.gr.ell, tcount);
       int best = INT_MAX;
+      // K5t: stored weights below thr can lower this Gamma's bound
+      int thr = 127;
+      if constexpr (CW == 3)
+        thr = max(0, min(127, ((volatile int*)a.bound)[1 + c.gr.gamma] - gamma_woff(a, c.gr.gamma)));
       for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
         const int ab = grp % NA;
-        mbar_wait(afull(ab), (grp / NA) & 1);
+        mbar_wait_sel<1>(afull(ab), (grp / NA) & 1);
         int wt[kUmmaMA];
 #pragma unroll
         for (int j = 0; j < kUmmaMA; ++j) wt[j] = s_wt[(ab * kUmmaMA + j) * kUmmaM + r];
@@ -781,12 +878,13 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
 #pragma unroll
         for (int j = 0; j < kUmmaMA; ++j) rmin[j] = INT_MAX / 2;
         float fmin_acc = __int_as_float(0x7f800000);  // K5: +inf
+        int lx = 128;  // K5q: this row's bytes below lx can still lower its minimum
         for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount) {
           if (EGRP > 1 && (int)(tcount % EGRP) != egroup) continue;
           const int buf = tcount % ACC;
           const int hb = buf * SPLIT + part;
           if (warp == 0 && lane == 0) k4_trace(a, 8, tcount, toff);
-          mbar_wait(accfull(hb), (tcount / ACC) & 1);
+          mbar_wait_sel<2>(accfull(hb), (tcount / ACC) & 1);
           if (warp == 0 && lane == 0) k4_trace(a, 9, tcount, toff);
           if (!BZ_K5_NOFENCE) tc_fence_after();
           if (warp == 0 && lane == 0) k4_trace(a, 2, tcount, toff);
@@ -799,27 +897,122 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
             if (lane == 0) mbar_arrive(accempty(hb));
             continue;
           }
-          if constexpr (PR) {
+          if constexpr (Q) {
+            // K5q: every column holds 2^23 + x_a + 2^8 x_b, x = wt + 128 -
+            // thr (thr = wt[0], the producer's threshold for this row): the
+            // low 16 bits of two columns are four bytes per register, and a
+            // codeword can lower the bound iff its byte has bit 7 clear.
+            // One 3-input AND per two registers; exact minima only then.
+            constexpr int NP = EC / 2;
+            const int la = c.slice - t * TR - EC * slice_id;  // half-a columns < la valid
+            uint32_t v[NP];
+            tmem_ld_cols_p<EC>(tb, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i + 1 < NP; i += 2) asm volatile("" : "+r"(v[i]), "+r"(v[i + 1]) : : "memory");
+            if (NP % 2) asm volatile("" : "+r"(v[NP - 1]) : : "memory");
+            if (!BZ_K5_NOFENCE) tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(accempty(hb));  // accumulators are in registers
+            if (la - N < EC) {
+#pragma unroll
+              for (int i = 0; i < NP; ++i) {
+                if (2 * i >= la) v[i] |= 0x000000FFu;
+                if (2 * i >= la - N) v[i] |= 0x0000FF00u;
+                if (2 * i + 1 >= la) v[i] |= 0x00FF0000u;
+                if (2 * i + 1 >= la - N) v[i] |= 0xFF000000u;
+              }
+            }
+            uint32_t acc = 0xFFFFFFFFu;
+#pragma unroll
+            for (int i = 0; i + 1 < NP; i += 2) acc &= v[i] & v[i + 1];
+            if (NP % 2) acc &= v[NP - 1];
+            if ((~acc) & 0x80808080u) {
+              // some byte is below the producer's threshold; below this
+              // row's own minimum so far?  (x - lx*0x01010101) & ~x has bit
+              // 7 of the lowest such byte set, lx <= 128)
+              const uint32_t kx = (uint32_t)lx * 0x01010101u;
+              uint32_t h = 0;
+#pragma unroll
+              for (int i = 0; i < NP; ++i) h |= (v[i] - kx) & ~v[i];
+              if (h & 0x80808080u) {
+                int mn = lx;
+#pragma unroll
+                for (int i = 0; i < NP; ++i)
+#pragma unroll
+                  for (int b = 0; b < 4; ++b) mn = min(mn, (int)((v[i] >> (8 * b)) & 0xFFu));
+                lx = mn;
+                const int w = mn - 128 + wt[0];
+                rmin[0] = min(rmin[0], w);
+                // publish at once: the producers' next thresholds tighten
+                const int wg = w + gamma_woff(a, c.gr.gamma);
+                if (wg < ((volatile int*)a.bound)[1 + c.gr.gamma]) {
+                  atomicMin(a.bound + 1 + c.gr.gamma, wg);
+                  atomicMin(a.bound, wg);
+                }
+              }
+            }
+          } else if constexpr (CW == 3) {
+            // K5t: every column holds three codewords, 2^23 + wt_a + 2^8 wt_b
+            // + 2^16 wt_c: bytes 0..2 are stored weights <= 96, byte 3 the
+            // exponent.  A SWAR test finds whether any byte is below this
+            // row's threshold thr (x - thr*0x010101 borrows into bit 7 of the
+            // lowest such byte; no byte exceeds 127); only then are the
+            // exact minima taken (rare once the bound has settled).
+            const int la = c.slice - t * TR - EC * slice_id;  // part-0 columns < la valid
+            uint32_t v[EC];
+            tmem_ld_cols<EC>(tb, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < EC; i += 4) tmem_regs4_after_wait(v + i);
+            if (!BZ_K5_NOFENCE) tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(accempty(hb));  // accumulators are in registers
+            if (la - 2 * N < EC) {
+#pragma unroll
+              for (int i = 0; i < EC; ++i)
+#pragma unroll
+                for (int q = 0; q < 3; ++q)
+                  if (i >= la - q * N) v[i] |= 0x7Fu << (8 * q);  // 127: never below thr
+            }
+            const uint32_t kthr = (uint32_t)thr * 0x00010101u;
+            uint32_t acc = 0;
+#pragma unroll
+            for (int i = 0; i + 1 < EC; i += 2) acc |= (v[i] - kthr) | (v[i + 1] - kthr);
+            if (EC & 1) acc |= v[EC - 1] - kthr;
+            if (acc & 0x00808080u) {
+              int mn = INT_MAX / 2;
+#pragma unroll
+              for (int i = 0; i < EC; ++i)
+                mn = min(mn, min((int)(v[i] & 0x7Fu),
+                                 min((int)((v[i] >> 8) & 0x7Fu), (int)((v[i] >> 16) & 0x7Fu))));
+              rmin[0] = min(rmin[0], mn);
+              thr = min(thr, mn);
+            }
+          } else if constexpr (PR) {
             // K5p: every column holds two codewords, 2^23 + wt_a + 2^16 wt_b
             // (stored weights <= 96): bits 0..15 = wt_a, bits 16..31 =
             // 0x4B00 + wt_b, so one s16x2 minimum serves both.  Two loads of
             // EC/2 columns (register budget), then the buffer is released.
-            constexpr int H = EC / 2;
+            constexpr int NPH = EC > 64 ? 2 : 1;
+            constexpr int H = EC / NPH;
+            static_assert(H * NPH == EC && H % 4 == 0, "K5p epilogue phases");
             const int la = c.slice - t * TR - EC * slice_id;  // half-a columns < la valid
             const int lb = la - N;                             // half-b columns < lb valid
             uint32_t m0 = 0x7FFF7FFFu, m1 = 0x7FFF7FFFu;
 #pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
+            for (int hh = 0; hh < NPH; ++hh) {
               uint32_t v[H];
               tmem_ld_cols<H>(tb + hh * H, v);
               tmem_ld_wait();
 #pragma unroll
               for (int i = 0; i < H; i += 4) tmem_regs4_after_wait(v + i);
-              if (hh == 1) {
+              if (hh == NPH - 1) {
                 if (!BZ_K5_NOFENCE) tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(accempty(hb));  // accumulators are in registers
               }
+              if (a.debug & 64) continue;  // timing experiment: loads only
               if (lb < EC) {
 #pragma unroll
                 for (int i = 0; i < H; ++i) {
@@ -969,7 +1162,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
     uint32_t grp = 0;
     for (uint32_t qi = 0;; ++qi) {
       const int qs = qi % kChunkQ;
-      mbar_wait(qfull(qs), (qi / kChunkQ) & 1);
+      mbar_wait_sel<4>(qfull(qs), (qi / kChunkQ) & 1);
       const long long qchunk = s_q[qs];
       __syncwarp();
       if (lane == 0) mbar_arrive(qempty(qs));
@@ -989,7 +1182,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       wk.init(cnt > 0 ? first : c.bfirst, a.g - 1 - c.gr.depth, c.gr.ell, R, a.binom);
       for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
         const int ab = grp % NA;
-        mbar_wait(aempty(ab), ((grp / NA) & 1) ^ 1);
+        mbar_wait_sel<4>(aempty(ab), ((grp / NA) & 1) ^ 1);
 #pragma unroll 1
         for (int j = 0; j < kUmmaMA; ++j) {
           // step j of the group; past this row's range the last prefix repeats
@@ -1014,11 +1207,25 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
               *reinterpret_cast<uint4*>(dst + umma_off_c(r, 2 * jj + 1, CA)) = hi;
             }
           }
-          if constexpr (PR) {
-            // offset chunks: w(P) (half a, scale 1) and w(P) + 128 (half b,
-            // scale 2^16, which also supplies the 2^23 offset)
-            *reinterpret_cast<uint4*>(dst + umma_off_c(r, W, CA)) = k5p_offset_chunk(wt);
-            *reinterpret_cast<uint4*>(dst + umma_off_c(r, W + 1, CA)) = k5p_offset_chunk(wt + 128);
+          if constexpr (Q) {
+            // K5q: both fields read x = wt + 128 - thr (thr: this Gamma's
+            // bound less the weight offset, as this thread sees it now), so
+            // a codeword can lower the bound iff bit 7 of its byte is clear;
+            // block 1 of the second chunk (scale 2^16) is the 2^23 offset
+            const int thr = max(0, min(127, ((volatile int*)a.bound)[1 + c.gr.gamma] -
+                                                gamma_woff(a, c.gr.gamma)));
+            const int x = wt + 128 - thr;
+            *reinterpret_cast<uint4*>(dst + umma_off_c(r, W, CA)) = pad_chunk(x, 0);
+            *reinterpret_cast<uint4*>(dst + umma_off_c(r, W + 1, CA)) = pad_chunk(x, 128);
+            wt = thr;  // the epilogue needs thr to turn a byte back into a weight
+          } else if constexpr (PR) {
+            // offset chunks: w(P) for every part (so each field is a whole
+            // stored weight), + 128 on the last (its scale 2^16 makes that the
+            // 2^23 offset)
+#pragma unroll
+            for (int q = 0; q < CW; ++q)
+              *reinterpret_cast<uint4*>(dst + umma_off_c(r, W + q, CA)) =
+                  k5p_offset_chunk(q == CW - 1 ? wt + 128 : wt);
           }
           s_wt[(ab * kUmmaMA + j) * kUmmaM + r] = wt;
         }
@@ -1052,7 +1259,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       uint32_t grp = 0, tcount = 0, toff = k4_trace_off(a);
       for (uint32_t qi = 0;; ++qi) {
         const int qs = qi % kChunkQ;
-        mbar_wait_fast(qfull(qs), (qi / kChunkQ) & 1);
+        mbar_wait_fast_sel<8>(qfull(qs), (qi / kChunkQ) & 1);
         const long long qchunk = s_q[qs];
         __syncwarp();
         if (lane == 0) mbar_arrive(qempty(qs));
@@ -1067,7 +1274,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
           // (every issuer waits for every step, so no issuer's arrivals run
           // ahead into a later phase of the A-buffer barriers)
           const int t0 = (int)((mb - (int)(tcount % ACC) + ACC) % ACC);
-          mbar_wait_fast(afull(ab), (grp / NA) & 1);
+          mbar_wait_fast_sel<8>(afull(ab), (grp / NA) & 1);
           for (int i = t0; i < ntile; i += ACC) {
             const uint32_t tc = tcount + (uint32_t)i;  // global tile number
             const int stg = (int)(tc % S);
@@ -1075,12 +1282,13 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
             // accumulator hand-back (the critical loop) is the last wait
             // before the MMAs
             if (lane == 0) k4_trace(a, 5, tc, toff);
-            mbar_wait_fast(bfull(stg), (tc / S) & 1);
+            mbar_wait_fast_sel<16>(bfull(stg), (tc / S) & 1);
             if (lane == 0) k4_trace(a, 6, tc, toff);
             const int valid = min(N, c.slice - (c.tile_lo + i) * TR);
 #pragma unroll
             for (int h = 0; h < SPLIT; ++h) {
-              mbar_wait_fast(accempty(mb * SPLIT + h), ((tc / ACC) & 1) ^ 1);
+              if (!(a.debug & 128))  // timing experiment: MMAs never wait for the epilogue
+                mbar_wait_fast_sel<16>(accempty(mb * SPLIT + h), ((tc / ACC) & 1) ^ 1);
               if (lane == 0 && h == 1) k4_trace(a, 13, tc, toff);
               if (!BZ_K5_NOFENCE) tc_fence_after();
               if (lane == 0 && h == 0) k4_trace(a, 1, tc, toff);
@@ -1093,20 +1301,26 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
                 // a part holding no valid suffix is only committed (its
                 // columns are masked anyway)
                 if (PR && !(a.debug & 4)) {
-                  // K5p: half a (table rows [0, N) of the stage, unit scales),
-                  // then half b (rows [N, 2N), B scale 2^16); the last half-b
-                  // MMA reads A chunks W-1 and W+1 (LBO 256 B) so it meets
-                  // the second offset chunk
+                  // K5p / K5t: part q of the column (table rows [qN, (q+1)N)
+                  // of the stage) with B scale 2^(8q) (K5t) / 2^(16q) (K5p);
+                  // its last MMA reads A chunks W-1 and W+q (LBO (q+1)*128 B)
+                  // so it meets offset chunk q
                   const uint32_t dj = dbase;
                   const uint64_t adj = a_desc0 + (uint64_t)(ab * (TA >> 4));
-                  const uint64_t bd1 = bd0 + (uint64_t)((N / 8) * CB * 8);
 #pragma unroll
-                  for (int kb = 0; kb < P; ++kb)
-                    umma_mxf4(dj, adj + 16u * kb, bd0 + 16u * kb, IDESC, kb > 0 ? 1u : 0u, sfa, sfb);
+                  for (int q = 0; q < NC; ++q) {
+                    const uint64_t bdq = bd0 + (uint64_t)(q * (N / 8) * CB * 8);
+                    const uint32_t sfq = q == 0 ? sfb : (CW == 3 && q == 1 ? sfp : sfm);
 #pragma unroll
-                  for (int kb = 0; kb < P; ++kb)
-                    umma_mxf4(dj, adj + 16u * kb + (kb == P - 1 ? (uint64_t)8 << 16 : 0ull),
-                              bd1 + 16u * kb, IDESC, 1u, sfa, sfm);
+                    for (int kb = 0; kb < P; ++kb) {
+                      const uint64_t ad = adj + 16u * kb + (kb == P - 1 ? (uint64_t)(8 * q) << 16 : 0ull);
+                      if constexpr (Q)  // K5q: A scale 256 on the offset block of the last MMA
+                        umma_nvf4(dj, ad, bdq + 16u * kb, IDESC, (q | kb) ? 1u : 0u,
+                                  (q == 1 && kb == P - 1) ? sfp : sfa, sfq);
+                      else
+                        umma_mxf4(dj, ad, bdq + 16u * kb, IDESC, (q | kb) ? 1u : 0u, sfa, sfq);
+                    }
+                  }
                 } else if (!(a.debug & 4) && valid > h * NH) {
 #pragma unroll
                   for (int j = 0; j < kUmmaMA; ++j) {
@@ -1148,7 +1362,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       volatile int* vb = a.bound;
       for (uint32_t qi = 0;; ++qi) {
         const int qs = qi % kChunkQ;
-        mbar_wait(qempty(qs), ((qi / kChunkQ) & 1) ^ 1);
+        mbar_wait_sel<32>(qempty(qs), ((qi / kChunkQ) & 1) ^ 1);
         // next chunk of this shard, or -1 (done, or U reached L_prev)
         const unsigned long long cidx = atomicAdd(a.counter, 1ull);
         const unsigned long long ch = cidx * (unsigned long long)a.nshards + a.shard;
@@ -1167,7 +1381,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
         for (long long p = 0; p < c.maxcnt; p += kUmmaMA) {
           for (int t = c.tile_lo; t < c.tile_hi; ++t, ++bcount) {
             const int stg = bcount % S;
-            mbar_wait(bempty(stg), ((bcount / S) & 1) ^ 1);
+            mbar_wait_sel<32>(bempty(stg), ((bcount / S) & 1) ^ 1);
             k4_trace(a, 0, bcount, toff);
             // only the rows this tile needs (8-row granularity); the rest of
             // the stage keeps stale rows whose columns the epilogue masks

@@ -27,11 +27,11 @@ def ctx():
     return _native.context(0)
 
 
-@pytest.fixture(params=["popc", "imma", "umma", "mxf4", "mxf4p"])
+@pytest.fixture(params=["popc", "imma", "umma", "mxf4", "mxf4p", "mxf4t", "mxf4q"])
 def engine(request):
     """Every kernel: K1 (XOR+POPC), K3 (legacy IMMA, g >= 4), K4 (tcgen05
-    kind::i8), K5 (kind::mxf4) and K5p (two codewords per accumulator
-    column; W = 1, 3 -- other widths run K5)."""
+    kind::i8), K5 (kind::mxf4), K5p / K5t (two / three codewords per
+    accumulator column; W = 1, 3 -- other widths run K5)."""
     _native.context(0).set_engine(request.param)
     yield request.param
     _native.context(0).set_engine("auto")
@@ -232,7 +232,7 @@ def test_early_exit_all_engines(ctx, engine):
 @pytest.mark.parametrize("k,g,floors", [(12, 6, "4,7"), (14, 8, "5,9"), (12, 5, "6"),
                                         (20, 7, "8,13"), (11, 9, "0,3")])
 @pytest.mark.parametrize("n", [20, 37, 70, 96, 160, 230])
-@pytest.mark.parametrize("kernel", ["mxf4", "mxf4p"])
+@pytest.mark.parametrize("kernel", ["mxf4", "mxf4p", "mxf4t", "mxf4q"])
 def test_mxf4_levels(monkeypatch, ctx, k, g, floors, n, kernel):
     """K5 / K5p with forced suffix levels (depth-4/5 tables): exact minima and
     combination counts per Gamma against the oracle (K5p runs at n = 20, 70,
@@ -336,17 +336,18 @@ def test_brute_force_rank_deficient():
 
 @pytest.mark.parametrize("n", [1, 17, 32, 33, 64, 80, 95, 96])
 @pytest.mark.parametrize("density", [0.05, 0.5, 0.97])
-def test_mxf4p_weight_range(ctx, n, density):
-    """K5p packs two stored weights into one fp32 accumulator (bits 0..15 and
-    16..22): every weight from 0 to n <= 96 must come back exact, including
-    all-zero and all-one codewords, slices crossing the 480-row tile and
-    both halves of a column."""
+@pytest.mark.parametrize("kernel", ["mxf4p", "mxf4t", "mxf4q"])
+def test_mxf4p_weight_range(ctx, n, density, kernel):
+    """K5p / K5t pack two / three stored weights into one fp32 accumulator
+    (bits 0..15 and 16..22 / bytes 0..2): every weight from 0 to n <= 96 must
+    come back exact, including all-zero and all-one codewords, slices
+    crossing the 480/720-row tile and every part of a column."""
     rng = random.Random(n * 100 + int(density * 100))
     k = 24
     rows = [sum(1 << b for b in range(n) if rng.random() < density) for _ in range(k)]
     rows[3] = rows[4]                      # a zero codeword at every even g >= 2
     rows[5] = (1 << n) - 1                 # an all-ones row
-    ctx.set_engine("mxf4p")
+    ctx.set_engine(kernel)
     try:
         ctx.load(family_words([BitMatrix(rows, n), BitMatrix(rows[::-1], n)], n), n)
         for g in (4, 5, 6, 7):
@@ -358,12 +359,13 @@ def test_mxf4p_weight_range(ctx, n, density):
 
 
 @pytest.mark.parametrize("n", [40, 96])
-def test_mxf4p_all_heavy(ctx, n):
+@pytest.mark.parametrize("kernel", ["mxf4p", "mxf4t", "mxf4q"])
+def test_mxf4p_all_heavy(ctx, n, kernel):
     """Every codeword heavy (odd g over identical all-ones rows: weight n),
     so the minimum is the largest value the packed fields carry."""
     k = 15
     rows = [(1 << n) - 1] * k
-    ctx.set_engine("mxf4p")
+    ctx.set_engine(kernel)
     try:
         ctx.load(family_words([BitMatrix(rows, n)], n), n)
         for g in (5, 7, 9):
@@ -372,5 +374,42 @@ def test_mxf4p_all_heavy(ctx, n):
         for g in (4, 6):
             mins, _ = ctx.round(g, -1, 1 << 30)
             assert mins == [0], (g, mins)
+    finally:
+        ctx.set_engine("auto")
+
+
+@pytest.mark.parametrize("kernel", ["mxf4p", "mxf4t", "mxf4q"])
+def test_packed_clipping(ctx, kernel):
+    """The K5t threshold test starts from the incoming bound: a bound at or
+    below the true minimum reports the bound, one above it the minimum."""
+    rng = random.Random(77)
+    n, k = 90, 30
+    rows = [rng.getrandbits(n) for _ in range(k)]
+    ctx.set_engine(kernel)
+    try:
+        ctx.load(family_words([BitMatrix(rows, n)], n), n)
+        want = oracle.min_weight(rows, n, 5)[0]
+        for upper in (want - 3, want, want + 1, want + 40, 1 << 20):
+            mins, combos = ctx.round(5, -1, upper)
+            assert mins == [min(want, upper)] and combos == [comb(k, 5)], (upper, mins, want)
+    finally:
+        ctx.set_engine("auto")
+
+
+@pytest.mark.parametrize("engine_name", ["auto", "mxf4", "popc"])
+def test_batched_rounds_chain_u(ctx, engine_name):
+    """bz_rounds: round g0 starts from `upper`, each later round from the U
+    its predecessor ended with -- exactly the per-round calls with the
+    running U (no early exit here: lower_prev = 0)."""
+    G, gs, _ = code("cfg2", 1)
+    ctx.set_engine(engine_name)
+    try:
+        ctx.load(family_words(gs.gammas, 96), 96)
+        res = ctx.rounds(1, [0] * 6, 10**6)
+        U = 10**6
+        for i, (mins, combos) in enumerate(res):
+            want_min, want_c = ctx.round(1 + i, 0, U)
+            assert (mins, combos) == (want_min, want_c), (1 + i, mins, want_min)
+            U = min([U] + mins)
     finally:
         ctx.set_engine("auto")

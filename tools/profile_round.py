@@ -38,7 +38,9 @@ def main():
     else:
         # --noexit: lower_prev = -1, so debug ablations that wreck the
         # minima never trigger the early exit
-        res = ctx.round(g, -(1 << 30) if "--noexit" in sys.argv else 0, 1 << 30)
+        upper = next((int(a.split("=", 1)[1]) for a in sys.argv[1:] if a.startswith("--upper=")),
+                     1 << 30)
+        res = ctx.round(g, -(1 << 30) if "--noexit" in sys.argv else 0, upper)
     dt = time.perf_counter() - t0
     print(f"{name} g={g}: {res} kernel {ctx.last_kernel_ms():.3f} ms wall {dt*1e3:.1f} ms")
 
