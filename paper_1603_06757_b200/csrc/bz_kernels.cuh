@@ -140,10 +140,33 @@ __device__ __forceinline__ void colex_next(Mask& x, int& i0, int& i1, int& i2) {
 }
 
 // Colex unrank of rank r among the q-subsets of [0, ell).
+// Shared-memory copy of C(c, i) for c < 128, i <= kSBinomQ (row-major,
+// kSBinomQ + 1 per row): walker unranks read it instead of the 133 KB global
+// table, whose L2 round trips made a chunk start cost microseconds.
+constexpr int kSBinomQ = 8;
+constexpr int kSBinomBytes = kMaxK * (kSBinomQ + 1) * 8;
+
 __device__ __forceinline__ Mask colex_unrank(unsigned long long r, int q, int ell,
-                                             const unsigned long long* __restrict__ binom) {
+                                             const unsigned long long* __restrict__ binom,
+                                             const unsigned long long* sb) {
   Mask x{0ull, 0ull};
   int c = ell - 1;
+  if (q <= kSBinomQ) {
+    // element i: the largest c' <= c with C(c', i) <= r (binary search;
+    // C(i - 1, i) = 0 bounds it below)
+    for (int i = q; i >= 1; --i) {
+      int lo = i - 1, hi = c;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (sb[mid * (kSBinomQ + 1) + i] <= r) lo = mid; else hi = mid - 1;
+      }
+      c = lo;
+      r -= sb[c * (kSBinomQ + 1) + i];
+      if (c < 64) x.lo |= 1ull << c; else x.hi |= 1ull << (c - 64);
+      --c;
+    }
+    return x;
+  }
   for (int i = q; i >= 1; --i) {
     while (__ldg(binom + c * kBinomDim + i) > r) --c;
     r -= __ldg(binom + c * kBinomDim + i);
@@ -215,7 +238,8 @@ struct Walker {
   uint32_t acc[W];
 
   __device__ __forceinline__ void init(unsigned long long rank, int q, int ell,
-                                       const uint32_t* R, const unsigned long long* binom) {
+                                       const uint32_t* R, const unsigned long long* binom,
+                                       const unsigned long long* sb) {
     constexpr int WP = padded_words(W);
 #pragma unroll
     for (int j = 0; j < W; ++j) acc[j] = 0u;
@@ -223,7 +247,7 @@ struct Walker {
     if (ell < 0) return;
     xor_row<W>(acc, R + ell * WP);
     if (q > 0) {
-      x = colex_unrank(rank, q, ell, binom);
+      x = colex_unrank(rank, q, ell, binom, sb);
       Mask y = x;
       while (y.lo | y.hi) {
         const int b = mask_ctz(y);
@@ -268,7 +292,16 @@ __host__ __device__ inline size_t smem_base_bytes(int m, int k, int ngroups) {
   size_t words = (size_t)m * k * WP + (size_t)m * (k + 1) * PS;
   size_t bytes = words * 4;
   bytes = (bytes + 15) & ~size_t(15);
-  return bytes + (size_t)ngroups * sizeof(Group);
+  bytes += (size_t)ngroups * sizeof(Group);
+  bytes = (bytes + 15) & ~size_t(15);
+  return bytes + kSBinomBytes;  // the small binomial table (colex_unrank)
+}
+
+// the small binomial table at the end of the staged region
+template <int W>
+__device__ __forceinline__ unsigned long long* smem_binom(unsigned char* smem, const RoundArgs& a) {
+  return reinterpret_cast<unsigned long long*>(smem + smem_base_bytes<W>(a.m, a.k, a.ngroups) -
+                                               kSBinomBytes);
 }
 
 template <int W>
@@ -293,6 +326,11 @@ __device__ __forceinline__ void stage(const RoundArgs& a, uint32_t*& srows,
   const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(a.groups);
   uint32_t* gdst = reinterpret_cast<uint32_t*>(sgroups);
   for (int i = threadIdx.x; i < gw; i += blockDim.x) gdst[i] = gsrc[i];
+  unsigned long long* sb = smem_binom<W>(smem, a);
+  for (int i = threadIdx.x; i < kMaxK * (kSBinomQ + 1); i += blockDim.x) {
+    const int c = i / (kSBinomQ + 1), j = i - c * (kSBinomQ + 1);
+    sb[i] = a.binom[c * kBinomDim + j];
+  }
   __syncthreads();
 }
 
@@ -376,6 +414,7 @@ k1_round_min(const RoundArgs a) {
   uint32_t *srows, *spx;
   Group* sgroups;
   stage<W>(a, srows, spx, sgroups, smem);
+  const unsigned long long* sbinom = smem_binom<W>(smem, a);
   if (a.chain && threadIdx.x == 0) {
     // batched round: start from the U the previous round ended with
     const int u = ((volatile const int*)a.chain)[0];
@@ -404,8 +443,8 @@ k1_round_min(const RoundArgs a) {
     const int e0 = v.gr.ell + 1;
 
     Walker<W> A, B;
-    if (v.cnt > 0) A.init(v.first, q, v.gr.ell, R, a.binom);
-    if (cb > 0) B.init(v.first + ca, q, v.gr.ell, R, a.binom);
+    if (v.cnt > 0) A.init(v.first, q, v.gr.ell, R, a.binom, sbinom);
+    if (cb > 0) B.init(v.first + ca, q, v.gr.ell, R, a.binom, sbinom);
 
     int best = INT_MAX;
     for (long long p = 0; p < maxca; ++p) {
@@ -458,6 +497,7 @@ k1h_histogram(const RoundArgs a) {
   for (int i = threadIdx.x; i < nbins; i += blockDim.x) bhist[i] = 0u;
   for (int i = threadIdx.x; i < nbins * (int)blockDim.x; i += blockDim.x) th[i] = 0;
   stage<W>(a, srows, spx, sgroups, smem);  // ends with __syncthreads
+  const unsigned long long* sbinom = smem_binom<W>(smem, a);
 
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -497,8 +537,8 @@ k1h_histogram(const RoundArgs a) {
     since_flush += chunk_work;
 
     Walker<W> A, B;
-    if (v.cnt > 0) A.init(v.first, q, v.gr.ell, R, a.binom);
-    if (cb > 0) B.init(v.first + ca, q, v.gr.ell, R, a.binom);
+    if (v.cnt > 0) A.init(v.first, q, v.gr.ell, R, a.binom, sbinom);
+    if (cb > 0) B.init(v.first + ca, q, v.gr.ell, R, a.binom, sbinom);
     for (long long p = 0; p < maxca; ++p) {
       if (p < ca) {
         const bool with_b = p < cb;

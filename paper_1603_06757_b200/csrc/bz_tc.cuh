@@ -124,6 +124,7 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   uint32_t *srows, *spx;
   Group* sgroups;
   stage<W>(a, srows, spx, sgroups, smem);  // ends with __syncthreads
+  const unsigned long long* sbinom = smem_binom<W>(smem, a);
   if (a.chain && threadIdx.x == 0) {
     // batched round: start from the U the previous round ended with
     const int u = ((volatile const int*)a.chain)[0];
@@ -180,7 +181,7 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
 
     // lanes without prefixes duplicate the block's first prefix
     Walker<W> wk;
-    wk.init(cnt > 0 ? first : bfirst, q, gr.ell, R, a.binom);
+    wk.init(cnt > 0 ? first : bfirst, q, gr.ell, R, a.binom, sbinom);
 
     auto load_tile = [&](int tile, int buf) {
       const uint8_t* src = tsrc + (size_t)tile * TILE_BYTES;

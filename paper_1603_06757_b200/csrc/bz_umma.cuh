@@ -793,6 +793,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
   Group* sgroups;
   tc_fence_before();
   stage<W>(a, srows, spx, sgroups, smem);  // ends with __syncthreads
+  const unsigned long long* sbinom = smem_binom<W>(smem, a);
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
   if (a.chain && tid == 0) {
@@ -1146,12 +1147,14 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
 #pragma unroll
         for (int j = 0; j < kUmmaMA; ++j) best = min(best, rmin[j] + (PR ? 0 : wt[j]));
       }
-      int wbest = __reduce_min_sync(FULL, best);
-      if (wbest < INT_MAX / 2) wbest += gamma_woff(a, c.gr.gamma);
+      const int wbest = __reduce_min_sync(FULL, best);
       if (lane == 0) {
-        volatile int* vb = a.bound;
-        if (wbest < vb[1 + c.gr.gamma]) atomicMin(a.bound + 1 + c.gr.gamma, wbest);
-        if (wbest < vb[0]) atomicMin(a.bound, wbest);
+        if (wbest < INT_MAX / 2) {
+          // fire-and-forget reductions (RED.MIN): no load round trip stalls
+          // the epilogue at a chunk boundary
+          atomicMin(a.bound + 1 + c.gr.gamma, wbest + gamma_woff(a, c.gr.gamma));
+          atomicMin(a.bound, wbest + gamma_woff(a, c.gr.gamma));
+        }
         long long* ct = k4_ctrace(a, qi);
         if (ct && warp == 0) { ct[2] = clock64(); ct[3] = global_ns(); }
       }
@@ -1179,7 +1182,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       const uint32_t* PX = spx + c.gr.gamma * (k + 1) * px_stride(W);
       Walker<W> wk;
       // rows without prefixes duplicate the block's first prefix
-      wk.init(cnt > 0 ? first : c.bfirst, a.g - 1 - c.gr.depth, c.gr.ell, R, a.binom);
+      wk.init(cnt > 0 ? first : c.bfirst, a.g - 1 - c.gr.depth, c.gr.ell, R, a.binom, sbinom);
       for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
         const int ab = grp % NA;
         mbar_wait_sel<4>(aempty(ab), ((grp / NA) & 1) ^ 1);

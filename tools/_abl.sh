@@ -1,4 +1,2 @@
 cd $GRAFT_REPO_ROOT
-for v in b2_e16 b3_e16 b2_e8 b3_e8 b3_e12; do for e in mxf4q; do
-  echo "$v $e"; BZ_LIB=build/var/libbz_$v.so python tools/profile_round.py cfg5 8 --engine=$e --upper=18;  BZ_LIB=build/var/libbz_$v.so python tools/profile_round.py cfg5 8 --engine=$e --upper=18
-done; done > gpurun_out/var.txt 2>&1
+for g in 4 5 6 7; do echo "g=$g"; BZ_K4_DEBUG=32 BZ_K4_CTRACE=gpurun_out/ct$g.bin python tools/profile_round.py cfg5 $g --upper=30; python tools/chunk_times.py gpurun_out/ct$g.bin; done > gpurun_out/ct.txt 2>&1
