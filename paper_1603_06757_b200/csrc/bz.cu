@@ -175,7 +175,17 @@ bool k5p_ok(int w32) { return w32 == 1 || w32 == 3; }
 
 // w32: stored words of the loaded family (0 = unknown, host-only plans):
 // AUTO takes K5q where it applies (odd W <= 3), else K5
-PlanShape pass_shape(int engine, int g, bool hist, int w32 = 0) {
+double binom_d(int p, int q);
+
+// AUTO keeps K1 (D = 1) for rounds this small: their tensor-core groups
+// hold few prefixes (g = 4: one per group), so a K5 launch is all fixed
+// latency (~40 us warm on B200; K1 runs cfg5's g = 4 in 32 us)
+constexpr double kAutoK1Combos = 1e7;
+
+PlanShape pass_shape(int engine, int g, bool hist, int w32 = 0, int m = 0, int k = 0) {
+  if (!hist && g >= 4 && engine == BZ_ENGINE_AUTO && m > 0 &&
+      binom_d(k, g) * m <= kAutoK1Combos)
+    return {1, 32, 0, 1};  // D = 1: many short prefixes keep every warp busy
   if (!hist && g >= 4) {
     if (engine == BZ_ENGINE_IMMA) return {3, bz::kTcThreads, bz::kTileRows, 3};
     if (engine == BZ_ENGINE_UMMA) return {3, bz::kUmmaM, bz::kUmmaN, 4};
@@ -326,6 +336,7 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
     lane_target = (long long)(total / ((unsigned long long)shape.lanes * 148ull * 16ull *
                                        (unsigned long long)std::max(1, nshards)));
     lane_target = std::min(1ll << 20, std::max(4096ll, lane_target));
+    if (const char* sc = getenv("BZ_K5_CHUNK_SCALE")) lane_target = (long long)(lane_target * atof(sc));
   }
   // suffix levels: K5 may split the round over depths 3..5, every other
   // kernel runs one depth with floor ell + 1
@@ -667,7 +678,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   }
   for (int i = 0; i < count; ++i) {
     const int g = g0 + i;
-    const PlanShape shape = pass_shape(ctx->engine, g, hist, ctx->w32);
+    const PlanShape shape = pass_shape(ctx->engine, g, hist, ctx->w32, ctx->m, ctx->k);
     if (shape.kernel == 3 || shape.kernel == 4) {
       rc = ensure_triples(ctx, shape.kernel);
       if (rc) return rc;

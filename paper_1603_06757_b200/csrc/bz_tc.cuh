@@ -125,8 +125,10 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
   Group* sgroups;
   stage<W>(a, srows, spx, sgroups, smem);  // ends with __syncthreads
   const unsigned long long* sbinom = smem_binom<W>(smem, a);
-  if (a.chain && threadIdx.x == 0) {
-    // batched round: start from the U the previous round ended with
+  if (a.chain && threadIdx.x == 0 && blockIdx.x == 0) {
+    // batched round: start from the U the previous round ended with (one
+    // thread of the grid: atomics on one address serialise; blocks that read
+    // the bound before it lands just see the looser start value)
     const int u = ((volatile const int*)a.chain)[0];
     for (int j = 0; j <= a.m; ++j) atomicMin(a.bound + j, u);
   }

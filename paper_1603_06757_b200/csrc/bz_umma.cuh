@@ -796,10 +796,11 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
   const unsigned long long* sbinom = smem_binom<W>(smem, a);
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
-  if (a.chain && tid == 0) {
+  if (a.chain && tid == 0 && blockIdx.x == 0) {
     // a batched round starts from the U its predecessor ended with (the
     // running U the reference clips with, m/engine.py:209-211); atomicMin
-    // keeps it race-free against blocks already lowering the bound
+    // keeps it race-free against blocks already lowering the bound; one
+    // thread of the grid (atomics on one address serialise)
     const int u = ((volatile const int*)a.chain)[0];
     for (int j = 0; j <= a.m; ++j) atomicMin(a.bound + j, u);
   }

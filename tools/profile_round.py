@@ -40,7 +40,11 @@ def main():
         # minima never trigger the early exit
         upper = next((int(a.split("=", 1)[1]) for a in sys.argv[1:] if a.startswith("--upper=")),
                      1 << 30)
-        res = ctx.round(g, -(1 << 30) if "--noexit" in sys.argv else 0, upper)
+        lp = -(1 << 30) if "--noexit" in sys.argv else 0
+        if "--cold" not in sys.argv:
+            ctx.round(g, lp, upper)  # warm-up: lazy module loading, tables
+            t0 = time.perf_counter()
+        res = ctx.round(g, lp, upper)
     dt = time.perf_counter() - t0
     print(f"{name} g={g}: {res} kernel {ctx.last_kernel_ms():.3f} ms wall {dt*1e3:.1f} ms")
 
