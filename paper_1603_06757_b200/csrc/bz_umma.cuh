@@ -661,7 +661,7 @@ __device__ __forceinline__ void k4_trace(const RoundArgs& a, int slot, uint32_t 
 // debug per-chunk timeline (BZ_K4_DEBUG & 32): per block, the first 64
 // chunks as {chunk, dequeued (clock64), done (clock64), done (globaltimer)}
 __device__ __forceinline__ long long* k4_ctrace(const RoundArgs& a, uint32_t qi) {
-  return (a.ctrace && qi < 64) ? a.ctrace + ((size_t)blockIdx.x * 64 + qi) * 4 : nullptr;
+  return (a.ctrace && qi < 63) ? a.ctrace + ((size_t)blockIdx.x * 64 + qi) * 4 : nullptr;
 }
 __device__ __forceinline__ long long global_ns() {
   long long t;
@@ -789,6 +789,10 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  // per-block lifetime (BZ_K4_DEBUG & 32): slot 63 = {entry, prologue done,
+  // exit} in globaltimer ns
+  long long* const life = a.ctrace ? a.ctrace + ((size_t)blockIdx.x * 64 + 63) * 4 : nullptr;
+  if (life && tid == 0) life[0] = global_ns();
   uint32_t *srows, *spx;
   Group* sgroups;
   tc_fence_before();
@@ -844,6 +848,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
   }
   const int k = a.k;
   const unsigned FULL = 0xffffffffu;
+  if (life && tid == 0) life[1] = global_ns();
 
   if (warp < E) {
     // ================= epilogue: warp e reads TMEM lanes 32(e%4).. (rows),
@@ -1360,21 +1365,50 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
     }
     __syncwarp();
   } else {
-    // ================= loader: TMA bulk copies of triple tiles
+    // ================= loader: TMA bulk copies of triple tiles, and the
+    // chunk queue.  Chunks are published up to kChunkQ ahead of the one
+    // being loaded (non-blocking between tiles), so the producers' walker
+    // unrank and first A rows of the next chunk overlap this chunk's tiles
+    // instead of waiting for its last TMA.
     if (lane == 0) {
       uint32_t bcount = 0, toff = k4_trace_off(a);
       volatile int* vb = a.bound;
-      for (uint32_t qi = 0;; ++qi) {
-        const int qs = qi % kChunkQ;
-        mbar_wait_sel<32>(qempty(qs), ((qi / kChunkQ) & 1) ^ 1);
-        // next chunk of this shard, or -1 (done, or U reached L_prev)
-        const unsigned long long cidx = atomicAdd(a.counter, 1ull);
-        const unsigned long long ch = cidx * (unsigned long long)a.nshards + a.shard;
-        const long long qchunk = (ch < a.nchunks && vb[0] > a.lower_prev) ? (long long)ch : -1;
-        s_q[qs] = qchunk;
-        long long* ct = k4_ctrace(a, qi);
-        if (ct) { ct[0] = qchunk; ct[1] = clock64(); }
-        mbar_arrive(qfull(qs));
+      uint32_t qpub = 0;   // chunk entries published
+      bool qdone = false;  // the -1 entry is out
+      // publish queue entries while slots are free (blocking for the first
+      // one when `block`); never more than kChunkQ ahead of entry `qload`
+      auto publish = [&](uint32_t qload, bool block) {
+        while (!qdone && qpub < qload + kChunkQ) {
+          const int qs = qpub % kChunkQ;
+          const uint32_t par = ((qpub / kChunkQ) & 1) ^ 1;
+          if (block) {
+            mbar_wait_sel<32>(qempty(qs), par);
+            block = false;
+          } else {
+            uint32_t ok;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(ok)
+                : "r"(qempty(qs)), "r"(par)
+                : "memory");
+            if (!ok) return;
+          }
+          // next chunk of this shard, or -1 (done, or U reached L_prev)
+          const unsigned long long cidx = atomicAdd(a.counter, 1ull);
+          const unsigned long long ch = cidx * (unsigned long long)a.nshards + a.shard;
+          const long long qchunk = (ch < a.nchunks && vb[0] > a.lower_prev) ? (long long)ch : -1;
+          s_q[qs] = qchunk;
+          long long* ct = k4_ctrace(a, qpub);
+          if (ct) { ct[0] = qchunk; ct[1] = clock64(); }
+          mbar_arrive(qfull(qs));
+          ++qpub;
+          if (qchunk < 0) qdone = true;
+        }
+      };
+      for (uint32_t qload = 0;; ++qload) {
+        publish(qload, qload == qpub);
+        const long long qchunk = s_q[qload % kChunkQ];
         if (qchunk < 0) break;
         const unsigned long long chunk = (unsigned long long)qchunk;
         const K4Chunk c = k4_decode<TR>(sgroups, a.ngroups, chunk, k);
@@ -1389,8 +1423,9 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
             k4_trace(a, 0, bcount, toff);
             // only the rows this tile needs (8-row granularity); the rest of
             // the stage keeps stale rows whose columns the epilogue masks
-            // (K5p: always the whole tile -- both halves of a column must
-            // hold in-range table rows, which the zeroed table tail provides)
+            // (K5p/K5q/K5t: always the whole tile -- every part of a column
+            // must hold in-range table rows, which the empty-subset tail
+            // provides)
             const int valid = min(TR, c.slice - t * TR);
             const uint32_t bytes = PR ? TB : (uint32_t)((valid + 7) / 8) * (CB * 128);
             if (a.debug & 2) {
@@ -1400,6 +1435,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
               tma_load_1d(sB_s + stg * TB, tsrc + (size_t)t * TB, bytes, bfull(stg));
               k4_trace(a, 15, bcount, toff);
             }
+            publish(qload + 1, false);
           }
         }
       }
@@ -1409,6 +1445,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
 
   tc_fence_before();
   __syncthreads();
+  if (life && tid == 0) life[2] = global_ns();
   if (warp == RL::MMA0) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),

@@ -9,6 +9,8 @@ import sys
 import numpy as np
 
 ct = np.fromfile(sys.argv[1], dtype=np.int64).reshape(1024, 64, 4)
+life = ct[:, 63, :3].copy()
+ct[:, 63, 0] = -1
 valid = ct[:, :, 0] >= 0
 nblk = int(valid.any(axis=1).sum())
 per = valid.sum(axis=1)[:nblk]
@@ -23,3 +25,12 @@ for b in range(nblk):
     span.append(ct[b, v, 2].max() - ct[b, v, 1].min())
 print(f"block span (dequeue first -> done last, clk): median {np.median(span):.0f} max {max(span)}")
 print(f"done spread across blocks (ns): {t_done.max() - t_done.min()}")
+
+lv = life[:nblk]
+if (lv > 0).all():
+    t0 = lv[:, 0].min()
+    first_done = np.array([ct[b, valid[b], 3].min() for b in range(nblk)]) - t0
+    print(f"block entry skew {lv[:, 0].max() - t0} ns; prologue median "
+          f"{np.median(lv[:, 1] - lv[:, 0]):.0f} ns; first chunk done median "
+          f"{np.median(first_done):.0f} ns; last chunk done {t_done.max() - t0} ns; "
+          f"block exit max {lv[:, 2].max() - t0} ns")
