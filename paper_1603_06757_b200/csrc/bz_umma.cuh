@@ -551,6 +551,13 @@ __global__ void k_build_subsets_mxf4(const uint32_t* __restrict__ rows,
                                      const unsigned long long* __restrict__ binom) {
   constexpr int WP = padded_words(W);
   constexpr int C = k4_row_bytes<true>(W) / 16;  // chunks per row (+ offset chunk)
+  // binomials C(x, 0..5) for x <= k in shared memory (every search below
+  // is a binary search over them)
+  __shared__ unsigned long long sbt[kBinomDim * 6];
+  for (int i = threadIdx.x; i < (k + 1) * 6; i += blockDim.x)
+    sbt[i] = binom[(i / 6) * kBinomDim + (i % 6)];
+  __syncthreads();
+  auto B = [&](int x, int q) { return sbt[x * 6 + q]; };
   const unsigned long long row = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= gamma_stride_rows) return;
   const int j = blockIdx.y;
@@ -566,22 +573,32 @@ __global__ void k_build_subsets_mxf4(const uint32_t* __restrict__ rows,
   }
   const uint32_t* R = rows + (size_t)j * k * WP;
   // smallest element a: rows of a start at C(k-1-a, D); x = k-1-a is the
-  // largest x with C(x, D) <= row
-  int x = D - 1;  // C(D-1, D) = 0: row 0 is the subset {k-D, ..., k-1}
-  while (x + 1 <= k - 1 && binom[(x + 1) * kBinomDim + D] <= row) ++x;
+  // largest x <= k-1 with C(x, D) <= row (C(D-1, D) = 0: row 0 is the subset
+  // {k-D, ..., k-1})
+  int lo = D - 1, hi = k - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (B(mid, D) <= row) lo = mid; else hi = mid - 1;
+  }
+  const int x = lo;
   const int a = k - 1 - x;
-  unsigned long long r = row - binom[x * kBinomDim + D];
+  unsigned long long r = row - B(x, D);
   uint32_t v[W];
 #pragma unroll
   for (int w = 0; w < W; ++w) v[w] = R[a * WP + w];
-  // lex unrank of r among the (D-1)-subsets of [a+1, k)
+  // lex unrank of r among the (D-1)-subsets of [a+1, k): element i's value
+  // e1 is the smallest e1 >= e with C(k-1-e1, i) < C(k-e, i) - r (the
+  // skipped blocks C(k-1-e', i-1), e <= e' < e1, sum to C(k-e, i) - C(k-e1, i))
   int e = a + 1;
   for (int i = D - 1; i >= 1; --i) {
-    for (;; ++e) {
-      const unsigned long long c = binom[(k - 1 - e) * kBinomDim + (i - 1)];
-      if (r < c) break;
-      r -= c;
+    const unsigned long long T = B(k - e, i) - r;
+    int l2 = e, h2 = k - i;  // C(k-1-(k-i), i) = C(i-1, i) = 0 < T
+    while (l2 < h2) {
+      const int mid = (l2 + h2) >> 1;
+      if (B(k - 1 - mid, i) < T) h2 = mid; else l2 = mid + 1;
     }
+    r = r - B(k - e, i) + B(k - l2, i);
+    e = l2;
 #pragma unroll
     for (int w = 0; w < W; ++w) v[w] ^= R[e * WP + w];
     ++e;
