@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define BZ_ABI_VERSION 7
+#define BZ_ABI_VERSION 8
 
 /* limits of the device kernels */
 #define BZ_MAX_K 128 /* rows per Gamma (prefix masks are 128-bit)      */
@@ -195,6 +195,10 @@ int bz_timer_stop(bz_ctx *ctx, float *ms);
 /* Device time (ms) of the enumeration kernel of the last bz_round /
  * bz_enumerate / bz_histogram call, from CUDA events around that launch. */
 int bz_last_kernel_ms(bz_ctx *ctx, float *ms);
+
+/* Per-round device time (ms) of the last bz_round / bz_rounds call: CUDA
+ * events between consecutive launches, count <= rounds of that call. */
+int bz_round_ms(bz_ctx *ctx, float *out_ms, int count);
 
 /* Number of kernels this context has launched so far. */
 int bz_launch_count(bz_ctx *ctx, uint64_t *out);

@@ -18,7 +18,7 @@ from .errors import (DeviceError, InvalidArity, InvalidDimensions, MindistError,
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BZ_LIB") or os.path.join(PKG_DIR, "libbz.so")
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 BZ_OK = 0
 _CODES = {
@@ -38,7 +38,7 @@ SYMBOLS = ("bz_abi_version", "bz_device_count", "bz_create", "bz_destroy",
            "bz_round", "bz_rounds",
            "bz_enumerate",
            "bz_histogram", "bz_plan", "bz_timer_start", "bz_timer_stop",
-           "bz_last_kernel_ms", "bz_launch_count", "bz_measure_int_peaks")
+           "bz_last_kernel_ms", "bz_round_ms", "bz_launch_count", "bz_measure_int_peaks")
 
 _lib = None
 
@@ -79,6 +79,7 @@ def lib():
     L.bz_timer_start.argtypes = [vp]
     L.bz_timer_stop.argtypes = [vp, ctypes.POINTER(c_float)]
     L.bz_last_kernel_ms.argtypes = [vp, ctypes.POINTER(c_float)]
+    L.bz_round_ms.argtypes = [vp, ctypes.POINTER(c_float), c_int]
     L.bz_launch_count.argtypes = [vp, u64p]
     L.bz_measure_int_peaks.argtypes = [vp, c_int, ctypes.POINTER(c_double)]
     if L.bz_abi_version() != ABI_VERSION:
@@ -235,6 +236,13 @@ class Context:
         m = self.m
         return [([int(v) for v in mins[i * m:(i + 1) * m]],
                  [int(v) for v in combos[i * m:(i + 1) * m]]) for i in range(count)]
+
+    def round_ms(self, count: int) -> list[float]:
+        """Per-round device ms of the last round / rounds call."""
+        out = np.zeros(max(count, 1), dtype=np.float32)
+        check(lib().bz_round_ms(self.handle, _ptr(out, ctypes.c_float), count), self.handle,
+              "bz_round_ms")
+        return [float(v) for v in out[:count]]
 
     def enumerate(self, gamma: int, g: int, shard: int = 0, nshards: int = 1):
         mn = np.zeros(1, dtype=np.int32)

@@ -38,6 +38,8 @@ struct bz_ctx {
   std::string err;
   uint64_t launches = 0;
   float last_kernel_ms = 0.f;
+  std::vector<cudaEvent_t> ev_round;  // one per launch boundary of the last batch
+  std::vector<float> round_ms;        // per-round device ms of the last batch
 
   // loaded family
   int m = 0, k = 0, n = 0, w32 = 0, wp = 0;
@@ -737,12 +739,19 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     CK(cudaMemsetAsync(ctx->d_hist, 0, sizeof(unsigned long long) * (ctx->n + 1), ctx->stream));
   CK(cudaMemcpyAsync(ctx->d_io, ctx->h_io, l.size * (size_t)count, cudaMemcpyHostToDevice,
                      ctx->stream));
+  while ((int)ctx->ev_round.size() < count + 1) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    ctx->ev_round.push_back(e);
+  }
   CK(cudaEventRecord(ctx->ev_k0, ctx->stream));
   for (int i = 0; i < count; ++i) {
+    if (count > 1) CK(cudaEventRecord(ctx->ev_round[i], ctx->stream));
     if (!todo[i].run) continue;
     rc = launch(ctx, todo[i].a, hist, todo[i].shape);
     if (rc) return rc;
   }
+  if (count > 1) CK(cudaEventRecord(ctx->ev_round[count], ctx->stream));
   CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
   CK(cudaMemcpyAsync(ctx->h_io, ctx->d_io, l.size * (size_t)(count - 1) + l.off_groups,
                      cudaMemcpyDeviceToHost, ctx->stream));
@@ -751,6 +760,13 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
                        cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaEventElapsedTime(&ctx->last_kernel_ms, ctx->ev_k0, ctx->ev_k1));
+  ctx->round_ms.assign(count, 0.f);
+  if (count == 1) {
+    ctx->round_ms[0] = ctx->last_kernel_ms;
+  } else {
+    for (int i = 0; i < count; ++i)
+      CK(cudaEventElapsedTime(&ctx->round_ms[i], ctx->ev_round[i], ctx->ev_round[i + 1]));
+  }
   if (ctrace) {
     // BZ_K4_DEBUG & 32: per-chunk timeline to $BZ_K4_CTRACE (raw int64)
     std::vector<long long> h(1024 * 64 * 4);
@@ -873,6 +889,7 @@ void bz_destroy(bz_ctx* ctx) {
     if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
     if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
     if (ctx->ev_k0) cudaEventDestroy(ctx->ev_k0);
+    for (cudaEvent_t e : ctx->ev_round) cudaEventDestroy(e);
     if (ctx->ev_k1) cudaEventDestroy(ctx->ev_k1);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
   }
@@ -1196,6 +1213,15 @@ int bz_timer_stop(bz_ctx* ctx, float* ms) {
   CK(cudaEventRecord(ctx->ev_b, ctx->stream));
   CK(cudaEventSynchronize(ctx->ev_b));
   CK(cudaEventElapsedTime(ms, ctx->ev_a, ctx->ev_b));
+  return BZ_OK;
+}
+
+int bz_round_ms(bz_ctx* ctx, float* out_ms, int count) {
+  if (!ctx || !out_ms || count < 0) return BZ_ERR_ARGUMENT;
+  if (count > (int)ctx->round_ms.size())
+    return fail(ctx, BZ_ERR_ARGUMENT, "%d rounds requested, last call ran %zu", count,
+                ctx->round_ms.size());
+  for (int i = 0; i < count; ++i) out_ms[i] = ctx->round_ms[i];
   return BZ_OK;
 }
 

@@ -86,11 +86,16 @@ class EngineConfig:
     device: int | None = None
     distributed: bool = False
     early_exit: bool = True  # stop a round once U reaches the previous L
-    # consecutive rounds with at most this many combinations in total run as
-    # one batch (one launch sequence, one synchronisation; replicated, not
-    # sharded, across ranks); 0 disables batching
+    # consecutive rounds with at most this many combinations in total (per
+    # rank) run as one batch (one launch sequence, one synchronisation, one
+    # exchange); 0 disables batching
     batch_combinations: int = 2_000_000_000
-    engine: str = "auto"     # "auto" | "mxf4" | "umma" | "imma" | "popc" (kernel; same results)
+    # on a single device the batch may run far ahead: each batched round
+    # starts on the device from the U its predecessor ended with and exits
+    # at once if that U already meets its L (the run had terminated), so a
+    # speculative round costs a launch, not its enumeration
+    batch_combinations_single: int = 100_000_000_000
+    engine: str = "auto"     # "auto" | "mxf4q" | "mxf4" | ... | "popc" (kernel; same results)
     elide_identity: bool = True  # drop each full-rank Gamma's identity columns (+g; exact)
 
 
@@ -175,7 +180,7 @@ class GpuRounds:
         round, then one exchange for all of them: [(mins, combos)] per round
         and the batch's kernel ms."""
         res = self.ctx.rounds(g0, lower_prevs, upper, self.comm.rank, self.comm.world)
-        ms = self.ctx.last_kernel_ms()
+        ms = self.ctx.round_ms(len(lower_prevs))
         return combine_rounds(self.comm, res), ms
 
 
@@ -236,7 +241,8 @@ def run_rounds(backend, gs: GammaSet, k: int, config: EngineConfig, st: LoopStat
             # the next rounds whose total size fits the batch budget (per
             # rank: a batch is sharded like a round)
             world = getattr(getattr(backend, "comm", None), "world", 1)
-            budget = config.batch_combinations * world
+            budget = (config.batch_combinations * world if world > 1
+                      else max(config.batch_combinations, config.batch_combinations_single))
             count, total = 0, 0
             while (st.g + count <= min(k, config.max_g)
                    and total + m * comb(k, st.g + count) <= budget):
@@ -249,8 +255,11 @@ def run_rounds(backend, gs: GammaSet, k: int, config: EngineConfig, st: LoopStat
                                if config.early_exit else 0)
                 res, batch_ms = backend.run_batch(st.g, lps, st.U)
                 for i, (mn, cb) in enumerate(res):
-                    share = (m * comb(k, st.g + i)) / total if total else 0.0
-                    queued.append((st.g + i, mn, cb, batch_ms * share))
+                    if isinstance(batch_ms, list):  # per-round device times
+                        ms = batch_ms[i]
+                    else:  # one time for the batch: split by combinations
+                        ms = batch_ms * ((m * comb(k, st.g + i)) / total if total else 0.0)
+                    queued.append((st.g + i, mn, cb, ms))
         if queued and queued[0][0] == st.g:
             _, mins, combos, kernel_ms = queued.pop(0)
         else:

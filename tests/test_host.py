@@ -171,11 +171,19 @@ class OracleBatchRounds(OracleRounds):
     batches: list = []
 
     def run_batch(self, g0, lower_prevs, upper):
+        """Mirrors bz_rounds: round i > 0 starts from the U round i-1 ended
+        with and exits at once when that U already meets its lower_prev
+        (a round past termination)."""
         OracleBatchRounds.batches.append((g0, len(lower_prevs)))
         out = []
+        U = upper
         for i in range(len(lower_prevs)):
+            if i > 0 and U <= lower_prevs[i]:
+                out.append(([U] * len(self.gammas), [0] * len(self.gammas)))
+                continue
             res = [oracle.min_weight(rows, self.n, g0 + i, threads=2) for rows in self.gammas]
-            out.append(([min(mn, upper) for mn, _ in res], [c for _, c in res]))
+            out.append(([min(mn, U) for mn, _ in res], [c for _, c in res]))
+            U = min([U] + out[-1][0])
         return out, 0.0
 
 
