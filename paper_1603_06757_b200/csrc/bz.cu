@@ -17,6 +17,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -430,6 +431,32 @@ int check_g(bz_ctx* ctx, int g) {
   return BZ_OK;
 }
 
+// Host-side launch preparation, memoised: the dynamic shared memory limit
+// is raised once per kernel and the occupancy query runs once per (device,
+// kernel, block size, shared memory).  Uncached they cost more host time per
+// launch than a small round's kernel runs, which left the stream idle
+// between the batched early rounds.
+int prep_launch(bz_ctx* ctx, const void* fn, int threads, size_t smem, int* per_sm) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*>, size_t> attr;
+  static std::map<std::tuple<int, const void*, int, size_t>, int> occ;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = attr[{ctx->device, fn}];
+  if (smem > have) {
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    have = smem;
+  }
+  const auto key = std::make_tuple(ctx->device, fn, threads, smem);
+  auto it = occ.find(key);
+  if (it == occ.end()) {
+    int n = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem));
+    it = occ.emplace(key, n).first;
+  }
+  *per_sm = it->second;
+  return BZ_OK;
+}
+
 template <int W, int D>
 int launch_wd(bz_ctx* ctx, const RoundArgs& a, bool hist) {
   size_t smem = bz::smem_base_bytes<W>(a.m, a.k, a.ngroups);
@@ -442,17 +469,11 @@ int launch_wd(bz_ctx* ctx, const RoundArgs& a, bool hist) {
     while (threads > 32 && smem + (size_t)(a.n + 1) * threads * 2 > (size_t)dev_max / 2)
       threads /= 2;
     smem += (size_t)(a.n + 1) * threads * 2;
-    CK(cudaFuncSetAttribute(bz::k1h_histogram<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
-  } else {
-    CK(cudaFuncSetAttribute(bz::k1_round_min<W, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
   }
   int per_sm = 0;
-  if (hist)
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bz::k1h_histogram<W, D>, threads, smem));
-  else
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bz::k1_round_min<W, D>, threads, smem));
+  const void* fn = hist ? (const void*)bz::k1h_histogram<W, D> : (const void*)bz::k1_round_min<W, D>;
+  int rc = prep_launch(ctx, fn, threads, smem, &per_sm);
+  if (rc) return rc;
   if (per_sm < 1) return fail(ctx, BZ_ERR_TOO_LARGE, "kernel does not fit on an SM (smem %zu)", smem);
   // persistent grid: one wave, but no more warps than chunks need
   unsigned long long warps_needed = (a.nchunks + a.nshards - 1) / a.nshards;
@@ -472,10 +493,9 @@ template <int W>
 int launch_tc(bz_ctx* ctx, const RoundArgs& a) {
   const size_t smem = bz::k3_smem_bytes<W>(a.m, a.k, a.ngroups);
   const int threads = bz::kTcThreads;
-  CK(cudaFuncSetAttribute(bz::k3_round_gemm<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem));
   int per_sm = 0;
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bz::k3_round_gemm<W>, threads, smem));
+  int rc = prep_launch(ctx, (const void*)bz::k3_round_gemm<W>, threads, smem, &per_sm);
+  if (rc) return rc;
   if (per_sm < 1) return fail(ctx, BZ_ERR_TOO_LARGE, "K3 does not fit on an SM (smem %zu)", smem);
   const unsigned long long blocks_needed = (a.nchunks + a.nshards - 1) / a.nshards;
   long long blocks = (long long)per_sm * ctx->sm_count;
@@ -492,8 +512,16 @@ int launch_umma(bz_ctx* ctx, const RoundArgs& a) {
   const size_t smem = bz::k4_smem_bytes<W, F4, CW>(a.m, a.k, a.ngroups);
   if (smem > 232448)
     return fail(ctx, BZ_ERR_TOO_LARGE, "K%d does not fit on an SM (smem %zu)", F4 ? 5 : 4, smem);
-  CK(cudaFuncSetAttribute(bz::k4_round_umma<W, F4, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem));
+  {
+    static std::mutex mu;
+    static std::map<int, size_t> have;  // per device: the attribute is per function
+    std::lock_guard<std::mutex> lock(mu);
+    if (smem > have[ctx->device]) {
+      CK(cudaFuncSetAttribute(bz::k4_round_umma<W, F4, CW>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      have[ctx->device] = smem;
+    }
+  }
   const unsigned long long mine = (a.nchunks + a.nshards - 1 - a.shard) / a.nshards;
   long long blocks = std::max(1ll, std::min((long long)ctx->sm_count, (long long)mine));
   bz::K4Tables tabs{};

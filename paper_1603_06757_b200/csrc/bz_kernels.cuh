@@ -317,7 +317,12 @@ __device__ __forceinline__ void stage(const RoundArgs& a, uint32_t*& srows,
   spx = srows + nrow_words;
   size_t off = ((size_t)(nrow_words + npx_words) * 4 + 15) & ~size_t(15);
   sgroups = reinterpret_cast<Group*>(smem + off);
+  // the loops are unrolled so several global loads are in flight per
+  // thread: a load-store-load chain would pay one L2 round trip per word
+  // and made the prologue of a short launch cost microseconds
+#pragma unroll 8
   for (int i = threadIdx.x; i < nrow_words; i += blockDim.x) srows[i] = a.rows[i];
+#pragma unroll 8
   for (int i = threadIdx.x; i < npx_words; i += blockDim.x) {
     const int r = i / PS, j = i - r * PS;
     spx[i] = j < W ? a.px[r * WP + j] : 0u;
@@ -325,8 +330,10 @@ __device__ __forceinline__ void stage(const RoundArgs& a, uint32_t*& srows,
   const int gw = a.ngroups * (int)(sizeof(Group) / 4);
   const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(a.groups);
   uint32_t* gdst = reinterpret_cast<uint32_t*>(sgroups);
+#pragma unroll 8
   for (int i = threadIdx.x; i < gw; i += blockDim.x) gdst[i] = gsrc[i];
   unsigned long long* sb = smem_binom<W>(smem, a);
+#pragma unroll 8
   for (int i = threadIdx.x; i < kMaxK * (kSBinomQ + 1); i += blockDim.x) {
     const int c = i / (kSBinomQ + 1), j = i - c * (kSBinomQ + 1);
     sb[i] = a.binom[c * kBinomDim + j];
