@@ -949,34 +949,44 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
         return fail(ctx, BZ_ERR_INVALID_DIMENSIONS,
                     "Gamma %d row %d has bits outside columns 0..%d", j, r, n - 1);
     }
-  auto bit = [&](int j, int r, int c) -> int {
-    return (int)((rows[((size_t)j * k + r) * w64 + (c >> 6)] >> (c & 63)) & 1ull);
-  };
+  auto row_of = [&](int j, int r) { return rows + ((size_t)j * k + r) * w64; };
   // Identity-column elision: a Gamma with one unit column per row (every
   // full-rank information set, m/gf2.py:133-199) has exactly one 1 of those
   // columns in each chosen row, so the weight of any g-combination is
   // g + the weight of its other n - k columns.  Those columns are dropped
-  // here and the kernels add g back (RoundArgs::elide).
-  std::vector<std::vector<int>> keep_cols(m);
+  // here and the kernels add g back (RoundArgs::elide).  Word-level: set
+  // bits are visited with ctz, kept columns gathered by rank.
+  std::vector<std::vector<uint64_t>> keep(m, std::vector<uint64_t>(w64, 0ull));
   unsigned long long elide = 0;
   int n_eff = 1;
   for (int j = 0; j < m; ++j) {
-    std::vector<char> drop(n, 0);
+    std::vector<uint64_t>& km = keep[j];
+    for (int w = 0; w < w64; ++w) {
+      const int bits = std::min(64, n - 64 * w);
+      km[w] = bits >= 64 ? ~0ull : ((1ull << bits) - 1ull);
+    }
     bool ok = ctx->elision && m <= 64 && k < n;
-    // column weights, then each row's first column of weight 1
     std::vector<int> ones(n, 0);
     for (int r = 0; ok && r < k; ++r)
-      for (int c = 0; c < n; ++c) ones[c] += bit(j, r, c);
+      for (int w = 0; w < w64; ++w)
+        for (uint64_t x = row_of(j, r)[w]; x; x &= x - 1) ++ones[64 * w + __builtin_ctzll(x)];
+    std::vector<uint64_t> drop(w64, 0ull);
     for (int r = 0; ok && r < k; ++r) {
       int unit = -1;
-      for (int c = 0; c < n && unit < 0; ++c)
-        if (ones[c] == 1 && bit(j, r, c)) unit = c;
-      if (unit < 0) ok = false; else drop[unit] = 1;
+      for (int w = 0; w < w64 && unit < 0; ++w)
+        for (uint64_t x = row_of(j, r)[w]; x && unit < 0; x &= x - 1) {
+          const int c = 64 * w + __builtin_ctzll(x);
+          if (ones[c] == 1) unit = c;
+        }
+      if (unit < 0) ok = false; else drop[unit >> 6] |= 1ull << (unit & 63);
     }
-    for (int c = 0; c < n; ++c)
-      if (!(ok && drop[c])) keep_cols[j].push_back(c);
-    if (ok) elide |= 1ull << j;
-    n_eff = std::max(n_eff, (int)keep_cols[j].size());
+    if (ok) {
+      for (int w = 0; w < w64; ++w) km[w] &= ~drop[w];
+      elide |= 1ull << j;
+    }
+    int cnt = 0;
+    for (int w = 0; w < w64; ++w) cnt += __builtin_popcountll(km[w]);
+    n_eff = std::max(n_eff, cnt);
   }
   const int w32 = (n_eff + 31) / 32;
   const int wp = bz::padded_words(w32);
@@ -984,10 +994,19 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
   std::vector<uint32_t> img((size_t)m * k * wp, 0u);
   std::vector<uint32_t> px((size_t)m * (k + 1) * wp, 0u);
   for (int j = 0; j < m; ++j) {
+    // kept columns below word w: the gathered index base of word w
+    std::vector<int> base(w64 + 1, 0);
+    for (int w = 0; w < w64; ++w) base[w + 1] = base[w] + __builtin_popcountll(keep[j][w]);
     for (int r = 0; r < k; ++r) {
       uint32_t* dst = img.data() + ((size_t)j * k + r) * wp;
-      for (size_t i = 0; i < keep_cols[j].size(); ++i)
-        if (bit(j, r, keep_cols[j][i])) dst[i >> 5] |= 1u << (i & 31);
+      for (int w = 0; w < w64; ++w) {
+        const uint64_t km = keep[j][w];
+        for (uint64_t x = row_of(j, r)[w] & km; x; x &= x - 1) {
+          const int b = __builtin_ctzll(x);
+          const int i = base[w] + __builtin_popcountll(km & ((1ull << b) - 1ull));
+          dst[i >> 5] |= 1u << (i & 31);
+        }
+      }
     }
     for (int r = 0; r < k; ++r)
       for (int w = 0; w < wp; ++w)

@@ -36,7 +36,7 @@ class EnumerationResult:
 def family_words(gammas, n: int) -> np.ndarray:
     """(m, k, ceil(n/64)) uint64 image of a family (BitMatrix.to_numpy at
     word width 64, gf2.py:74-79) -- the layout bz_load_gammas expects."""
-    mats = [gm.with_word_width(64).to_numpy() for gm in gammas]
+    mats = [gm.words64() for gm in gammas]
     return np.ascontiguousarray(np.stack(mats, axis=0), dtype=np.uint64)
 
 
