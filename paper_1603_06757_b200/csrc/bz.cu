@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -410,15 +411,38 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
 }
 
 // Build the round's group table into I/O slot `slot` (host side).
+// A plan depends only on (m, k, g, Gamma filter, kernel shape, shard count)
+// and the planning knobs, never on the matrices, so plans are memoised per
+// process: a repeated run (same dimensions) copies its group tables instead
+// of re-planning every round before the first launch.
 int plan_round(bz_ctx* ctx, int g, int gamma_only, PlanShape shape, int nshards, int slot,
                int* out_ngroups, unsigned long long* out_nchunks) {
-  std::vector<Group> gs;
-  int rc = build_plan(ctx, ctx->m, ctx->k, g, gamma_only, shape, nshards, gs, out_nchunks);
-  if (rc) return rc;
+  struct Plan {
+    std::vector<Group> groups;
+    unsigned long long nchunks;
+  };
+  static std::mutex mu;
+  static std::map<std::string, Plan> memo;
+  const char* floors = getenv("BZ_K5_FLOORS");
+  const char* scale = getenv("BZ_K5_CHUNK_SCALE");
+  char key[256];
+  snprintf(key, sizeof key, "%d/%d/%d/%d/%d/%d/%d/%d/%d/%s/%s", ctx->m, ctx->k, g, gamma_only,
+           shape.kernel, shape.depth, shape.lanes, shape.tile_rows, nshards, floors ? floors : "",
+           scale ? scale : "");
   const IoSlot l = io_layout(ctx->m, ctx->k);
-  std::memcpy(slot_ptr<Group>(ctx->h_io, l, slot, l.off_groups), gs.data(),
-              gs.size() * sizeof(Group));
-  *out_ngroups = (int)gs.size();
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = memo.find(key);
+  if (it == memo.end()) {
+    Plan p;
+    int rc = build_plan(ctx, ctx->m, ctx->k, g, gamma_only, shape, nshards, p.groups, &p.nchunks);
+    if (rc) return rc;
+    if (memo.size() > 4096) memo.clear();
+    it = memo.emplace(key, std::move(p)).first;
+  }
+  std::memcpy(slot_ptr<Group>(ctx->h_io, l, slot, l.off_groups), it->second.groups.data(),
+              it->second.groups.size() * sizeof(Group));
+  *out_ngroups = (int)it->second.groups.size();
+  *out_nchunks = it->second.nchunks;
   return BZ_OK;
 }
 
@@ -706,6 +730,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
       ctrace = d_ct;
     }
   }
+  const auto t_plan0 = std::chrono::steady_clock::now();
   for (int i = 0; i < count; ++i) {
     const int g = g0 + i;
     const PlanShape shape = pass_shape(ctx->engine, g, hist, ctx->w32, ctx->m, ctx->k);
@@ -763,6 +788,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     todo[i].shape = shape;
     todo[i].run = nchunks > 0 && (unsigned long long)shard < nchunks;
   }
+  const auto t_plan1 = std::chrono::steady_clock::now();
   if (hist)
     CK(cudaMemsetAsync(ctx->d_hist, 0, sizeof(unsigned long long) * (ctx->n + 1), ctx->stream));
   CK(cudaMemcpyAsync(ctx->d_io, ctx->h_io, l.size * (size_t)count, cudaMemcpyHostToDevice,
@@ -781,12 +807,19 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   }
   if (count > 1) CK(cudaEventRecord(ctx->ev_round[count], ctx->stream));
   CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
+  const auto t_launch1 = std::chrono::steady_clock::now();
   CK(cudaMemcpyAsync(ctx->h_io, ctx->d_io, l.size * (size_t)(count - 1) + l.off_groups,
                      cudaMemcpyDeviceToHost, ctx->stream));
   if (hist)
     CK(cudaMemcpyAsync(ctx->h_hist, ctx->d_hist, sizeof(unsigned long long) * (ctx->n + 1),
                        cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
+  if (getenv("BZ_HOST_TIMING")) {
+    auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    fprintf(stderr, "run_batch g0=%d count=%d: plan %.1f us, launches %.1f us, wait %.1f us\n", g0,
+            count, us(t_plan0, t_plan1), us(t_plan1, t_launch1),
+            us(t_launch1, std::chrono::steady_clock::now()));
+  }
   CK(cudaEventElapsedTime(&ctx->last_kernel_ms, ctx->ev_k0, ctx->ev_k1));
   ctx->round_ms.assign(count, 0.f);
   if (count == 1) {
