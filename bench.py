@@ -65,7 +65,13 @@ def dist_env():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled during the timed region.
+
+    nvidia-smi polls every 10 ms; a reader thread stamps each line with the
+    host clock, entering waits for the first line (so the poller is running
+    when the timed region starts) and the summary keeps the lines stamped
+    inside the region (or the last one before it when the region is shorter
+    than a poll period)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -74,32 +80,50 @@ class ClockSampler:
     def __init__(self, gpu_index: int):
         self.gpu = gpu_index
         self.proc = None
+        self.stamped = []
+        self.t0 = self.t1 = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            if ln.strip():
+                self.stamped.append((time.perf_counter(), ln))
 
     def __enter__(self):
+        import threading
+
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "10"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.reader = threading.Thread(target=self._read, daemon=True)
+            self.reader.start()
+            deadline = time.perf_counter() + 5.0
+            while not self.stamped and time.perf_counter() < deadline:
+                time.sleep(0.002)
         except OSError:
             self.proc = None
+        self.t0 = time.perf_counter()
         return self
 
     def __exit__(self, *exc):
-        self.lines = []
+        self.t1 = time.perf_counter()
         if self.proc is not None:
+            time.sleep(0.02)  # the poll that covers the region's last milliseconds
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
+                self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
-                out, _ = self.proc.communicate()
-            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            self.reader.join(timeout=5)
 
     def summary(self):
+        inside = [ln for t, ln in self.stamped if self.t0 <= t <= self.t1 + 0.02]
+        before = [ln for t, ln in self.stamped if t < self.t0]
+        lines = inside or before[-1:]
         sm, mx, reasons = [], None, set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in getattr(self, "lines", []):
+        for ln in lines:
             p = [x.strip() for x in ln.split(",")]
             if len(p) < 9:
                 continue
@@ -112,7 +136,9 @@ class ClockSampler:
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "samples_in_region": len(inside),
+                "region_ms": None if self.t1 is None else round((self.t1 - self.t0) * 1e3, 2)}
 
 
 def cpu_baseline(G, gs, sample_g: int) -> dict:
@@ -269,11 +295,15 @@ def main():
     w_eff = (max(n_eff, 1) + 31) // 32
     wp = 1 if w_eff <= 1 else 2 if w_eff <= 2 else 4 if w_eff <= 4 else 8
     h2d = m * k * wp * 4 + m * (k + 1) * wp * 4  # padded rows + prefix-XOR table
+    # per round: a result record {cursor, combos[m], bounds[m+1]} both ways
+    # and the round's plan (56-byte groups, 256-byte aligned) host -> device
+    # (bz.cu io_layout / run_batch)
+    record = (8 + 8 * m + 4 * (m + 1) + 15) // 16 * 16
     d2h = 0
     for (g, L, U) in rep.bounds_trace:
         groups, _ = _native.plan(m, k, g)
-        h2d += len(groups) * 32 + (m + 1) * 4  # work plan + bound init
-        d2h += (m + 1) * 4 + m * 8             # minima + counters
+        h2d += record + (len(groups) * 56 + 255) // 256 * 256
+        d2h += record
 
     if rank != 0:
         if distributed:

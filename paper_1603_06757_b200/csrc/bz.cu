@@ -133,19 +133,23 @@ struct IoSlot {
   size_t off_combos, off_bound, off_groups, size;
 };
 
+// I/O image of a batch of rounds: first every round's result record
+// {cursor, combos[m], bound[m+1]} (off_groups bytes each, contiguous: the
+// only part read back), then each round's plan at a variable offset
+// (ctx->gbase[i]; only the used groups travel host -> device).
 IoSlot io_layout(int m, int k) {
   IoSlot l;
   l.off_combos = 8;
   l.off_bound = l.off_combos + 8 * (size_t)m;
-  l.off_groups = (l.off_bound + 4 * (size_t)(m + 1) + 15) & ~size_t(15);
+  l.off_groups = (l.off_bound + 4 * (size_t)(m + 1) + 15) & ~size_t(15);  // record size
   const size_t max_groups = (size_t)m * (size_t)(3 * k + 6) + 1;  // K5: up to 3 levels
-  l.size = (l.off_groups + sizeof(Group) * max_groups + 255) & ~size_t(255);
+  l.size = (l.off_groups + sizeof(Group) * max_groups + 255) & ~size_t(255);  // worst case
   return l;
 }
 
 int ensure_io(bz_ctx* ctx, int nslots) {
   const IoSlot l = io_layout(ctx->m, ctx->k);
-  const size_t total = l.size * (size_t)std::max(nslots, 1);
+  const size_t total = l.size * (size_t)std::max(nslots, 1) + 256;
   if (total > ctx->io_cap) {
     if (ctx->d_io) cudaFree(ctx->d_io);
     if (ctx->h_io) cudaFreeHost(ctx->h_io);
@@ -160,9 +164,10 @@ int ensure_io(bz_ctx* ctx, int nslots) {
 }
 
 // host / device views of slot i
+// result record of round i (off < l.off_groups)
 template <typename T>
 T* slot_ptr(unsigned char* base, const IoSlot& l, int i, size_t off) {
-  return reinterpret_cast<T*>(base + l.size * (size_t)i + off);
+  return reinterpret_cast<T*>(base + l.off_groups * (size_t)i + off);
 }
 
 // Work plan of one round (host only): one Group per (Gamma, ell) with its
@@ -415,7 +420,7 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
 // and the planning knobs, never on the matrices, so plans are memoised per
 // process: a repeated run (same dimensions) copies its group tables instead
 // of re-planning every round before the first launch.
-int plan_round(bz_ctx* ctx, int g, int gamma_only, PlanShape shape, int nshards, int slot,
+int plan_round(bz_ctx* ctx, int g, int gamma_only, PlanShape shape, int nshards, size_t goff,
                int* out_ngroups, unsigned long long* out_nchunks) {
   struct Plan {
     std::vector<Group> groups;
@@ -439,8 +444,8 @@ int plan_round(bz_ctx* ctx, int g, int gamma_only, PlanShape shape, int nshards,
     if (memo.size() > 4096) memo.clear();
     it = memo.emplace(key, std::move(p)).first;
   }
-  std::memcpy(slot_ptr<Group>(ctx->h_io, l, slot, l.off_groups), it->second.groups.data(),
-              it->second.groups.size() * sizeof(Group));
+  (void)l;
+  std::memcpy(ctx->h_io + goff, it->second.groups.data(), it->second.groups.size() * sizeof(Group));
   *out_ngroups = (int)it->second.groups.size();
   *out_nchunks = it->second.nchunks;
   return BZ_OK;
@@ -731,6 +736,8 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     }
   }
   const auto t_plan0 = std::chrono::steady_clock::now();
+  // plans follow the result records; goff = where round i's groups go
+  size_t goff = ((size_t)count * l.off_groups + 255) & ~size_t(255);
   for (int i = 0; i < count; ++i) {
     const int g = g0 + i;
     const PlanShape shape = pass_shape(ctx->engine, g, hist, ctx->w32, ctx->m, ctx->k);
@@ -740,12 +747,13 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     }
     int ngroups = 0;
     unsigned long long nchunks = 0;
-    rc = plan_round(ctx, g, gamma_only, shape, nshards, i, &ngroups, &nchunks);
+    const size_t gthis = goff;
+    rc = plan_round(ctx, g, gamma_only, shape, nshards, gthis, &ngroups, &nchunks);
     if (rc) return rc;
     if (shape.kernel >= 5) {
       // the suffix tables this round's levels read
       int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX};
-      const Group* gp = slot_ptr<Group>(ctx->h_io, l, i, l.off_groups);
+      const Group* gp = reinterpret_cast<const Group*>(ctx->h_io + gthis);
       for (int q = 0; q < ngroups; ++q)
         lo[gp[q].depth - 3] = std::min(lo[gp[q].depth - 3], gp[q].sfloor);
       for (int D = 3; D <= 5; ++D)
@@ -763,7 +771,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     a = RoundArgs{};
     a.rows = ctx->d_rows;
     a.px = ctx->d_px;
-    a.groups = slot_ptr<Group>(ctx->d_io, l, i, l.off_groups);
+    a.groups = reinterpret_cast<const Group*>(ctx->d_io + gthis);
     a.binom = ctx->d_binom;
     a.bound = slot_ptr<int>(ctx->d_io, l, i, l.off_bound);
     a.combos = slot_ptr<unsigned long long>(ctx->d_io, l, i, l.off_combos);
@@ -787,11 +795,13 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     a.chain = i > 0 ? todo[i - 1].a.bound : nullptr;
     todo[i].shape = shape;
     todo[i].run = nchunks > 0 && (unsigned long long)shard < nchunks;
+    goff = (gthis + (size_t)ngroups * sizeof(Group) + 255) & ~size_t(255);
   }
   const auto t_plan1 = std::chrono::steady_clock::now();
   if (hist)
     CK(cudaMemsetAsync(ctx->d_hist, 0, sizeof(unsigned long long) * (ctx->n + 1), ctx->stream));
-  CK(cudaMemcpyAsync(ctx->d_io, ctx->h_io, l.size * (size_t)count, cudaMemcpyHostToDevice,
+  // the used image only: result records + each round's groups
+  CK(cudaMemcpyAsync(ctx->d_io, ctx->h_io, goff, cudaMemcpyHostToDevice,
                      ctx->stream));
   while ((int)ctx->ev_round.size() < count + 1) {
     cudaEvent_t e;
@@ -808,7 +818,8 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   if (count > 1) CK(cudaEventRecord(ctx->ev_round[count], ctx->stream));
   CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
   const auto t_launch1 = std::chrono::steady_clock::now();
-  CK(cudaMemcpyAsync(ctx->h_io, ctx->d_io, l.size * (size_t)(count - 1) + l.off_groups,
+  // the result records only
+  CK(cudaMemcpyAsync(ctx->h_io, ctx->d_io, l.off_groups * (size_t)count,
                      cudaMemcpyDeviceToHost, ctx->stream));
   if (hist)
     CK(cudaMemcpyAsync(ctx->h_hist, ctx->d_hist, sizeof(unsigned long long) * (ctx->n + 1),

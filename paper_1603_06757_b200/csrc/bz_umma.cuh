@@ -85,6 +85,9 @@ constexpr int kUmmaM = 128;       // prefixes per A tile = producer threads
 #ifndef BZ_K5P_EPI_WARPS
 #define BZ_K5P_EPI_WARPS 16
 #endif
+#ifndef BZ_K5P_EPI_GROUPS
+#define BZ_K5P_EPI_GROUPS 1  // K5q: epilogue groups taking alternate tiles
+#endif
 // K5 accumulators start at 1.5 * 2^23 (one extra MMA per part from two tiny
 // constant operands): the fp32 sum then carries the integer dot product in
 // its low 16 bits, so the epilogue reads them with .pack::16b (half the
@@ -133,7 +136,7 @@ struct K4Roles {
   // group covers the whole accumulator), so a group has EGRP tile periods
   // for its loads and reductions while the other groups take the tiles in
   // between
-  static constexpr int EGRP = F4 ? BZ_K5_EPI_GROUPS : 1;
+  static constexpr int EGRP = CW == 4 ? BZ_K5P_EPI_GROUPS : (CW > 1 ? 1 : (F4 ? BZ_K5_EPI_GROUPS : 1));
   static constexpr int EW = E / EGRP;  // warps per group
   static_assert(E % 4 == 0 && ACC * SPLIT <= kMaxAcc && EW % 4 == 0 && (EW / 4) % SPLIT == 0 &&
                     ACC % EGRP == 0,
@@ -725,7 +728,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
   static_assert(!F4 || kUmmaMA == 1, "K5 runs one A tile per B tile");
   static_assert(CW >= 1 && CW <= 4, "kernel form");
   static_assert(!PR || (F4 && kK5Magic && (W & 1) && W <= 3 && BZ_K5_SPLIT == 1 &&
-                        BZ_K5_EPI_GROUPS == 1),
+                        (CW == 4 || BZ_K5_EPI_GROUPS == 1)),
                 "K5p/K5t: odd W <= 3 (stored weights <= 127 fit the 7-bit fields)");
   constexpr int N = k4_n<F4, CW>();
   constexpr int TR = k4_tile_rows<F4, CW>();  // table rows per B tile
