@@ -249,9 +249,12 @@ double binom_d(int p, int q) {
 
 double k5_cost(int k, int g, const Levels& lv, int tile_rows) {
   // K5 clocks per tile / per prefix step (cfg5, B200); K5p/K5q tiles hold
-  // twice the rows for ~1.2x the time
+  // twice the rows
   const bool pair = tile_rows > bz::kUmmaN4;
-  const double kTile = pair ? 880.0 : 727.0, kStep = 1271.0;
+  // (K5q measured: ~625 clocks per tile in steady state; a prefix step --
+  // walker step, A rows, the first tile's latency -- weighs ~3500)
+  double kTile = pair ? 650.0 : 727.0, kStep = pair ? 3500.0 : 1271.0;
+  if (const char* env = getenv("BZ_K5_COST")) sscanf(env, "%lf,%lf", &kTile, &kStep);
   double cost = 0;
   for (int D = 3; D <= lv.dmax; ++D) {
     const int hi = std::min(lv.floor[D + 1] - 1, k - 1 - D);
@@ -275,8 +278,10 @@ Levels k5_levels(int k, int g, int tile_rows) {
   static std::mutex mu;
   static std::map<std::string, Levels> memo;
   const char* env = getenv("BZ_K5_FLOORS");
+  const char* cost = getenv("BZ_K5_COST");
   const std::string key = std::to_string(k) + "/" + std::to_string(g) + "/" +
-                          std::to_string(tile_rows) + "/" + (env ? env : "");
+                          std::to_string(tile_rows) + "/" + (env ? env : "") + "/" +
+                          (cost ? cost : "");
   std::lock_guard<std::mutex> lock(mu);
   auto it = memo.find(key);
   if (it != memo.end()) return it->second;
@@ -430,10 +435,11 @@ int plan_round(bz_ctx* ctx, int g, int gamma_only, PlanShape shape, int nshards,
   static std::map<std::string, Plan> memo;
   const char* floors = getenv("BZ_K5_FLOORS");
   const char* scale = getenv("BZ_K5_CHUNK_SCALE");
-  char key[256];
-  snprintf(key, sizeof key, "%d/%d/%d/%d/%d/%d/%d/%d/%d/%s/%s", ctx->m, ctx->k, g, gamma_only,
+  const char* cost = getenv("BZ_K5_COST");
+  char key[320];
+  snprintf(key, sizeof key, "%d/%d/%d/%d/%d/%d/%d/%d/%d/%s/%s/%s", ctx->m, ctx->k, g, gamma_only,
            shape.kernel, shape.depth, shape.lanes, shape.tile_rows, nshards, floors ? floors : "",
-           scale ? scale : "");
+           scale ? scale : "", cost ? cost : "");
   const IoSlot l = io_layout(ctx->m, ctx->k);
   std::lock_guard<std::mutex> lock(mu);
   auto it = memo.find(key);

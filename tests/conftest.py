@@ -52,3 +52,11 @@ def hexrows(rows):
 # cfg4 histogram checksum (independent numpy
 # restatement of the level-3 saved-additions walk)
 CFG4_HIST_SHA256 = "8d397da157d31b1e67746a3a522b01cb624e4d54d42a27b6fbd403a6da02252b"
+
+
+@pytest.fixture(scope="session")
+def cfg5_traces():
+    g = load_json("cfg5_traces.json")
+    if g is None:
+        pytest.skip("cfg5 seed traces not generated yet")
+    return g
