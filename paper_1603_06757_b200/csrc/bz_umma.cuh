@@ -105,7 +105,7 @@ constexpr int kUmmaMA = BZ_K4_MA; // K4 A tiles (consecutive prefix steps) per B
 constexpr int kTmemCols = 512;    // accumulators (+ K5 scale factors)
 constexpr int kSfCol = 480;       // K5 scale-factor columns [480, 512)
 constexpr int kUmmaN4 = kSfCol / BZ_K5_BUFS;  // K5 triples per B tile (240 / 120)
-constexpr int kUmmaN4P = kSfCol / BZ_K5P_BUFS;  // K5p accumulator columns per tile
+constexpr int kUmmaN4P = (kSfCol / BZ_K5P_BUFS) & ~15;  // K5p/K5q accumulator columns per tile
 constexpr int kMaxStages = 8;
 constexpr int kMaxAcc = 8;
 constexpr int kMaxABuf = 4;

@@ -126,6 +126,17 @@ __global__ void __launch_bounds__(544, 1) probe(int variant, int tiles, long lon
 //   4  SPLIT: each tile's accumulator is two halves of N/2 columns with
 //      their own barriers; the MMAs of half h only wait for half h
 //   8  the epilogue releases, then does 30 VIMNMX3 on what it loaded
+//  16  one issuer warp per accumulator buffer (else warp 0 issues all)
+//  32 / 64  8 / 4 epilogue warps instead of 16
+// 128  epilogue waits with the tight PTX loop
+// 256  no epilogue hand-off at all (issue-only timing)
+// 512  no tcgen05 fences around the hand-off
+// 1024 one waiting warp per lane quarter, named barriers for the rest
+//
+// Measured (B200): the MMA pattern alone and two issuers without hand-off
+// run at 480 clk per tile (peak); one issuer 559; the hand-off with 16
+// epilogue warps ~570-720 (run to run), 4 warps ~565; fences cost nothing;
+// named-barrier leaders and more, smaller buffers are slower.
 constexpr int kPipeWarps = 20;  // up to 3 issuers (mode 16) + 16 epilogue warps
 __global__ void __launch_bounds__(32 * kPipeWarps, 1) pipe_probe(int mode, int acc_bufs, int tiles,
                                                               long long* clk) {
@@ -142,7 +153,7 @@ __global__ void __launch_bounds__(32 * kPipeWarps, 1) pipe_probe(int mode, int a
   if (threadIdx.x == 0) {
     for (int i = 0; i < 16; ++i) {
       mbar_init(accfull(i), 1);
-      mbar_init(accempty(i), ((mode & 64) ? 4 : (mode & 32) ? 8 : 16) / (split ? 2 : 1));
+      mbar_init(accempty(i), (mode & 1024) ? 4 : ((mode & 64) ? 4 : (mode & 32) ? 8 : 16) / (split ? 2 : 1));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -186,7 +197,7 @@ __global__ void __launch_bounds__(32 * kPipeWarps, 1) pipe_probe(int mode, int a
       const uint64_t ad = a0 + (uint64_t)(ab * (kTA >> 4));
       for (int h = 0; h < parts; ++h) {
         const int hb = buf * parts + h;
-        mbar_wait_fast(accempty(hb), ((t / acc_bufs) & 1) ^ 1);
+        if (!(mode & 256)) mbar_wait_fast(accempty(hb), ((t / acc_bufs) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + (uint32_t)(buf * N + h * (N / parts));
         if (elect_one()) {
@@ -210,9 +221,16 @@ __global__ void __launch_bounds__(32 * kPipeWarps, 1) pipe_probe(int mode, int a
     for (int t = 0; t < tiles; ++t) {
       const int buf = t % acc_bufs;
       const int hb = buf * parts + h;
-      if (mode & 128) mbar_wait_fast(accfull(hb), (t / acc_bufs) & 1);
-      else mbar_wait(accfull(hb), (t / acc_bufs) & 1);
-      tc_fence_after();
+      if (mode & 256) break;  // mode 256: no epilogue at all (issue-only timing)
+      // mode 1024: one warp per lane quarter waits on the mbarrier and
+      // releases the quarter's other warps through a named barrier
+      const bool lead = !(mode & 1024) || e < 4;
+      if (lead) {
+        if (mode & 128) mbar_wait_fast(accfull(hb), (t / acc_bufs) & 1);
+        else mbar_wait(accfull(hb), (t / acc_bufs) & 1);
+      }
+      if (mode & 1024) asm volatile("bar.sync %0, 128;" ::"r"(1 + quarter) : "memory");
+      if (!(mode & 512)) tc_fence_after();
       const uint32_t tb = tmem + ((uint32_t)(32 * quarter) << 16) + (uint32_t)(buf * N + cols * sl);
       uint32_t v[64];
       if (mode & 1) {
@@ -227,9 +245,14 @@ __global__ void __launch_bounds__(32 * kPipeWarps, 1) pipe_probe(int mode, int a
         for (int i = 0; i < 28; i += 4) tmem_regs4_after_wait(v + i);
         tmem_regs4_after_wait(v + 26);
       }
-      tc_fence_before();
+      if (!(mode & 512)) tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(accempty(hb));
+      if (mode & 1024) {
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + quarter) : "memory");
+        if (e < 4 && lane == 0) mbar_arrive(accempty(hb));
+      } else if (lane == 0) {
+        mbar_arrive(accempty(hb));
+      }
       if (mode & 8) {
 #pragma unroll
         for (int i = 0; i + 1 < 60; i += 2) sink = __vimin3_s16x2(sink, v[i], v[i + 1]);
@@ -268,7 +291,9 @@ int main() {
            128.0 * kN * 64 / per_mma);
   }
   cudaFuncSetAttribute(pipe_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int cfgs[][2] = {{16, 2}, {25, 2}};
+  // {mode, buffers}: see the mode bits above pipe_probe
+  const int cfgs[][2] = {{0, 2},   {16, 2},  {17, 2},  {18, 2}, {25, 2}, {80, 2},
+                         {272, 2}, {256, 2}, {528, 2}, {1040, 2}, {16, 3}, {272, 3}};
   for (auto& c : cfgs) {
     for (int rep = 0; rep < 2; ++rep) {
       pipe_probe<<<148, 32 * kPipeWarps, smem>>>(c[0], c[1], tiles, d);
