@@ -524,6 +524,55 @@ int launch_wd(bz_ctx* ctx, const RoundArgs& a, bool hist) {
   return BZ_OK;
 }
 
+// Consecutive K1 rounds of one batch in one launch (k1_rounds).
+template <int W, int D>
+int launch_k1_fused(bz_ctx* ctx, const RoundArgs* as, int count) {
+  bz::K1Batch b{};
+  int cap = 0;
+  unsigned long long warps = 0;
+  for (int i = 0; i < count; ++i) {
+    cap = std::max(cap, as[i].ngroups);
+    warps = std::max(warps, (as[i].nchunks + as[i].nshards - 1) / as[i].nshards);
+  }
+  for (int i = 0; i < count; ++i) {
+    b.a[i] = as[i];
+    b.a[i].sgroups_cap = cap;
+    b.a[i].chain = nullptr;
+  }
+  b.count = count;
+  const size_t smem = bz::smem_base_bytes<W>(as[0].m, as[0].k, cap);
+  const int threads = 256;
+  int per_sm = 0;
+  int rc = prep_launch(ctx, (const void*)bz::k1_rounds<W, D>, threads, smem, &per_sm);
+  if (rc) return rc;
+  if (per_sm < 1) return fail(ctx, BZ_ERR_TOO_LARGE, "kernel does not fit on an SM (smem %zu)", smem);
+  long long blocks = (long long)per_sm * ctx->sm_count;
+  blocks = std::max(1ll, std::min(blocks, (long long)((warps + 7) / 8)));
+  bz::k1_rounds<W, D><<<(unsigned)blocks, threads, smem, ctx->stream>>>(b);
+  CK(cudaGetLastError());
+  ctx->launches += 1;
+  return BZ_OK;
+}
+
+template <int W>
+int launch_fused_w(bz_ctx* ctx, const RoundArgs* as, int count, int depth) {
+  return depth == 2 ? launch_k1_fused<W, 2>(ctx, as, count) : launch_k1_fused<W, 1>(ctx, as, count);
+}
+
+int launch_fused(bz_ctx* ctx, const RoundArgs* as, int count, int depth) {
+  switch (ctx->w32) {
+    case 1: return launch_fused_w<1>(ctx, as, count, depth);
+    case 2: return launch_fused_w<2>(ctx, as, count, depth);
+    case 3: return launch_fused_w<3>(ctx, as, count, depth);
+    case 4: return launch_fused_w<4>(ctx, as, count, depth);
+    case 5: return launch_fused_w<5>(ctx, as, count, depth);
+    case 6: return launch_fused_w<6>(ctx, as, count, depth);
+    case 7: return launch_fused_w<7>(ctx, as, count, depth);
+    case 8: return launch_fused_w<8>(ctx, as, count, depth);
+    default: return fail(ctx, BZ_ERR_TOO_LARGE, "unsupported word count %d", ctx->w32);
+  }
+}
+
 template <int W>
 int launch_tc(bz_ctx* ctx, const RoundArgs& a) {
   const size_t smem = bz::k3_smem_bytes<W>(a.m, a.k, a.ngroups);
@@ -818,6 +867,23 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   for (int i = 0; i < count; ++i) {
     if (count > 1) CK(cudaEventRecord(ctx->ev_round[i], ctx->stream));
     if (!todo[i].run) continue;
+    // consecutive small K1 rounds of the same depth share one launch (their
+    // per-round times then all land on the first of them)
+    int f = 1;
+    while (!hist && todo[i].shape.kernel == 1 && f < bz::kK1MaxFused && i + f < count &&
+           todo[i + f].run && todo[i + f].shape.kernel == 1 &&
+           todo[i + f].shape.depth == todo[i].shape.depth && !debug)
+      ++f;
+    if (f > 1) {
+      std::vector<RoundArgs> as;
+      for (int q = 0; q < f; ++q) as.push_back(todo[i + q].a);
+      rc = launch_fused(ctx, as.data(), f, todo[i].shape.depth);
+      if (rc) return rc;
+      for (int q = 1; q < f; ++q)
+        if (count > 1) CK(cudaEventRecord(ctx->ev_round[i + q], ctx->stream));
+      i += f - 1;
+      continue;
+    }
     rc = launch(ctx, todo[i].a, hist, todo[i].shape);
     if (rc) return rc;
   }
@@ -1114,11 +1180,19 @@ int bz_rounds(bz_ctx* ctx, int g0, int count, const int32_t* lower_prev, int upp
   std::vector<int> lp(lower_prev, lower_prev + std::max(count, 0));
   int rc = run_batch(ctx, g0, count, -1, lp.data(), upper, shard, nshards, false);
   if (rc) return rc;
-  for (int i = 0; i < count; ++i)
+  // round i reports its minima clipped to the U round i-1 ended with (the
+  // device chain already starts it there; rounds fused into one launch are
+  // clipped here)
+  int U = upper;
+  for (int i = 0; i < count; ++i) {
+    const int Ui = U;
     for (int j = 0; j < ctx->m; ++j) {
-      out_min[(size_t)i * ctx->m + j] = std::min(slot_bound(ctx, i)[1 + j], upper);
+      const int v = std::min(slot_bound(ctx, i)[1 + j], Ui);
+      out_min[(size_t)i * ctx->m + j] = v;
       out_combos[(size_t)i * ctx->m + j] = slot_combos(ctx, i)[j];
+      U = std::min(U, v);
     }
+  }
   return BZ_OK;
 }
 

@@ -76,6 +76,8 @@ struct RoundArgs {
   long long* ctrace;           // K4/K5 per-chunk timeline (BZ_K4_DEBUG & 32), else null
   const int* chain;            // batched rounds: the previous round's bounds (its U
                                // after the round tightens this round's start), or null
+  int sgroups_cap;             // shared-memory room for this many groups (fused K1
+                               // launches stage several plans in turn), 0 = ngroups
 };
 
 __host__ __device__ constexpr int padded_words(int w) {
@@ -300,8 +302,9 @@ __host__ __device__ inline size_t smem_base_bytes(int m, int k, int ngroups) {
 // the small binomial table at the end of the staged region
 template <int W>
 __device__ __forceinline__ unsigned long long* smem_binom(unsigned char* smem, const RoundArgs& a) {
-  return reinterpret_cast<unsigned long long*>(smem + smem_base_bytes<W>(a.m, a.k, a.ngroups) -
-                                               kSBinomBytes);
+  return reinterpret_cast<unsigned long long*>(
+      smem + smem_base_bytes<W>(a.m, a.k, a.ngroups > a.sgroups_cap ? a.ngroups : a.sgroups_cap) -
+      kSBinomBytes);
 }
 
 template <int W>
@@ -414,22 +417,10 @@ __device__ __forceinline__ ChunkView open_chunk(const Group* sg, int ngroups,
 // XOR/POPC chains).  When the range is odd the second walker duplicates the
 // first on the last step -- harmless for a minimum.
 template <int W, int D>
-__global__ void __launch_bounds__(256)
-k1_round_min(const RoundArgs a) {
+__device__ __forceinline__ void k1_chunks(const RoundArgs& a, const uint32_t* srows,
+                                          const uint32_t* spx, const Group* sgroups,
+                                          const unsigned long long* sbinom) {
   constexpr int WP = padded_words(W);
-  extern __shared__ __align__(128) unsigned char smem[];
-  uint32_t *srows, *spx;
-  Group* sgroups;
-  stage<W>(a, srows, spx, sgroups, smem);
-  const unsigned long long* sbinom = smem_binom<W>(smem, a);
-  if (a.chain && threadIdx.x == 0 && blockIdx.x == 0) {
-    // batched round: start from the U the previous round ended with (one
-    // thread of the grid: atomics on one address serialise; blocks that read
-    // the bound before it lands just see the looser start value)
-    const int u = ((volatile const int*)a.chain)[0];
-    for (int j = 0; j <= a.m; ++j) atomicMin(a.bound + j, u);
-  }
-
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int k = a.k, q = a.g - 1 - D;
@@ -473,15 +464,70 @@ k1_round_min(const RoundArgs a) {
       }
     }
 
-    // chunk epilogue: warp min -> per-Gamma and round minima; combos count
+    // chunk epilogue: warp min -> per-Gamma and round minima (fire-and-
+    // forget reductions); combos count
     int wbest = __reduce_min_sync(FULL, best);
     if (wbest != INT_MAX) wbest += gamma_woff(a, v.gr.gamma);
     const unsigned tot = __reduce_add_sync(FULL, (unsigned)v.cnt);
     if (lane == 0) {
-      if (wbest < vbound[1 + v.gr.gamma]) atomicMin(a.bound + 1 + v.gr.gamma, wbest);
-      if (wbest < vbound[0]) atomicMin(a.bound, wbest);
+      if (wbest != INT_MAX) {
+        atomicMin(a.bound + 1 + v.gr.gamma, wbest);
+        atomicMin(a.bound, wbest);
+      }
       atomicAdd(a.combos + v.gr.gamma, (unsigned long long)tot * suffix_count<D>(k, e0));
     }
+  }
+}
+
+template <int W, int D>
+__global__ void __launch_bounds__(256)
+k1_round_min(const RoundArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint32_t *srows, *spx;
+  Group* sgroups;
+  stage<W>(a, srows, spx, sgroups, smem);
+  const unsigned long long* sbinom = smem_binom<W>(smem, a);
+  if (a.chain && threadIdx.x == 0 && blockIdx.x == 0) {
+    // batched round: start from the U the previous round ended with (one
+    // thread of the grid: atomics on one address serialise; blocks that read
+    // the bound before it lands just see the looser start value)
+    const int u = ((volatile const int*)a.chain)[0];
+    for (int j = 0; j <= a.m; ++j) atomicMin(a.bound + j, u);
+  }
+  k1_chunks<W, D>(a, srows, spx, sgroups, sbinom);
+}
+
+// Several small rounds (same family, same suffix depth) in one launch: the
+// rows, prefix table and binomials are staged once, each round's work plan
+// in turn; a block moves to round r+1 once round r's chunk cursor is
+// exhausted, so the rounds overlap across blocks.  (No device-side U chain
+// between them: bz_rounds clips each round's minima to its predecessor's U
+// on the host, which gives the same results.)
+constexpr int kK1MaxFused = 4;
+struct K1Batch {
+  RoundArgs a[kK1MaxFused];
+  int count;
+};
+
+template <int W, int D>
+__global__ void __launch_bounds__(256) k1_rounds(const K1Batch b) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint32_t *srows, *spx;
+  Group* sgroups;
+  stage<W>(b.a[0], srows, spx, sgroups, smem);
+  const unsigned long long* sbinom = smem_binom<W>(smem, b.a[0]);
+  for (int r = 0; r < b.count; ++r) {
+    const RoundArgs& a = b.a[r];
+    if (r > 0) {
+      __syncthreads();  // every warp is done with round r-1's plan
+      const int gw = a.ngroups * (int)(sizeof(Group) / 4);
+      const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(a.groups);
+      uint32_t* gdst = reinterpret_cast<uint32_t*>(sgroups);
+#pragma unroll 8
+      for (int i = threadIdx.x; i < gw; i += blockDim.x) gdst[i] = gsrc[i];
+      __syncthreads();
+    }
+    k1_chunks<W, D>(a, srows, spx, sgroups, sbinom);
   }
 }
 
