@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define BZ_ABI_VERSION 8
+#define BZ_ABI_VERSION 9
 
 /* limits of the device kernels */
 #define BZ_MAX_K 128 /* rows per Gamma (prefix masks are 128-bit)      */
@@ -104,6 +104,16 @@ int bz_brute_force(bz_ctx *ctx, const uint64_t *rows, int k, int n, int max_k,
  * rank to *out_rank.  Needs no device. */
 int bz_reduce_on_columns(uint64_t *rows, int k, int n, const int32_t *cols, int ncols,
                          int32_t *out_pivots, int *out_rank);
+
+/* Host only: the information-set family of build_gamma_set
+ * (m/gf2.py:168-199) in one call.  Greedy Gauss-Jordan on the still-unused
+ * columns (leftmost first), each pass continuing from the previous reduced
+ * matrix; full-rank passes append Gamma_j, the first deficient pass with
+ * rank > 0 is the remainder.  rows: k x ceil(n/64) words of G.  out_rows:
+ * m_max x k x ceil(n/64), out_pivots: m_max x k, out_ranks: m_max.  *out_m =
+ * 0 with out_ranks[0] = rank means G itself is rank deficient. */
+int bz_gamma_family(const uint64_t *rows, int k, int n, int m_max, uint64_t *out_rows,
+                    int32_t *out_pivots, int32_t *out_ranks, int *out_m);
 
 /* Identity-column elision (default on; applies from the next
  * bz_load_gammas): a Gamma with one unit column per row -- every full-rank

@@ -18,7 +18,7 @@ from .errors import (DeviceError, InvalidArity, InvalidDimensions, MindistError,
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BZ_LIB") or os.path.join(PKG_DIR, "libbz.so")
-ABI_VERSION = 8
+ABI_VERSION = 9
 
 BZ_OK = 0
 _CODES = {
@@ -38,7 +38,7 @@ SYMBOLS = ("bz_abi_version", "bz_device_count", "bz_create", "bz_destroy",
            "bz_round", "bz_rounds",
            "bz_enumerate",
            "bz_histogram", "bz_plan", "bz_timer_start", "bz_timer_stop",
-           "bz_last_kernel_ms", "bz_round_ms", "bz_launch_count", "bz_measure_int_peaks")
+           "bz_last_kernel_ms", "bz_round_ms", "bz_gamma_family", "bz_launch_count", "bz_measure_int_peaks")
 
 _lib = None
 
@@ -80,6 +80,8 @@ def lib():
     L.bz_timer_stop.argtypes = [vp, ctypes.POINTER(c_float)]
     L.bz_last_kernel_ms.argtypes = [vp, ctypes.POINTER(c_float)]
     L.bz_round_ms.argtypes = [vp, ctypes.POINTER(c_float), c_int]
+    L.bz_gamma_family.argtypes = [u64p, c_int, c_int, c_int, u64p, i32p, i32p,
+                                  ctypes.POINTER(c_int)]
     L.bz_launch_count.argtypes = [vp, u64p]
     L.bz_measure_int_peaks.argtypes = [vp, c_int, ctypes.POINTER(c_double)]
     if L.bz_abi_version() != ABI_VERSION:

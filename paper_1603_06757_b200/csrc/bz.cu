@@ -1314,6 +1314,43 @@ int bz_reduce_on_columns(uint64_t* rows, int k, int n, const int32_t* cols, int 
   return BZ_OK;
 }
 
+int bz_gamma_family(const uint64_t* rows, int k, int n, int m_max, uint64_t* out_rows,
+                    int32_t* out_pivots, int32_t* out_ranks, int* out_m) {
+  if (!rows || !out_rows || !out_pivots || !out_ranks || !out_m || m_max < 1)
+    return BZ_ERR_ARGUMENT;
+  if (k < 1 || n < 1 || k > 4096 || n > 65536) return BZ_ERR_INVALID_DIMENSIONS;
+  const int w = (n + 63) / 64;
+  const size_t img = (size_t)k * w;
+  std::vector<uint64_t> cur(rows, rows + img);
+  std::vector<char> used(n, 0);
+  std::vector<int32_t> free_cols, piv(k);
+  int nused = 0, m = 0;
+  *out_m = 0;
+  while (nused < n) {
+    free_cols.clear();
+    for (int c = 0; c < n; ++c)
+      if (!used[c]) free_cols.push_back(c);
+    int rank = 0;
+    int rc = bz_reduce_on_columns(cur.data(), k, n, free_cols.data(), (int)free_cols.size(),
+                                  piv.data(), &rank);
+    if (rc) return rc;
+    if (m == 0 && rank < k) {  // G itself is rank deficient
+      out_ranks[0] = rank;
+      return BZ_OK;
+    }
+    if (rank == 0) break;
+    if (m >= m_max) return BZ_ERR_ARGUMENT;
+    std::copy(cur.begin(), cur.end(), out_rows + (size_t)m * img);
+    std::copy(piv.begin(), piv.begin() + rank, out_pivots + (size_t)m * k);
+    out_ranks[m++] = rank;
+    if (rank < k) break;  // the first deficient pass is the remainder Gamma_m
+    for (int i = 0; i < rank; ++i) used[piv[i]] = 1;
+    nused += rank;
+  }
+  *out_m = m;
+  return BZ_OK;
+}
+
 int bz_set_elision(bz_ctx* ctx, int on) {
   if (!ctx) return BZ_ERR_ARGUMENT;
   ctx->elision = on ? 1 : 0;
