@@ -206,8 +206,10 @@ int bz_timer_stop(bz_ctx *ctx, float *ms);
  * bz_enumerate / bz_histogram call, from CUDA events around that launch. */
 int bz_last_kernel_ms(bz_ctx *ctx, float *ms);
 
-/* Per-round device time (ms) of the last bz_round / bz_rounds call: CUDA
- * events between consecutive launches, count <= rounds of that call. */
+/* Per-round device time (ms) of the last bz_round / bz_rounds call, count
+ * <= rounds of that call.  The largest round of a batch is bracketed by CUDA
+ * events; the other rounds (launched as programmatic dependents, so their
+ * kernels overlap) share the rest of the batch time by combination count. */
 int bz_round_ms(bz_ctx *ctx, float *out_ms, int count);
 
 /* Number of kernels this context has launched so far. */

@@ -42,6 +42,7 @@ struct bz_ctx {
   float last_kernel_ms = 0.f;
   std::vector<cudaEvent_t> ev_round;  // one per launch boundary of the last batch
   std::vector<float> round_ms;        // per-round device ms of the last batch
+  bool pdl_next = false;              // the next round launch may overlap the previous one
 
   // loaded family
   int m = 0, k = 0, n = 0, w32 = 0, wp = 0;
@@ -618,9 +619,20 @@ int launch_umma(bz_ctx* ctx, const RoundArgs& a) {
     tabs.t[0] = ctx->d_trip4;
     tabs.stride_rows[0] = ctx->trip4_rows;
   }
-  bz::k4_round_umma<W, F4, CW><<<(unsigned)blocks, bz::K4Roles<F4, CW>::THREADS, smem, ctx->stream>>>(
-      a, tabs);
-  CK(cudaGetLastError());
+  // programmatic dependent launch after another round kernel: this
+  // launch's CTAs take SMs as the previous round's CTAs exit (the rounds
+  // are independent; the optional U chain tolerates an early read)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)blocks);
+  cfg.blockDim = dim3(bz::K4Roles<F4, CW>::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx->stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = ctx->pdl_next ? 1 : 0;
+  CK(cudaLaunchKernelEx(&cfg, bz::k4_round_umma<W, F4, CW>, a, tabs));
   ctx->launches += 1;
   return BZ_OK;
 }
@@ -863,31 +875,47 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     CK(cudaEventCreate(&e));
     ctx->ev_round.push_back(e);
   }
+  // Launch order: back to back on one stream; a round kernel that follows
+  // another round kernel is launched as a programmatic dependent (it fills
+  // SMs as the previous one drains).  Only the largest round of the batch
+  // is bracketed by events (an event between two kernels would serialise
+  // them): its device time is measured, the others share the remainder by
+  // combination count.
+  int big = 0;
+  for (int i = 1; i < count; ++i)
+    if (todo[i].run && todo[i].a.g >= todo[big].a.g) big = i;
   CK(cudaEventRecord(ctx->ev_k0, ctx->stream));
+  bool prev_round = false;
+  const bool timed = count > 1;
   for (int i = 0; i < count; ++i) {
-    if (count > 1) CK(cudaEventRecord(ctx->ev_round[i], ctx->stream));
+    if (timed && i == big) {
+      CK(cudaEventRecord(ctx->ev_round[0], ctx->stream));
+      prev_round = false;
+    }
     if (!todo[i].run) continue;
-    // consecutive small K1 rounds of the same depth share one launch (their
-    // per-round times then all land on the first of them)
+    ctx->pdl_next = prev_round && !debug;
+    // consecutive small K1 rounds of the same depth share one launch
     int f = 1;
     while (!hist && todo[i].shape.kernel == 1 && f < bz::kK1MaxFused && i + f < count &&
            todo[i + f].run && todo[i + f].shape.kernel == 1 &&
-           todo[i + f].shape.depth == todo[i].shape.depth && !debug)
+           todo[i + f].shape.depth == todo[i].shape.depth && !debug && i + f != big)
       ++f;
     if (f > 1) {
       std::vector<RoundArgs> as;
       for (int q = 0; q < f; ++q) as.push_back(todo[i + q].a);
       rc = launch_fused(ctx, as.data(), f, todo[i].shape.depth);
-      if (rc) return rc;
-      for (int q = 1; q < f; ++q)
-        if (count > 1) CK(cudaEventRecord(ctx->ev_round[i + q], ctx->stream));
-      i += f - 1;
-      continue;
+    } else {
+      rc = launch(ctx, todo[i].a, hist, todo[i].shape);
     }
-    rc = launch(ctx, todo[i].a, hist, todo[i].shape);
+    ctx->pdl_next = false;
     if (rc) return rc;
+    prev_round = true;
+    if (timed && i <= big && big < i + f) {
+      CK(cudaEventRecord(ctx->ev_round[1], ctx->stream));
+      prev_round = false;
+    }
+    i += f - 1;
   }
-  if (count > 1) CK(cudaEventRecord(ctx->ev_round[count], ctx->stream));
   CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
   const auto t_launch1 = std::chrono::steady_clock::now();
   // the result records only
@@ -908,8 +936,15 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   if (count == 1) {
     ctx->round_ms[0] = ctx->last_kernel_ms;
   } else {
+    float big_ms = 0.f;
+    CK(cudaEventElapsedTime(&big_ms, ctx->ev_round[0], ctx->ev_round[1]));
+    ctx->round_ms[big] = big_ms;
+    double rest = 0;
     for (int i = 0; i < count; ++i)
-      CK(cudaEventElapsedTime(&ctx->round_ms[i], ctx->ev_round[i], ctx->ev_round[i + 1]));
+      if (i != big && todo[i].run) rest += binom_d(ctx->k, todo[i].a.g);
+    for (int i = 0; i < count; ++i)
+      if (i != big && todo[i].run && rest > 0)
+        ctx->round_ms[i] = (float)((ctx->last_kernel_ms - big_ms) * binom_d(ctx->k, todo[i].a.g) / rest);
   }
   if (ctrace) {
     // BZ_K4_DEBUG & 32: per-chunk timeline to $BZ_K4_CTRACE (raw int64)

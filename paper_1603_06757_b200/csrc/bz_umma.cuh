@@ -809,6 +809,9 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
                  "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  // the next round's kernel (programmatic dependent launch) may start its
+  // CTAs as this kernel's CTAs exit: rounds are independent
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // per-block lifetime (BZ_K4_DEBUG & 32): slot 63 = {entry, prologue done,
   // exit} in globaltimer ns
   long long* const life = a.ctrace ? a.ctrace + ((size_t)blockIdx.x * 64 + 63) * 4 : nullptr;
@@ -1417,7 +1420,12 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
           // next chunk of this shard, or -1 (done, or U reached L_prev)
           const unsigned long long cidx = atomicAdd(a.counter, 1ull);
           const unsigned long long ch = cidx * (unsigned long long)a.nshards + a.shard;
-          const long long qchunk = (ch < a.nchunks && vb[0] > a.lower_prev) ? (long long)ch : -1;
+          // (a.chain: the previous round of the batch, running concurrently
+          // under programmatic launch -- once its minimum meets this round's
+          // L_prev the run has terminated and this round is not needed)
+          const bool live = vb[0] > a.lower_prev &&
+                            (!a.chain || ((volatile const int*)a.chain)[0] > a.lower_prev);
+          const long long qchunk = (ch < a.nchunks && live) ? (long long)ch : -1;
           s_q[qs] = qchunk;
           long long* ct = k4_ctrace(a, qpub);
           if (ct) { ct[0] = qchunk; ct[1] = clock64(); }
