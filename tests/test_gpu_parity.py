@@ -413,3 +413,24 @@ def test_batched_rounds_chain_u(ctx, engine_name):
             U = min([U] + mins)
     finally:
         ctx.set_engine("auto")
+
+
+def test_batched_rounds_past_termination_exit(ctx):
+    """A batch that runs ahead of termination: the rounds after the one
+    where L >= U start from (or, launched as programmatic dependents, watch)
+    the predecessor's U, find it already <= their L_prev and stop at once,
+    while the rounds up to termination are exact."""
+    G, gs, _ = code("cfg2", 1)  # trace (1,4,16) (2,6,15) (3,8,12) (4,10,12) (5,12,11)
+    ctx.set_engine("auto")
+    ctx.load(family_words(gs.gammas, 96), 96)
+    k, m = 48, 2
+    lps = [0] + [2 * (g + 1) for g in range(1, 8)]  # L after round g (m = 2 full sets)
+    res = ctx.rounds(1, lps, 10**6)
+    U = 10**6
+    for g, (mins, combos) in enumerate(res[:5], start=1):
+        U = min([U] + mins)
+        assert combos == [comb(k, g)] * m or U <= lps[g - 1], (g, combos)
+    assert U == 11
+    for g, (mins, combos) in enumerate(res[5:], start=6):
+        assert min(mins) <= 11
+        assert sum(combos) < 0.05 * m * comb(k, g), (g, combos)
