@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define BZ_ABI_VERSION 9
+#define BZ_ABI_VERSION 10
 
 /* limits of the device kernels */
 #define BZ_MAX_K 128 /* rows per Gamma (prefix masks are 128-bit)      */
@@ -121,6 +121,22 @@ int bz_gamma_family(const uint64_t *rows, int k, int n, int m_max, uint64_t *out
  * without those k columns and its weights get + g, which is exact because
  * each chosen row carries exactly one of them.  The remainder Gamma (rank <
  * k) keeps all n columns.  Results are identical either way. */
+/* Multi-GPU shared bound (one process per GPU).  Rank 0 allocates the
+ * mirror and exports a 64-byte CUDA IPC handle (bz_shared_bound_export),
+ * every rank opens it (rank 0 with handle = NULL, i.e. its own array), and
+ * before each minimum-distance run every rank sets the same epoch.  Round
+ * kernels then RED.MIN their chunk minima into the mirror over NVLink and
+ * stop taking work as soon as any rank's running minimum meets L_prev, so
+ * a batch of rounds can run ahead of termination on every rank.  Results
+ * are still each rank's own shard (combine them as before). */
+int bz_shared_bound_export(bz_ctx *ctx, void *out_handle /* 64 bytes */);
+int bz_shared_bound_open(bz_ctx *ctx, const void *handle /* NULL: own */);
+int bz_shared_bound_epoch(bz_ctx *ctx, uint32_t epoch);
+/* The shared running minimum of round g in the current epoch (INT32_MAX if
+ * none yet), read through this rank's mapping (diagnostics, tests). */
+int bz_shared_bound_read(bz_ctx *ctx, int g, int32_t *out);
+int bz_shared_bound_close(bz_ctx *ctx);
+
 int bz_set_elision(bz_ctx *ctx, int on);
 
 /* Bit j set: Gamma j of the loaded family was stored with its identity

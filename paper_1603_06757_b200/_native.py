@@ -18,7 +18,7 @@ from .errors import (DeviceError, InvalidArity, InvalidDimensions, MindistError,
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BZ_LIB") or os.path.join(PKG_DIR, "libbz.so")
-ABI_VERSION = 9
+ABI_VERSION = 10
 
 BZ_OK = 0
 _CODES = {
@@ -38,7 +38,10 @@ SYMBOLS = ("bz_abi_version", "bz_device_count", "bz_create", "bz_destroy",
            "bz_round", "bz_rounds",
            "bz_enumerate",
            "bz_histogram", "bz_plan", "bz_timer_start", "bz_timer_stop",
-           "bz_last_kernel_ms", "bz_round_ms", "bz_gamma_family", "bz_launch_count", "bz_measure_int_peaks")
+           "bz_last_kernel_ms", "bz_round_ms", "bz_gamma_family",
+           "bz_shared_bound_export", "bz_shared_bound_open", "bz_shared_bound_epoch",
+           "bz_shared_bound_read",
+           "bz_shared_bound_close", "bz_launch_count", "bz_measure_int_peaks")
 
 _lib = None
 
@@ -80,6 +83,11 @@ def lib():
     L.bz_timer_stop.argtypes = [vp, ctypes.POINTER(c_float)]
     L.bz_last_kernel_ms.argtypes = [vp, ctypes.POINTER(c_float)]
     L.bz_round_ms.argtypes = [vp, ctypes.POINTER(c_float), c_int]
+    L.bz_shared_bound_export.argtypes = [vp, ctypes.c_char_p]
+    L.bz_shared_bound_open.argtypes = [vp, ctypes.c_char_p]
+    L.bz_shared_bound_epoch.argtypes = [vp, ctypes.c_uint32]
+    L.bz_shared_bound_close.argtypes = [vp]
+    L.bz_shared_bound_read.argtypes = [vp, c_int, i32p]
     L.bz_gamma_family.argtypes = [u64p, c_int, c_int, c_int, u64p, i32p, i32p,
                                   ctypes.POINTER(c_int)]
     L.bz_launch_count.argtypes = [vp, u64p]
@@ -176,6 +184,34 @@ class Context:
             raise ValueError(f"unknown engine {engine!r}")
         check(lib().bz_set_engine(self.handle, ENGINES[engine]), self.handle, "bz_set_engine")
         self.engine = engine
+
+    def shared_bound_export(self) -> bytes:
+        """Allocate this context's shared-bound mirror; its 64-byte CUDA IPC
+        handle (see bz_shared_bound_export)."""
+        buf = ctypes.create_string_buffer(64)
+        check(lib().bz_shared_bound_export(self.handle, buf), self.handle,
+              "bz_shared_bound_export")
+        return buf.raw
+
+    def shared_bound_open(self, handle: bytes | None) -> None:
+        """Use the mirror of `handle` (None: this context's own)."""
+        if handle is not None and len(handle) != 64:
+            raise ValueError("IPC handle must be 64 bytes")
+        check(lib().bz_shared_bound_open(self.handle, handle), self.handle,
+              "bz_shared_bound_open")
+
+    def shared_bound_epoch(self, epoch: int) -> None:
+        check(lib().bz_shared_bound_epoch(self.handle, epoch & 0xffffffff), self.handle,
+              "bz_shared_bound_epoch")
+
+    def shared_bound_read(self, g: int) -> int:
+        out = np.zeros(1, dtype=np.int32)
+        check(lib().bz_shared_bound_read(self.handle, g, _ptr(out, ctypes.c_int32)), self.handle,
+              "bz_shared_bound_read")
+        return int(out[0])
+
+    def shared_bound_close(self) -> None:
+        check(lib().bz_shared_bound_close(self.handle), self.handle, "bz_shared_bound_close")
 
     def set_elision(self, on: bool) -> None:
         """Identity-column elision for the next load (see bz_set_elision);

@@ -43,6 +43,13 @@ struct bz_ctx {
   std::vector<cudaEvent_t> ev_round;  // one per launch boundary of the last batch
   std::vector<float> round_ms;        // per-round device ms of the last batch
   bool pdl_next = false;              // the next round launch may overlap the previous one
+  // multi-GPU shared bound mirror (bz_shared_bound_*): this rank's own array
+  // (allocated on export), the array the kernels use (the owner's, mapped
+  // over CUDA IPC, or this rank's own), and the run tag
+  unsigned long long* d_gbound_own = nullptr;
+  unsigned long long* d_gbound = nullptr;
+  bool gbound_ipc = false;
+  unsigned long long gtag = 0;
 
   // loaded family
   int m = 0, k = 0, n = 0, w32 = 0, wp = 0;
@@ -860,6 +867,8 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     a.ctrace = (i == count - 1) ? ctrace : nullptr;
     a.trace_ell = getenv("BZ_K4_TRACE_ELL") ? atoi(getenv("BZ_K4_TRACE_ELL")) : -1;
     a.chain = i > 0 ? todo[i - 1].a.bound : nullptr;
+    a.gbound = gamma_only < 0 ? ctx->d_gbound : nullptr;  // whole rounds only
+    a.gtag = ctx->gtag;
     todo[i].shape = shape;
     todo[i].run = nchunks > 0 && (unsigned long long)shard < nchunks;
     goff = (gthis + (size_t)ngroups * sizeof(Group) + 255) & ~size_t(255);
@@ -1067,6 +1076,8 @@ void bz_destroy(bz_ctx* ctx) {
     if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
     if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
     if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
+    if (ctx->gbound_ipc && ctx->d_gbound) cudaIpcCloseMemHandle(ctx->d_gbound);
+    cudaFree(ctx->d_gbound_own);
     if (ctx->ev_k0) cudaEventDestroy(ctx->ev_k0);
     for (cudaEvent_t e : ctx->ev_round) cudaEventDestroy(e);
     if (ctx->ev_k1) cudaEventDestroy(ctx->ev_k1);
@@ -1383,6 +1394,74 @@ int bz_gamma_family(const uint64_t* rows, int k, int n, int m_max, uint64_t* out
     nused += rank;
   }
   *out_m = m;
+  return BZ_OK;
+}
+
+// ---- multi-GPU shared bound mirror
+constexpr int kGBoundWords = BZ_MAX_K + 2;  // one word per round g (1..k)
+
+int bz_shared_bound_export(bz_ctx* ctx, void* out_handle) {
+  if (!ctx || !out_handle) return BZ_ERR_ARGUMENT;
+  if (ctx->device < 0) return fail(ctx, BZ_ERR_NO_DEVICE, "context has no device");
+  CK(cudaSetDevice(ctx->device));
+  if (!ctx->d_gbound_own) {
+    CK(cudaMalloc(&ctx->d_gbound_own, kGBoundWords * sizeof(unsigned long long)));
+    // all ones: tag 0xffffffff (older than every run) = empty
+    CK(cudaMemset(ctx->d_gbound_own, 0xff, kGBoundWords * sizeof(unsigned long long)));
+  }
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, ctx->d_gbound_own));
+  std::memcpy(out_handle, &h, sizeof h);
+  return BZ_OK;
+}
+
+int bz_shared_bound_open(bz_ctx* ctx, const void* handle) {
+  if (!ctx) return BZ_ERR_ARGUMENT;
+  if (ctx->device < 0) return fail(ctx, BZ_ERR_NO_DEVICE, "context has no device");
+  CK(cudaSetDevice(ctx->device));
+  if (ctx->gbound_ipc && ctx->d_gbound) {
+    cudaIpcCloseMemHandle(ctx->d_gbound);
+    ctx->gbound_ipc = false;
+  }
+  ctx->d_gbound = nullptr;
+  if (!handle) {  // the owner: its own array
+    if (!ctx->d_gbound_own)
+      return fail(ctx, BZ_ERR_STATE, "bz_shared_bound_export first");
+    ctx->d_gbound = ctx->d_gbound_own;
+    return BZ_OK;
+  }
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  void* p = nullptr;
+  CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  ctx->d_gbound = static_cast<unsigned long long*>(p);
+  ctx->gbound_ipc = true;
+  return BZ_OK;
+}
+
+int bz_shared_bound_epoch(bz_ctx* ctx, uint32_t epoch) {
+  if (!ctx) return BZ_ERR_ARGUMENT;
+  ctx->gtag = (unsigned long long)(0xffffffffu - epoch) << 32;
+  return BZ_OK;
+}
+
+int bz_shared_bound_read(bz_ctx* ctx, int g, int32_t* out) {
+  if (!ctx || !out) return BZ_ERR_ARGUMENT;
+  if (!ctx->d_gbound) return fail(ctx, BZ_ERR_STATE, "no shared bound mapped");
+  if (g < 1 || g >= kGBoundWords) return fail(ctx, BZ_ERR_ARGUMENT, "g=%d out of range", g);
+  CK(cudaSetDevice(ctx->device));
+  unsigned long long v = 0;
+  CK(cudaMemcpy(&v, ctx->d_gbound + g, sizeof v, cudaMemcpyDeviceToHost));
+  *out = (v >> 32) == (ctx->gtag >> 32) ? (int32_t)(v & 0xffffffffull) : INT32_MAX;
+  return BZ_OK;
+}
+
+int bz_shared_bound_close(bz_ctx* ctx) {
+  if (!ctx) return BZ_ERR_ARGUMENT;
+  if (ctx->device >= 0) cudaSetDevice(ctx->device);
+  if (ctx->gbound_ipc && ctx->d_gbound) cudaIpcCloseMemHandle(ctx->d_gbound);
+  ctx->gbound_ipc = false;
+  ctx->d_gbound = nullptr;
   return BZ_OK;
 }
 

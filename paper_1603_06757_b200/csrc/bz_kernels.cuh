@@ -78,7 +78,36 @@ struct RoundArgs {
                                // after the round tightens this round's start), or null
   int sgroups_cap;             // shared-memory room for this many groups (fused K1
                                // launches stage several plans in turn), 0 = ngroups
+  // Multi-GPU: the running minimum of every round g across all ranks, one
+  // 64-bit word per g in one rank's device memory, mapped into every rank
+  // (CUDA IPC over NVLink) -- kernels RED.MIN their chunk minima into it and
+  // read it for the early exits, so a rank stops as soon as ANY rank has
+  // met the bound.  Words carry the run's tag in their high half (newer
+  // runs have smaller tags and win the min; stale words read as empty).
+  // Null on a single device.
+  unsigned long long* gbound;
+  unsigned long long gtag;     // (0xffffffff - epoch) << 32
 };
+
+// shared-bound helpers (no-ops without a mapped mirror)
+__device__ __forceinline__ int gbound_read(const RoundArgs& a, int g) {
+  if (!a.gbound || g < 1) return INT_MAX;
+  const unsigned long long v = ((volatile unsigned long long*)a.gbound)[g];
+  return (v >> 32) == (a.gtag >> 32) ? (int)(unsigned)(v & 0xffffffffull) : INT_MAX;
+}
+__device__ __forceinline__ void gbound_publish(const RoundArgs& a, int w) {
+  if (a.gbound && w >= 0) atomicMin(a.gbound + a.g, a.gtag | (unsigned long long)(unsigned)w);
+}
+// a round may stop taking work: its own running minimum, any rank's (the
+// shared mirror), or the previous round's (chain / mirror) already meets
+// L_prev -- the run has terminated or this round's result is exactly L_prev
+__device__ __forceinline__ bool round_done(const RoundArgs& a) {
+  if (((volatile const int*)a.bound)[0] <= a.lower_prev) return true;
+  if (a.chain && ((volatile const int*)a.chain)[0] <= a.lower_prev) return true;
+  if (a.gbound && (gbound_read(a, a.g) <= a.lower_prev || gbound_read(a, a.g - 1) <= a.lower_prev))
+    return true;
+  return false;
+}
 
 __host__ __device__ constexpr int padded_words(int w) {
   return w <= 1 ? 1 : (w <= 2 ? 2 : (w <= 4 ? 4 : 8));
@@ -432,7 +461,7 @@ __device__ __forceinline__ void k1_chunks(const RoundArgs& a, const uint32_t* sr
     c = __shfl_sync(FULL, c, 0);
     const unsigned long long chunk = c * (unsigned long long)a.nshards + a.shard;
     if (chunk >= a.nchunks) break;
-    if (vbound[0] <= a.lower_prev) break;
+    if (round_done(a)) break;
 
     const ChunkView v = open_chunk(sgroups, a.ngroups, chunk, lane);
     const long long ca = (v.cnt + 1) >> 1;  // walker A: [first, first+ca)
@@ -473,6 +502,7 @@ __device__ __forceinline__ void k1_chunks(const RoundArgs& a, const uint32_t* sr
       if (wbest != INT_MAX) {
         atomicMin(a.bound + 1 + v.gr.gamma, wbest);
         atomicMin(a.bound, wbest);
+        gbound_publish(a, wbest);
       }
       atomicAdd(a.combos + v.gr.gamma, (unsigned long long)tot * suffix_count<D>(k, e0));
     }

@@ -979,6 +979,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
                 if (wg < ((volatile int*)a.bound)[1 + c.gr.gamma]) {
                   atomicMin(a.bound + 1 + c.gr.gamma, wg);
                   atomicMin(a.bound, wg);
+                  gbound_publish(a, wg);
                 }
               }
             }
@@ -1183,6 +1184,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
           // the epilogue at a chunk boundary
           atomicMin(a.bound + 1 + c.gr.gamma, wbest + gamma_woff(a, c.gr.gamma));
           atomicMin(a.bound, wbest + gamma_woff(a, c.gr.gamma));
+          gbound_publish(a, wbest + gamma_woff(a, c.gr.gamma));
         }
         long long* ct = k4_ctrace(a, qi);
         if (ct && warp == 0) { ct[2] = clock64(); ct[3] = global_ns(); }
@@ -1420,12 +1422,11 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
           // next chunk of this shard, or -1 (done, or U reached L_prev)
           const unsigned long long cidx = atomicAdd(a.counter, 1ull);
           const unsigned long long ch = cidx * (unsigned long long)a.nshards + a.shard;
-          // (a.chain: the previous round of the batch, running concurrently
-          // under programmatic launch -- once its minimum meets this round's
-          // L_prev the run has terminated and this round is not needed)
-          const bool live = vb[0] > a.lower_prev &&
-                            (!a.chain || ((volatile const int*)a.chain)[0] > a.lower_prev);
-          const long long qchunk = (ch < a.nchunks && live) ? (long long)ch : -1;
+          // (round_done: this round's or the previous round's running
+          // minimum -- local, chained, or any rank's through the shared
+          // mirror -- already meets L_prev)
+          (void)vb;
+          const long long qchunk = (ch < a.nchunks && !round_done(a)) ? (long long)ch : -1;
           s_q[qs] = qchunk;
           long long* ct = k4_ctrace(a, qpub);
           if (ct) { ct[0] = qchunk; ct[1] = clock64(); }

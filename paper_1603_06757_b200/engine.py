@@ -95,6 +95,10 @@ class EngineConfig:
     # at once if that U already meets its L (the run had terminated), so a
     # speculative round costs a launch, not its enumeration
     batch_combinations_single: int = 100_000_000_000
+    # multi-GPU: share each round's running minimum across ranks through
+    # peer memory (kernels stop as soon as any rank meets the bound), which
+    # lets the batch run ahead there too
+    shared_bound: bool = True
     engine: str = "auto"     # "auto" | "mxf4q" | "mxf4" | ... | "popc" (kernel; same results)
     elide_identity: bool = True  # drop each full-rank Gamma's identity columns (+g; exact)
 
@@ -165,6 +169,25 @@ class GpuRounds:
         if self.ctx.elision != config.elide_identity:
             self.ctx.set_elision(config.elide_identity)
         self.comm = comm
+        # multi-GPU: the shared bound mirror (rank 0's array, mapped into
+        # every rank over CUDA IPC), set up once per context and world
+        self.shared = False
+        if comm.world > 1 and config.shared_bound:
+            key = ("shared", comm.world)
+            if getattr(self.ctx, "shared_key", None) != key:
+                handle = self.ctx.shared_bound_export() if comm.rank == 0 else None
+                handle = comm.broadcast_bytes(handle)
+                self.ctx.shared_bound_open(None if comm.rank == 0 else handle)
+                self.ctx.shared_key = key
+                self.ctx.shared_epoch = 0
+            self.shared = True
+
+    def begin_run(self) -> None:
+        """A new minimum-distance run: a fresh shared-bound tag (every rank
+        counts its runs alike)."""
+        if self.shared:
+            self.ctx.shared_epoch += 1
+            self.ctx.shared_bound_epoch(self.ctx.shared_epoch)
 
     def load(self, gs: GammaSet, n: int) -> None:
         self.ctx.load(family_words(gs.gammas, n), n)
@@ -231,6 +254,8 @@ def run_rounds(backend, gs: GammaSet, k: int, config: EngineConfig, st: LoopStat
     m_arg, km_arg = line7_args(gs, k)
     m = gs.matrix_count
     batch_ok = config.batch_combinations > 0 and hasattr(backend, "run_batch")
+    if hasattr(backend, "begin_run"):
+        backend.begin_run()
     queued: list = []  # precomputed (g, mins, combos, kernel_ms) of a batch
     while st.g <= k and st.L < st.U:
         if st.g > config.max_g:
@@ -241,8 +266,9 @@ def run_rounds(backend, gs: GammaSet, k: int, config: EngineConfig, st: LoopStat
             # the next rounds whose total size fits the batch budget (per
             # rank: a batch is sharded like a round)
             world = getattr(getattr(backend, "comm", None), "world", 1)
-            budget = (config.batch_combinations * world if world > 1
-                      else max(config.batch_combinations, config.batch_combinations_single))
+            ahead = world == 1 or getattr(backend, "shared", False)
+            budget = (max(config.batch_combinations * world, config.batch_combinations_single)
+                      if ahead else config.batch_combinations * world)
             count, total = 0, 0
             while (st.g + count <= min(k, config.max_g)
                    and total + m * comb(k, st.g + count) <= budget):

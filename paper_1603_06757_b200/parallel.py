@@ -25,6 +25,9 @@ class LocalComm:
     def barrier(self) -> None:
         pass
 
+    def broadcast_bytes(self, data: bytes | None, src: int = 0) -> bytes | None:
+        return data
+
 
 class TorchComm:
     """torch.distributed default group (nccl on GPUs, gloo on CPU)."""
@@ -67,6 +70,12 @@ class TorchComm:
 
     def barrier(self) -> None:
         self._dist.barrier(group=self.group)
+
+    def broadcast_bytes(self, data: bytes | None, src: int = 0) -> bytes:
+        """Rank src's bytes on every rank."""
+        obj = [data if self.rank == src else None]
+        self._dist.broadcast_object_list(obj, src=src, group=self.group)
+        return obj[0]
 
 
 def combine_rounds(comm, res):
