@@ -198,6 +198,9 @@ double binom_d(int p, int q);
 // hold few prefixes (g = 4: one per group), so a K5 launch is all fixed
 // latency (~40 us warm on B200; K1 runs cfg5's g = 4 in 32 us)
 constexpr double kAutoK1Combos = 1e7;
+// sharded calls: rounds below this many combinations x (nshards - 1) run
+// whole on one rank (run_batch)
+constexpr double kOwnWholeCombos = 6e8;
 
 PlanShape pass_shape(int engine, int g, bool hist, int w32 = 0, int m = 0, int k = 0) {
   if (!hist && g >= 4 && engine == BZ_ENGINE_AUTO && m > 0 &&
@@ -809,6 +812,19 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
       ctrace = d_ct;
     }
   }
+  // Sharded calls: a round too small to be worth splitting (its fixed
+  // launch-and-fill latency, ~25 us, exceeds what the split saves) is run
+  // whole by one rank, round-robin over such rounds; the other ranks
+  // report nothing for it (upper / 0), which the exchange's min / sum
+  // absorbs.  Every rank decides alike from (m, k, g, nshards).
+  std::vector<int> owner(count, -1);
+  if (nshards > 1 && !hist) {
+    int owned = 0;
+    const double mult = gamma_only < 0 ? (double)m : 1.0;
+    for (int i = 0; i < count; ++i)
+      if (mult * binom_d(ctx->k, g0 + i) < kOwnWholeCombos * (nshards - 1))
+        owner[i] = owned++ % nshards;
+  }
   const auto t_plan0 = std::chrono::steady_clock::now();
   // plans follow the result records; goff = where round i's groups go
   size_t goff = ((size_t)count * l.off_groups + 255) & ~size_t(255);
@@ -822,7 +838,8 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     int ngroups = 0;
     unsigned long long nchunks = 0;
     const size_t gthis = goff;
-    rc = plan_round(ctx, g, gamma_only, shape, nshards, gthis, &ngroups, &nchunks);
+    const int r_shard = owner[i] >= 0 ? 0 : shard, r_nshards = owner[i] >= 0 ? 1 : nshards;
+    rc = plan_round(ctx, g, gamma_only, shape, r_nshards, gthis, &ngroups, &nchunks);
     if (rc) return rc;
     if (shape.kernel >= 5) {
       // the suffix tables this round's levels read
@@ -857,8 +874,8 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     a.k = ctx->k;
     a.g = g;
     a.n = ctx->n;
-    a.shard = shard;
-    a.nshards = nshards;
+    a.shard = r_shard;
+    a.nshards = r_nshards;
     a.lower_prev = lower_prev ? lower_prev[i] : 0;
     a.elide = ctx->elide_mask;
     a.debug = debug;
@@ -870,7 +887,8 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     a.gbound = gamma_only < 0 ? ctx->d_gbound : nullptr;  // whole rounds only
     a.gtag = ctx->gtag;
     todo[i].shape = shape;
-    todo[i].run = nchunks > 0 && (unsigned long long)shard < nchunks;
+    todo[i].run = nchunks > 0 && (unsigned long long)r_shard < nchunks &&
+                  (owner[i] < 0 || owner[i] == shard);
     goff = (gthis + (size_t)ngroups * sizeof(Group) + 255) & ~size_t(255);
   }
   const auto t_plan1 = std::chrono::steady_clock::now();

@@ -98,6 +98,22 @@ __device__ __forceinline__ int gbound_read(const RoundArgs& a, int g) {
 __device__ __forceinline__ void gbound_publish(const RoundArgs& a, int w) {
   if (a.gbound && w >= 0) atomicMin(a.gbound + a.g, a.gtag | (unsigned long long)(unsigned)w);
 }
+// Round start (one thread of the grid): the running U the previous round
+// ended with -- chained on this device, or any rank's through the shared
+// mirror -- clips this round's bounds, and the mirror word of this round
+// inherits the previous one, so it carries the global running U after
+// round g (what the next round's termination test needs).
+__device__ __forceinline__ void round_start(const RoundArgs& a) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  int u = INT_MAX;
+  if (a.chain) u = ((volatile const int*)a.chain)[0];
+  const int v = gbound_read(a, a.g - 1);
+  if (v < u) u = v;
+  if (u == INT_MAX) return;
+  for (int j = 0; j <= a.m; ++j) atomicMin(a.bound + j, u);
+  if (v < INT_MAX) gbound_publish(a, v);
+}
+
 // a round may stop taking work: its own running minimum, any rank's (the
 // shared mirror), or the previous round's (chain / mirror) already meets
 // L_prev -- the run has terminated or this round's result is exactly L_prev
@@ -517,13 +533,10 @@ k1_round_min(const RoundArgs a) {
   Group* sgroups;
   stage<W>(a, srows, spx, sgroups, smem);
   const unsigned long long* sbinom = smem_binom<W>(smem, a);
-  if (a.chain && threadIdx.x == 0 && blockIdx.x == 0) {
-    // batched round: start from the U the previous round ended with (one
-    // thread of the grid: atomics on one address serialise; blocks that read
-    // the bound before it lands just see the looser start value)
-    const int u = ((volatile const int*)a.chain)[0];
-    for (int j = 0; j <= a.m; ++j) atomicMin(a.bound + j, u);
-  }
+  // batched round: start from the U the previous round ended with (one
+  // thread of the grid: atomics on one address serialise; blocks that read
+  // the bound before it lands just see the looser start value)
+  round_start(a);
   k1_chunks<W, D>(a, srows, spx, sgroups, sbinom);
 }
 
@@ -557,6 +570,7 @@ __global__ void __launch_bounds__(256) k1_rounds(const K1Batch b) {
       for (int i = threadIdx.x; i < gw; i += blockDim.x) gdst[i] = gsrc[i];
       __syncthreads();
     }
+    if (a.gbound) round_start(a);  // (no device chain inside a fused launch)
     k1_chunks<W, D>(a, srows, spx, sgroups, sbinom);
   }
 }

@@ -823,14 +823,10 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
   const unsigned long long* sbinom = smem_binom<W>(smem, a);
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
-  if (a.chain && tid == 0 && blockIdx.x == 0) {
-    // a batched round starts from the U its predecessor ended with (the
-    // running U the reference clips with, m/engine.py:209-211); atomicMin
-    // keeps it race-free against blocks already lowering the bound; one
-    // thread of the grid (atomics on one address serialise)
-    const int u = ((volatile const int*)a.chain)[0];
-    for (int j = 0; j <= a.m; ++j) atomicMin(a.bound + j, u);
-  }
+  // a batched round starts from the U its predecessor ended with (the
+  // running U the reference clips with, m/engine.py:209-211): chained on this
+  // device and/or through the shared mirror (round_start)
+  round_start(a);
   if constexpr (F4) {
     // unit block scales (ue8m0 0x7F = 2^0) in TMEM columns [kSfCol, 512);
     // the zero K-padding chunk of both A buffers (odd W)

@@ -55,20 +55,24 @@ def _worker(rank: int, world: int, port: int, out_dir: str) -> None:
     rep = minimum_distance(G, EngineConfig(device=0, distributed=True))
     out["cfg5/7"] = [rep.distance, [list(t) for t in rep.bounds_trace],
                      rep.counters.combinations]
-    # a shard's view of a batch run far past termination (cfg2 seed 1 ends
-    # at g = 5): the shared mirror stops rounds 6..8 on both ranks at once
+    # cross-rank early exit through the shared mirror, deterministically:
+    # rank 0 runs rounds 1..5 of cfg2 seed 1 (terminated after g = 5: U = 11
+    # <= L = 12), then rank 1 -- which never ran them -- starts rounds 6..8
+    # and must stop them at once, seeing round 5's minimum in the mirror
+    from math import comb
     G, gs, _ = code("cfg2", 1)
     backend = engine.make_backend(EngineConfig(device=0, distributed=True),
                                   engine._make_comm(EngineConfig(distributed=True)))
     backend.load(gs, 96)
     backend.begin_run()
     lps = [0] + [2 * (g + 1) for g in range(1, 8)]
-    res = backend.ctx.rounds(1, lps, 10**6, rank, world)
-    from math import comb
-    out["past_termination_stopped"] = all(
-        sum(c) < 0.05 * comb(48, g) for g, (_, c) in zip(range(6, 9), res[5:]))
-    # every rank reads the global running minima, whichever rank found them
-    # (once both ranks' kernels are done)
+    if rank == 0:
+        backend.ctx.rounds(1, lps[:5], 10**6, 0, 1)
+    dist.barrier()
+    if rank == 1:
+        res = backend.ctx.rounds(6, lps[5:], 10**6, 0, 1)
+        out["stopped_combos"] = [sum(c) for _, c in res]
+    # every rank reads the global running minima (once both are done)
     dist.barrier()
     out["shared_minima"] = [backend.ctx.shared_bound_read(g) for g in range(1, 6)]
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as fh:
@@ -83,6 +87,7 @@ def test_two_ranks_shared_bound(tmp_path, goldens, cfg5_golden):
     world = 2
     mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
     outs = [json.load(open(tmp_path / f"rank{r}.json")) for r in range(world)]
+    stopped = outs[1].pop("stopped_combos")
     assert outs[0] == outs[1]  # every rank holds the same results
     got = outs[0]
     for fx in goldens["configs"]:
@@ -95,7 +100,9 @@ def test_two_ranks_shared_bound(tmp_path, goldens, cfg5_golden):
     assert d == cfg5_golden["distance"]
     assert trace == [list(t) for t in cfg5_golden["bounds_trace"]]
     assert combos == cfg5_golden["combinations"]
-    assert got["past_termination_stopped"]
+    from math import comb
+    for g, c in zip(range(6, 9), stopped):
+        assert c < 0.01 * 2 * comb(48, g), (g, c)
     # cfg2 seed 1: rounds 1, 2, 3 and 5 have minima 16, 15, 12, 11 (round 4's
     # own minimum is only known to be >= 12)
     sm = got["shared_minima"]
