@@ -60,7 +60,7 @@ extern "C" {
 #define BZ_ERR_ARGUMENT 7           /* null pointer, bad shard                   */
 
 /* enumeration engines (bz_set_engine) */
-#define BZ_ENGINE_AUTO 0 /* K5q (W = 1, 3) or K5 for g >= 4, K1 otherwise   */
+#define BZ_ENGINE_AUTO 0 /* K5q (stored weights <= 127) or K5 for g >= 4   */
 #define BZ_ENGINE_POPC 1 /* K1 only: XOR + POPC on the integer pipes       */
 #define BZ_ENGINE_IMMA 2 /* K3 (legacy warp-level IMMA) for g >= 4        */
 #define BZ_ENGINE_UMMA 3 /* K4 (tcgen05.mma kind::i8, TMEM) for g >= 4     */
@@ -68,7 +68,8 @@ extern "C" {
 #define BZ_ENGINE_MXF4P 5 /* K5p: K5 with two codewords per accumulator     \
                              column (stored words W = 1 or 3; else K5)     */
 #define BZ_ENGINE_MXF4T 6 /* K5t: three codewords per column (W = 1, 3)     */
-#define BZ_ENGINE_MXF4Q 7 /* K5q: two codewords as bytes (mxf4nvf4, W = 1, 3) */
+#define BZ_ENGINE_MXF4Q 7 /* K5q: two codewords as bytes (mxf4nvf4; W <= 4,
+                             stored columns <= 127; else K5)              */
 
 typedef struct bz_ctx bz_ctx;
 

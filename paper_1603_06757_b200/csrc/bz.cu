@@ -52,7 +52,7 @@ struct bz_ctx {
   unsigned long long gtag = 0;
 
   // loaded family
-  int m = 0, k = 0, n = 0, w32 = 0, wp = 0;
+  int m = 0, k = 0, n = 0, w32 = 0, wp = 0, n_eff = 0;
   int engine = BZ_ENGINE_AUTO;
   int elision = 1;                   // bz_set_elision (applies at the next load)
   unsigned long long elide_mask = 0; // Gammas loaded with identity columns dropped
@@ -202,7 +202,11 @@ constexpr double kAutoK1Combos = 1e7;
 // whole on one rank (run_batch)
 constexpr double kOwnWholeCombos = 6e8;
 
-PlanShape pass_shape(int engine, int g, bool hist, int w32 = 0, int m = 0, int k = 0) {
+// K5q: stored weights <= 127 (byte fields), W <= 4
+bool k5q_ok(int w32, int n_eff) { return w32 >= 1 && w32 <= 4 && n_eff <= 127; }
+
+PlanShape pass_shape(int engine, int g, bool hist, int w32 = 0, int m = 0, int k = 0,
+                     int n_eff = 0) {
   if (!hist && g >= 4 && engine == BZ_ENGINE_AUTO && m > 0 &&
       binom_d(k, g) * m <= kAutoK1Combos)
     return {1, 32, 0, 1};  // D = 1: many short prefixes keep every warp busy
@@ -211,8 +215,8 @@ PlanShape pass_shape(int engine, int g, bool hist, int w32 = 0, int m = 0, int k
     if (engine == BZ_ENGINE_UMMA) return {3, bz::kUmmaM, bz::kUmmaN, 4};
     const bool packed_ok = w32 == 0 || k5p_ok(w32);
     if (engine == BZ_ENGINE_MXF4T && packed_ok) return {3, bz::kUmmaM, bz::k4_tile_rows<true, 3>(), 7};
-    if (engine == BZ_ENGINE_MXF4Q && packed_ok) return {3, bz::kUmmaM, bz::k4_tile_rows<true, 4>(), 8};
-    if (engine == BZ_ENGINE_AUTO && k5p_ok(w32))
+    const bool q_ok = w32 == 0 || k5q_ok(w32, n_eff);
+    if ((engine == BZ_ENGINE_MXF4Q || engine == BZ_ENGINE_AUTO) && q_ok)
       return {3, bz::kUmmaM, bz::k4_tile_rows<true, 4>(), 8};  // K5q
     if (engine == BZ_ENGINE_MXF4P && packed_ok) return {3, bz::kUmmaM, bz::k4_tile_rows<true, 2>(), 6};
     if (engine == BZ_ENGINE_AUTO || engine == BZ_ENGINE_MXF4 || engine == BZ_ENGINE_MXF4P ||
@@ -743,9 +747,10 @@ int launch_w(bz_ctx* ctx, const RoundArgs& a, bool hist, const PlanShape& shape)
   if constexpr (W == 1 || W == 3) {
     if (shape.kernel == 6) return launch_umma<W, true, 2>(ctx, a);
     if (shape.kernel == 7) return launch_umma<W, true, 3>(ctx, a);
-    if (shape.kernel == 8) return launch_umma<W, true, 4>(ctx, a);
   }
-  if (shape.kernel >= 6) return fail(ctx, BZ_ERR_STATE, "K5p/K5t need W = 1 or 3, not %d", W);
+  if constexpr (W <= 4)
+    if (shape.kernel == 8) return launch_umma<W, true, 4>(ctx, a);
+  if (shape.kernel >= 6) return fail(ctx, BZ_ERR_STATE, "K5p/K5t/K5q do not support W = %d", W);
   if (shape.kernel == 5) return launch_umma<W, true>(ctx, a);
   if (shape.kernel == 4) return launch_umma<W, false>(ctx, a);
   if (shape.kernel == 3) return launch_tc<W>(ctx, a);
@@ -830,7 +835,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   size_t goff = ((size_t)count * l.off_groups + 255) & ~size_t(255);
   for (int i = 0; i < count; ++i) {
     const int g = g0 + i;
-    const PlanShape shape = pass_shape(ctx->engine, g, hist, ctx->w32, ctx->m, ctx->k);
+    const PlanShape shape = pass_shape(ctx->engine, g, hist, ctx->w32, ctx->m, ctx->k, ctx->n_eff);
     if (shape.kernel == 3 || shape.kernel == 4) {
       rc = ensure_triples(ctx, shape.kernel);
       if (rc) return rc;
@@ -1216,6 +1221,7 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
   ctx->n = n;
   ctx->w32 = w32;
   ctx->wp = wp;
+  ctx->n_eff = n_eff;
   ctx->elide_mask = elide;
   return BZ_OK;
 }

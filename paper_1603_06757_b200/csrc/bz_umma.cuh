@@ -727,9 +727,9 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
   constexpr int NC = k5_ncw(CW);  // codewords per accumulator column
   static_assert(!F4 || kUmmaMA == 1, "K5 runs one A tile per B tile");
   static_assert(CW >= 1 && CW <= 4, "kernel form");
-  static_assert(!PR || (F4 && kK5Magic && (W & 1) && W <= 3 && BZ_K5_SPLIT == 1 &&
-                        (CW == 4 || BZ_K5_EPI_GROUPS == 1)),
-                "K5p/K5t: odd W <= 3 (stored weights <= 127 fit the 7-bit fields)");
+  static_assert(!PR || (F4 && kK5Magic && ((W & 1) || CW == 4) && W <= (CW == 4 ? 4 : 3) &&
+                        BZ_K5_SPLIT == 1 && (CW == 4 || BZ_K5_EPI_GROUPS == 1)),
+                "K5p/K5t: odd W <= 3, K5q: W <= 4 (stored weights <= 127 fit the fields)");
   constexpr int N = k4_n<F4, CW>();
   constexpr int TR = k4_tile_rows<F4, CW>();  // table rows per B tile
   constexpr int S = k4_stages<F4, CW>(W);
@@ -844,12 +844,20 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
     if (kK5Magic && tid < (int)kMagicBytes / 16) {
-      // two K-chunks x 8 rows x 16 B per operand; element 0 of every row:
-      // A = 1.5 (0x3), B = 1.0 (0x2); scaled by 2^23 the product is the
-      // 1.5 * 2^23 the accumulators start from
+      // two K-chunks x 8 rows x 16 B per operand (SBO = 0: every 8-row group
+      // reads these rows)
       const int op = tid / 16, row16 = tid % 16;  // row16 < 8: chunk 0
       uint4 z = make_uint4(0, 0, 0, 0);
-      if (row16 < 8) z.x = op == 0 ? 0x3u : 0x2u;
+      if constexpr (Q) {
+        // K5q, even W: the B side of the offset MMAs (the tables carry no
+        // offset chunk): op 0 = [offset pattern, 0] (part a), op 1 =
+        // [0, offset pattern] (part b), against A chunks (pad_a, pad_b)
+        if ((row16 < 8) == (op == 0)) z = k5_table_offset_chunk();
+      } else {
+        // element 0 of every row: A = 1.5 (0x3), B = 1.0 (0x2); scaled by
+        // 2^23 the product is the 1.5 * 2^23 the accumulators start from
+        if (row16 < 8) z.x = op == 0 ? 0x3u : 0x2u;
+      }
       *reinterpret_cast<uint4*>(sMagic + op * 256 + row16 * 16) = z;
       fence_proxy_async();
     }
@@ -1337,6 +1345,20 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
                   // so it meets offset chunk q
                   const uint32_t dj = dbase;
                   const uint64_t adj = a_desc0 + (uint64_t)(ab * (TA >> 4));
+                  if constexpr (Q && !(W & 1)) {
+                    // K5q, even W: W/2 data MMAs per part, then one offset MMA
+                    // of A chunks (pad_a, pad_b) against a constant B
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                      const uint64_t bdq = bd0 + (uint64_t)(q * (N / 8) * CB * 8);
+#pragma unroll
+                      for (int kb = 0; kb < W / 2; ++kb)
+                        umma_nvf4(dj, adj + 16u * kb, bdq + 16u * kb, IDESC, (q | kb) ? 1u : 0u,
+                                  sfa, q ? sfm : sfb);
+                      umma_nvf4(dj, adj + 16u * (W / 2), q ? magic_b : magic_a, IDESC, 1u,
+                                q ? sfp : sfa, q ? sfm : sfb);
+                    }
+                  } else
 #pragma unroll
                   for (int q = 0; q < NC; ++q) {
                     const uint64_t bdq = bd0 + (uint64_t)(q * (N / 8) * CB * 8);
