@@ -176,6 +176,29 @@ def other_seeds(args, cfg, local, flush) -> dict:
     return out
 
 
+def section6_c1(cfg) -> dict:
+    """Side measurement: the paper's new code C1 = [234,51] (section 6;
+    generator from tests/golden/section6_codes.json, built by the reference
+    package) to its exact distance through minimum_distance, wall time
+    (one warm-up run first)."""
+    from paper_1603_06757_b200 import BitMatrix, minimum_distance
+
+    path = os.path.join(ROOT, "tests", "golden", "section6_codes.json")
+    if not os.path.exists(path):
+        return {"skipped": "tests/golden/section6_codes.json missing"}
+    with open(path) as fh:
+        fx = [c for c in json.load(fh)["codes"] if c["name"] == "C1"][0]
+    G = BitMatrix([int(r, 16) for r in fx["rows"]], fx["n"])
+    minimum_distance(G, cfg)
+    t0 = time.perf_counter()
+    rep = minimum_distance(G, cfg)
+    dt = time.perf_counter() - t0
+    return {"code": f"[{fx['n']},{fx['k']}]", "d": rep.distance, "paper_d": fx["paper_d"],
+            "status": rep.status, "g_final": rep.g_reached,
+            "combinations": rep.counters.combinations, "wall_s": round(dt, 3),
+            "value": rep.counters.combinations / dt, "unit": UNIT}
+
+
 def cpu_baseline(G, gs, sample_g: int) -> dict:
     """Oracle (C restatement of enumerate_stack) on all host cores over one
     bounded sample: every g-combination of Gamma_1 at g = sample_g."""
@@ -468,6 +491,7 @@ def main():
     }
     if args.config == "cfg5" and not args.no_extra and world == 1:
         line["cfg5_other_seeds"] = other_seeds(args, cfg, local, flush)
+        line["section6_C1"] = section6_c1(cfg)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(G, gs, args.cpu_sample_g)
     print(json.dumps(line), flush=True)

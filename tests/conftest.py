@@ -60,3 +60,11 @@ def cfg5_traces():
     if g is None:
         pytest.skip("cfg5 seed traces not generated yet")
     return g
+
+
+@pytest.fixture(scope="session")
+def section6():
+    g = load_json("section6_codes.json")
+    if g is None:
+        pytest.skip("section-6 codes not generated yet")
+    return g
