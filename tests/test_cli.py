@@ -79,3 +79,33 @@ def test_brute(goldens, tmp_path, capsys):
     assert cli.main(["brute", "--in", str(path)]) == cli.EXIT_OK
     assert f"distance={fx['distance']}" in capsys.readouterr().out
     assert cli.main(["brute", "--in", str(path), "--max-k", "10"]) == cli.EXIT_TOO_LARGE
+
+
+def test_construct_script(tmp_path, section6):
+    """`construct` builds C3 = extend([234,51]) from a script with the
+    paper's polynomials, bit-identical to the reference's matrix; script
+    errors map to the reference's exit codes."""
+    from conftest import hexrows
+    from paper_1603_06757_b200 import cli
+    from paper_1603_06757_b200.gf2 import read_matrix_file
+
+    m = section6["m"]
+    f2 = "116," + ",".join(str(e) for e in range(115, -1, -1))  # (x^117-1)/(x+1) = all ones
+    script = tmp_path / "c3.txt"
+    script.write_text("# section 6, C3\n"
+                      f"m = {m}\n"
+                      f"f1 = {','.join(map(str, section6['f1_exps']))}\n"
+                      f"f2 = {f2}\n"
+                      f"p = {','.join(map(str, section6['p1_exps']))}\n"
+                      "extend\n")
+    out = tmp_path / "c3.mat"
+    assert cli.main(["construct", "--in", str(script), "--out", str(out), "--quiet"]) == 0
+    G = read_matrix_file(str(out))
+    fx = [c for c in section6["codes"] if c["name"] == "C3"][0]
+    assert (G.num_cols, G.num_rows) == (fx["n"], fx["k"])
+    assert list(G.rows) == hexrows(fx["rows"])
+    bad = tmp_path / "bad.txt"
+    bad.write_text("m = 7\nf1 = 2,1,0\nf2 = 0\np = 0\n")
+    assert cli.main(["construct", "--in", str(bad), "--quiet"]) == cli.EXIT_NOT_A_DIVISOR
+    bad.write_text("m = 7\nbogus = 1\n")
+    assert cli.main(["construct", "--in", str(bad), "--quiet"]) == cli.EXIT_SCRIPT
