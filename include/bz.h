@@ -43,17 +43,19 @@
 extern "C" {
 #endif
 
-#define BZ_ABI_VERSION 10
+#define BZ_ABI_VERSION 11
 
 /* limits of the device kernels */
 #define BZ_MAX_K 128 /* rows per Gamma (prefix masks are 128-bit)      */
-#define BZ_MAX_N 256 /* columns: 8 x 32-bit words per row              */
+#define BZ_MAX_N 384 /* columns of the uploaded rows (k + 256 at most)   */
+#define BZ_MAX_N_STORED 256 /* columns a Gamma keeps on the device after
+                               identity-column elision: 8 x 32-bit words  */
 
 /* status codes */
 #define BZ_OK 0
 #define BZ_ERR_INVALID_ARITY 1      /* g outside 1..k        -> InvalidArity      */
 #define BZ_ERR_INVALID_DIMENSIONS 2 /* bad m/k/n/padding     -> InvalidDimensions */
-#define BZ_ERR_TOO_LARGE 3          /* k>128, n>256, C(k,g) >= 2^62 -> TooLarge  */
+#define BZ_ERR_TOO_LARGE 3          /* k>128, n>384, >256 stored columns, C(k,g) >= 2^62 -> TooLarge  */
 #define BZ_ERR_CUDA 4               /* CUDA runtime failure                      */
 #define BZ_ERR_NO_DEVICE 5          /* no sm_100 device visible                  */
 #define BZ_ERR_STATE 6              /* no Gamma loaded / bad gamma index         */

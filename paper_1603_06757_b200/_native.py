@@ -18,7 +18,7 @@ from .errors import (DeviceError, InvalidArity, InvalidDimensions, MindistError,
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BZ_LIB") or os.path.join(PKG_DIR, "libbz.so")
-ABI_VERSION = 10
+ABI_VERSION = 11
 
 BZ_OK = 0
 _CODES = {

@@ -1173,6 +1173,10 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
     for (int w = 0; w < w64; ++w) cnt += __builtin_popcountll(km[w]);
     n_eff = std::max(n_eff, cnt);
   }
+  if (n_eff > BZ_MAX_N_STORED)
+    return fail(ctx, BZ_ERR_TOO_LARGE,
+                "a Gamma keeps %d columns on the device (limit %d; identity columns of a "
+                "systematic Gamma are not stored)", n_eff, BZ_MAX_N_STORED);
   const int w32 = (n_eff + 31) / 32;
   const int wp = bz::padded_words(w32);
   // repack the kept columns to padded 32-bit rows, build prefix-XOR tables
@@ -1306,7 +1310,8 @@ int bz_brute_force(bz_ctx* ctx, const uint64_t* rows, int k, int n, int max_k,
   if (ctx->device < 0) return fail(ctx, BZ_ERR_NO_DEVICE, "context has no device");
   if (!rows || !out_distance) return fail(ctx, BZ_ERR_ARGUMENT, "null argument");
   if (k < 1 || n < 1) return fail(ctx, BZ_ERR_INVALID_DIMENSIONS, "need k, n >= 1");
-  if (n > BZ_MAX_N) return fail(ctx, BZ_ERR_TOO_LARGE, "n=%d exceeds %d", n, BZ_MAX_N);
+  if (n > BZ_MAX_N_STORED)
+    return fail(ctx, BZ_ERR_TOO_LARGE, "brute force: n=%d exceeds %d", n, BZ_MAX_N_STORED);
   const int cap = std::min(max_k, bz::kBruteMaxK);
   if (k > cap)
     return fail(ctx, BZ_ERR_TOO_LARGE, "brute force limited to k <= %d (got %d)", cap, k);

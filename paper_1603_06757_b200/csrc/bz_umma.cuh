@@ -74,6 +74,9 @@ constexpr int kUmmaM = 128;       // prefixes per A tile = producer threads
 #ifndef BZ_K5_NOFENCE
 #define BZ_K5_NOFENCE 0  // timing experiment only: drops the per-tile tcgen05 fences
 #endif
+#ifndef BZ_K5_EVEN_F32
+#define BZ_K5_EVEN_F32 0  // K5, even W: f32 accumulators instead of the offset MMA
+#endif
 #ifndef BZ_K5_MAGIC
 #define BZ_K5_MAGIC 1
 #endif
@@ -727,6 +730,8 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
   constexpr int NC = k5_ncw(CW);  // codewords per accumulator column
   static_assert(!F4 || kUmmaMA == 1, "K5 runs one A tile per B tile");
   static_assert(CW >= 1 && CW <= 4, "kernel form");
+  // offset accumulators (packed s16 epilogue) for this instantiation
+  constexpr bool MG = kK5Magic && (CW > 1 || (W & 1) || !BZ_K5_EVEN_F32);
   static_assert(!PR || (F4 && kK5Magic && ((W & 1) || CW == 4) && W <= (CW == 4 ? 4 : 3) &&
                         BZ_K5_SPLIT == 1 && (CW == 4 || BZ_K5_EPI_GROUPS == 1)),
                 "K5p/K5t: odd W <= 3, K5q: W <= 4 (stored weights <= 127 fit the fields)");
@@ -843,7 +848,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
                                                 : 0x7F7F7F7Fu));
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
-    if (kK5Magic && tid < (int)kMagicBytes / 16) {
+    if (MG && tid < (int)kMagicBytes / 16) {
       // two K-chunks x 8 rows x 16 B per operand (SBO = 0: every 8-row group
       // reads these rows)
       const int op = tid / 16, row16 = tid % 16;  // row16 < 8: chunk 0
@@ -1066,7 +1071,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
             const uint32_t m = __vmins2(m0, m1);
             const int lo = (int)(m & 0xffffu), hi = (int)(m >> 16) - 0x4B00;
             rmin[0] = min(rmin[0], min(lo, hi));
-          } else if constexpr (F4 && kK5Magic) {
+          } else if constexpr (F4 && MG) {
             // EC accumulators as packed s16 pairs (low halves of 1.5*2^23 + D)
             constexpr int NP = EC / 2;
             uint32_t v[NP];
@@ -1171,7 +1176,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
           }
           if (warp == 0 && lane == 0) k4_trace(a, 3, tcount, toff);
         }
-        if constexpr (F4 && !kK5Magic) {
+        if constexpr (F4 && !MG) {
           // |D| <= n, so a finite minimum converts exactly; +inf (every
           // column of this slice masked) stays out of the way
           if (fmin_acc < 1.0e6f) rmin[0] = (int)fmin_acc;
@@ -1378,7 +1383,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
                   for (int j = 0; j < kUmmaMA; ++j) {
                     const uint32_t dj = dbase + (uint32_t)(j * N + h * NH);
                     const uint64_t adj = a_desc0 + (uint64_t)((ab * kUmmaMA + j) * (TA >> 4));
-                    constexpr bool kExtra = F4 && kK5Magic && !k5_padmagic(W);
+                    constexpr bool kExtra = F4 && MG && !k5_padmagic(W);
                     if constexpr (kExtra) umma_mxf4(dj, magic_a, magic_b, IDESC, 0u, sfm, sfb);
 #pragma unroll
                     for (int kb = 0; kb < P; ++kb) {

@@ -190,6 +190,43 @@ def test_too_large(ctx):
         enumerate_gpu(M, 40)
 
 
+_WIDE: dict = {}
+
+
+@pytest.mark.parametrize("k,n", [(28, 280), (32, 288), (36, 290)])
+def test_codes_wider_than_256(k, n, engine):
+    """n up to 384: every Gamma keeps n - k <= 256 columns after identity
+    elision (the remainder Gamma too), so the device rows still fit 8 words."""
+    rng = random.Random(1000 * k + n)
+    rows = [rng.getrandbits(n) for _ in range(k)]
+    if (k, n) not in _WIDE:  # the C oracle, once per code (~5 s for k = 36)
+        _WIDE[(k, n)] = oracle.minimum_distance(rows, n)
+    want = _WIDE[(k, n)]
+    try:
+        rep = minimum_distance(BitMatrix(rows, n), EngineConfig(engine=engine))
+    except TooLarge:
+        if engine in ("umma", "imma"):  # legacy s8 engines: W = 8 tiles + m Gammas
+            pytest.skip("staged rows and tiles exceed shared memory")  # fail loudly, not wrong
+        raise
+    assert rep.distance == want["distance"]
+    assert rep.bounds_trace == [tuple(t) for t in want["bounds_trace"]]
+    assert (rep.m, rep.k_m) == (want["m"], want["k_m"])
+    assert rep.counters.combinations == want["combinations"]
+
+
+def test_stored_columns_limit():
+    """More than 256 stored columns, or n > 384, fail loudly."""
+    rng = random.Random(5)
+    rows = [rng.getrandbits(290) for _ in range(28)]  # n - k = 262 stored
+    with pytest.raises(TooLarge):
+        minimum_distance(BitMatrix(rows, 290))
+    rows = [rng.getrandbits(400) for _ in range(128)]
+    with pytest.raises(TooLarge):
+        minimum_distance(BitMatrix(rows, 400))
+    with pytest.raises(TooLarge):  # not systematic: every column is stored
+        enumerate_gpu(BitMatrix([rng.getrandbits(300) for _ in range(20)], 300), 2)
+
+
 @pytest.mark.parametrize("k,n,g", [(4, 9, 4), (5, 40, 4), (128, 256, 4), (100, 200, 5),
                                    (40, 224, 6), (30, 33, 7)])
 def test_tensor_engine_shapes(k, n, g, engine):
