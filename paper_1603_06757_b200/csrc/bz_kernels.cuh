@@ -352,6 +352,32 @@ __device__ __forceinline__ unsigned long long* smem_binom(unsigned char* smem, c
       kSBinomBytes);
 }
 
+// dst[i] = load(i) for i < n, block-strided, 8 loads in flight per thread
+template <typename Load, typename T>
+__device__ __forceinline__ void stage_copy(int n, Load&& load, T* dst) {
+  constexpr int U = 8;
+  for (int base = threadIdx.x; base < n; base += U * blockDim.x) {
+    T t[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * (int)blockDim.x;
+      if (i < n) t[u] = load(i);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * (int)blockDim.x;
+      if (i < n) dst[i] = t[u];
+    }
+  }
+}
+
+// the round's work plan into shared memory
+__device__ __forceinline__ void stage_groups(const RoundArgs& a, Group* sgroups) {
+  const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(a.groups);
+  stage_copy(a.ngroups * (int)(sizeof(Group) / 4), [&](int i) { return gsrc[i]; },
+             reinterpret_cast<uint32_t*>(sgroups));
+}
+
 template <int W>
 __device__ __forceinline__ void stage(const RoundArgs& a, uint32_t*& srows,
                                       uint32_t*& spx, Group*& sgroups,
@@ -365,27 +391,21 @@ __device__ __forceinline__ void stage(const RoundArgs& a, uint32_t*& srows,
   spx = srows + nrow_words;
   size_t off = ((size_t)(nrow_words + npx_words) * 4 + 15) & ~size_t(15);
   sgroups = reinterpret_cast<Group*>(smem + off);
-  // the loops are unrolled so several global loads are in flight per
-  // thread: a load-store-load chain would pay one L2 round trip per word
-  // and made the prologue of a short launch cost microseconds
-#pragma unroll 8
-  for (int i = threadIdx.x; i < nrow_words; i += blockDim.x) srows[i] = a.rows[i];
-#pragma unroll 8
-  for (int i = threadIdx.x; i < npx_words; i += blockDim.x) {
+  // every copy issues 8 predicated loads per thread before its stores: a
+  // load-store chain (what a bounds-checked unrolled loop compiles to) pays
+  // one L2 round trip per element and made short launches' prologues cost
+  // microseconds
+  stage_copy(nrow_words, [&](int i) { return a.rows[i]; }, srows);
+  stage_copy(npx_words, [&](int i) {
     const int r = i / PS, j = i - r * PS;
-    spx[i] = j < W ? a.px[r * WP + j] : 0u;
-  }
-  const int gw = a.ngroups * (int)(sizeof(Group) / 4);
-  const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(a.groups);
-  uint32_t* gdst = reinterpret_cast<uint32_t*>(sgroups);
-#pragma unroll 8
-  for (int i = threadIdx.x; i < gw; i += blockDim.x) gdst[i] = gsrc[i];
+    return j < W ? a.px[r * WP + j] : 0u;
+  }, spx);
+  stage_groups(a, sgroups);
   unsigned long long* sb = smem_binom<W>(smem, a);
-#pragma unroll 8
-  for (int i = threadIdx.x; i < kMaxK * (kSBinomQ + 1); i += blockDim.x) {
+  stage_copy(kMaxK * (kSBinomQ + 1), [&](int i) {
     const int c = i / (kSBinomQ + 1), j = i - c * (kSBinomQ + 1);
-    sb[i] = a.binom[c * kBinomDim + j];
-  }
+    return a.binom[c * kBinomDim + j];
+  }, sb);
   __syncthreads();
 }
 
@@ -461,7 +481,11 @@ __device__ __forceinline__ ChunkView open_chunk(const Group* sg, int ngroups,
 // every broadcast row load feeds two codewords (and two independent
 // XOR/POPC chains).  When the range is odd the second walker duplicates the
 // first on the last step -- harmless for a minimum.
-template <int W, int D>
+// Chunks are dealt by an atomic cursor (long rounds: uneven prefix walks
+// balance themselves), or -- kStatic, the fused small rounds, about one
+// chunk per warp -- round-robin by global warp index: there a returning
+// atomic on one address per warp and round was the kernel's main stall.
+template <int W, int D, bool kStatic = false>
 __device__ __forceinline__ void k1_chunks(const RoundArgs& a, const uint32_t* srows,
                                           const uint32_t* spx, const Group* sgroups,
                                           const unsigned long long* sbinom) {
@@ -469,12 +493,18 @@ __device__ __forceinline__ void k1_chunks(const RoundArgs& a, const uint32_t* sr
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int k = a.k, q = a.g - 1 - D;
-  volatile int* vbound = a.bound;
 
+  const unsigned long long nwarps = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+  unsigned long long c_next = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   while (true) {
     unsigned long long c = 0;
-    if (lane == 0) c = atomicAdd(a.counter, 1ull);
-    c = __shfl_sync(FULL, c, 0);
+    if constexpr (kStatic) {
+      c = c_next;
+      c_next += nwarps;
+    } else {
+      if (lane == 0) c = atomicAdd(a.counter, 1ull);
+      c = __shfl_sync(FULL, c, 0);
+    }
     const unsigned long long chunk = c * (unsigned long long)a.nshards + a.shard;
     if (chunk >= a.nchunks) break;
     if (round_done(a)) break;
@@ -563,15 +593,11 @@ __global__ void __launch_bounds__(256) k1_rounds(const K1Batch b) {
     const RoundArgs& a = b.a[r];
     if (r > 0) {
       __syncthreads();  // every warp is done with round r-1's plan
-      const int gw = a.ngroups * (int)(sizeof(Group) / 4);
-      const uint32_t* gsrc = reinterpret_cast<const uint32_t*>(a.groups);
-      uint32_t* gdst = reinterpret_cast<uint32_t*>(sgroups);
-#pragma unroll 8
-      for (int i = threadIdx.x; i < gw; i += blockDim.x) gdst[i] = gsrc[i];
+      stage_groups(a, sgroups);
       __syncthreads();
     }
     if (a.gbound) round_start(a);  // (no device chain inside a fused launch)
-    k1_chunks<W, D>(a, srows, spx, sgroups, sbinom);
+    k1_chunks<W, D, true>(a, srows, spx, sgroups, sbinom);
   }
 }
 
