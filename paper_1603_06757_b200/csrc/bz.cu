@@ -545,9 +545,10 @@ int launch_k1_fused(bz_ctx* ctx, const RoundArgs* as, int count) {
   bz::K1Batch b{};
   int cap = 0;
   unsigned long long warps = 0;
-  for (int i = 0; i < count; ++i) {
-    cap = std::max(cap, as[i].ngroups);
-    warps = std::max(warps, (as[i].nchunks + as[i].nshards - 1) / as[i].nshards);
+  for (int i = 0; i < count; ++i) {  // the plans side by side, one chunk space
+    cap += as[i].ngroups;
+    if (as[i].nchunks > (unsigned long long)as[i].shard)
+      warps += (as[i].nchunks - as[i].shard + as[i].nshards - 1) / as[i].nshards;
   }
   for (int i = 0; i < count; ++i) {
     b.a[i] = as[i];
@@ -928,10 +929,15 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     ctx->pdl_next = prev_round && !debug;
     // consecutive small K1 rounds of the same depth share one launch
     int f = 1;
+    size_t fused_groups = (size_t)todo[i].a.ngroups;
     while (!hist && todo[i].shape.kernel == 1 && f < bz::kK1MaxFused && i + f < count &&
            todo[i + f].run && todo[i + f].shape.kernel == 1 &&
-           todo[i + f].shape.depth == todo[i].shape.depth && !debug && i + f != big)
+           todo[i + f].shape.depth == todo[i].shape.depth && !debug && i + f != big &&
+           (fused_groups + todo[i + f].a.ngroups) * sizeof(bz::Group) <=
+               (size_t)bz::kK1FusedGroupBytes) {
+      fused_groups += todo[i + f].a.ngroups;
       ++f;
+    }
     if (f > 1) {
       std::vector<RoundArgs> as;
       for (int q = 0; q < f; ++q) as.push_back(todo[i + q].a);

@@ -481,34 +481,17 @@ __device__ __forceinline__ ChunkView open_chunk(const Group* sg, int ngroups,
 // every broadcast row load feeds two codewords (and two independent
 // XOR/POPC chains).  When the range is odd the second walker duplicates the
 // first on the last step -- harmless for a minimum.
-// Chunks are dealt by an atomic cursor (long rounds: uneven prefix walks
-// balance themselves), or -- kStatic, the fused small rounds, about one
-// chunk per warp -- round-robin by global warp index: there a returning
-// atomic on one address per warp and round was the kernel's main stall.
-template <int W, int D, bool kStatic = false>
-__device__ __forceinline__ void k1_chunks(const RoundArgs& a, const uint32_t* srows,
-                                          const uint32_t* spx, const Group* sgroups,
-                                          const unsigned long long* sbinom) {
+// One chunk (a warp's share of the plan) of round a.
+template <int W, int D>
+__device__ __forceinline__ void k1_chunk(const RoundArgs& a, unsigned long long chunk,
+                                         const uint32_t* srows, const uint32_t* spx,
+                                         const Group* sgroups, const unsigned long long* sbinom) {
   constexpr int WP = padded_words(W);
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
   const int k = a.k, q = a.g - 1 - D;
 
-  const unsigned long long nwarps = (unsigned long long)gridDim.x * (blockDim.x >> 5);
-  unsigned long long c_next = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  while (true) {
-    unsigned long long c = 0;
-    if constexpr (kStatic) {
-      c = c_next;
-      c_next += nwarps;
-    } else {
-      if (lane == 0) c = atomicAdd(a.counter, 1ull);
-      c = __shfl_sync(FULL, c, 0);
-    }
-    const unsigned long long chunk = c * (unsigned long long)a.nshards + a.shard;
-    if (chunk >= a.nchunks) break;
-    if (round_done(a)) break;
-
+  {
     const ChunkView v = open_chunk(sgroups, a.ngroups, chunk, lane);
     const long long ca = (v.cnt + 1) >> 1;  // walker A: [first, first+ca)
     const long long cb = v.cnt - ca;        // walker B: [first+ca, first+cnt)
@@ -555,6 +538,21 @@ __device__ __forceinline__ void k1_chunks(const RoundArgs& a, const uint32_t* sr
   }
 }
 
+// Chunks dealt by an atomic cursor: uneven prefix walks balance themselves.
+template <int W, int D>
+__device__ __forceinline__ void k1_chunks(const RoundArgs& a, const uint32_t* srows,
+                                          const uint32_t* spx, const Group* sgroups,
+                                          const unsigned long long* sbinom) {
+  while (true) {
+    unsigned long long c = 0;
+    if ((threadIdx.x & 31) == 0) c = atomicAdd(a.counter, 1ull);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    const unsigned long long chunk = c * (unsigned long long)a.nshards + a.shard;
+    if (chunk >= a.nchunks || round_done(a)) break;
+    k1_chunk<W, D>(a, chunk, srows, spx, sgroups, sbinom);
+  }
+}
+
 template <int W, int D>
 __global__ void __launch_bounds__(256)
 k1_round_min(const RoundArgs a) {
@@ -571,12 +569,15 @@ k1_round_min(const RoundArgs a) {
 }
 
 // Several small rounds (same family, same suffix depth) in one launch: the
-// rows, prefix table and binomials are staged once, each round's work plan
-// in turn; a block moves to round r+1 once round r's chunk cursor is
-// exhausted, so the rounds overlap across blocks.  (No device-side U chain
-// between them: bz_rounds clips each round's minima to its predecessor's U
-// on the host, which gives the same results.)
+// rows, prefix table and binomials are staged once, every round's work plan
+// side by side, and the rounds' chunks form one space dealt round-robin by
+// global warp index (about one chunk per warp: a returning atomic cursor per
+// warp and round was this kernel's main stall), so the rounds run
+// concurrently.  (No device-side U chain between them: bz_rounds clips each
+// round's minima to its predecessor's U on the host, which gives the same
+// results.)
 constexpr int kK1MaxFused = 4;
+constexpr int kK1FusedGroupBytes = 64 * 1024;  // shared-memory budget for the plans
 struct K1Batch {
   RoundArgs a[kK1MaxFused];
   int count;
@@ -587,17 +588,39 @@ __global__ void __launch_bounds__(256) k1_rounds(const K1Batch b) {
   extern __shared__ __align__(128) unsigned char smem[];
   uint32_t *srows, *spx;
   Group* sgroups;
-  stage<W>(b.a[0], srows, spx, sgroups, smem);
+  stage<W>(b.a[0], srows, spx, sgroups, smem);  // round 0's plan at sgroups
   const unsigned long long* sbinom = smem_binom<W>(smem, b.a[0]);
-  for (int r = 0; r < b.count; ++r) {
-    const RoundArgs& a = b.a[r];
-    if (r > 0) {
-      __syncthreads();  // every warp is done with round r-1's plan
-      stage_groups(a, sgroups);
-      __syncthreads();
+  int goff[kK1MaxFused];
+  unsigned long long cend[kK1MaxFused];  // this shard's chunks of rounds <= r
+  unsigned long long total = 0;
+  int go = 0;
+#pragma unroll
+  for (int r = 0; r < kK1MaxFused; ++r) {
+    if (r < b.count) {
+      const RoundArgs& a = b.a[r];
+      goff[r] = go;
+      if (r > 0) stage_groups(a, sgroups + go);
+      go += a.ngroups;
+      const unsigned long long mine =
+          a.nchunks > (unsigned long long)a.shard
+              ? (a.nchunks - a.shard + a.nshards - 1) / a.nshards : 0ull;
+      total += mine;
+      cend[r] = total;
+      if (a.gbound) round_start(a);
     }
-    if (a.gbound) round_start(a);  // (no device chain inside a fused launch)
-    k1_chunks<W, D, true>(a, srows, spx, sgroups, sbinom);
+  }
+  __syncthreads();
+  const unsigned long long nwarps = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+  for (unsigned long long c = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       c < total; c += nwarps) {
+    int r = 0;
+#pragma unroll
+    for (int i = 0; i + 1 < kK1MaxFused; ++i)
+      if (i + 1 < b.count && c >= cend[i]) r = i + 1;
+    const RoundArgs& a = b.a[r];
+    const unsigned long long local = c - (r > 0 ? cend[r - 1] : 0ull);
+    if (round_done(a)) continue;
+    k1_chunk<W, D>(a, local * a.nshards + a.shard, srows, spx, sgroups + goff[r], sbinom);
   }
 }
 
