@@ -610,6 +610,9 @@ __global__ void __launch_bounds__(256) k1_rounds(const K1Batch b) {
     }
   }
   __syncthreads();
+  // the next round kernel (a programmatic dependent) may take SMs as these
+  // blocks retire
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const unsigned long long nwarps = (unsigned long long)gridDim.x * (blockDim.x >> 5);
   for (unsigned long long c = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
        c < total; c += nwarps) {
