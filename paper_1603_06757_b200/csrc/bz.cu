@@ -197,7 +197,10 @@ double binom_d(int p, int q);
 // AUTO keeps K1 (D = 1) for rounds this small: their tensor-core groups
 // hold few prefixes (g = 4: one per group), so a K5 launch is all fixed
 // latency (~40 us warm on B200; K1 runs cfg5's g = 4 in 32 us)
-constexpr double kAutoK1Combos = 1e7;
+#ifndef BZ_AUTO_K1_COMBOS
+#define BZ_AUTO_K1_COMBOS 1e7
+#endif
+constexpr double kAutoK1Combos = BZ_AUTO_K1_COMBOS;
 // sharded calls: rounds below this many combinations x (nshards - 1) run
 // whole on one rank (run_batch)
 constexpr double kOwnWholeCombos = 6e8;
