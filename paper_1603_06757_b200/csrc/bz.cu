@@ -197,6 +197,12 @@ double binom_d(int p, int q);
 // AUTO keeps K1 (D = 1) for rounds this small: their tensor-core groups
 // hold few prefixes (g = 4: one per group), so a K5 launch is all fixed
 // latency (~40 us warm on B200; K1 runs cfg5's g = 4 in 32 us)
+// K4 / K5 chunk size: ~kK5ChunksPerCta chunks per persistent CTA, and at
+// least kK5LaneMin prefixes x suffix rows per lane (a chunk costs a walker
+// unrank per producer thread).  Swept on config 5 (tools/_lm.sh): 16 / 4096
+// -> 11 / 8192 takes ~1 % off a run (g = 5..7 launches; g = 8 unchanged).
+constexpr long long kK5ChunksPerCta = 11;
+constexpr long long kK5LaneMin = 8192;
 #ifndef BZ_AUTO_K1_COMBOS
 #define BZ_AUTO_K1_COMBOS 1e7
 #endif
@@ -363,11 +369,14 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
   long long lane_target = (long long)(total / (32ull * kChunksTarget));
   lane_target = std::min(kLaneMax, std::max(kLaneMin, lane_target));
   if (shape.kernel >= 4) {
-    // K4 / K5: one persistent CTA per SM walks ~16 chunks; a chunk costs a walker
-    // unrank per producer thread, so chunks are large
-    lane_target = (long long)(total / ((unsigned long long)shape.lanes * 148ull * 16ull *
+    // K4 / K5: one persistent CTA per SM walks ~kK5ChunksPerCta chunks; a
+    // chunk costs a walker unrank per producer thread, so chunks are large
+    lane_target = (long long)(total / ((unsigned long long)shape.lanes * 148ull *
+                                       (unsigned long long)kK5ChunksPerCta *
                                        (unsigned long long)std::max(1, nshards)));
-    lane_target = std::min(1ll << 20, std::max(4096ll, lane_target));
+    long long lane_min = kK5LaneMin;
+    if (const char* lm = getenv("BZ_K5_LANE_MIN")) lane_min = atoll(lm);
+    lane_target = std::min(1ll << 20, std::max(lane_min, lane_target));
     if (const char* sc = getenv("BZ_K5_CHUNK_SCALE")) lane_target = (long long)(lane_target * atof(sc));
   }
   // suffix levels: K5 may split the round over depths 3..5, every other
@@ -454,10 +463,11 @@ int plan_round(bz_ctx* ctx, int g, int gamma_only, PlanShape shape, int nshards,
   const char* floors = getenv("BZ_K5_FLOORS");
   const char* scale = getenv("BZ_K5_CHUNK_SCALE");
   const char* cost = getenv("BZ_K5_COST");
-  char key[320];
-  snprintf(key, sizeof key, "%d/%d/%d/%d/%d/%d/%d/%d/%d/%s/%s/%s", ctx->m, ctx->k, g, gamma_only,
+  const char* lmin = getenv("BZ_K5_LANE_MIN");
+  char key[384];
+  snprintf(key, sizeof key, "%d/%d/%d/%d/%d/%d/%d/%d/%d/%s/%s/%s/%s", ctx->m, ctx->k, g, gamma_only,
            shape.kernel, shape.depth, shape.lanes, shape.tile_rows, nshards, floors ? floors : "",
-           scale ? scale : "", cost ? cost : "");
+           scale ? scale : "", cost ? cost : "", lmin ? lmin : "");
   const IoSlot l = io_layout(ctx->m, ctx->k);
   std::lock_guard<std::mutex> lock(mu);
   auto it = memo.find(key);
