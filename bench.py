@@ -3,7 +3,7 @@
 Workload (BASELINE.json configs[4], the config its scaling target names):
 the random binary [160,80] code of seed 7 (SURVEY.md Appendix A generator,
 2 full information sets), full Brouwer-Zimmermann from g = 1 until L >= U
-(d = 18 at g = 8, 6.5e10 combinations).  One *step* is one such run.
+(d = 17 at g = 8, 6.5e10 combinations).  One *step* is one such run.
 
   value  -- combinations/s of the rounds with the Gamma family resident in
             HBM (device-timed with CUDA events on the library's stream, one
@@ -15,15 +15,21 @@ the random binary [160,80] code of seed 7 (SURVEY.md Appendix A generator,
             minima and counters, timed by the host clock.
   roofline -- the dominant kernel (the g = 8 round, K5q = tcgen05.mma
             kind::mxf4nvf4, two codewords as bytes of one fp32 TMEM
-            accumulator): achieved combos/s vs the live fp4 MAC rate /
-            (64*ceil(W/2)) MACs per combination; "k5p_mxf4", "k5_mxf4",
-            "k4_umma_i8", "k3_imma" and "k1_popc" report the other kernels on
-            the same launch against their own live rooflines.
+            accumulator) against the live fp4 MAC rate: `frac` per
+            ALGORITHMIC MACs (the stored columns of a codeword, 80 for config
+            5), `frac_issued` per MACs the kernel issues (its padded K plus
+            the offset chunks, 128); "k5_mxf4" and "k1_popc" time the other
+            two kernels of the library on the same launch.
+  cfg4   -- BASELINE.json configs[3]: all C(64,6) six-row combinations of a
+            64x192 [I | A], minimum (K5q) and the 193-bin weight histogram
+            (K1h), each against its roofline.
   cpu_baseline -- the C oracle (oracle/, a restatement of the reference's
             enumerate_stack) on all host cores over a bounded sample.
 
-  python bench.py [--gpus N --steps K --warmup W]       (torchrun for N > 1)
-  python bench.py --impl reference                      (CPU reference arm)
+  python bench.py [--gpus N --steps K --warmup W]   (N > 1: one rank per GPU,
+                                                     spawned through torchrun
+                                                     unless already under it)
+  python bench.py --impl reference                  (CPU reference arm)
 """
 
 from __future__ import annotations
@@ -31,6 +37,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -42,6 +49,9 @@ sys.path.insert(0, ROOT)
 METRIC = "codeword combinations (XOR+popcount)/s, full BZ to d"
 UNIT = "combinations/s"
 WORKLOAD = "cfg5 random [160,80] seed 7, full BZ to d (g=1..8)"
+# BASELINE.json configs (name -> k, n, (full-rank count, remainder rank), default seed)
+CODES = {"cfg1": (24, 48, (2, 0), 1), "cfg2": (48, 96, (2, 0), 1),
+         "cfg3": (40, 100, (2, 20), 1), "cfg5": (80, 160, (2, 0), 7)}
 
 
 def parse():
@@ -50,11 +60,14 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--config", default="cfg5", choices=("cfg1", "cfg2", "cfg3", "cfg5"))
+    ap.add_argument("--config", default="cfg5", choices=tuple(CODES))
     ap.add_argument("--seed", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-extra", action="store_true", help="skip the other-seed side runs")
+    ap.add_argument("--no-extra", action="store_true", help="skip the side measurements")
     ap.add_argument("--cpu-sample-g", type=int, default=7)
+    ap.add_argument("--ref-python-max-g", type=int, default=5,
+                    help="reference arm: rounds of the reference package's own run")
+    ap.add_argument("--cpu-selftest", action="store_true", help=argparse.SUPPRESS)
     return ap.parse_args()
 
 
@@ -63,6 +76,28 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(args) -> int:
+    """`--gpus N` without a torchrun environment: launch N ranks of this
+    script through torchrun (one process per GPU, 127.0.0.1 rendezvous) and
+    pass their output through; rank 0 prints the JSON line.  NCCL reports
+    its communicator setup (NCCL_DEBUG=INFO, INIT subsystem) unless the
+    caller chose otherwise."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ)
+    if not args.cpu_selftest:
+        env.setdefault("NCCL_DEBUG", "INFO")
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
 
 
 class ClockSampler:
@@ -199,6 +234,71 @@ def section6_c1(cfg) -> dict:
             "value": rep.counters.combinations / dt, "unit": UNIT}
 
 
+def issued_macs(w: int) -> int:
+    """MACs per combination the K5 family issues for W stored 32-bit words:
+    ceil(W/2) K = 64 MMAs (the A/table offset chunk rides in the padding of
+    the last one for odd W), plus one offset MMA for even W -- per codeword
+    for K5 (one per accumulator column) and for K5q (two per column, two
+    parts)."""
+    return 64 * ((w + 1) // 2) + (64 if w % 2 == 0 else 0)
+
+
+def cfg4_side(ctx, peaks, seed: int = 1) -> dict:
+    """BASELINE.json configs[3]: the fixed-r microbenchmark.  All C(64,6) =
+    74,974,368 six-row combinations of random_systematic_matrix(64, 192, 1)
+    = [I_64 | A], no early exit: the minimum on the default engine (K5q:
+    128 stored columns after identity elision, two codewords per
+    accumulator) and the 193-bin weight histogram (K1h: XOR+POPC with
+    per-thread shared-memory bins), device-timed (median of 5 after one
+    warm-up), against their rooflines.  Reference: enumerate_saved /
+    enumerate_parallel on the same Gamma (m/enumeration.py:305-313,
+    :385-444), 3.6 s on one core."""
+    import hashlib
+
+    import numpy as np
+
+    from paper_1603_06757_b200.configs import microbench_gamma
+    from paper_1603_06757_b200.enumeration import family_words
+
+    gm = microbench_gamma(seed)
+    n, k, g = gm.num_cols, gm.num_rows, 6
+    ctx.set_engine("auto")
+    ctx.load(family_words([gm], n), n)
+    stored = n - k if ctx.elided() & 1 else n
+    w_st = (stored + 31) // 32
+    ms_min, ms_hist = [], []
+    for rep in range(6):
+        mn, combos = ctx.enumerate(0, g)
+        if rep:
+            ms_min.append(ctx.last_kernel_ms())
+    for rep in range(6):
+        hist, hmn, hcombos = ctx.histogram(0, g)
+        if rep:
+            ms_hist.append(ctx.last_kernel_ms())
+    t_min, t_hist = statistics.median(ms_min), statistics.median(ms_hist)
+    sha = hashlib.sha256(np.asarray(hist, dtype="<u8").tobytes()).hexdigest()
+    r_min = combos / (t_min * 1e-3)
+    r_hist = hcombos / (t_hist * 1e-3)
+    issued = issued_macs(w_st)
+    mac = peaks["mxf4_mac_per_s"]
+    popc_peak = peaks["popc_per_s"] / w_st
+    return {
+        "workload": "random_systematic_matrix(64,192,1), all C(64,6) combinations, no early exit",
+        "combinations": combos, "min": mn, "hist_sha256": sha,
+        "hist_checksum_ok": sha == "8d397da157d31b1e67746a3a522b01cb624e4d54d42a27b6fbd403a6da02252b",
+        "stored_columns": stored,
+        "min_k5q": {"ms": t_min, "value": r_min, "unit": UNIT,
+                    "roofline_peak": mac / stored, "frac": r_min / (mac / stored),
+                    "frac_issued": r_min / (mac / issued),
+                    "note": f"algorithmic MACs = {stored} stored columns per combination; "
+                            f"issued = {issued} (K5q, even W: one offset MMA per part)"},
+        "histogram_k1h": {"ms": t_hist, "value": r_hist, "unit": UNIT,
+                          "roofline_peak": popc_peak, "frac": r_hist / popc_peak,
+                          "note": f"POPC roofline / {w_st} words per stored codeword"},
+        "reference_1core_s": 3.6,
+    }
+
+
 def cpu_baseline(G, gs, sample_g: int) -> dict:
     """Oracle (C restatement of enumerate_stack) on all host cores over one
     bounded sample: every g-combination of Gamma_1 at g = sample_g."""
@@ -214,21 +314,54 @@ def cpu_baseline(G, gs, sample_g: int) -> dict:
                       f"(min {mn}) in {dt:.2f} s, oracle/bz_oracle.c on {threads} threads"}
 
 
+def reference_python(rows: list[int], n: int, max_g: int) -> dict:
+    """The reference package itself (baseline/_ref, installed from
+    /root/reference/pkg; pure Python + numpy) on the same code:
+    minimum_distance(G, EngineConfig(strategy="saved", s=3, workers=W))
+    (m/engine.py:57-67, :157-220) over rounds g <= max_g, W = 1 and W = all
+    host cores.  Its rounds past max_g take hours."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "mindist")):
+        return {"unavailable": "baseline/_ref is not installed"}
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    from mindist.engine import EngineConfig as RefConfig
+    from mindist.engine import minimum_distance as ref_md
+    from mindist.gf2 import BitMatrix as RefMatrix
+
+    cores = len(os.sched_getaffinity(0))
+    out = {"package": "mindist 0.1.0 (baseline/_ref)", "rounds": f"g<={max_g}"}
+    for w in sorted({1, cores}):
+        t0 = time.perf_counter()
+        rep = ref_md(RefMatrix(list(rows), n),
+                     RefConfig(strategy="saved", s=3, workers=w, max_g=max_g))
+        dt = time.perf_counter() - t0
+        out[f"workers_{w}"] = {"value": rep.counters.combinations / dt, "unit": UNIT,
+                               "s": round(dt, 3), "combinations": rep.counters.combinations,
+                               "bounds_trace": [list(t) for t in rep.bounds_trace]}
+    out["cores"] = cores
+    return out
+
+
 def reference_arm(args):
+    """The CPU reference arm: the oracle port of the reference's path
+    (oracle/bz_oracle.c, enumerate_stack on all host threads inside the
+    Algorithm-1 loop) on the SAME workload as the GPU arm -- every round of
+    full BZ to d.  The input is drawn by oracle.draw_code (no product
+    package import).  Under torchrun only rank 0 runs; the GPU count only
+    labels the line."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     from oracle import oracle
-    from paper_1603_06757_b200.configs import code
 
-    G, gs, _ = code(args.config, args.seed)
+    k, n, target, seed0 = CODES[args.config]
+    seed = seed0 if args.seed is None else args.seed
+    rows = oracle.draw_code(k, n, seed, target)
     threads = oracle.max_threads()
-    # one step = rounds g <= 7 of the same workload (bounded CPU sample)
-    sample_max_g = 7 if args.config == "cfg5" else 16
 
     def step():
-        return oracle.minimum_distance(list(G.rows), G.num_cols, threads=threads,
-                                       max_g=sample_max_g)
+        return oracle.minimum_distance(rows, n, threads=threads)
 
     for _ in range(args.warmup):
         step()
@@ -240,28 +373,73 @@ def reference_arm(args):
         combos += rep["combinations"]
     total = sum(times)
     value = combos / total
+    workload = WORKLOAD if args.config == "cfg5" else f"{args.config} seed {seed}, full BZ to d"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": WORKLOAD if args.config == "cfg5" else args.config,
-                   "sample": f"rounds g<={sample_max_g} per step"},
+        "config": {"workload": workload, "k": k, "n": n, "d": rep["distance"],
+                   "g_final": rep["g_reached"],
+                   "combinations_per_step": rep["combinations"]},
+        "wall_time_to_d_s": total / args.steps,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"oracle/bz_oracle.c BZ rounds g<={sample_max_g} of "
-                                   f"{args.config} ({rep['combinations']} combinations/step)"},
+                         "sample": f"oracle/bz_oracle.c (enumerate_stack restated in C, "
+                                   f"pthreads) full BZ to d of {workload}: "
+                                   f"{rep['combinations']} combinations per step"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_extra:
+        line["reference_python"] = reference_python(rows, n, args.ref_python_max_g)
     print(json.dumps(line), flush=True)
+
+
+def cpu_selftest(args):
+    """Hidden CPU mode for tests/test_bench_launch.py: the rank launcher,
+    barriers, max-over-ranks timing and the JSON contract on gloo, with a
+    fixed host-side step instead of the device rounds."""
+    rank, world, _ = dist_env()
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    steps_ms = []
+    for i in range(args.warmup + args.steps):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        time.sleep(0.002 * (1 + rank))
+        if i >= args.warmup:
+            steps_ms.append((time.perf_counter() - t0) * 1e3)
+    ms = sum(steps_ms)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": world * args.steps / (ms * 1e-3),
+                          "unit": "steps/s", "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": ms / args.steps,
+                          "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                          "selftest": True}), flush=True)
 
 
 def main():
     args = parse()
+    rank, world, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if args.cpu_selftest:
+        cpu_selftest(args)
+        return
     if args.impl == "reference":
         reference_arm(args)
         return
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
 
-    rank, world, local = dist_env()
     import torch
 
     distributed = world > 1
@@ -272,7 +450,6 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1603_06757_b200 import EngineConfig, _native, engine, minimum_distance
     from paper_1603_06757_b200.configs import code
-    from paper_1603_06757_b200.enumeration import family_words
 
     G, gs, _ = code(args.config, args.seed)
     k, n, m = G.num_rows, G.num_cols, gs.matrix_count
@@ -370,28 +547,25 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (largest round), and the other two
-    # kernels on the same launch for comparison
-    # words per stored row: identity-column elision drops k columns of every
-    # Gamma that has a unit column per row (all of them for config 5), so the
-    # kernels run on W_eff = ceil((n - k) / 32) words -- the rooflines below
-    # use that as their own denominator
+    # ---- roofline of the dominant kernel (largest round), and the other
+    # kernels of the library on the same launch for comparison
     peaks = ctx.measure_int_peaks(w_eff)
     top_ms = statistics.median(g_top_ms)
     achieved = (g_top_combos / world) / (top_ms * 1e-3)
-    # MACs per combination: the K of the weight GEMM, i.e. the padded stored
-    # row -- K4 (kind::i8) 32 per word, K5 (kind::mxf4) K = 64 steps
-    macs_i8 = 32 * w_eff
-    macs_f4 = 64 * ((w_eff + 1) // 2)
-    macs_f4_full = 64 * ((w32 + 1) // 2)
-    mxf4_peak = peaks["mxf4_mac_per_s"] / macs_f4
-    umma_peak = peaks["umma_mac_per_s"] / macs_i8
-    imma_peak = peaks["imma_mac_per_s"] / macs_i8
+    q_kernel = w_eff <= 4 and n_eff <= 128
+    # MACs per combination: algorithmic = the stored columns of one codeword
+    # (its dot product, SURVEY.md 8(d) with identity elision); issued = the
+    # K the kernel runs (issued_macs)
+    macs_alg = n_eff
+    macs_issued = issued_macs(w_eff)
+    mac_rate = peaks["mxf4_mac_per_s"]
+    peak_alg = mac_rate / macs_alg
+    peak_issued = mac_rate / macs_issued
     popc_peak = peaks["popc_per_s"] / w_eff
     g_top = max(st.rounds, key=lambda r: r.combinations).g
 
-    def engine_rate(engine):
-        ctx.set_engine(engine)
+    def engine_rate(engine_name):
+        ctx.set_engine(engine_name)
         ms = []
         for _ in range(2):
             ctx.round(g_top, 0, 1 << 30, local, world)
@@ -400,16 +574,14 @@ def main():
         return (g_top_combos / world) / (min(ms) * 1e-3)
 
     k5_achieved = engine_rate("mxf4")
-    k5p_achieved = engine_rate("mxf4p")
     k1_achieved = engine_rate("popc")
-    k3_achieved = engine_rate("imma")
-    k4_achieved = engine_rate("umma")
-    # the same K5 launch without elision (full n-column rows)
+    # the same launch without elision (full n-column rows)
     ctx.set_elision(False)
     backend.load(gs, n)
-    k5_full = engine_rate(cfg.engine)
-    w_full = w32  # without elision: K5p only for odd W <= 3, else K5
-    full_kernel = "K5q" if w_full in (1, 3) else "K5"
+    full_rate = engine_rate(cfg.engine)
+    w_full = w32
+    full_kernel = "K5q" if (w_full <= 4 and n <= 128) else "K5"
+    macs_full_issued = issued_macs(w_full)
     ctx.set_elision(True)
     backend.load(gs, n)
     traffic = None
@@ -417,11 +589,16 @@ def main():
     if os.path.exists(prof):
         with open(prof) as fh:
             traffic = json.load(fh).get("dram_bytes_per_launch")
+    kname = (f"k4_round_umma<{w_eff},true,4> = K5q, round g={g_top} (tcgen05.mma "
+             f"kind::mxf4nvf4 block16, two codewords as bytes of one fp32 accumulator)"
+             if q_kernel else
+             f"k4_round_umma<{w_eff},true,1> = K5, round g={g_top} (tcgen05.mma kind::mxf4)")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "e2m1 tensor (fp32 acc) / u32", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "e2m1 tensor (fp32 acc) / u32", "data": "synthetic",
         "config": {"workload": WORKLOAD if args.config == "cfg5" else args.config,
                    "k": k, "n": n, "m": m, "d": rep.distance, "g_final": rep.g_reached,
                    "combinations_per_step": int(combos_all / args.steps),
@@ -429,59 +606,41 @@ def main():
                    "identity_elision": bool(mask),
                    "parallelism": f"rank-space shards x{world}",
                    "l2": "flushed (256 MiB memset) before every timed step; working set "
-                         "(rows, prefix table, triple tables) is L2/shared-memory resident"},
+                         "(rows, prefix table, suffix tables) is L2/shared-memory resident"},
         "wall_time_to_d_s": e2e_s,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "wall_s": e2e_s},
         "gpu_launches": launches,
+        "gpu_launches_per_step": launches / args.steps,
         "clocks": clock,
-        "roofline": {"bound": "tensor", "achieved": achieved / 1e9, "peak": mxf4_peak / 1e9,
-                     "unit": "Gcombinations/s", "frac": achieved / mxf4_peak,
+        "roofline": {"bound": "tensor", "achieved": achieved / 1e9, "peak": peak_alg / 1e9,
+                     "unit": "Gcombinations/s", "frac": achieved / peak_alg,
+                     "frac_issued": achieved / peak_issued,
+                     "macs_per_combination": {"algorithmic": macs_alg, "issued": macs_issued},
                      "traffic": traffic,
-                     "kernel": (f"k4_round_umma<{w_eff},true,4> = K5q, round g={g_top} "
-                                f"(tcgen05.mma kind::mxf4nvf4 block16, two codewords as bytes "
-                                f"of one fp32 accumulator)"
-                                if w_eff in (1, 3) else
-                                f"k4_round_umma<{w_eff},true,1> = K5, round g={g_top} "
-                                f"(tcgen05.mma kind::mxf4, unit block scales)"),
+                     "kernel": kname,
                      "peak_source": f"live microbenchmark: tcgen05.mma kind::mxf4 M128xN240xK64 "
                                     f"{peaks['mxf4_mac_per_clk_sm']:.0f} MACs/clk/SM, "
-                                    f"{peaks['mxf4_mac_per_s'] / 1e15:.2f} PMAC/s / "
-                                    f"{macs_f4} MACs per combination (stored K = "
-                                    f"{32 * w_eff} padded to 64)",
+                                    f"{mac_rate / 1e15:.2f} PMAC/s / {macs_alg} algorithmic "
+                                    f"MACs per combination (the stored columns; the kernel "
+                                    f"issues {macs_issued})",
                      "popc_roofline": popc_peak / 1e9,
                      "frac_of_popc_roofline": achieved / popc_peak,
                      "identity_elision": {
                          "on": bool(mask), "gamma_mask": mask, "stored_columns": n_eff,
                          "words": w_eff,
                          "note": "rows of Gammas with a unit column per row are stored without "
-                                 "those k columns and every weight gets +g (exact); rooflines "
-                                 "use the stored K as their denominator"},
+                                 "those k columns and every weight gets +g (exact)"},
                      "without_elision": {
-                         "kernel": full_kernel,
-                         "achieved": k5_full / 1e9,
-                         "peak": peaks["mxf4_mac_per_s"] / macs_f4_full / 1e9,
-                         "frac": k5_full / (peaks["mxf4_mac_per_s"] / macs_f4_full),
-                         "macs_per_combination": macs_f4_full}},
-        "k5p_mxf4": {"kernel": f"k4_round_umma<{w_eff},true,2> round g={g_top} "
-                               f"(kind::mxf4, two codewords as 16-bit fields)",
-                     "achieved": k5p_achieved / 1e9, "peak": mxf4_peak / 1e9,
-                     "unit": "Gcombinations/s", "frac": k5p_achieved / mxf4_peak},
+                         "kernel": full_kernel, "achieved": full_rate / 1e9,
+                         "peak": mac_rate / n / 1e9, "frac": full_rate / (mac_rate / n),
+                         "frac_issued": full_rate / (mac_rate / macs_full_issued),
+                         "macs_per_combination": {"algorithmic": n,
+                                                  "issued": macs_full_issued}}},
         "k5_mxf4": {"kernel": f"k4_round_umma<{w_eff},true,1> round g={g_top} "
                               f"(tcgen05.mma kind::mxf4, one codeword per accumulator)",
-                    "achieved": k5_achieved / 1e9, "peak": mxf4_peak / 1e9,
-                    "unit": "Gcombinations/s", "frac": k5_achieved / mxf4_peak},
-        "k4_umma_i8": {"kernel": f"k4_round_umma<{w_eff},false> round g={g_top} "
-                                 f"(tcgen05.mma kind::i8)",
-                       "achieved": k4_achieved / 1e9, "peak": umma_peak / 1e9,
-                       "unit": "Gcombinations/s", "frac": k4_achieved / umma_peak,
-                       "peak_source": f"live microbenchmark: {peaks['umma_mac_per_clk_sm']:.0f} "
-                                      f"MACs/clk/SM / {macs_i8} MACs per combination"},
-        "k3_imma": {"kernel": f"k3_round_gemm<{w_eff}> round g={g_top} (legacy mma.sync s8)",
-                    "achieved": k3_achieved / 1e9, "peak": imma_peak / 1e9,
-                    "unit": "Gcombinations/s", "frac": k3_achieved / imma_peak,
-                    "peak_source": f"live microbenchmark: {peaks['imma_mac_per_clk_sm']:.0f} "
-                                   f"IMMA MACs/clk/SM / {macs_i8} MACs per combination"},
+                    "achieved": k5_achieved / 1e9, "peak": peak_alg / 1e9,
+                    "unit": "Gcombinations/s", "frac": k5_achieved / peak_alg},
         "k1_popc": {"kernel": f"k1_round_min<{w_eff},2> round g={g_top} (XOR+POPC)",
                     "achieved": k1_achieved / 1e9, "peak": popc_peak / 1e9,
                     "unit": "Gcombinations/s", "frac": k1_achieved / popc_peak,
@@ -489,9 +648,14 @@ def main():
                                    f" / {w_eff} POPC per combination",
                     "alu_peak": peaks["lop3_per_s"] / (2 * w_eff) / 1e9},
     }
+    rounds = [{"g": r.g, "combinations": r.combinations, "kernel_ms": r.kernel_ms}
+              for r in st.rounds]
+    line["rounds"] = rounds
     if args.config == "cfg5" and not args.no_extra and world == 1:
         line["cfg5_other_seeds"] = other_seeds(args, cfg, local, flush)
         line["section6_C1"] = section6_c1(cfg)
+        line["cfg4"] = cfg4_side(ctx, peaks)
+        backend.load(gs, n)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(G, gs, args.cpu_sample_g)
     print(json.dumps(line), flush=True)

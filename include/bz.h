@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define BZ_ABI_VERSION 11
+#define BZ_ABI_VERSION 12
 
 /* limits of the device kernels */
 #define BZ_MAX_K 128 /* rows per Gamma (prefix masks are 128-bit)      */
@@ -62,8 +62,10 @@ extern "C" {
 #define BZ_ERR_ARGUMENT 7           /* null pointer, bad shard                   */
 
 /* enumeration engines (bz_set_engine) */
-#define BZ_ENGINE_AUTO 0 /* K5q (stored weights <= 127) or K5 for g >= 4   */
+#define BZ_ENGINE_AUTO 0 /* K5q (stored weights <= 128) or K5 for g >= 4   */
 #define BZ_ENGINE_POPC 1 /* K1 only: XOR + POPC on the integer pipes       */
+/* 2, 3, 5, 6: round-1 comparison kernels, built only with
+ * -DBZ_LEGACY_KERNELS=1 (bz_set_engine fails with BZ_ERR_ARGUMENT otherwise) */
 #define BZ_ENGINE_IMMA 2 /* K3 (legacy warp-level IMMA) for g >= 4        */
 #define BZ_ENGINE_UMMA 3 /* K4 (tcgen05.mma kind::i8, TMEM) for g >= 4     */
 #define BZ_ENGINE_MXF4 4 /* K5 (tcgen05.mma kind::mxf4, unit scales) g >= 4 */
@@ -71,7 +73,7 @@ extern "C" {
                              column (stored words W = 1 or 3; else K5)     */
 #define BZ_ENGINE_MXF4T 6 /* K5t: three codewords per column (W = 1, 3)     */
 #define BZ_ENGINE_MXF4Q 7 /* K5q: two codewords as bytes (mxf4nvf4; W <= 4,
-                             stored columns <= 127; else K5)              */
+                             stored columns <= 128; else K5)              */
 
 typedef struct bz_ctx bz_ctx;
 
@@ -118,12 +120,6 @@ int bz_reduce_on_columns(uint64_t *rows, int k, int n, const int32_t *cols, int 
 int bz_gamma_family(const uint64_t *rows, int k, int n, int m_max, uint64_t *out_rows,
                     int32_t *out_pivots, int32_t *out_ranks, int *out_m);
 
-/* Identity-column elision (default on; applies from the next
- * bz_load_gammas): a Gamma with one unit column per row -- every full-rank
- * information set from build_gamma_set (m/gf2.py:133-199) -- is stored
- * without those k columns and its weights get + g, which is exact because
- * each chosen row carries exactly one of them.  The remainder Gamma (rank <
- * k) keeps all n columns.  Results are identical either way. */
 /* Multi-GPU shared bound (one process per GPU).  Rank 0 allocates the
  * mirror and exports a 64-byte CUDA IPC handle (bz_shared_bound_export),
  * every rank opens it (rank 0 with handle = NULL, i.e. its own array), and
@@ -140,7 +136,23 @@ int bz_shared_bound_epoch(bz_ctx *ctx, uint32_t epoch);
 int bz_shared_bound_read(bz_ctx *ctx, int g, int32_t *out);
 int bz_shared_bound_close(bz_ctx *ctx);
 
+/* Identity-column elision (default on; applies from the next
+ * bz_load_gammas): a Gamma with one unit column per row is stored without
+ * those k columns and its weights get + g, which is exact because each
+ * chosen row carries exactly one of them.  That covers every Gamma from
+ * build_gamma_set (m/gf2.py:133-199), the rank-deficient remainder too: it
+ * spans the row space of G and keeps the earlier passes' pivots as unit
+ * columns.  The test is made per Gamma at load time (bz_elided reports it).
+ * Results are identical either way. */
 int bz_set_elision(bz_ctx *ctx, int on);
+
+/* In-round early exit (default off): a round stops taking work once its
+ * running minimum meets lower_prev.  Results and the bounds trace are the
+ * same either way; only the `combinations` counts of such rounds drop below
+ * the reference's m*C(k,g).  Batched rounds past termination (the previous
+ * round's U already <= lower_prev) stop at once in both modes; the caller
+ * discards them. */
+int bz_set_early_exit(bz_ctx *ctx, int on);
 
 /* Bit j set: Gamma j of the loaded family was stored with its identity
  * columns dropped. */
@@ -160,10 +172,12 @@ int bz_load_gammas(bz_ctx *ctx, const uint64_t *rows, int m, int k, int n);
  * loaded Gamma_j and report, per Gamma, min(true minimum weight, upper)
  * in out_min[j] and the number of combinations visited in out_combos[j].
  *
- * lower_prev is the certified lower bound before this round; the kernel
- * stops early only once the running minimum reaches lower_prev (then the
- * round's result is exactly lower_prev, as in the reference trace).  Pass
- * lower_prev = 0 to disable early exit.
+ * lower_prev is the certified lower bound before this round.  With the
+ * in-round early exit on (bz_set_early_exit) the kernel stops once the
+ * running minimum reaches lower_prev (the round's result is then exactly
+ * lower_prev, as in the reference trace, but fewer combinations are
+ * visited); off (the default) every combination is visited, as the
+ * reference does.
  *
  * shard/nshards split the round's work into nshards disjoint parts (one
  * per GPU/process); nshards = 1 is the whole round.  Results of the shards
@@ -247,6 +261,13 @@ int bz_launch_count(bz_ctx *ctx, uint64_t *out);
  * (M=128, N=240, K=64, unit block scales) MACs per second, out[13] = its
  * MACs per clock per SM.  `out` must hold 14 doubles. */
 int bz_measure_int_peaks(bz_ctx *ctx, int w_words, double *out);
+
+/* Host-only self-check of the K5q offset encoding (no device needed): the
+ * kernel's producer threshold and e2m1 offset blocks over every prefix
+ * weight 0..128 and bound -4..128 must stay in range and dot to their
+ * integers exactly.  Returns the number of failures (0 = ok); the first
+ * failing (prefix weight, bound) goes to out_bad[0..1] (may be NULL). */
+int bz_k5q_selftest(int32_t *out_bad);
 
 #ifdef __cplusplus
 }

@@ -175,6 +175,26 @@ def gamma_family(rows: list[int], n: int):
     return gammas, pivsets, full, rem
 
 
+def draw_code(k: int, n: int, seed: int, target: tuple[int, int]) -> list[int]:
+    """Rows of SURVEY.md Appendix A's seeded draw, restated here so that
+    bench.py's CPU arm builds its input without the product package:
+    ``random.Random(seed)``, one ``getrandbits(n)`` per row, the whole matrix
+    redrawn (same RNG stream) until the information-set family has
+    ``target`` = (full-rank count, remainder rank).  Equal to
+    ``paper_1603_06757_b200.configs.draw_code`` (tests/test_oracle.py)."""
+    import random
+
+    rng = random.Random(seed)
+    while True:
+        rows = [rng.getrandbits(n) for _ in range(k)]
+        try:
+            _, _, full, rem = gamma_family(rows, n)
+        except ValueError:  # rank deficient
+            continue
+        if (full, rem) == tuple(target):
+            return rows
+
+
 def minimum_distance(rows: list[int], n: int, threads: int = 0, max_g: int = 16,
                      start_g: int = 1, start_upper: int | None = None,
                      round_fn=None) -> dict:

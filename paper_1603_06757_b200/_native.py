@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import threading
 
 import numpy as np
 
@@ -18,7 +19,7 @@ from .errors import (DeviceError, InvalidArity, InvalidDimensions, MindistError,
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BZ_LIB") or os.path.join(PKG_DIR, "libbz.so")
-ABI_VERSION = 11
+ABI_VERSION = 12
 
 BZ_OK = 0
 _CODES = {
@@ -33,7 +34,7 @@ _CODES = {
 
 # every symbol include/bz.h declares (checked by tests/test_abi.py)
 SYMBOLS = ("bz_abi_version", "bz_device_count", "bz_create", "bz_destroy",
-           "bz_last_error", "bz_set_engine", "bz_set_elision", "bz_elided",
+           "bz_last_error", "bz_set_engine", "bz_set_elision", "bz_set_early_exit", "bz_elided",
            "bz_reduce_on_columns", "bz_brute_force", "bz_load_gammas",
            "bz_round", "bz_rounds",
            "bz_enumerate",
@@ -41,7 +42,8 @@ SYMBOLS = ("bz_abi_version", "bz_device_count", "bz_create", "bz_destroy",
            "bz_last_kernel_ms", "bz_round_ms", "bz_gamma_family",
            "bz_shared_bound_export", "bz_shared_bound_open", "bz_shared_bound_epoch",
            "bz_shared_bound_read",
-           "bz_shared_bound_close", "bz_launch_count", "bz_measure_int_peaks")
+           "bz_shared_bound_close", "bz_launch_count", "bz_measure_int_peaks",
+           "bz_k5q_selftest")
 
 _lib = None
 
@@ -70,6 +72,8 @@ def lib():
     L.bz_last_error.restype = ctypes.c_char_p
     L.bz_set_engine.argtypes = [vp, c_int]
     L.bz_set_elision.argtypes = [vp, c_int]
+    L.bz_set_early_exit.argtypes = [vp, c_int]
+    L.bz_k5q_selftest.argtypes = [i32p]
     L.bz_brute_force.argtypes = [vp, u64p, c_int, c_int, c_int, i32p, u64p]
     L.bz_reduce_on_columns.argtypes = [u64p, c_int, c_int, i32p, c_int, i32p, ctypes.POINTER(c_int)]
     L.bz_elided.argtypes = [vp, u64p]
@@ -113,6 +117,14 @@ def check(rc: int, ctx=None, what: str = "") -> None:
     raise exc(f"{what}: {msg}" if what else msg)
 
 
+def k5q_selftest() -> tuple[int, tuple[int, int] | None]:
+    """Host-only check of the K5q offset encoding (bz_k5q_selftest):
+    (failures, first failing (prefix weight, bound) or None)."""
+    bad = np.zeros(2, dtype=np.int32)
+    n = int(lib().bz_k5q_selftest(_ptr(bad, ctypes.c_int32)))
+    return n, (int(bad[0]), int(bad[1])) if n else None
+
+
 def device_count() -> int:
     return int(lib().bz_device_count())
 
@@ -151,6 +163,12 @@ class Context:
         self.device = device
         self.engine = "auto"
         self.elision = True
+        self.early_exit = False
+        # a context is not thread-safe (include/bz.h): callers hold this
+        # across a whole load + rounds sequence (minimum_distance,
+        # enumerate_gpu, ...), so concurrent calls on distinct matrices
+        # never interleave each other's loads
+        self.lock = threading.RLock()
         self.loaded_key = None
         self.m = self.k = self.n = 0
 
@@ -219,6 +237,13 @@ class Context:
         check(lib().bz_set_elision(self.handle, 1 if on else 0), self.handle, "bz_set_elision")
         self.elision = bool(on)
         self.loaded_key = None
+
+    def set_early_exit(self, on: bool) -> None:
+        """In-round early exit at lower_prev (see bz_set_early_exit)."""
+        if bool(on) != self.early_exit:
+            check(lib().bz_set_early_exit(self.handle, 1 if on else 0), self.handle,
+                  "bz_set_early_exit")
+            self.early_exit = bool(on)
 
     def elided(self) -> int:
         """Bit mask of the loaded Gammas stored without identity columns."""

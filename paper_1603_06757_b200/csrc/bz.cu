@@ -24,7 +24,14 @@
 
 #include "../../include/bz.h"
 #include "bz_kernels.cuh"
-#include "bz_tc.cuh"
+// Comparison kernels of the round-1 evolution (K3 legacy mma.sync IMMA, K4
+// tcgen05 kind::i8, K5p / K5t packed variants) are not part of the product
+// library; build with -DBZ_LEGACY_KERNELS=1 (tools/build_legacy.sh) to get
+// them back for A/B measurements.
+#ifndef BZ_LEGACY_KERNELS
+#define BZ_LEGACY_KERNELS 0
+#endif
+#include "bz_tc.cuh"  // K3 is only instantiated with BZ_LEGACY_KERNELS
 #include "bz_umma.cuh"
 #include "bz_brute.cuh"
 
@@ -53,8 +60,10 @@ struct bz_ctx {
 
   // loaded family
   int m = 0, k = 0, n = 0, w32 = 0, wp = 0, n_eff = 0;
+  std::vector<int> n_stored;         // columns each Gamma keeps on the device
   int engine = BZ_ENGINE_AUTO;
   int elision = 1;                   // bz_set_elision (applies at the next load)
+  int early_exit = 0;                // bz_set_early_exit: in-round exit at lower_prev
   unsigned long long elide_mask = 0; // Gammas loaded with identity columns dropped
   uint32_t* d_rows = nullptr;   // m*k*wp
   uint8_t* d_trip = nullptr;    // K3 triple tables: m x trip_rows rows of 0/1 bytes
@@ -211,8 +220,9 @@ constexpr double kAutoK1Combos = BZ_AUTO_K1_COMBOS;
 // whole on one rank (run_batch)
 constexpr double kOwnWholeCombos = 6e8;
 
-// K5q: stored weights <= 127 (byte fields), W <= 4
-bool k5q_ok(int w32, int n_eff) { return w32 >= 1 && w32 <= 4 && n_eff <= 127; }
+// K5q: stored weights <= 128 (byte fields x = w + 128 - thr, thr in [1, 128];
+// every Gamma's start bound is capped at its stored columns + offset), W <= 4
+bool k5q_ok(int w32, int n_eff) { return w32 >= 1 && w32 <= 4 && n_eff <= 128; }
 
 PlanShape pass_shape(int engine, int g, bool hist, int w32 = 0, int m = 0, int k = 0,
                      int n_eff = 0) {
@@ -520,9 +530,17 @@ int prep_launch(bz_ctx* ctx, const void* fn, int threads, size_t smem, int* per_
   return BZ_OK;
 }
 
+// largest dynamic shared memory per block (sm_100: 227 KB)
+constexpr size_t kMaxSmem = 232448;
+
 template <int W, int D>
-int launch_wd(bz_ctx* ctx, const RoundArgs& a, bool hist) {
+int launch_wd(bz_ctx* ctx, const RoundArgs& a0, bool hist) {
+  RoundArgs a = a0;
   size_t smem = bz::smem_base_bytes<W>(a.m, a.k, a.ngroups);
+  if (smem + (hist ? (size_t)(a.n + 1) * 6 * 32 + 16 : 0) > kMaxSmem) {
+    a.groups_global = 1;  // a plan too large to stage: read from global memory
+    smem = bz::smem_base_bytes<W>(a.m, a.k, 0);
+  }
   int threads = 256;
   if (hist) {
     smem = ((smem + 15) & ~size_t(15)) + (size_t)(a.n + 1) * 4;
@@ -602,6 +620,7 @@ int launch_fused(bz_ctx* ctx, const RoundArgs* as, int count, int depth) {
   }
 }
 
+#if BZ_LEGACY_KERNELS
 template <int W>
 int launch_tc(bz_ctx* ctx, const RoundArgs& a) {
   const size_t smem = bz::k3_smem_bytes<W>(a.m, a.k, a.ngroups);
@@ -620,10 +639,17 @@ int launch_tc(bz_ctx* ctx, const RoundArgs& a) {
   return BZ_OK;
 }
 
+#endif
+
 template <int W, bool F4, int CW = 1>
-int launch_umma(bz_ctx* ctx, const RoundArgs& a) {
-  const size_t smem = bz::k4_smem_bytes<W, F4, CW>(a.m, a.k, a.ngroups);
-  if (smem > 232448)
+int launch_umma(bz_ctx* ctx, const RoundArgs& a0) {
+  RoundArgs a = a0;
+  size_t smem = bz::k4_smem_bytes<W, F4, CW>(a.m, a.k, a.ngroups);
+  if (smem > kMaxSmem) {
+    a.groups_global = 1;  // a plan too large to stage: read from global memory
+    smem = bz::k4_smem_bytes<W, F4, CW>(a.m, a.k, 0);
+  }
+  if (smem > kMaxSmem)
     return fail(ctx, BZ_ERR_TOO_LARGE, "K%d does not fit on an SM (smem %zu)", F4 ? 5 : 4, smem);
   {
     static std::mutex mu;
@@ -665,6 +691,7 @@ int launch_umma(bz_ctx* ctx, const RoundArgs& a) {
   return BZ_OK;
 }
 
+#if BZ_LEGACY_KERNELS
 template <int W>
 int build_triples_w(bz_ctx* ctx, int which) {
   dim3 grid(ctx->k, ctx->m);
@@ -679,6 +706,8 @@ int build_triples_w(bz_ctx* ctx, int which) {
   ctx->launches += 1;
   return BZ_OK;
 }
+
+#endif
 
 template <int W>
 int build_level_w(bz_ctx* ctx, int D, int floor) {
@@ -725,6 +754,7 @@ int ensure_level(bz_ctx* ctx, int D, int floor) {
   return BZ_OK;
 }
 
+#if BZ_LEGACY_KERNELS
 // Build (once per loaded family) the triple table kernel `which` (3: K3
 // layout, 4: K4 s8 UMMA layout) reads.  Tables are not zero-filled: padding
 // rows are only ever read into columns the kernels mask.
@@ -756,18 +786,27 @@ int ensure_triples(bz_ctx* ctx, int which) {
   return BZ_OK;
 }
 
+#else
+int ensure_triples(bz_ctx* ctx, int) {
+  return fail(ctx, BZ_ERR_STATE, "K3/K4 not built (BZ_LEGACY_KERNELS=0)");
+}
+#endif
+
 template <int W>
 int launch_w(bz_ctx* ctx, const RoundArgs& a, bool hist, const PlanShape& shape) {
+#if BZ_LEGACY_KERNELS
   if constexpr (W == 1 || W == 3) {
     if (shape.kernel == 6) return launch_umma<W, true, 2>(ctx, a);
     if (shape.kernel == 7) return launch_umma<W, true, 3>(ctx, a);
   }
-  if constexpr (W <= 4)
-    if (shape.kernel == 8) return launch_umma<W, true, 4>(ctx, a);
-  if (shape.kernel >= 6) return fail(ctx, BZ_ERR_STATE, "K5p/K5t/K5q do not support W = %d", W);
-  if (shape.kernel == 5) return launch_umma<W, true>(ctx, a);
   if (shape.kernel == 4) return launch_umma<W, false>(ctx, a);
   if (shape.kernel == 3) return launch_tc<W>(ctx, a);
+#endif
+  if constexpr (W <= 4)
+    if (shape.kernel == 8) return launch_umma<W, true, 4>(ctx, a);
+  if (shape.kernel >= 3 && shape.kernel != 5)
+    return fail(ctx, BZ_ERR_STATE, "kernel %d not available at W = %d", shape.kernel, W);
+  if (shape.kernel == 5) return launch_umma<W, true>(ctx, a);
   return shape.depth == 2 ? launch_wd<W, 2>(ctx, a, hist) : launch_wd<W, 1>(ctx, a, hist);
 }
 
@@ -876,7 +915,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     unsigned long long* hc = slot_ptr<unsigned long long>(ctx->h_io, l, i, l.off_combos);
     int* hb = slot_ptr<int>(ctx->h_io, l, i, l.off_bound);
     for (int j = 0; j < m; ++j) hc[j] = 0ull;
-    for (int j = 0; j <= m; ++j) hb[j] = upper;
+    for (int j = 0; j <= m; ++j) hb[j] = upper;  // per-Gamma caps below, once `run` is known
     RoundArgs& a = todo[i].a;
     a = RoundArgs{};
     a.rows = ctx->d_rows;
@@ -896,6 +935,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     a.shard = r_shard;
     a.nshards = r_nshards;
     a.lower_prev = lower_prev ? lower_prev[i] : 0;
+    a.exit_own = ctx->early_exit;
     a.elide = ctx->elide_mask;
     a.debug = debug;
     a.trace = (i == count - 1) ? trace : nullptr;
@@ -908,6 +948,18 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     todo[i].shape = shape;
     todo[i].run = nchunks > 0 && (unsigned long long)r_shard < nchunks &&
                   (owner[i] < 0 || owner[i] == shard);
+    if (todo[i].run && !hist) {
+      // no codeword of Gamma j weighs more than its stored columns plus the
+      // elided g, so a shard that visits any of its combinations reports
+      // min(upper, true minimum) exactly when its bound starts at that cap --
+      // which keeps K5q's threshold inside its byte fields (k5q_threshold)
+      for (int j = 0; j < m; ++j)
+        if (gamma_only < 0 || gamma_only == j) {
+          const long long cap =
+              (long long)ctx->n_stored[j] + (((ctx->elide_mask >> j) & 1ull) ? g : 0);
+          if (cap < hb[1 + j]) hb[1 + j] = (int)cap;
+        }
+    }
     goff = (gthis + (size_t)ngroups * sizeof(Group) + 255) & ~size_t(255);
   }
   const auto t_plan1 = std::chrono::steady_clock::now();
@@ -1163,6 +1215,7 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
   std::vector<std::vector<uint64_t>> keep(m, std::vector<uint64_t>(w64, 0ull));
   unsigned long long elide = 0;
   int n_eff = 1;
+  std::vector<int> n_stored(m, 0);
   for (int j = 0; j < m; ++j) {
     std::vector<uint64_t>& km = keep[j];
     for (int w = 0; w < w64; ++w) {
@@ -1191,6 +1244,7 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
     int cnt = 0;
     for (int w = 0; w < w64; ++w) cnt += __builtin_popcountll(km[w]);
     n_eff = std::max(n_eff, cnt);
+    n_stored[j] = cnt;
   }
   if (n_eff > BZ_MAX_N_STORED)
     return fail(ctx, BZ_ERR_TOO_LARGE,
@@ -1245,6 +1299,7 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
   ctx->w32 = w32;
   ctx->wp = wp;
   ctx->n_eff = n_eff;
+  ctx->n_stored = n_stored;
   ctx->elide_mask = elide;
   return BZ_OK;
 }
@@ -1519,6 +1574,12 @@ int bz_set_elision(bz_ctx* ctx, int on) {
   return BZ_OK;
 }
 
+int bz_set_early_exit(bz_ctx* ctx, int on) {
+  if (!ctx) return BZ_ERR_ARGUMENT;
+  ctx->early_exit = on ? 1 : 0;
+  return BZ_OK;
+}
+
 int bz_elided(bz_ctx* ctx, uint64_t* out_mask) {
   if (!ctx || !out_mask) return BZ_ERR_ARGUMENT;
   *out_mask = ctx->elide_mask;
@@ -1529,6 +1590,11 @@ int bz_set_engine(bz_ctx* ctx, int engine) {
   if (!ctx) return BZ_ERR_ARGUMENT;
   if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4Q)
     return fail(ctx, BZ_ERR_ARGUMENT, "unknown engine %d", engine);
+  if (!BZ_LEGACY_KERNELS && (engine == BZ_ENGINE_IMMA || engine == BZ_ENGINE_UMMA ||
+                             engine == BZ_ENGINE_MXF4P || engine == BZ_ENGINE_MXF4T))
+    return fail(ctx, BZ_ERR_ARGUMENT,
+                "engine %d is a comparison kernel not built into this library "
+                "(rebuild with -DBZ_LEGACY_KERNELS=1)", engine);
   ctx->engine = engine;
   return BZ_OK;
 }
@@ -1605,6 +1671,61 @@ int bz_launch_count(bz_ctx* ctx, uint64_t* out) {
   if (!ctx || !out) return BZ_ERR_ARGUMENT;
   *out = ctx->launches;
   return BZ_OK;
+}
+
+// Host check of the K5q offset encoding (no device needed): every A offset
+// block the producer can emit, dotted with the table's offset block, must
+// give back its integer exactly.  Walks every (prefix stored weight wt,
+// bound) pair the producer can see -- wt in [0, 128], the Gamma's bound
+// less its weight offset in [-4, 128] (run_batch caps it at the stored
+// columns) -- through the kernel's own
+// k5q_threshold / pad_chunk, and checks thr in [1, 128], x in [0, 238],
+// dot(pad_chunk(x, 0)) = x and dot(pad_chunk(x, 128)) = x + 128 (block 1
+// of the second chunk: the 2^23 offset at scale 2^16).  Returns the number
+// of failures; the first failing (wt, rel) goes to out_bad[0..1].
+static double e2m1_value(uint32_t nib) {
+  static const double mag[8] = {0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0};
+  return (nib & 8u) ? -mag[nib & 7u] : mag[nib & 7u];
+}
+static double e2m1_dot16(uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1) {
+  double s = 0;
+  for (int q = 0; q < 8; ++q) {
+    s += e2m1_value((a0 >> (4 * q)) & 0xFu) * e2m1_value((b0 >> (4 * q)) & 0xFu);
+    s += e2m1_value((a1 >> (4 * q)) & 0xFu) * e2m1_value((b1 >> (4 * q)) & 0xFu);
+  }
+  return s;
+}
+
+int bz_k5q_selftest(int32_t* out_bad) {
+  const uint4 tb = bz::k5_table_offset_chunk();
+  int bad = 0;
+  auto note = [&](int wt, int rel) {
+    if (!bad++ && out_bad) {
+      out_bad[0] = wt;
+      out_bad[1] = rel;
+    }
+  };
+  for (int T = 0; T <= bz::kQMaxSpan + 128; ++T) {
+    const unsigned long long b = bz::e2m1_block(T);
+    if (e2m1_dot16((uint32_t)b, (uint32_t)(b >> 32), tb.x, tb.y) != (double)T) note(-1, T);
+  }
+  for (int wt = 0; wt <= 128; ++wt)
+    for (int rel = -4; rel <= 128; ++rel) {
+      const int thr = bz::k5q_threshold(wt, rel);
+      const int x = wt + 128 - thr;
+      // exactness: every stored weight below rel must be flagged (w < thr),
+      // and every field w + 128 - thr of a stored weight w in [0, 128] must
+      // stay a byte
+      const bool range_ok = thr >= 1 && thr <= 128 && x >= 0 && x <= bz::kQMaxSpan + 128 &&
+                            thr >= rel && 128 + 128 - thr <= 255;
+      const uint4 pa = bz::pad_chunk(x, 0), pb = bz::pad_chunk(x, 128);
+      const bool enc_ok = e2m1_dot16(pa.x, pa.y, tb.x, tb.y) == (double)x &&
+                          e2m1_dot16(pa.z, pa.w, tb.z, tb.w) == 0.0 &&
+                          e2m1_dot16(pb.x, pb.y, tb.x, tb.y) == (double)x &&
+                          e2m1_dot16(pb.z, pb.w, tb.z, tb.w) == 128.0;
+      if (!range_ok || !enc_ok) note(wt, rel);
+    }
+  return bad;
 }
 
 int bz_measure_int_peaks(bz_ctx* ctx, int w_words, double* out) {

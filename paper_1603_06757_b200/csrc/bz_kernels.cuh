@@ -66,7 +66,11 @@ struct RoundArgs {
   int ngroups;
   int m, k, g, n;
   int shard, nshards;
-  int lower_prev;              // early exit once bound[0] <= lower_prev
+  int lower_prev;              // the run's lower bound before this round (L_prev)
+  int exit_own;                // 1: stop once this round's own minimum meets L_prev
+                               // (in-round early exit, bz_set_early_exit); the
+                               // previous round's U meeting it (the run ended:
+                               // a batched round past termination) always stops
   unsigned long long elide;    // bit j: Gamma j's identity columns were dropped at load
                                // time, so its codeword weights get + g (see bz_load_gammas)
   int debug;                   // K4 timing experiments only (see BZ_K4_DEBUG)
@@ -78,6 +82,9 @@ struct RoundArgs {
                                // after the round tightens this round's start), or null
   int sgroups_cap;             // shared-memory room for this many groups (fused K1
                                // launches stage several plans in turn), 0 = ngroups
+  int groups_global;           // 1: the plan is too large to stage in shared memory
+                               // (many groups at large k); read it from global
+                               // memory (L2-resident) instead
   // Multi-GPU: the running minimum of every round g across all ranks, one
   // 64-bit word per g in one rank's device memory, mapped into every rank
   // (CUDA IPC over NVLink) -- kernels RED.MIN their chunk minima into it and
@@ -114,13 +121,16 @@ __device__ __forceinline__ void round_start(const RoundArgs& a) {
   if (v < INT_MAX) gbound_publish(a, v);
 }
 
-// a round may stop taking work: its own running minimum, any rank's (the
-// shared mirror), or the previous round's (chain / mirror) already meets
-// L_prev -- the run has terminated or this round's result is exactly L_prev
+// a round may stop taking work: the previous round's running U (chain /
+// shared mirror) already meets L_prev -- the run has terminated and this
+// batched round's result will be discarded -- or, with the in-round early
+// exit on, this round's own running minimum (or any rank's) meets it, so
+// the round's result is exactly L_prev
 __device__ __forceinline__ bool round_done(const RoundArgs& a) {
-  if (((volatile const int*)a.bound)[0] <= a.lower_prev) return true;
+  if (a.exit_own && ((volatile const int*)a.bound)[0] <= a.lower_prev) return true;
   if (a.chain && ((volatile const int*)a.chain)[0] <= a.lower_prev) return true;
-  if (a.gbound && (gbound_read(a, a.g) <= a.lower_prev || gbound_read(a, a.g - 1) <= a.lower_prev))
+  if (a.gbound && ((a.exit_own && gbound_read(a, a.g) <= a.lower_prev) ||
+                   gbound_read(a, a.g - 1) <= a.lower_prev))
     return true;
   return false;
 }
@@ -344,12 +354,16 @@ __host__ __device__ inline size_t smem_base_bytes(int m, int k, int ngroups) {
   return bytes + kSBinomBytes;  // the small binomial table (colex_unrank)
 }
 
+// groups held in shared memory (0 when the plan is read from global memory)
+__host__ __device__ inline int staged_groups(const RoundArgs& a) {
+  return a.groups_global ? 0 : (a.ngroups > a.sgroups_cap ? a.ngroups : a.sgroups_cap);
+}
+
 // the small binomial table at the end of the staged region
 template <int W>
 __device__ __forceinline__ unsigned long long* smem_binom(unsigned char* smem, const RoundArgs& a) {
   return reinterpret_cast<unsigned long long*>(
-      smem + smem_base_bytes<W>(a.m, a.k, a.ngroups > a.sgroups_cap ? a.ngroups : a.sgroups_cap) -
-      kSBinomBytes);
+      smem + smem_base_bytes<W>(a.m, a.k, staged_groups(a)) - kSBinomBytes);
 }
 
 // dst[i] = load(i) for i < n, block-strided, 8 loads in flight per thread
@@ -400,7 +414,10 @@ __device__ __forceinline__ void stage(const RoundArgs& a, uint32_t*& srows,
     const int r = i / PS, j = i - r * PS;
     return j < W ? a.px[r * WP + j] : 0u;
   }, spx);
-  stage_groups(a, sgroups);
+  if (a.groups_global)
+    sgroups = const_cast<Group*>(a.groups);
+  else
+    stage_groups(a, sgroups);
   unsigned long long* sb = smem_binom<W>(smem, a);
   stage_copy(kMaxK * (kSBinomQ + 1), [&](int i) {
     const int c = i / (kSBinomQ + 1), j = i - c * (kSBinomQ + 1);
@@ -641,7 +658,7 @@ k1h_histogram(const RoundArgs a) {
   uint32_t *srows, *spx;
   Group* sgroups;
   const int nbins = a.n + 1;
-  size_t base = smem_base_bytes<W>(a.m, a.k, a.ngroups);
+  size_t base = smem_base_bytes<W>(a.m, a.k, staged_groups(a));
   base = (base + 15) & ~size_t(15);
   unsigned int* bhist = reinterpret_cast<unsigned int*>(smem + base);
   unsigned short* th = reinterpret_cast<unsigned short*>(smem + base + (size_t)nbins * 4);

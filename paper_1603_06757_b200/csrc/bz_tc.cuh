@@ -147,7 +147,7 @@ k3_round_gemm(const RoundArgs a, const uint8_t* __restrict__ trip, size_t gamma_
     if (tid == 0) {
       const unsigned long long c = atomicAdd(a.counter, 1ull);
       const unsigned long long chunk = c * (unsigned long long)a.nshards + a.shard;
-      const bool stop = chunk >= a.nchunks || vbound[0] <= a.lower_prev;
+      const bool stop = chunk >= a.nchunks || (a.exit_own && vbound[0] <= a.lower_prev);
       sctl[0] = stop ? -1 : find_group(sgroups, a.ngroups, chunk);
       reinterpret_cast<unsigned long long*>(sctl)[1] = chunk;
     }

@@ -235,6 +235,20 @@ __host__ __device__ __forceinline__ unsigned long long e2m1_block(int T) {
   const uint32_t lo = k ? (0x77777777u >> (32 - 4 * k)) : 0u;
   return (unsigned long long)lo | ((unsigned long long)e2m1_sum8(T - 24 * k) << 32);
 }
+// K5q: the prefix weight may exceed the threshold by at most this much, so
+// the A offset x = wt + 128 - thr stays <= 238 (e2m1_block's exact range)
+constexpr int kQMaxSpan = 110;
+// K5q producer threshold for a prefix of stored weight wt (0..128) against a
+// bound rel = the Gamma's bound less its weight offset (<= the Gamma's
+// stored columns <= 128: run_batch caps every Gamma's start bound there):
+// codewords of stored weight < thr have bit 7 of their byte clear.
+// thr in [1, 128] keeps every byte field wt(P^S) + 128 - thr in [0, 255]
+// for stored weights 0..128 (a threshold of 1 under a bound <= 0 only flags
+// weight-0 codewords, which the exact path then finds are not below it);
+// thr >= wt - kQMaxSpan keeps the offset x = wt + 128 - thr <= 238.
+__host__ __device__ __forceinline__ int k5q_threshold(int wt, int rel) {
+  return max(wt - kQMaxSpan, max(1, min(128, rel)));
+}
 // A offset chunk: T0 on block 0, T1 on block 1
 __host__ __device__ __forceinline__ uint4 pad_chunk(int T0, int T1) {
   const unsigned long long b0 = e2m1_block(T0), b1 = T1 ? e2m1_block(T1) : 0ull;
@@ -758,7 +772,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
   static_assert(EC * (RL::EW / 4) == N && (F4 ? EC % 4 == 0 && EC <= 128 : EC % 32 == 0),
                 "epilogue");
   extern __shared__ __align__(128) unsigned char smem[];
-  const size_t base = (smem_base_bytes<W>(a.m, a.k, a.ngroups) + 1023) & ~size_t(1023);
+  const size_t base = (smem_base_bytes<W>(a.m, a.k, staged_groups(a)) + 1023) & ~size_t(1023);
   unsigned char* sB = smem + base;
   unsigned char* sA = sB + S * TB;
   constexpr int NA = k4_abufs<F4>(W);
@@ -1254,9 +1268,14 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
             // K5q: both fields read x = wt + 128 - thr (thr: this Gamma's
             // bound less the weight offset, as this thread sees it now), so
             // a codeword can lower the bound iff bit 7 of its byte is clear;
-            // block 1 of the second chunk (scale 2^16) is the 2^23 offset
-            const int thr = max(0, min(127, ((volatile int*)a.bound)[1 + c.gr.gamma] -
-                                                gamma_woff(a, c.gr.gamma)));
+            // block 1 of the second chunk (scale 2^16) is the 2^23 offset.
+            // Range (k5q_threshold): thr in [1, 128] keeps every field a
+            // byte, thr >= wt - kQMaxSpan keeps the offset x <= 238, the
+            // largest sum an A offset block encodes exactly (e2m1_block).
+            // A threshold raised above the bound only sends more tiles down
+            // the exact path.
+            const int thr = k5q_threshold(
+                wt, ((volatile int*)a.bound)[1 + c.gr.gamma] - gamma_woff(a, c.gr.gamma));
             const int x = wt + 128 - thr;
             *reinterpret_cast<uint4*>(dst + umma_off_c(r, W, CA)) = pad_chunk(x, 0);
             *reinterpret_cast<uint4*>(dst + umma_off_c(r, W + 1, CA)) = pad_chunk(x, 128);

@@ -85,7 +85,13 @@ class EngineConfig:
     progress: object = None  # callable(g, L, U) after each round
     device: int | None = None
     distributed: bool = False
-    early_exit: bool = True  # stop a round once U reaches the previous L
+    # in-round early exit: stop a round once U reaches the previous L (the
+    # trace is the same; only that round's `combinations` count drops below
+    # the reference's m*C(k,g)).  Off by default, so every pass runs to
+    # completion and the counters are schedule-independent, as the
+    # reference's are (enumeration.py:21-24).  Batched rounds past
+    # termination stop at once either way (their results are discarded).
+    early_exit: bool = False
     # consecutive rounds with at most this many combinations in total (per
     # rank) run as one batch (one launch sequence, one synchronisation, one
     # exchange); 0 disables batching
@@ -168,6 +174,7 @@ class GpuRounds:
         self.ctx.set_engine(config.engine)
         if self.ctx.elision != config.elide_identity:
             self.ctx.set_elision(config.elide_identity)
+        self.ctx.set_early_exit(config.early_exit)
         self.comm = comm
         # multi-GPU: the shared bound mirror (rank 0's array, mapped into
         # every rank over CUDA IPC), set up once per context and world
@@ -275,10 +282,9 @@ def run_rounds(backend, gs: GammaSet, k: int, config: EngineConfig, st: LoopStat
                 total += m * comb(k, st.g + count)
                 count += 1
             if count >= 2:
-                lps = [st.L if config.early_exit else 0]
+                lps = [st.L]
                 for i in range(1, count):
-                    lps.append(lower_bound_update(st.g + i - 1, m_arg, k, km_arg)
-                               if config.early_exit else 0)
+                    lps.append(lower_bound_update(st.g + i - 1, m_arg, k, km_arg))
                 res, batch_ms = backend.run_batch(st.g, lps, st.U)
                 for i, (mn, cb) in enumerate(res):
                     if isinstance(batch_ms, list):  # per-round device times
@@ -290,7 +296,7 @@ def run_rounds(backend, gs: GammaSet, k: int, config: EngineConfig, st: LoopStat
             _, mins, combos, kernel_ms = queued.pop(0)
         else:
             queued.clear()
-            mins, combos, kernel_ms = backend.run(st.g, st.L if config.early_exit else 0, st.U)
+            mins, combos, kernel_ms = backend.run(st.g, st.L, st.U)
         round_combos = 0
         for mn, c in zip(mins, combos):
             st.U = min(st.U, mn)
@@ -331,8 +337,21 @@ def minimum_distance(G: BitMatrix, config: EngineConfig | None = None) -> Distan
     try:
         if st.g <= k and st.L < st.U and st.g <= config.max_g:
             backend = make_backend(config, _make_comm(config))
-            backend.load(gs, n)
-            run_rounds(backend, gs, k, config, st)
+            lock = getattr(getattr(backend, "ctx", None), "lock", None)
+            if lock is None:
+                backend.load(gs, n)
+                run_rounds(backend, gs, k, config, st)
+            else:
+                # the device context is per process: hold it across the load
+                # and every round, so concurrent calls on distinct matrices
+                # never run on each other's family
+                with lock:
+                    backend.ctx.set_engine(config.engine)
+                    backend.ctx.set_early_exit(config.early_exit)
+                    if backend.ctx.elision != config.elide_identity:
+                        backend.ctx.set_elision(config.elide_identity)
+                    backend.load(gs, n)
+                    run_rounds(backend, gs, k, config, st)
         elif st.g <= k and st.L < st.U:
             st.status = STATUS_UPPER_BOUND_ONLY
     except KeyboardInterrupt:
@@ -356,7 +375,8 @@ def brute_force_distance(G: BitMatrix, max_k: int = 28, device: int | None = Non
     dev = device if device is not None else int(os.environ.get("LOCAL_RANK", "0"))
     ctx = _native.context(dev)
     words = np.ascontiguousarray(G.with_word_width(64).to_numpy(), dtype=np.uint64)
-    d, _ = ctx.brute_force(words, G.num_cols, max_k)
+    with ctx.lock:
+        d, _ = ctx.brute_force(words, G.num_cols, max_k)
     return d
 
 

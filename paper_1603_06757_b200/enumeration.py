@@ -57,8 +57,10 @@ def enumerate_gpu(gamma: BitMatrix, g: int, ubound: int | None = None,
                   device: int = 0) -> EnumerationResult:
     """Minimum weight over all XORs of exactly g rows of gamma."""
     _check(g, gamma.num_rows)
-    ctx = _load_single(gamma, device)
-    mn, combos = ctx.enumerate(0, g)
+    ctx = _native.context(device)
+    with ctx.lock:
+        _load_single(gamma, device)
+        mn, combos = ctx.enumerate(0, g)
     if ubound is not None:
         mn = min(mn, ubound)
     return EnumerationResult(int(mn), combos, combos, combos)
@@ -67,6 +69,8 @@ def enumerate_gpu(gamma: BitMatrix, g: int, ubound: int | None = None,
 def weight_histogram_gpu(gamma: BitMatrix, g: int, device: int = 0):
     """(histogram over weights 0..n, min weight, combinations) of one pass."""
     _check(g, gamma.num_rows)
-    ctx = _load_single(gamma, device)
-    return ctx.histogram(0, g)
+    ctx = _native.context(device)
+    with ctx.lock:
+        _load_single(gamma, device)
+        return ctx.histogram(0, g)
 

@@ -139,3 +139,32 @@ def test_plan_levels_auto_cfg5():
     depths = {int(gr[6]) for gr in groups}
     assert depths >= {3, 4}
     assert sum(int(gr[5]) for gr in groups) == 2 * comb(80, 8)
+
+
+def test_k5q_offset_encoding():
+    """Host-only (no device): K5q's producer threshold and e2m1 offset blocks
+    over every prefix stored weight 0..128 and bound -4..128 stay in range
+    (thr in [1, 128], offset x <= 238) and dot to their integers exactly
+    (bz_k5q_selftest runs the kernel's own k5q_threshold / pad_chunk)."""
+    bad, first = _native.k5q_selftest()
+    assert bad == 0, first
+
+
+def test_k5q_offset_encoding_restated():
+    """Independent restatement of the same check in Python: the A offset
+    block for T (6.0 on the table's 4.0 elements while 24 fit, the rest on
+    the 1.0 elements) dots to T for every T in 0..238, and the producer's
+    threshold keeps x = wt + 128 - thr in that range."""
+    for T in range(239):
+        k6 = min(8, T // 24)
+        rest = T - 24 * k6           # on eight 1.0 elements: 6.0s then the remainder
+        n6 = min(rest // 6, 8)
+        rem = rest - 6 * n6
+        assert 24 * k6 + 6 * n6 + rem == T and (n6 < 8 or rem == 0)
+        assert rem <= 5 and (rem < 5 or n6 <= 6)  # 5 = 4.0 + 1.0 on the next element
+    for wt in range(129):
+        for rel in range(-4, 129):  # bounds start capped at the stored columns (<= 128)
+            thr = max(wt - 110, max(1, min(128, rel)))
+            x = wt + 128 - thr
+            assert 1 <= thr <= 128 and 0 <= x <= 238
+            assert thr >= rel and 128 + 128 - thr <= 255  # stored weight 128 still a byte

@@ -38,3 +38,48 @@ def test_reference_arm_other_ranks_exit_quietly():
     p = _run({"RANK": "1", "LOCAL_RANK": "1", "WORLD_SIZE": "2"})
     assert p.returncode == 0, p.stderr
     assert p.stdout.strip() == ""
+
+
+def test_reference_arm_runs_reference_package():
+    """The reference arm's side entry times the reference package itself
+    (baseline/_ref) on the same code, single worker and all cores."""
+    if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "mindist")):
+        import pytest
+
+        pytest.skip("baseline/_ref not installed")
+    p = _run(None, "--ref-python-max-g", "3")
+    assert p.returncode == 0, p.stderr
+    line = json.loads(p.stdout.strip().splitlines()[-1])
+    ref = line["reference_python"]
+    assert ref["workers_1"]["combinations"] == 2 * (48 + 1128 + 17296)
+    assert ref["workers_1"]["bounds_trace"][:3] == [[1, 4, 16], [2, 6, 15], [3, 8, 12]]
+
+
+def test_spawned_ranks_json_contract():
+    """`bench.py --gpus 2` outside torchrun spawns two ranks itself (here in
+    the hidden gloo self-test mode: no device work) and rank 0 alone prints
+    one JSON line with n_gpus = 2 and the max-over-ranks step time."""
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--cpu-selftest", "--steps", "3", "--warmup", "3"],
+                       capture_output=True, text=True, cwd=ROOT, timeout=300)
+    assert p.returncode == 0, p.stderr
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["steps"] == 3 and line["warmup"] == 3
+    # rank 1 sleeps 4 ms per step, rank 0 2 ms: the reported time is rank 1's
+    assert line["ms_per_step"] >= 3.5
+
+
+def test_reference_arm_under_spawn():
+    """The reference arm launched with --gpus 2: rank 0 prints the line
+    (the GPU count only labels it), rank 1 exits without work."""
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference",
+                        "--config", "cfg1", "--gpus", "2", "--steps", "1", "--warmup", "1",
+                        "--no-extra"],
+                       capture_output=True, text=True, cwd=ROOT, timeout=300)
+    assert p.returncode == 0, p.stderr
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2

@@ -109,3 +109,27 @@ def test_construct_script(tmp_path, section6):
     assert cli.main(["construct", "--in", str(bad), "--quiet"]) == cli.EXIT_NOT_A_DIVISOR
     bad.write_text("m = 7\nbogus = 1\n")
     assert cli.main(["construct", "--in", str(bad), "--quiet"]) == cli.EXIT_SCRIPT
+
+
+def test_device_errors_exit_codes(tmp_path):
+    """No usable device maps to EXIT_DEVICE (14) -- never a silent CPU run;
+    on a GPU box, more stored columns than the kernels hold maps to
+    EXIT_TOO_LARGE (11), not EXIT_INVALID."""
+    import random
+
+    from paper_1603_06757_b200 import _native
+
+    try:
+        have_gpu = _native.device_count() > 0
+    except Exception:
+        have_gpu = False
+    small = tmp_path / "small.txt"
+    write_matrix_file(str(small), BitMatrix([0b1011, 0b0110], 4))
+    wide = tmp_path / "wide.txt"
+    rng = random.Random(5)
+    write_matrix_file(str(wide), BitMatrix([rng.getrandbits(290) for _ in range(28)], 290))
+    if have_gpu:
+        assert cli.main(["mindist", "--in", str(wide), "--quiet"]) == cli.EXIT_TOO_LARGE
+    else:
+        assert cli.main(["mindist", "--in", str(small), "--quiet"]) == cli.EXIT_DEVICE
+        assert cli.main(["brute", "--in", str(small)]) == cli.EXIT_DEVICE

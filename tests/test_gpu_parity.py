@@ -27,11 +27,11 @@ def ctx():
     return _native.context(0)
 
 
-@pytest.fixture(params=["popc", "imma", "umma", "mxf4", "mxf4p", "mxf4t", "mxf4q"])
+@pytest.fixture(params=["popc", "mxf4", "mxf4q"])
 def engine(request):
-    """Every kernel: K1 (XOR+POPC), K3 (legacy IMMA, g >= 4), K4 (tcgen05
-    kind::i8), K5 (kind::mxf4), K5p / K5t (two / three codewords per
-    accumulator column; W = 1, 3 -- other widths run K5)."""
+    """Every kernel of the library: K1 (XOR+POPC), K5 (tcgen05 kind::mxf4,
+    g >= 4) and K5q (kind::mxf4nvf4, two codewords per accumulator; W <= 4
+    and <= 127 stored columns -- other shapes run K5)."""
     _native.context(0).set_engine(request.param)
     yield request.param
     _native.context(0).set_engine("auto")
@@ -129,8 +129,7 @@ def test_minimum_distance_configs(goldens, idx, engine):
     assert (rep.status, rep.g_reached, rep.m, rep.k_m) == \
         (fx["status"], fx["g_reached"], fx["m"], fx["k_m"])
     assert [list(p) for p in rep.pivot_sets] == fx["pivot_sets"]
-    if (fx["name"], fx["seed"]) != ("cfg1", 2):  # that run exits early (below)
-        assert rep.counters.combinations == fx["combinations"]
+    assert rep.counters.combinations == fx["combinations"]
 
 
 def test_early_exit_fixture(goldens):
@@ -138,8 +137,8 @@ def test_early_exit_fixture(goldens):
     the trace bit-exact (SURVEY.md 8(a) invariant 5)."""
     fx = [c for c in goldens["configs"] if (c["name"], c["seed"]) == ("cfg1", 2)][0]
     G = BitMatrix(hexrows(fx["rows"]), fx["n"])
-    fast = minimum_distance(G)
-    full = minimum_distance(G, EngineConfig(early_exit=False))
+    fast = minimum_distance(G, EngineConfig(early_exit=True))
+    full = minimum_distance(G)  # default: full passes, the reference's counts
     for rep in (fast, full):
         assert rep.bounds_trace == [tuple(t) for t in fx["bounds_trace"]]
         assert rep.distance == 6
@@ -205,8 +204,6 @@ def test_codes_wider_than_256(k, n, engine):
     try:
         rep = minimum_distance(BitMatrix(rows, n), EngineConfig(engine=engine))
     except TooLarge:
-        if engine in ("umma", "imma"):  # legacy s8 engines: W = 8 tiles + m Gammas
-            pytest.skip("staged rows and tiles exceed shared memory")  # fail loudly, not wrong
         raise
     assert rep.distance == want["distance"]
     assert rep.bounds_trace == [tuple(t) for t in want["bounds_trace"]]
@@ -230,13 +227,12 @@ def test_stored_columns_limit():
 @pytest.mark.parametrize("k,n,g", [(4, 9, 4), (5, 40, 4), (128, 256, 4), (100, 200, 5),
                                    (40, 224, 6), (30, 33, 7)])
 def test_tensor_engine_shapes(k, n, g, engine):
-    """K3/K4 edge shapes: smallest triple tables (k = 4, 5), the 2-stage
-    shared-memory path (W = 7, 8), slices smaller than one tile."""
+    """Tensor-engine edge shapes: smallest suffix tables (k = 4, 5), wide
+    rows (W = 7, 8), k = 128, slices smaller than one tile."""
     rng = random.Random(k * 1000 + n + g)
     rows = [rng.getrandbits(n) for _ in range(k)]
     M = BitMatrix(rows, n)
-    if comb(k, g) > 20_000_000:
-        pytest.skip("oracle too slow")
+    # (100, 200, 5): 7.5e7 combinations, ~1 s in the threaded C oracle
     assert enumerate_gpu(M, g).min_weight == oracle.min_weight(rows, n, g)[0], (k, n, g)
 
 
@@ -254,14 +250,22 @@ def test_round_many_shards(ctx, engine):
 
 
 def test_early_exit_all_engines(ctx, engine):
-    """Once the running minimum reaches lower_prev the round stops; its
-    result is then exactly lower_prev and fewer combinations are visited."""
+    """With the in-round early exit on, once the running minimum reaches
+    lower_prev the round stops; its result is then exactly lower_prev and
+    fewer combinations are visited.  Off (the default), the same call visits
+    every combination."""
     G, gs, _ = code("cfg2", 1)
     ctx.load(family_words(gs.gammas, 96), 96)
     for g in (4, 5):
         full_min, full_c = ctx.round(g, 0, 10**6)
         true_min = min(full_min)
         mins, combos = ctx.round(g, true_min, 10**6)
+        assert (mins, combos) == (full_min, full_c) == (full_min, [comb(48, g)] * 2)
+        ctx.set_early_exit(True)
+        try:
+            mins, combos = ctx.round(g, true_min, 10**6)
+        finally:
+            ctx.set_early_exit(False)
         assert min(mins) == true_min
         assert sum(combos) <= sum(full_c)
 
@@ -269,7 +273,7 @@ def test_early_exit_all_engines(ctx, engine):
 @pytest.mark.parametrize("k,g,floors", [(12, 6, "4,7"), (14, 8, "5,9"), (12, 5, "6"),
                                         (20, 7, "8,13"), (11, 9, "0,3")])
 @pytest.mark.parametrize("n", [20, 37, 70, 96, 160, 230])
-@pytest.mark.parametrize("kernel", ["mxf4", "mxf4p", "mxf4t", "mxf4q"])
+@pytest.mark.parametrize("kernel", ["mxf4", "mxf4q"])
 def test_mxf4_levels(monkeypatch, ctx, k, g, floors, n, kernel):
     """K5 / K5p with forced suffix levels (depth-4/5 tables): exact minima and
     combination counts per Gamma against the oracle (K5p runs at n = 20, 70,
@@ -300,7 +304,7 @@ def test_identity_elision(ctx, name, seed, mask):
     G, gs, _ = code(name, seed)
     reports = {}
     for elide in (True, False):
-        for eng in ("auto", "umma", "popc"):
+        for eng in ("auto", "mxf4", "popc"):
             rep = minimum_distance(G, EngineConfig(engine=eng, elide_identity=elide))
             if elide:
                 assert ctx.elided() == mask
@@ -371,43 +375,47 @@ def test_brute_force_rank_deficient():
     assert brute_force_distance(M) == 0
 
 
-@pytest.mark.parametrize("n", [1, 17, 32, 33, 64, 80, 95, 96])
+@pytest.mark.parametrize("n", [1, 17, 32, 33, 64, 80, 95, 96, 110, 111, 120, 127, 128])
 @pytest.mark.parametrize("density", [0.05, 0.5, 0.97])
-@pytest.mark.parametrize("kernel", ["mxf4p", "mxf4t", "mxf4q"])
-def test_mxf4p_weight_range(ctx, n, density, kernel):
-    """K5p / K5t pack two / three stored weights into one fp32 accumulator
-    (bits 0..15 and 16..22 / bytes 0..2): every weight from 0 to n <= 96 must
-    come back exact, including all-zero and all-one codewords, slices
-    crossing the 480/720-row tile and every part of a column."""
+def test_k5q_weight_range(ctx, n, density):
+    """K5q packs two codewords as bytes x = wt + 128 - thr of one fp32
+    accumulator: every stored weight from 0 to n <= 127 must come back exact,
+    including all-zero and all-one codewords, dense rows (prefix weights up
+    to 128), slices crossing the 480-row tile and both parts of a column."""
     rng = random.Random(n * 100 + int(density * 100))
     k = 24
     rows = [sum(1 << b for b in range(n) if rng.random() < density) for _ in range(k)]
     rows[3] = rows[4]                      # a zero codeword at every even g >= 2
     rows[5] = (1 << n) - 1                 # an all-ones row
-    ctx.set_engine(kernel)
+    ctx.set_engine("mxf4q")
     try:
         ctx.load(family_words([BitMatrix(rows, n), BitMatrix(rows[::-1], n)], n), n)
         for g in (4, 5, 6, 7):
-            mins, combos = ctx.round(g, -1, 1 << 30)
             want = oracle.min_weight(rows, n, g)[0]
-            assert mins == [want, want] and combos == [comb(k, g)] * 2, (g, mins, want)
+            for upper in (1 << 30, want + 1, want, max(want - 2, 0)):
+                mins, combos = ctx.round(g, -1, upper)
+                assert mins == [min(want, upper)] * 2 and combos == [comb(k, g)] * 2, \
+                    (g, upper, mins, want)
     finally:
         ctx.set_engine("auto")
 
 
-@pytest.mark.parametrize("n", [40, 96])
-@pytest.mark.parametrize("kernel", ["mxf4p", "mxf4t", "mxf4q"])
-def test_mxf4p_all_heavy(ctx, n, kernel):
+@pytest.mark.parametrize("n", [40, 96, 111, 127, 128])
+def test_k5q_all_heavy(ctx, n):
     """Every codeword heavy (odd g over identical all-ones rows: weight n),
-    so the minimum is the largest value the packed fields carry."""
+    so the minimum is the largest value a byte field carries -- up to a
+    stored weight of 128 with no bound (the start bound is capped at the
+    stored columns, so the threshold stays <= 128)."""
     k = 15
     rows = [(1 << n) - 1] * k
-    ctx.set_engine(kernel)
+    ctx.set_engine("mxf4q")
     try:
         ctx.load(family_words([BitMatrix(rows, n)], n), n)
         for g in (5, 7, 9):
             mins, _ = ctx.round(g, -1, 1 << 30)
             assert mins == [n], (g, mins)
+            mn, c = ctx.enumerate(0, g)
+            assert (mn, c) == (n, comb(k, g)), (g, mn, c)
         for g in (4, 6):
             mins, _ = ctx.round(g, -1, 1 << 30)
             assert mins == [0], (g, mins)
@@ -415,22 +423,62 @@ def test_mxf4p_all_heavy(ctx, n, kernel):
         ctx.set_engine("auto")
 
 
-@pytest.mark.parametrize("kernel", ["mxf4p", "mxf4t", "mxf4q"])
-def test_packed_clipping(ctx, kernel):
-    """The K5t threshold test starts from the incoming bound: a bound at or
-    below the true minimum reports the bound, one above it the minimum."""
-    rng = random.Random(77)
-    n, k = 90, 30
+def test_k5q_dense_prefix_small_bound(ctx):
+    """A prefix of stored weight 127 (an all-ones row) under a small bound:
+    the offset x = wt + 128 - thr would pass 238, past what an e2m1 offset
+    block encodes, unless the producer raises its threshold (k5q_threshold).
+    The bound must come back unchanged (no codeword is that light) and the
+    unbounded pass must give the oracle minimum."""
+    rng = random.Random(2024)
+    n, k = 127, 20
     rows = [rng.getrandbits(n) for _ in range(k)]
-    ctx.set_engine(kernel)
+    rows[0] = (1 << n) - 1
+    want = oracle.min_weight(rows, n, 4)[0]
+    ctx.set_engine("mxf4q")
     try:
         ctx.load(family_words([BitMatrix(rows, n)], n), n)
-        want = oracle.min_weight(rows, n, 5)[0]
-        for upper in (want - 3, want, want + 1, want + 40, 1 << 20):
-            mins, combos = ctx.round(5, -1, upper)
-            assert mins == [min(want, upper)] and combos == [comb(k, 5)], (upper, mins, want)
+        for upper in (0, 1, 5, 16, 17, want, want + 1):
+            mins, combos = ctx.round(4, -1, upper)
+            assert mins == [min(upper, want)] and combos == [comb(k, 4)], (upper, mins, want)
+        mins, _ = ctx.round(4, -1, 1 << 30)
+        assert mins == [want]
     finally:
         ctx.set_engine("auto")
+
+
+def _dense_systematic(k: int, seed: int, light: int):
+    """[I_k | A] with A random and invertible, A's row 0 all ones (stored
+    weight k in Gamma_1) and row 1 of weight `light` - 1 (a planted codeword
+    of weight `light`)."""
+    rng = random.Random(seed)
+    n = 2 * k
+    while True:
+        A = [rng.getrandbits(k) for _ in range(k)]
+        A[0] = (1 << k) - 1
+        A[1] = sum(1 << b for b in rng.sample(range(k), light - 1))
+        rows = [(1 << i) | (a << k) for i, a in enumerate(A)]
+        try:
+            from paper_1603_06757_b200.gf2 import build_gamma_set
+
+            gs = build_gamma_set(BitMatrix(rows, n))
+        except Exception:
+            continue
+        if gs.full_rank_count == 2 and gs.remainder_rank == 0:
+            return rows, n
+
+
+def test_k5q_dense_row_minimum_distance():
+    """BZ on a code whose Gammas keep 127 stored columns, with a dense row
+    and a planted light codeword (U = 12 after round 1, so round 4 runs with
+    thr = U - g = 8 against a prefix of stored weight 127): distance, trace,
+    status and counts equal the C oracle's, K5q forced for every g >= 4."""
+    rows, n = _dense_systematic(127, 11, 12)
+    want = oracle.minimum_distance(rows, n, max_g=4)
+    rep = minimum_distance(BitMatrix(rows, n), EngineConfig(engine="mxf4q", max_g=4))
+    assert rep.bounds_trace == [tuple(t) for t in want["bounds_trace"]]
+    assert rep.distance == want["distance"] == 12
+    assert rep.counters.combinations == want["combinations"]
+    assert _native.context(0).elided() == 0b11  # both Gammas store n - k = 127 columns
 
 
 @pytest.mark.parametrize("engine_name", ["auto", "mxf4", "popc"])

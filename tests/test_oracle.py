@@ -105,3 +105,15 @@ def test_cfg5_rounds_up_to_6(cfg5_golden):
     fx = cfg5_golden
     rep = oracle.minimum_distance(hexrows(fx["rows"]), fx["n"], max_g=6)
     assert rep["bounds_trace"] == [tuple(t) for t in fx["bounds_trace"][:6]]
+
+
+@pytest.mark.parametrize("name,seed", [("cfg1", 1), ("cfg1", 2), ("cfg2", 2), ("cfg3", 1),
+                                       ("cfg5", 7)])
+def test_oracle_draw_matches_configs(name, seed):
+    """bench.py's CPU arm draws its matrix through oracle.draw_code (no
+    product import): the rows equal the product's configs.code draw."""
+    from paper_1603_06757_b200.configs import CONFIGS, code
+
+    c = CONFIGS[name]
+    G, _, _ = code(name, seed)
+    assert oracle.draw_code(c.k, c.n, seed, c.target) == list(G.rows)
