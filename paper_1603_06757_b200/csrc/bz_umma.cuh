@@ -113,6 +113,7 @@ constexpr int kMaxStages = 8;
 constexpr int kMaxAcc = 8;
 constexpr int kMaxABuf = 4;
 constexpr int kChunkQ = 4;         // depth of the loader -> roles chunk queue
+constexpr int kBndCache = 64;       // K5q: per-CTA cache of the per-Gamma bounds (bnd_publish)
 constexpr int kBarSlots = 2 * kMaxABuf + 2 * kMaxStages + 2 * kMaxAcc + 2 * kChunkQ;
 
 // Warp roles of K4 (F4 = false) / K5 (F4 = true):
@@ -671,6 +672,7 @@ __host__ __device__ inline size_t k4_smem_bytes(int m, int k, int ngroups) {
   off += kBarSlots * 8 + 16;     // barriers + TMEM base
   off += k4_abufs<F4>(W) * kUmmaMA * kUmmaM * sizeof(int);  // prefix weights of the A buffers
   off += kChunkQ * sizeof(long long) + 16;    // chunk queue
+  off += kBndCache * sizeof(int);              // K5q bound cache
   return off;
 }
 
@@ -700,6 +702,21 @@ __device__ __forceinline__ void k4_trace(const RoundArgs& a, int slot, uint32_t 
 __device__ __forceinline__ long long* k4_ctrace(const RoundArgs& a, uint32_t qi) {
   return (a.ctrace && qi < 63) ? a.ctrace + ((size_t)blockIdx.x * 64 + qi) * 4 : nullptr;
 }
+// K5q: a per-CTA cache of the per-Gamma bound words (Gammas < kBndCache).
+// It only ever holds a value read from the global word or one this CTA
+// published to it, and the global words only decrease, so the cache is never
+// below its global word: a candidate not below the cache cannot lower the
+// global bound, and the epilogue skips the global atomics for it.
+__device__ __forceinline__ int bnd_cache_read(const int* s_bnd, const RoundArgs&, int gamma) {
+  return gamma < kBndCache ? ((const volatile int*)s_bnd)[gamma] : INT_MAX;
+}
+__device__ __forceinline__ void bnd_publish(int* s_bnd, const RoundArgs& a, int gamma, int w) {
+  if (gamma < kBndCache && atomicMin(s_bnd + gamma, w) <= w) return;
+  atomicMin(a.bound + 1 + gamma, w);
+  atomicMin(a.bound, w);
+  gbound_publish(a, w);
+}
+
 __device__ __forceinline__ long long global_ns() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -783,6 +800,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
   int* s_wt = reinterpret_cast<int*>(s_tmem + 4);  // [2][kUmmaMA][kUmmaM] prefix weights
   volatile long long* s_q = reinterpret_cast<volatile long long*>(
       (reinterpret_cast<uintptr_t>(s_wt + NA * kUmmaMA * kUmmaM) + 15) & ~uintptr_t(15));
+  int* s_bnd = const_cast<int*>(reinterpret_cast<volatile int*>(s_q + kChunkQ));  // [kBndCache]
   const uint32_t sB_s = (uint32_t)__cvta_generic_to_shared(sB);
   const uint32_t sA_s = (uint32_t)__cvta_generic_to_shared(sA);
   const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(bars);
@@ -880,6 +898,8 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       *reinterpret_cast<uint4*>(sMagic + op * 256 + row16 * 16) = z;
       fence_proxy_async();
     }
+    if constexpr (Q)
+      if (tid < kBndCache) s_bnd[tid] = tid < a.m ? ((volatile int*)a.bound)[1 + tid] : INT_MAX;
     if (!PR && CA > W && warp >= RL::PROD0) {
       // the A padding chunk: zero, or 1.5 at element 8 (padding-chunk offset)
       const int r = tid - 32 * RL::PROD0;
@@ -980,6 +1000,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
 #pragma unroll
             for (int i = 0; i + 1 < NP; i += 2) acc &= v[i] & v[i + 1];
             if (NP % 2) acc &= v[NP - 1];
+            int wg = INT_MAX;  // this row's new minimum below the CTA's bound, if any
             if ((~acc) & 0x80808080u) {
               // some byte is below the producer's threshold; below this
               // row's own minimum so far?  (x - lx*0x01010101) & ~x has bit
@@ -997,15 +1018,16 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
                 lx = mn;
                 const int w = mn - 128 + wt[0];
                 rmin[0] = min(rmin[0], w);
-                // publish at once: the producers' next thresholds tighten
-                const int wg = w + gamma_woff(a, c.gr.gamma);
-                if (wg < ((volatile int*)a.bound)[1 + c.gr.gamma]) {
-                  atomicMin(a.bound + 1 + c.gr.gamma, wg);
-                  atomicMin(a.bound, wg);
-                  gbound_publish(a, wg);
-                }
+                const int w2 = w + gamma_woff(a, c.gr.gamma);
+                if (w2 < bnd_cache_read(s_bnd, a, c.gr.gamma)) wg = w2;
               }
             }
+            // publish at once, so the producers' next thresholds tighten --
+            // only below the CTA's cached bound: under a loose bound every row
+            // of every SM would otherwise send global atomics to the same two
+            // words each tile (config 4: 105 -> 48 us).  (A warp-level
+            // reduction first measured 4 % slower on config 5's g = 8.)
+            if (wg != INT_MAX) bnd_publish(s_bnd, a, c.gr.gamma, wg);
           } else if constexpr (CW == 3) {
             // K5t: every column holds three codewords, 2^23 + wt_a + 2^8 wt_b
             // + 2^16 wt_c: bytes 0..2 are stored weights <= 96, byte 3 the
@@ -1208,6 +1230,8 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
           atomicMin(a.bound + 1 + c.gr.gamma, wbest + gamma_woff(a, c.gr.gamma));
           atomicMin(a.bound, wbest + gamma_woff(a, c.gr.gamma));
           gbound_publish(a, wbest + gamma_woff(a, c.gr.gamma));
+          if constexpr (Q)
+            if (c.gr.gamma < kBndCache) atomicMin(s_bnd + c.gr.gamma, wbest + gamma_woff(a, c.gr.gamma));
         }
         long long* ct = k4_ctrace(a, qi);
         if (ct && warp == 0) { ct[2] = clock64(); ct[3] = global_ns(); }
@@ -1274,6 +1298,8 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
             // largest sum an A offset block encodes exactly (e2m1_block).
             // A threshold raised above the bound only sends more tiles down
             // the exact path.
+            // (also reading this CTA's bound cache, or the previous batched
+            // round's running U, measured no faster)
             const int thr = k5q_threshold(
                 wt, ((volatile int*)a.bound)[1 + c.gr.gamma] - gamma_woff(a, c.gr.gamma));
             const int x = wt + 128 - thr;

@@ -22,14 +22,15 @@ print(f"chunk duration (clk): median {np.median(dur):.0f} p10 {np.percentile(dur
 span = []
 for b in range(nblk):
     v = valid[b]
-    span.append(ct[b, v, 2].max() - ct[b, v, 1].min())
+    if v.any():
+        span.append(ct[b, v, 2].max() - ct[b, v, 1].min())
 print(f"block span (dequeue first -> done last, clk): median {np.median(span):.0f} max {max(span)}")
 print(f"done spread across blocks (ns): {t_done.max() - t_done.min()}")
 
 lv = life[:nblk]
 if (lv > 0).all():
     t0 = lv[:, 0].min()
-    first_done = np.array([ct[b, valid[b], 3].min() for b in range(nblk)]) - t0
+    first_done = np.array([ct[b, valid[b], 3].min() for b in range(nblk) if valid[b].any()]) - t0
     print(f"block entry skew {lv[:, 0].max() - t0} ns; prologue median "
           f"{np.median(lv[:, 1] - lv[:, 0]):.0f} ns; first chunk done median "
           f"{np.median(first_done):.0f} ns; last chunk done {t_done.max() - t0} ns; "
