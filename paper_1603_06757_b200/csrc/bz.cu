@@ -641,12 +641,34 @@ int launch_tc(bz_ctx* ctx, const RoundArgs& a) {
 
 #endif
 
+// One tensor-core launch of `count` consecutive rounds (K5Batch): their
+// plans staged side by side (or all read from global memory when they do not
+// fit), their chunk spaces concatenated on round 0's cursor.
 template <int W, bool F4, int CW = 1>
-int launch_umma(bz_ctx* ctx, const RoundArgs& a0) {
-  RoundArgs a = a0;
-  size_t smem = bz::k4_smem_bytes<W, F4, CW>(a.m, a.k, a.ngroups);
+int launch_umma(bz_ctx* ctx, const RoundArgs* as, int count) {
+  bz::K5Batch bt{};
+  int total_groups = 0;
+  unsigned long long mine_total = 0;
+  for (int i = 0; i < count; ++i) {
+    bt.a[i] = as[i];
+    bt.goff[i] = total_groups;
+    total_groups += as[i].ngroups;
+    const RoundArgs& r = as[i];
+    mine_total += r.nchunks > (unsigned long long)r.shard
+                      ? (r.nchunks - r.shard + r.nshards - 1) / r.nshards : 0ull;
+    bt.cend[i] = mine_total;
+  }
+  bt.count = count;
+  for (int i = 0; i < count; ++i) {
+    bt.a[i].sgroups_cap = total_groups;
+    bt.a[i].trace = as[count - 1].trace;
+    bt.a[i].ctrace = as[count - 1].ctrace;
+  }
+  RoundArgs& a = bt.a[0];
+  size_t smem = bz::k4_smem_bytes<W, F4, CW>(a.m, a.k, total_groups);
   if (smem > kMaxSmem) {
-    a.groups_global = 1;  // a plan too large to stage: read from global memory
+    // plans too large to stage: read from global memory
+    for (int i = 0; i < count; ++i) bt.a[i].groups_global = 1;
     smem = bz::k4_smem_bytes<W, F4, CW>(a.m, a.k, 0);
   }
   if (smem > kMaxSmem)
@@ -661,8 +683,7 @@ int launch_umma(bz_ctx* ctx, const RoundArgs& a0) {
       have[ctx->device] = smem;
     }
   }
-  const unsigned long long mine = (a.nchunks + a.nshards - 1 - a.shard) / a.nshards;
-  long long blocks = std::max(1ll, std::min((long long)ctx->sm_count, (long long)mine));
+  long long blocks = std::max(1ll, std::min((long long)ctx->sm_count, (long long)mine_total));
   bz::K4Tables tabs{};
   if (F4) {
     for (int i = 0; i < 3; ++i) {
@@ -686,7 +707,7 @@ int launch_umma(bz_ctx* ctx, const RoundArgs& a0) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = ctx->pdl_next ? 1 : 0;
-  CK(cudaLaunchKernelEx(&cfg, bz::k4_round_umma<W, F4, CW>, a, tabs));
+  CK(cudaLaunchKernelEx(&cfg, bz::k4_round_umma<W, F4, CW>, bt, tabs));
   ctx->launches += 1;
   return BZ_OK;
 }
@@ -792,34 +813,37 @@ int ensure_triples(bz_ctx* ctx, int) {
 }
 #endif
 
+// `count` consecutive rounds of the same tensor-core shape in one launch
+// (count = 1 for every other kernel)
 template <int W>
-int launch_w(bz_ctx* ctx, const RoundArgs& a, bool hist, const PlanShape& shape) {
+int launch_w(bz_ctx* ctx, const RoundArgs* as, int count, bool hist, const PlanShape& shape) {
+  const RoundArgs& a = as[0];
 #if BZ_LEGACY_KERNELS
   if constexpr (W == 1 || W == 3) {
-    if (shape.kernel == 6) return launch_umma<W, true, 2>(ctx, a);
-    if (shape.kernel == 7) return launch_umma<W, true, 3>(ctx, a);
+    if (shape.kernel == 6) return launch_umma<W, true, 2>(ctx, as, count);
+    if (shape.kernel == 7) return launch_umma<W, true, 3>(ctx, as, count);
   }
-  if (shape.kernel == 4) return launch_umma<W, false>(ctx, a);
+  if (shape.kernel == 4) return launch_umma<W, false>(ctx, as, count);
   if (shape.kernel == 3) return launch_tc<W>(ctx, a);
 #endif
   if constexpr (W <= 4)
-    if (shape.kernel == 8) return launch_umma<W, true, 4>(ctx, a);
+    if (shape.kernel == 8) return launch_umma<W, true, 4>(ctx, as, count);
   if (shape.kernel >= 3 && shape.kernel != 5)
     return fail(ctx, BZ_ERR_STATE, "kernel %d not available at W = %d", shape.kernel, W);
-  if (shape.kernel == 5) return launch_umma<W, true>(ctx, a);
+  if (shape.kernel == 5) return launch_umma<W, true>(ctx, as, count);
   return shape.depth == 2 ? launch_wd<W, 2>(ctx, a, hist) : launch_wd<W, 1>(ctx, a, hist);
 }
 
-int launch(bz_ctx* ctx, const RoundArgs& a, bool hist, const PlanShape& depth) {
+int launch(bz_ctx* ctx, const RoundArgs* as, int count, bool hist, const PlanShape& depth) {
   switch (ctx->w32) {
-    case 1: return launch_w<1>(ctx, a, hist, depth);
-    case 2: return launch_w<2>(ctx, a, hist, depth);
-    case 3: return launch_w<3>(ctx, a, hist, depth);
-    case 4: return launch_w<4>(ctx, a, hist, depth);
-    case 5: return launch_w<5>(ctx, a, hist, depth);
-    case 6: return launch_w<6>(ctx, a, hist, depth);
-    case 7: return launch_w<7>(ctx, a, hist, depth);
-    case 8: return launch_w<8>(ctx, a, hist, depth);
+    case 1: return launch_w<1>(ctx, as, count, hist, depth);
+    case 2: return launch_w<2>(ctx, as, count, hist, depth);
+    case 3: return launch_w<3>(ctx, as, count, hist, depth);
+    case 4: return launch_w<4>(ctx, as, count, hist, depth);
+    case 5: return launch_w<5>(ctx, as, count, hist, depth);
+    case 6: return launch_w<6>(ctx, as, count, hist, depth);
+    case 7: return launch_w<7>(ctx, as, count, hist, depth);
+    case 8: return launch_w<8>(ctx, as, count, hist, depth);
     default: return fail(ctx, BZ_ERR_TOO_LARGE, "unsupported word count %d", ctx->w32);
   }
 }
@@ -985,35 +1009,47 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   CK(cudaEventRecord(ctx->ev_k0, ctx->stream));
   bool prev_round = false;
   const bool timed = count > 1;
+  // the launch holding the largest round is bracketed by events: rounds
+  // [big_lo, big_hi)
+  int big_lo = big, big_hi = big + 1;
   for (int i = 0; i < count; ++i) {
-    if (timed && i == big) {
-      CK(cudaEventRecord(ctx->ev_round[0], ctx->stream));
-      prev_round = false;
-    }
     if (!todo[i].run) continue;
-    ctx->pdl_next = prev_round && !debug;
-    // consecutive small K1 rounds of the same depth share one launch
+    // consecutive small K1 rounds of the same depth share one launch, and so
+    // do consecutive rounds on the same tensor-core kernel (K5 / K5q: one
+    // persistent launch runs them back to back, no launch, prologue or tail
+    // between them)
     int f = 1;
     size_t fused_groups = (size_t)todo[i].a.ngroups;
-    while (!hist && todo[i].shape.kernel == 1 && f < bz::kK1MaxFused && i + f < count &&
-           todo[i + f].run && todo[i + f].shape.kernel == 1 &&
-           todo[i + f].shape.depth == todo[i].shape.depth && !debug && i + f != big &&
-           (fused_groups + todo[i + f].a.ngroups) * sizeof(bz::Group) <=
-               (size_t)bz::kK1FusedGroupBytes) {
+    const int kern = todo[i].shape.kernel;
+    const bool tensor = kern == 5 || kern == 8;
+    while (!hist && !debug && i + f < count && todo[i + f].run &&
+           todo[i + f].shape.kernel == kern &&
+           ((kern == 1 && f < bz::kK1MaxFused && todo[i + f].shape.depth == todo[i].shape.depth &&
+             i + f != big &&
+             (fused_groups + todo[i + f].a.ngroups) * sizeof(bz::Group) <=
+                 (size_t)bz::kK1FusedGroupBytes) ||
+            (tensor && f < bz::kK5MaxFused))) {
       fused_groups += todo[i + f].a.ngroups;
       ++f;
     }
-    if (f > 1) {
-      std::vector<RoundArgs> as;
-      for (int q = 0; q < f; ++q) as.push_back(todo[i + q].a);
-      rc = launch_fused(ctx, as.data(), f, todo[i].shape.depth);
-    } else {
-      rc = launch(ctx, todo[i].a, hist, todo[i].shape);
+    const bool has_big = timed && i <= big && big < i + f;
+    if (has_big) {
+      CK(cudaEventRecord(ctx->ev_round[0], ctx->stream));
+      prev_round = false;
+      big_lo = i;
+      big_hi = i + f;
     }
+    ctx->pdl_next = prev_round && !debug;
+    std::vector<RoundArgs> as;
+    for (int q = 0; q < f; ++q) as.push_back(todo[i + q].a);
+    if (f > 1 && kern == 1)
+      rc = launch_fused(ctx, as.data(), f, todo[i].shape.depth);
+    else
+      rc = launch(ctx, as.data(), f, hist, todo[i].shape);
     ctx->pdl_next = false;
     if (rc) return rc;
     prev_round = true;
-    if (timed && i <= big && big < i + f) {
+    if (has_big) {
       CK(cudaEventRecord(ctx->ev_round[1], ctx->stream));
       prev_round = false;
     }
@@ -1039,15 +1075,21 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   if (count == 1) {
     ctx->round_ms[0] = ctx->last_kernel_ms;
   } else {
+    // the bracketed launch's time over its rounds, the rest of the batch
+    // time over the other rounds, by combination count
     float big_ms = 0.f;
     CK(cudaEventElapsedTime(&big_ms, ctx->ev_round[0], ctx->ev_round[1]));
-    ctx->round_ms[big] = big_ms;
-    double rest = 0;
+    double in_big = 0, rest = 0;
     for (int i = 0; i < count; ++i)
-      if (i != big && todo[i].run) rest += binom_d(ctx->k, todo[i].a.g);
-    for (int i = 0; i < count; ++i)
-      if (i != big && todo[i].run && rest > 0)
-        ctx->round_ms[i] = (float)((ctx->last_kernel_ms - big_ms) * binom_d(ctx->k, todo[i].a.g) / rest);
+      if (todo[i].run) (i >= big_lo && i < big_hi ? in_big : rest) += binom_d(ctx->k, todo[i].a.g);
+    for (int i = 0; i < count; ++i) {
+      if (!todo[i].run) continue;
+      const double share = binom_d(ctx->k, todo[i].a.g);
+      if (i >= big_lo && i < big_hi)
+        ctx->round_ms[i] = in_big > 0 ? (float)(big_ms * share / in_big) : 0.f;
+      else if (rest > 0)
+        ctx->round_ms[i] = (float)((ctx->last_kernel_ms - big_ms) * share / rest);
+    }
   }
   if (ctrace) {
     // BZ_K4_DEBUG & 32: per-chunk timeline to $BZ_K4_CTRACE (raw int64)

@@ -114,6 +114,7 @@ constexpr int kMaxAcc = 8;
 constexpr int kMaxABuf = 4;
 constexpr int kChunkQ = 4;         // depth of the loader -> roles chunk queue
 constexpr int kBndCache = 64;       // K5q: per-CTA cache of the per-Gamma bounds (bnd_publish)
+constexpr int kBndPerRound = kBndCache / 4;  // ... for Gammas < 16 of each fused round
 constexpr int kBarSlots = 2 * kMaxABuf + 2 * kMaxStages + 2 * kMaxAcc + 2 * kChunkQ;
 
 // Warp roles of K4 (F4 = false) / K5 (F4 = true):
@@ -553,6 +554,21 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t* v) {
   }
 }
 
+// Consecutive rounds of one bz_rounds call on the same tensor-core kernel in
+// ONE launch (K5q rounds g = 5..8 of config 5): the rows, prefix table and
+// binomials are staged once, the rounds' plans side by side, and the rounds'
+// chunk spaces concatenated into one cursor (round 0's counter), so the
+// persistent CTAs run the rounds back to back without a launch, prologue or
+// tail between them.  A queue entry carries its round in bits 56..63.
+constexpr int kK5MaxFused = 4;
+struct K5Batch {
+  RoundArgs a[kK5MaxFused];
+  unsigned long long cend[kK5MaxFused];  // this shard's chunks of rounds <= r, cumulative
+  int goff[kK5MaxFused];                 // round r's first group in the staged plans
+  int count;
+};
+constexpr int kQRoundShift = 56;
+
 // Suffix tables of one round: level D = 3 + i at t[i], stride_rows[i] rows
 // per Gamma (K4 uses t[0] only).
 struct K4Tables {
@@ -707,11 +723,12 @@ __device__ __forceinline__ long long* k4_ctrace(const RoundArgs& a, uint32_t qi)
 // published to it, and the global words only decrease, so the cache is never
 // below its global word: a candidate not below the cache cannot lower the
 // global bound, and the epilogue skips the global atomics for it.
-__device__ __forceinline__ int bnd_cache_read(const int* s_bnd, const RoundArgs&, int gamma) {
-  return gamma < kBndCache ? ((const volatile int*)s_bnd)[gamma] : INT_MAX;
+__device__ __forceinline__ int bnd_cache_read(const int* s_bnd, int round, int gamma) {
+  return gamma < kBndPerRound ? ((const volatile int*)s_bnd)[round * kBndPerRound + gamma] : INT_MAX;
 }
-__device__ __forceinline__ void bnd_publish(int* s_bnd, const RoundArgs& a, int gamma, int w) {
-  if (gamma < kBndCache && atomicMin(s_bnd + gamma, w) <= w) return;
+__device__ __forceinline__ void bnd_publish(int* s_bnd, const RoundArgs& a, int round, int gamma,
+                                            int w) {
+  if (gamma < kBndPerRound && atomicMin(s_bnd + round * kBndPerRound + gamma, w) <= w) return;
   atomicMin(a.bound + 1 + gamma, w);
   atomicMin(a.bound, w);
   gbound_publish(a, w);
@@ -755,7 +772,10 @@ __device__ __forceinline__ K4Chunk k4_decode(const Group* sg, int ngroups,
 // accumulator type (s32 read as packed s16 / f32) and tile geometry.
 template <int W, bool F4, int CW>
 __global__ void __launch_bounds__(K4Roles<F4, CW>::THREADS, 1)
-k4_round_umma(const RoundArgs a, const K4Tables tabs) {
+k4_round_umma(const K5Batch bt, const K4Tables tabs) {
+  // round 0's arguments: everything the fused rounds share (rows, prefix
+  // table, m, k, n, binomials, the chunk cursor, debug and trace switches)
+  const RoundArgs& a = bt.a[0];
   constexpr bool PR = CW > 1;  // K5p (CW = 2) / K5t (CW = 3) / K5q (CW = 4)
   constexpr bool Q = CW == 4;  // K5q: two codewords as bytes, block16 scales
   constexpr int NC = k5_ncw(CW);  // codewords per accumulator column
@@ -858,12 +878,20 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
   tc_fence_before();
   stage<W>(a, srows, spx, sgroups, smem);  // ends with __syncthreads
   const unsigned long long* sbinom = smem_binom<W>(smem, a);
+  // the other fused rounds' plans after round 0's (made visible by the
+  // __syncthreads below)
+  for (int rr = 1; rr < bt.count; ++rr)
+    if (!a.groups_global) stage_groups(bt.a[rr], sgroups + bt.goff[rr]);
+  // round rr's plan: staged, or in global memory
+  auto plan_of = [&](int rr) -> const Group* {
+    return a.groups_global ? bt.a[rr].groups : sgroups + bt.goff[rr];
+  };
   tc_fence_after();
   const uint32_t tmem = *s_tmem;
   // a batched round starts from the U its predecessor ended with (the
   // running U the reference clips with, m/engine.py:209-211): chained on this
   // device and/or through the shared mirror (round_start)
-  round_start(a);
+  for (int rr = 0; rr < bt.count; ++rr) round_start(bt.a[rr]);
   if constexpr (F4) {
     // unit block scales (ue8m0 0x7F = 2^0) in TMEM columns [kSfCol, 512);
     // the zero K-padding chunk of both A buffers (odd W)
@@ -899,7 +927,10 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       fence_proxy_async();
     }
     if constexpr (Q)
-      if (tid < kBndCache) s_bnd[tid] = tid < a.m ? ((volatile int*)a.bound)[1 + tid] : INT_MAX;
+      if (tid < kBndCache) {
+        const int rr = tid / kBndPerRound, j = tid % kBndPerRound;
+        s_bnd[tid] = rr < bt.count && j < a.m ? ((volatile int*)bt.a[rr].bound)[1 + j] : INT_MAX;
+      }
     if (!PR && CA > W && warp >= RL::PROD0) {
       // the A padding chunk: zero, or 1.5 at element 8 (padding-chunk offset)
       const int r = tid - 32 * RL::PROD0;
@@ -931,14 +962,16 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       __syncwarp();
       if (lane == 0) mbar_arrive(qempty(qs));
       if (qchunk < 0) break;
-      const unsigned long long chunk = (unsigned long long)qchunk;
-      const K4Chunk c = k4_decode<TR>(sgroups, a.ngroups, chunk, k);
+      const int rr = (int)((unsigned long long)qchunk >> kQRoundShift);
+      const RoundArgs& ar = bt.a[rr];
+      const unsigned long long chunk = (unsigned long long)qchunk & ((1ull << kQRoundShift) - 1);
+      const K4Chunk c = k4_decode<TR>(plan_of(rr), ar.ngroups, chunk, k);
       k4_trace_chunk(a, toff, c.gr.ell, tcount);
       int best = INT_MAX;
       // K5t: stored weights below thr can lower this Gamma's bound
       int thr = 127;
       if constexpr (CW == 3)
-        thr = max(0, min(127, ((volatile int*)a.bound)[1 + c.gr.gamma] - gamma_woff(a, c.gr.gamma)));
+        thr = max(0, min(127, ((volatile int*)ar.bound)[1 + c.gr.gamma] - gamma_woff(ar, c.gr.gamma)));
       for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
         const int ab = grp % NA;
         mbar_wait_sel<1>(afull(ab), (grp / NA) & 1);
@@ -1018,8 +1051,8 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
                 lx = mn;
                 const int w = mn - 128 + wt[0];
                 rmin[0] = min(rmin[0], w);
-                const int w2 = w + gamma_woff(a, c.gr.gamma);
-                if (w2 < bnd_cache_read(s_bnd, a, c.gr.gamma)) wg = w2;
+                const int w2 = w + gamma_woff(ar, c.gr.gamma);
+                if (w2 < bnd_cache_read(s_bnd, rr, c.gr.gamma)) wg = w2;
               }
             }
             // publish at once, so the producers' next thresholds tighten --
@@ -1027,7 +1060,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
             // of every SM would otherwise send global atomics to the same two
             // words each tile (config 4: 105 -> 48 us).  (A warp-level
             // reduction first measured 4 % slower on config 5's g = 8.)
-            if (wg != INT_MAX) bnd_publish(s_bnd, a, c.gr.gamma, wg);
+            if (wg != INT_MAX) bnd_publish(s_bnd, ar, rr, c.gr.gamma, wg);
           } else if constexpr (CW == 3) {
             // K5t: every column holds three codewords, 2^23 + wt_a + 2^8 wt_b
             // + 2^16 wt_c: bytes 0..2 are stored weights <= 96, byte 3 the
@@ -1227,11 +1260,12 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
         if (wbest < INT_MAX / 2) {
           // fire-and-forget reductions (RED.MIN): no load round trip stalls
           // the epilogue at a chunk boundary
-          atomicMin(a.bound + 1 + c.gr.gamma, wbest + gamma_woff(a, c.gr.gamma));
-          atomicMin(a.bound, wbest + gamma_woff(a, c.gr.gamma));
-          gbound_publish(a, wbest + gamma_woff(a, c.gr.gamma));
+          const int wb = wbest + gamma_woff(ar, c.gr.gamma);
+          atomicMin(ar.bound + 1 + c.gr.gamma, wb);
+          atomicMin(ar.bound, wb);
+          gbound_publish(ar, wb);
           if constexpr (Q)
-            if (c.gr.gamma < kBndCache) atomicMin(s_bnd + c.gr.gamma, wbest + gamma_woff(a, c.gr.gamma));
+            if (c.gr.gamma < kBndPerRound) atomicMin(s_bnd + rr * kBndPerRound + c.gr.gamma, wb);
         }
         long long* ct = k4_ctrace(a, qi);
         if (ct && warp == 0) { ct[2] = clock64(); ct[3] = global_ns(); }
@@ -1248,8 +1282,10 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       __syncwarp();
       if (lane == 0) mbar_arrive(qempty(qs));
       if (qchunk < 0) break;
-      const unsigned long long chunk = (unsigned long long)qchunk;
-      const K4Chunk c = k4_decode<TR>(sgroups, a.ngroups, chunk, k);
+      const int rr = (int)((unsigned long long)qchunk >> kQRoundShift);
+      const RoundArgs& ar = bt.a[rr];
+      const unsigned long long chunk = (unsigned long long)qchunk & ((1ull << kQRoundShift) - 1);
+      const K4Chunk c = k4_decode<TR>(plan_of(rr), ar.ngroups, chunk, k);
       const unsigned long long first = c.bfirst + (unsigned long long)r * c.gr.ppl;
       long long cnt = 0;
       if (first < c.gr.nprefix) {
@@ -1260,7 +1296,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       const uint32_t* PX = spx + c.gr.gamma * (k + 1) * px_stride(W);
       Walker<W> wk;
       // rows without prefixes duplicate the block's first prefix
-      wk.init(cnt > 0 ? first : c.bfirst, a.g - 1 - c.gr.depth, c.gr.ell, R, a.binom, sbinom);
+      wk.init(cnt > 0 ? first : c.bfirst, ar.g - 1 - c.gr.depth, c.gr.ell, R, a.binom, sbinom);
       for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
         const int ab = grp % NA;
         mbar_wait_sel<4>(aempty(ab), ((grp / NA) & 1) ^ 1);
@@ -1298,10 +1334,14 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
             // largest sum an A offset block encodes exactly (e2m1_block).
             // A threshold raised above the bound only sends more tiles down
             // the exact path.
-            // (also reading this CTA's bound cache, or the previous batched
-            // round's running U, measured no faster)
-            const int thr = k5q_threshold(
-                wt, ((volatile int*)a.bound)[1 + c.gr.gamma] - gamma_woff(a, c.gr.gamma));
+            // The bound: this Gamma's word and this CTA's cache of it, and in
+            // a fused launch the running minima of the earlier rounds (they
+            // ran first, and the host's U will not exceed them; without them
+            // a round would start from its loose start bound and send its
+            // first tiles down the exact path).
+            int ub = min(((volatile int*)ar.bound)[1 + c.gr.gamma], bnd_cache_read(s_bnd, rr, c.gr.gamma));
+            for (int q = 0; q < rr; ++q) ub = min(ub, ((volatile const int*)bt.a[q].bound)[0]);
+            const int thr = k5q_threshold(wt, ub - gamma_woff(ar, c.gr.gamma));
             const int x = wt + 128 - thr;
             *reinterpret_cast<uint4*>(dst + umma_off_c(r, W, CA)) = pad_chunk(x, 0);
             *reinterpret_cast<uint4*>(dst + umma_off_c(r, W + 1, CA)) = pad_chunk(x, 128);
@@ -1326,7 +1366,7 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
       if (lane == 0 && tot) {
         const long long cols = min((long long)c.tile_hi * TR, (long long)c.slice) -
                                (long long)c.tile_lo * TR;
-        atomicAdd(a.combos + c.gr.gamma, (unsigned long long)tot * (unsigned long long)cols);
+        atomicAdd(ar.combos + c.gr.gamma, (unsigned long long)tot * (unsigned long long)cols);
       }
     }
   } else if (warp < RL::LOAD) {
@@ -1352,8 +1392,10 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
         __syncwarp();
         if (lane == 0) mbar_arrive(qempty(qs));
         if (qchunk < 0) break;
-        const unsigned long long chunk = (unsigned long long)qchunk;
-        const K4Chunk c = k4_decode<TR>(sgroups, a.ngroups, chunk, k);
+        const int rr = (int)((unsigned long long)qchunk >> kQRoundShift);
+        const RoundArgs& ar = bt.a[rr];
+        const unsigned long long chunk = (unsigned long long)qchunk & ((1ull << kQRoundShift) - 1);
+        const K4Chunk c = k4_decode<TR>(plan_of(rr), ar.ngroups, chunk, k);
         k4_trace_chunk(a, toff, c.gr.ell, tcount);
         const int ntile = c.tile_hi - c.tile_lo;
         for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
@@ -1488,13 +1530,21 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
             if (!ok) return;
           }
           // next chunk of this shard, or -1 (done, or U reached L_prev)
+          // (the fused rounds' chunk spaces one after the other on round
+          // 0's cursor; round_done: this round's or the previous round's
+          // running minimum -- local, chained, or any rank's through the
+          // shared mirror -- already meets L_prev, so the run has ended at
+          // or before this round and every later round is void too)
           const unsigned long long cidx = atomicAdd(a.counter, 1ull);
-          const unsigned long long ch = cidx * (unsigned long long)a.nshards + a.shard;
-          // (round_done: this round's or the previous round's running
-          // minimum -- local, chained, or any rank's through the shared
-          // mirror -- already meets L_prev)
+          int rq = 0;
+          while (rq + 1 < bt.count && cidx >= bt.cend[rq]) ++rq;
+          const RoundArgs& aq = bt.a[rq];
+          const unsigned long long local = cidx - (rq > 0 ? bt.cend[rq - 1] : 0ull);
+          const unsigned long long ch = local * (unsigned long long)aq.nshards + aq.shard;
           (void)vb;
-          const long long qchunk = (ch < a.nchunks && !round_done(a)) ? (long long)ch : -1;
+          const long long qchunk = (cidx < bt.cend[bt.count - 1] && ch < aq.nchunks && !round_done(aq))
+                                       ? (long long)(((unsigned long long)rq << kQRoundShift) | ch)
+                                       : -1;
           s_q[qs] = qchunk;
           long long* ct = k4_ctrace(a, qpub);
           if (ct) { ct[0] = qchunk; ct[1] = clock64(); }
@@ -1507,8 +1557,10 @@ k4_round_umma(const RoundArgs a, const K4Tables tabs) {
         publish(qload, qload == qpub);
         const long long qchunk = s_q[qload % kChunkQ];
         if (qchunk < 0) break;
-        const unsigned long long chunk = (unsigned long long)qchunk;
-        const K4Chunk c = k4_decode<TR>(sgroups, a.ngroups, chunk, k);
+        const int rr = (int)((unsigned long long)qchunk >> kQRoundShift);
+        const RoundArgs& ar = bt.a[rr];
+        const unsigned long long chunk = (unsigned long long)qchunk & ((1ull << kQRoundShift) - 1);
+        const K4Chunk c = k4_decode<TR>(plan_of(rr), ar.ngroups, chunk, k);
         k4_trace_chunk(a, toff, c.gr.ell, bcount);
         const int lvl = c.gr.depth - 3;  // suffix table of this group's level
         const uint8_t* tsrc =
