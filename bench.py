@@ -234,6 +234,36 @@ def section6_c1(cfg) -> dict:
             "value": rep.counters.combinations / dt, "unit": UNIT}
 
 
+def configs_wall(cfg) -> dict:
+    """Side measurement: wall time to d of BASELINE.json configs 1-3 (two
+    seeds each, the Appendix-A generator) through the public API
+    minimum_distance(G, ...) from a host BitMatrix -- Gamma family, upload,
+    every round, read-back -- median of 5 after one warm-up.  These configs
+    are launch-latency bound: the wall time to d, not the
+    combination rate, is their number.  The reference reports the same
+    `elapsed` (m/engine.py:168, :246)."""
+    from paper_1603_06757_b200 import minimum_distance
+    from paper_1603_06757_b200.configs import code
+
+    out = {}
+    for name in ("cfg1", "cfg2", "cfg3"):
+        for seed in (1, 2):
+            G, _, _ = code(name, seed)
+            minimum_distance(G, cfg)
+            walls = []
+            for _ in range(5):
+                t0 = time.perf_counter()
+                rep = minimum_distance(G, cfg)
+                walls.append(time.perf_counter() - t0)
+            wall = statistics.median(walls)
+            out[f"{name}_seed{seed}"] = {
+                "n": G.num_cols, "k": G.num_rows, "d": rep.distance, "g_final": rep.g_reached,
+                "trace": [list(t) for t in rep.bounds_trace],
+                "combinations": rep.counters.combinations, "wall_ms": round(wall * 1e3, 3),
+                "value": rep.counters.combinations / wall, "unit": UNIT}
+    return out
+
+
 def issued_macs(w: int) -> int:
     """MACs per combination the K5 family issues for W stored 32-bit words:
     ceil(W/2) K = 64 MMAs (the A/table offset chunk rides in the padding of
@@ -547,11 +577,18 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (largest round), and the other
-    # kernels of the library on the same launch for comparison
+    # ---- roofline of the dominant launch: the tensor-core launch that runs
+    # rounds g >= 5 back to back (K5Batch; the library fuses consecutive
+    # rounds of one tensor-core kernel).  Its device time is bracketed by
+    # CUDA events on the library stream inside the timed steps (bz_round_ms
+    # splits it over its rounds by combination count, so the largest round's
+    # combinations / its share is the launch's rate); the other kernels of
+    # the library and the largest round alone are timed after the region.
     peaks = ctx.measure_int_peaks(w_eff)
     top_ms = statistics.median(g_top_ms)
     achieved = (g_top_combos / world) / (top_ms * 1e-3)
+    fused = [r for r in st.rounds if r.combinations >= 1e7 * 0.999]
+    fused_g = (min(r.g for r in fused), max(r.g for r in fused)) if fused else (0, 0)
     q_kernel = w_eff <= 4 and n_eff <= 128
     # MACs per combination: algorithmic = the stored columns of one codeword
     # (its dot product, SURVEY.md 8(d) with identity elision); issued = the
@@ -573,6 +610,7 @@ def main():
         ctx.set_engine(cfg.engine)
         return (g_top_combos / world) / (min(ms) * 1e-3)
 
+    alone_achieved = engine_rate(cfg.engine)
     k5_achieved = engine_rate("mxf4")
     k1_achieved = engine_rate("popc")
     # the same launch without elision (full n-column rows)
@@ -589,10 +627,12 @@ def main():
     if os.path.exists(prof):
         with open(prof) as fh:
             traffic = json.load(fh).get("dram_bytes_per_launch")
-    kname = (f"k4_round_umma<{w_eff},true,4> = K5q, round g={g_top} (tcgen05.mma "
-             f"kind::mxf4nvf4 block16, two codewords as bytes of one fp32 accumulator)"
+    kname = (f"k4_round_umma<{w_eff},true,4> = K5q, rounds g={fused_g[0]}..{fused_g[1]} in one "
+             f"launch (tcgen05.mma kind::mxf4nvf4 block16, two codewords as bytes of one fp32 "
+             f"accumulator)"
              if q_kernel else
-             f"k4_round_umma<{w_eff},true,1> = K5, round g={g_top} (tcgen05.mma kind::mxf4)")
+             f"k4_round_umma<{w_eff},true,1> = K5, rounds g={fused_g[0]}..{fused_g[1]} in one "
+             f"launch (tcgen05.mma kind::mxf4)")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
@@ -637,6 +677,11 @@ def main():
                          "frac_issued": full_rate / (mac_rate / macs_full_issued),
                          "macs_per_combination": {"algorithmic": n,
                                                   "issued": macs_full_issued}}},
+        "largest_round_alone": {"kernel": f"{'K5q' if q_kernel else 'K5'} round g={g_top} in its own "
+                                          f"launch", "achieved": alone_achieved / 1e9,
+                                "peak": peak_alg / 1e9, "unit": "Gcombinations/s",
+                                "frac": alone_achieved / peak_alg,
+                                "frac_issued": alone_achieved / peak_issued},
         "k5_mxf4": {"kernel": f"k4_round_umma<{w_eff},true,1> round g={g_top} "
                               f"(tcgen05.mma kind::mxf4, one codeword per accumulator)",
                     "achieved": k5_achieved / 1e9, "peak": peak_alg / 1e9,
@@ -654,6 +699,7 @@ def main():
     if args.config == "cfg5" and not args.no_extra and world == 1:
         line["cfg5_other_seeds"] = other_seeds(args, cfg, local, flush)
         line["section6_C1"] = section6_c1(cfg)
+        line["configs_1_3"] = configs_wall(cfg)
         line["cfg4"] = cfg4_side(ctx, peaks)
         backend.load(gs, n)
     if not args.no_cpu_baseline:

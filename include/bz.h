@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define BZ_ABI_VERSION 12
+#define BZ_ABI_VERSION 13
 
 /* limits of the device kernels */
 #define BZ_MAX_K 128 /* rows per Gamma (prefix masks are 128-bit)      */
@@ -201,6 +201,23 @@ int bz_rounds(bz_ctx *ctx, int g0, int count, const int32_t *lower_prev, int upp
  * minimum weight (INT32_MAX when the shard is empty). */
 int bz_enumerate(bz_ctx *ctx, int gamma, int g, int shard, int nshards,
                  int32_t *out_min, uint64_t *out_combos);
+
+/* Row-level operation counters of the last bz_round / bz_rounds /
+ * bz_enumerate call (count <= its rounds; count x m values, round-major; for
+ * bz_enumerate only the enumerated Gamma's entries are non-zero) -- the
+ * device analogue of the reference's EnumerationResult.row_additions /
+ * row_accesses (m/enumeration.py:19-24, :254-302):
+ *   out_adds: full-row additions performed for the visited combinations --
+ *     one per codeword (its prefix sum combined with its last stored row:
+ *     a XOR in K1, the tensor-core dot product in K5/K5q), K1's D = 2
+ *     partial sums (prefix ^ R[e1], once per e1), and the prefix walkers'
+ *     updates (q rows per colex unrank, 2 or 3 prefix-XOR rows per step);
+ *   out_accs: rows brought into the working set -- every stored suffix row
+ *     a warp (K1) or CTA (K5/K5q: shared memory, up to 128 prefixes per
+ *     load) loads per prefix step, plus the table rows the walkers read.
+ * Suffix-table construction is not included (cf. store_build_additions).
+ * bz_plan + the oracle's chunk walk reproduce both exactly. */
+int bz_counters(bz_ctx *ctx, int count, uint64_t *out_adds, uint64_t *out_accs);
 
 /* Weight histogram of one (Gamma_gamma, g) pass: out_hist[w] (n+1 bins)
  * counts the g-combinations whose codeword has weight w. */

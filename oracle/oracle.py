@@ -17,7 +17,10 @@ What it restates (paths relative to the reference's pkg/src/mindist/):
   (engine.py:157-220) with ``initial_bounds`` (:90-94),
   ``lower_bound_update`` (:97-103) and ``_line7_args`` (:106-116).
 * ``enumerate_chunks`` -- pure-Python walk over the device work plan
-  (bz_plan, include/bz.h) used to check that shards partition the rank space.
+  (bz_plan, include/bz.h) used to check that shards partition the rank space;
+  ``expected_counters`` -- the row additions / accesses the device counts
+  for that plan (bz_counters), restating the reference's counter semantics
+  (enumeration.py:19-24, :254-302).
 
 Pinned by tests/test_oracle.py against tests/golden/goldens.json and
 tests/golden/cfg5_seed7.json, which tests/golden/make_golden.py produced
@@ -290,6 +293,82 @@ def enumerate_chunks(gammas: list[list[int]], k: int, g: int, groups, nchunks: i
                     cnt[gamma] += 1
                     seen.append((gamma, tuple(prefix + list(suf))))
     return mins, cnt, seen
+
+
+def _walk_cost(first: int, cnt: int, q: int, ell: int) -> int:
+    """Row additions of one prefix walker over colex ranks [first,
+    first+cnt): the init folds R[ell] and the q rows of the first subset (q
+    additions), each colex successor adds 2 prefix-XOR rows, 3 when the low
+    run of the subset's bits is longer than one (bz_kernels.cuh Walker)."""
+    if cnt <= 0:
+        return 0
+    cost = max(q, 0)
+    if q <= 0:
+        return cost
+    x = 0
+    for b in colex_unrank(first, q, ell):
+        x |= 1 << b
+    for _ in range(cnt - 1):
+        s = (x & -x).bit_length() - 1
+        run = 0
+        while (x >> (s + run)) & 1:
+            run += 1
+        cost += 3 if run >= 2 else 2
+        u = x & -x
+        v = x + u
+        x = v | (((v ^ x) // u) >> 2)
+    return cost
+
+
+def expected_counters(m: int, k: int, g: int, groups, nchunks: int, shard: int = 0,
+                      nshards: int = 1):
+    """Per-Gamma (row_additions, row_accesses) the device reports
+    (bz_counters, include/bz.h) for the chunks of `shard`, from the work
+    plan alone: K1 groups (32 lanes, two walkers per lane over the halves of
+    its prefix range) and K5/K5q groups (128 lanes, one walker each, every
+    stored suffix row of the chunk streamed once per prefix step).  Restates
+    the counting of the reference's strategies (enumeration.py:19-24,
+    :254-302) for the device's prefix-sum + stored-row decomposition."""
+    adds = [0] * m
+    accs = [0] * m
+    starts = [gr[0] for gr in groups]
+    for chunk in range(shard, nchunks, nshards):
+        gi = max(i for i, st in enumerate(starts) if st <= chunk)
+        begin, nprefix, gamma, ell, ppl, _, depth, lanes, spc, nsb, sfloor = groups[gi]
+        q = g - 1 - depth
+        local = chunk - begin
+        if depth < 3:
+            # K1: one warp, lane-major ranges, walkers A / B on the halves
+            e0 = ell + 1
+            per_prefix = comb(k - e0, depth) + (max(0, k - 1 - e0) if depth == 2 else 0)
+            maxca = 0
+            for lane in range(32):
+                first = (local * 32 + lane) * ppl
+                cnt = max(0, min(ppl, nprefix - first))
+                ca = (cnt + 1) >> 1
+                cb = cnt - ca
+                if lane == 0:
+                    maxca = ca
+                w = _walk_cost(first, ca, q, ell) + _walk_cost(first + ca, cb, q, ell)
+                ninit = (cnt > 0) + (cb > 0)
+                adds[gamma] += w + cnt * per_prefix
+                accs[gamma] += w + ninit
+            accs[gamma] += maxca * per_prefix
+        else:
+            # K5 / K5q: one CTA, 128 producer rows, tiles of the suffix block
+            pb, sb = divmod(local, nsb)
+            slice_rows = comb(k - sfloor, depth)
+            cols = min(spc, slice_rows - sb * spc)
+            bfirst = pb * 128 * ppl
+            maxcnt = min(ppl, nprefix - bfirst)
+            for r in range(128):
+                first = bfirst + r * ppl
+                cnt = max(0, min(ppl, nprefix - first))
+                w = _walk_cost(first, cnt, q, ell)
+                adds[gamma] += w + cnt * cols
+                accs[gamma] += w + (cnt > 0)
+            accs[gamma] += maxcnt * cols
+    return adds, accs
 
 
 def suffix_order(ell: int, k: int, depth: int, floor: int | None = None):

@@ -19,7 +19,7 @@ from .errors import (DeviceError, InvalidArity, InvalidDimensions, MindistError,
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BZ_LIB") or os.path.join(PKG_DIR, "libbz.so")
-ABI_VERSION = 12
+ABI_VERSION = 13
 
 BZ_OK = 0
 _CODES = {
@@ -36,7 +36,7 @@ _CODES = {
 SYMBOLS = ("bz_abi_version", "bz_device_count", "bz_create", "bz_destroy",
            "bz_last_error", "bz_set_engine", "bz_set_elision", "bz_set_early_exit", "bz_elided",
            "bz_reduce_on_columns", "bz_brute_force", "bz_load_gammas",
-           "bz_round", "bz_rounds",
+           "bz_round", "bz_rounds", "bz_counters",
            "bz_enumerate",
            "bz_histogram", "bz_plan", "bz_timer_start", "bz_timer_stop",
            "bz_last_kernel_ms", "bz_round_ms", "bz_gamma_family",
@@ -81,6 +81,7 @@ def lib():
     L.bz_round.argtypes = [vp, c_int, c_int, c_int, c_int, c_int, i32p, u64p]
     L.bz_rounds.argtypes = [vp, c_int, c_int, i32p, c_int, c_int, c_int, i32p, u64p]
     L.bz_enumerate.argtypes = [vp, c_int, c_int, c_int, c_int, i32p, u64p]
+    L.bz_counters.argtypes = [vp, c_int, u64p, u64p]
     L.bz_histogram.argtypes = [vp, c_int, c_int, c_int, c_int, u64p, i32p, u64p]
     L.bz_plan.argtypes = [c_int, c_int, c_int, c_int, c_int, i64p, c_int, i32p, u64p]
     L.bz_timer_start.argtypes = [vp]
@@ -275,37 +276,58 @@ class Context:
         self.m, self.k, self.n = m, k, n
         self.loaded_key = key
 
+    def _buf(self, name: str, dtype, size: int):
+        """A reusable host buffer and its ctypes pointer (ctypes pointer
+        objects cost microseconds each; the batched rounds sit on the timed
+        path of every run)."""
+        bufs = self.__dict__.setdefault("_bufs", {})
+        hit = bufs.get(name)
+        if hit is None or hit[0].size < size:
+            arr = np.zeros(max(size, 1), dtype=dtype)
+            hit = (arr, arr.ctypes.data_as(ctypes.POINTER(np.ctypeslib.as_ctypes_type(dtype))))
+            bufs[name] = hit
+        return hit
+
     def round(self, g: int, lower_prev: int, upper: int, shard: int = 0,
               nshards: int = 1):
-        mins = np.zeros(max(self.m, 1), dtype=np.int32)
-        combos = np.zeros(max(self.m, 1), dtype=np.uint64)
-        check(lib().bz_round(self.handle, g, lower_prev, upper, shard, nshards,
-                             _ptr(mins, ctypes.c_int32), _ptr(combos, ctypes.c_uint64)),
+        m = max(self.m, 1)
+        mins, pmin = self._buf("mins", np.int32, m)
+        combos, pcb = self._buf("combos", np.uint64, m)
+        check(lib().bz_round(self.handle, g, lower_prev, upper, shard, nshards, pmin, pcb),
               self.handle, f"bz_round(g={g})")
-        return [int(v) for v in mins[:self.m]], [int(v) for v in combos[:self.m]]
+        return mins[:self.m].tolist(), combos[:self.m].tolist()
 
     def rounds(self, g0: int, lower_prev: list[int], upper: int, shard: int = 0,
                nshards: int = 1):
         """Rounds g0 .. g0+len(lower_prev)-1 in one call (see bz_rounds);
         returns [(mins, combos)] per round."""
         count = len(lower_prev)
-        lp = np.ascontiguousarray(lower_prev, dtype=np.int32)
-        mins = np.zeros(count * max(self.m, 1), dtype=np.int32)
-        combos = np.zeros(count * max(self.m, 1), dtype=np.uint64)
-        check(lib().bz_rounds(self.handle, g0, count, _ptr(lp, ctypes.c_int32), upper, shard,
-                              nshards, _ptr(mins, ctypes.c_int32),
-                              _ptr(combos, ctypes.c_uint64)),
+        m = max(self.m, 1)
+        lp, plp = self._buf("lp", np.int32, count)
+        lp[:count] = lower_prev
+        mins, pmin = self._buf("mins", np.int32, count * m)
+        combos, pcb = self._buf("combos", np.uint64, count * m)
+        check(lib().bz_rounds(self.handle, g0, count, plp, upper, shard, nshards, pmin, pcb),
               self.handle, f"bz_rounds(g0={g0}, count={count})")
-        m = self.m
-        return [([int(v) for v in mins[i * m:(i + 1) * m]],
-                 [int(v) for v in combos[i * m:(i + 1) * m]]) for i in range(count)]
+        mn = mins[:count * m].reshape(count, m).tolist()
+        cb = combos[:count * m].reshape(count, m).tolist()
+        return list(zip(mn, cb))
+
+    def counters(self, count: int = 1):
+        """Row additions and row accesses (count x m, round-major) of the
+        last round / rounds / enumerate call (bz_counters)."""
+        m = max(self.m, 1)
+        adds, pad = self._buf("adds", np.uint64, count * m)
+        accs, pac = self._buf("accs", np.uint64, count * m)
+        check(lib().bz_counters(self.handle, count, pad, pac), self.handle, "bz_counters")
+        return (adds[:count * m].reshape(count, m).tolist(),
+                accs[:count * m].reshape(count, m).tolist())
 
     def round_ms(self, count: int) -> list[float]:
         """Per-round device ms of the last round / rounds call."""
-        out = np.zeros(max(count, 1), dtype=np.float32)
-        check(lib().bz_round_ms(self.handle, _ptr(out, ctypes.c_float), count), self.handle,
-              "bz_round_ms")
-        return [float(v) for v in out[:count]]
+        out, pout = self._buf("round_ms", np.float32, count)
+        check(lib().bz_round_ms(self.handle, pout, count), self.handle, "bz_round_ms")
+        return out[:count].tolist()
 
     def enumerate(self, gamma: int, g: int, shard: int = 0, nshards: int = 1):
         mn = np.zeros(1, dtype=np.int32)

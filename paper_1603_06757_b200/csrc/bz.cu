@@ -40,6 +40,7 @@ using bz::RoundArgs;
 
 struct bz_ctx {
   int device = -1;
+  int last_count = 0;  // rounds of the last run_batch (bz_counters)
   int sm_count = 0;
   cudaStream_t stream = nullptr;
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;      // user timer
@@ -147,17 +148,19 @@ cudaError_t grow(bz_ctx*, void** p, size_t* cap, size_t bytes) {
 // [pad][groups].  A batch of rounds uses consecutive slots; the whole block
 // goes to the device in one copy and comes back in one copy.
 struct IoSlot {
-  size_t off_combos, off_bound, off_groups, size;
+  size_t off_combos, off_adds, off_accs, off_bound, off_groups, size;
 };
 
 // I/O image of a batch of rounds: first every round's result record
-// {cursor, combos[m], bound[m+1]} (off_groups bytes each, contiguous: the
+// {cursor, combos[m], adds[m], accs[m], bound[m+1]} (off_groups bytes each, contiguous: the
 // only part read back), then each round's plan at a variable offset
 // (ctx->gbase[i]; only the used groups travel host -> device).
 IoSlot io_layout(int m, int k) {
   IoSlot l;
   l.off_combos = 8;
-  l.off_bound = l.off_combos + 8 * (size_t)m;
+  l.off_adds = l.off_combos + 8 * (size_t)m;
+  l.off_accs = l.off_adds + 8 * (size_t)m;
+  l.off_bound = l.off_accs + 8 * (size_t)m;
   l.off_groups = (l.off_bound + 4 * (size_t)(m + 1) + 15) & ~size_t(15);  // record size
   const size_t max_groups = (size_t)m * (size_t)(3 * k + 6) + 1;  // K5: up to 3 levels
   l.size = (l.off_groups + sizeof(Group) * max_groups + 255) & ~size_t(255);  // worst case
@@ -938,7 +941,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     *slot_ptr<unsigned long long>(ctx->h_io, l, i, 0) = 0ull;
     unsigned long long* hc = slot_ptr<unsigned long long>(ctx->h_io, l, i, l.off_combos);
     int* hb = slot_ptr<int>(ctx->h_io, l, i, l.off_bound);
-    for (int j = 0; j < m; ++j) hc[j] = 0ull;
+    for (int j = 0; j < 3 * m; ++j) hc[j] = 0ull;  // combos, adds, accs
     for (int j = 0; j <= m; ++j) hb[j] = upper;  // per-Gamma caps below, once `run` is known
     RoundArgs& a = todo[i].a;
     a = RoundArgs{};
@@ -948,6 +951,8 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     a.binom = ctx->d_binom;
     a.bound = slot_ptr<int>(ctx->d_io, l, i, l.off_bound);
     a.combos = slot_ptr<unsigned long long>(ctx->d_io, l, i, l.off_combos);
+    a.adds = hist ? nullptr : slot_ptr<unsigned long long>(ctx->d_io, l, i, l.off_adds);
+    a.accs = hist ? nullptr : slot_ptr<unsigned long long>(ctx->d_io, l, i, l.off_accs);
     a.counter = slot_ptr<unsigned long long>(ctx->d_io, l, i, 0);
     a.hist = ctx->d_hist;
     a.nchunks = nchunks;
@@ -1071,6 +1076,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
             us(t_launch1, std::chrono::steady_clock::now()));
   }
   CK(cudaEventElapsedTime(&ctx->last_kernel_ms, ctx->ev_k0, ctx->ev_k1));
+  ctx->last_count = hist ? 0 : count;
   ctx->round_ms.assign(count, 0.f);
   if (count == 1) {
     ctx->round_ms[0] = ctx->last_kernel_ms;
@@ -1122,6 +1128,14 @@ const int* slot_bound(bz_ctx* ctx, int i) {
 const unsigned long long* slot_combos(bz_ctx* ctx, int i) {
   const IoSlot l = io_layout(ctx->m, ctx->k);
   return slot_ptr<unsigned long long>(ctx->h_io, l, i, l.off_combos);
+}
+const unsigned long long* slot_adds(bz_ctx* ctx, int i) {
+  const IoSlot l = io_layout(ctx->m, ctx->k);
+  return slot_ptr<unsigned long long>(ctx->h_io, l, i, l.off_adds);
+}
+const unsigned long long* slot_accs(bz_ctx* ctx, int i) {
+  const IoSlot l = io_layout(ctx->m, ctx->k);
+  return slot_ptr<unsigned long long>(ctx->h_io, l, i, l.off_accs);
 }
 
 }  // namespace
@@ -1399,6 +1413,20 @@ int bz_enumerate(bz_ctx* ctx, int gamma, int g, int shard, int nshards, int32_t*
   if (rc) return rc;
   *out_min = slot_bound(ctx, 0)[1 + gamma];
   *out_combos = slot_combos(ctx, 0)[gamma];
+  return BZ_OK;
+}
+
+int bz_counters(bz_ctx* ctx, int count, uint64_t* out_adds, uint64_t* out_accs) {
+  if (!ctx) return BZ_ERR_ARGUMENT;
+  if (!out_adds || !out_accs) return fail(ctx, BZ_ERR_ARGUMENT, "null output");
+  if (count < 1 || count > ctx->last_count)
+    return fail(ctx, BZ_ERR_ARGUMENT, "count %d not in 1..%d (rounds of the last call)", count,
+                ctx->last_count);
+  for (int i = 0; i < count; ++i)
+    for (int j = 0; j < ctx->m; ++j) {
+      out_adds[(size_t)i * ctx->m + j] = slot_adds(ctx, i)[j];
+      out_accs[(size_t)i * ctx->m + j] = slot_accs(ctx, i)[j];
+    }
   return BZ_OK;
 }
 

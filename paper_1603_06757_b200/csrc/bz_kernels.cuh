@@ -60,6 +60,13 @@ struct RoundArgs {
   const unsigned long long* binom;  // kBinomDim^2 saturating binomials
   int* bound;                  // [0] round minimum, [1+j] per-Gamma minimum
   unsigned long long* combos;  // per-Gamma visited combinations
+  // per-Gamma row-level operation counters (null: not counted), the
+  // device analogue of the reference's (m/enumeration.py:19-24):
+  // adds = full-row additions (XORs, and the tensor-core dot products that
+  // combine a prefix sum with a stored row), accs = rows brought into the
+  // working set (table rows a warp / CTA loads once for all its codewords)
+  unsigned long long* adds;
+  unsigned long long* accs;
   unsigned long long* counter; // dynamic chunk cursor
   unsigned long long* hist;    // n+1 bins (histogram kernel only)
   unsigned long long nchunks;  // chunks of the whole round (all shards)
@@ -314,15 +321,24 @@ struct Walker {
     }
   }
 
-  // colex successor; PX[0] = 0, so the third row only matters for runs > 1
-  __device__ __forceinline__ void step(const uint32_t* PX) {
+  // colex successor; PX[0] = 0, so the third row only matters for runs > 1.
+  // Returns the prefix-XOR rows it added (2 or 3).
+  __device__ __forceinline__ int step(const uint32_t* PX) {
     int i0, i1, i2;
     colex_next(x, i0, i1, i2);
     xor_px<W>(acc, PX, i0);
     xor_px<W>(acc, PX, i1);
     if (i2 > 0) xor_px<W>(acc, PX, i2);
+    return i2 > 0 ? 3 : 2;
   }
 };
+
+// 64-bit sum over the warp (all lanes active)
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
 
 // Weight of the dropped identity columns of Gamma j: every chosen row has
 // exactly one of them set.
@@ -520,6 +536,10 @@ __device__ __forceinline__ void k1_chunk(const RoundArgs& a, unsigned long long 
     Walker<W> A, B;
     if (v.cnt > 0) A.init(v.first, q, v.gr.ell, R, a.binom, sbinom);
     if (cb > 0) B.init(v.first + ca, q, v.gr.ell, R, a.binom, sbinom);
+    // walker row additions: an init folds R[ell] and q more rows (q
+    // additions), a step adds 2 or 3 prefix-XOR rows
+    const int ninit = (v.cnt > 0) + (cb > 0);
+    unsigned long long wadd = (unsigned long long)ninit * (unsigned long long)max(q, 0);
 
     int best = INT_MAX;
     for (long long p = 0; p < maxca; ++p) {
@@ -534,8 +554,8 @@ __device__ __forceinline__ void k1_chunk(const RoundArgs& a, unsigned long long 
           pb = min(pb, wb);
         });
         best = min(best, min(pa, pb));
-        if (p + 1 < ca) A.step(PX);
-        if (p + 1 < cb) B.step(PX);
+        if (p + 1 < ca) wadd += (unsigned long long)A.step(PX);
+        if (p + 1 < cb) wadd += (unsigned long long)B.step(PX);
       }
     }
 
@@ -551,6 +571,21 @@ __device__ __forceinline__ void k1_chunk(const RoundArgs& a, unsigned long long 
         gbound_publish(a, wbest);
       }
       atomicAdd(a.combos + v.gr.gamma, (unsigned long long)tot * suffix_count<D>(k, e0));
+    }
+    if (a.adds) {
+      // every codeword is one row addition (prefix sum ^ its last suffix
+      // row); D = 2 adds the partial sum prefix ^ R[e1] once per e1.  A
+      // suffix row is loaded once per walker-pair step for the whole warp;
+      // the walkers read one table row per addition plus R[ell] per init.
+      const unsigned long long per_prefix =
+          suffix_count<D>(k, e0) + (D == 2 ? (unsigned long long)max(0, k - 1 - e0) : 0ull);
+      const unsigned long long adds = warp_sum_u64(wadd + (unsigned long long)v.cnt * per_prefix);
+      const unsigned long long accs = warp_sum_u64(wadd + (unsigned long long)ninit) +
+                                      (unsigned long long)maxca * per_prefix;
+      if (lane == 0) {
+        atomicAdd(a.adds + v.gr.gamma, adds);
+        atomicAdd(a.accs + v.gr.gamma, accs);
+      }
     }
   }
 }

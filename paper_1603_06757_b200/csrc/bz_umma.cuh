@@ -1297,13 +1297,15 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
       Walker<W> wk;
       // rows without prefixes duplicate the block's first prefix
       wk.init(cnt > 0 ? first : c.bfirst, ar.g - 1 - c.gr.depth, c.gr.ell, R, a.binom, sbinom);
+      // walker row additions of this row's valid prefixes (counters)
+      unsigned long long wadd = cnt > 0 ? (unsigned long long)max(ar.g - 1 - c.gr.depth, 0) : 0ull;
       for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
         const int ab = grp % NA;
         mbar_wait_sel<4>(aempty(ab), ((grp / NA) & 1) ^ 1);
 #pragma unroll 1
         for (int j = 0; j < kUmmaMA; ++j) {
           // step j of the group; past this row's range the last prefix repeats
-          if (p + j > 0 && p + j < cnt) wk.step(PX);
+          if (p + j > 0 && p + j < cnt) wadd += (unsigned long long)wk.step(PX);
           unsigned char* dst = sA + (ab * kUmmaMA + j) * TA;
           int wt = 0;
           if (a.debug & 16) continue;  // timing experiment: no A rows
@@ -1363,10 +1365,21 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
       }
       // visited combinations of this chunk
       const unsigned tot = __reduce_add_sync(FULL, (unsigned)cnt);
-      if (lane == 0 && tot) {
-        const long long cols = min((long long)c.tile_hi * TR, (long long)c.slice) -
-                               (long long)c.tile_lo * TR;
+      const long long cols = min((long long)c.tile_hi * TR, (long long)c.slice) -
+                             (long long)c.tile_lo * TR;
+      if (lane == 0 && tot)
         atomicAdd(ar.combos + c.gr.gamma, (unsigned long long)tot * (unsigned long long)cols);
+      if (ar.adds) {
+        // one tensor-core addition per codeword (the prefix sum combined
+        // with a stored suffix row), plus the walkers' prefix-XOR rows; the
+        // walkers read one table row per addition and R[ell] per init (the
+        // loader counts the stored rows it streams)
+        const unsigned long long wsum = warp_sum_u64(wadd);
+        const unsigned long long winit = (unsigned long long)__popc(__ballot_sync(FULL, cnt > 0));
+        if (lane == 0) {
+          atomicAdd(ar.adds + c.gr.gamma, wsum + (unsigned long long)tot * (unsigned long long)cols);
+          atomicAdd(ar.accs + c.gr.gamma, wsum + winit);
+        }
       }
     }
   } else if (warp < RL::LOAD) {
@@ -1562,6 +1575,13 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
         const unsigned long long chunk = (unsigned long long)qchunk & ((1ull << kQRoundShift) - 1);
         const K4Chunk c = k4_decode<TR>(plan_of(rr), ar.ngroups, chunk, k);
         k4_trace_chunk(a, toff, c.gr.ell, bcount);
+        if (ar.accs) {
+          // stored suffix rows streamed into shared memory: every tile of
+          // the chunk once per prefix step, each shared by up to 128 prefixes
+          const long long cols = min((long long)c.tile_hi * TR, (long long)c.slice) -
+                                 (long long)c.tile_lo * TR;
+          atomicAdd(ar.accs + c.gr.gamma, (unsigned long long)c.maxcnt * (unsigned long long)cols);
+        }
         const int lvl = c.gr.depth - 3;  // suffix table of this group's level
         const uint8_t* tsrc =
             tabs.t[lvl] + (size_t)c.gr.gamma * tabs.stride_rows[lvl] * (CB * 16);

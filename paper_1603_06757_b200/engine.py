@@ -33,7 +33,7 @@ from math import comb
 import numpy as np
 
 from . import _native
-from .enumeration import EnumerationResult, family_words
+from .enumeration import EnumerationResult, PassCount, family_words, split_count
 from .errors import InvalidArity, InvalidDimensions, Interrupted, TooLarge
 from .gf2 import BitMatrix, GammaSet, build_gamma_set
 from .parallel import LocalComm, combine_rounds
@@ -202,8 +202,10 @@ class GpuRounds:
     def run(self, g: int, lower_prev: int, upper: int):
         mins, combos = self.ctx.round(g, lower_prev, upper, self.comm.rank, self.comm.world)
         kernel_ms = self.ctx.last_kernel_ms()
-        mins, combos = self.comm.combine(mins, combos)
-        return mins, combos, kernel_ms
+        adds, accs = self.ctx.counters(1)
+        m = len(mins)
+        mins, sums = self.comm.combine(mins, combos + adds[0] + accs[0])
+        return mins, [PassCount(*sums[j::m]) for j in range(m)], kernel_ms
 
     def run_batch(self, g0: int, lower_prevs: list[int], upper: int):
         """Rounds g0.. in one call, each sharded over the ranks like a single
@@ -211,7 +213,13 @@ class GpuRounds:
         and the batch's kernel ms."""
         res = self.ctx.rounds(g0, lower_prevs, upper, self.comm.rank, self.comm.world)
         ms = self.ctx.round_ms(len(lower_prevs))
-        return combine_rounds(self.comm, res), ms
+        adds, accs = self.ctx.counters(len(lower_prevs))
+        res = [(mn, cb + ad + ac) for (mn, cb), ad, ac in zip(res, adds, accs)]
+        out = []
+        for mn, sums in combine_rounds(self.comm, res):
+            m = len(mn)
+            out.append((mn, [PassCount(*sums[j::m]) for j in range(m)]))
+        return out, ms
 
 
 def make_backend(config: EngineConfig, comm):
@@ -298,9 +306,10 @@ def run_rounds(backend, gs: GammaSet, k: int, config: EngineConfig, st: LoopStat
             queued.clear()
             mins, combos, kernel_ms = backend.run(st.g, st.L, st.U)
         round_combos = 0
-        for mn, c in zip(mins, combos):
+        for mn, cnt in zip(mins, combos):
             st.U = min(st.U, mn)
-            st.counters.add(EnumerationResult(st.U, c, c, c))
+            c, adds, accs = split_count(cnt)
+            st.counters.add(EnumerationResult(st.U, c, adds, accs))
             round_combos += c
         st.rounds.append(RoundStat(st.g, round_combos, kernel_ms,
                                    (time.perf_counter() - tr) * 1e3))

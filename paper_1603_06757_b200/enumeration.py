@@ -7,15 +7,19 @@ clipped to ``ubound`` (enumeration.py:60-64) and ``InvalidArity`` for g
 outside 1..k (enumeration.py:67-69).  The work runs in the sm_100a kernel
 K1 behind the C ABI (include/bz.h); there is no CPU path.
 
-Counters: ``combinations`` is exact (C(k, g) per pass).  In the GPU
-algorithm every codeword costs exactly one row addition (prefix XOR ^ row
-e) and one row access (the broadcast read of row e), so ``row_additions`` and
-``row_accesses`` both equal ``combinations``; the prefix-maintenance XORs
-(three prefix-table rows per prefix step) are not counted.
+Counters: ``combinations`` is exact (C(k, g) per pass).  ``row_additions``
+and ``row_accesses`` are counted on the device (bz_counters, include/bz.h)
+with the reference's meaning (enumeration.py:19-24): one addition per
+codeword (its prefix sum combined with its last stored row -- a XOR in K1,
+the tensor-core dot product in K5/K5q), K1's partial sums, and the prefix
+walkers' updates; accesses are the rows a warp (K1) or CTA (K5/K5q, up to
+128 prefixes per stored row load) brings into its working set.  The paper's
+point -- many additions per row access -- is their ratio.
 """
 
 from __future__ import annotations
 
+from collections import namedtuple
 from dataclasses import dataclass
 
 import numpy as np
@@ -31,6 +35,17 @@ class EnumerationResult:
     combinations: int
     row_additions: int
     row_accesses: int
+
+
+# one pass's counts as the backends report them (an int = combinations only)
+PassCount = namedtuple("PassCount", "combinations additions accesses")
+
+
+def split_count(v) -> tuple[int, int, int]:
+    """(combinations, row_additions, row_accesses) of a backend's count."""
+    if isinstance(v, PassCount):
+        return int(v.combinations), int(v.additions), int(v.accesses)
+    return int(v), int(v), int(v)
 
 
 def family_words(gammas, n: int) -> np.ndarray:
@@ -61,9 +76,10 @@ def enumerate_gpu(gamma: BitMatrix, g: int, ubound: int | None = None,
     with ctx.lock:
         _load_single(gamma, device)
         mn, combos = ctx.enumerate(0, g)
+        adds, accs = ctx.counters(1)
     if ubound is not None:
         mn = min(mn, ubound)
-    return EnumerationResult(int(mn), combos, combos, combos)
+    return EnumerationResult(int(mn), combos, adds[0][0], accs[0][0])
 
 
 def weight_histogram_gpu(gamma: BitMatrix, g: int, device: int = 0):

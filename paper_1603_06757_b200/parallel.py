@@ -54,12 +54,13 @@ class TorchComm:
         if self.world == 1:
             return list(mins), list(combos)
         m = len(mins)
+        width = m + len(combos)  # minima, then the summed counts
         mine = torch.tensor(list(mins) + list(combos), dtype=torch.int64,
                             device=self.device)
         if self.device.type == "cuda":
-            allv = torch.empty(self.world * 2 * m, dtype=torch.int64, device=self.device)
+            allv = torch.empty(self.world * width, dtype=torch.int64, device=self.device)
             dist.all_gather_into_tensor(allv, mine, group=self.group)
-            allv = allv.view(self.world, 2 * m)
+            allv = allv.view(self.world, width)
         else:
             parts = [torch.empty_like(mine) for _ in range(self.world)]
             dist.all_gather(parts, mine, group=self.group)
@@ -84,7 +85,8 @@ def combine_rounds(comm, res):
     if comm.world == 1 or not res:
         return [(list(mn), list(cb)) for mn, cb in res]
     m = len(res[0][0])
+    c = len(res[0][1])  # counts per round (m combinations, or more counters)
     mins, combos = comm.combine([v for mn, _ in res for v in mn],
                                 [v for _, cb in res for v in cb])
-    return [(mins[i * m:(i + 1) * m], combos[i * m:(i + 1) * m]) for i in range(len(res))]
+    return [(mins[i * m:(i + 1) * m], combos[i * c:(i + 1) * c]) for i in range(len(res))]
 
