@@ -601,14 +601,18 @@ def main():
     popc_peak = peaks["popc_per_s"] / w_eff
     g_top = max(st.rounds, key=lambda r: r.combinations).g
 
+    # the round as the run meets it: the L and U the previous round left
+    prev = [t for t in st.trace if t[0] == g_top - 1]
+    l_prev, u_prev = (prev[0][1], prev[0][2]) if prev else (0, 1 << 30)
+
     def engine_rate(engine_name):
         ctx.set_engine(engine_name)
         ms = []
-        for _ in range(2):
-            ctx.round(g_top, 0, 1 << 30, local, world)
+        for _ in range(3):
+            ctx.round(g_top, l_prev, u_prev, local, world)
             ms.append(ctx.last_kernel_ms())
         ctx.set_engine(cfg.engine)
-        return (g_top_combos / world) / (min(ms) * 1e-3)
+        return (g_top_combos / world) / (statistics.median(ms) * 1e-3)
 
     alone_achieved = engine_rate(cfg.engine)
     k5_achieved = engine_rate("mxf4")

@@ -74,6 +74,11 @@ extern "C" {
 #define BZ_ENGINE_MXF4T 6 /* K5t: three codewords per column (W = 1, 3)     */
 #define BZ_ENGINE_MXF4Q 7 /* K5q: two codewords as bytes (mxf4nvf4; W <= 4,
                              stored columns <= 128; else K5)              */
+#define BZ_ENGINE_MXF4W 8 /* K5w: two codewords as 11-bit fields (mxf4,
+                             ue8m0 scales; any W >= 2, rows wider than
+                             K5q's 128 stored columns; W = 1 runs K5).
+                             On request: measured no faster than K5 on the
+                             section-6 codes      */
 
 typedef struct bz_ctx bz_ctx;
 
@@ -279,11 +284,12 @@ int bz_launch_count(bz_ctx *ctx, uint64_t *out);
  * MACs per clock per SM.  `out` must hold 14 doubles. */
 int bz_measure_int_peaks(bz_ctx *ctx, int w_words, double *out);
 
-/* Host-only self-check of the K5q offset encoding (no device needed): the
- * kernel's producer threshold and e2m1 offset blocks over every prefix
- * weight 0..128 and bound -4..128 must stay in range and dot to their
- * integers exactly.  Returns the number of failures (0 = ok); the first
- * failing (prefix weight, bound) goes to out_bad[0..1] (may be NULL). */
+/* Host-only self-check of the K5q and K5w offset encodings (no device
+ * needed): the producers' thresholds and e2m1 offset chunks over every
+ * prefix weight (K5q 0..128, bound -4..128; K5w 0..256, bound -4..400) must
+ * stay in range and dot to their integers exactly.  Returns the number of
+ * failures (0 = ok); the first failing (prefix weight, bound) goes to
+ * out_bad[0..1] (may be NULL; K5w bounds are reported + 1000). */
 int bz_k5q_selftest(int32_t *out_bad);
 
 #ifdef __cplusplus

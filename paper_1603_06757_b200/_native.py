@@ -130,7 +130,8 @@ def device_count() -> int:
     return int(lib().bz_device_count())
 
 
-ENGINES = {"auto": 0, "popc": 1, "imma": 2, "umma": 3, "mxf4": 4, "mxf4p": 5, "mxf4t": 6, "mxf4q": 7}
+ENGINES = {"auto": 0, "popc": 1, "imma": 2, "umma": 3, "mxf4": 4, "mxf4p": 5, "mxf4t": 6, "mxf4q": 7,
+           "mxf4w": 8}
 
 
 def plan(m: int, k: int, g: int, engine: str = "auto", nshards: int = 1):

@@ -196,7 +196,8 @@ T* slot_ptr(unsigned char* base, const IoSlot& l, int i, size_t off) {
 // triples per tile.  K4 (tcgen05) and K3 (legacy IMMA) take D = 3 for
 // g >= 4; K1 (POPC) takes D = 2 for g >= 4, else 1.  Histograms run on K1.
 struct PlanShape {
-  int depth, lanes, tile_rows, kernel;  // kernel: 1 = K1, 3 = K3, 4 = K4, 5 = K5, 6 = K5p
+  int depth, lanes, tile_rows, kernel;  // kernel: 1 = K1, 3 = K3, 4 = K4, 5 = K5, 6 = K5p,
+                                        // 7 = K5t, 8 = K5q, 9 = K5w
 };
 
 // K5p (two codewords per accumulator column) needs odd W <= 3 stored words
@@ -240,6 +241,13 @@ PlanShape pass_shape(int engine, int g, bool hist, int w32 = 0, int m = 0, int k
     const bool q_ok = w32 == 0 || k5q_ok(w32, n_eff);
     if ((engine == BZ_ENGINE_MXF4Q || engine == BZ_ENGINE_AUTO) && q_ok)
       return {3, bz::kUmmaM, bz::k4_tile_rows<true, 4>(), 8};  // K5q
+    // K5w (two codewords per column as 11-bit fields) on request only: on
+    // the wide section-6 codes it measured no faster than K5 (C1 round 12:
+    // 70.0 vs 64.2 ms, tools/s6_rates.py) -- their rounds are bound by the
+    // per-prefix-step cost (~13 tiles per step), and 480-row tiles fit
+    // their suffix slices worse (tile efficiency 0.89 vs 0.94)
+    if (engine == BZ_ENGINE_MXF4W && w32 != 1)
+      return {3, bz::kUmmaM, bz::k4_tile_rows<true, 5>(), 9};
     if (engine == BZ_ENGINE_MXF4P && packed_ok) return {3, bz::kUmmaM, bz::k4_tile_rows<true, 2>(), 6};
     if (engine == BZ_ENGINE_AUTO || engine == BZ_ENGINE_MXF4 || engine == BZ_ENGINE_MXF4P ||
         engine == BZ_ENGINE_MXF4T || engine == BZ_ENGINE_MXF4Q)
@@ -831,6 +839,8 @@ int launch_w(bz_ctx* ctx, const RoundArgs* as, int count, bool hist, const PlanS
 #endif
   if constexpr (W <= 4)
     if (shape.kernel == 8) return launch_umma<W, true, 4>(ctx, as, count);
+  if constexpr (W >= 2)
+    if (shape.kernel == 9) return launch_umma<W, true, 5>(ctx, as, count);
   if (shape.kernel >= 3 && shape.kernel != 5)
     return fail(ctx, BZ_ERR_STATE, "kernel %d not available at W = %d", shape.kernel, W);
   if (shape.kernel == 5) return launch_umma<W, true>(ctx, as, count);
@@ -1026,7 +1036,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     int f = 1;
     size_t fused_groups = (size_t)todo[i].a.ngroups;
     const int kern = todo[i].shape.kernel;
-    const bool tensor = kern == 5 || kern == 8;
+    const bool tensor = kern == 5 || kern == 8 || kern == 9;
     while (!hist && !debug && i + f < count && todo[i + f].run &&
            todo[i + f].shape.kernel == kern &&
            ((kern == 1 && f < bz::kK1MaxFused && todo[i + f].shape.depth == todo[i].shape.depth &&
@@ -1658,7 +1668,7 @@ int bz_elided(bz_ctx* ctx, uint64_t* out_mask) {
 
 int bz_set_engine(bz_ctx* ctx, int engine) {
   if (!ctx) return BZ_ERR_ARGUMENT;
-  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4Q)
+  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4W)
     return fail(ctx, BZ_ERR_ARGUMENT, "unknown engine %d", engine);
   if (!BZ_LEGACY_KERNELS && (engine == BZ_ENGINE_IMMA || engine == BZ_ENGINE_UMMA ||
                              engine == BZ_ENGINE_MXF4P || engine == BZ_ENGINE_MXF4T))
@@ -1678,7 +1688,7 @@ int bz_plan(int m, int k, int g, int engine, int nshards, int64_t* out, int cap,
   if (binom_sat(k, g) >= (1ull << 62)) return BZ_ERR_TOO_LARGE;
   std::vector<Group> gs;
   unsigned long long nchunks = 0;
-  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4Q) return BZ_ERR_ARGUMENT;
+  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4W) return BZ_ERR_ARGUMENT;
   if (nshards < 1) return BZ_ERR_ARGUMENT;
   int rc = build_plan(nullptr, m, k, g, -1, pass_shape(engine, g, false), nshards, gs, &nchunks);
   if (rc) return rc;
@@ -1794,6 +1804,25 @@ int bz_k5q_selftest(int32_t* out_bad) {
                           e2m1_dot16(pb.x, pb.y, tb.x, tb.y) == (double)x &&
                           e2m1_dot16(pb.z, pb.w, tb.z, tb.w) == 128.0;
       if (!range_ok || !enc_ok) note(wt, rel);
+    }
+  // K5w: R = wt - thr against the offset pattern, the constant chunks, and
+  // the 11-bit field range x = w + 1024 - thr for stored weights 0..256
+  for (int R = -bz::kWMaxSpan; R <= bz::kWMaxSpan; ++R) {
+    const uint4 c = bz::k5w_r_chunk(R);
+    if (e2m1_dot16(c.x, c.y, tb.x, tb.y) + e2m1_dot16(c.z, c.w, tb.z, tb.w) != (double)R)
+      note(-2, R);
+  }
+  const uint4 ca = bz::k5w_const_chunk(0), cb = bz::k5w_const_chunk(1);
+  if (e2m1_dot16(ca.x, ca.y, 0x22u, 0u) != 5.0 || e2m1_dot16(cb.x, cb.y, 0x22u, 0u) != 1.0)
+    note(-3, 0);
+  static_assert(5ll * (1ll << 21) + (1ll << 10) == (1ll << 23) + 1024 + 2048ll * 1024,
+                "K5w offset constants");
+  for (int wt = 0; wt <= 256; ++wt)
+    for (int rel = -4; rel <= 400; ++rel) {
+      const int thr = bz::k5w_threshold(wt, rel);
+      const bool ok = thr >= 1 && thr >= std::min(rel, 257) && wt - thr >= -bz::kWMaxSpan &&
+                      wt - thr <= bz::kWMaxSpan && 0 + 1024 - thr >= 0 && 256 + 1024 - thr <= 2047;
+      if (!ok) note(wt, 1000 + rel);
     }
   return bad;
 }

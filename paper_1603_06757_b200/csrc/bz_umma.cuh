@@ -161,10 +161,15 @@ template <bool F4> __host__ __device__ constexpr int k4_row_bytes(int w) {
 // CW codewords per accumulator column carry CW offset chunks after the W
 // data chunks)
 // codewords per accumulator column of kernel form CW (1 = K5, 2 = K5p,
-// 3 = K5t, 4 = K5q: two codewords as bytes)
-__host__ __device__ constexpr int k5_ncw(int cw) { return cw == 4 ? 2 : cw; }
+// 3 = K5t, 4 = K5q: two codewords as bytes, 5 = K5w: two codewords as 11-bit
+// fields, for wide rows)
+__host__ __device__ constexpr int k5_ncw(int cw) { return (cw == 4 || cw == 5) ? 2 : cw; }
+// K5w A row: the data chunks padded to whole K = 64 MMAs (a zero chunk for
+// odd W meets the table's offset chunk), then the offset chunks R, Ca, Cb
+__host__ __device__ constexpr int k5w_data_chunks(int w) { return 2 * ((w + 1) / 2); }
 template <bool F4, int CW = 1> __host__ __device__ constexpr int k4_a_chunks(int w) {
-  return CW > 1 ? w + k5_ncw(CW) : (F4 ? 2 * ((w + 1) / 2) : 2 * w);
+  return CW == 5 ? k5w_data_chunks(w) + 3
+                 : (CW > 1 ? w + k5_ncw(CW) : (F4 ? 2 * ((w + 1) / 2) : 2 * w));
 }
 // MMAs per tile (per half for K5p)
 template <bool F4> __host__ __device__ constexpr int k4_passes(int w) { return k4_a_chunks<F4>(w) / 2; }
@@ -178,15 +183,26 @@ template <bool F4, int CW = 1> __host__ __device__ constexpr uint32_t k4_tile_b(
 template <bool F4, int CW = 1> __host__ __device__ constexpr uint32_t k4_tile_a(int w) {
   return (uint32_t)(kUmmaM * 16 * k4_a_chunks<F4, CW>(w));
 }
-// A-tile ring depth (producers run that many prefix steps ahead)
-template <bool F4> __host__ __device__ constexpr int k4_abufs(int w) {
-  return F4 && w <= 6 ? 4 : 2;
+// A-tile ring depth (producers run that many prefix steps ahead; K5w's wide
+// A rows and B tiles leave room for two)
+#ifndef BZ_K5W_ABUFS
+#define BZ_K5W_ABUFS 2
+#endif
+#ifndef BZ_K5W_STAGE_BYTES
+#define BZ_K5W_STAGE_BYTES 140000
+#endif
+template <bool F4, int CW = 1> __host__ __device__ constexpr int k4_abufs(int w) {
+  return CW == 5 ? BZ_K5W_ABUFS : (F4 && w <= 6 ? 4 : 2);
 }
 // B-tile ring depth: K5 ~136 KB of stages, K4 4 x 40 KB at W = 5
 #ifndef BZ_K5P_STAGE_BYTES
 #define BZ_K5P_STAGE_BYTES 160000
 #endif
 template <bool F4, int CW = 1> __host__ __device__ constexpr int k4_stages(int w) {
+  if (CW == 5) {
+    const int s = BZ_K5W_STAGE_BYTES / (int)k4_tile_b<true, CW>(w);
+    return s < 2 ? 2 : (s > kMaxStages ? kMaxStages : s);
+  }
   return F4 ? ((CW > 1 ? BZ_K5P_STAGE_BYTES : 136000) / (int)k4_tile_b<true, CW>(w) < kMaxStages
                    ? (CW > 1 ? BZ_K5P_STAGE_BYTES : 136000) / (int)k4_tile_b<true, CW>(w)
                    : kMaxStages)
@@ -257,6 +273,46 @@ __host__ __device__ __forceinline__ uint4 pad_chunk(int T0, int T1) {
   return make_uint4((uint32_t)b0, (uint32_t)(b0 >> 32), (uint32_t)b1, (uint32_t)(b1 >> 32));
 }
 __host__ __device__ __forceinline__ uint4 k5p_offset_chunk(int T) { return pad_chunk(T, 0); }
+
+// K5w (wide rows, two codewords per accumulator column as 11-bit fields):
+//   acc = 2^23 + x_a + 2^11 x_b,  x = w(P ^ S) + 1024 - thr  in [0, 2047],
+// so a codeword can lower the bound iff bit 10 of its field is clear.  Part b
+// (table rows N + c) runs with B scale 2^11; each part's offset MMA adds
+// R = w(P) - thr from the A chunk R (against the table-offset pattern: 16
+// elements of 4.0, 16 of 1.0) and a constant from chunk Ca (part a: 5 x
+// 2^21) or Cb (part b: 1 x 2^10) against B = (1.0, 1.0, 0, ...), ue8m0
+// block scales (1, 2^21) / (2^11, 2^10): the constants sum to 2^23 + 1024 +
+// 2^11 * 1024.  Every product and partial sum is an integer below 2^24.
+constexpr int kWMaxSpan = 450;  // |R| <= 450: 4 * S4 + S1 with S4, S1 <= 90
+// producer threshold for a prefix of stored weight wt (<= 256) against a
+// bound rel (<= stored columns + g <= 384): raised to wt - kWMaxSpan at most
+// (only more tiles take the exact path), never lowered below rel
+__host__ __device__ __forceinline__ int k5w_threshold(int wt, int rel) {
+  return max(wt - kWMaxSpan, max(1, min(384, rel)));
+}
+// 16 e2m1 elements (two words of 8) summing to S (0 <= S <= 90)
+__host__ __device__ __forceinline__ void e2m1_sum16(int S, uint32_t& w0, uint32_t& w1) {
+  const int a = S < 46 ? S : 46;
+  w0 = e2m1_sum8(a);
+  w1 = e2m1_sum8(S - a);
+}
+// chunk R: R = 4 * S4 + S1 (sign on every nibble), S4 on the elements facing
+// the pattern's 4.0s (words 0, 2), S1 on its 1.0s (words 1, 3)
+__host__ __device__ __forceinline__ uint4 k5w_r_chunk(int R) {
+  const int A = R < 0 ? -R : R;
+  const int S4 = min(A / 4, 90), S1 = A - 4 * S4;
+  uint4 c;
+  e2m1_sum16(S4, c.x, c.z);
+  e2m1_sum16(S1, c.y, c.w);
+  if (R < 0) {
+    c.x |= 0x88888888u; c.y |= 0x88888888u; c.z |= 0x88888888u; c.w |= 0x88888888u;
+  }
+  return c;
+}
+// chunks Ca (4.0, 1.0 against B's 1.0, 1.0: 5) and Cb (1.0: 1)
+__host__ __device__ __forceinline__ uint4 k5w_const_chunk(int part) {
+  return make_uint4(part == 0 ? 0x26u : 0x02u, 0u, 0u, 0u);
+}
 
 // tcgen05 shared-memory matrix descriptor, SWIZZLE_NONE, K-major:
 // LBO = distance between the two 16-byte K chunks of one MMA (128 B here),
@@ -683,10 +739,10 @@ template <int W, bool F4, int CW = 1>
 __host__ __device__ inline size_t k4_smem_bytes(int m, int k, int ngroups) {
   size_t off = (smem_base_bytes<W>(m, k, ngroups) + 1023) & ~size_t(1023);
   off += (size_t)k4_stages<F4, CW>(W) * k4_tile_b<F4, CW>(W);
-  off += (size_t)k4_abufs<F4>(W) * kUmmaMA * k4_tile_a<F4, CW>(W);
+  off += (size_t)k4_abufs<F4, CW>(W) * kUmmaMA * k4_tile_a<F4, CW>(W);
   off += F4 ? kMagicBytes : 0;   // K5 magic operands
   off += kBarSlots * 8 + 16;     // barriers + TMEM base
-  off += k4_abufs<F4>(W) * kUmmaMA * kUmmaM * sizeof(int);  // prefix weights of the A buffers
+  off += k4_abufs<F4, CW>(W) * kUmmaMA * kUmmaM * sizeof(int);  // prefix weights of the A buffers
   off += kChunkQ * sizeof(long long) + 16;    // chunk queue
   off += kBndCache * sizeof(int);              // K5q bound cache
   return off;
@@ -766,6 +822,34 @@ __device__ __forceinline__ K4Chunk k4_decode(const Group* sg, int ngroups,
   return c;
 }
 
+// K5w epilogue: H columns c0.. of 2^23 + x_a + 2^11 x_b (11-bit fields);
+// columns past the valid part-a (la) / part-b (lb) range get bit 10 / 21
+// set.  Returns the smallest field below lx (lx if none).  The common case
+// -- every column in range, every field at or above the threshold -- is one
+// 3-input AND per two columns and one test; masking and the exact scan only
+// run on the slice's last tile / when some threshold bit is clear.
+template <int H>
+__device__ __forceinline__ int k5w_scan(uint32_t* v, int c0, int la, int lb, int lx) {
+  constexpr uint32_t kFlags = (1u << 10) | (1u << 21);
+  if (lb < c0 + H) {  // uniform: some column of this slice is past a range
+#pragma unroll
+    for (int i = 0; i < H; ++i) {
+      if (c0 + i >= la) v[i] |= 1u << 10;
+      if (c0 + i >= lb) v[i] |= 1u << 21;
+    }
+  }
+  uint32_t acc = 0xFFFFFFFFu;
+#pragma unroll
+  for (int i = 0; i + 1 < H; i += 2) acc &= v[i] & v[i + 1];
+  if (H & 1) acc &= v[H - 1];
+  if (__builtin_expect(!((~acc) & kFlags), 1)) return lx;
+  int mn = lx;
+#pragma unroll
+  for (int i = 0; i < H; ++i)
+    mn = min(mn, min((int)(v[i] & 0x7FFu), (int)((v[i] >> 11) & 0x7FFu)));
+  return mn;
+}
+
 // K4 (F4 = false, tcgen05.mma kind::i8) and K5 (F4 = true, kind::mxf4 with
 // unit block scales): one persistent CTA per SM, warp-specialised (see the
 // file comment).  The two differ only in operand encoding, MMA kind,
@@ -778,13 +862,16 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
   const RoundArgs& a = bt.a[0];
   constexpr bool PR = CW > 1;  // K5p (CW = 2) / K5t (CW = 3) / K5q (CW = 4)
   constexpr bool Q = CW == 4;  // K5q: two codewords as bytes, block16 scales
+  constexpr bool WQ = CW == 5;  // K5w: two codewords as 11-bit fields (wide rows)
+  constexpr bool QQ = Q || WQ;  // threshold-offset forms (bit test, bound cache)
   constexpr int NC = k5_ncw(CW);  // codewords per accumulator column
   static_assert(!F4 || kUmmaMA == 1, "K5 runs one A tile per B tile");
-  static_assert(CW >= 1 && CW <= 4, "kernel form");
+  static_assert(CW >= 1 && CW <= 5, "kernel form");
   // offset accumulators (packed s16 epilogue) for this instantiation
   constexpr bool MG = kK5Magic && (CW > 1 || (W & 1) || !BZ_K5_EVEN_F32);
-  static_assert(!PR || (F4 && kK5Magic && ((W & 1) || CW == 4) && W <= (CW == 4 ? 4 : 3) &&
-                        BZ_K5_SPLIT == 1 && (CW == 4 || BZ_K5_EPI_GROUPS == 1)),
+  static_assert(!PR || (F4 && kK5Magic && BZ_K5_SPLIT == 1 &&
+                        (WQ ? W >= 2 : (((W & 1) || CW == 4) && W <= (CW == 4 ? 4 : 3) &&
+                                        (CW == 4 || BZ_K5_EPI_GROUPS == 1)))),
                 "K5p/K5t: odd W <= 3, K5q: W <= 4 (stored weights <= 127 fit the fields)");
   constexpr int N = k4_n<F4, CW>();
   constexpr int TR = k4_tile_rows<F4, CW>();  // table rows per B tile
@@ -812,7 +899,7 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
   const size_t base = (smem_base_bytes<W>(a.m, a.k, staged_groups(a)) + 1023) & ~size_t(1023);
   unsigned char* sB = smem + base;
   unsigned char* sA = sB + S * TB;
-  constexpr int NA = k4_abufs<F4>(W);
+  constexpr int NA = k4_abufs<F4, CW>(W);
   unsigned char* sMagic = sA + NA * kUmmaMA * TA;  // K5: A, B magic core matrices
   unsigned long long* bars =
       reinterpret_cast<unsigned long long*>(sMagic + (F4 ? kMagicBytes : 0));
@@ -898,7 +985,11 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
     if (warp < 4) {
       for (int c = 0; c < 512 - kSfCol; c += 8)
         tmem_st8(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(kSfCol + c),
-                 Q ? (kSfCol + c == kSfColMagic ? 0x78787878u   // ue4m3 256: half b
+                 WQ ? (c == 0 ? 0x7F7F7F7Fu                             // ue8m0 1
+                       : c == 8 ? 0x8A8A8A8Au                           // 2^11: part b
+                       : kSfCol + c == kSfColMagic ? 0x7F7F947Fu        // (1, 2^21): part a offset
+                                                   : 0x7F7F898Au)       // (2^11, 2^10): part b
+                 : Q ? (kSfCol + c == kSfColMagic ? 0x78787878u   // ue4m3 256: half b
                       : kSfCol + c == kSfColPad ? 0x78383838u  // A: 256 on block 3
                                                 : 0x38383838u) // ue4m3 1.0
                  : kSfCol + c == kSfColMagic
@@ -913,7 +1004,11 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
       // reads these rows)
       const int op = tid / 16, row16 = tid % 16;  // row16 < 8: chunk 0
       uint4 z = make_uint4(0, 0, 0, 0);
-      if constexpr (Q) {
+      if constexpr (WQ) {
+        // K5w: B of both parts' offset MMAs (op 1) = [offset pattern,
+        // (1.0, 1.0, 0, ...)] against A chunks (R, Ca) / (R, Cb)
+        if (op == 1) z = row16 < 8 ? k5_table_offset_chunk() : make_uint4(0x22u, 0u, 0u, 0u);
+      } else if constexpr (Q) {
         // K5q, even W: the B side of the offset MMAs (the tables carry no
         // offset chunk): op 0 = [offset pattern, 0] (part a), op 1 =
         // [0, offset pattern] (part b), against A chunks (pad_a, pad_b)
@@ -926,11 +1021,24 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
       *reinterpret_cast<uint4*>(sMagic + op * 256 + row16 * 16) = z;
       fence_proxy_async();
     }
-    if constexpr (Q)
+    if constexpr (QQ)
       if (tid < kBndCache) {
         const int rr = tid / kBndPerRound, j = tid % kBndPerRound;
         s_bnd[tid] = rr < bt.count && j < a.m ? ((volatile int*)bt.a[rr].bound)[1 + j] : INT_MAX;
       }
+    if (WQ && warp >= RL::PROD0) {
+      // K5w: the constant A chunks of both A buffers -- zero padding (odd
+      // W: it meets the table's offset chunk), Ca, Cb
+      const int r = tid - 32 * RL::PROD0;
+      constexpr int WD = k5w_data_chunks(W);
+      for (int ab = 0; ab < NA; ++ab) {
+        unsigned char* row = sA + ab * TA;
+        if (WD > W) *reinterpret_cast<uint4*>(row + umma_off_c(r, W, CA)) = make_uint4(0u, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(row + umma_off_c(r, WD + 1, CA)) = k5w_const_chunk(0);
+        *reinterpret_cast<uint4*>(row + umma_off_c(r, WD + 2, CA)) = k5w_const_chunk(1);
+      }
+      fence_proxy_async();
+    }
     if (!PR && CA > W && warp >= RL::PROD0) {
       // the A padding chunk: zero, or 1.5 at element 8 (padding-chunk offset)
       const int r = tid - 32 * RL::PROD0;
@@ -985,6 +1093,7 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
         for (int j = 0; j < kUmmaMA; ++j) rmin[j] = INT_MAX / 2;
         float fmin_acc = __int_as_float(0x7f800000);  // K5: +inf
         int lx = 128;  // K5q: this row's bytes below lx can still lower its minimum
+        int lx1024 = 1024;  // K5w: this row's fields below lx1024 can still lower it
         for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount) {
           if (EGRP > 1 && (int)(tcount % EGRP) != egroup) continue;
           const int buf = tcount % ACC;
@@ -1061,6 +1170,37 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
             // words each tile (config 4: 105 -> 48 us).  (A warp-level
             // reduction first measured 4 % slower on config 5's g = 8.)
             if (wg != INT_MAX) bnd_publish(s_bnd, ar, rr, c.gr.gamma, wg);
+          } else if constexpr (WQ) {
+            // K5w: every column holds 2^23 + x_a + 2^11 x_b, x = w + 1024 -
+            // thr (thr = wt[0]): a codeword can lower the bound iff bit 10 of
+            // its field is clear.  Two loads (register budget), each tested
+            // before the next; the buffer is released after the second.
+            constexpr int H0 = EC > 32 ? 32 : EC, H1 = EC - H0;
+            static_assert(H0 % 4 == 0 && H1 % 4 == 0, "K5w epilogue phases");
+            const int la = c.slice - t * TR - EC * slice_id;  // part-a columns < la valid
+            uint32_t v[H0];
+            tmem_ld_cols<H0>(tb, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < H0; i += 4) tmem_regs4_after_wait(v + i);
+            int mn = k5w_scan<H0>(v, 0, la, la - N, lx1024);
+            if constexpr (H1 > 0) {
+              tmem_ld_cols<H1>(tb + H0, v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < H1; i += 4) tmem_regs4_after_wait(v + i);
+            }
+            if (!BZ_K5_NOFENCE) tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(accempty(hb));  // accumulators are in registers
+            if constexpr (H1 > 0) mn = k5w_scan<H1>(v, H0, la, la - N, mn);
+            if (mn < lx1024) {
+              lx1024 = mn;
+              const int w = mn - 1024 + wt[0];
+              rmin[0] = min(rmin[0], w);
+              const int w2 = w + gamma_woff(ar, c.gr.gamma);
+              if (w2 < bnd_cache_read(s_bnd, rr, c.gr.gamma)) bnd_publish(s_bnd, ar, rr, c.gr.gamma, w2);
+            }
           } else if constexpr (CW == 3) {
             // K5t: every column holds three codewords, 2^23 + wt_a + 2^8 wt_b
             // + 2^16 wt_c: bytes 0..2 are stored weights <= 96, byte 3 the
@@ -1264,7 +1404,7 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
           atomicMin(ar.bound + 1 + c.gr.gamma, wb);
           atomicMin(ar.bound, wb);
           gbound_publish(ar, wb);
-          if constexpr (Q)
+          if constexpr (QQ)
             if (c.gr.gamma < kBndPerRound) atomicMin(s_bnd + rr * kBndPerRound + c.gr.gamma, wb);
         }
         long long* ct = k4_ctrace(a, qi);
@@ -1348,6 +1488,14 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
             *reinterpret_cast<uint4*>(dst + umma_off_c(r, W, CA)) = pad_chunk(x, 0);
             *reinterpret_cast<uint4*>(dst + umma_off_c(r, W + 1, CA)) = pad_chunk(x, 128);
             wt = thr;  // the epilogue needs thr to turn a byte back into a weight
+          } else if constexpr (WQ) {
+            // K5w: chunk R = w(P) - thr, so both 11-bit fields read
+            // x = w(P ^ S) + 1024 - thr (k5w_threshold keeps |R| <= 450)
+            int ub = min(((volatile int*)ar.bound)[1 + c.gr.gamma], bnd_cache_read(s_bnd, rr, c.gr.gamma));
+            for (int q = 0; q < rr; ++q) ub = min(ub, ((volatile const int*)bt.a[q].bound)[0]);
+            const int thr = k5w_threshold(wt, ub - gamma_woff(ar, c.gr.gamma));
+            *reinterpret_cast<uint4*>(dst + umma_off_c(r, k5w_data_chunks(W), CA)) = k5w_r_chunk(wt - thr);
+            wt = thr;  // the epilogue turns a field back into a weight with it
           } else if constexpr (PR) {
             // offset chunks: w(P) for every part (so each field is a whole
             // stored weight), + 128 on the last (its scale 2^16 makes that the
@@ -1450,7 +1598,23 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
                   // so it meets offset chunk q
                   const uint32_t dj = dbase;
                   const uint64_t adj = a_desc0 + (uint64_t)(ab * (TA >> 4));
-                  if constexpr (Q && !(W & 1)) {
+                  if constexpr (WQ) {
+                    // K5w: per part the data MMAs (part b with B scale 2^11),
+                    // then one offset MMA of A chunks (R, Ca) / (R, Cb) (LBO
+                    // 128 / 256 B) against the constant B operand
+                    constexpr int WD = k5w_data_chunks(W);
+                    const uint32_t sf1 = tmem + kSfCol, sf11 = tmem + kSfCol + 8;
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                      const uint64_t bdq = bd0 + (uint64_t)(q * (N / 8) * CB * 8);
+#pragma unroll
+                      for (int kb = 0; kb < WD / 2; ++kb)
+                        umma_mxf4(dj, adj + 16u * kb, bdq + 16u * kb, IDESC, (q | kb) ? 1u : 0u,
+                                  sf1, q ? sf11 : sf1);
+                      umma_mxf4(dj, adj + 8u * WD + ((uint64_t)(8 * q) << 16), magic_b, IDESC, 1u,
+                                q ? sfp : sfm, sf1);
+                    }
+                  } else if constexpr (Q && !(W & 1)) {
                     // K5q, even W: W/2 data MMAs per part, then one offset MMA
                     // of A chunks (pad_a, pad_b) against a constant B
 #pragma unroll

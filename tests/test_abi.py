@@ -37,7 +37,8 @@ def test_header_symbols_exported():
     assert L.bz_abi_version() == _native.ABI_VERSION
 
 
-@pytest.mark.parametrize("engine", ["auto", "popc", "imma", "umma", "mxf4", "mxf4p", "mxf4t", "mxf4q"])
+@pytest.mark.parametrize("engine", ["auto", "popc", "imma", "umma", "mxf4", "mxf4p", "mxf4t", "mxf4q",
+                                    "mxf4w"])
 def test_plan_counts(engine):
     for (m, k, g) in [(1, 5, 1), (2, 24, 3), (2, 80, 8), (3, 40, 8), (1, 64, 6), (2, 128, 4)]:
         groups, nchunks = _native.plan(m, k, g, engine)
@@ -50,7 +51,7 @@ def test_plan_counts(engine):
             assert nsb >= 1 and (depth < 3 or spc * nsb >= comb(k - sfloor, depth))
             assert lanes == ({"imma": 256}.get(engine, 128) if depth >= 3 else 32)
             want = 3 if (engine != "popc" and g >= 4) else (2 if g >= 4 else 1)
-            if engine in ("auto", "mxf4", "mxf4p", "mxf4t", "mxf4q") and g >= 4:
+            if engine in ("auto", "mxf4", "mxf4p", "mxf4t", "mxf4q", "mxf4w") and g >= 4:
                 # K5 suffix levels: depth 3..5, floors above ell + 1
                 assert 3 <= depth <= min(5, g - 1) and sfloor >= ell + 1
             else:
@@ -59,7 +60,8 @@ def test_plan_counts(engine):
             assert combos == nprefix * comb(k - sfloor, depth)
 
 
-@pytest.mark.parametrize("engine", ["auto", "popc", "imma", "umma", "mxf4", "mxf4p", "mxf4t", "mxf4q"])
+@pytest.mark.parametrize("engine", ["auto", "popc", "imma", "umma", "mxf4", "mxf4p", "mxf4t", "mxf4q",
+                                    "mxf4w"])
 @pytest.mark.parametrize("m,k,g", [(1, 6, 1), (1, 7, 2), (2, 9, 3), (1, 12, 5),
                                    (2, 10, 10), (1, 40, 3), (1, 34, 4), (1, 20, 6)])
 def test_plan_partitions_rank_space(m, k, g, engine):
@@ -123,7 +125,8 @@ def test_plan_levels_partition(monkeypatch, m, k, g, floors):
     expect = sorted(oracle.all_combinations(m, k, g))
     groups, _ = _native.plan(m, k, g, "mxf4")
     assert max(collections.Counter(int(gr[6]) for gr in groups)) > 3  # deeper levels in use
-    for engine, nshards in (("mxf4", 1), ("mxf4", 3), ("mxf4p", 1), ("mxf4p", 3), ("mxf4t", 3), ("mxf4q", 3)):
+    for engine, nshards in (("mxf4", 1), ("mxf4", 3), ("mxf4p", 1), ("mxf4p", 3), ("mxf4t", 3), ("mxf4q", 3),
+                            ("mxf4w", 2)):
         groups, nchunks = _native.plan(m, k, g, engine, nshards)
         seen = []
         for s in range(nshards):

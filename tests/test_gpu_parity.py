@@ -27,11 +27,12 @@ def ctx():
     return _native.context(0)
 
 
-@pytest.fixture(params=["popc", "mxf4", "mxf4q"])
+@pytest.fixture(params=["popc", "mxf4", "mxf4q", "mxf4w"])
 def engine(request):
     """Every kernel of the library: K1 (XOR+POPC), K5 (tcgen05 kind::mxf4,
-    g >= 4) and K5q (kind::mxf4nvf4, two codewords per accumulator; W <= 4
-    and <= 127 stored columns -- other shapes run K5)."""
+    g >= 4), K5q (kind::mxf4nvf4, two codewords per accumulator as bytes;
+    W <= 4 and <= 128 stored columns -- other shapes run K5) and K5w
+    (kind::mxf4, two codewords as 11-bit fields; W >= 2)."""
     _native.context(0).set_engine(request.param)
     yield request.param
     _native.context(0).set_engine("auto")
@@ -273,7 +274,7 @@ def test_early_exit_all_engines(ctx, engine):
 @pytest.mark.parametrize("k,g,floors", [(12, 6, "4,7"), (14, 8, "5,9"), (12, 5, "6"),
                                         (20, 7, "8,13"), (11, 9, "0,3")])
 @pytest.mark.parametrize("n", [20, 37, 70, 96, 160, 230])
-@pytest.mark.parametrize("kernel", ["mxf4", "mxf4q"])
+@pytest.mark.parametrize("kernel", ["mxf4", "mxf4q", "mxf4w"])
 def test_mxf4_levels(monkeypatch, ctx, k, g, floors, n, kernel):
     """K5 / K5p with forced suffix levels (depth-4/5 tables): exact minima and
     combination counts per Gamma against the oracle (K5p runs at n = 20, 70,
@@ -446,16 +447,18 @@ def test_k5q_dense_prefix_small_bound(ctx):
         ctx.set_engine("auto")
 
 
-def _dense_systematic(k: int, seed: int, light: int):
-    """[I_k | A] with A random and invertible, A's row 0 all ones (stored
-    weight k in Gamma_1) and row 1 of weight `light` - 1 (a planted codeword
-    of weight `light`)."""
+def _dense_systematic(k: int, seed: int, light: int, r: int | None = None):
+    """[I_k | A] with A (k x r, r = k by default) random, A's row 0 all ones
+    (stored weight r in Gamma_1) and row 1 of weight `light` - 1 (a planted
+    codeword of weight `light`); at least two full information sets (exactly
+    two, no remainder, when r = k)."""
     rng = random.Random(seed)
-    n = 2 * k
+    r = k if r is None else r
+    n = k + r
     while True:
-        A = [rng.getrandbits(k) for _ in range(k)]
-        A[0] = (1 << k) - 1
-        A[1] = sum(1 << b for b in rng.sample(range(k), light - 1))
+        A = [rng.getrandbits(r) for _ in range(k)]
+        A[0] = (1 << r) - 1
+        A[1] = sum(1 << b for b in rng.sample(range(r), light - 1))
         rows = [(1 << i) | (a << k) for i, a in enumerate(A)]
         try:
             from paper_1603_06757_b200.gf2 import build_gamma_set
@@ -463,7 +466,7 @@ def _dense_systematic(k: int, seed: int, light: int):
             gs = build_gamma_set(BitMatrix(rows, n))
         except Exception:
             continue
-        if gs.full_rank_count == 2 and gs.remainder_rank == 0:
+        if gs.full_rank_count == 2 and (gs.remainder_rank == 0 or r > k):
             return rows, n
 
 
@@ -479,6 +482,68 @@ def test_k5q_dense_row_minimum_distance():
     assert rep.distance == want["distance"] == 12
     assert rep.counters.combinations == want["combinations"]
     assert _native.context(0).elided() == 0b11  # both Gammas store n - k = 127 columns
+
+
+@pytest.mark.parametrize("n", [129, 160, 185, 192, 193, 224, 255, 256])
+@pytest.mark.parametrize("density", [0.05, 0.5, 0.97])
+def test_k5w_weight_range(ctx, n, density):
+    """K5w packs two codewords as 11-bit fields x = w + 1024 - thr of one
+    fp32 accumulator (rows wider than K5q's 128 stored columns): every stored
+    weight from 0 to 256 must come back exact -- zero codewords, all-one rows,
+    dense prefixes (R = w(P) - thr up to 450 in the offset chunk), slices
+    crossing the 480-row tile and both parts of a column -- under loose,
+    exact and too-tight bounds."""
+    rng = random.Random(n * 100 + int(density * 100))
+    k = 22
+    rows = [sum(1 << b for b in range(n) if rng.random() < density) for _ in range(k)]
+    rows[3] = rows[4]                      # a zero codeword at every even g >= 2
+    rows[5] = (1 << n) - 1                 # an all-ones row
+    ctx.set_engine("mxf4w")
+    try:
+        ctx.load(family_words([BitMatrix(rows, n), BitMatrix(rows[::-1], n)], n), n)
+        for g in (4, 5, 6, 7):
+            want = oracle.min_weight(rows, n, g)[0]
+            for upper in (1 << 30, want + 1, want, max(want - 2, 0)):
+                mins, combos = ctx.round(g, -1, upper)
+                assert mins == [min(want, upper)] * 2 and combos == [comb(k, g)] * 2, \
+                    (g, upper, mins, want)
+    finally:
+        ctx.set_engine("auto")
+
+
+@pytest.mark.parametrize("n", [150, 200, 256])
+def test_k5w_all_heavy(ctx, n):
+    """Odd g over identical all-ones rows: every codeword has stored weight
+    n (up to 256, the widest field value); even g: weight 0."""
+    k = 15
+    rows = [(1 << n) - 1] * k
+    ctx.set_engine("mxf4w")
+    try:
+        ctx.load(family_words([BitMatrix(rows, n)], n), n)
+        for g in (5, 7, 9):
+            mins, _ = ctx.round(g, -1, 1 << 30)
+            assert mins == [n], (g, mins)
+            mn, c = ctx.enumerate(0, g)
+            assert (mn, c) == (n, comb(k, g)), (g, mn, c)
+        for g in (4, 6):
+            mins, _ = ctx.round(g, -1, 1 << 30)
+            assert mins == [0], (g, mins)
+    finally:
+        ctx.set_engine("auto")
+
+
+@pytest.mark.parametrize("engine_name", ["auto", "mxf4w"])
+def test_k5w_dense_row_minimum_distance(engine_name):
+    """BZ on a [280, 100] code whose Gammas keep 180 stored columns (AUTO
+    runs K5 there, mxf4w forces K5w for g >= 4; two full information sets and
+    a remainder), with an all-ones row and a planted light codeword: trace,
+    distance and counts equal the C oracle's."""
+    rows, n = _dense_systematic(100, 13, 14, r=180)
+    want = oracle.minimum_distance(rows, n, max_g=4)
+    rep = minimum_distance(BitMatrix(rows, n), EngineConfig(engine=engine_name, max_g=4))
+    assert rep.bounds_trace == [tuple(t) for t in want["bounds_trace"]]
+    assert rep.distance == want["distance"] == 14
+    assert rep.counters.combinations == want["combinations"]
 
 
 @pytest.mark.parametrize("engine_name", ["auto", "mxf4", "popc"])
