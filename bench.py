@@ -563,11 +563,12 @@ def main():
     # per round: a result record {cursor, combos[m], bounds[m+1]} both ways
     # and the round's plan (56-byte groups, 256-byte aligned) host -> device
     # (bz.cu io_layout / run_batch)
-    record = (8 + 8 * m + 4 * (m + 1) + 15) // 16 * 16
+    # (the round plans stay resident on the device between runs of the same
+    # shape -- bz.cu run_batch -- so a repeated run uploads records only)
+    record = (8 + 3 * 8 * m + 4 * (m + 1) + 15) // 16 * 16
     d2h = 0
     for (g, L, U) in rep.bounds_trace:
-        groups, _ = _native.plan(m, k, g)
-        h2d += record + (len(groups) * 56 + 255) // 256 * 256
+        h2d += record
         d2h += record
 
     if rank != 0:

@@ -89,6 +89,10 @@ struct bz_ctx {
   unsigned char* d_io = nullptr;
   unsigned char* h_io = nullptr;  // pinned mirror
   size_t io_cap = 0;
+  // the plan keys and offsets of the last batch whose group tables are in
+  // h_io and d_io: an identical round (same key, same offset) is neither
+  // copied nor uploaded again
+  std::vector<std::pair<std::string, size_t>> io_plans;
   unsigned long long* d_hist = nullptr;    // BZ_MAX_N + 1
   // pinned histogram staging
   unsigned long long* h_hist = nullptr;
@@ -175,6 +179,7 @@ int ensure_io(bz_ctx* ctx, int nslots) {
     if (ctx->h_io) cudaFreeHost(ctx->h_io);
     ctx->d_io = ctx->h_io = nullptr;
     ctx->io_cap = 0;
+    ctx->io_plans.clear();
     const size_t cap = std::max<size_t>(total, 64 * 1024);
     CK(cudaMalloc(&ctx->d_io, cap));
     CK(cudaMallocHost(&ctx->h_io, cap));
@@ -474,7 +479,7 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
 // process: a repeated run (same dimensions) copies its group tables instead
 // of re-planning every round before the first launch.
 int plan_round(bz_ctx* ctx, int g, int gamma_only, PlanShape shape, int nshards, size_t goff,
-               int* out_ngroups, unsigned long long* out_nchunks) {
+               int* out_ngroups, unsigned long long* out_nchunks, int slot, bool* out_fresh) {
   struct Plan {
     std::vector<Group> groups;
     unsigned long long nchunks;
@@ -500,7 +505,15 @@ int plan_round(bz_ctx* ctx, int g, int gamma_only, PlanShape shape, int nshards,
     it = memo.emplace(key, std::move(p)).first;
   }
   (void)l;
-  std::memcpy(ctx->h_io + goff, it->second.groups.data(), it->second.groups.size() * sizeof(Group));
+  // already in place from the last batch (host image and device copy)?
+  const bool same = slot < (int)ctx->io_plans.size() && ctx->io_plans[slot].first == key &&
+                    ctx->io_plans[slot].second == goff;
+  if (!same) {
+    std::memcpy(ctx->h_io + goff, it->second.groups.data(), it->second.groups.size() * sizeof(Group));
+    if ((int)ctx->io_plans.size() <= slot) ctx->io_plans.resize(slot + 1);
+    ctx->io_plans[slot] = {key, goff};
+  }
+  *out_fresh = !same;
   *out_ngroups = (int)it->second.groups.size();
   *out_nchunks = it->second.nchunks;
   return BZ_OK;
@@ -923,6 +936,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   const auto t_plan0 = std::chrono::steady_clock::now();
   // plans follow the result records; goff = where round i's groups go
   size_t goff = ((size_t)count * l.off_groups + 255) & ~size_t(255);
+  size_t first_fresh = SIZE_MAX;  // first group table this batch has to upload
   for (int i = 0; i < count; ++i) {
     const int g = g0 + i;
     const PlanShape shape = pass_shape(ctx->engine, g, hist, ctx->w32, ctx->m, ctx->k, ctx->n_eff);
@@ -934,8 +948,10 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     unsigned long long nchunks = 0;
     const size_t gthis = goff;
     const int r_shard = owner[i] >= 0 ? 0 : shard, r_nshards = owner[i] >= 0 ? 1 : nshards;
-    rc = plan_round(ctx, g, gamma_only, shape, r_nshards, gthis, &ngroups, &nchunks);
+    bool fresh = true;
+    rc = plan_round(ctx, g, gamma_only, shape, r_nshards, gthis, &ngroups, &nchunks, i, &fresh);
     if (rc) return rc;
+    if (fresh && first_fresh == SIZE_MAX) first_fresh = gthis;
     if (shape.kernel >= 5) {
       // the suffix tables this round's levels read
       int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX};
@@ -1001,12 +1017,19 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     }
     goff = (gthis + (size_t)ngroups * sizeof(Group) + 255) & ~size_t(255);
   }
+  // entries past this batch describe memory it may have overwritten
+  ctx->io_plans.resize(count);
   const auto t_plan1 = std::chrono::steady_clock::now();
   if (hist)
     CK(cudaMemsetAsync(ctx->d_hist, 0, sizeof(unsigned long long) * (ctx->n + 1), ctx->stream));
-  // the used image only: result records + each round's groups
-  CK(cudaMemcpyAsync(ctx->d_io, ctx->h_io, goff, cudaMemcpyHostToDevice,
+  // the used image only: the result records, and the group tables from the
+  // first one that is not already on the device (a repeated run of the same
+  // shape uploads its records alone)
+  CK(cudaMemcpyAsync(ctx->d_io, ctx->h_io, (size_t)count * l.off_groups, cudaMemcpyHostToDevice,
                      ctx->stream));
+  if (first_fresh != SIZE_MAX)
+    CK(cudaMemcpyAsync(ctx->d_io + first_fresh, ctx->h_io + first_fresh, goff - first_fresh,
+                       cudaMemcpyHostToDevice, ctx->stream));
   while ((int)ctx->ev_round.size() < count + 1) {
     cudaEvent_t e;
     CK(cudaEventCreate(&e));
