@@ -33,7 +33,7 @@ from math import comb
 import numpy as np
 
 from . import _native
-from .enumeration import EnumerationResult, PassCount, family_words, split_count
+from .enumeration import EnumerationResult, PassCount, family_words
 from .errors import InvalidArity, InvalidDimensions, Interrupted, TooLarge
 from .gf2 import BitMatrix, GammaSet, build_gamma_set
 from .parallel import LocalComm, combine_rounds
@@ -214,6 +214,9 @@ class GpuRounds:
         res = self.ctx.rounds(g0, lower_prevs, upper, self.comm.rank, self.comm.world)
         ms = self.ctx.round_ms(len(lower_prevs))
         adds, accs = self.ctx.counters(len(lower_prevs))
+        if self.comm.world == 1:
+            return [(mn, [PassCount(c, a, x) for c, a, x in zip(cb, ad, ac)])
+                    for (mn, cb), ad, ac in zip(res, adds, accs)], ms
         res = [(mn, cb + ad + ac) for (mn, cb), ad, ac in zip(res, adds, accs)]
         out = []
         for mn, sums in combine_rounds(self.comm, res):
@@ -265,60 +268,88 @@ def start_state(gs: GammaSet, n: int, k: int, config: EngineConfig) -> LoopState
 def run_rounds(backend, gs: GammaSet, k: int, config: EngineConfig, st: LoopState) -> None:
     """The loop of engine.py:204-217 with one device round per g: fold the
     per-Gamma minima into U in Gamma order, then raise L, append (g, L, U),
-    report progress.  ``backend`` already holds the family on the device."""
+    report progress.  ``backend`` already holds the family on the device.
+
+    (This loop sits inside every timed run: it keeps to plain locals and
+    arithmetic -- the L formula inlined, counters summed once per round.)"""
     m_arg, km_arg = line7_args(gs, k)
     m = gs.matrix_count
     batch_ok = config.batch_combinations > 0 and hasattr(backend, "run_batch")
     if hasattr(backend, "begin_run"):
         backend.begin_run()
+    max_g = config.max_g
+    progress = config.progress
+    g, L, U = st.g, st.L, st.U
+    trace, rounds, ctr = st.trace, st.rounds, st.counters
+
+    def lower(gg: int) -> int:  # lower_bound_update (engine.py:97-103)
+        return (m_arg - 1) * (gg + 1) + max(0, gg + 1 - k + km_arg)
+
     queued: list = []  # precomputed (g, mins, combos, kernel_ms) of a batch
-    while st.g <= k and st.L < st.U:
-        if st.g > config.max_g:
-            st.status = STATUS_UPPER_BOUND_ONLY
-            break
-        tr = time.perf_counter()
-        if not queued and batch_ok:
-            # the next rounds whose total size fits the batch budget (per
-            # rank: a batch is sharded like a round)
-            world = getattr(getattr(backend, "comm", None), "world", 1)
-            ahead = world == 1 or getattr(backend, "shared", False)
-            budget = (max(config.batch_combinations * world, config.batch_combinations_single)
-                      if ahead else config.batch_combinations * world)
-            count, total = 0, 0
-            while (st.g + count <= min(k, config.max_g)
-                   and total + m * comb(k, st.g + count) <= budget):
-                total += m * comb(k, st.g + count)
-                count += 1
-            if count >= 2:
-                lps = [st.L]
-                for i in range(1, count):
-                    lps.append(lower_bound_update(st.g + i - 1, m_arg, k, km_arg))
-                res, batch_ms = backend.run_batch(st.g, lps, st.U)
-                for i, (mn, cb) in enumerate(res):
-                    if isinstance(batch_ms, list):  # per-round device times
-                        ms = batch_ms[i]
-                    else:  # one time for the batch: split by combinations
-                        ms = batch_ms * ((m * comb(k, st.g + i)) / total if total else 0.0)
-                    queued.append((st.g + i, mn, cb, ms))
-        if queued and queued[0][0] == st.g:
-            _, mins, combos, kernel_ms = queued.pop(0)
-        else:
-            queued.clear()
-            mins, combos, kernel_ms = backend.run(st.g, st.L, st.U)
-        round_combos = 0
-        for mn, cnt in zip(mins, combos):
-            st.U = min(st.U, mn)
-            c, adds, accs = split_count(cnt)
-            st.counters.add(EnumerationResult(st.U, c, adds, accs))
-            round_combos += c
-        st.rounds.append(RoundStat(st.g, round_combos, kernel_ms,
-                                   (time.perf_counter() - tr) * 1e3))
-        st.L = lower_bound_update(st.g, m_arg, k, km_arg)
-        st.trace.append((st.g, st.L, st.U))
-        st.g_reached = st.g
-        if config.progress is not None:
-            config.progress(st.g, st.L, st.U)
-        st.g += 1
+    qi = 0
+    try:
+        while g <= k and L < U:
+            if g > max_g:
+                st.status = STATUS_UPPER_BOUND_ONLY
+                break
+            tr = time.perf_counter()
+            if qi == len(queued) and batch_ok:
+                # the next rounds whose total size fits the batch budget (per
+                # rank: a batch is sharded like a round)
+                world = getattr(getattr(backend, "comm", None), "world", 1)
+                ahead = world == 1 or getattr(backend, "shared", False)
+                budget = (max(config.batch_combinations * world, config.batch_combinations_single)
+                          if ahead else config.batch_combinations * world)
+                count, total = 0, 0
+                top = min(k, max_g)
+                while g + count <= top:
+                    c = m * comb(k, g + count)
+                    if total + c > budget:
+                        break
+                    total += c
+                    count += 1
+                if count >= 2:
+                    lps = [L] + [lower(g + i - 1) for i in range(1, count)]
+                    res, batch_ms = backend.run_batch(g, lps, U)
+                    per_round = isinstance(batch_ms, list)
+                    queued = []
+                    qi = 0
+                    for i, (mn, cb) in enumerate(res):
+                        ms = (batch_ms[i] if per_round else
+                              batch_ms * ((m * comb(k, g + i)) / total if total else 0.0))
+                        queued.append((g + i, mn, cb, ms))
+            if qi < len(queued) and queued[qi][0] == g:
+                _, mins, combos, kernel_ms = queued[qi]
+                qi += 1
+            else:
+                queued, qi = [], 0
+                mins, combos, kernel_ms = backend.run(g, L, U)
+            rc = ra = rx = 0
+            for mn, cnt in zip(mins, combos):
+                if mn < U:
+                    U = mn
+                if isinstance(cnt, PassCount):
+                    rc += cnt.combinations
+                    ra += cnt.additions
+                    rx += cnt.accesses
+                else:
+                    rc += cnt
+                    ra += cnt
+                    rx += cnt
+            ctr.combinations += rc
+            ctr.row_additions += ra
+            ctr.row_accesses += rx
+            rounds.append(RoundStat(g, rc, kernel_ms, (time.perf_counter() - tr) * 1e3))
+            L = lower(g)
+            trace.append((g, L, U))
+            st.g_reached = g
+            st.L, st.U = L, U
+            if progress is not None:
+                progress(g, L, U)
+            g += 1
+            st.g = g
+    finally:
+        st.g, st.L, st.U = g, L, U
 
 
 def minimum_distance(G: BitMatrix, config: EngineConfig | None = None) -> DistanceReport:
