@@ -837,6 +837,29 @@ int ensure_triples(bz_ctx* ctx, int) {
 }
 #endif
 
+template <int W>
+int launch_seed_w(bz_ctx* ctx, const RoundArgs& a, int gamma_only) {
+  if (a.g > bz::kSeedMaxG) return BZ_OK;
+  bz::k_seed_bound<W><<<(unsigned)ctx->sm_count, 128, 0, ctx->stream>>>(a, gamma_only, 1);
+  CK(cudaGetLastError());
+  ctx->launches += 1;
+  return BZ_OK;
+}
+
+int launch_seed(bz_ctx* ctx, const RoundArgs& a, int gamma_only) {
+  switch (ctx->w32) {
+    case 1: return launch_seed_w<1>(ctx, a, gamma_only);
+    case 2: return launch_seed_w<2>(ctx, a, gamma_only);
+    case 3: return launch_seed_w<3>(ctx, a, gamma_only);
+    case 4: return launch_seed_w<4>(ctx, a, gamma_only);
+    case 5: return launch_seed_w<5>(ctx, a, gamma_only);
+    case 6: return launch_seed_w<6>(ctx, a, gamma_only);
+    case 7: return launch_seed_w<7>(ctx, a, gamma_only);
+    case 8: return launch_seed_w<8>(ctx, a, gamma_only);
+    default: return fail(ctx, BZ_ERR_TOO_LARGE, "unsupported word count %d", ctx->w32);
+  }
+}
+
 // `count` consecutive rounds of the same tensor-core shape in one launch
 // (count = 1 for every other kernel)
 template <int W>
@@ -896,6 +919,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     RoundArgs a;
     PlanShape shape;
     bool run;
+    bool seed;  // a threshold kernel starting with no bound: seed it first
   };
   std::vector<Pending> todo(count);
   long long* trace = nullptr;
@@ -1008,12 +1032,15 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
       // elided g, so a shard that visits any of its combinations reports
       // min(upper, true minimum) exactly when its bound starts at that cap --
       // which keeps K5q's threshold inside its byte fields (k5q_threshold)
+      bool loose = shape.kernel == 8 || shape.kernel == 9;
       for (int j = 0; j < m; ++j)
         if (gamma_only < 0 || gamma_only == j) {
           const long long cap =
               (long long)ctx->n_stored[j] + (((ctx->elide_mask >> j) & 1ull) ? g : 0);
           if (cap < hb[1 + j]) hb[1 + j] = (int)cap;
+          else loose = false;  // the caller's bound already says something
         }
+      todo[i].seed = loose && !debug;
     }
     goff = (gthis + (size_t)ngroups * sizeof(Group) + 255) & ~size_t(255);
   }
@@ -1076,6 +1103,13 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
       prev_round = false;
       big_lo = i;
       big_hi = i + f;
+    }
+    if (todo[i].seed && !hist) {
+      // a threshold kernel (K5q / K5w) with no bound to start from: a
+      // sample of the pass lowers it first (k_seed_bound)
+      rc = launch_seed(ctx, todo[i].a, gamma_only);
+      if (rc) return rc;
+      prev_round = false;
     }
     ctx->pdl_next = prev_round && !debug;
     std::vector<RoundArgs> as;

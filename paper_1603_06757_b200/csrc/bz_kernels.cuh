@@ -680,6 +680,74 @@ __global__ void __launch_bounds__(256) k1_rounds(const K1Batch b) {
 }
 
 // ---------------------------------------------------------------------------
+// Bound seed for the threshold kernels (K5q / K5w).  Their producers write
+// each prefix row against the Gamma's bound as it stands, and every
+// codeword under that threshold takes the exact path in the epilogue; a pass
+// that starts with no bound at all (bz_enumerate, config 4) would send its
+// first prefix steps on every SM down that path.  Before such a pass, every
+// thread weighs a few pseudo-random g-combinations of the pass (colex
+// unrank of a hashed rank) and lowers the bounds with their weights -- true
+// codeword weights of this pass, so the result stays min(start, true
+// minimum) exactly; only the thresholds get tight from the first tile on.
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+constexpr int kSeedMaxG = 16;  // deeper rounds always start from a bound
+
+template <int W>
+__global__ void __launch_bounds__(128) k_seed_bound(const RoundArgs a, int gamma_only, int samples) {
+  constexpr int WP = padded_words(W);
+  // C(c, q) for c <= k, q <= g and the Gamma's rows in shared memory: the
+  // unrank's binary searches would otherwise wait on L2 at every step
+  __shared__ unsigned long long sb[kBinomDim * (kSeedMaxG + 1)];
+  __shared__ __align__(16) uint32_t sr[kMaxK * kMaxW];
+  const int k = a.k, g = a.g;
+  for (int i = threadIdx.x; i < (k + 1) * (g + 1); i += blockDim.x)
+    sb[i] = a.binom[(i / (g + 1)) * kBinomDim + i % (g + 1)];
+  const int j0 = gamma_only < 0 ? 0 : gamma_only, j1 = gamma_only < 0 ? a.m : gamma_only + 1;
+  const unsigned long long total = a.binom[k * kBinomDim + g];
+  const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int j = j0; j < j1; ++j) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < k * WP; i += blockDim.x) sr[i] = a.rows[(size_t)j * k * WP + i];
+    __syncthreads();
+    int best = INT_MAX;
+    for (int i = 0; i < samples; ++i) {
+      unsigned long long r = mix64(tid * 0x100000001B3ull + (unsigned long long)i * 7919 + j) % total;
+      uint32_t acc[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) acc[w] = 0u;
+      int hi = k - 1;
+      for (int q = g; q >= 1; --q) {
+        // colex unrank: the largest c <= hi with C(c, q) <= r (C(q-1, q) = 0)
+        int lo = q - 1;
+        while (lo < hi) {
+          const int mid = (lo + hi + 1) >> 1;
+          if (sb[mid * (g + 1) + q] <= r) lo = mid; else hi = mid - 1;
+        }
+        r -= sb[lo * (g + 1) + q];
+        xor_row<W>(acc, sr + lo * WP);
+        hi = lo - 1;
+      }
+      int wt = 0;
+#pragma unroll
+      for (int w = 0; w < W; ++w) wt += __popc(acc[w]);
+      best = min(best, wt);
+    }
+    best = __reduce_min_sync(0xffffffffu, best);
+    if ((threadIdx.x & 31) == 0) {
+      const int wg = best + gamma_woff(a, j);
+      atomicMin(a.bound + 1 + j, wg);
+      if (gamma_only < 0) atomicMin(a.bound, wg);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // K1h: weight histogram of one (Gamma, g) pass.  Each thread owns a private
 // u16 histogram column in shared memory (layout [bin][thread]: conflict-free
 // for any bin pattern), flushed into a block-wide u32 histogram before it

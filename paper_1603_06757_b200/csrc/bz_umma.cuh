@@ -68,6 +68,9 @@ constexpr int kUmmaM = 128;       // prefixes per A tile = producer threads
 #ifndef BZ_K5_SPLIT
 #define BZ_K5_SPLIT 1
 #endif
+#ifndef BZ_K5Q_SPLIT
+#define BZ_K5Q_SPLIT 1  // K5q: accumulator column halves with their own barriers
+#endif
 #ifndef BZ_K5_EPI_GROUPS
 #define BZ_K5_EPI_GROUPS 1
 #endif
@@ -136,7 +139,7 @@ struct K4Roles {
   // column parts of each accumulator with their own full/empty barriers:
   // the epilogue drains part 0 while the MMAs of part 1 still run, and the
   // next tile's part-0 MMAs start as soon as part 0 is drained
-  static constexpr int SPLIT = F4 ? BZ_K5_SPLIT : 1;
+  static constexpr int SPLIT = CW == 4 ? BZ_K5Q_SPLIT : (CW > 1 ? 1 : (F4 ? BZ_K5_SPLIT : 1));
   // epilogue groups: group q drains the tiles t with t % EGRP == q (each
   // group covers the whole accumulator), so a group has EGRP tile periods
   // for its loads and reductions while the other groups take the tiles in
@@ -869,7 +872,7 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
   static_assert(CW >= 1 && CW <= 5, "kernel form");
   // offset accumulators (packed s16 epilogue) for this instantiation
   constexpr bool MG = kK5Magic && (CW > 1 || (W & 1) || !BZ_K5_EVEN_F32);
-  static_assert(!PR || (F4 && kK5Magic && BZ_K5_SPLIT == 1 &&
+  static_assert(!PR || (F4 && kK5Magic && (Q || BZ_K5_SPLIT == 1) &&
                         (WQ ? W >= 2 : (((W & 1) || CW == 4) && W <= (CW == 4 ? 4 : 3) &&
                                         (CW == 4 || BZ_K5_EPI_GROUPS == 1)))),
                 "K5p/K5t: odd W <= 3, K5q: W <= 4 (stored weights <= 127 fit the fields)");
@@ -1596,7 +1599,7 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
                   // of the stage) with B scale 2^(8q) (K5t) / 2^(16q) (K5p);
                   // its last MMA reads A chunks W-1 and W+q (LBO (q+1)*128 B)
                   // so it meets offset chunk q
-                  const uint32_t dj = dbase;
+                  const uint32_t dj = dbase + (uint32_t)(h * NH);
                   const uint64_t adj = a_desc0 + (uint64_t)(ab * (TA >> 4));
                   if constexpr (WQ) {
                     // K5w: per part the data MMAs (part b with B scale 2^11),
