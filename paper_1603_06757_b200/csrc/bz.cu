@@ -89,6 +89,10 @@ struct bz_ctx {
   unsigned char* d_io = nullptr;
   unsigned char* h_io = nullptr;  // pinned mirror
   size_t io_cap = 0;
+  unsigned char* h_stage = nullptr;  // pinned staging of the row images (bz_load_gammas)
+  size_t stage_cap = 0;
+  cudaEvent_t ev_load = nullptr;     // the last staging upload
+  bool ev_load_pending = false;
   // the plan keys and offsets of the last batch whose group tables are in
   // h_io and d_io: an identical round (same key, same offset) is neither
   // copied nor uploaded again
@@ -758,8 +762,9 @@ template <int W>
 int build_level_w(bz_ctx* ctx, int D, int floor) {
   const unsigned long long n = binom_sat(ctx->k - floor, D);
   // every row of the Gamma's stride: the subsets, then the empty-subset tail
-  dim3 grid((unsigned)((ctx->lvl_rows[D - 3] + 255) / 256), ctx->m);
-  bz::k_build_subsets_mxf4<W><<<grid, 256, 0, ctx->stream>>>(
+  // kBuildRows rows per thread (k_build_subsets_mxf4)
+  dim3 grid((unsigned)((ctx->lvl_rows[D - 3] / bz::kBuildRows + 127) / 128), ctx->m);
+  bz::k_build_subsets_mxf4<W><<<grid, 128, 0, ctx->stream>>>(
       ctx->d_rows, ctx->d_lvl[D - 3], ctx->k, D, n, ctx->lvl_rows[D - 3], ctx->d_binom);
   CK(cudaGetLastError());
   ctx->launches += 1;
@@ -1263,6 +1268,7 @@ int bz_create(int device, bz_ctx** out) {
   CK(cudaEventCreate(&ctx->ev_b));
   CK(cudaEventCreate(&ctx->ev_k0));
   CK(cudaEventCreate(&ctx->ev_k1));
+  CK(cudaEventCreateWithFlags(&ctx->ev_load, cudaEventDisableTiming));
   // binomial table, saturating at UINT64_MAX
   std::vector<unsigned long long> tab(bz::kBinomDim * bz::kBinomDim);
   for (int p = 0; p < bz::kBinomDim; ++p)
@@ -1290,6 +1296,8 @@ void bz_destroy(bz_ctx* ctx) {
     cudaFree(ctx->d_io);
     cudaFree(ctx->d_hist);
     if (ctx->h_io) cudaFreeHost(ctx->h_io);
+    if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+    if (ctx->ev_load) cudaEventDestroy(ctx->ev_load);
     if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
     if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
     if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
@@ -1400,11 +1408,29 @@ int bz_load_gammas(bz_ctx* ctx, const uint64_t* rows, int m, int k, int n) {
   }
   CK(grow(ctx, (void**)&ctx->d_rows, &ctx->rows_cap, img.size() * 4));
   CK(grow(ctx, (void**)&ctx->d_px, &ctx->px_cap, px.size() * 4));
-  CK(cudaMemcpyAsync(ctx->d_rows, img.data(), img.size() * 4, cudaMemcpyHostToDevice,
+  // one asynchronous H2D from a pinned staging buffer (no stream
+  // synchronisation: the rounds that read the rows follow on the stream;
+  // the staging buffer is reused only once the previous upload has landed)
+  const size_t stage_bytes = (img.size() + px.size()) * 4;
+  if (ctx->ev_load_pending) {
+    CK(cudaEventSynchronize(ctx->ev_load));
+    ctx->ev_load_pending = false;
+  }
+  if (stage_bytes > ctx->stage_cap) {
+    if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
+    ctx->h_stage = nullptr;
+    ctx->stage_cap = 0;
+    CK(cudaMallocHost(&ctx->h_stage, stage_bytes));
+    ctx->stage_cap = stage_bytes;
+  }
+  std::memcpy(ctx->h_stage, img.data(), img.size() * 4);
+  std::memcpy(ctx->h_stage + img.size() * 4, px.data(), px.size() * 4);
+  CK(cudaMemcpyAsync(ctx->d_rows, ctx->h_stage, img.size() * 4, cudaMemcpyHostToDevice,
                      ctx->stream));
-  CK(cudaMemcpyAsync(ctx->d_px, px.data(), px.size() * 4, cudaMemcpyHostToDevice,
-                     ctx->stream));
-  CK(cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
+  CK(cudaMemcpyAsync(ctx->d_px, ctx->h_stage + img.size() * 4, px.size() * 4,
+                     cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaEventRecord(ctx->ev_load, ctx->stream));
+  ctx->ev_load_pending = true;
   // triple tables (K3, K4) are sized here and built lazily by the first
   // round that needs them
   ctx->trip_built = ctx->trip4_built = false;
@@ -1589,10 +1615,24 @@ int bz_reduce_on_columns(uint64_t* rows, int k, int n, const int32_t* cols, int 
     if (hit < 0) continue;
     if (hit != top)
       for (int x = 0; x < w; ++x) std::swap(rows[(size_t)hit * w + x], rows[(size_t)top * w + x]);
+    // eliminate the pivot column from every other row, branch-free (the
+    // data-dependent branch mispredicted on half the rows: this loop was
+    // most of the Gamma family's host time)
     const uint64_t* pr = rows + (size_t)top * w;
-    for (int r = 0; r < k; ++r)
-      if (r != top && (rows[(size_t)r * w + cw] & cb))
-        for (int x = 0; x < w; ++x) rows[(size_t)r * w + x] ^= pr[x];
+    const int sh = col & 63;
+    if (w <= 8) {
+      uint64_t p8[8];
+      for (int x = 0; x < w; ++x) p8[x] = pr[x];
+      for (int r = 0; r < k; ++r) {
+        uint64_t* rr = rows + (size_t)r * w;
+        const uint64_t mask = (r == top) ? 0ull : (0ull - ((rr[cw] >> sh) & 1ull));
+        for (int x = 0; x < w; ++x) rr[x] ^= p8[x] & mask;
+      }
+    } else {
+      for (int r = 0; r < k; ++r)
+        if (r != top && (rows[(size_t)r * w + cw] & cb))
+          for (int x = 0; x < w; ++x) rows[(size_t)r * w + x] ^= pr[x];
+    }
     if (out_pivots) out_pivots[top] = col;
     ++top;
   }

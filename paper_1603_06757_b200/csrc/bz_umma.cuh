@@ -640,6 +640,11 @@ struct K4Tables {
 // first C(k - f, D) rows), then the other D - 1 elements lex.  One thread per
 // table row (grid.y = Gamma); rows stored as e2m1 0 / 1.0 nibbles in the
 // UMMA K-major no-swizzle layout (+ the offset chunk for odd W).
+#ifndef BZ_BUILD_ROWS
+#define BZ_BUILD_ROWS 2
+#endif
+constexpr int kBuildRows = BZ_BUILD_ROWS;  // suffix-table rows per builder thread (divides 8)
+
 template <int W>
 __global__ void k_build_subsets_mxf4(const uint32_t* __restrict__ rows,
                                      uint8_t* __restrict__ out, int k, int D,
@@ -647,62 +652,80 @@ __global__ void k_build_subsets_mxf4(const uint32_t* __restrict__ rows,
                                      const unsigned long long* __restrict__ binom) {
   constexpr int WP = padded_words(W);
   constexpr int C = k4_row_bytes<true>(W) / 16;  // chunks per row (+ offset chunk)
-  // binomials C(x, 0..5) for x <= k in shared memory (every search below
-  // is a binary search over them)
+  // binomials C(x, 0..5) for x <= k in shared memory (the one unrank per
+  // thread is a binary search over them)
   __shared__ unsigned long long sbt[kBinomDim * 6];
   for (int i = threadIdx.x; i < (k + 1) * 6; i += blockDim.x)
     sbt[i] = binom[(i / 6) * kBinomDim + (i % 6)];
   __syncthreads();
   auto B = [&](int x, int q) { return sbt[x * 6 + q]; };
-  const unsigned long long row = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (row >= gamma_stride_rows) return;
+  // kBuildRows consecutive rows per thread: it unranks the first once and
+  // steps to the others with the table order's successor (the unrank's
+  // binary searches were the builder's cost)
+  const unsigned long long row0 =
+      ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) * (unsigned long long)kBuildRows;
+  if (row0 >= gamma_stride_rows) return;
   const int j = blockIdx.y;
-  uint8_t* grp = out + (size_t)j * gamma_stride_rows * (16 * C) + (size_t)(row >> 3) * (8 * 16 * C) +
-                 (row & 7) * 16;
-  if (row >= nrows) {
-    // tail rows (read by whole-tile copies, their columns masked): the
-    // empty subset, so every column a K5p tile pairs stays in range
-#pragma unroll
-    for (int w = 0; w < W; ++w) *reinterpret_cast<uint4*>(grp + w * 128) = make_uint4(0u, 0u, 0u, 0u);
-    if constexpr (C > W) *reinterpret_cast<uint4*>(grp + W * 128) = k5_table_offset_chunk();
-    return;
-  }
+  uint8_t* grp = out + (size_t)j * gamma_stride_rows * (16 * C);
   const uint32_t* R = rows + (size_t)j * k * WP;
-  // smallest element a: rows of a start at C(k-1-a, D); x = k-1-a is the
-  // largest x <= k-1 with C(x, D) <= row (C(D-1, D) = 0: row 0 is the subset
-  // {k-D, ..., k-1})
-  int lo = D - 1, hi = k - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (B(mid, D) <= row) lo = mid; else hi = mid - 1;
-  }
-  const int x = lo;
-  const int a = k - 1 - x;
-  unsigned long long r = row - B(x, D);
-  uint32_t v[W];
-#pragma unroll
-  for (int w = 0; w < W; ++w) v[w] = R[a * WP + w];
-  // lex unrank of r among the (D-1)-subsets of [a+1, k): element i's value
-  // e1 is the smallest e1 >= e with C(k-1-e1, i) < C(k-e, i) - r (the
-  // skipped blocks C(k-1-e', i-1), e <= e' < e1, sum to C(k-e, i) - C(k-e1, i))
-  int e = a + 1;
-  for (int i = D - 1; i >= 1; --i) {
-    const unsigned long long T = B(k - e, i) - r;
-    int l2 = e, h2 = k - i;  // C(k-1-(k-i), i) = C(i-1, i) = 0 < T
-    while (l2 < h2) {
-      const int mid = (l2 + h2) >> 1;
-      if (B(k - 1 - mid, i) < T) h2 = mid; else l2 = mid + 1;
+  int e[5];  // the subset, e[0] = smallest element a, e[1..D-1] ascending
+  if (row0 < nrows) {
+    // smallest element a: rows of a start at C(k-1-a, D); x = k-1-a is the
+    // largest x <= k-1 with C(x, D) <= row (C(D-1, D) = 0)
+    int lo = D - 1, hi = k - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (B(mid, D) <= row0) lo = mid; else hi = mid - 1;
     }
-    r = r - B(k - e, i) + B(k - l2, i);
-    e = l2;
-#pragma unroll
-    for (int w = 0; w < W; ++w) v[w] ^= R[e * WP + w];
-    ++e;
+    e[0] = k - 1 - lo;
+    unsigned long long r = row0 - B(lo, D);
+    // lex unrank of r among the (D-1)-subsets of [a+1, k)
+    int at = e[0] + 1;
+    for (int i = D - 1; i >= 1; --i) {
+      const unsigned long long T = B(k - at, i) - r;
+      int l2 = at, h2 = k - i;
+      while (l2 < h2) {
+        const int mid = (l2 + h2) >> 1;
+        if (B(k - 1 - mid, i) < T) h2 = mid; else l2 = mid + 1;
+      }
+      r = r - B(k - at, i) + B(k - l2, i);
+      e[D - i] = l2;
+      at = l2 + 1;
+    }
   }
+  for (int q = 0; q < kBuildRows; ++q) {
+    const unsigned long long row = row0 + (unsigned long long)q;
+    uint8_t* dst = grp + (size_t)(row >> 3) * (8 * 16 * C) + (row & 7) * 16;
+    if (row >= nrows) {
+      // tail rows (read by whole-tile copies, their columns masked): the
+      // empty subset, so every column a K5p/K5q tile pairs stays in range
 #pragma unroll
-  for (int w = 0; w < W; ++w) *reinterpret_cast<uint4*>(grp + w * 128) = e2m1_bits01(v[w]);
-  if constexpr (C > W)  // offset chunk
-    *reinterpret_cast<uint4*>(grp + W * 128) = k5_table_offset_chunk();
+      for (int w = 0; w < W; ++w) *reinterpret_cast<uint4*>(dst + w * 128) = make_uint4(0u, 0u, 0u, 0u);
+      if constexpr (C > W) *reinterpret_cast<uint4*>(dst + W * 128) = k5_table_offset_chunk();
+      continue;
+    }
+    uint32_t v[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) v[w] = R[e[0] * WP + w];
+    for (int i = 1; i < D; ++i)
+#pragma unroll
+      for (int w = 0; w < W; ++w) v[w] ^= R[e[i] * WP + w];
+#pragma unroll
+    for (int w = 0; w < W; ++w) *reinterpret_cast<uint4*>(dst + w * 128) = e2m1_bits01(v[w]);
+    if constexpr (C > W)  // offset chunk
+      *reinterpret_cast<uint4*>(dst + W * 128) = k5_table_offset_chunk();
+    // successor in table order: the next (D-1)-subset of [a+1, k) in lex
+    // order, or (after the last one) a - 1 with its first subset
+    int i = D - 1;
+    while (i >= 1 && e[i] == k - D + i) --i;
+    if (i >= 1) {
+      ++e[i];
+      for (int t = i + 1; t < D; ++t) e[t] = e[t - 1] + 1;
+    } else {
+      --e[0];
+      for (int t = 1; t < D; ++t) e[t] = e[0] + t;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
