@@ -93,6 +93,11 @@ struct bz_ctx {
   size_t stage_cap = 0;
   cudaEvent_t ev_load = nullptr;     // the last staging upload
   bool ev_load_pending = false;
+  // suffix tables are built on a side stream, overlapping the small rounds'
+  // K1 launch; the first tensor-core launch waits for them
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_main = nullptr, ev_side = nullptr;
+  bool side_pending = false;
   // the plan keys and offsets of the last batch whose group tables are in
   // h_io and d_io: an identical round (same key, same offset) is neither
   // copied nor uploaded again
@@ -764,7 +769,13 @@ int build_level_w(bz_ctx* ctx, int D, int floor) {
   // every row of the Gamma's stride: the subsets, then the empty-subset tail
   // kBuildRows rows per thread (k_build_subsets_mxf4)
   dim3 grid((unsigned)((ctx->lvl_rows[D - 3] / bz::kBuildRows + 127) / 128), ctx->m);
-  bz::k_build_subsets_mxf4<W><<<grid, 128, 0, ctx->stream>>>(
+  if (!ctx->side_pending) {
+    // the side stream starts after everything enqueued so far (the rows)
+    CK(cudaEventRecord(ctx->ev_main, ctx->stream));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->ev_main, 0));
+    ctx->side_pending = true;
+  }
+  bz::k_build_subsets_mxf4<W><<<grid, 128, 0, ctx->side>>>(
       ctx->d_rows, ctx->d_lvl[D - 3], ctx->k, D, n, ctx->lvl_rows[D - 3], ctx->d_binom);
   CK(cudaGetLastError());
   ctx->launches += 1;
@@ -1116,6 +1127,12 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
       if (rc) return rc;
       prev_round = false;
     }
+    if (ctx->side_pending && (kern >= 3 || todo[i].seed)) {
+      // the suffix tables this launch reads were built on the side stream
+      CK(cudaEventRecord(ctx->ev_side, ctx->side));
+      CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_side, 0));
+      ctx->side_pending = false;
+    }
     ctx->pdl_next = prev_round && !debug;
     std::vector<RoundArgs> as;
     for (int q = 0; q < f; ++q) as.push_back(todo[i + q].a);
@@ -1131,6 +1148,11 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
       prev_round = false;
     }
     i += f - 1;
+  }
+  if (ctx->side_pending) {  // tables built but not read by this batch: still join
+    CK(cudaEventRecord(ctx->ev_side, ctx->side));
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_side, 0));
+    ctx->side_pending = false;
   }
   CK(cudaEventRecord(ctx->ev_k1, ctx->stream));
   const auto t_launch1 = std::chrono::steady_clock::now();
@@ -1269,6 +1291,9 @@ int bz_create(int device, bz_ctx** out) {
   CK(cudaEventCreate(&ctx->ev_k0));
   CK(cudaEventCreate(&ctx->ev_k1));
   CK(cudaEventCreateWithFlags(&ctx->ev_load, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ctx->ev_main, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&ctx->ev_side, cudaEventDisableTiming));
   // binomial table, saturating at UINT64_MAX
   std::vector<unsigned long long> tab(bz::kBinomDim * bz::kBinomDim);
   for (int p = 0; p < bz::kBinomDim; ++p)
@@ -1298,6 +1323,12 @@ void bz_destroy(bz_ctx* ctx) {
     if (ctx->h_io) cudaFreeHost(ctx->h_io);
     if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
     if (ctx->ev_load) cudaEventDestroy(ctx->ev_load);
+    if (ctx->side) {
+      cudaStreamSynchronize(ctx->side);
+      cudaStreamDestroy(ctx->side);
+    }
+    if (ctx->ev_main) cudaEventDestroy(ctx->ev_main);
+    if (ctx->ev_side) cudaEventDestroy(ctx->ev_side);
     if (ctx->h_hist) cudaFreeHost(ctx->h_hist);
     if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
     if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
