@@ -58,6 +58,7 @@ def _bind(path: str):
     L.bz_enumerate.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                _i32p, _u64p]
     L.bz_launch_count.argtypes = [_vp, _u64p]
+    L.bz_counters.argtypes = [_vp, ctypes.c_int, _u64p, _u64p]
     return L
 
 
@@ -116,15 +117,19 @@ class GpuPasses:
                                        combos.ctypes.data_as(_u64p))
             if rc:
                 self._fail(rc, ctx, "bz_enumerate")
+            adds = np.zeros(1, np.uint64)
+            accs = np.zeros(1, np.uint64)
+            rc = self.lib.bz_counters(ctx, 1, adds.ctypes.data_as(_u64p), accs.ctypes.data_as(_u64p))
+            if rc:
+                self._fail(rc, ctx, "bz_counters")
         best = int(mn[0])
         if ubound is not None:
             best = min(best, ubound)
         c = int(combos[0])
         assert c == comb(k, g), (c, k, g)
-        # row-level counters of the device walk: one row addition (the
-        # stored suffix combined with the prefix sum) and one row access per
-        # codeword -- strategy-specific, as the reference's are
-        return self.enumeration_result(best, c, c, c)
+        # the device's row additions / row accesses for this pass
+        # (bz_counters) -- strategy-specific, as the reference's are
+        return self.enumeration_result(best, c, int(adds[0]), int(accs[0]))
 
     def close(self):
         for ctx, _ in self.ctxs.values():

@@ -100,6 +100,10 @@ def test_repetition_and_hamming():
     parsed = ref_engine.parse_report(text)
     assert parsed["distance"] == 3 and parsed["bounds_trace"] == rep.bounds_trace
     assert parsed["combinations"] == rep.counters.combinations
+    # the device's row counters ride along (one addition per codeword at
+    # least; rows are loaded once for many codewords)
+    assert rep.counters.row_additions >= rep.counters.combinations > 0
+    assert rep.counters.row_accesses > 0
 
 
 @gpu
