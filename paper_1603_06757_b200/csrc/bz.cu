@@ -487,18 +487,24 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
 // and the planning knobs, never on the matrices, so plans are memoised per
 // process: a repeated run (same dimensions) copies its group tables instead
 // of re-planning every round before the first launch.
+// the planning knobs (test and tuning hooks), read once per batch
+struct PlanKnobs {
+  const char *floors, *scale, *cost, *lmin;
+  PlanKnobs()
+      : floors(getenv("BZ_K5_FLOORS")), scale(getenv("BZ_K5_CHUNK_SCALE")),
+        cost(getenv("BZ_K5_COST")), lmin(getenv("BZ_K5_LANE_MIN")) {}
+};
+
 int plan_round(bz_ctx* ctx, int g, int gamma_only, PlanShape shape, int nshards, size_t goff,
-               int* out_ngroups, unsigned long long* out_nchunks, int slot, bool* out_fresh) {
+               int* out_ngroups, unsigned long long* out_nchunks, int slot, bool* out_fresh,
+               const PlanKnobs& kn) {
   struct Plan {
     std::vector<Group> groups;
     unsigned long long nchunks;
   };
   static std::mutex mu;
   static std::map<std::string, Plan> memo;
-  const char* floors = getenv("BZ_K5_FLOORS");
-  const char* scale = getenv("BZ_K5_CHUNK_SCALE");
-  const char* cost = getenv("BZ_K5_COST");
-  const char* lmin = getenv("BZ_K5_LANE_MIN");
+  const char *floors = kn.floors, *scale = kn.scale, *cost = kn.cost, *lmin = kn.lmin;
   char key[384];
   snprintf(key, sizeof key, "%d/%d/%d/%d/%d/%d/%d/%d/%d/%s/%s/%s/%s", ctx->m, ctx->k, g, gamma_only,
            shape.kernel, shape.depth, shape.lanes, shape.tile_rows, nshards, floors ? floors : "",
@@ -977,6 +983,12 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   // plans follow the result records; goff = where round i's groups go
   size_t goff = ((size_t)count * l.off_groups + 255) & ~size_t(255);
   size_t first_fresh = SIZE_MAX;  // first group table this batch has to upload
+  const PlanKnobs knobs;
+  int trace_from = 0, trace_ell = -1;
+  if (debug) {
+    if (const char* e = getenv("BZ_K4_TRACE_FROM")) trace_from = atoi(e);
+    if (const char* e = getenv("BZ_K4_TRACE_ELL")) trace_ell = atoi(e);
+  }
   for (int i = 0; i < count; ++i) {
     const int g = g0 + i;
     const PlanShape shape = pass_shape(ctx->engine, g, hist, ctx->w32, ctx->m, ctx->k, ctx->n_eff);
@@ -989,7 +1001,8 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     const size_t gthis = goff;
     const int r_shard = owner[i] >= 0 ? 0 : shard, r_nshards = owner[i] >= 0 ? 1 : nshards;
     bool fresh = true;
-    rc = plan_round(ctx, g, gamma_only, shape, r_nshards, gthis, &ngroups, &nchunks, i, &fresh);
+    rc = plan_round(ctx, g, gamma_only, shape, r_nshards, gthis, &ngroups, &nchunks, i, &fresh,
+                    knobs);
     if (rc) return rc;
     if (fresh && first_fresh == SIZE_MAX) first_fresh = gthis;
     if (shape.kernel >= 5) {
@@ -1034,9 +1047,9 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     a.elide = ctx->elide_mask;
     a.debug = debug;
     a.trace = (i == count - 1) ? trace : nullptr;
-    a.trace_from = getenv("BZ_K4_TRACE_FROM") ? atoi(getenv("BZ_K4_TRACE_FROM")) : 0;
+    a.trace_from = trace_from;
     a.ctrace = (i == count - 1) ? ctrace : nullptr;
-    a.trace_ell = getenv("BZ_K4_TRACE_ELL") ? atoi(getenv("BZ_K4_TRACE_ELL")) : -1;
+    a.trace_ell = trace_ell;
     a.chain = i > 0 ? todo[i - 1].a.bound : nullptr;
     a.gbound = gamma_only < 0 ? ctx->d_gbound : nullptr;  // whole rounds only
     a.gtag = ctx->gtag;

@@ -287,6 +287,15 @@ def run_rounds(backend, gs: GammaSet, k: int, config: EngineConfig, st: LoopStat
 
     queued: list = []  # precomputed (g, mins, combos, kernel_ms) of a batch
     qi = 0
+    # A batch need not run past the round where the loop must stop: round g
+    # runs only while L(g - 1) < U, and every row of every Gamma is a
+    # codeword, so U never exceeds the lightest row once round 1 is in.
+    # (Only the batch length depends on this; results do not.)
+    u_rows = U
+    for gm in gs.gammas:
+        w = int(np.bitwise_count(gm.words64()).sum(axis=1).min())
+        if w < u_rows:
+            u_rows = w
     try:
         while g <= k and L < U:
             if g > max_g:
@@ -302,7 +311,8 @@ def run_rounds(backend, gs: GammaSet, k: int, config: EngineConfig, st: LoopStat
                           if ahead else config.batch_combinations * world)
                 count, total = 0, 0
                 top = min(k, max_g)
-                while g + count <= top:
+                u_cap = min(U, u_rows)
+                while g + count <= top and (count == 0 or lower(g + count - 1) < u_cap):
                     c = m * comb(k, g + count)
                     if total + c > budget:
                         break
