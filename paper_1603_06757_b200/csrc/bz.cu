@@ -451,6 +451,10 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
         const long long step_cost =
             tiled ? std::max(work, (long long)shape.tile_rows) + 256 : work;
         long long ppl = std::max(1ll, lt / std::max(1ll, step_cost));
+        // K1 lanes walk their range with two walkers (halves): a lane with a
+        // single prefix runs its second walker on a duplicate, so give every
+        // lane two prefixes where the group has them (config 4: 2x the work)
+        if (!tiled) ppl = std::max(ppl, 2ll);
         ppl = std::min(ppl, std::max(1ll, spread));
         // D >= 3: a chunk is lanes prefixes x ppl steps x tpc tiles; a slice
         // too large for one chunk is split into tile blocks
