@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define BZ_ABI_VERSION 13
+#define BZ_ABI_VERSION 14
 
 /* limits of the device kernels */
 #define BZ_MAX_K 128 /* rows per Gamma (prefix masks are 128-bit)      */
@@ -201,6 +201,37 @@ int bz_round(bz_ctx *ctx, int g, int lower_prev, int upper, int shard,
  * out_min / out_combos hold count x m values, round-major. */
 int bz_rounds(bz_ctx *ctx, int g0, int count, const int32_t *lower_prev, int upper,
               int shard, int nshards, int32_t *out_min, uint64_t *out_combos);
+
+/* The Algorithm-1 loop itself (m/engine.py:204-217, one rank), one device
+ * call per bz_advance: from st = (g, L, U) it takes the next rounds whose
+ * m*C(k, g') total fits batch_budget (at least one; batch_budget <= 0: one
+ * round per call), not past min(k, max_g) and not past the first round g'
+ * with L(g'-1) >= min(U, u_rows) (u_rows: the weight of the lightest row of
+ * any Gamma, an upper bound on U once round 1 is in), runs them as
+ * bz_rounds does, and folds them in order: U = min(U, every Gamma's
+ * minimum), L = (m_arg-1)(g'+1) + max(0, g'+1-k+km_arg)
+ * (lower_bound_update, engine.py:97-103), one record (g', L, U, counters
+ * summed over the Gammas, device ms) per round -- rounds past termination
+ * are discarded.  st->status: BZ_LOOP_RUNNING while the loop goes on,
+ * BZ_LOOP_DONE once L >= U or g > k (exact), BZ_LOOP_MAX_G when it would
+ * continue past max_g (upper bound only).  Writes at most `cap` records. */
+#define BZ_LOOP_RUNNING 0
+#define BZ_LOOP_DONE 1
+#define BZ_LOOP_MAX_G 2
+typedef struct {
+  int32_t g, L, U;   /* in/out: the next round and the bounds before it */
+  int32_t g_reached; /* out: last round folded in                       */
+  int32_t status;    /* in/out: BZ_LOOP_*                                */
+} bz_loop_state;
+typedef struct {
+  int32_t g, L, U;   /* the trace entry (g, L, U) after round g          */
+  int32_t pad;
+  uint64_t combinations, row_additions, row_accesses;
+  float kernel_ms;
+  int32_t pad2;
+} bz_round_record;
+int bz_advance(bz_ctx *ctx, int m_arg, int km_arg, int max_g, int u_rows, int64_t batch_budget,
+               bz_loop_state *st, bz_round_record *out, int cap, int *n_out);
 
 /* One (Gamma_gamma, g) pass without early exit; out_min is the unclipped
  * minimum weight (INT32_MAX when the shard is empty). */

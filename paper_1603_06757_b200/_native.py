@@ -19,9 +19,15 @@ from .errors import (DeviceError, InvalidArity, InvalidDimensions, MindistError,
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BZ_LIB") or os.path.join(PKG_DIR, "libbz.so")
-ABI_VERSION = 13
+ABI_VERSION = 14
 
 BZ_OK = 0
+BZ_LOOP_RUNNING, BZ_LOOP_DONE, BZ_LOOP_MAX_G = 0, 1, 2
+# bz_round_record (include/bz.h)
+ROUND_RECORD = np.dtype([("g", np.int32), ("L", np.int32), ("U", np.int32), ("pad", np.int32),
+                         ("combinations", np.uint64), ("row_additions", np.uint64),
+                         ("row_accesses", np.uint64), ("kernel_ms", np.float32),
+                         ("pad2", np.int32)])
 _CODES = {
     1: InvalidArity,
     2: InvalidDimensions,
@@ -36,7 +42,7 @@ _CODES = {
 SYMBOLS = ("bz_abi_version", "bz_device_count", "bz_create", "bz_destroy",
            "bz_last_error", "bz_set_engine", "bz_set_elision", "bz_set_early_exit", "bz_elided",
            "bz_reduce_on_columns", "bz_brute_force", "bz_load_gammas",
-           "bz_round", "bz_rounds", "bz_counters",
+           "bz_round", "bz_rounds", "bz_advance", "bz_counters",
            "bz_enumerate",
            "bz_histogram", "bz_plan", "bz_timer_start", "bz_timer_stop",
            "bz_last_kernel_ms", "bz_round_ms", "bz_gamma_family",
@@ -80,6 +86,8 @@ def lib():
     L.bz_load_gammas.argtypes = [vp, u64p, c_int, c_int, c_int]
     L.bz_round.argtypes = [vp, c_int, c_int, c_int, c_int, c_int, i32p, u64p]
     L.bz_rounds.argtypes = [vp, c_int, c_int, i32p, c_int, c_int, c_int, i32p, u64p]
+    L.bz_advance.argtypes = [vp, c_int, c_int, c_int, c_int, ctypes.c_int64, i32p, vp, c_int,
+                             ctypes.POINTER(c_int)]
     L.bz_enumerate.argtypes = [vp, c_int, c_int, c_int, c_int, i32p, u64p]
     L.bz_counters.argtypes = [vp, c_int, u64p, u64p]
     L.bz_histogram.argtypes = [vp, c_int, c_int, c_int, c_int, u64p, i32p, u64p]
@@ -313,6 +321,26 @@ class Context:
         mn = mins[:count * m].reshape(count, m).tolist()
         cb = combos[:count * m].reshape(count, m).tolist()
         return list(zip(mn, cb))
+
+    def advance(self, m_arg: int, km_arg: int, max_g: int, u_rows: int, budget: int,
+                state):
+        """One step of the Algorithm-1 loop (bz_advance).  ``state`` is an
+        int32 array [g, L, U, g_reached, status], updated in place; returns
+        the records of the rounds folded in as ROUND_RECORD tuples (g, L, U,
+        pad, combinations, row_additions, row_accesses, kernel_ms, pad)."""
+        k = max(self.k, 1)
+        recs = self.__dict__.get("_recs")
+        if recs is None or len(recs) < k:
+            recs = np.zeros(k, dtype=ROUND_RECORD)
+            self._recs = recs
+            self._recs_p = ctypes.c_void_p(recs.ctypes.data)
+            self._nrec = c_int()
+            self._nrec_p = ctypes.byref(self._nrec)
+        check(lib().bz_advance(self.handle, m_arg, km_arg, min(max_g, 1 << 30), u_rows, budget,
+                               state.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                               self._recs_p, len(recs), self._nrec_p),
+              self.handle, f"bz_advance(g={int(state[0])})")
+        return recs[:self._nrec.value].tolist()
 
     def counters(self, count: int = 1):
         """Row additions and row accesses (count x m, round-major) of the

@@ -989,6 +989,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   size_t first_fresh = SIZE_MAX;  // first group table this batch has to upload
   const PlanKnobs knobs;
   int trace_from = 0, trace_ell = -1;
+  int lvl_lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX};  // lowest floor per level (D = 3..5)
   if (debug) {
     if (const char* e = getenv("BZ_K4_TRACE_FROM")) trace_from = atoi(e);
     if (const char* e = getenv("BZ_K4_TRACE_ELL")) trace_ell = atoi(e);
@@ -1011,15 +1012,9 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     if (fresh && first_fresh == SIZE_MAX) first_fresh = gthis;
     if (shape.kernel >= 5) {
       // the suffix tables this round's levels read
-      int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX};
       const Group* gp = reinterpret_cast<const Group*>(ctx->h_io + gthis);
       for (int q = 0; q < ngroups; ++q)
-        lo[gp[q].depth - 3] = std::min(lo[gp[q].depth - 3], gp[q].sfloor);
-      for (int D = 3; D <= 5; ++D)
-        if (lo[D - 3] != INT32_MAX) {
-          rc = ensure_level(ctx, D, D == 3 ? 0 : lo[D - 3]);
-          if (rc) return rc;
-        }
+        lvl_lo[gp[q].depth - 3] = std::min(lvl_lo[gp[q].depth - 3], gp[q].sfloor);
     }
     *slot_ptr<unsigned long long>(ctx->h_io, l, i, 0) = 0ull;
     unsigned long long* hc = slot_ptr<unsigned long long>(ctx->h_io, l, i, l.off_combos);
@@ -1079,6 +1074,15 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   }
   // entries past this batch describe memory it may have overwritten
   ctx->io_plans.resize(count);
+  // every suffix table once, at the lowest floor any round of the batch
+  // reads (a table for a lower floor holds a higher floor's rows as its
+  // first rows): rounds g = 5, 6, 7 ... lower the D = 4, 5 floors in turn,
+  // and building per round rebuilt each table up to three times
+  for (int D = 3; D <= 5; ++D)
+    if (lvl_lo[D - 3] != INT32_MAX) {
+      rc = ensure_level(ctx, D, D == 3 ? 0 : lvl_lo[D - 3]);
+      if (rc) return rc;
+    }
   const auto t_plan1 = std::chrono::steady_clock::now();
   if (hist)
     CK(cudaMemsetAsync(ctx->d_hist, 0, sizeof(unsigned long long) * (ctx->n + 1), ctx->stream));
@@ -1538,6 +1542,78 @@ int bz_rounds(bz_ctx* ctx, int g0, int count, const int32_t* lower_prev, int upp
       U = std::min(U, v);
     }
   }
+  return BZ_OK;
+}
+
+// The Algorithm-1 loop (m/engine.py:204-217) one device call at a time: the
+// batch rule and the fold of engine.py run_rounds, natively (see bz.h).
+int bz_advance(bz_ctx* ctx, int m_arg, int km_arg, int max_g, int u_rows, int64_t batch_budget,
+               bz_loop_state* st, bz_round_record* out, int cap, int* n_out) {
+  if (!ctx) return BZ_ERR_ARGUMENT;
+  if (!st || !n_out || (!out && cap > 0)) return fail(ctx, BZ_ERR_ARGUMENT, "null argument");
+  *n_out = 0;
+  if (ctx->device < 0) return fail(ctx, BZ_ERR_NO_DEVICE, "context has no device");
+  if (!ctx->d_rows) return fail(ctx, BZ_ERR_STATE, "no Gamma family loaded");
+  const int k = ctx->k, m = ctx->m;
+  // lower_bound_update (engine.py:97-103)
+  auto lower = [&](int gg) { return (m_arg - 1) * (gg + 1) + std::max(0, gg + 1 - k + km_arg); };
+  auto settle = [&]() {
+    if (!(st->g <= k && st->L < st->U)) st->status = BZ_LOOP_DONE;
+    else if (st->g > max_g) st->status = BZ_LOOP_MAX_G;
+  };
+  settle();
+  if (st->status != BZ_LOOP_RUNNING) return BZ_OK;
+  if (cap < 1) return fail(ctx, BZ_ERR_ARGUMENT, "no room for a round record");
+  CK(cudaSetDevice(ctx->device));
+  // the batch: the next rounds whose combinations fit the budget, not past
+  // max_g, not past the round where the loop must stop (L(g-1) >= U, and U
+  // never exceeds the lightest row once round 1 is in) -- engine.py's rule
+  const int g = st->g;
+  const int top = std::min(k, max_g);
+  const int u_cap = std::min(st->U, u_rows);
+  int count = 0;
+  double total = 0;
+  while (g + count <= top && count < cap && (count == 0 || lower(g + count - 1) < u_cap)) {
+    const double c = (double)m * binom_d(k, g + count);
+    if (batch_budget > 0 && total + c > (double)batch_budget) break;
+    total += c;
+    ++count;
+  }
+  if (batch_budget <= 0 || count < 1) count = 1;
+  std::vector<int> lp(count);
+  lp[0] = st->L;
+  for (int i = 1; i < count; ++i) lp[i] = lower(g + i - 1);
+  int rc = run_batch(ctx, g, count, -1, lp.data(), st->U, 0, 1, false);
+  if (rc) return rc;
+  // fold the rounds in order (engine.py:209-216); rounds past termination
+  // are discarded, their counters too
+  int n = 0;
+  for (int i = 0; i < count; ++i) {
+    if (i > 0) {
+      settle();
+      if (st->status != BZ_LOOP_RUNNING) break;
+    }
+    const int gi = g + i;
+    bz_round_record& r = out[n++];
+    r = bz_round_record{};
+    int U = st->U;
+    for (int j = 0; j < m; ++j) {
+      U = std::min(U, slot_bound(ctx, i)[1 + j]);
+      r.combinations += slot_combos(ctx, i)[j];
+      r.row_additions += slot_adds(ctx, i)[j];
+      r.row_accesses += slot_accs(ctx, i)[j];
+    }
+    r.kernel_ms = i < (int)ctx->round_ms.size() ? ctx->round_ms[i] : 0.f;
+    st->U = U;
+    st->L = lower(gi);
+    st->g_reached = gi;
+    st->g = gi + 1;
+    r.g = gi;
+    r.L = st->L;
+    r.U = st->U;
+  }
+  *n_out = n;
+  settle();
   return BZ_OK;
 }
 

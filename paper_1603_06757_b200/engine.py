@@ -107,6 +107,9 @@ class EngineConfig:
     shared_bound: bool = True
     engine: str = "auto"     # "auto" | "mxf4q" | "mxf4" | ... | "popc" (kernel; same results)
     elide_identity: bool = True  # drop each full-rank Gamma's identity columns (+g; exact)
+    # one rank: the loop itself runs natively (bz_advance: the same batch
+    # rule and fold, one library call per batch); False keeps it in Python
+    native_loop: bool = True
 
 
 @dataclass
@@ -265,6 +268,53 @@ def start_state(gs: GammaSet, n: int, k: int, config: EngineConfig) -> LoopState
     return LoopState(L=L, U=U, g=g, g_reached=g - 1)
 
 
+def lightest_row(gs: GammaSet) -> int:
+    """Weight of the lightest row of any Gamma (every row is a codeword, so
+    U never exceeds it once round 1 is in); cached on the family."""
+    w = getattr(gs, "_lightest_row", None)
+    if w is None:
+        w = min(int(np.bitwise_count(gm.words64()).sum(axis=1).min()) for gm in gs.gammas)
+        object.__setattr__(gs, "_lightest_row", w)  # frozen dataclass: a cache only
+    return w
+
+
+def _run_rounds_native(backend, gs: GammaSet, k: int, config: EngineConfig, st: LoopState,
+                       m_arg: int, km_arg: int) -> None:
+    """run_rounds on one rank through bz_advance: the batch rule and the
+    fold of the Python loop below, one library call per batch (the loop is
+    on the timed path of every run)."""
+    ctx = backend.ctx
+    backend.begin_run()
+    budget = (max(config.batch_combinations, config.batch_combinations_single)
+              if config.batch_combinations > 0 else 0)
+    u_rows = lightest_row(gs)
+    state = np.array([st.g, st.L, st.U, st.g_reached, 0], dtype=np.int32)
+    progress = config.progress
+    trace, rounds, ctr = st.trace, st.rounds, st.counters
+    while True:
+        t0 = time.perf_counter()
+        recs = ctx.advance(m_arg, km_arg, config.max_g, u_rows, budget, state)
+        wall = (time.perf_counter() - t0) * 1e3
+        # st follows the records (an interrupt between two calls leaves it
+        # at the last round folded in, as the Python loop does)
+        for g, L, U, _, c, a, x, ms, _ in recs:
+            ctr.combinations += c
+            ctr.row_additions += a
+            ctr.row_accesses += x
+            rounds.append(RoundStat(g, c, ms, wall))
+            wall = 0.0
+            trace.append((g, L, U))
+            st.g_reached = g
+            st.g, st.L, st.U = g + 1, L, U
+            if progress is not None:
+                progress(g, L, U)
+        status = int(state[4])
+        if status == _native.BZ_LOOP_MAX_G:
+            st.status = STATUS_UPPER_BOUND_ONLY
+        if status != _native.BZ_LOOP_RUNNING:
+            break
+
+
 def run_rounds(backend, gs: GammaSet, k: int, config: EngineConfig, st: LoopState) -> None:
     """The loop of engine.py:204-217 with one device round per g: fold the
     per-Gamma minima into U in Gamma order, then raise L, append (g, L, U),
@@ -273,6 +323,9 @@ def run_rounds(backend, gs: GammaSet, k: int, config: EngineConfig, st: LoopStat
     (This loop sits inside every timed run: it keeps to plain locals and
     arithmetic -- the L formula inlined, counters summed once per round.)"""
     m_arg, km_arg = line7_args(gs, k)
+    if (config.native_loop and isinstance(backend, GpuRounds) and backend.comm.world == 1
+            and not backend.shared):
+        return _run_rounds_native(backend, gs, k, config, st, m_arg, km_arg)
     m = gs.matrix_count
     batch_ok = config.batch_combinations > 0 and hasattr(backend, "run_batch")
     if hasattr(backend, "begin_run"):
@@ -291,11 +344,7 @@ def run_rounds(backend, gs: GammaSet, k: int, config: EngineConfig, st: LoopStat
     # runs only while L(g - 1) < U, and every row of every Gamma is a
     # codeword, so U never exceeds the lightest row once round 1 is in.
     # (Only the batch length depends on this; results do not.)
-    u_rows = U
-    for gm in gs.gammas:
-        w = int(np.bitwise_count(gm.words64()).sum(axis=1).min())
-        if w < u_rows:
-            u_rows = w
+    u_rows = min(U, lightest_row(gs))
     try:
         while g <= k and L < U:
             if g > max_g:

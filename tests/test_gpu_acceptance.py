@@ -107,3 +107,36 @@ def test_property_enumerate_matches_oracle():
         assert res.combinations == comb(k, g)
 
     check()
+
+
+@pytest.mark.parametrize("batch", [2_000_000_000, 0])
+def test_native_loop_equals_python_loop(batch):
+    """The loop on one rank runs natively (bz_advance); the Python loop it
+    replaces (EngineConfig(native_loop=False)) gives the same report: trace,
+    status, g_reached, every counter and each round's combinations -- with
+    batching on and off, under max_g, and resumed from start_g /
+    start_upper."""
+    from paper_1603_06757_b200.configs import code
+
+    rng = random.Random(5)
+    cases = [code(name, seed)[0] for name, seed in (("cfg1", 1), ("cfg1", 2), ("cfg2", 1),
+                                                     ("cfg3", 1), ("cfg5", 7))]
+    cases += [BitMatrix([rng.getrandbits(n) for _ in range(k)], n)
+              for k, n in ((9, 30), (20, 47), (33, 70), (60, 61))]
+    extra = [dict(), dict(max_g=2), dict(max_g=1), dict(start_g=3, start_upper=30)]
+    for G in cases:
+        for kw in extra:
+            try:
+                a = minimum_distance(G, EngineConfig(batch_combinations=batch, **kw))
+            except RankDeficient:
+                break
+            b = minimum_distance(G, EngineConfig(batch_combinations=batch, native_loop=False,
+                                                 **kw))
+            assert (a.distance, a.status, a.g_reached, a.bounds_trace) == \
+                (b.distance, b.status, b.g_reached, b.bounds_trace), (G.num_rows, kw)
+            assert (a.counters.combinations, a.counters.row_additions,
+                    a.counters.row_accesses) == (b.counters.combinations,
+                                                 b.counters.row_additions,
+                                                 b.counters.row_accesses)
+            assert [(r.g, r.combinations) for r in a.rounds] == \
+                [(r.g, r.combinations) for r in b.rounds]
