@@ -247,7 +247,8 @@ int bz_enumerate(bz_ctx *ctx, int gamma, int g, int shard, int nshards,
  *     one per codeword (its prefix sum combined with its last stored row:
  *     a XOR in K1, the tensor-core dot product in K5/K5q), K1's D = 2
  *     partial sums (prefix ^ R[e1], once per e1), and the prefix walkers'
- *     updates (q rows per colex unrank, 2 or 3 prefix-XOR rows per step);
+ *     updates (q rows per colex unrank, 2 or 3 prefix-XOR rows per step;
+ *     once per K1 prefix block, not per suffix lane repeating them);
  *   out_accs: rows brought into the working set -- every stored suffix row
  *     a warp (K1) or CTA (K5/K5q: shared memory, up to 128 prefixes per
  *     load) loads per prefix step, plus the table rows the walkers read.
@@ -261,15 +262,18 @@ int bz_histogram(bz_ctx *ctx, int gamma, int g, int shard, int nshards,
                  uint64_t *out_hist, int32_t *out_min, uint64_t *out_combos);
 
 /* Host-only: the work plan bz_round uses for (m, k, g, nshards), for inspection and
- * for the CPU tests of the sharding logic.  Writes *out_ngroups groups of 11
+ * for the CPU tests of the sharding logic.  Writes *out_ngroups groups of 12
  * int64 each -- chunk_begin, nprefix, gamma, ell, prefixes_per_lane,
  * combinations, depth, lanes_per_chunk, suffixes_per_chunk, suffix_blocks,
- * suffix_floor -- into out (capacity `cap` groups; out may be NULL to query
- * the count) and the round's chunk count into *out_nchunks.  Chunk c of the
- * round belongs to shard c % nshards.  Within group (gamma, ell, depth),
- * local chunk index c_local = pb * suffix_blocks + sb: lane l (0 <= l <
- * lanes_per_chunk: 32 for a warp of K1, 256 for a block of K3, 128 for K4 /
- * K5) walks the colex ranks [(pb*lanes + l)*ppl, +ppl) of the
+ * suffix_floor, suffix_lanes -- into out (capacity `cap` groups; out may be
+ * NULL to query the count) and the round's chunk count into *out_nchunks.
+ * Chunk c of the round belongs to shard c % nshards.  Within group (gamma,
+ * ell, depth), local chunk index c_local = pb * suffix_blocks + sb: prefix
+ * block l (0 <= l < lanes = lanes_per_chunk / suffix_lanes; lanes_per_chunk
+ * is 32 for a warp of K1, 256 for a block of K3, 128 for K4 / K5, and
+ * suffix_lanes > 1 only in K1, whose lanes l*suffix_lanes + s share block l
+ * and take its first suffix rows suffix_floor + s, + 2 suffix_lanes, ...)
+ * walks the colex ranks [(pb*lanes + l)*ppl, +ppl) of the
  * (g-1-depth)-subsets of [0, ell), each extended by ell and then by every
  * depth-subset of the suffix rows [suffix_floor, k) -- for depth >= 3 only
  * those with index in [sb*S, (sb+1)*S) of the table order (smallest element

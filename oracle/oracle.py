@@ -270,7 +270,8 @@ def enumerate_chunks(gammas: list[list[int]], k: int, g: int, groups, nchunks: i
     starts = [gr[0] for gr in groups]
     for chunk in range(shard, nchunks, nshards):
         gi = max(i for i, s in enumerate(starts) if s <= chunk)
-        begin, nprefix, gamma, ell, ppl, _, depth, lanes, spc, nsb, sfloor = groups[gi]
+        begin, nprefix, gamma, ell, ppl, _, depth, lanes, spc, nsb, sfloor, sl = groups[gi]
+        lanes //= sl  # K1: prefix blocks per warp (suffix lanes share a block)
         local = chunk - begin
         pb, sb = divmod(local, nsb)
         rows = gammas[gamma]
@@ -334,16 +335,19 @@ def expected_counters(m: int, k: int, g: int, groups, nchunks: int, shard: int =
     starts = [gr[0] for gr in groups]
     for chunk in range(shard, nchunks, nshards):
         gi = max(i for i, st in enumerate(starts) if st <= chunk)
-        begin, nprefix, gamma, ell, ppl, _, depth, lanes, spc, nsb, sfloor = groups[gi]
+        begin, nprefix, gamma, ell, ppl, _, depth, lanes, spc, nsb, sfloor, sl = groups[gi]
         q = g - 1 - depth
         local = chunk - begin
         if depth < 3:
-            # K1: one warp, lane-major ranges, walkers A / B on the halves
+            # K1: one warp, 32 / sl prefix blocks (lane-major ranges, walkers
+            # A / B on the halves) x sl suffix lanes taking every sl-th
+            # first suffix row
             e0 = ell + 1
             per_prefix = comb(k - e0, depth) + (max(0, k - 1 - e0) if depth == 2 else 0)
             maxca = 0
             for lane in range(32):
-                first = (local * 32 + lane) * ppl
+                blk, s0 = divmod(lane, sl)
+                first = (local * (32 // sl) + blk) * ppl
                 cnt = max(0, min(ppl, nprefix - first))
                 ca = (cnt + 1) >> 1
                 cb = cnt - ca
@@ -351,7 +355,14 @@ def expected_counters(m: int, k: int, g: int, groups, nchunks: int, shard: int =
                     maxca = ca
                 w = _walk_cost(first, ca, q, ell) + _walk_cost(first + ca, cb, q, ell)
                 ninit = (cnt > 0) + (cb > 0)
-                adds[gamma] += w + cnt * per_prefix
+                if depth == 1:
+                    lane_pp = len(range(e0 + s0, k, sl))
+                else:
+                    firsts = range(e0 + s0, k - 1, sl)
+                    lane_pp = sum(k - 1 - e1 for e1 in firsts) + len(firsts)
+                if s0:  # the block's walkers are counted on its first lane
+                    w = ninit = 0
+                adds[gamma] += w + cnt * lane_pp
                 accs[gamma] += w + ninit
             accs[gamma] += maxca * per_prefix
         else:

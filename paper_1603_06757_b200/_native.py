@@ -150,7 +150,7 @@ def plan(m: int, k: int, g: int, engine: str = "auto", nshards: int = 1):
     nc = np.zeros(1, dtype=np.uint64)
     check(L.bz_plan(m, k, g, e, nshards, None, 0, _ptr(ng, ctypes.c_int32),
                     _ptr(nc, ctypes.c_uint64)), what="bz_plan")
-    out = np.zeros((int(ng[0]), 11), dtype=np.int64)
+    out = np.zeros((int(ng[0]), 12), dtype=np.int64)
     check(L.bz_plan(m, k, g, e, nshards, _ptr(out, ctypes.c_int64), int(ng[0]),
                     _ptr(ng, ctypes.c_int32), _ptr(nc, ctypes.c_uint64)), what="bz_plan")
     return [tuple(int(v) for v in row) for row in out], int(nc[0])

@@ -114,7 +114,7 @@ namespace {
 // problem size, so every process computes the same plan.
 constexpr long long kChunksTarget = 40000;
 constexpr long long kLaneMin = 32, kLaneMax = 4096;
-constexpr int kPlanCols = 11;  // int64 columns per group in bz_plan
+constexpr int kPlanCols = 12;  // int64 columns per group in bz_plan
 
 int fail(bz_ctx* c, int code, const char* fmt, ...) {
   char buf[512];
@@ -443,18 +443,35 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
         const long long lt =
             (shape.kernel >= 4 && done >= fine_from) ? std::max(4096ll, lane_target / 8) : lane_target;
         done += np * (unsigned long long)work;
-        const long long lanes_ll = shape.lanes;
-        const long long spread = (long long)((np + lanes_ll - 1) / lanes_ll);
         // D >= 3: every prefix step also rebuilds the A operand and streams
         // at least one whole tile, which bounds chunk duration for the tiny
         // slices near ell = k - 4
         const long long step_cost =
             tiled ? std::max(work, (long long)shape.tile_rows) + 256 : work;
-        long long ppl = std::max(1ll, lt / std::max(1ll, step_cost));
+        // K1: the warp's 32 lanes are 32/sl prefix blocks x sl suffix lanes
+        // (each takes every sl-th first suffix row).  A group with fewer
+        // than 64 prefixes would leave lanes idle while others walk every
+        // suffix (g = 1: one lane walked all k rows at ~125 clocks each), so
+        // its suffixes are spread over the idle lanes.  (Spreading larger
+        // groups too, for more and shorter chunks, measured slower: a
+        // chunk's fixed cost -- group lookup, walker unrank -- is several
+        // thousand clocks, config 5's fused g <= 4 went 25 -> 28 us.)
+        long long sl = 1;
+        if (!tiled) {
+          const long long first_rows = depth == 1 ? k - sfloor : k - 1 - sfloor;
+          while (sl < 32 && 2 * sl <= first_rows && 32 / sl > (long long)((np + 1) / 2))
+            sl *= 2;
+        }
+        const long long lanes_ll = tiled ? shape.lanes : 32 / sl;
+        const long long spread = (long long)((np + lanes_ll - 1) / lanes_ll);
+        long long ppl = std::max(1ll, lt * sl / std::max(1ll, step_cost));
         // K1 lanes walk their range with two walkers (halves): a lane with a
         // single prefix runs its second walker on a duplicate, so give every
         // lane two prefixes where the group has them (config 4: 2x the work)
         if (!tiled) ppl = std::max(ppl, 2ll);
+        // one-element prefix tails (g - 1 - D <= 1): a fresh init is one row,
+        // cheaper than a colex step (two), so walkers take one prefix each
+        if (!tiled && g - 1 - depth <= 1) ppl = 2;
         ppl = std::min(ppl, std::max(1ll, spread));
         // D >= 3: a chunk is lanes prefixes x ppl steps x tpc tiles; a slice
         // too large for one chunk is split into tile blocks
@@ -476,6 +493,7 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
         gr.tile_rows = shape.tile_rows;
         gr.slice = (int)work;
         gr.sfloor = sfloor;
+        gr.sl = (int)sl;
         const unsigned long long per_chunk = (unsigned long long)lanes_ll * (unsigned long long)ppl;
         chunk += (np + per_chunk - 1) / per_chunk * (unsigned long long)ntb;
         gs.push_back(gr);
@@ -1930,6 +1948,7 @@ int bz_plan(int m, int k, int g, int engine, int nshards, int64_t* out, int cap,
       o[8] = gs[i].depth >= 3 ? (int64_t)gs[i].tpc * gs[i].tile_rows : 0;
       o[9] = gs[i].ntb;
       o[10] = gs[i].sfloor;
+      o[11] = gs[i].sl;
     }
   }
   return BZ_OK;

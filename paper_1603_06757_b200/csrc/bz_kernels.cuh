@@ -51,6 +51,7 @@ struct Group {
   int tile_rows;                   // D >= 3: suffixes per table tile
   int slice;                       // suffixes per prefix: C(k - sfloor, D)
   int sfloor;                      // smallest suffix row: max(ell + 1, level floor)
+  int sl;                          // K1: suffix lanes per prefix block (1, 2, .., 32)
 };
 
 struct RoundArgs {
@@ -449,20 +450,23 @@ __device__ __forceinline__ void stage(const RoundArgs& a, uint32_t*& srows,
 // receives the weight of each codeword of A and of B.
 template <int W, int D, typename Visit>
 __device__ __forceinline__ void suffix_pair(const uint32_t (&a)[W], const uint32_t (&b)[W],
-                                            const uint32_t* R, int e0, int k, Visit&& visit) {
+                                            const uint32_t* R, int e0, int k, int s0, int ss,
+                                            Visit&& visit) {
   constexpr int WP = padded_words(W);
+  // this lane's share of the first suffix row: e0 + s0, e0 + s0 + ss, ...
+  // (ss = the group's suffix lanes; 1: every row)
   if constexpr (D == 1) {
-    const uint32_t* re = R + e0 * WP;
+    const uint32_t* re = R + (e0 + s0) * WP;
 #pragma unroll 2
-    for (int e = e0; e < k; ++e, re += WP) {
+    for (int e = e0 + s0; e < k; e += ss, re += ss * WP) {
       uint32_t r0[W];
       load_row<W>(r0, re);
       visit(weight_xor<W>(a, r0), weight_xor<W>(b, r0));
     }
   } else {
-    const uint32_t* r1p = R + e0 * WP;
+    const uint32_t* r1p = R + (e0 + s0) * WP;
 #pragma unroll 1
-    for (int e1 = e0; e1 < k - 1; ++e1, r1p += WP) {
+    for (int e1 = e0 + s0; e1 < k - 1; e1 += ss, r1p += ss * WP) {
       uint32_t r1[W], a1[W], b1[W];
       load_row<W>(r1, r1p);
 #pragma unroll
@@ -487,19 +491,44 @@ __device__ __forceinline__ unsigned long long suffix_count(int k, int e0) {
   return D == 1 ? t : t * (t - 1) / 2;
 }
 
+// A lane's share of one prefix's suffixes (first row e0 + s0, stride ss):
+// codewords, and for D = 2 the partial sums prefix ^ R[e1] it forms
+template <int D>
+__device__ __forceinline__ void lane_suffixes(int k, int e0, int s0, int ss,
+                                              unsigned long long& words,
+                                              unsigned long long& partial) {
+  const int f = e0 + s0;
+  const int last = D == 1 ? k : k - 1;  // first-row values below `last`
+  const long long t = f < last ? (last - f + ss - 1) / ss : 0;
+  if (D == 1) {
+    words = (unsigned long long)t;
+    partial = 0ull;
+  } else {
+    // sum over j < t of (k - 1 - (f + j ss))
+    words = (unsigned long long)(t * (long long)(k - 1 - f) - (long long)ss * t * (t - 1) / 2);
+    partial = (unsigned long long)t;
+  }
+}
+
 // Shared prologue of a chunk: the lane's prefix range [first, first+cnt).
 struct ChunkView {
   Group gr;
   unsigned long long first;
   long long cnt;
+  int s0;  // this lane's first suffix offset (stride gr.sl)
 };
 
+// K1 lanes: 32 / sl prefix blocks of ppl colex ranks (block-major) x sl
+// suffix lanes sharing each block (lane = block * sl + s0)
 __device__ __forceinline__ ChunkView open_chunk(const Group* sg, int ngroups,
                                                 unsigned long long chunk, int lane) {
   ChunkView v;
   v.gr = sg[find_group(sg, ngroups, chunk)];
   const unsigned long long local = chunk - v.gr.chunk_begin;
-  v.first = (local * 32ull + lane) * (unsigned long long)v.gr.ppl;
+  const int sl = v.gr.sl;
+  v.s0 = lane & (sl - 1);
+  v.first = (local * (unsigned long long)(32 / sl) + (unsigned long long)(lane / sl)) *
+            (unsigned long long)v.gr.ppl;
   v.cnt = 0;
   if (v.first < v.gr.nprefix) {
     const unsigned long long left = v.gr.nprefix - v.first;
@@ -515,10 +544,41 @@ __device__ __forceinline__ ChunkView open_chunk(const Group* sg, int ngroups,
 // XOR/POPC chains).  When the range is odd the second walker duplicates the
 // first on the last step -- harmless for a minimum.
 // One chunk (a warp's share of the plan) of round a.
+// Per-block tallies of one round in shared memory: a chunk's counts and
+// minimum go here with shared-memory atomics and reach the round's global
+// words once per block (k1_tally_flush) -- thousands of short chunks of a
+// small round otherwise queue that many atomics on the same few L2 words.
+// A chunk minimum below the block's best so far is still published at once.
+constexpr int kTallyM = 16;  // Gammas tallied per block (more: per-chunk atomics)
+struct K1Tally {
+  unsigned long long combos[kTallyM], adds[kTallyM], accs[kTallyM];
+  int best[kTallyM];
+};
+
+__device__ __forceinline__ void k1_tally_init(K1Tally* t, int count) {
+  for (int i = threadIdx.x; i < count * kTallyM; i += blockDim.x) {
+    K1Tally& u = t[i / kTallyM];
+    const int j = i % kTallyM;
+    u.combos[j] = u.adds[j] = u.accs[j] = 0ull;
+    u.best[j] = INT_MAX;
+  }
+}
+
+// after a __syncthreads that follows every chunk of the block
+__device__ __forceinline__ void k1_tally_flush(const RoundArgs& a, const K1Tally& t) {
+  const int m = min(a.m, kTallyM);
+  for (int j = threadIdx.x; j < m; j += blockDim.x) {
+    if (t.combos[j]) atomicAdd(a.combos + j, t.combos[j]);
+    if (a.adds && t.adds[j]) atomicAdd(a.adds + j, t.adds[j]);
+    if (a.accs && t.accs[j]) atomicAdd(a.accs + j, t.accs[j]);
+  }
+}
+
 template <int W, int D>
 __device__ __forceinline__ void k1_chunk(const RoundArgs& a, unsigned long long chunk,
                                          const uint32_t* srows, const uint32_t* spx,
-                                         const Group* sgroups, const unsigned long long* sbinom) {
+                                         const Group* sgroups, const unsigned long long* sbinom,
+                                         K1Tally* tally) {
   constexpr int WP = padded_words(W);
   const unsigned FULL = 0xffffffffu;
   const int lane = threadIdx.x & 31;
@@ -549,7 +609,7 @@ __device__ __forceinline__ void k1_chunk(const RoundArgs& a, unsigned long long 
           for (int j = 0; j < W; ++j) B.acc[j] = A.acc[j];
         }
         int pa = INT_MAX, pb = INT_MAX;
-        suffix_pair<W, D>(A.acc, B.acc, R, e0, k, [&](int wa, int wb) {
+        suffix_pair<W, D>(A.acc, B.acc, R, e0, k, v.s0, v.gr.sl, [&](int wa, int wb) {
           pa = min(pa, wa);
           pb = min(pb, wb);
         });
@@ -563,45 +623,64 @@ __device__ __forceinline__ void k1_chunk(const RoundArgs& a, unsigned long long 
     // forget reductions); combos count
     int wbest = __reduce_min_sync(FULL, best);
     if (wbest != INT_MAX) wbest += gamma_woff(a, v.gr.gamma);
-    const unsigned tot = __reduce_add_sync(FULL, (unsigned)v.cnt);
+    unsigned long long lw, lp;  // this lane's codewords / partial sums per prefix
+    lane_suffixes<D>(k, e0, v.s0, v.gr.sl, lw, lp);
+    const unsigned tot = __reduce_add_sync(FULL, (unsigned)((unsigned long long)v.cnt * lw));
+    const bool tallied = v.gr.gamma < kTallyM;
     if (lane == 0) {
-      if (wbest != INT_MAX) {
+      if (wbest != INT_MAX && (!tallied || wbest < tally->best[v.gr.gamma])) {
+        if (tallied) atomicMin(tally->best + v.gr.gamma, wbest);
         atomicMin(a.bound + 1 + v.gr.gamma, wbest);
         atomicMin(a.bound, wbest);
         gbound_publish(a, wbest);
       }
-      atomicAdd(a.combos + v.gr.gamma, (unsigned long long)tot * suffix_count<D>(k, e0));
+      if (tallied) atomicAdd(tally->combos + v.gr.gamma, (unsigned long long)tot);
+      else atomicAdd(a.combos + v.gr.gamma, (unsigned long long)tot);
     }
     if (a.adds) {
       // every codeword is one row addition (prefix sum ^ its last suffix
       // row); D = 2 adds the partial sum prefix ^ R[e1] once per e1.  A
-      // suffix row is loaded once per walker-pair step for the whole warp;
-      // the walkers read one table row per addition plus R[ell] per init.
+      // suffix row is loaded once per walker-pair step for the whole warp
+      // (sl > 1: each by the suffix lanes owning it); the walkers read one
+      // table row per addition plus R[ell] per init -- counted once per
+      // prefix block (its other suffix lanes repeat the same prefix sums)
       const unsigned long long per_prefix =
           suffix_count<D>(k, e0) + (D == 2 ? (unsigned long long)max(0, k - 1 - e0) : 0ull);
-      const unsigned long long adds = warp_sum_u64(wadd + (unsigned long long)v.cnt * per_prefix);
-      const unsigned long long accs = warp_sum_u64(wadd + (unsigned long long)ninit) +
+      if (v.s0 != 0) wadd = 0ull;
+      const unsigned long long adds = warp_sum_u64(wadd + (unsigned long long)v.cnt * (lw + lp));
+      const unsigned long long accs = warp_sum_u64(wadd + (v.s0 == 0 ? (unsigned long long)ninit : 0ull)) +
                                       (unsigned long long)maxca * per_prefix;
       if (lane == 0) {
-        atomicAdd(a.adds + v.gr.gamma, adds);
-        atomicAdd(a.accs + v.gr.gamma, accs);
+        if (tallied) {
+          atomicAdd(tally->adds + v.gr.gamma, adds);
+          atomicAdd(tally->accs + v.gr.gamma, accs);
+        } else {
+          atomicAdd(a.adds + v.gr.gamma, adds);
+          atomicAdd(a.accs + v.gr.gamma, accs);
+        }
       }
     }
   }
 }
 
-// Chunks dealt by an atomic cursor: uneven prefix walks balance themselves.
-template <int W, int D>
-__device__ __forceinline__ void k1_chunks(const RoundArgs& a, const uint32_t* srows,
-                                          const uint32_t* spx, const Group* sgroups,
-                                          const unsigned long long* sbinom) {
-  while (true) {
-    unsigned long long c = 0;
-    if ((threadIdx.x & 31) == 0) c = atomicAdd(a.counter, 1ull);
-    c = __shfl_sync(0xffffffffu, c, 0);
-    const unsigned long long chunk = c * (unsigned long long)a.nshards + a.shard;
-    if (chunk >= a.nchunks || round_done(a)) break;
-    k1_chunk<W, D>(a, chunk, srows, spx, sgroups, sbinom);
+// This shard's chunks: warp w first takes chunk w (no atomic), then, when
+// the grid has fewer warps than chunks, draws the rest from an atomic
+// cursor (uneven prefix walks balance themselves).  A small round's warps
+// each run one chunk and never touch the cursor.
+template <bool kMayStop = true, typename Body>
+__device__ __forceinline__ void deal_chunks(const RoundArgs& a, Body&& body) {
+  const unsigned long long nw = (unsigned long long)gridDim.x * (blockDim.x >> 5);
+  const unsigned long long mine =
+      a.nchunks > (unsigned long long)a.shard
+          ? (a.nchunks - a.shard + a.nshards - 1) / a.nshards : 0ull;
+  unsigned long long c = (unsigned long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  while (c < mine) {
+    if (kMayStop && round_done(a)) break;
+    body(c * (unsigned long long)a.nshards + a.shard);
+    if (nw >= mine) break;
+    unsigned long long nx = 0;
+    if ((threadIdx.x & 31) == 0) nx = atomicAdd(a.counter, 1ull);
+    c = nw + __shfl_sync(0xffffffffu, nx, 0);
   }
 }
 
@@ -609,15 +688,21 @@ template <int W, int D>
 __global__ void __launch_bounds__(256)
 k1_round_min(const RoundArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ K1Tally tally;
   uint32_t *srows, *spx;
   Group* sgroups;
-  stage<W>(a, srows, spx, sgroups, smem);
+  k1_tally_init(&tally, 1);
+  stage<W>(a, srows, spx, sgroups, smem);  // ends with __syncthreads
   const unsigned long long* sbinom = smem_binom<W>(smem, a);
   // batched round: start from the U the previous round ended with (one
   // thread of the grid: atomics on one address serialise; blocks that read
   // the bound before it lands just see the looser start value)
   round_start(a);
-  k1_chunks<W, D>(a, srows, spx, sgroups, sbinom);
+  deal_chunks(a, [&](unsigned long long chunk) {
+    k1_chunk<W, D>(a, chunk, srows, spx, sgroups, sbinom, &tally);
+  });
+  __syncthreads();
+  k1_tally_flush(a, tally);
 }
 
 // Several small rounds (same family, same suffix depth) in one launch: the
@@ -638,8 +723,10 @@ struct K1Batch {
 template <int W, int D>
 __global__ void __launch_bounds__(256) k1_rounds(const K1Batch b) {
   extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ K1Tally tally[kK1MaxFused];
   uint32_t *srows, *spx;
   Group* sgroups;
+  k1_tally_init(tally, b.count);
   stage<W>(b.a[0], srows, spx, sgroups, smem);  // round 0's plan at sgroups
   const unsigned long long* sbinom = smem_binom<W>(smem, b.a[0]);
   int goff[kK1MaxFused];
@@ -675,8 +762,13 @@ __global__ void __launch_bounds__(256) k1_rounds(const K1Batch b) {
     const RoundArgs& a = b.a[r];
     const unsigned long long local = c - (r > 0 ? cend[r - 1] : 0ull);
     if (round_done(a)) continue;
-    k1_chunk<W, D>(a, local * a.nshards + a.shard, srows, spx, sgroups + goff[r], sbinom);
+    k1_chunk<W, D>(a, local * a.nshards + a.shard, srows, spx, sgroups + goff[r], sbinom,
+                   tally + r);
   }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kK1MaxFused; ++r)
+    if (r < b.count) k1_tally_flush(b.a[r], tally[r]);
 }
 
 // ---------------------------------------------------------------------------
@@ -789,13 +881,8 @@ k1h_histogram(const RoundArgs a) {
     since_flush = 0;
   };
 
-  while (true) {
-    unsigned long long c = 0;
-    if (lane == 0) c = atomicAdd(a.counter, 1ull);
-    c = __shfl_sync(FULL, c, 0);
-    const unsigned long long chunk = c * (unsigned long long)a.nshards + a.shard;
-    if (chunk >= a.nchunks) break;
-
+  unsigned long long wcombos = 0;  // this warp's combinations (one atomic at the end)
+  deal_chunks<false>(a, [&](unsigned long long chunk) {  // every combination
     const ChunkView v = open_chunk(sgroups, a.ngroups, chunk, lane);
     const long long ca = (v.cnt + 1) >> 1;
     const long long cb = v.cnt - ca;
@@ -803,7 +890,9 @@ k1h_histogram(const RoundArgs a) {
     const uint32_t* R = srows + v.gr.gamma * k * WP;
     const uint32_t* PX = spx + v.gr.gamma * (k + 1) * px_stride(W);
     const int e0 = v.gr.ell + 1;
-    const unsigned chunk_work = (unsigned)((unsigned long long)v.cnt * suffix_count<D>(k, e0));
+    unsigned long long lw, lp;  // this lane's codewords per prefix
+    lane_suffixes<D>(k, e0, v.s0, v.gr.sl, lw, lp);
+    const unsigned chunk_work = (unsigned)((unsigned long long)v.cnt * lw);
     if (since_flush + chunk_work > 65535u) flush();
     since_flush += chunk_work;
 
@@ -813,7 +902,7 @@ k1h_histogram(const RoundArgs a) {
     for (long long p = 0; p < maxca; ++p) {
       if (p < ca) {
         const bool with_b = p < cb;
-        suffix_pair<W, D>(A.acc, B.acc, R, e0, k, [&](int wa, int wb) {
+        suffix_pair<W, D>(A.acc, B.acc, R, e0, k, v.s0, v.gr.sl, [&](int wa, int wb) {
           best = min(best, wa);
           unsigned short* h = th + wa * bd + tid;
           *h = (unsigned short)(*h + 1);
@@ -827,11 +916,11 @@ k1h_histogram(const RoundArgs a) {
         if (p + 1 < cb) B.step(PX);
       }
     }
-    const unsigned tot = __reduce_add_sync(FULL, (unsigned)v.cnt);
-    if (lane == 0)
-      atomicAdd(a.combos + v.gr.gamma, (unsigned long long)tot * suffix_count<D>(k, e0));
-  }
+    wcombos += __reduce_add_sync(FULL, chunk_work);
+  });
   flush();
+  // the pass is one Gamma
+  if (lane == 0 && wcombos && a.ngroups > 0) atomicAdd(a.combos + sgroups[0].gamma, wcombos);
   // the pass is one Gamma (all groups share it): shift by its dropped
   // identity weight
   const int off = a.ngroups > 0 ? gamma_woff(a, sgroups[0].gamma) : 0;

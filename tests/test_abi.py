@@ -47,8 +47,9 @@ def test_plan_counts(engine):
         starts = [gr[0] for gr in groups]
         assert starts == sorted(starts) and starts[0] == 0
         for gr in groups:
-            begin, nprefix, gamma, ell, ppl, combos, depth, lanes, spc, nsb, sfloor = gr
+            begin, nprefix, gamma, ell, ppl, combos, depth, lanes, spc, nsb, sfloor, sl = gr
             assert nsb >= 1 and (depth < 3 or spc * nsb >= comb(k - sfloor, depth))
+            assert sl in (1, 2, 4, 8, 16, 32) and (depth < 3 or sl == 1)
             assert lanes == ({"imma": 256}.get(engine, 128) if depth >= 3 else 32)
             want = 3 if (engine != "popc" and g >= 4) else (2 if g >= 4 else 1)
             if engine in ("auto", "mxf4", "mxf4p", "mxf4t", "mxf4q", "mxf4w") and g >= 4:

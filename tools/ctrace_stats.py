@@ -30,7 +30,7 @@ def main():
 
     def info(c):
         gi = bisect.bisect_right(begins, c) - 1
-        b, npf, gam, ell, ppl, combs, depth, lanes, spc, nsb, sfloor = (int(x) for x in groups[gi])
+        b, npf, gam, ell, ppl, combs, depth, lanes, spc, nsb, sfloor, _ = (int(x) for x in groups[gi])
         local = c - b
         pb, tb = divmod(local, nsb)
         steps = min(ppl, npf - pb * lanes * ppl)
