@@ -461,6 +461,19 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
           const long long first_rows = depth == 1 ? k - sfloor : k - 1 - sfloor;
           while (sl < 32 && 2 * sl <= first_rows && 32 / sl > (long long)((np + 1) / 2))
             sl *= 2;
+          // D = 2: a prefix carries up to C(k - 1, 2) codewords, so two of
+          // them can be a chunk thousands of times longer than the round's
+          // average -- the SMs holding those finish last (config 4's
+          // histogram: SMs active 59 % of the launch).  Spread such
+          // prefixes' first suffix rows over lanes until a lane's share is
+          // near an even split of the round over 16 warps per SM (swept
+          // 2..512: config-4 histogram 191 -> 127 us, its K1 minimum 156 ->
+          // 101 us, config 5's g = 5 on K1 184 -> 65 us).
+          if (depth == 2) {
+            const long long even = (long long)(total / (32ull * 148ull * 16ull));
+            const long long lt_w = std::max(lane_target, even);
+            while (sl < 32 && 2 * sl <= first_rows && 2 * work / sl > lt_w) sl *= 2;
+          }
         }
         const long long lanes_ll = tiled ? shape.lanes : 32 / sl;
         const long long spread = (long long)((np + lanes_ll - 1) / lanes_ll);
