@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define BZ_ABI_VERSION 14
+#define BZ_ABI_VERSION 15
 
 /* limits of the device kernels */
 #define BZ_MAX_K 128 /* rows per Gamma (prefix masks are 128-bit)      */
@@ -79,6 +79,12 @@ extern "C" {
                              K5q's 128 stored columns; W = 1 runs K5).
                              On request: measured no faster than K5 on the
                              section-6 codes      */
+#define BZ_ENGINE_MXF4F 9 /* K5f: K5q's byte fields from folded MMAs (odd
+                             W <= 3 whose last stored word holds <= 16
+                             columns, e.g. config 5's 80: 3 MMAs per tile
+                             instead of 4); else as BZ_ENGINE_MXF4Q.  On
+                             request: measured slower than K5q (2.31 against
+                             2.02 ms on config 5's g = 8 round)         */
 
 typedef struct bz_ctx bz_ctx;
 

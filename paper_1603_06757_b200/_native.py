@@ -19,7 +19,7 @@ from .errors import (DeviceError, InvalidArity, InvalidDimensions, MindistError,
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BZ_LIB") or os.path.join(PKG_DIR, "libbz.so")
-ABI_VERSION = 14
+ABI_VERSION = 15
 
 BZ_OK = 0
 BZ_LOOP_RUNNING, BZ_LOOP_DONE, BZ_LOOP_MAX_G = 0, 1, 2
@@ -139,7 +139,7 @@ def device_count() -> int:
 
 
 ENGINES = {"auto": 0, "popc": 1, "imma": 2, "umma": 3, "mxf4": 4, "mxf4p": 5, "mxf4t": 6, "mxf4q": 7,
-           "mxf4w": 8}
+           "mxf4w": 8, "mxf4f": 9}
 
 
 def plan(m: int, k: int, g: int, engine: str = "auto", nshards: int = 1):

@@ -78,6 +78,7 @@ struct bz_ctx {
   size_t lvl_cap[3] = {0, 0, 0};
   size_t lvl_rows[3] = {0, 0, 0};
   int lvl_floor[3] = {-1, -1, -1};
+  int lvl_form = 1;                  // row format the level tables were built in (ensure_level)
   // grow-only capacities (bytes) so repeated loads do not reallocate
   size_t rows_cap = 0, px_cap = 0, trip_cap = 0, trip4_cap = 0;
   // tables are built on first use
@@ -211,7 +212,7 @@ T* slot_ptr(unsigned char* base, const IoSlot& l, int i, size_t off) {
 // g >= 4; K1 (POPC) takes D = 2 for g >= 4, else 1.  Histograms run on K1.
 struct PlanShape {
   int depth, lanes, tile_rows, kernel;  // kernel: 1 = K1, 3 = K3, 4 = K4, 5 = K5, 6 = K5p,
-                                        // 7 = K5t, 8 = K5q, 9 = K5w
+                                        // 7 = K5t, 8 = K5q, 9 = K5w, 10 = K5f
 };
 
 // K5p (two codewords per accumulator column) needs odd W <= 3 stored words
@@ -253,7 +254,15 @@ PlanShape pass_shape(int engine, int g, bool hist, int w32 = 0, int m = 0, int k
     const bool packed_ok = w32 == 0 || k5p_ok(w32);
     if (engine == BZ_ENGINE_MXF4T && packed_ok) return {3, bz::kUmmaM, bz::k4_tile_rows<true, 3>(), 7};
     const bool q_ok = w32 == 0 || k5q_ok(w32, n_eff);
-    if ((engine == BZ_ENGINE_MXF4Q || engine == BZ_ENGINE_AUTO) && q_ok)
+    // K5f: K5q's fields from folded MMAs (3 instead of 4 per tile at W = 3)
+    // where the last stored word is at most half used (bz::k5f_ok); a
+    // host-only plan (w32 = 0) has K5q's shape either way.  On request only:
+    // config 5's g = 8 round measured 2.31 ms against K5q's 2.02 ms -- the
+    // epilogue's wait / load / release chain per accumulator bounds both, and
+    // K5f adds an IMAD per register to it
+    if (engine == BZ_ENGINE_MXF4F && w32 != 0 && bz::k5f_ok(w32, n_eff))
+      return {3, bz::kUmmaM, bz::k4_tile_rows<true, 6>(), 10};
+    if ((engine == BZ_ENGINE_MXF4Q || engine == BZ_ENGINE_MXF4F || engine == BZ_ENGINE_AUTO) && q_ok)
       return {3, bz::kUmmaM, bz::k4_tile_rows<true, 4>(), 8};  // K5q
     // K5w (two codewords per column as 11-bit fields) on request only: on
     // the wide section-6 codes it measured no faster than K5 (C1 round 12:
@@ -264,7 +273,7 @@ PlanShape pass_shape(int engine, int g, bool hist, int w32 = 0, int m = 0, int k
       return {3, bz::kUmmaM, bz::k4_tile_rows<true, 5>(), 9};
     if (engine == BZ_ENGINE_MXF4P && packed_ok) return {3, bz::kUmmaM, bz::k4_tile_rows<true, 2>(), 6};
     if (engine == BZ_ENGINE_AUTO || engine == BZ_ENGINE_MXF4 || engine == BZ_ENGINE_MXF4P ||
-        engine == BZ_ENGINE_MXF4T || engine == BZ_ENGINE_MXF4Q)
+        engine == BZ_ENGINE_MXF4T || engine == BZ_ENGINE_MXF4Q || engine == BZ_ENGINE_MXF4F)
       return {3, bz::kUmmaM, bz::kUmmaN4, 5};
   }
   // D = 2 needs enough (g-3)-prefixes per group to fill a warp; at g = 3
@@ -804,7 +813,7 @@ int build_triples_w(bz_ctx* ctx, int which) {
 
 #endif
 
-template <int W>
+template <int W, int FORM = 1>
 int build_level_w(bz_ctx* ctx, int D, int floor) {
   const unsigned long long n = binom_sat(ctx->k - floor, D);
   // every row of the Gamma's stride: the subsets, then the empty-subset tail
@@ -816,7 +825,7 @@ int build_level_w(bz_ctx* ctx, int D, int floor) {
     CK(cudaStreamWaitEvent(ctx->side, ctx->ev_main, 0));
     ctx->side_pending = true;
   }
-  bz::k_build_subsets_mxf4<W><<<grid, 128, 0, ctx->side>>>(
+  bz::k_build_subsets_mxf4<W, FORM><<<grid, 128, 0, ctx->side>>>(
       ctx->d_rows, ctx->d_lvl[D - 3], ctx->k, D, n, ctx->lvl_rows[D - 3], ctx->d_binom);
   CK(cudaGetLastError());
   ctx->launches += 1;
@@ -827,8 +836,15 @@ int build_level_w(bz_ctx* ctx, int D, int floor) {
 // (grow-only: a table built for a lower floor already holds these subsets
 // as its first rows).  Not zero-filled: padding rows are only ever read into
 // columns the kernel masks.
-int ensure_level(bz_ctx* ctx, int D, int floor) {
+// form: the row format -- 6 for K5f (the last chunk half data, half offset
+// pattern), else 1 (K5 / K5q / K5w rows); tables of another format are
+// rebuilt.
+int ensure_level(bz_ctx* ctx, int D, int floor, int form) {
   const int i = D - 3;
+  if (ctx->lvl_form != form) {
+    for (int q = 0; q < 3; ++q) ctx->lvl_floor[q] = -1;
+    ctx->lvl_form = form;
+  }
   if (ctx->lvl_floor[i] >= 0 && ctx->lvl_floor[i] <= floor) return BZ_OK;
   if (ctx->k - floor < D) return BZ_OK;  // no subsets: nothing reads it
   const size_t n = (size_t)binom_sat(ctx->k - floor, D);
@@ -836,14 +852,14 @@ int ensure_level(bz_ctx* ctx, int D, int floor) {
   // one tile of slack
   const size_t N = bz::k4_tile_rows<true, 3>();
   ctx->lvl_rows[i] = (n + N - 1) / N * N + N;
-  const size_t row_bytes = 16 * (size_t)(bz::k5_padmagic(ctx->w32) ? ctx->w32 + 1 : ctx->w32);
+  const size_t row_bytes = (size_t)bz::k4_row_bytes<true>(ctx->w32, form);
   const size_t bytes = (size_t)ctx->m * ctx->lvl_rows[i] * row_bytes;
   CK(grow(ctx, (void**)&ctx->d_lvl[i], &ctx->lvl_cap[i], bytes));
   int rc;
   switch (ctx->w32) {
-    case 1: rc = build_level_w<1>(ctx, D, floor); break;
+    case 1: rc = form == 6 ? build_level_w<1, 6>(ctx, D, floor) : build_level_w<1>(ctx, D, floor); break;
     case 2: rc = build_level_w<2>(ctx, D, floor); break;
-    case 3: rc = build_level_w<3>(ctx, D, floor); break;
+    case 3: rc = form == 6 ? build_level_w<3, 6>(ctx, D, floor) : build_level_w<3>(ctx, D, floor); break;
     case 4: rc = build_level_w<4>(ctx, D, floor); break;
     case 5: rc = build_level_w<5>(ctx, D, floor); break;
     case 6: rc = build_level_w<6>(ctx, D, floor); break;
@@ -934,6 +950,8 @@ int launch_w(bz_ctx* ctx, const RoundArgs* as, int count, bool hist, const PlanS
     if (shape.kernel == 8) return launch_umma<W, true, 4>(ctx, as, count);
   if constexpr (W >= 2)
     if (shape.kernel == 9) return launch_umma<W, true, 5>(ctx, as, count);
+  if constexpr (W == 1 || W == 3)
+    if (shape.kernel == 10) return launch_umma<W, true, 6>(ctx, as, count);
   if (shape.kernel >= 3 && shape.kernel != 5)
     return fail(ctx, BZ_ERR_STATE, "kernel %d not available at W = %d", shape.kernel, W);
   if (shape.kernel == 5) return launch_umma<W, true>(ctx, as, count);
@@ -1021,6 +1039,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   const PlanKnobs knobs;
   int trace_from = 0, trace_ell = -1;
   int lvl_lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX};  // lowest floor per level (D = 3..5)
+  int lvl_form = 1;                                   // row format of the batch's tables
   if (debug) {
     if (const char* e = getenv("BZ_K4_TRACE_FROM")) trace_from = atoi(e);
     if (const char* e = getenv("BZ_K4_TRACE_ELL")) trace_ell = atoi(e);
@@ -1046,6 +1065,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
       const Group* gp = reinterpret_cast<const Group*>(ctx->h_io + gthis);
       for (int q = 0; q < ngroups; ++q)
         lvl_lo[gp[q].depth - 3] = std::min(lvl_lo[gp[q].depth - 3], gp[q].sfloor);
+      if (shape.kernel == 10) lvl_form = 6;
     }
     *slot_ptr<unsigned long long>(ctx->h_io, l, i, 0) = 0ull;
     unsigned long long* hc = slot_ptr<unsigned long long>(ctx->h_io, l, i, l.off_combos);
@@ -1091,7 +1111,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
       // elided g, so a shard that visits any of its combinations reports
       // min(upper, true minimum) exactly when its bound starts at that cap --
       // which keeps K5q's threshold inside its byte fields (k5q_threshold)
-      bool loose = shape.kernel == 8 || shape.kernel == 9;
+      bool loose = shape.kernel == 8 || shape.kernel == 9 || shape.kernel == 10;
       for (int j = 0; j < m; ++j)
         if (gamma_only < 0 || gamma_only == j) {
           const long long cap =
@@ -1111,7 +1131,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
   // and building per round rebuilt each table up to three times
   for (int D = 3; D <= 5; ++D)
     if (lvl_lo[D - 3] != INT32_MAX) {
-      rc = ensure_level(ctx, D, D == 3 ? 0 : lvl_lo[D - 3]);
+      rc = ensure_level(ctx, D, D == 3 ? 0 : lvl_lo[D - 3], lvl_form);
       if (rc) return rc;
     }
   const auto t_plan1 = std::chrono::steady_clock::now();
@@ -1154,7 +1174,7 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
     int f = 1;
     size_t fused_groups = (size_t)todo[i].a.ngroups;
     const int kern = todo[i].shape.kernel;
-    const bool tensor = kern == 5 || kern == 8 || kern == 9;
+    const bool tensor = kern == 5 || kern == 8 || kern == 9 || kern == 10;
     while (!hist && !debug && i + f < count && todo[i + f].run &&
            todo[i + f].shape.kernel == kern &&
            ((kern == 1 && f < bz::kK1MaxFused && todo[i + f].shape.depth == todo[i].shape.depth &&
@@ -1920,7 +1940,7 @@ int bz_elided(bz_ctx* ctx, uint64_t* out_mask) {
 
 int bz_set_engine(bz_ctx* ctx, int engine) {
   if (!ctx) return BZ_ERR_ARGUMENT;
-  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4W)
+  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4F)
     return fail(ctx, BZ_ERR_ARGUMENT, "unknown engine %d", engine);
   if (!BZ_LEGACY_KERNELS && (engine == BZ_ENGINE_IMMA || engine == BZ_ENGINE_UMMA ||
                              engine == BZ_ENGINE_MXF4P || engine == BZ_ENGINE_MXF4T))
@@ -1940,7 +1960,7 @@ int bz_plan(int m, int k, int g, int engine, int nshards, int64_t* out, int cap,
   if (binom_sat(k, g) >= (1ull << 62)) return BZ_ERR_TOO_LARGE;
   std::vector<Group> gs;
   unsigned long long nchunks = 0;
-  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4W) return BZ_ERR_ARGUMENT;
+  if (engine < BZ_ENGINE_AUTO || engine > BZ_ENGINE_MXF4F) return BZ_ERR_ARGUMENT;
   if (nshards < 1) return BZ_ERR_ARGUMENT;
   int rc = build_plan(nullptr, m, k, g, -1, pass_shape(engine, g, false), nshards, gs, &nchunks);
   if (rc) return rc;

@@ -45,6 +45,8 @@
 // descriptor describes.
 #pragma once
 
+#include <type_traits>
+
 #include "bz_tc.cuh"
 
 namespace bz {
@@ -70,6 +72,12 @@ constexpr int kUmmaM = 128;       // prefixes per A tile = producer threads
 #endif
 #ifndef BZ_K5Q_SPLIT
 #define BZ_K5Q_SPLIT 1  // K5q: accumulator column halves with their own barriers
+#endif
+#ifndef BZ_K5_LEAN
+#define BZ_K5_LEAN 1  // K5q / K5f epilogue: the lean tile loop (0: the general one)
+#endif
+#ifndef BZ_K5F_SPLIT
+#define BZ_K5F_SPLIT 1  // K5f: accumulator column halves with their own barriers
 #endif
 #ifndef BZ_K5_EPI_GROUPS
 #define BZ_K5_EPI_GROUPS 1
@@ -139,7 +147,8 @@ struct K4Roles {
   // column parts of each accumulator with their own full/empty barriers:
   // the epilogue drains part 0 while the MMAs of part 1 still run, and the
   // next tile's part-0 MMAs start as soon as part 0 is drained
-  static constexpr int SPLIT = CW == 4 ? BZ_K5Q_SPLIT : (CW > 1 ? 1 : (F4 ? BZ_K5_SPLIT : 1));
+  static constexpr int SPLIT =
+      CW == 4 ? BZ_K5Q_SPLIT : CW == 6 ? BZ_K5F_SPLIT : (CW > 1 ? 1 : (F4 ? BZ_K5_SPLIT : 1));
   // epilogue groups: group q drains the tiles t with t % EGRP == q (each
   // group covers the whole accumulator), so a group has EGRP tile periods
   // for its loads and reductions while the other groups take the tiles in
@@ -157,22 +166,24 @@ template <bool F4, int CW = 1> __host__ __device__ constexpr int k4_n() {
 // bytes per table (B) row: K4 one byte per column, K5 one nibble
 // K5 with the padding-chunk offset (odd W): tables carry the pad chunk
 __host__ __device__ constexpr bool k5_padmagic(int w) { return kK5Magic && (w & 1); }
-template <bool F4> __host__ __device__ constexpr int k4_row_bytes(int w) {
-  return F4 ? 16 * (k5_padmagic(w) ? w + 1 : w) : 32 * w;
+// (K5f, form 6: W chunks, the last one half data, half offset pattern)
+template <bool F4> __host__ __device__ constexpr int k4_row_bytes(int w, int cw = 1) {
+  return F4 ? 16 * (cw != 6 && k5_padmagic(w) ? w + 1 : w) : 32 * w;
 }
 // 16-byte K chunks per A row (K5 pads to whole K = 64 MMAs; K5p / K5t with
 // CW codewords per accumulator column carry CW offset chunks after the W
 // data chunks)
 // codewords per accumulator column of kernel form CW (1 = K5, 2 = K5p,
 // 3 = K5t, 4 = K5q: two codewords as bytes, 5 = K5w: two codewords as 11-bit
-// fields, for wide rows)
-__host__ __device__ constexpr int k5_ncw(int cw) { return (cw == 4 || cw == 5) ? 2 : cw; }
+// fields, for wide rows, 6 = K5f: K5q's bytes from folded MMAs, see k5f_ok)
+__host__ __device__ constexpr int k5_ncw(int cw) { return (cw >= 4 && cw <= 6) ? 2 : cw; }
 // K5w A row: the data chunks padded to whole K = 64 MMAs (a zero chunk for
 // odd W meets the table's offset chunk), then the offset chunks R, Ca, Cb
 __host__ __device__ constexpr int k5w_data_chunks(int w) { return 2 * ((w + 1) / 2); }
 template <bool F4, int CW = 1> __host__ __device__ constexpr int k4_a_chunks(int w) {
   return CW == 5 ? k5w_data_chunks(w) + 3
-                 : (CW > 1 ? w + k5_ncw(CW) : (F4 ? 2 * ((w + 1) / 2) : 2 * w));
+         : CW == 6 ? w + 1  // K5f: W - 1 whole chunks, then the tail chunk once per part
+                   : (CW > 1 ? w + k5_ncw(CW) : (F4 ? 2 * ((w + 1) / 2) : 2 * w));
 }
 // MMAs per tile (per half for K5p)
 template <bool F4> __host__ __device__ constexpr int k4_passes(int w) { return k4_a_chunks<F4>(w) / 2; }
@@ -181,7 +192,7 @@ template <bool F4, int CW = 1> __host__ __device__ constexpr int k4_tile_rows() 
   return k5_ncw(CW) * k4_n<F4, CW>();
 }
 template <bool F4, int CW = 1> __host__ __device__ constexpr uint32_t k4_tile_b(int w) {
-  return (uint32_t)(k4_tile_rows<F4, CW>() * k4_row_bytes<F4>(w));
+  return (uint32_t)(k4_tile_rows<F4, CW>() * k4_row_bytes<F4>(w, CW));
 }
 template <bool F4, int CW = 1> __host__ __device__ constexpr uint32_t k4_tile_a(int w) {
   return (uint32_t)(kUmmaM * 16 * k4_a_chunks<F4, CW>(w));
@@ -276,6 +287,52 @@ __host__ __device__ __forceinline__ uint4 pad_chunk(int T0, int T1) {
   return make_uint4((uint32_t)b0, (uint32_t)(b0 >> 32), (uint32_t)b1, (uint32_t)(b1 >> 32));
 }
 __host__ __device__ __forceinline__ uint4 k5p_offset_chunk(int T) { return pad_chunk(T, 0); }
+
+// K5f (form 6): K5q's byte fields from fewer MMAs, for odd W whose last
+// stored word holds at most 16 columns (stored columns <= 32 (W - 1) + 16:
+// config 5's 80).  The last K chunk of a row is then half free: its 16 data
+// columns move to block 0 (k5f_spread + the usual nibble order) and block 1
+// carries offsets, so both parts' tails fit ONE K = 64 MMA whose B descriptor
+// steps from table row c to row N + c (LBO = (N / 8) SBO):
+//   table row, last chunk   [ data16 | offset pattern (8 x 4.0, 8 x 1.0) ]
+//   A row, chunk W - 1 (ta) [ data16 | 4.0 on the pattern's 4.0s: 128    ]
+//   A row, chunk W     (tb) [ data16 | e2m1_block(X), X = wt + 128 - thr ]
+//   ue4m3 block scales      A (1, 256, 1, 1) x B (1, 256, 256, 256)
+//   = d_a(tail) + 2^23 + 256 d_b(tail) + 256 X.
+// With the whole chunks' MMAs (part b with B scale 256) an accumulator is
+// 2^23 + d_a + 256 x_b, d = w(P ^ S) - w(P), x = w(P ^ S) + 128 - thr: part
+// b's byte is K5q's, part a's lacks its X -- three offset classes (X, 256 X,
+// 2^23) do not fit the two free blocks -- and the epilogue adds X to both
+// 16-bit halves of every packed register (one IADD per four codewords), after
+// which the registers equal K5q's bit for bit.  thr <= 127 keeps x_b >= 1, so
+// a half d_a + 256 x_b is never negative and the add never carries across
+// halves.  MMAs per tile at W = 3: 3 (96 MACs per codeword) against K5q's 4,
+// table rows 48 B against 64.
+__host__ __device__ constexpr bool k5f_ok(int w, int n_eff) {
+  return (w == 1 || w == 3) && n_eff <= 32 * (w - 1) + 16;
+}
+// bit pair i (bits 2i, 2i + 1) of the low 16 bits -> bits 4i, 4i + 1: the
+// elements e2m1_bits01 / e2m1_pm1 put into words x and y (block 0)
+__host__ __device__ __forceinline__ uint32_t k5f_spread(uint32_t v) {
+  v = (v | (v << 8)) & 0x00FF00FFu;
+  v = (v | (v << 4)) & 0x0F0F0F0Fu;
+  return (v | (v << 2)) & 0x33333333u;
+}
+__host__ __device__ __forceinline__ int k5f_threshold(int wt, int rel) {
+  return max(wt - kQMaxSpan, max(1, min(127, rel)));
+}
+// table row, last chunk (tail word v: its low 16 bits are columns)
+__host__ __device__ __forceinline__ uint4 k5f_table_tail(uint32_t v) {
+  const uint4 d = e2m1_bits01(k5f_spread(v));
+  return make_uint4(d.x, d.y, 0x66666666u, 0x22222222u);
+}
+// A row, chunks ta (part 0) and tb (part 1) of tail word v and offset x
+__host__ __device__ __forceinline__ uint4 k5f_a_tail(uint32_t v, int part, int x) {
+  const uint4 d = e2m1_pm1(k5f_spread(v));
+  if (part == 0) return make_uint4(d.x, d.y, 0x66666666u, 0u);
+  const unsigned long long b = e2m1_block(x);
+  return make_uint4(d.x, d.y, (uint32_t)b, (uint32_t)(b >> 32));
+}
 
 // K5w (wide rows, two codewords per accumulator column as 11-bit fields):
 //   acc = 2^23 + x_a + 2^11 x_b,  x = w(P ^ S) + 1024 - thr  in [0, 2047],
@@ -645,13 +702,14 @@ struct K4Tables {
 #endif
 constexpr int kBuildRows = BZ_BUILD_ROWS;  // suffix-table rows per builder thread (divides 8)
 
-template <int W>
+template <int W, int FORM = 1>
 __global__ void k_build_subsets_mxf4(const uint32_t* __restrict__ rows,
                                      uint8_t* __restrict__ out, int k, int D,
                                      unsigned long long nrows, size_t gamma_stride_rows,
                                      const unsigned long long* __restrict__ binom) {
   constexpr int WP = padded_words(W);
-  constexpr int C = k4_row_bytes<true>(W) / 16;  // chunks per row (+ offset chunk)
+  constexpr int C = k4_row_bytes<true>(W, FORM) / 16;  // chunks per row (+ offset chunk)
+  constexpr bool FD = FORM == 6;  // K5f rows: the last chunk half data, half offset pattern
   // binomials C(x, 0..5) for x <= k in shared memory (the one unrank per
   // thread is a binary search over them)
   __shared__ unsigned long long sbt[kBinomDim * 6];
@@ -702,6 +760,7 @@ __global__ void k_build_subsets_mxf4(const uint32_t* __restrict__ rows,
 #pragma unroll
       for (int w = 0; w < W; ++w) *reinterpret_cast<uint4*>(dst + w * 128) = make_uint4(0u, 0u, 0u, 0u);
       if constexpr (C > W) *reinterpret_cast<uint4*>(dst + W * 128) = k5_table_offset_chunk();
+      if constexpr (FD) *reinterpret_cast<uint4*>(dst + (W - 1) * 128) = k5f_table_tail(0u);
       continue;
     }
     uint32_t v[W];
@@ -711,7 +770,9 @@ __global__ void k_build_subsets_mxf4(const uint32_t* __restrict__ rows,
 #pragma unroll
       for (int w = 0; w < W; ++w) v[w] ^= R[e[i] * WP + w];
 #pragma unroll
-    for (int w = 0; w < W; ++w) *reinterpret_cast<uint4*>(dst + w * 128) = e2m1_bits01(v[w]);
+    for (int w = 0; w < (FD ? W - 1 : W); ++w)
+      *reinterpret_cast<uint4*>(dst + w * 128) = e2m1_bits01(v[w]);
+    if constexpr (FD) *reinterpret_cast<uint4*>(dst + (W - 1) * 128) = k5f_table_tail(v[W - 1]);
     if constexpr (C > W)  // offset chunk
       *reinterpret_cast<uint4*>(dst + W * 128) = k5_table_offset_chunk();
     // successor in table order: the next (D-1)-subset of [a+1, k) in lex
@@ -787,6 +848,9 @@ __device__ __forceinline__ void k4_trace_chunk(const RoundArgs& a, uint32_t& tof
 }
 #ifndef BZ_K4_TRACE
 #define BZ_K4_TRACE 0  // build with -DBZ_K4_TRACE=1 for the BZ_K4_DEBUG & 8 timeline
+#endif
+#ifndef BZ_K4_TRACE_WARP
+#define BZ_K4_TRACE_WARP -1  // second traced epilogue warp (slots 7, 14); default the last
 #endif
 __device__ __forceinline__ void k4_trace(const RoundArgs& a, int slot, uint32_t tile,
                                          uint32_t toff) {
@@ -876,6 +940,56 @@ __device__ __forceinline__ int k5w_scan(uint32_t* v, int c0, int la, int lb, int
   return mn;
 }
 
+// K5f epilogue: NPH packed registers = 2 NPH accumulator columns (low 16 bits
+// each: d_a + 256 x_b) of one row.  Adds the row offset X to both halves of
+// every register (x * 0x10001 + v: one IMAD on the FMA pipe, which the rest of
+// the epilogue leaves idle, interleaved with the AND pass on the ALU pipe),
+// after which the registers are K5q's: bytes x = w + 128 - thr, and a
+// codeword can lower the bound iff bit 7 of its byte is clear.  Columns at or
+// past la (part a) / lb (part b), relative to the first, are masked.  Returns
+// the smallest byte below lx (and lowers lx to it), else INT_MAX.
+template <int NPH, bool ADD = true>
+__device__ __forceinline__ int k5f_scan(uint32_t* v, uint32_t xoff, int la, int lb, int& lx) {
+  static_assert(NPH % 2 == 0, "register pairs");
+  uint32_t acc = 0xFFFFFFFFu;
+#pragma unroll
+  for (int i = 0; i < NPH; i += 2) {
+    if constexpr (ADD) {  // (K5q's registers carry X already)
+      v[i] += xoff * 0x00010001u;
+      v[i + 1] += xoff * 0x00010001u;
+    }
+    acc &= v[i] & v[i + 1];
+  }
+  if (lb < 2 * NPH) {  // uniform: a slice's last tile
+#pragma unroll
+    for (int i = 0; i < NPH; ++i) {
+      if (2 * i >= la) v[i] |= 0x000000FFu;
+      if (2 * i >= lb) v[i] |= 0x0000FF00u;
+      if (2 * i + 1 >= la) v[i] |= 0x00FF0000u;
+      if (2 * i + 1 >= lb) v[i] |= 0xFF000000u;
+    }
+    acc = 0xFFFFFFFFu;
+#pragma unroll
+    for (int i = 0; i < NPH; i += 2) acc &= v[i] & v[i + 1];
+  }
+  if (__builtin_expect(!((~acc) & 0x80808080u), 1)) return INT_MAX;
+  // some byte is below the producer's threshold; below this row's own
+  // minimum so far?  ((x - lx * 0x01010101) & ~x has bit 7 of the lowest
+  // such byte set, lx <= 128)
+  const uint32_t kx = (uint32_t)lx * 0x01010101u;
+  uint32_t h = 0;
+#pragma unroll
+  for (int i = 0; i < NPH; ++i) h |= (v[i] - kx) & ~v[i];
+  if (!(h & 0x80808080u)) return INT_MAX;
+  int mn = lx;
+#pragma unroll
+  for (int i = 0; i < NPH; ++i)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) mn = min(mn, (int)((v[i] >> (8 * b)) & 0xFFu));
+  lx = mn;
+  return mn;
+}
+
 // K4 (F4 = false, tcgen05.mma kind::i8) and K5 (F4 = true, kind::mxf4 with
 // unit block scales): one persistent CTA per SM, warp-specialised (see the
 // file comment).  The two differ only in operand encoding, MMA kind,
@@ -887,12 +1001,13 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
   // table, m, k, n, binomials, the chunk cursor, debug and trace switches)
   const RoundArgs& a = bt.a[0];
   constexpr bool PR = CW > 1;  // K5p (CW = 2) / K5t (CW = 3) / K5q (CW = 4)
-  constexpr bool Q = CW == 4;  // K5q: two codewords as bytes, block16 scales
+  constexpr bool FD = CW == 6;  // K5f: K5q's bytes from folded MMAs (k5f_ok)
+  constexpr bool Q = CW == 4 || FD;  // K5q: two codewords as bytes, block16 scales
   constexpr bool WQ = CW == 5;  // K5w: two codewords as 11-bit fields (wide rows)
   constexpr bool QQ = Q || WQ;  // threshold-offset forms (bit test, bound cache)
   constexpr int NC = k5_ncw(CW);  // codewords per accumulator column
   static_assert(!F4 || kUmmaMA == 1, "K5 runs one A tile per B tile");
-  static_assert(CW >= 1 && CW <= 5, "kernel form");
+  static_assert(CW >= 1 && CW <= 6, "kernel form");
   // offset accumulators (packed s16 epilogue) for this instantiation
   constexpr bool MG = kK5Magic && (CW > 1 || (W & 1) || !BZ_K5_EVEN_F32);
   static_assert(!PR || (F4 && kK5Magic && (Q || BZ_K5_SPLIT == 1) &&
@@ -904,12 +1019,13 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
   constexpr int S = k4_stages<F4, CW>(W);
   constexpr int P = k4_passes<F4>(W);        // MMAs per tile (K5p: per half)
   constexpr int CA = k4_a_chunks<F4, CW>(W); // 16-byte K chunks per A row
-  constexpr int CB = k4_row_bytes<F4>(W) / 16;  // ... per B row
+  constexpr int CB = k4_row_bytes<F4>(W, CW) / 16;  // ... per B row
   constexpr uint32_t TB = k4_tile_b<F4, CW>(W);
   constexpr uint32_t TA = k4_tile_a<F4, CW>(W);
   using RL = K4Roles<F4, CW>;
   constexpr int ACC = RL::ACC;
   constexpr int E = RL::E;
+  constexpr int TW = (BZ_K4_TRACE_WARP >= 0 && BZ_K4_TRACE_WARP < E) ? BZ_K4_TRACE_WARP : E - 1;
   constexpr int EGRP = RL::EGRP;
   constexpr int EC = N / (RL::EW / 4);  // columns per epilogue warp and A tile
   constexpr int SPLIT = RL::SPLIT;
@@ -1015,6 +1131,10 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
                        : c == 8 ? 0x8A8A8A8Au                           // 2^11: part b
                        : kSfCol + c == kSfColMagic ? 0x7F7F947Fu        // (1, 2^21): part a offset
                                                    : 0x7F7F898Au)       // (2^11, 2^10): part b
+                 : FD ? (kSfCol + c == kSfColMagic ? 0x78787878u  // ue4m3 256: part b
+                       : kSfCol + c == kSfColPad ? 0x38387838u   // A tail: (1, 256, 1, 1)
+                       : c == 8 ? 0x78787838u                    // B tail: (1, 256, 256, 256)
+                                : 0x38383838u)                   // ue4m3 1.0
                  : Q ? (kSfCol + c == kSfColMagic ? 0x78787878u   // ue4m3 256: half b
                       : kSfCol + c == kSfColPad ? 0x78383838u  // A: 256 on block 3
                                                 : 0x38383838u) // ue4m3 1.0
@@ -1120,6 +1240,59 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
         float fmin_acc = __int_as_float(0x7f800000);  // K5: +inf
         int lx = 128;  // K5q: this row's bytes below lx can still lower its minimum
         int lx1024 = 1024;  // K5w: this row's fields below lx1024 can still lower it
+        // K5q / K5f: the step's tiles in a lean loop -- the tile loop below
+        // with the debug switches, trace points and per-tile address
+        // arithmetic hoisted and the two accumulator buffers unrolled (the
+        // epilogue warps of a scheduler share its issue slots, and per-tile
+        // bookkeeping was most of what they issued)
+        bool lean = false;
+        if constexpr (Q && SPLIT == 1 && EGRP == 1 && ACC == 2 && kUmmaMA == 1 && !BZ_K4_TRACE &&
+                      BZ_K5_LEAN) {
+          if (!a.debug) {
+            lean = true;
+            constexpr int NP = EC / 2;
+            const uint32_t tq = tmem + ((uint32_t)(32 * quarter) << 16) + (uint32_t)(EC * slice_id);
+            const bool l0 = lane == 0;
+            const int thr = FD ? (wt[0] & 0xFFFF) : wt[0];
+            const uint32_t xoff = FD ? (uint32_t)(wt[0] >> 16) : 0u;
+            int la = c.slice - c.tile_lo * TR - EC * slice_id;  // part-a columns < la valid
+            auto tile = [&](auto bufc) {
+              constexpr int BUF = decltype(bufc)::value;
+              mbar_wait_fast(accfull(BUF), (tcount >> 1) & 1);
+              tc_fence_after();
+              uint32_t v[NP];
+              tmem_ld_cols_p<EC>(tq + (uint32_t)(BUF * N), v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i + 1 < NP; i += 2) asm volatile("" : "+r"(v[i]), "+r"(v[i + 1]) : : "memory");
+              tc_fence_before();
+              __syncwarp();
+              if (l0) mbar_arrive(accempty(BUF));  // the accumulator is in registers
+              const int mn = k5f_scan<NP, FD>(v, xoff, la, la - N, lx);
+              if (mn != INT_MAX) {
+                const int w = mn - 128 + thr;
+                rmin[0] = min(rmin[0], w);
+                const int w2 = w + gamma_woff(ar, c.gr.gamma);
+                // publish at once (the producers' next thresholds tighten),
+                // only below the CTA's cached bound
+                if (w2 < bnd_cache_read(s_bnd, rr, c.gr.gamma)) bnd_publish(s_bnd, ar, rr, c.gr.gamma, w2);
+              }
+              ++tcount;
+              la -= TR;
+            };
+            int nt = c.tile_hi - c.tile_lo;
+            if (nt > 0 && (tcount & 1)) {
+              tile(std::integral_constant<int, 1>{});
+              --nt;
+            }
+            for (; nt >= 2; nt -= 2) {
+              tile(std::integral_constant<int, 0>{});
+              tile(std::integral_constant<int, 1>{});
+            }
+            if (nt) tile(std::integral_constant<int, 0>{});
+          }
+        }
+        if (!lean)
         for (int t = c.tile_lo; t < c.tile_hi; ++t, ++tcount) {
           if (EGRP > 1 && (int)(tcount % EGRP) != egroup) continue;
           const int buf = tcount % ACC;
@@ -1129,7 +1302,7 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
           if (warp == 0 && lane == 0) k4_trace(a, 9, tcount, toff);
           if (!BZ_K5_NOFENCE) tc_fence_after();
           if (warp == 0 && lane == 0) k4_trace(a, 2, tcount, toff);
-          if (warp == E - 1 && lane == 0) k4_trace(a, 7, tcount, toff);
+          if (warp == TW && lane == 0) k4_trace(a, 7, tcount, toff);
           const int lim = min(N, c.slice - t * TR) - EC * slice_id;
           const uint32_t tb = tmem + ((uint32_t)(32 * quarter) << 16) +
                               (uint32_t)(buf * kUmmaMA * N + EC * slice_id);
@@ -1152,9 +1325,23 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
 #pragma unroll
             for (int i = 0; i + 1 < NP; i += 2) asm volatile("" : "+r"(v[i]), "+r"(v[i + 1]) : : "memory");
             if (NP % 2) asm volatile("" : "+r"(v[NP - 1]) : : "memory");
+            if (warp == 0 && lane == 0) k4_trace(a, 10, tcount, toff);
             if (!BZ_K5_NOFENCE) tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(accempty(hb));  // accumulators are in registers
+            if (warp == 0 && lane == 0) k4_trace(a, 11, tcount, toff);
+            if (warp == TW && lane == 0) k4_trace(a, 14, tcount, toff);
+            if (a.debug & 64) continue;  // timing experiment: loads only
+            if constexpr (FD) {
+              const int mn = k5f_scan<NP>(v, (uint32_t)(wt[0] >> 16), la, la - N, lx);
+              if (mn != INT_MAX) {
+                const int w = mn - 128 + (wt[0] & 0xFFFF);
+                rmin[0] = min(rmin[0], w);
+                const int w2 = w + gamma_woff(ar, c.gr.gamma);
+                if (w2 < bnd_cache_read(s_bnd, rr, c.gr.gamma)) bnd_publish(s_bnd, ar, rr, c.gr.gamma, w2);
+              }
+              continue;
+            }
             if (la - N < EC) {
 #pragma unroll
               for (int i = 0; i < NP; ++i) {
@@ -1322,7 +1509,7 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
             __syncwarp();
             if (lane == 0) mbar_arrive(accempty(hb));  // accumulators are in registers
             if (warp == 0 && lane == 0) k4_trace(a, 11, tcount, toff);
-            if (warp == E - 1 && lane == 0) k4_trace(a, 14, tcount, toff);
+            if (warp == TW && lane == 0) k4_trace(a, 14, tcount, toff);
             if (lim < EC) {
 #pragma unroll
               for (int i = 0; i < NP; ++i) {
@@ -1356,7 +1543,7 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
             __syncwarp();
             if (lane == 0) mbar_arrive(accempty(hb));  // accumulators are in registers
             if (warp == 0 && lane == 0) k4_trace(a, 11, tcount, toff);
-            if (warp == E - 1 && lane == 0) k4_trace(a, 14, tcount, toff);
+            if (warp == TW && lane == 0) k4_trace(a, 14, tcount, toff);
             if (lim < EC) {
 #pragma unroll
               for (int i = 0; i < EC; ++i)
@@ -1479,7 +1666,10 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
           for (int jj = 0; jj < W; ++jj) {
             const uint32_t v = wk.acc[jj];
             wt += __popc(v);
-            if constexpr (F4) {
+            if constexpr (FD) {
+              // (the tail word's chunks ta / tb follow with the offsets)
+              if (jj < W - 1) *reinterpret_cast<uint4*>(dst + umma_off_c(r, jj, CA)) = e2m1_pm1(v);
+            } else if constexpr (F4) {
               // e2m1 +1 (0x2) for a 0 bit, -1 (0xA) for a 1 bit
               *reinterpret_cast<uint4*>(dst + umma_off_c(r, jj, CA)) = e2m1_pm1(v);
             } else {
@@ -1509,11 +1699,21 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
             // first tiles down the exact path).
             int ub = min(((volatile int*)ar.bound)[1 + c.gr.gamma], bnd_cache_read(s_bnd, rr, c.gr.gamma));
             for (int q = 0; q < rr; ++q) ub = min(ub, ((volatile const int*)bt.a[q].bound)[0]);
+            if constexpr (FD) {
+              // K5f: the tail word once per part, ta with the 2^23 block, tb
+              // with X; the epilogue adds X to part a's bytes (thr | X << 16)
+              const int thr = k5f_threshold(wt, ub - gamma_woff(ar, c.gr.gamma));
+              const int x = wt + 128 - thr;
+              *reinterpret_cast<uint4*>(dst + umma_off_c(r, W - 1, CA)) = k5f_a_tail(wk.acc[W - 1], 0, x);
+              *reinterpret_cast<uint4*>(dst + umma_off_c(r, W, CA)) = k5f_a_tail(wk.acc[W - 1], 1, x);
+              wt = thr | (x << 16);
+            } else {
             const int thr = k5q_threshold(wt, ub - gamma_woff(ar, c.gr.gamma));
             const int x = wt + 128 - thr;
             *reinterpret_cast<uint4*>(dst + umma_off_c(r, W, CA)) = pad_chunk(x, 0);
             *reinterpret_cast<uint4*>(dst + umma_off_c(r, W + 1, CA)) = pad_chunk(x, 128);
             wt = thr;  // the epilogue needs thr to turn a byte back into a weight
+            }
           } else if constexpr (WQ) {
             // K5w: chunk R = w(P) - thr, so both 11-bit fields read
             // x = w(P ^ S) + 1024 - thr (k5w_threshold keeps |R| <= 450)
@@ -1564,6 +1764,8 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
     {
       const uint64_t a_desc0 = umma_desc(sA_s, 128, CA * 128);
       const uint64_t b_desc0 = umma_desc(sB_s, 128, CB * 128);
+      const uint64_t b_fold0 = umma_desc(sB_s, (N / 8) * CB * 128, CB * 128);  // K5f tail fold
+      (void)b_fold0;
       const uint32_t sfa = tmem + kSfCol, sfb = tmem + kSfCol + 8, sfm = tmem + kSfColMagic;
       const uint32_t sfp = tmem + kSfColPad;
       // magic operands: one core matrix per K chunk, SBO = 0 (every 8-row
@@ -1640,6 +1842,23 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
                       umma_mxf4(dj, adj + 8u * WD + ((uint64_t)(8 * q) << 16), magic_b, IDESC, 1u,
                                 q ? sfp : sfm, sf1);
                     }
+                  } else if constexpr (FD) {
+                    // K5f: the whole chunks per part (part b with B scale
+                    // 256), then both parts' tails in one MMA: A chunks (ta,
+                    // tb), B the last chunk of table rows c and N + c (LBO =
+                    // N / 8 row groups)
+                    constexpr int F2 = (W - 1) / 2;
+#pragma unroll
+                    for (int q = 0; q < 2; ++q) {
+                      const uint64_t bdq = bd0 + (uint64_t)(q * (N / 8) * CB * 8);
+#pragma unroll
+                      for (int kb = 0; kb < F2; ++kb)
+                        umma_nvf4(dj, adj + 16u * kb, bdq + 16u * kb, IDESC, (q | kb) ? 1u : 0u,
+                                  sfa, q ? sfm : sfa);
+                    }
+                    const uint64_t bfold = b_fold0 + (uint64_t)(stg * (TB >> 4)) + 8u * (W - 1) +
+                                           (uint64_t)(h * (NH / 8) * CB * 8);
+                    umma_nvf4(dj, adj + 8u * (W - 1), bfold, IDESC, F2 ? 1u : 0u, sfp, sfb);
                   } else if constexpr (Q && !(W & 1)) {
                     // K5q, even W: W/2 data MMAs per part, then one offset MMA
                     // of A chunks (pad_a, pad_b) against a constant B

@@ -38,7 +38,7 @@ def test_header_symbols_exported():
 
 
 @pytest.mark.parametrize("engine", ["auto", "popc", "imma", "umma", "mxf4", "mxf4p", "mxf4t", "mxf4q",
-                                    "mxf4w"])
+                                    "mxf4w", "mxf4f"])
 def test_plan_counts(engine):
     for (m, k, g) in [(1, 5, 1), (2, 24, 3), (2, 80, 8), (3, 40, 8), (1, 64, 6), (2, 128, 4)]:
         groups, nchunks = _native.plan(m, k, g, engine)
@@ -52,7 +52,7 @@ def test_plan_counts(engine):
             assert sl in (1, 2, 4, 8, 16, 32) and (depth < 3 or sl == 1)
             assert lanes == ({"imma": 256}.get(engine, 128) if depth >= 3 else 32)
             want = 3 if (engine != "popc" and g >= 4) else (2 if g >= 4 else 1)
-            if engine in ("auto", "mxf4", "mxf4p", "mxf4t", "mxf4q", "mxf4w") and g >= 4:
+            if engine in ("auto", "mxf4", "mxf4p", "mxf4t", "mxf4q", "mxf4w", "mxf4f") and g >= 4:
                 # K5 suffix levels: depth 3..5, floors above ell + 1
                 assert 3 <= depth <= min(5, g - 1) and sfloor >= ell + 1
             else:
@@ -62,7 +62,7 @@ def test_plan_counts(engine):
 
 
 @pytest.mark.parametrize("engine", ["auto", "popc", "imma", "umma", "mxf4", "mxf4p", "mxf4t", "mxf4q",
-                                    "mxf4w"])
+                                    "mxf4w", "mxf4f"])
 @pytest.mark.parametrize("m,k,g", [(1, 6, 1), (1, 7, 2), (2, 9, 3), (1, 12, 5),
                                    (2, 10, 10), (1, 40, 3), (1, 34, 4), (1, 20, 6)])
 def test_plan_partitions_rank_space(m, k, g, engine):
@@ -127,7 +127,7 @@ def test_plan_levels_partition(monkeypatch, m, k, g, floors):
     groups, _ = _native.plan(m, k, g, "mxf4")
     assert max(collections.Counter(int(gr[6]) for gr in groups)) > 3  # deeper levels in use
     for engine, nshards in (("mxf4", 1), ("mxf4", 3), ("mxf4p", 1), ("mxf4p", 3), ("mxf4t", 3), ("mxf4q", 3),
-                            ("mxf4w", 2)):
+                            ("mxf4w", 2), ("mxf4f", 2)):
         groups, nchunks = _native.plan(m, k, g, engine, nshards)
         seen = []
         for s in range(nshards):

@@ -21,7 +21,7 @@ import pytest
 from oracle import oracle
 from paper_1603_06757_b200 import _native
 
-ENGINES = ("popc", "mxf4", "mxf4q", "mxf4w")
+ENGINES = ("popc", "mxf4", "mxf4q", "mxf4w", "mxf4f")
 
 
 def _plan(m, k, g, engine, nshards=1):

@@ -31,7 +31,7 @@ def _random_codes(count: int, seed: int):
     return out
 
 
-@pytest.mark.parametrize("engine", ["auto", "popc", "mxf4", "mxf4q", "mxf4w"])
+@pytest.mark.parametrize("engine", ["auto", "popc", "mxf4", "mxf4q", "mxf4w", "mxf4f"])
 def test_random_codes_match_brute_force(engine):
     """500 random codes (k <= 14, sparse / balanced / dense rows): the GPU
     distance equals the brute force over all 2^k - 1 messages, the status

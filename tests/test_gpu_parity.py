@@ -27,12 +27,14 @@ def ctx():
     return _native.context(0)
 
 
-@pytest.fixture(params=["popc", "mxf4", "mxf4q", "mxf4w"])
+@pytest.fixture(params=["popc", "mxf4", "mxf4q", "mxf4w", "mxf4f"])
 def engine(request):
     """Every kernel of the library: K1 (XOR+POPC), K5 (tcgen05 kind::mxf4,
     g >= 4), K5q (kind::mxf4nvf4, two codewords per accumulator as bytes;
     W <= 4 and <= 128 stored columns -- other shapes run K5) and K5w
-    (kind::mxf4, two codewords as 11-bit fields; W >= 2)."""
+    (kind::mxf4, two codewords as 11-bit fields; W >= 2); K5f (K5q's bytes from
+    folded MMAs, odd W <= 3 whose last stored word holds <= 16 columns -- other
+    shapes run K5q / K5)."""
     _native.context(0).set_engine(request.param)
     yield request.param
     _native.context(0).set_engine("auto")
@@ -273,8 +275,8 @@ def test_early_exit_all_engines(ctx, engine):
 
 @pytest.mark.parametrize("k,g,floors", [(12, 6, "4,7"), (14, 8, "5,9"), (12, 5, "6"),
                                         (20, 7, "8,13"), (11, 9, "0,3")])
-@pytest.mark.parametrize("n", [20, 37, 70, 96, 160, 230])
-@pytest.mark.parametrize("kernel", ["mxf4", "mxf4q", "mxf4w"])
+@pytest.mark.parametrize("n", [20, 37, 70, 88, 96, 160, 230])
+@pytest.mark.parametrize("kernel", ["mxf4", "mxf4q", "mxf4w", "mxf4f"])
 def test_mxf4_levels(monkeypatch, ctx, k, g, floors, n, kernel):
     """K5 / K5p with forced suffix levels (depth-4/5 tables): exact minima and
     combination counts per Gamma against the oracle (K5p runs at n = 20, 70,

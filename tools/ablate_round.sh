@@ -11,11 +11,13 @@ from paper_1603_06757_b200.configs import code
 from paper_1603_06757_b200.enumeration import family_words
 G, gs, _ = code("cfg5", 7)
 ctx = _native.context(0)
+import os
+ctx.set_engine(os.environ.get("ENGINE", "auto"))
 ctx.load(family_words(gs.gammas, 160), 160)
 ms = []
 for i in range(4):
     ctx.round(8, -1, 18)
     if i: ms.append(ctx.last_kernel_ms())
-print(f"debug {sys.argv[1]:>3}: g=8 {sorted(ms)[1]:.3f} ms")
+print(f"{os.environ.get('ENGINE', 'auto')} debug {sys.argv[1]:>3}: g=8 {sorted(ms)[1]:.3f} ms")
 PY
 done
