@@ -476,7 +476,8 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
           // histogram: SMs active 59 % of the launch).  Spread such
           // prefixes' first suffix rows over lanes until a lane's share is
           // near an even split of the round over 16 warps per SM (swept
-          // 2..512: config-4 histogram 191 -> 127 us, its K1 minimum 156 ->
+          // 2..512, and again 16..128 with K1h at 32 warps per SM: flat to
+          // 32, slower beyond: config-4 histogram 191 -> 127 us, its K1 minimum 156 ->
           // 101 us, config 5's g = 5 on K1 184 -> 65 us).
           if (depth == 2) {
             const long long even = (long long)(total / (32ull * 148ull * 16ull));
@@ -620,19 +621,23 @@ template <int W, int D>
 int launch_wd(bz_ctx* ctx, const RoundArgs& a0, bool hist) {
   RoundArgs a = a0;
   size_t smem = bz::smem_base_bytes<W>(a.m, a.k, a.ngroups);
-  if (smem + (hist ? (size_t)(a.n + 1) * 6 * 32 + 16 : 0) > kMaxSmem) {
+  if (smem + (hist ? (size_t)bz::k1h_bins<W>(a.n) * 4 + (size_t)(bz::kK1hWindow + 1) * 2 * bz::kK1hMinThreads + 32 : 0) > kMaxSmem) {
     a.groups_global = 1;  // a plan too large to stage: read from global memory
     smem = bz::smem_base_bytes<W>(a.m, a.k, 0);
   }
   int threads = 256;
   if (hist) {
-    smem = ((smem + 15) & ~size_t(15)) + (size_t)(a.n + 1) * 4;
-    // per-thread u16 histogram columns
+    // bins for the stored weights only (at most 32 W stored columns: the
+    // dropped identity weight is added when the block's bins are flushed)
+    const size_t nbins = (size_t)bz::k1h_bins<W>(a.n);
+    smem = ((smem + 15) & ~size_t(15)) + ((nbins + 3) & ~size_t(3)) * 4;
+    // per-thread 16-bit counters over the window
     int dev_max = 0;
     CK(cudaDeviceGetAttribute(&dev_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-    while (threads > 32 && smem + (size_t)(a.n + 1) * threads * 2 > (size_t)dev_max / 2)
+    const size_t win = (size_t)bz::k1h_window((int)nbins);
+    while (threads > bz::kK1hMinThreads && smem + (win + 1) * threads * 2 > (size_t)dev_max / 2)
       threads /= 2;
-    smem += (size_t)(a.n + 1) * threads * 2;
+    smem += (win + 1) * threads * 2;  // + the trash row
   }
   int per_sm = 0;
   const void* fn = hist ? (const void*)bz::k1h_histogram<W, D> : (const void*)bz::k1_round_min<W, D>;

@@ -841,44 +841,103 @@ __global__ void __launch_bounds__(128) k_seed_bound(const RoundArgs a, int gamma
 
 // ---------------------------------------------------------------------------
 // K1h: weight histogram of one (Gamma, g) pass.  Each thread owns a private
-// u16 histogram column in shared memory (layout [bin][thread]: conflict-free
-// for any bin pattern), flushed into a block-wide u32 histogram before it
-// can overflow, and finally into the global u64 bins.  Same two-walker
-// structure as K1; on an odd range the second walker's last step is masked.
+// 16-bit counter per bin of a WINDOW of kK1hWindow weights in shared memory,
+// flushed into a block-wide u32 histogram (all bins) before it can overflow,
+// and finally into the global u64 bins; a weight outside the window goes to
+// the block histogram directly.  The window is centred on the weight a sum of
+// g rows of this density would have if the rows were random
+// (n/2 (1 - (1 - 2p)^g), p from the staged rows), computed alike by every
+// block; it only steers which path a codeword takes -- any placement gives
+// the same bins -- and on the codes of BASELINE's configs a codeword leaves
+// it about once in 1e7.  64 instead of n + 1 private bins per thread is what
+// lets 4 blocks (32 warps) share an SM instead of 2.
+// Layout [bin][slot]: warps 2j and 2j + 1 own the low and high halves of the
+// same 32 words, so a warp's 32 lanes touch 32 distinct banks for any bin
+// pattern (adjacent threads sharing a word made every access a 2-way
+// conflict); a count is a 16-bit load / add / store (one shared-memory atomic
+// on the word, +1 or +65536, measured slower: 158 against 128 us on config 4:
+// shared atomics issue at a fraction of the load / store rate).  The round's
+// minimum is the lowest
+// occupied bin, read off the block histogram at the end instead of a min per
+// codeword.  Same two-walker structure as K1; on an odd range the second
+// walker's last step is masked.
+constexpr int kK1hWindow = 64;
+constexpr int kK1hMinThreads = 64;  // two warps share a word
+// bins of a block's shared histogram: stored weights 0 .. min(n, 32 W)
+template <int W> __host__ __device__ constexpr int k1h_bins(int n) {
+  return (n < 32 * W ? n : 32 * W) + 1;
+}
+__host__ __device__ constexpr int k1h_window(int nbins) {
+  return nbins < kK1hWindow ? nbins : kK1hWindow;
+}
 template <int W, int D>
 __global__ void __launch_bounds__(256)
 k1h_histogram(const RoundArgs a) {
   constexpr int WP = padded_words(W);
   extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ unsigned int s_pop;
   uint32_t *srows, *spx;
   Group* sgroups;
-  const int nbins = a.n + 1;
+  const int nbins = k1h_bins<W>(a.n);
+  const int win = k1h_window(nbins);
+  const int tid = threadIdx.x;
+  const int bd = blockDim.x;
   size_t base = smem_base_bytes<W>(a.m, a.k, staged_groups(a));
   base = (base + 15) & ~size_t(15);
   unsigned int* bhist = reinterpret_cast<unsigned int*>(smem + base);
-  unsigned short* th = reinterpret_cast<unsigned short*>(smem + base + (size_t)nbins * 4);
-  for (int i = threadIdx.x; i < nbins; i += blockDim.x) bhist[i] = 0u;
-  for (int i = threadIdx.x; i < nbins * (int)blockDim.x; i += blockDim.x) th[i] = 0;
+  unsigned int* th32 = bhist + ((nbins + 3) & ~3);
+  unsigned short* th = reinterpret_cast<unsigned short*>(th32);
+  if (tid == 0) s_pop = 0u;
+  for (int i = tid; i < nbins; i += bd) bhist[i] = 0u;
+  for (int i = tid; i < (win + 1) * (bd >> 1); i += bd) th32[i] = 0u;  // + the trash row
   stage<W>(a, srows, spx, sgroups, smem);  // ends with __syncthreads
   const unsigned long long* sbinom = smem_binom<W>(smem, a);
 
   const unsigned FULL = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const int tid = threadIdx.x;
-  const int bd = blockDim.x;
+  const int lane = tid & 31;
   const int k = a.k, q = a.g - 1 - D;
   unsigned int since_flush = 0;
-  int best = INT_MAX;
+  // this thread's half-word of a bin row (see the layout above)
+  const int wrp = tid >> 5;
+  unsigned short* const mine = th + 64 * (wrp >> 1) + 2 * lane + (wrp & 1);
+  // window start: the expected weight of a sum of g of this Gamma's rows
+  int lo = 0;
+  if (nbins > win) {
+    const int gam = a.ngroups > 0 ? sgroups[0].gamma : 0;
+    const uint32_t* R0 = srows + gam * k * WP;
+    unsigned int pc = 0;
+    for (int i = tid; i < k * WP; i += bd) pc += __popc(R0[i]);
+    pc = __reduce_add_sync(FULL, pc);
+    if (lane == 0 && pc) atomicAdd(&s_pop, pc);
+    __syncthreads();
+    const int ncols = max(1, min(a.n - (((a.elide >> gam) & 1ull) ? k : 0), 32 * W));
+    const float dens = fminf(1.0f, (float)s_pop / ((float)k * (float)ncols));
+    const float c = 0.5f * (float)ncols * (1.0f - powf(1.0f - 2.0f * dens, (float)a.g));
+    lo = max(0, min(nbins - win, (int)(c + 0.5f) - win / 2));
+  }
 
   auto flush = [&]() {
-    for (int b = 0; b < nbins; ++b) {
-      const unsigned short v = th[b * bd + tid];
+    for (int b = 0; b < win; ++b) {
+      const unsigned int v = mine[b * bd];
       if (v) {
-        atomicAdd(bhist + b, (unsigned)v);
-        th[b * bd + tid] = 0;
+        atomicAdd(bhist + lo + b, v);
+        mine[b * bd] = 0;
       }
     }
     since_flush = 0;
+  };
+  // The hot loop is branch-free: a weight outside the window (and the
+  // masked second walker) counts into a trash row, oow keeps the step's
+  // largest window offset, and a step that saw one outside is walked again
+  // for just those codewords (rare).
+  const unsigned int uwin = (unsigned int)win;
+  auto count2 = [&](int wa, int wb, unsigned int notb, unsigned int& oow) {
+    const unsigned int da = (unsigned int)(wa - lo), db = (unsigned int)(wb - lo);
+    oow = max(oow, max(da, db));
+    unsigned short* ha = mine + min(da, uwin) * (unsigned int)bd;
+    *ha = (unsigned short)(*ha + 1);
+    unsigned short* hb = mine + min(db | notb, uwin) * (unsigned int)bd;
+    *hb = (unsigned short)(*hb + 1);
   };
 
   unsigned long long wcombos = 0;  // this warp's combinations (one atomic at the end)
@@ -902,16 +961,15 @@ k1h_histogram(const RoundArgs a) {
     for (long long p = 0; p < maxca; ++p) {
       if (p < ca) {
         const bool with_b = p < cb;
-        suffix_pair<W, D>(A.acc, B.acc, R, e0, k, v.s0, v.gr.sl, [&](int wa, int wb) {
-          best = min(best, wa);
-          unsigned short* h = th + wa * bd + tid;
-          *h = (unsigned short)(*h + 1);
-          if (with_b) {
-            best = min(best, wb);
-            unsigned short* hb = th + wb * bd + tid;
-            *hb = (unsigned short)(*hb + 1);
-          }
-        });
+        const unsigned int notb = with_b ? 0u : 0xFFFFFFFFu;
+        unsigned int oow = 0u;
+        suffix_pair<W, D>(A.acc, B.acc, R, e0, k, v.s0, v.gr.sl,
+                          [&](int wa, int wb) { count2(wa, wb, notb, oow); });
+        if (oow >= uwin)
+          suffix_pair<W, D>(A.acc, B.acc, R, e0, k, v.s0, v.gr.sl, [&](int wa, int wb) {
+            if ((unsigned int)(wa - lo) >= uwin) atomicAdd(bhist + wa, 1u);
+            if (with_b && (unsigned int)(wb - lo) >= uwin) atomicAdd(bhist + wb, 1u);
+          });
         if (p + 1 < ca) A.step(PX);
         if (p + 1 < cb) B.step(PX);
       }
@@ -924,11 +982,15 @@ k1h_histogram(const RoundArgs a) {
   // the pass is one Gamma (all groups share it): shift by its dropped
   // identity weight
   const int off = a.ngroups > 0 ? gamma_woff(a, sgroups[0].gamma) : 0;
+  __syncthreads();
+  int best = INT_MAX;  // the lowest occupied bin
+  for (int b = tid; b < nbins && b + off <= a.n; b += bd)
+    if (bhist[b]) {
+      atomicAdd(a.hist + b + off, (unsigned long long)bhist[b]);
+      best = min(best, b);
+    }
   const int wbest = __reduce_min_sync(FULL, best);
   if (lane == 0 && wbest < INT_MAX) atomicMin(a.bound, wbest + off);
-  __syncthreads();
-  for (int b = tid; b + off < nbins; b += bd)
-    if (bhist[b]) atomicAdd(a.hist + b + off, (unsigned long long)bhist[b]);
 }
 
 // ---------------------------------------------------------------------------

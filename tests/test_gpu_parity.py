@@ -176,6 +176,32 @@ def test_histogram_small_vs_oracle():
         assert np.array_equal(hist, oracle.histogram(rows, n, g)), (k, n, g)
 
 
+@pytest.mark.gpu
+def test_histogram_outside_window():
+    """K1h keeps private counters for a window of 64 weights around the
+    expected weight and sends the rest through its exact slow path: rows of
+    very different densities spread the weights over the whole range."""
+    rng = random.Random(23)
+    for (k, n, g) in [(18, 200, 3), (16, 250, 4), (14, 130, 2), (12, 256, 3)]:
+        full = (1 << n) - 1
+        rows = []
+        for i in range(k):
+            r = rng.getrandbits(n)
+            if i % 3 == 0:
+                r &= rng.getrandbits(n) & rng.getrandbits(n)  # sparse
+            elif i % 3 == 1:
+                r |= rng.getrandbits(n) | rng.getrandbits(n)  # dense
+            rows.append(r & full)
+        rows[0] = 0
+        rows[1] = full
+        hist, mn, c = weight_histogram_gpu(BitMatrix(rows, n), g)
+        want = oracle.histogram(rows, n, g)
+        assert np.array_equal(hist, want), (k, n, g)
+        assert c == comb(k, g) and mn == int(np.flatnonzero(want)[0])
+        nz = np.flatnonzero(want)
+        assert nz[-1] - nz[0] >= 64  # wider than the window
+
+
 def test_cfg5_full(cfg5_golden, engine):
     fx = cfg5_golden
     G, gs, draws = code("cfg5", 7)
