@@ -83,8 +83,8 @@ extern "C" {
                              W <= 3 whose last stored word holds <= 16
                              columns, e.g. config 5's 80: 3 MMAs per tile
                              instead of 4); else as BZ_ENGINE_MXF4Q.  On
-                             request: measured slower than K5q (2.31 against
-                             2.02 ms on config 5's g = 8 round)         */
+                             request: measured no faster than K5q (1.97
+                             against 1.92 ms on config 5's g = 8 round)  */
 
 typedef struct bz_ctx bz_ctx;
 

@@ -257,9 +257,9 @@ PlanShape pass_shape(int engine, int g, bool hist, int w32 = 0, int m = 0, int k
     // K5f: K5q's fields from folded MMAs (3 instead of 4 per tile at W = 3)
     // where the last stored word is at most half used (bz::k5f_ok); a
     // host-only plan (w32 = 0) has K5q's shape either way.  On request only:
-    // config 5's g = 8 round measured 2.31 ms against K5q's 2.02 ms -- the
-    // epilogue's wait / load / release chain per accumulator bounds both, and
-    // K5f adds an IMAD per register to it
+    // config 5's g = 8 round measured 1.97 ms against K5q's 1.92 ms -- the
+    // release chain of an accumulator buffer bounds both, and K5f adds an
+    // IMAD per register to the epilogue (K5q)
     if (engine == BZ_ENGINE_MXF4F && w32 != 0 && bz::k5f_ok(w32, n_eff))
       return {3, bz::kUmmaM, bz::k4_tile_rows<true, 6>(), 10};
     if ((engine == BZ_ENGINE_MXF4Q || engine == BZ_ENGINE_MXF4F || engine == BZ_ENGINE_AUTO) && q_ok)

@@ -76,6 +76,9 @@ constexpr int kUmmaM = 128;       // prefixes per A tile = producer threads
 #ifndef BZ_K5_LEAN
 #define BZ_K5_LEAN 1  // K5q / K5f epilogue: the lean tile loop (0: the general one)
 #endif
+#ifndef BZ_K5_LD64
+#define BZ_K5_LD64 1  // lean epilogue: one 64-column packed load per tile
+#endif
 #ifndef BZ_K5F_SPLIT
 #define BZ_K5F_SPLIT 1  // K5f: accumulator column halves with their own barriers
 #endif
@@ -591,6 +594,21 @@ __device__ __forceinline__ void tmem_ld16p(uint32_t taddr, uint32_t* v) {
       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
         "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
         "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+}
+// 64 columns as 32 registers in ONE load (the K5q / K5f lean epilogue reads
+// its 60 columns with it: ptxas cannot slide arithmetic on the first
+// registers between the pieces of a split load and reuse their registers for
+// the later pieces, which is what delayed K5f's last loads and its release)
+__device__ __forceinline__ void tmem_ld32p(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.pack::16b.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
+      "%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_regs16_after_wait(uint32_t* v) {
@@ -1260,8 +1278,11 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
               constexpr int BUF = decltype(bufc)::value;
               mbar_wait_fast(accfull(BUF), (tcount >> 1) & 1);
               tc_fence_after();
-              uint32_t v[NP];
-              tmem_ld_cols_p<EC>(tq + (uint32_t)(BUF * N), v);
+              uint32_t v[BZ_K5_LD64 && EC > 32 ? 32 : NP];
+              // (a 60-column slice read as 64: the 4 extra columns -- the next
+              // buffer's or the scale factors' -- land in v[30], v[31], unused)
+              if constexpr (BZ_K5_LD64 && EC > 32) tmem_ld32p(tq + (uint32_t)(BUF * N), v);
+              else tmem_ld_cols_p<EC>(tq + (uint32_t)(BUF * N), v);
               tmem_ld_wait();
 #pragma unroll
               for (int i = 0; i + 1 < NP; i += 2) asm volatile("" : "+r"(v[i]), "+r"(v[i + 1]) : : "memory");
