@@ -35,6 +35,7 @@ the random binary [160,80] code of seed 7 (SURVEY.md Appendix A generator,
 from __future__ import annotations
 
 import argparse
+import itertools
 import json
 import os
 import socket
@@ -208,6 +209,12 @@ def other_seeds(args, cfg, local, flush) -> dict:
         ms = statistics.median(times)
         out[f"seed{seed}"] = {"value": combos / (ms * 1e-3), "unit": UNIT, "ms_per_run": ms,
                               "combinations": combos, "d": st.U, "g_final": st.g_reached}
+        if seed == 1:
+            # the same per-shard measurement as the headline's, on a typical
+            # code (g = 9: 8x the work per run)
+            out["seed1"]["shards_on_one_gpu"] = shard_times(
+                ctx, st, engine.start_state(gs, n, k, cfg).U, gs.matrix_count, flush,
+                lambda: torch.cuda.synchronize(local), reps=1)
     return out
 
 
@@ -327,6 +334,84 @@ def cfg4_side(ctx, peaks, seed: int = 1) -> dict:
                           "note": f"POPC roofline / {w_st} words per stored codeword"},
         "reference_1core_s": 3.6,
     }
+
+
+_SHARD_EPOCH = itertools.count(0x7000)
+
+
+def shard_times(ctx, st, u0: int, m: int, flush, sync, reps: int = 2) -> dict:
+    """What one rank of an N-GPU run does, measured on THIS GPU: the run's
+    rounds as shard s of N (bz_rounds(..., shard=s, nshards=N): the chunks
+    with c % N == s; rounds too small to split go whole to one rank) for every
+    s in turn, device time of each by CUDA events on the library stream.  The
+    slowest shard is the device time a rank would need at N GPUs -- without
+    the per-batch exchange (one all-gather of 4m int64) -- so t(1) / slowest
+    is the device-side scaling the rank-space sharding allows, not a
+    multi-GPU measurement.  Two brackets of what the ranks' shared bound (the
+    CUDA-IPC mirror every rank's kernels publish to and tighten their
+    thresholds from) does for a rank: "own_bound" -- no mirror, a shard only
+    knows its own finds (the lower bracket); "shared_bound" -- the mirror
+    mapped in this one process and filled by an untimed pass over all
+    shards, so every timed shard starts from the job's minima as if another
+    rank had just found them (the upper bracket).  Also checks the sharding
+    on the device: per round, the minimum over shards and the sum of their
+    combination counts equal the unsharded run's."""
+    lp = [0] + [t[1] for t in st.trace[:-1]]  # L_prev of round g = L after round g - 1
+    full = [(t[2], r.combinations) for t, r in zip(st.trace, st.rounds)]
+
+    def run(s, nsh):
+        flush.zero_()
+        sync()
+        ctx.timer_start()
+        res = ctx.rounds(1, lp, u0, s, nsh)
+        return ctx.timer_stop(), res
+
+    def folded(results):
+        """min over shards / sum of counts per round == the unsharded run's?"""
+        mins, sums = None, None
+        for res in results:
+            mn = [min(r[0]) for r in res]
+            cb = [sum(r[1]) for r in res]
+            mins = mn if mins is None else [min(a, b) for a, b in zip(mins, mn)]
+            sums = cb if sums is None else [a + b for a, b in zip(sums, cb)]
+        # U after round g is the running minimum of the rounds' minima
+        run_min, ok = u0, True
+        for g, (u_full, c_full) in enumerate(full):
+            run_min = min(run_min, mins[g])
+            ok = ok and run_min == u_full and sums[g] == c_full
+        return ok
+
+    def sweep(nsh, check=None):
+        times, results = [], []
+        for s in range(nsh):
+            ms, res = min((run(s, nsh) for _ in range(reps)), key=lambda x: x[0])
+            times.append(ms)
+            results.append(res)
+        return {"shard_ms": [round(t, 4) for t in times], "slowest_ms": max(times),
+                "device_speedup": t1 / max(times),
+                "matches_unsharded": folded(results) if check is None else check}
+
+    out = {"rounds": len(lp), "note": "per-shard device time on one GPU, shards run one after "
+                                      "another, no exchange; own_bound / shared_bound bracket the "
+                                      "effect of the ranks' shared bound"}
+    t1 = statistics.median(run(0, 1)[0] for _ in range(3))
+    out["unsharded_ms"] = t1
+    for nsh in (2, 4, 8):
+        out[f"N{nsh}"] = {"own_bound": sweep(nsh)}
+    ctx.shared_bound_export()
+    ctx.shared_bound_open(None)
+    try:
+        for nsh in (2, 4, 8):
+            ctx.shared_bound_epoch(next(_SHARD_EPOCH))  # a newer tag per sweep
+            # untimed: every shard's minima into the mirror, each shard seeing
+            # the finds of the ones before it -- the fold of THIS pass is the
+            # sharded result (in the timed pass the mirror already holds every
+            # minimum, so no shard finds anything below it to report)
+            ok = folded([ctx.rounds(1, lp, u0, s, nsh) for s in range(nsh)])
+            out[f"N{nsh}"]["shared_bound"] = sweep(nsh, check=ok)
+    finally:
+        ctx.shared_bound_close()
+    return out
 
 
 def cpu_baseline(G, gs, sample_g: int) -> dict:
@@ -707,6 +792,8 @@ def main():
         line["configs_1_3"] = configs_wall(cfg)
         line["cfg4"] = cfg4_side(ctx, peaks)
         backend.load(gs, n)
+        line["shards_on_one_gpu"] = shard_times(ctx, st, engine.start_state(gs, n, k, cfg).U, m,
+                                                flush, barrier)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(G, gs, args.cpu_sample_g)
     print(json.dumps(line), flush=True)

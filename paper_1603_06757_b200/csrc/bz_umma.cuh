@@ -1988,6 +1988,22 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
           const long long qchunk = (cidx < bt.cend[bt.count - 1] && ch < aq.nchunks && !round_done(aq))
                                        ? (long long)(((unsigned long long)rq << kQRoundShift) | ch)
                                        : -1;
+          // Multi-GPU: any rank's running minimum of this round and of the
+          // fused rounds before it (the shared mirror, one peer load each per
+          // chunk) tightens this CTA's cached bounds, so the producers'
+          // thresholds follow the whole job's U, not just this rank's finds.
+          // A minimum found here at or above it is then not published -- the
+          // rank that holds the lower one reports it, and the fold over ranks
+          // is a min (the same clip the earlier fused rounds' minima apply).
+          if constexpr (QQ) {
+            if (aq.gbound && qchunk >= 0) {
+              int sv = gbound_read(aq, aq.g);
+              for (int q = 0; q < rq; ++q) sv = min(sv, gbound_read(bt.a[q], bt.a[q].g));
+              if (sv < INT_MAX)
+                for (int j = 0; j < aq.m && j < kBndPerRound; ++j)
+                  atomicMin(s_bnd + rq * kBndPerRound + j, sv);
+            }
+          }
           s_q[qs] = qchunk;
           long long* ct = k4_ctrace(a, qpub);
           if (ct) { ct[0] = qchunk; ct[1] = clock64(); }
