@@ -236,8 +236,13 @@ constexpr long long kK5LaneMin = 8192;
 #endif
 constexpr double kAutoK1Combos = BZ_AUTO_K1_COMBOS;
 // sharded calls: rounds below this many combinations x (nshards - 1) run
-// whole on one rank (run_batch)
-constexpr double kOwnWholeCombos = 6e8;
+// whole on one rank (run_batch).  Only the trivial rounds: a batch's K1 rounds
+// share one launch and its tensor-core rounds another, so splitting a small
+// round adds no launch to any rank, while a rank that owned g = 5 or g = 6
+// whole was the slowest of the job (config 5 as shard s of 8 on one GPU,
+// slowest shard: 6e8 0.54 ms, 1e8 0.52, 1e7 .. 0 0.45-0.46 ms;
+// tools/_own_sweep.sh)
+constexpr double kOwnWholeCombos = 1e5;
 
 // K5q: stored weights <= 128 (byte fields x = w + 128 - thr, thr in [1, 128];
 // every Gamma's start bound is capped at its stored columns + offset), W <= 4
@@ -1024,17 +1029,19 @@ int run_batch(bz_ctx* ctx, int g0, int count, int gamma_only, const int* lower_p
       ctrace = d_ct;
     }
   }
-  // Sharded calls: a round too small to be worth splitting (its fixed
-  // launch-and-fill latency, ~25 us, exceeds what the split saves) is run
+  // Sharded calls: a round too small to be worth splitting (a few hundred
+  // thousand combinations: kOwnWholeCombos) is run
   // whole by one rank, round-robin over such rounds; the other ranks
   // report nothing for it (upper / 0), which the exchange's min / sum
   // absorbs.  Every rank decides alike from (m, k, g, nshards).
   std::vector<int> owner(count, -1);
   if (nshards > 1 && !hist) {
     int owned = 0;
+    double own_whole = kOwnWholeCombos;
+    if (const char* e = getenv("BZ_OWN_WHOLE")) own_whole = atof(e);  // (experiments; alike on every rank)
     const double mult = gamma_only < 0 ? (double)m : 1.0;
     for (int i = 0; i < count; ++i)
-      if (mult * binom_d(ctx->k, g0 + i) < kOwnWholeCombos * (nshards - 1))
+      if (mult * binom_d(ctx->k, g0 + i) < own_whole * (nshards - 1))
         owner[i] = owned++ % nshards;
   }
   const auto t_plan0 = std::chrono::steady_clock::now();

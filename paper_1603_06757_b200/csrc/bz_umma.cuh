@@ -76,6 +76,9 @@ constexpr int kUmmaM = 128;       // prefixes per A tile = producer threads
 #ifndef BZ_K5_LEAN
 #define BZ_K5_LEAN 1  // K5q / K5f epilogue: the lean tile loop (0: the general one)
 #endif
+#ifndef BZ_GBOUND_THR
+#define BZ_GBOUND_THR 1  // K5q / K5w thresholds also follow the other ranks' minima
+#endif
 #ifndef BZ_K5_LD64
 #define BZ_K5_LD64 1  // lean epilogue: one 64-column packed load per tile
 #endif
@@ -1641,6 +1644,7 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
           if constexpr (QQ)
             if (c.gr.gamma < kBndPerRound) atomicMin(s_bnd + rr * kBndPerRound + c.gr.gamma, wb);
         }
+
         long long* ct = k4_ctrace(a, qi);
         if (ct && warp == 0) { ct[2] = clock64(); ct[3] = global_ns(); }
       }
@@ -1808,6 +1812,20 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
         const K4Chunk c = k4_decode<TR>(plan_of(rr), ar.ngroups, chunk, k);
         k4_trace_chunk(a, toff, c.gr.ell, tcount);
         const int ntile = c.tile_hi - c.tile_lo;
+        // Multi-GPU: any rank's running minimum of this round (the shared
+        // mirror) tightens this CTA's cached bounds, so the producers'
+        // thresholds follow the whole job's U, not just this rank's finds.
+        // One peer load per chunk and CTA, issued here by the first issuer's
+        // lane 0 and consumed at the chunk's end, so nothing waits for it
+        // (polled by the loader before each chunk it cost a shard 27 us of
+        // 460; held in the epilogue's registers across its tile loop, 9 us).
+        // A minimum found here at or above the mirror's is then not published
+        // -- the rank that holds the lower one reports it, and the fold over
+        // ranks is a min (the same clip the earlier fused rounds' minima
+        // apply).
+        unsigned long long graw = ~0ull;
+        if constexpr (QQ && BZ_GBOUND_THR)
+          if (mb == 0 && lane == 0 && ar.gbound) graw = ((volatile unsigned long long*)ar.gbound)[ar.g];
         for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {
           const int ab = grp % NA;
           // first tile of this step that falls to this issuer
@@ -1939,6 +1957,12 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
           __syncwarp();
           tcount += (uint32_t)ntile;
         }
+        if constexpr (QQ && BZ_GBOUND_THR)
+          if (ar.gbound && (graw >> 32) == (ar.gtag >> 32)) {  // this run's word (cf. gbound_read)
+            const int sv = (int)(unsigned)(graw & 0xffffffffull);
+            for (int j = 0; j < ar.m && j < kBndPerRound; ++j)
+              atomicMin(s_bnd + rr * kBndPerRound + j, sv);
+          }
       }
     }
     __syncwarp();
@@ -1988,22 +2012,6 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
           const long long qchunk = (cidx < bt.cend[bt.count - 1] && ch < aq.nchunks && !round_done(aq))
                                        ? (long long)(((unsigned long long)rq << kQRoundShift) | ch)
                                        : -1;
-          // Multi-GPU: any rank's running minimum of this round and of the
-          // fused rounds before it (the shared mirror, one peer load each per
-          // chunk) tightens this CTA's cached bounds, so the producers'
-          // thresholds follow the whole job's U, not just this rank's finds.
-          // A minimum found here at or above it is then not published -- the
-          // rank that holds the lower one reports it, and the fold over ranks
-          // is a min (the same clip the earlier fused rounds' minima apply).
-          if constexpr (QQ) {
-            if (aq.gbound && qchunk >= 0) {
-              int sv = gbound_read(aq, aq.g);
-              for (int q = 0; q < rq; ++q) sv = min(sv, gbound_read(bt.a[q], bt.a[q].g));
-              if (sv < INT_MAX)
-                for (int j = 0; j < aq.m && j < kBndPerRound; ++j)
-                  atomicMin(s_bnd + rq * kBndPerRound + j, sv);
-            }
-          }
           s_q[qs] = qchunk;
           long long* ct = k4_ctrace(a, qpub);
           if (ct) { ct[0] = qchunk; ct[1] = clock64(); }

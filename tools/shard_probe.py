@@ -13,6 +13,7 @@ from paper_1603_06757_b200.configs import code  # noqa: E402
 from paper_1603_06757_b200.enumeration import family_words  # noqa: E402
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 8
+MIRROR = "--mirror" in sys.argv  # map the shared-bound mirror (own memory) and pre-fill it
 G, gs, _ = code("cfg5", 7)
 ctx = _native.context(0)
 ctx.load(family_words(gs.gammas, 160), 160)
@@ -30,6 +31,12 @@ def t(fn, reps=5):
     return sorted(ms)[len(ms) // 2]
 
 
+if MIRROR:
+    ctx.shared_bound_export()
+    ctx.shared_bound_open(None)
+    ctx.shared_bound_epoch(int(os.environ.get("EPOCH", "77")))
+    for s in range(N):
+        ctx.rounds(1, lp, 81, s, N)
 full = t(lambda: ctx.rounds(1, lp, 81, 0, 1))
 full8 = t(lambda: ctx.round(8, 16, 18, 0, 1))
 print(f"unsharded: batch {full:.4f} ms  g=8 alone {full8:.4f} ms")
