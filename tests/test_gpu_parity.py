@@ -212,6 +212,42 @@ def test_cfg5_full(cfg5_golden, engine):
     assert rep.counters.combinations == fx["combinations"]
 
 
+@pytest.mark.parametrize("mirror", [False, True])
+@pytest.mark.parametrize("nshards", [2, 8])
+def test_cfg5_batch_sharded(cfg5_golden, ctx, nshards, mirror):
+    """BASELINE's multi-GPU configuration at full size, one rank at a time on
+    this device: rounds 1..8 of config 5 as shard s of N in one batch each
+    (what rank s launches), folded like the host exchange -- min of the
+    minima, sum of the counts per round -- must reproduce the reference's U
+    trajectory and combination count.  With the shared-bound mirror mapped
+    (this context's own memory) every shard also thresholds with the finds of
+    the shards before it and does not report minima at or above them: the
+    fold must not change."""
+    fx = cfg5_golden
+    G, gs, _ = code("cfg5", 7)
+    trace = [tuple(t) for t in fx["bounds_trace"]]
+    lp = [0] + [t[1] for t in trace[:-1]]
+    u0 = 160 - 80 + 1
+    with ctx.lock:
+        ctx.set_engine("auto")
+        ctx.load(family_words(gs.gammas, 160), 160)
+        if mirror:
+            ctx.shared_bound_export()
+            ctx.shared_bound_open(None)
+            ctx.shared_bound_epoch(0x5000 + nshards)
+        try:
+            res = [ctx.rounds(1, lp, u0, s, nshards) for s in range(nshards)]
+        finally:
+            if mirror:
+                ctx.shared_bound_close()
+    run_min, total = u0, 0
+    for g, (_, _, u_ref) in enumerate(trace):
+        run_min = min([run_min] + [min(r[g][0]) for r in res])
+        total += sum(sum(r[g][1]) for r in res)
+        assert run_min == u_ref, (g + 1, run_min, u_ref)
+    assert total == fx["combinations"]
+
+
 def test_too_large(ctx):
     M = BitMatrix([(1 << i) for i in range(128)], 200)
     with pytest.raises(TooLarge):
