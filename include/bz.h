@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define BZ_ABI_VERSION 15
+#define BZ_ABI_VERSION 16
 
 /* limits of the device kernels */
 #define BZ_MAX_K 128 /* rows per Gamma (prefix masks are 128-bit)      */
@@ -286,6 +286,11 @@ int bz_histogram(bz_ctx *ctx, int gamma, int g, int shard, int nshards,
  * descending, then the rest lex), S = suffixes_per_chunk.  suffix_floor is
  * ell + 1 except in K5's deeper levels (depth 4, 5), which take the
  * combinations whose top `depth` elements all lie in rows >= a level floor.
+ * In those levels every prefix whose last element is below the floor has the
+ * same suffix slice, and they are consecutive in colex order, so they form
+ * ONE group, marked suffix_lanes = 0 (ABI 16): its ell is the last such
+ * element, nprefix = C(ell + 1, g - depth), and a lane walks the colex ranks
+ * of the (g-depth)-subsets of [0, ell + 1) with no fixed last row.
  * depth = 3..5 (K5) or 3 (K3, K4) for g >= 4 unless engine ==
  * BZ_ENGINE_POPC, else 2 for g >= 4, else 1 (g = 1: ell = -1, empty
  * prefix). */

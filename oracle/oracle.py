@@ -271,7 +271,9 @@ def enumerate_chunks(gammas: list[list[int]], k: int, g: int, groups, nchunks: i
     for chunk in range(shard, nchunks, nshards):
         gi = max(i for i, s in enumerate(starts) if s <= chunk)
         begin, nprefix, gamma, ell, ppl, _, depth, lanes, spc, nsb, sfloor, sl = groups[gi]
-        lanes //= sl  # K1: prefix blocks per warp (suffix lanes share a block)
+        merged = depth >= 3 and sl == 0  # K5 family: (g - depth)-subsets of [0, ell + 1)
+        if not merged:
+            lanes //= sl  # K1: prefix blocks per warp (suffix lanes share a block)
         local = chunk - begin
         pb, sb = divmod(local, nsb)
         rows = gammas[gamma]
@@ -281,7 +283,12 @@ def enumerate_chunks(gammas: list[list[int]], k: int, g: int, groups, nchunks: i
         for lane in range(lanes):
             first = (pb * lanes + lane) * ppl
             for p in range(first, min(first + ppl, nprefix)):
-                prefix = [] if g == 1 else colex_unrank(p, g - 1 - depth, ell) + [ell]
+                if g == 1:
+                    prefix = []
+                elif merged:
+                    prefix = colex_unrank(p, g - depth, ell + 1)
+                else:
+                    prefix = colex_unrank(p, g - 1 - depth, ell) + [ell]
                 acc = 0
                 for i in prefix:
                     acc ^= rows[i]
@@ -296,18 +303,20 @@ def enumerate_chunks(gammas: list[list[int]], k: int, g: int, groups, nchunks: i
     return mins, cnt, seen
 
 
-def _walk_cost(first: int, cnt: int, q: int, ell: int) -> int:
+def _walk_cost(first: int, cnt: int, q: int, ell: int, merged: bool = False) -> int:
     """Row additions of one prefix walker over colex ranks [first,
     first+cnt): the init folds R[ell] and the q rows of the first subset (q
     additions), each colex successor adds 2 prefix-XOR rows, 3 when the low
-    run of the subset's bits is longer than one (bz_kernels.cuh Walker)."""
+    run of the subset's bits is longer than one (bz_kernels.cuh Walker).  A
+    merged group's prefixes are the (q + 1)-subsets of [0, ell + 1): the same
+    q additions for the first one."""
     if cnt <= 0:
         return 0
     cost = max(q, 0)
-    if q <= 0:
+    if q <= 0 and not merged:
         return cost
     x = 0
-    for b in colex_unrank(first, q, ell):
+    for b in (colex_unrank(first, q + 1, ell + 1) if merged else colex_unrank(first, q, ell)):
         x |= 1 << b
     for _ in range(cnt - 1):
         s = (x & -x).bit_length() - 1
@@ -375,7 +384,7 @@ def expected_counters(m: int, k: int, g: int, groups, nchunks: int, shard: int =
             for r in range(128):
                 first = bfirst + r * ppl
                 cnt = max(0, min(ppl, nprefix - first))
-                w = _walk_cost(first, cnt, q, ell)
+                w = _walk_cost(first, cnt, q, ell, merged=(sl == 0))
                 adds[gamma] += w + cnt * cols
                 accs[gamma] += w + (cnt > 0)
             accs[gamma] += maxcnt * cols

@@ -19,7 +19,7 @@ from .errors import (DeviceError, InvalidArity, InvalidDimensions, MindistError,
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("BZ_LIB") or os.path.join(PKG_DIR, "libbz.so")
-ABI_VERSION = 15
+ABI_VERSION = 16
 
 BZ_OK = 0
 BZ_LOOP_RUNNING, BZ_LOOP_DONE, BZ_LOOP_MAX_G = 0, 1, 2

@@ -320,6 +320,12 @@ double binom_d(int p, int q) {
   return t[p * (BZ_MAX_K + 1) + q];
 }
 
+// (BZ_K5_MERGE=0: one group per ell, as before -- for A/B runs)
+static bool merge_groups() {
+  const char* e = getenv("BZ_K5_MERGE");
+  return !e || atoi(e) != 0;
+}
+
 double k5_cost(int k, int g, const Levels& lv, int tile_rows) {
   // K5 clocks per tile / per prefix step (cfg5, B200); K5p/K5q tiles hold
   // twice the rows
@@ -331,6 +337,11 @@ double k5_cost(int k, int g, const Levels& lv, int tile_rows) {
   double cost = 0;
   for (int D = 3; D <= lv.dmax; ++D) {
     const int hi = std::min(lv.floor[D + 1] - 1, k - 1 - D);
+    // (per ell, although build_plan merges the prefixes below a level's
+    // floor into one group: floors chosen with the merged groups' fewer
+    // steps counted -- (23, 42) instead of (26, 52) for config 5's g = 8 --
+    // measured slower, 1.94 against 1.91 ms; the step weight was fitted to
+    // the unmerged plans)
     for (int ell = g - 1 - D; ell <= hi; ++ell) {
       const double np = binom_d(ell, g - 1 - D);
       const int f = std::max(ell + 1, lv.floor[D]);
@@ -445,8 +456,21 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
     for (int depth = dmin; depth <= lv.dmax; ++depth) {
       const int ell_lo = g == 1 ? -1 : g - 1 - depth;
       const int ell_hi = g == 1 ? -1 : std::min(k - 1 - depth, lv.floor[depth + 1] - 1);
-      for (int ell = ell_lo; ell <= ell_hi; ++ell) {
-        const unsigned long long np = g == 1 ? 1ull : binom_sat(ell, g - 1 - depth);
+      // K5 family, levels above the first: every prefix whose last element
+      // is below the level's floor has the same suffix slice [floor, k), and
+      // those prefixes -- (g - D)-subsets of [0, bound) -- are consecutive
+      // in colex order, so they form ONE group (sl = 0) instead of one per
+      // ell: a group's last prefix step is partly empty, and the deep levels
+      // have few prefixes per ell and thousands of tiles per step (config 5:
+      // 7.7 % fewer tiles at g = 7, 2.7 % at g = 8, 0.9 % at g = 9).
+      int merged_to = ell_lo - 1;  // last ell folded into the merged group
+      if (shape.kernel >= 5 && g > 1 && depth > dmin && lv.floor[depth] - 1 > ell_lo && merge_groups())
+        merged_to = std::min(ell_hi, lv.floor[depth] - 1);
+      for (int ell = std::max(ell_lo, merged_to); ell <= ell_hi; ++ell) {
+        const bool merged = ell == merged_to;
+        const unsigned long long np = g == 1    ? 1ull
+                                      : merged ? binom_sat(ell + 1, g - depth)
+                                               : binom_sat(ell, g - 1 - depth);
         if (np == 0) continue;
         if (np >= (1ull << 62))
           return fail(ctx, BZ_ERR_TOO_LARGE, "C(%d,%d) prefixes exceed 2^62", ell, g - 1 - depth);
@@ -521,7 +545,7 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
         gr.tile_rows = shape.tile_rows;
         gr.slice = (int)work;
         gr.sfloor = sfloor;
-        gr.sl = (int)sl;
+        gr.sl = merged ? 0 : (int)sl;
         const unsigned long long per_chunk = (unsigned long long)lanes_ll * (unsigned long long)ppl;
         chunk += (np + per_chunk - 1) / per_chunk * (unsigned long long)ntb;
         gs.push_back(gr);
@@ -539,10 +563,11 @@ int build_plan(bz_ctx* ctx, int m, int k, int g, int gamma_only, PlanShape shape
 // of re-planning every round before the first launch.
 // the planning knobs (test and tuning hooks), read once per batch
 struct PlanKnobs {
-  const char *floors, *scale, *cost, *lmin;
+  const char *floors, *scale, *cost, *lmin, *merge;
   PlanKnobs()
       : floors(getenv("BZ_K5_FLOORS")), scale(getenv("BZ_K5_CHUNK_SCALE")),
-        cost(getenv("BZ_K5_COST")), lmin(getenv("BZ_K5_LANE_MIN")) {}
+        cost(getenv("BZ_K5_COST")), lmin(getenv("BZ_K5_LANE_MIN")),
+        merge(getenv("BZ_K5_MERGE")) {}
 };
 
 int plan_round(bz_ctx* ctx, int g, int gamma_only, PlanShape shape, int nshards, size_t goff,
@@ -556,9 +581,9 @@ int plan_round(bz_ctx* ctx, int g, int gamma_only, PlanShape shape, int nshards,
   static std::map<std::string, Plan> memo;
   const char *floors = kn.floors, *scale = kn.scale, *cost = kn.cost, *lmin = kn.lmin;
   char key[384];
-  snprintf(key, sizeof key, "%d/%d/%d/%d/%d/%d/%d/%d/%d/%s/%s/%s/%s", ctx->m, ctx->k, g, gamma_only,
+  snprintf(key, sizeof key, "%d/%d/%d/%d/%d/%d/%d/%d/%d/%s/%s/%s/%s/%s", ctx->m, ctx->k, g, gamma_only,
            shape.kernel, shape.depth, shape.lanes, shape.tile_rows, nshards, floors ? floors : "",
-           scale ? scale : "", cost ? cost : "", lmin ? lmin : "");
+           scale ? scale : "", cost ? cost : "", lmin ? lmin : "", kn.merge ? kn.merge : "");
   const IoSlot l = io_layout(ctx->m, ctx->k);
   std::lock_guard<std::mutex> lock(mu);
   auto it = memo.find(key);

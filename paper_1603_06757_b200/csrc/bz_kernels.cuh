@@ -51,7 +51,10 @@ struct Group {
   int tile_rows;                   // D >= 3: suffixes per table tile
   int slice;                       // suffixes per prefix: C(k - sfloor, D)
   int sfloor;                      // smallest suffix row: max(ell + 1, level floor)
-  int sl;                          // K1: suffix lanes per prefix block (1, 2, .., 32)
+  int sl;                          // K1: suffix lanes per prefix block (1, 2, .., 32);
+                                   // K5 family: 1, or 0 for a merged group -- its
+                                   // prefixes are the (g - D)-subsets of [0, ell + 1),
+                                   // nprefix = C(ell + 1, g - D), no fixed last row
 };
 
 struct RoundArgs {
@@ -302,15 +305,19 @@ struct Walker {
   Mask x;
   uint32_t acc[W];
 
+  // The prefix of colex rank `rank`: a q-subset of [0, ell) plus row ell --
+  // or, for a merged group (fixed = false: every prefix whose last element is
+  // below a level's floor shares one suffix slice, and those prefixes are
+  // consecutive in colex order), a q-subset of [0, ell) alone.
   __device__ __forceinline__ void init(unsigned long long rank, int q, int ell,
                                        const uint32_t* R, const unsigned long long* binom,
-                                       const unsigned long long* sb) {
+                                       const unsigned long long* sb, bool fixed = true) {
     constexpr int WP = padded_words(W);
 #pragma unroll
     for (int j = 0; j < W; ++j) acc[j] = 0u;
     x = Mask{0ull, 0ull};
     if (ell < 0) return;
-    xor_row<W>(acc, R + ell * WP);
+    if (fixed) xor_row<W>(acc, R + ell * WP);
     if (q > 0) {
       x = colex_unrank(rank, q, ell, binom, sb);
       Mask y = x;

@@ -1674,7 +1674,10 @@ k4_round_umma(const K5Batch bt, const K4Tables tabs) {
       const uint32_t* PX = spx + c.gr.gamma * (k + 1) * px_stride(W);
       Walker<W> wk;
       // rows without prefixes duplicate the block's first prefix
-      wk.init(cnt > 0 ? first : c.bfirst, ar.g - 1 - c.gr.depth, c.gr.ell, R, a.binom, sbinom);
+      // (a merged group, sl == 0: (g - D)-subsets of [0, ell + 1), no fixed row)
+      const bool merged = c.gr.sl == 0;
+      wk.init(cnt > 0 ? first : c.bfirst, ar.g - 1 - c.gr.depth + (merged ? 1 : 0),
+              c.gr.ell + (merged ? 1 : 0), R, a.binom, sbinom, !merged);
       // walker row additions of this row's valid prefixes (counters)
       unsigned long long wadd = cnt > 0 ? (unsigned long long)max(ar.g - 1 - c.gr.depth, 0) : 0ull;
       for (long long p = 0; p < c.maxcnt; p += kUmmaMA, ++grp) {

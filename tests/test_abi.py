@@ -49,7 +49,10 @@ def test_plan_counts(engine):
         for gr in groups:
             begin, nprefix, gamma, ell, ppl, combos, depth, lanes, spc, nsb, sfloor, sl = gr
             assert nsb >= 1 and (depth < 3 or spc * nsb >= comb(k - sfloor, depth))
-            assert sl in (1, 2, 4, 8, 16, 32) and (depth < 3 or sl == 1)
+            # (K5 family: sl = 0 marks a merged group -- every prefix below a
+            # level's floor, the (g - depth)-subsets of [0, ell + 1))
+            assert sl in (1, 2, 4, 8, 16, 32) if depth < 3 else sl in (0, 1)
+            merged = depth >= 3 and sl == 0
             assert lanes == ({"imma": 256}.get(engine, 128) if depth >= 3 else 32)
             want = 3 if (engine != "popc" and g >= 4) else (2 if g >= 4 else 1)
             if engine in ("auto", "mxf4", "mxf4p", "mxf4t", "mxf4q", "mxf4w", "mxf4f") and g >= 4:
@@ -57,7 +60,9 @@ def test_plan_counts(engine):
                 assert 3 <= depth <= min(5, g - 1) and sfloor >= ell + 1
             else:
                 assert depth == want and sfloor == ell + 1
-            assert nprefix == (1 if g == 1 else comb(ell, g - 1 - depth))
+            assert nprefix == (1 if g == 1 else comb(ell + 1, g - depth) if merged
+                               else comb(ell, g - 1 - depth))
+            assert not merged or depth > 3
             assert combos == nprefix * comb(k - sfloor, depth)
 
 
