@@ -331,8 +331,12 @@ double k5_cost(int k, int g, const Levels& lv, int tile_rows) {
   // twice the rows
   const bool pair = tile_rows > bz::kUmmaN4;
   // (K5q measured: ~625 clocks per tile in steady state; a prefix step --
-  // walker step, A rows, the first tile's latency -- weighs ~3500)
-  double kTile = pair ? 650.0 : 727.0, kStep = pair ? 3500.0 : 1271.0;
+  // walker step, A rows, the first tile's latency -- weighed ~3500 when every
+  // ell was its own group.  The model still counts one group per ell while
+  // build_plan merges the ells below a floor, and with merged plans a heavier
+  // step weight finds better floors: swept 1500 .. 40000 on config 5, batch
+  // 2.32 / 2.28 (3500) / 2.27 (8000) / 2.256 (12000 .. 20000) / 2.30 ms)
+  double kTile = pair ? 650.0 : 727.0, kStep = pair ? 16000.0 : 1271.0;
   if (const char* env = getenv("BZ_K5_COST")) sscanf(env, "%lf,%lf", &kTile, &kStep);
   double cost = 0;
   for (int D = 3; D <= lv.dmax; ++D) {
